@@ -1,0 +1,21 @@
+"""CPU oracle for RSRS -- TEST INFRASTRUCTURE, NOT PART OF THE PRODUCT PATH.
+
+A plain, slow, obviously correct CPU implementation (numpy/scipy, LAPACK,
+FP64 / complex128) of what the hot path computes, written from PAPER.md
+(arXiv 2311.01451) step by step.  It shares no code with the CUDA path
+(paper_2311_01451_b200/); neither imports the other.  Only tests/,
+__graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs may
+import it.
+
+Pins (tests/test_oracle_*.py, run with -m "not gpu"): Fig. 1 tree example,
+brute-force neighbours, nullification identities,
+extraction exactness on block-sparse operators (Fig. 2b), ID bounds and exact
+low-rank recovery, the sample-consistency invariant Y = A_g Omega after every
+step, the decoupling invariant, the zero-far-field special
+case, dense LU solve / relerr at c1, solve(apply(x)) = x.
+Parity unpinned: exact skeleton index sets at near-tie pivots (covered only by
+the +-2 rank and 10 eps solution tolerances); see DESIGN.md.
+"""
+from .tree import build_tree, Tree, Level, morton_encode, morton_decode  # noqa: F401
+from .rsrs import (factor, solve, apply, Factorization, Step, RSRSError,  # noqa: F401
+                   null_basis, pinv_right, row_id, atol_schedule)

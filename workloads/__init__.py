@@ -1,0 +1,194 @@
+"""Seeded synthetic workloads for RSRS (shared by oracle/, tests/ and bench.py).
+
+This module holds ONLY input generation -- point sets, the kernel operator
+A (the black box the method samples), seeded Gaussian test matrices and the
+configuration table -- and none of the method's arithmetic (no nullification,
+ID, extraction, elimination or solve).  Both sides (the CPU oracle and the
+CUDA path) consume what it produces.
+
+Configurations (BASELINE.json `configs`):
+
+  c1  2D, 64x64 cell-centred grid in [0,1]^2, h=1/64,
+      A_ij = delta_ij + h^2 log|x_i - x_j| (i != j), A_ii = 1, FP64
+  c2  as c1 on a 512x512 grid, h=1/512
+  c3  Fibonacci sphere N=262144, A_ij = delta_ij + w/(4 pi |x_i-x_j|), w=4pi/N
+  c4  as c2 with A_ij = delta_ij + h^2 (i/4) H0^(1)(kappa |x_i-x_j|), kappa=25,
+      complex128
+  c5  Fibonacci sphere N=1048576, c3's kernel
+
+Readings: cell centres ((i+1/2)h, (j+1/2)h) (SURVEY c.2
+#14); Fibonacci lattice z_i = 1-(2i+1)/N, phi_i = i*pi*(3-sqrt 5) (c.2 #15);
+A_ii = 1 exactly, no self term (c.2 #16, "The singularity
+... can be handled with an appropriate quadrature rule"); complex Gaussian
+(N(0,1) + i N(0,1))/sqrt 2 (c.2 #17).  Omega, Psi ~ N(0, I) per
+PAPER.md:128-131 (eq. rand_sample_setting).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+# Streams of the counter-keyed generator (SURVEY c.2 #18).
+STREAM_OMEGA = 0
+STREAM_PSI = 1
+STREAM_RHS = 2
+
+
+@dataclass(frozen=True)
+class Config:
+    name: str
+    geometry: str          # "grid2d" | "sphere"
+    n: int                 # grid side (grid2d) or number of points (sphere)
+    kernel: str            # "log2d" | "lap3d" | "helm2d"
+    dtype: str             # "f64" | "c128"
+    leaf: int = 64
+    eps: float = 1e-6
+    p: int = 640           # sample count (frozen per config)
+    seed: int = 1
+    kappa: float = 25.0
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def N(self) -> int:
+        return self.n * self.n if self.geometry == "grid2d" else self.n
+
+    @property
+    def d(self) -> int:
+        return 2 if self.geometry == "grid2d" else 3
+
+    @property
+    def is_complex(self) -> bool:
+        return self.dtype == "c128"
+
+    @property
+    def np_dtype(self):
+        return np.complex128 if self.is_complex else np.float64
+
+    def root(self):
+        """Root cube (lo, side) of the tree (SURVEY c.2 #12)."""
+        if self.geometry == "grid2d":
+            return np.zeros(2), 1.0
+        return -np.ones(3), 2.0
+
+    def scaled(self, n: int, p: int | None = None, **kw) -> "Config":
+        """Same workload family at another size (test cases)."""
+        return replace(self, name=f"{self.name}@{n}", n=n, p=p if p is not None else self.p, **kw)
+
+
+CONFIGS = {
+    "c1": Config("c1", "grid2d", 64, "log2d", "f64", p=640, seed=1),
+    "c2": Config("c2", "grid2d", 512, "log2d", "f64", p=640, seed=2),
+    "c3": Config("c3", "sphere", 262144, "lap3d", "f64", p=1216, seed=3),
+    "c4": Config("c4", "grid2d", 512, "helm2d", "c128", p=640, seed=4),
+    "c5": Config("c5", "sphere", 1048576, "lap3d", "f64", p=1216, seed=5),
+}
+
+
+# ----------------------------------------------------------------------------
+# point sets
+# ----------------------------------------------------------------------------
+def grid_points(n_side: int) -> np.ndarray:
+    """Cell centres of an n x n grid in [0,1]^2, row-major (x fastest)."""
+    h = 1.0 / n_side
+    c = (np.arange(n_side) + 0.5) * h
+    X, Yc = np.meshgrid(c, c, indexing="xy")
+    return np.stack([X.ravel(), Yc.ravel()], axis=1).astype(np.float64)
+
+
+def fibonacci_sphere(N: int) -> np.ndarray:
+    """Fibonacci lattice on the unit sphere (SURVEY c.2 #15)."""
+    i = np.arange(N, dtype=np.float64)
+    z = 1.0 - (2.0 * i + 1.0) / N
+    phi = i * (math.pi * (3.0 - math.sqrt(5.0)))
+    rho = np.sqrt(np.maximum(0.0, 1.0 - z * z))
+    return np.stack([rho * np.cos(phi), rho * np.sin(phi), z], axis=1)
+
+
+def points(cfg: Config) -> np.ndarray:
+    if cfg.geometry == "grid2d":
+        return grid_points(cfg.n)
+    return fibonacci_sphere(cfg.n)
+
+
+# ----------------------------------------------------------------------------
+# the operator A (black box)
+# ----------------------------------------------------------------------------
+def kernel_weight(cfg: Config) -> float:
+    if cfg.geometry == "grid2d":
+        h = 1.0 / cfg.n
+        return h * h
+    return 1.0 / cfg.N        # w/(4 pi) with w = 4 pi / N
+
+
+def kernel_block(cfg: Config, X: np.ndarray, rows: np.ndarray, cols: np.ndarray) -> np.ndarray:
+    """Dense block A[rows, cols] (original point indices) of the config's operator."""
+    rows = np.asarray(rows)
+    cols = np.asarray(cols)
+    xi = X[rows][:, None, :]
+    xj = X[cols][None, :, :]
+    r = np.sqrt(((xi - xj) ** 2).sum(-1))
+    same = rows[:, None] == cols[None, :]
+    rs = np.where(same, 1.0, r)
+    wgt = kernel_weight(cfg)
+    if cfg.kernel == "log2d":
+        K = wgt * np.log(rs)
+    elif cfg.kernel == "lap3d":
+        K = wgt / rs
+    elif cfg.kernel == "helm2d":
+        from scipy.special import hankel1
+        K = wgt * 0.25j * hankel1(0, cfg.kappa * rs)
+    else:
+        raise ValueError(cfg.kernel)
+    K = np.where(same, 0.0, K)
+    A = K + same.astype(np.float64)
+    return A.astype(cfg.np_dtype)
+
+
+def dense_matrix(cfg: Config, X: np.ndarray | None = None) -> np.ndarray:
+    """Full dense A (small N only)."""
+    if X is None:
+        X = points(cfg)
+    idx = np.arange(X.shape[0])
+    return kernel_block(cfg, X, idx, idx)
+
+
+# ----------------------------------------------------------------------------
+# seeded Gaussian test matrices
+# ----------------------------------------------------------------------------
+def _rng(seed: int, stream: int) -> np.random.Generator:
+    return np.random.Generator(np.random.Philox(np.random.SeedSequence([int(seed), int(stream)])))
+
+
+def gaussian(shape, seed: int, stream: int, is_complex: bool = False) -> np.ndarray:
+    """i.i.d. N(0,1) (real) or (N(0,1)+iN(0,1))/sqrt2 (complex), keyed by (seed, stream).
+
+    Rows index ORIGINAL point order; callers permute to tree order.
+    """
+    g = _rng(seed, stream)
+    if not is_complex:
+        return g.standard_normal(shape)
+    re = g.standard_normal(shape)
+    im = g.standard_normal(shape)
+    return (re + 1j * im) * (1.0 / math.sqrt(2.0))
+
+
+def test_matrices(cfg: Config, N: int | None = None, p: int | None = None):
+    """(Omega, Psi) of shape N x p in ORIGINAL point order."""
+    N = cfg.N if N is None else N
+    p = cfg.p if p is None else p
+    Om = gaussian((N, p), cfg.seed, STREAM_OMEGA, cfg.is_complex)
+    Ps = gaussian((N, p), cfg.seed, STREAM_PSI, cfg.is_complex)
+    return Om, Ps
+
+
+def rhs(cfg: Config, N: int | None = None, nrhs: int = 1) -> np.ndarray:
+    N = cfg.N if N is None else N
+    b = gaussian((N, nrhs), cfg.seed, STREAM_RHS, cfg.is_complex)
+    return b[:, 0] if nrhs == 1 else b
+
+
+def dense_samples(A: np.ndarray, Om: np.ndarray, Ps: np.ndarray):
+    """Y = A Omega, Z = A^* Psi for a small dense operator."""
+    return A @ Om, A.conj().T @ Ps
