@@ -1,0 +1,177 @@
+/*
+ * rsrs.h -- C ABI of the B200-native RSRS (randomized strong recursive
+ * skeletonization) hot path, arXiv 2311.01451 (Yesypenko & Martinsson).
+ *
+ * The library builds an invertible factorization K ~= A of an N x N
+ * rank-structured operator A that is known only through the samples
+ *     Y = A Omega,   Z = A^* Psi,   Omega, Psi ~ N(0, I)  (N x p)
+ * (PAPER.md:53-61, 128-131 eq. rand_sample_setting; 1180-1183 section 5),
+ * then applies K^-1 (solve) or K (apply).  All compute runs in the library's
+ * own sm_100a CUDA kernels; there is no CPU fallback: without a CUDA device
+ * every compute entry point returns RSRS_ERR_CUDA.
+ *
+ * Conventions shared by all entry points
+ *   - Every call returns rsrs_status; a human-readable message for the last
+ *     failure on the calling thread is returned by rsrs_last_error().
+ *     No C++ exception crosses this boundary.
+ *   - Handles (rsrs_tree, rsrs_factorization) are created by the library and freed
+ *     with the matching *_destroy; a factor keeps a reference to nothing the
+ *     caller owns (it copies what it needs from the tree).
+ *   - Real data (RSRS_F64) are IEEE doubles; complex data (RSRS_C128) are
+ *     interleaved {re, im} double pairs.  Matrices are ROW-MAJOR: element
+ *     (i, j) of an n x m matrix with leading dimension ld is at [i*ld + j]
+ *     (complex: at element index, i.e. byte offset 16*(i*ld + j)).
+ *   - "tree order": rows permuted so that each box's points are contiguous;
+ *     row t of a tree-ordered array holds original point perm[t]
+ *     (rsrs_tree_perm).
+ */
+#ifndef RSRS_H_
+#define RSRS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RSRS_OK = 0,
+  RSRS_ERR_INVALID = 1,   /* bad argument (null pointer, size, dtype, ld < p, ...) */
+  RSRS_ERR_SAMPLES = 2,   /* too few samples: p - r < k + l for some box (message names level/box/deficit) */
+  RSRS_ERR_SINGULAR = 3,  /* X_rr, the near-field Gram or the top block is numerically singular */
+  RSRS_ERR_CUDA = 4,      /* CUDA runtime failure or no device */
+  RSRS_ERR_NCCL = 5,      /* reserved for the multi-GPU path */
+  RSRS_ERR_NOMEM = 6,     /* device or host allocation failed */
+  RSRS_ERR_STATE = 7      /* call not valid in the handle's state (e.g. unsupported nranks) */
+} rsrs_status;
+
+typedef enum { RSRS_F64 = 0, RSRS_C128 = 1 } rsrs_dtype;
+
+typedef struct rsrs_tree_s* rsrs_tree;
+typedef struct rsrs_factor_s* rsrs_factorization;
+
+/* Options of rsrs_factor. */
+typedef struct {
+  double eps;          /* user tolerance epsilon ("atol at the leaf level") */
+  double level_growth; /* g: atol(l) = id_scale * eps * g^(L - l) ("successively relaxed") */
+  double id_scale;     /* c_id (default 1.0) */
+  int oversample;      /* l: require p - r >= k + l (default 10) */
+  int top_level;       /* last compressed level ("typically on level 2") */
+  int rank;            /* this process's rank; must be 0 in this build */
+  int nranks;          /* number of ranks; must be 1 in this build (RSRS_ERR_STATE otherwise) */
+  void* nccl_comm;     /* reserved (ncclComm_t), must be NULL */
+  void* stream;        /* cudaStream_t the factorization runs on (NULL = legacy default stream) */
+} rsrs_opts;
+
+/* Statistics of a factorization (Table 1). */
+typedef struct {
+  int64_t N, p;
+  int L, top_level, nlevels_compressed;
+  int64_t nsteps;            /* boxes eliminated (steps with |I_r| > 0) */
+  int64_t top_size;          /* |S| */
+  int64_t max_rank;          /* max k over boxes */
+  int64_t memory_scalars;    /* M: stored scalars of T, G_L, G_U, X_rr, A_SS */
+  double factor_ms;          /* device time of the last rsrs_factor (CUDA events) */
+  double flops_model;        /* algorithmic flop count (SURVEY 8(d) model, real-equivalent) */
+  double bytes_model;        /* algorithmic HBM bytes of the sweep */
+  int64_t launches;          /* kernels launched by the last rsrs_factor */
+} rsrs_stats;
+
+/* ---------------------------------------------------------------------------
+ * rsrs_build_tree -- uniform 2^d-tree (section 4.1; neighbours
+ * = boxes sharing an edge or corner, Fig. 1 caption PAPER.md:182-184).
+ *   pts       host, N x d row-major doubles (d in 1..3); not retained.
+ *   leaf_max  m: depth L = smallest L with max leaf occupancy <= m.
+ *   root_lo   host, d doubles, lower corner of the root cube (NULL: bounding cube).
+ *   root_side side of the root cube (ignored when root_lo == NULL).
+ *   nranks    number of Morton ranges to plan (1 in this build).
+ *   out       receives the handle.
+ * Errors: RSRS_ERR_INVALID (N < 1, d out of range, leaf_max < 1, depth > 20).
+ * Host-only integer work; safe without a GPU.
+ * ------------------------------------------------------------------------- */
+rsrs_status rsrs_build_tree(const double* pts, int64_t N, int d, int leaf_max,
+                            const double* root_lo, double root_side, int nranks,
+                            rsrs_tree* out);
+
+/* Depth L, dimension d and N of a tree. Any out pointer may be NULL. */
+rsrs_status rsrs_tree_info(rsrs_tree t, int* L, int* d, int64_t* N);
+
+/* perm[t] = original index of the point at tree position t (host, N int64). */
+rsrs_status rsrs_tree_perm(rsrs_tree t, int64_t* perm);
+
+/* Sizes of level `level` (0..L): number of nonempty boxes and total
+ * neighbour-list length. */
+rsrs_status rsrs_tree_level_size(rsrs_tree t, int level, int64_t* nboxes, int64_t* nnbr);
+
+/* Level arrays (host buffers sized from rsrs_tree_level_size; any may be NULL):
+ *   keys[nboxes]      Morton keys, ascending (bit b of coordinate i -> bit b*d+i)
+ *   start[nboxes+1]   tree-position ranges of the boxes' points
+ *   parent[nboxes]    index of the parent box on level-1 (-1 on level 0)
+ *   colour[nboxes]    sum_i (c_i mod 3) 3^i  (boxes of one colour are >= 3 apart)
+ *   nbr_off[nboxes+1], nbr[nnbr]  neighbour CSR (self included, Morton order) */
+rsrs_status rsrs_tree_level(rsrs_tree t, int level, uint64_t* keys, int64_t* start,
+                            int32_t* parent, int32_t* colour, int32_t* nbr_off, int32_t* nbr);
+
+/* Leaf-level sample-count bound max_b(r_b) + kmax_guess + oversample rounded up
+ * to a multiple of 32 ("p = (3m + k)", generalised; coarse levels
+ * are checked during the factorization). */
+rsrs_status rsrs_plan_samples(rsrs_tree t, int kmax_guess, int oversample, int64_t* p_min);
+
+void rsrs_tree_destroy(rsrs_tree t);
+
+/* ---------------------------------------------------------------------------
+ * rsrs_factor -- the level-by-level compress-and-eliminate sweep
+ * (section 5; per box: nullification 1195-1200,
+ * ID 613-666, extraction 1213-1218, elimination 934-955, sample updates
+ * 1205-1212 / 1219-1227 in the consistency-forced orientation, R1).
+ *   t                tree (only read; may be destroyed after the call returns)
+ *   dt               RSRS_F64 or RSRS_C128
+ *   p                number of samples (columns used of each array)
+ *   Y, Z, Omega, Psi DEVICE pointers, N x ld row-major, TREE order.  BORROWED
+ *                    AND OVERWRITTEN: the sweep updates them in place; their
+ *                    contents are unspecified on return.
+ *   ld               leading dimension (>= p, even)
+ *   opts             options (NULL: defaults eps=1e-6, g=1, c_id=1, l=10, top_level=2)
+ *   out              receives the factorization handle
+ * Synchronous: returns after the device work completes so that device-side
+ * errors can be reported.  Errors: RSRS_ERR_INVALID, RSRS_ERR_SAMPLES,
+ * RSRS_ERR_SINGULAR, RSRS_ERR_CUDA, RSRS_ERR_NOMEM, RSRS_ERR_STATE.
+ * ------------------------------------------------------------------------- */
+rsrs_status rsrs_factor(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, void* Z,
+                        void* Omega, void* Psi, int64_t ld, const rsrs_opts* opts,
+                        rsrs_factorization* out);
+
+/* ---------------------------------------------------------------------------
+ * rsrs_solve -- B <- K^-1 B, K = V_1..V_n A~_diag W_n..W_1 (PAPER.md:1130-1143,
+ * 958-960; elim inverse = sign toggle 572-575).
+ *   B     DEVICE, N x ldb row-major in ORIGINAL point order, nrhs columns used
+ *         (ldb >= nrhs); overwritten with the solution.
+ *   s     cudaStream_t (NULL = legacy default stream); stream-ordered, asynchronous.
+ * Errors: RSRS_ERR_INVALID (bad arguments), RSRS_ERR_CUDA.
+ * rsrs_apply -- X <- K X with the same layout.
+ * ------------------------------------------------------------------------- */
+rsrs_status rsrs_solve(rsrs_factorization f, void* B, int64_t ldb, int64_t nrhs, void* s);
+rsrs_status rsrs_apply(rsrs_factorization f, void* X, int64_t ldx, int64_t nrhs, void* s);
+
+/* Statistics of the factorization (host struct). */
+rsrs_status rsrs_factor_stats(rsrs_factorization f, rsrs_stats* st);
+
+/* Per-box ranks of a level (host, int32 per box of that level in Morton order):
+ * k = skeleton count, or -1 for an empty box; cap = capacity of k[]. */
+rsrs_status rsrs_factor_ranks(rsrs_factorization f, int level, int32_t* k, int64_t cap);
+
+/* Final skeleton set S (tree positions, host int64, ascending) and its size. */
+rsrs_status rsrs_factor_top(rsrs_factorization f, int64_t* S, int64_t cap, int64_t* size);
+
+void rsrs_factor_destroy(rsrs_factorization f);
+
+/* Message of the last failed call on this thread ("" if none). */
+const char* rsrs_last_error(void);
+
+/* Library version string. */
+const char* rsrs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSRS_H_ */

@@ -1,0 +1,101 @@
+// Device-side common definitions for the RSRS sm_100a kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#define RSRS_DI __device__ __forceinline__
+
+namespace rsrs {
+
+typedef long long i64;
+
+// FP64 tensor-core MMA (DMMA) m8n8k4, row.col: one A element per lane
+// (row = lane>>2, col = lane&3), one B element per lane (k = lane&3,
+// n = lane>>2), two accumulators per lane (row = lane>>2, cols 2*(lane&3)+{0,1}).
+RSRS_DI void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// 16-byte async copy global -> shared with zero fill beyond src_bytes (0, 8 or 16).
+RSRS_DI void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+RSRS_DI void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+RSRS_DI void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Per-box record of one (level, colour) batch.  Static fields are written by
+// the host planner; k, nr, nc, status by the device (ID kernel).
+struct BoxDev {
+  int nb, r, self_pos, row0;  // |I_b|, |near|, position of b inside near, first store row of b
+  int ldaug;                  // leading dimension of the augmented Gram (>= r, even)
+  int level, box;             // for error messages
+  int pad0;
+  i64 off_aug;                // doubles: Omega-side [C; B] ((r+nb) x ldaug); Psi side follows
+  i64 off_yz;                 // doubles: [Y'' Z''] (nb x ldyz)
+  i64 off_h;                  // doubles: H (nb x nb)
+  i64 off_xy, off_xz;         // doubles: X_Y, X_Z (nb x r each, ld r)
+  i64 off_xrc, off_xcr;       // doubles: X_rc (nb x r, ld r), X_cr (r x nb, ld nb)
+  i64 off_rows;               // ints: [near rows (r); b rows (nb)]
+  i64 off_skelrow, off_redrow, off_crow, off_cpos;  // ints: nb, nb, r, r
+  i64 f_T, f_GL, f_GU, f_Xrr, f_Xinv;  // doubles in the level factor pool
+  i64 f_red, f_skel, f_c;              // ints (tree positions) in the level index pool
+  int k, nr, nc, status;               // dynamic
+};
+
+// status codes in BoxDev::status (0 = ok)
+enum { ST_OK = 0, ST_SAMPLES = 1, ST_SINGULAR_GRAM = 2, ST_SINGULAR_XRR = 3, ST_TOO_BIG = 4 };
+
+// C = alpha * A_rows B_rows^T (m x n), K columns; rows gathered by index lists.
+// Tiles entirely above the diagonal of the leading sym_rows x sym_rows block
+// are skipped (symmetric Gram; only the lower triangle is consumed).
+struct NTDesc {
+  const double* A;
+  const int* rowA;  // nullptr: contiguous rows
+  i64 lda;
+  const double* B;
+  const int* rowB;
+  i64 ldb;
+  double* C;
+  i64 ldc;
+  int m, n, K, sym_rows;
+  double alpha;
+  const int* pm;  // optional device size overrides
+  const int* pn;
+};
+
+// D[rowD(i), j] = beta * Cin[rowC(i), j] + alpha * sum_k opA(i, k) B[rowB(k), j]
+// opA(i, k) = transA ? A[k*lda + i] : A[i*lda + k]
+struct NNDesc {
+  const double* A;
+  i64 lda;
+  int transA, pad;
+  const double* B;
+  const int* rowB;
+  i64 ldb;
+  double* D;
+  const int* rowD;
+  i64 ldd;
+  const double* Cin;  // nullptr: Cin = D (in place, rowC = rowD)
+  const int* rowC;
+  i64 ldc;
+  int m, n, K, pad2;
+  double alpha, beta;
+  const int* pm;  // optional device size overrides
+  const int* pn;
+  const int* pK;
+};
+
+struct CholDesc {  // augmented Cholesky of [C; B] ((r + mextra) x r), see kernels.cuh
+  double* A;
+  i64 lda;
+  int r, mextra;
+  int* status;
+};
+
+}  // namespace rsrs

@@ -1,0 +1,857 @@
+// RSRS factor driver (host C++) and the factor / solve / apply C ABI.
+//
+// The sweep (section 5) runs level by level
+// (L .. top_level), colour by colour; all boxes of one colour are processed by
+// one launch of each per-box kernel (boxes of one colour are >= 3 apart, so
+// their near sets are disjoint and the batch equals the sequential order,
+// DESIGN.md R10).  Per colour batch:
+//   gemm_nt      [Omega_near; Y_b] Omega_near^T, [Psi_near; Z_b] Psi_near^T
+//   chol_aug     L L^T = Gram, u = B L^-T
+//   trsm_back    W = u L^-1 = Y_b Omega_near^dagger
+//   gemm_nn      Y'' = Y_b - W Omega_near (= Y_b null(Omega_near) null^T)
+//   gemm_nt      H = [Y'' Z''][Y'' Z'']^T / (2w)
+//   id_kernel    skeletons, T
+//   gemm_nn      E/F sample updates
+//   extract_lu   X_{r,near}, X_{near,r}, LU(X_rr), X_rr^-1
+//   gemm_nn      G_U = X_rr^-1 X_rc, G_L = X_cr X_rr^-1
+//   gemm_nn      L/U sample updates
+// then compaction of the skeleton rows into the next level's store.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "dense.cuh"
+#include "gemm.cuh"
+#include "internal.h"
+#include "sweep.cuh"
+
+using rsrs::BoxDev;
+using rsrs::CholDesc;
+using rsrs::i64;
+using rsrs::NNDesc;
+using rsrs::NTDesc;
+
+namespace {
+
+struct CudaError {
+  std::string msg;
+};
+
+#define CK(x)                                                                                   \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess) throw CudaError{std::string(#x) + ": " + cudaGetErrorString(e_)};    \
+  } while (0)
+
+struct StatusError {
+  rsrs_status st;
+  std::string msg;
+};
+
+inline i64 even(i64 x) { return (x + 1) & ~1LL; }
+
+constexpr int SMEM_MAX = 227 * 1024 - 1024;  // dynamic-smem budget of the largest kernels
+
+int g_optin = 0;
+bool g_debug = false;  // RSRS_DEBUG_SYNC=1: synchronize and check after every launch
+
+template <class K>
+void set_smem(K kern, int want) {
+  cudaFuncAttributes fa;
+  CK(cudaFuncGetAttributes(&fa, kern));
+  const int mx = g_optin - (int)fa.sharedSizeBytes;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, want < 0 ? mx : std::min(want, mx)));
+}
+
+void init_kernels() {
+  static bool done = false;
+  if (done) return;
+  const char* dbg = getenv("RSRS_DEBUG_SYNC");
+  g_debug = dbg && dbg[0] == '1';
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&g_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  set_smem(rsrs::gemm_nt_kernel, rsrs::NT_SMEM);
+  set_smem(rsrs::gemm_nn_kernel, rsrs::NN_SMEM);
+  set_smem(rsrs::chol_aug_kernel<32>, -1);
+  set_smem(rsrs::chol_aug_kernel<16>, -1);
+  set_smem(rsrs::chol_aug_kernel<8>, -1);
+  set_smem(rsrs::id_kernel, -1);
+  set_smem(rsrs::extract_lu_kernel, -1);
+  set_smem(rsrs::solve_fwd_kernel, -1);
+  set_smem(rsrs::solve_bwd_kernel, -1);
+  set_smem(rsrs::apply_fwd_kernel, -1);
+  set_smem(rsrs::apply_bwd_kernel, -1);
+  set_smem(rsrs::top_solve_kernel, -1);
+  set_smem(rsrs::top_apply_kernel, -1);
+  // keep freed stream-ordered memory in the pool (repeated factorizations reuse it)
+  cudaMemPool_t pool;
+  CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t thr = UINT64_MAX;
+  CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  done = true;
+}
+
+// device buffer, stream-ordered
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaStream_t s = nullptr;
+  void alloc(size_t b, cudaStream_t st) {
+    release();
+    s = st;
+    bytes = b;
+    if (b) {
+      cudaError_t e = cudaMallocAsync(&p, b, st);
+      if (e != cudaSuccess) {
+        p = nullptr;
+        bytes = 0;
+        throw StatusError{RSRS_ERR_NOMEM, std::string("device allocation of ") + std::to_string(b) +
+                                              " bytes failed: " + cudaGetErrorString(e)};
+      }
+    }
+  }
+  void ensure(size_t b, cudaStream_t st) {
+    if (b > bytes) alloc(b, st);
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    bytes = 0;
+  }
+  ~DBuf() { release(); }
+  template <class T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+};
+
+
+void post(const char* name, cudaStream_t s, int64_t& launches) {
+  CK(cudaGetLastError());
+  ++launches;
+  if (g_debug) {
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) throw CudaError{std::string("kernel ") + name + ": " + cudaGetErrorString(e)};
+  }
+}
+
+int chol_nb(int m) {
+  if ((size_t)m * 36 * 8 <= (size_t)SMEM_MAX - 1024) return 32;
+  if ((size_t)m * 20 * 8 <= (size_t)SMEM_MAX - 1024) return 16;
+  if ((size_t)m * 12 * 8 <= (size_t)SMEM_MAX - 1024) return 8;
+  return 0;
+}
+
+void launch_chol(const CholDesc* d, int n, int mmax, cudaStream_t s, int64_t& launches) {
+  const int nb = chol_nb(mmax);
+  if (nb == 0) throw StatusError{RSRS_ERR_INVALID, "near field too large for the Cholesky panel (r + n_b = " +
+                                                       std::to_string(mmax) + ")"};
+  const size_t sm = (size_t)mmax * (nb + 4) * 8;
+  if (nb == 32) rsrs::chol_aug_kernel<32><<<n, 256, sm, s>>>(d);
+  else if (nb == 16) rsrs::chol_aug_kernel<16><<<n, 256, sm, s>>>(d);
+  else rsrs::chol_aug_kernel<8><<<n, 256, sm, s>>>(d);
+  post("chol_aug", s, launches);
+}
+
+void launch_nt(const NTDesc* d, int n, int mmax, int nmax, cudaStream_t s, int64_t& launches) {
+  if (n <= 0 || mmax <= 0 || nmax <= 0) return;
+  dim3 grid((nmax + 63) / 64, (mmax + 63) / 64, n);
+  rsrs::gemm_nt_kernel<<<grid, 128, rsrs::NT_SMEM, s>>>(d);
+  post("gemm_nt", s, launches);
+}
+
+void launch_nn(const NNDesc* d, int n, int mmax, int nmax, cudaStream_t s, int64_t& launches) {
+  if (n <= 0 || mmax <= 0 || nmax <= 0) return;
+  dim3 grid((nmax + 63) / 64, (mmax + 63) / 64, n);
+  rsrs::gemm_nn_kernel<<<grid, 128, rsrs::NN_SMEM, s>>>(d);
+  post("gemm_nn", s, launches);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+struct Batch {
+  int level = 0, colour = 0, nbox = 0;
+  BoxDev* d_boxes = nullptr;       // inside the level's box buffer
+  std::vector<BoxDev> h;
+  double* fpool = nullptr;         // the level's factor pools
+  int* ipool = nullptr;
+  int max_nb = 0, max_r = 0;
+};
+
+struct rsrs_factor_s {
+  rsrs_dtype dt = RSRS_F64;
+  int64_t N = 0, p = 0;
+  int L = 0, top_level = 2, d = 2;
+  std::vector<Batch> batches;
+  std::vector<std::unique_ptr<DBuf>> keep;        // factor-lifetime device buffers
+  std::vector<std::vector<int32_t>> ranks;        // [level][box] (-1 empty)
+  int nS = 0;
+  int ldS = 0;
+  int* d_S = nullptr;                             // tree positions of S
+  double* d_ASS = nullptr;                        // A~_SS
+  double* d_LU = nullptr;                         // LU of A~_SS
+  int* d_piv = nullptr;
+  std::vector<int64_t> S_host;
+  int64_t* d_perm = nullptr;
+  DBuf xtmp;
+  rsrs_stats stats{};
+  cudaStream_t stream = nullptr;
+};
+
+namespace {
+
+// algorithmic real flops of one box
+double model_flops_box(double NB, double R, double K, double P) {
+  const double nr = NB - K, nc = R - nr;
+  double f = 0;
+  f += 2 * (R * (R + 1) * P);                       // near-field Grams (symmetric), both sides
+  f += 2 * (2 * NB * R * P);                        // B = Y_b M^T
+  f += 2 * (R * R * R / 3.0);                       // Cholesky
+  f += 2 * (2 * NB * R * R);                        // u = B L^-T, W = u L^-1
+  f += 2 * (2 * NB * R * P);                        // Y'' = Y_b - W M
+  f += NB * (NB + 1) * 2 * P;                       // H (symmetric)
+  if (nr > 0) {
+    f += 4 * (2 * nr * K * P);                      // E/F updates
+    f += 2 * (2 * nr * K * R + 2 * nr * nr * K);    // extraction combinations
+    f += 2.0 * nr * nr * nr;                        // LU + inverse
+    f += 2 * (2 * nr * nr * nc);                    // G_U, G_L
+    f += 2 * (2 * nc * nr * P);                     // L/U updates
+  }
+  return f;
+}
+
+// algorithmic HBM bytes of one box (samples read/written once; factors written once)
+double model_bytes_box(double NB, double R, double K, double P) {
+  const double nr = NB - K, nc = R - nr;
+  double b = 2 * R * P + 2 * NB * P;                // near Omega/Psi rows, own Y/Z rows
+  if (nr > 0) b += 2 * 2 * nc * P + 2 * NB * P + nr * K + 2 * nc * nr + 2 * nr * nr;
+  return 8.0 * b;
+}
+
+struct Planner {
+  rsrs_factorization f;
+  const rsrs::Tree& T;
+  cudaStream_t s;
+  double eps = 1e-6, g = 1.0, cid = 1.0;
+  int l = 10;
+  int64_t launches = 0;
+  double flops = 0, bytes = 0;
+
+  Planner(rsrs_factorization f_, const rsrs::Tree& t, cudaStream_t st) : f(f_), T(t), s(st) {}
+
+  DBuf* keep(size_t nbytes) {
+    f->keep.emplace_back(new DBuf());
+    f->keep.back()->alloc(nbytes, s);
+    return f->keep.back().get();
+  }
+
+  void run(double* Y, double* Z, double* Om, double* Ps, i64 ld) {
+    const int L = T.L;
+    const int p = (int)f->p;
+    const int top = f->top_level;
+    const i64 nld = even(p);
+    DBuf store[2], gidx_buf[2];
+    int cur = -1;
+    std::vector<int> nb_box(T.levels[L].nboxes);
+    for (int64_t b = 0; b < T.levels[L].nboxes; ++b)
+      nb_box[b] = (int)(T.levels[L].start[b + 1] - T.levels[L].start[b]);
+    DBuf leaf_gidx;
+    {
+      std::vector<int> h(T.N);
+      for (int64_t i = 0; i < T.N; ++i) h[i] = (int)i;
+      leaf_gidx.alloc(sizeof(int) * T.N, s);
+      CK(cudaMemcpyAsync(leaf_gidx.p, h.data(), sizeof(int) * T.N, cudaMemcpyHostToDevice, s));
+      CK(cudaStreamSynchronize(s));
+    }
+    int* gidx = leaf_gidx.as<int>();
+    int64_t nrows = T.N;
+    DBuf ws, iws, descbuf, dstbuf;
+    f->ranks.assign(L + 1, std::vector<int32_t>());
+
+    for (int lev = L; lev >= top && lev >= 1; --lev) {
+      const rsrs::TreeLevel& lv = T.levels[lev];
+      const int nbox = (int)lv.nboxes;
+      const double atol = cid * eps * std::pow(g, (double)(L - lev));
+      std::vector<int> row0(nbox + 1, 0), rcount(nbox, 0), selfpos(nbox, 0);
+      for (int b = 0; b < nbox; ++b) row0[b + 1] = row0[b] + nb_box[b];
+      for (int b = 0; b < nbox; ++b) {
+        int r = 0;
+        for (int q = lv.nbr_off[b]; q < lv.nbr_off[b + 1]; ++q) {
+          const int j = lv.nbr[q];
+          if (j == b) selfpos[b] = r;
+          r += nb_box[j];
+        }
+        rcount[b] = r;
+        if (nb_box[b] > 0 && p - r < l + 1) {
+          std::ostringstream os;
+          os << "level " << lev << " box " << b << ": p - r = " << p - r << " < l + 1 = " << l + 1
+             << " (deficit " << (l + 1) - (p - r) << " samples)";
+          throw StatusError{RSRS_ERR_SAMPLES, os.str()};
+        }
+        if (nb_box[b] > 160) {
+          std::ostringstream os;
+          os << "level " << lev << " box " << b << ": |I_b| = " << nb_box[b] << " exceeds 160";
+          throw StatusError{RSRS_ERR_INVALID, os.str()};
+        }
+      }
+      int ncol = 1;
+      for (int i = 0; i < T.d; ++i) ncol *= 3;
+      std::vector<std::vector<int>> bycol(ncol);
+      for (int b = 0; b < nbox; ++b)
+        if (nb_box[b] > 0) bycol[lv.colour[b]].push_back(b);
+
+      // ---- host layout of the level --------------------------------------
+      std::vector<BoxDev> hb;
+      hb.reserve(nbox);
+      struct BInfo {
+        int first, count, max_nb, max_r, max_m;
+      };
+      std::vector<BInfo> binfo;
+      i64 foff = 0, fioff = 0, ioff = 0, ws_need = 0;
+      for (int c = 0; c < ncol; ++c) {
+        if (bycol[c].empty()) continue;
+        BInfo bi{(int)hb.size(), (int)bycol[c].size(), 0, 0, 0};
+        i64 wo = 0;
+        for (int b : bycol[c]) {
+          BoxDev x;
+          std::memset(&x, 0, sizeof(x));
+          const i64 nb = nb_box[b], r = rcount[b];
+          const i64 ldn = even(nb), ldr = even(r);
+          x.nb = (int)nb;
+          x.r = (int)r;
+          x.self_pos = selfpos[b];
+          x.row0 = row0[b];
+          x.ldaug = (int)ldr;
+          x.level = lev;
+          x.box = b;
+          x.off_aug = wo;   wo += 2 * (r + nb) * ldr;
+          x.off_yz = wo;    wo += nb * 2 * nld;
+          x.off_h = wo;     wo += nb * ldn;
+          x.off_xy = wo;    wo += even(nb * r);
+          x.off_xz = wo;    wo += even(nb * r);
+          x.off_xrc = wo;   wo += nb * ldr;
+          x.off_xcr = wo;   wo += r * ldn;
+          x.off_rows = ioff;    ioff += r + nb;
+          x.off_skelrow = ioff; ioff += nb;
+          x.off_redrow = ioff;  ioff += nb;
+          x.off_crow = ioff;    ioff += r;
+          x.off_cpos = ioff;    ioff += r;
+          x.f_T = foff;     foff += nb * ldn;
+          x.f_GL = foff;    foff += r * ldn;
+          x.f_GU = foff;    foff += nb * ldr;
+          x.f_Xrr = foff;   foff += nb * ldn;
+          x.f_Xinv = foff;  foff += nb * ldn;
+          x.f_red = fioff;  fioff += nb;
+          x.f_skel = fioff; fioff += nb;
+          x.f_c = fioff;    fioff += r;
+          hb.push_back(x);
+          bi.max_nb = std::max<int>(bi.max_nb, (int)nb);
+          bi.max_r = std::max<int>(bi.max_r, (int)r);
+          bi.max_m = std::max<int>(bi.max_m, (int)(r + nb));
+        }
+        ws_need = std::max(ws_need, wo);
+        binfo.push_back(bi);
+      }
+      DBuf* fpool_b = keep(sizeof(double) * std::max<i64>(foff, 2));
+      DBuf* ipool_b = keep(sizeof(int) * std::max<i64>(fioff, 2));
+      DBuf* boxes_b = keep(sizeof(BoxDev) * std::max<size_t>(hb.size(), 1));
+      double* fpool = fpool_b->as<double>();
+      int* ipool = ipool_b->as<int>();
+      BoxDev* dboxes = boxes_b->as<BoxDev>();
+      ws.ensure(sizeof(double) * std::max<i64>(ws_need, 2), s);
+      iws.ensure(sizeof(int) * std::max<i64>(ioff, 2), s);
+      double* dws = ws.as<double>();
+      int* diws = iws.as<int>();
+      {
+        std::vector<int> hrows(std::max<i64>(ioff, 1), 0);
+        for (const BoxDev& x : hb) {
+          int o = (int)x.off_rows;
+          const int b = x.box;
+          for (int q = lv.nbr_off[b]; q < lv.nbr_off[b + 1]; ++q) {
+            const int j = lv.nbr[q];
+            for (int t = 0; t < nb_box[j]; ++t) hrows[o++] = row0[j] + t;
+          }
+          for (int t = 0; t < x.nb; ++t) hrows[o++] = x.row0 + t;
+        }
+        CK(cudaMemcpyAsync(diws, hrows.data(), sizeof(int) * ioff, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(dboxes, hb.data(), sizeof(BoxDev) * hb.size(), cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
+      }
+
+      // ---- descriptors --------------------------------------------------
+      std::vector<NTDesc> nt_gram, nt_h;
+      std::vector<NNDesc> nn_proj, nn_ef, nn_g, nn_upd;
+      std::vector<CholDesc> chol;
+      for (size_t q = 0; q < hb.size(); ++q) {
+        const BoxDev& x = hb[q];
+        BoxDev* dx = dboxes + q;
+        const int nb = x.nb, r = x.r;
+        const i64 ldr = x.ldaug, ldn = even(nb);
+        const int* near = diws + x.off_rows;
+        const int* brows = near + r;
+        double* augO = dws + x.off_aug;
+        double* augP = augO + (i64)(r + nb) * ldr;
+        NTDesc a{};
+        a.A = Om; a.rowA = near; a.lda = ld; a.B = Om; a.rowB = near; a.ldb = ld;
+        a.C = augO; a.ldc = ldr; a.m = r; a.n = r; a.K = p; a.sym_rows = r; a.alpha = 1.0;
+        nt_gram.push_back(a);
+        a.A = Ps; a.B = Ps; a.C = augP;
+        nt_gram.push_back(a);
+        NTDesc bq{};
+        bq.A = Y; bq.rowA = brows; bq.lda = ld; bq.B = Om; bq.rowB = near; bq.ldb = ld;
+        bq.C = augO + (i64)r * ldr; bq.ldc = ldr; bq.m = nb; bq.n = r; bq.K = p; bq.sym_rows = 0; bq.alpha = 1.0;
+        nt_gram.push_back(bq);
+        bq.A = Z; bq.B = Ps; bq.C = augP + (i64)r * ldr;
+        nt_gram.push_back(bq);
+        chol.push_back(CholDesc{augO, ldr, r, nb, &dx->status});
+        chol.push_back(CholDesc{augP, ldr, r, nb, &dx->status});
+        double* yz = dws + x.off_yz;
+        NNDesc pr{};
+        pr.A = augO + (i64)r * ldr; pr.lda = ldr; pr.transA = 0;
+        pr.B = Om; pr.rowB = near; pr.ldb = ld;
+        pr.D = yz; pr.rowD = nullptr; pr.ldd = 2 * nld;
+        pr.Cin = Y + (i64)x.row0 * ld; pr.rowC = nullptr; pr.ldc = ld;
+        pr.m = nb; pr.n = p; pr.K = r; pr.alpha = -1.0; pr.beta = 1.0;
+        nn_proj.push_back(pr);
+        pr.A = augP + (i64)r * ldr; pr.B = Ps; pr.D = yz + nld; pr.Cin = Z + (i64)x.row0 * ld;
+        nn_proj.push_back(pr);
+        NTDesc h{};
+        h.A = yz; h.rowA = nullptr; h.lda = 2 * nld; h.B = yz; h.rowB = nullptr; h.ldb = 2 * nld;
+        h.C = dws + x.off_h; h.ldc = ldn; h.m = nb; h.n = nb; h.K = (int)(2 * nld); h.sym_rows = 0;
+        h.alpha = 1.0 / (2.0 * (double)(p - r));
+        nt_h.push_back(h);
+        const int* skelrow = diws + x.off_skelrow;
+        const int* redrow = diws + x.off_redrow;
+        double* Tm = fpool + x.f_T;
+        NNDesc e{};
+        e.A = Tm; e.lda = ldn; e.transA = 0; e.B = Y; e.rowB = skelrow; e.ldb = ld;
+        e.D = Y; e.rowD = redrow; e.ldd = ld; e.Cin = nullptr;
+        e.m = nb; e.n = p; e.K = nb; e.alpha = -1.0; e.beta = 1.0; e.pm = &dx->nr; e.pK = &dx->k;
+        nn_ef.push_back(e);
+        e.B = Z; e.D = Z;
+        nn_ef.push_back(e);
+        NNDesc fo{};
+        fo.A = Tm; fo.lda = ldn; fo.transA = 1; fo.B = Om; fo.rowB = redrow; fo.ldb = ld;
+        fo.D = Om; fo.rowD = skelrow; fo.ldd = ld; fo.Cin = nullptr;
+        fo.m = nb; fo.n = p; fo.K = nb; fo.alpha = 1.0; fo.beta = 1.0; fo.pm = &dx->k; fo.pK = &dx->nr;
+        nn_ef.push_back(fo);
+        fo.B = Ps; fo.D = Ps;
+        nn_ef.push_back(fo);
+        NNDesc gu{};
+        gu.A = fpool + x.f_Xinv; gu.lda = ldn; gu.B = dws + x.off_xrc; gu.rowB = nullptr; gu.ldb = ldr;
+        gu.D = fpool + x.f_GU; gu.ldd = ldr; gu.Cin = nullptr; gu.m = nb; gu.n = r; gu.K = nb;
+        gu.alpha = 1.0; gu.beta = 0.0; gu.pm = &dx->nr; gu.pn = &dx->nc; gu.pK = &dx->nr;
+        nn_g.push_back(gu);
+        NNDesc gl{};
+        gl.A = dws + x.off_xcr; gl.lda = ldn; gl.B = fpool + x.f_Xinv; gl.rowB = nullptr; gl.ldb = ldn;
+        gl.D = fpool + x.f_GL; gl.ldd = ldn; gl.Cin = nullptr; gl.m = r; gl.n = nb; gl.K = nb;
+        gl.alpha = 1.0; gl.beta = 0.0; gl.pm = &dx->nc; gl.pn = &dx->nr; gl.pK = &dx->nr;
+        nn_g.push_back(gl);
+        const int* crow = diws + x.off_crow;
+        NNDesc u{};
+        u.A = fpool + x.f_GL; u.lda = ldn; u.transA = 0; u.B = Y; u.rowB = redrow; u.ldb = ld;
+        u.D = Y; u.rowD = crow; u.ldd = ld; u.Cin = nullptr; u.m = r; u.n = p; u.K = nb;
+        u.alpha = -1.0; u.beta = 1.0; u.pm = &dx->nc; u.pK = &dx->nr;
+        nn_upd.push_back(u);
+        NNDesc uz = u;
+        uz.A = fpool + x.f_GU; uz.lda = ldr; uz.transA = 1; uz.B = Z; uz.D = Z;
+        nn_upd.push_back(uz);
+      }
+      std::vector<char> hdesc;
+      auto put = [&](const void* src, size_t n) {
+        const size_t at = hdesc.size();
+        hdesc.resize(at + ((n + 15) & ~size_t(15)));
+        if (n) std::memcpy(hdesc.data() + at, src, n);
+        return at;
+      };
+      const size_t o_gram = put(nt_gram.data(), sizeof(NTDesc) * nt_gram.size());
+      const size_t o_h = put(nt_h.data(), sizeof(NTDesc) * nt_h.size());
+      const size_t o_proj = put(nn_proj.data(), sizeof(NNDesc) * nn_proj.size());
+      const size_t o_ef = put(nn_ef.data(), sizeof(NNDesc) * nn_ef.size());
+      const size_t o_g = put(nn_g.data(), sizeof(NNDesc) * nn_g.size());
+      const size_t o_upd = put(nn_upd.data(), sizeof(NNDesc) * nn_upd.size());
+      const size_t o_chol = put(chol.data(), sizeof(CholDesc) * chol.size());
+      descbuf.ensure(hdesc.size() + 16, s);
+      CK(cudaMemcpyAsync(descbuf.p, hdesc.data(), hdesc.size(), cudaMemcpyHostToDevice, s));
+      CK(cudaStreamSynchronize(s));
+      const char* dd = descbuf.as<char>();
+      const NTDesc* Dgram = reinterpret_cast<const NTDesc*>(dd + o_gram);
+      const NTDesc* Dh = reinterpret_cast<const NTDesc*>(dd + o_h);
+      const NNDesc* Dproj = reinterpret_cast<const NNDesc*>(dd + o_proj);
+      const NNDesc* Def = reinterpret_cast<const NNDesc*>(dd + o_ef);
+      const NNDesc* Dg = reinterpret_cast<const NNDesc*>(dd + o_g);
+      const NNDesc* Dupd = reinterpret_cast<const NNDesc*>(dd + o_upd);
+      const CholDesc* Dchol = reinterpret_cast<const CholDesc*>(dd + o_chol);
+
+      // ---- colour batches --------------------------------------------------
+      for (const BInfo& bi : binfo) {
+        const int n = bi.count, q0 = bi.first;
+        BoxDev* dbx = dboxes + q0;
+        launch_nt(Dgram + 4 * q0, 4 * n, bi.max_r, bi.max_r, s, launches);
+        launch_chol(Dchol + 2 * q0, 2 * n, bi.max_m, s, launches);
+        rsrs::trsm_back_kernel<<<2 * n, 256, 0, s>>>(Dchol + 2 * q0);
+        post("trsm_back_kernel", s, launches);
+        launch_nn(Dproj + 2 * q0, 2 * n, bi.max_nb, p, s, launches);
+        launch_nt(Dh + q0, n, bi.max_nb, bi.max_nb, s, launches);
+        {
+          const size_t sm = (size_t)bi.max_nb * (bi.max_nb + 1) * 8 + 3 * (size_t)bi.max_nb * 4 + 64;
+          rsrs::id_kernel<<<n, 256, sm, s>>>(dbx, dws, diws, fpool, ipool, gidx, atol * atol, p, l);
+          post("id_kernel", s, launches);
+        }
+        launch_nn(Def + 4 * q0, 4 * n, bi.max_nb, p, s, launches);
+        {
+          const size_t sm = 2 * (size_t)bi.max_nb * (bi.max_nb + 1) * 8 + 3 * (size_t)bi.max_nb * 4 + 64;
+          rsrs::extract_lu_kernel<<<n, 256, sm, s>>>(dbx, dws, diws, fpool);
+          post("extract_lu_kernel", s, launches);
+        }
+        launch_nn(Dg + 2 * q0, 2 * n, bi.max_r, bi.max_r, s, launches);
+        launch_nn(Dupd + 2 * q0, 2 * n, bi.max_r, p, s, launches);
+      }
+      CK(cudaMemcpyAsync(hb.data(), dboxes, sizeof(BoxDev) * hb.size(), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      std::vector<int> newk(nbox, 0);
+      f->ranks[lev].assign(nbox, -1);
+      for (const BoxDev& x : hb) {
+        if (x.status != rsrs::ST_OK) {
+          std::ostringstream os;
+          rsrs_status st = RSRS_ERR_SINGULAR;
+          if (x.status == rsrs::ST_SAMPLES) {
+            st = RSRS_ERR_SAMPLES;
+            os << "level " << x.level << " box " << x.box << ": rank " << x.k << " > p - r - l = "
+               << (p - x.r - l) << " (deficit " << x.k - (p - x.r - l) << " samples)";
+          } else if (x.status == rsrs::ST_SINGULAR_GRAM) {
+            os << "level " << x.level << " box " << x.box << ": near-field Gram not positive definite";
+          } else {
+            os << "level " << x.level << " box " << x.box << ": X_rr singular";
+          }
+          throw StatusError{st, os.str()};
+        }
+        newk[x.box] = x.k;
+        f->ranks[lev][x.box] = x.k;
+        f->stats.max_rank = std::max<int64_t>(f->stats.max_rank, x.k);
+        if (x.nr > 0) {
+          f->stats.nsteps++;
+          f->stats.memory_scalars += (int64_t)x.nr * x.k + 2LL * x.nr * x.nc + (int64_t)x.nr * x.nr;
+        }
+        flops += model_flops_box(x.nb, x.r, x.k, p);
+        bytes += model_bytes_box(x.nb, x.r, x.k, p);
+      }
+      for (const BInfo& bi : binfo) {
+        Batch B;
+        B.level = lev;
+        B.colour = T.levels[lev].colour[hb[bi.first].box];
+        B.nbox = bi.count;
+        B.d_boxes = dboxes + bi.first;
+        B.h.assign(hb.begin() + bi.first, hb.begin() + bi.first + bi.count);
+        B.fpool = fpool;
+        B.ipool = ipool;
+        B.max_nb = bi.max_nb;
+        B.max_r = bi.max_r;
+        f->batches.push_back(std::move(B));
+      }
+      // ---- merge: skeleton rows into the parent level's store
+      const rsrs::TreeLevel& pl = T.levels[lev - 1];
+      std::vector<int> pnb(pl.nboxes, 0);
+      for (int b = 0; b < nbox; ++b) pnb[lv.parent[b]] += newk[b];
+      std::vector<int> pref(nbox + 1, 0);
+      for (int b = 0; b < nbox; ++b) pref[b + 1] = pref[b] + newk[b];
+      const int64_t nnew = pref[nbox];
+      std::vector<int> dst0(hb.size());
+      for (size_t q = 0; q < hb.size(); ++q) dst0[q] = pref[hb[q].box];
+      const int nxt = (cur == 0) ? 1 : 0;
+      store[nxt].ensure(sizeof(double) * std::max<i64>(2, 4 * nnew * nld), s);
+      gidx_buf[nxt].ensure(sizeof(int) * std::max<int64_t>(2, nnew), s);
+      double* nY = store[nxt].as<double>();
+      double* nZ = nY + nnew * nld;
+      double* nO = nZ + nnew * nld;
+      double* nP = nO + nnew * nld;
+      int* ng = gidx_buf[nxt].as<int>();
+      if (nnew > 0) {
+        dstbuf.ensure(sizeof(int) * dst0.size(), s);
+        CK(cudaMemcpyAsync(dstbuf.p, dst0.data(), sizeof(int) * dst0.size(), cudaMemcpyHostToDevice, s));
+        dim3 grid((unsigned)hb.size(), 4);
+        rsrs::compact_kernel<<<grid, 128, 0, s>>>(dboxes, diws, dstbuf.as<int>(), Y, Z, Om, Ps, ld, gidx, nY, nZ,
+                                                 nO, nP, nld, ng, p);
+        post("compact_kernel", s, launches);
+        bytes += 2.0 * 4 * nnew * p * 8;
+        CK(cudaStreamSynchronize(s));
+      }
+      Y = nY; Z = nZ; Om = nO; Ps = nP; ld = nld;
+      gidx = ng;
+      cur = nxt;
+      nrows = nnew;
+      nb_box = pnb;
+      f->stats.nlevels_compressed++;
+    }
+    finish_top(Y, Om, ld, gidx, (int)nrows);
+    f->stats.flops_model = flops;
+    f->stats.bytes_model = bytes;
+    f->stats.launches = launches;
+  }
+
+  // A~_SS = Y_S Omega_S^dagger, LU with partial pivoting
+  void finish_top(double* Y, double* Om, i64 ld, const int* gidx, int nS) {
+    f->nS = nS;
+    f->stats.top_size = nS;
+    if (nS == 0) return;
+    const int p = (int)f->p;
+    if (nS + l > p) {
+      std::ostringstream os;
+      os << "top block |S| = " << nS << " needs p >= |S| + l = " << nS + l << " (deficit " << nS + l - p
+         << " samples)";
+      throw StatusError{RSRS_ERR_SAMPLES, os.str()};
+    }
+    const i64 ldS = even(nS);
+    f->ldS = (int)ldS;
+    DBuf aug;
+    aug.alloc(sizeof(double) * 2 * nS * ldS, s);
+    DBuf* Sb = keep(sizeof(int) * nS);
+    DBuf* Ab = keep(sizeof(double) * nS * ldS);
+    DBuf* LUb = keep(sizeof(double) * nS * ldS);
+    DBuf* pv = keep(sizeof(int) * nS);
+    DBuf* st = keep(sizeof(int) * 4);
+    f->d_S = Sb->as<int>();
+    f->d_ASS = Ab->as<double>();
+    f->d_LU = LUb->as<double>();
+    f->d_piv = pv->as<int>();
+    CK(cudaMemcpyAsync(f->d_S, gidx, sizeof(int) * nS, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemsetAsync(st->p, 0, sizeof(int) * 4, s));
+    int* dstat = st->as<int>();
+    NTDesc hd[2]{};
+    hd[0].A = Om; hd[0].rowA = nullptr; hd[0].lda = ld; hd[0].B = Om; hd[0].rowB = nullptr; hd[0].ldb = ld;
+    hd[0].C = aug.as<double>(); hd[0].ldc = ldS; hd[0].m = nS; hd[0].n = nS; hd[0].K = p; hd[0].sym_rows = nS;
+    hd[0].alpha = 1.0;
+    hd[1] = hd[0];
+    hd[1].A = Y; hd[1].C = aug.as<double>() + (i64)nS * ldS; hd[1].sym_rows = 0;
+    CholDesc cd{aug.as<double>(), ldS, nS, nS, dstat};
+    DBuf dbuf;
+    dbuf.alloc(sizeof(hd) + sizeof(cd) + 64, s);
+    std::vector<char> h(sizeof(hd) + 16 + sizeof(cd));
+    std::memcpy(h.data(), hd, sizeof(hd));
+    const size_t oc = (sizeof(hd) + 15) & ~size_t(15);
+    std::memcpy(h.data() + oc, &cd, sizeof(cd));
+    CK(cudaMemcpyAsync(dbuf.p, h.data(), oc + sizeof(cd), cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    const NTDesc* dnt = dbuf.as<NTDesc>();
+    const CholDesc* dch = reinterpret_cast<const CholDesc*>(dbuf.as<char>() + oc);
+    launch_nt(dnt, 2, nS, nS, s, launches);
+    launch_chol(dch, 1, 2 * nS, s, launches);
+    rsrs::trsm_back_kernel<<<1, 256, 0, s>>>(dch);
+    post("trsm_back_kernel", s, launches);
+    CK(cudaMemcpy2DAsync(f->d_ASS, sizeof(double) * ldS, aug.as<double>() + (i64)nS * ldS, sizeof(double) * ldS,
+                         sizeof(double) * nS, nS, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpy2DAsync(f->d_LU, sizeof(double) * ldS, f->d_ASS, sizeof(double) * ldS, sizeof(double) * nS, nS,
+                         cudaMemcpyDeviceToDevice, s));
+    rsrs::top_lu_kernel<<<1, 1024, 0, s>>>(f->d_LU, ldS, nS, f->d_piv, dstat);
+    post("top_lu_kernel", s, launches);
+    int hst[4];
+    CK(cudaMemcpyAsync(hst, dstat, sizeof(hst), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (hst[0] != 0)
+      throw StatusError{RSRS_ERR_SINGULAR, hst[0] == rsrs::ST_SINGULAR_GRAM ? "top block: Gram of Omega_S not positive definite"
+                                                                            : "top block A~_SS singular"};
+    f->S_host.resize(nS);
+    std::vector<int> tmp(nS);
+    CK(cudaMemcpy(tmp.data(), f->d_S, sizeof(int) * nS, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < nS; ++i) f->S_host[i] = tmp[i];
+    f->stats.memory_scalars += (int64_t)nS * nS;
+    const double n = nS;
+    flops += n * (n + 1) * p + 2 * n * n * p + n * n * n / 3 + 2 * n * n * n + 2 * n * n * n / 3;
+  }
+};
+
+rsrs_status fail(rsrs_status st, const std::string& msg) {
+  rsrs::set_error(msg);
+  return st;
+}
+
+}  // namespace
+
+extern "C" {
+
+rsrs_status rsrs_factor(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, void* Z, void* Omega, void* Psi,
+                        int64_t ld, const rsrs_opts* opts, rsrs_factorization* out) {
+  rsrs::clear_error();
+  if (!out) return fail(RSRS_ERR_INVALID, "rsrs_factor: out is NULL");
+  *out = nullptr;
+  if (!t || !Y || !Z || !Omega || !Psi) return fail(RSRS_ERR_INVALID, "rsrs_factor: null argument");
+  if (p < 1 || ld < p || (ld & 1)) return fail(RSRS_ERR_INVALID, "rsrs_factor: need 1 <= p <= ld and ld even");
+  if (dt != RSRS_F64) return fail(RSRS_ERR_STATE, "rsrs_factor: RSRS_C128 is not built in this version");
+  rsrs_opts o{1e-6, 1.0, 1.0, 10, 2, 0, 1, nullptr, nullptr};
+  if (opts) o = *opts;
+  if (o.nranks != 1 || o.rank != 0 || o.nccl_comm)
+    return fail(RSRS_ERR_STATE, "rsrs_factor: only nranks == 1 is supported by this build");
+  if (!(o.eps > 0) || !(o.level_growth > 0) || !(o.id_scale > 0) || o.oversample < 0 || o.top_level < 1)
+    return fail(RSRS_ERR_INVALID, "rsrs_factor: invalid options");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(RSRS_ERR_CUDA, "rsrs_factor: no CUDA device (there is no CPU fallback)");
+  rsrs_factorization f = nullptr;
+  try {
+    init_kernels();
+    f = new rsrs_factor_s();
+    const rsrs::Tree& T = t->t;
+    f->dt = dt;
+    f->N = T.N;
+    f->p = p;
+    f->L = T.L;
+    f->d = T.d;
+    f->top_level = o.top_level;
+    f->stream = (cudaStream_t)o.stream;
+    cudaStream_t s = f->stream;
+    f->stats.N = T.N;
+    f->stats.p = p;
+    f->stats.L = T.L;
+    f->stats.top_level = o.top_level;
+    // tree -> original permutation on the device (solve / apply)
+    f->keep.emplace_back(new DBuf());
+    f->keep.back()->alloc(sizeof(int64_t) * T.N, s);
+    f->d_perm = f->keep.back()->as<int64_t>();
+    CK(cudaMemcpyAsync(f->d_perm, T.perm.data(), sizeof(int64_t) * T.N, cudaMemcpyHostToDevice, s));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, s));
+    Planner P(f, T, s);
+    P.eps = o.eps;
+    P.g = o.level_growth;
+    P.cid = o.id_scale;
+    P.l = o.oversample;
+    P.run((double*)Y, (double*)Z, (double*)Omega, (double*)Psi, ld);
+    CK(cudaEventRecord(e1, s));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    f->stats.factor_ms = ms;
+    *out = f;
+    return RSRS_OK;
+  } catch (const StatusError& e) {
+    delete f;
+    return fail(e.st, "rsrs_factor: " + e.msg);
+  } catch (const CudaError& e) {
+    delete f;
+    return fail(RSRS_ERR_CUDA, "rsrs_factor: " + e.msg);
+  } catch (const std::bad_alloc&) {
+    delete f;
+    return fail(RSRS_ERR_NOMEM, "rsrs_factor: out of host memory");
+  }
+}
+
+static rsrs_status sweep(rsrs_factorization f, void* Bv, int64_t ldb, int64_t nrhs, void* sv, bool solve) {
+  rsrs::clear_error();
+  const char* who = solve ? "rsrs_solve" : "rsrs_apply";
+  if (!f || !Bv) return fail(RSRS_ERR_INVALID, std::string(who) + ": null argument");
+  if (nrhs < 1 || ldb < nrhs) return fail(RSRS_ERR_INVALID, std::string(who) + ": need 1 <= nrhs <= ldb");
+  cudaStream_t s = (cudaStream_t)sv;
+  try {
+    double* B = (double*)Bv;
+    const int64_t N = f->N;
+    f->xtmp.ensure(sizeof(double) * N * nrhs, s);
+    double* x = f->xtmp.as<double>();
+    const int nr = (int)nrhs;
+    {
+      dim3 blk(32, 8);
+      dim3 grid((unsigned)((N + 7) / 8));
+      rsrs::permute_rows_kernel<<<grid, blk, 0, s>>>(B, ldb, x, nrhs, f->d_perm, N, nr, 0);
+      CK(cudaGetLastError());
+    }
+    if (solve) {
+      for (const Batch& b : f->batches) {
+        const size_t sm = sizeof(double) * 2 * (b.max_nb + 2);
+        rsrs::solve_fwd_kernel<<<b.nbox, 256, sm, s>>>(b.d_boxes, b.fpool, b.ipool, x, nrhs, nr);
+        CK(cudaGetLastError());
+      }
+      if (f->nS > 0) {
+        rsrs::top_solve_kernel<<<1, 1024, sizeof(double) * f->nS, s>>>(f->d_LU, f->ldS, f->nS, f->d_piv, f->d_S,
+                                                                       x, nrhs, nr);
+        CK(cudaGetLastError());
+      }
+      for (auto it = f->batches.rbegin(); it != f->batches.rend(); ++it) {
+        const size_t sm = sizeof(double) * (it->max_r + it->max_nb + 4);
+        rsrs::solve_bwd_kernel<<<it->nbox, 256, sm, s>>>(it->d_boxes, it->fpool, it->ipool, x, nrhs, nr);
+        CK(cudaGetLastError());
+      }
+    } else {
+      for (const Batch& b : f->batches) {
+        const size_t sm = sizeof(double) * (b.max_r + 2 * b.max_nb + 4);
+        rsrs::apply_fwd_kernel<<<b.nbox, 256, sm, s>>>(b.d_boxes, b.fpool, b.ipool, x, nrhs, nr);
+        CK(cudaGetLastError());
+      }
+      if (f->nS > 0) {
+        rsrs::top_apply_kernel<<<1, 1024, sizeof(double) * f->nS, s>>>(f->d_ASS, f->ldS, f->nS, f->d_S, x, nrhs,
+                                                                       nr);
+        CK(cudaGetLastError());
+      }
+      for (auto it = f->batches.rbegin(); it != f->batches.rend(); ++it) {
+        const size_t sm = sizeof(double) * (2 * it->max_nb + 4);
+        rsrs::apply_bwd_kernel<<<it->nbox, 256, sm, s>>>(it->d_boxes, it->fpool, it->ipool, x, nrhs, nr);
+        CK(cudaGetLastError());
+      }
+    }
+    {
+      dim3 blk(32, 8);
+      dim3 grid((unsigned)((N + 7) / 8));
+      rsrs::permute_rows_kernel<<<grid, blk, 0, s>>>(x, nrhs, B, ldb, f->d_perm, N, nr, 1);
+      CK(cudaGetLastError());
+    }
+    return RSRS_OK;
+  } catch (const StatusError& e) {
+    return fail(e.st, std::string(who) + ": " + e.msg);
+  } catch (const CudaError& e) {
+    return fail(RSRS_ERR_CUDA, std::string(who) + ": " + e.msg);
+  }
+}
+
+rsrs_status rsrs_solve(rsrs_factorization f, void* B, int64_t ldb, int64_t nrhs, void* s) {
+  return sweep(f, B, ldb, nrhs, s, true);
+}
+
+rsrs_status rsrs_apply(rsrs_factorization f, void* X, int64_t ldx, int64_t nrhs, void* s) {
+  return sweep(f, X, ldx, nrhs, s, false);
+}
+
+rsrs_status rsrs_factor_stats(rsrs_factorization f, rsrs_stats* st) {
+  if (!f || !st) return fail(RSRS_ERR_INVALID, "rsrs_factor_stats: null argument");
+  *st = f->stats;
+  return RSRS_OK;
+}
+
+rsrs_status rsrs_factor_ranks(rsrs_factorization f, int level, int32_t* k, int64_t cap) {
+  if (!f || !k || level < 0 || level > f->L) return fail(RSRS_ERR_INVALID, "rsrs_factor_ranks: invalid argument");
+  const auto& v = f->ranks[level];
+  if ((int64_t)v.size() > cap) return fail(RSRS_ERR_INVALID, "rsrs_factor_ranks: capacity too small");
+  for (size_t i = 0; i < v.size(); ++i) k[i] = v[i];
+  for (int64_t i = (int64_t)v.size(); i < cap; ++i) k[i] = -1;
+  return RSRS_OK;
+}
+
+rsrs_status rsrs_factor_top(rsrs_factorization f, int64_t* S, int64_t cap, int64_t* size) {
+  if (!f) return fail(RSRS_ERR_INVALID, "rsrs_factor_top: null factor");
+  if (size) *size = f->nS;
+  if (S) {
+    if (cap < f->nS) return fail(RSRS_ERR_INVALID, "rsrs_factor_top: capacity too small");
+    std::vector<int64_t> v(f->S_host);
+    std::sort(v.begin(), v.end());
+    std::copy(v.begin(), v.end(), S);
+  }
+  return RSRS_OK;
+}
+
+void rsrs_factor_destroy(rsrs_factorization f) {
+  if (!f) return;
+  cudaStreamSynchronize(f->stream);
+  delete f;
+}
+
+}  // extern "C"

@@ -1,0 +1,128 @@
+// Harness operator (NOT the factorization path): on-the-fly kernel matvec
+// Y = A X for the BASELINE.json workloads, A_ij = delta_ij + w k(|x_i - x_j|)
+// (PAPER.md:119-126 eq. kernel_eval; black-box access PAPER.md:53-61).
+// Used to draw the samples Y = A Omega, Z = A^* Psi (timed separately from the
+// sweep, BASELINE.json north_star) and residuals ||A x - b||.
+// A 64 x 32 kernel tile is evaluated into shared memory (FP64), then
+// contracted with a 32 x 64 tile of X on the FP64 tensor cores (DMMA).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/rsrs_sampler.h"
+#include "common.cuh"
+
+namespace {
+
+using rsrs::i64;
+
+constexpr int TM = 64, TN = 64, TK = 32;
+constexpr int SA = TK + 4;   // A tile [64][36]
+constexpr int SB = TN + 4;   // X tile [32][68]
+
+__device__ __forceinline__ double kval(int kind, double r, double w) {
+  if (kind == 0) return w * log(r);        // 2D log kernel
+  return w / r;                            // 3D Laplace single layer
+}
+
+__global__ void __launch_bounds__(128) matvec_real_kernel(const double* __restrict__ pts, int64_t N,
+                                                          const double* __restrict__ X, int64_t ldx,
+                                                          double* __restrict__ Y, int64_t ldy, int ncol,
+                                                          int kind, double w) {
+  __shared__ double As[TM * SA];
+  __shared__ double Bs[TK * SB];
+  __shared__ double Pi[TM * 3];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int wr = warp >> 1, wc = warp & 1;
+  const int64_t i0 = (int64_t)blockIdx.y * TM;
+  const int j0 = blockIdx.x * TN;
+  for (int t = tid; t < TM * 3; t += 128) {
+    const int64_t gi = i0 + t / 3;
+    Pi[t] = gi < N ? pts[gi * 3 + t % 3] : 0.0;
+  }
+  double acc[4][4][2];
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
+  __syncthreads();
+  for (int64_t k0 = 0; k0 < N; k0 += TK) {
+    // kernel tile A[i0:i0+64, k0:k0+32]
+    for (int t = tid; t < TM * TK; t += 128) {
+      const int ii = t / TK, kk = t % TK;
+      const int64_t gi = i0 + ii, gk = k0 + kk;
+      double v = 0.0;
+      if (gi < N && gk < N) {
+        if (gi == gk) {
+          v = 1.0;
+        } else {
+          const double dx = Pi[ii * 3] - pts[gk * 3];
+          const double dy = Pi[ii * 3 + 1] - pts[gk * 3 + 1];
+          const double dz = Pi[ii * 3 + 2] - pts[gk * 3 + 2];
+          v = kval(kind, sqrt(dx * dx + dy * dy + dz * dz), w);
+        }
+      }
+      As[ii * SA + kk] = v;
+    }
+    for (int t = tid; t < TK * TN; t += 128) {
+      const int kk = t / TN, jj = t % TN;
+      const int64_t gk = k0 + kk;
+      Bs[kk * SB + jj] = (gk < N && j0 + jj < ncol) ? X[gk * ldx + j0 + jj] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < TK / 4; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) a[t] = As[(wr * 32 + t * 8 + gid) * SA + kk * 4 + tig];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) b[u] = Bs[(kk * 4 + tig) * SB + wc * 32 + u * 8 + gid];
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) rsrs::dmma884(acc[t][u][0], acc[t][u][1], a[t], b[u]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int64_t i = i0 + wr * 32 + t * 8 + gid;
+    if (i >= N) continue;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = j0 + wc * 32 + u * 8 + 2 * tig;
+      if (j < ncol) Y[i * ldy + j] = acc[t][u][0];
+      if (j + 1 < ncol) Y[i * ldy + j + 1] = acc[t][u][1];
+    }
+  }
+}
+
+thread_local std::string g_err;
+
+}  // namespace
+
+extern "C" {
+
+const char* rsrs_sampler_last_error(void) { return g_err.c_str(); }
+
+int rsrs_sample_matvec(int kind, const double* pts, int64_t N, double weight, const void* X, int64_t ldx,
+                       void* Y, int64_t ldy, int64_t ncol, int adjoint, void* stream) {
+  (void)adjoint;  // real kernels here are symmetric: A^* = A
+  if (kind < 0 || kind > 1 || !pts || !X || !Y || N < 1 || ncol < 1 || ldx < ncol || ldy < ncol) {
+    g_err = "rsrs_sample_matvec: invalid argument";
+    return 1;
+  }
+  dim3 grid((unsigned)((ncol + TN - 1) / TN), (unsigned)((N + TM - 1) / TM));
+  matvec_real_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(pts, N, (const double*)X, ldx, (double*)Y, ldy,
+                                                             (int)ncol, kind, weight);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    g_err = std::string("rsrs_sample_matvec: ") + cudaGetErrorString(e);
+    return 4;
+  }
+  return 0;
+}
+
+}  // extern "C"

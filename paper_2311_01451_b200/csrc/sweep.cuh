@@ -1,0 +1,258 @@
+// Solve / apply sweeps and permutation kernels (HBM-bound; one CTA per box).
+// K = V_1..V_n A~_diag W_n..W_1, V = E L, W = U F;
+// inverses of elim() toggle the sign of the off-diagonal block.
+#pragma once
+#include "common.cuh"
+
+namespace rsrs {
+
+RSRS_DI double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// forward solve of one box: x_r -= T x_s ; x_c -= G_L x_r ; x_r <- X_rr^-1 x_r
+__global__ void __launch_bounds__(256) solve_fwd_kernel(const BoxDev* __restrict__ boxes,
+                                                         const double* __restrict__ fpool,
+                                                         const int* __restrict__ ipool, double* __restrict__ x,
+                                                         i64 ldx, int nrhs) {
+  extern __shared__ double sm[];
+  const BoxDev b = boxes[blockIdx.x];
+  const int nr = b.nr, k = b.k, nc = b.nc;
+  if (nr <= 0) return;
+  const int ldn = (b.nb + 1) & ~1;
+  double* xs = sm;
+  double* xr = xs + k;
+  const int* red = ipool + b.f_red;
+  const int* skel = ipool + b.f_skel;
+  const int* cc = ipool + b.f_c;
+  const double* T = fpool + b.f_T;
+  const double* GL = fpool + b.f_GL;
+  const double* Xi = fpool + b.f_Xinv;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int col = 0; col < nrhs; ++col) {
+    for (int s = tid; s < k; s += blockDim.x) xs[s] = x[(i64)skel[s] * ldx + col];
+    __syncthreads();
+    for (int i = tid; i < nr; i += blockDim.x) {
+      double v = x[(i64)red[i] * ldx + col];
+      for (int s = 0; s < k; ++s) v -= T[(i64)i * ldn + s] * xs[s];
+      xr[i] = v;
+    }
+    __syncthreads();
+    for (int ci = warp; ci < nc; ci += blockDim.x / 32) {
+      double v = 0.0;
+      for (int j = lane; j < nr; j += 32) v += GL[(i64)ci * ldn + j] * xr[j];
+      v = warp_sum(v);
+      if (lane == 0) x[(i64)cc[ci] * ldx + col] -= v;
+    }
+    for (int i = warp; i < nr; i += blockDim.x / 32) {
+      double v = 0.0;
+      for (int j = lane; j < nr; j += 32) v += Xi[(i64)i * ldn + j] * xr[j];
+      v = warp_sum(v);
+      if (lane == 0) x[(i64)red[i] * ldx + col] = v;
+    }
+    __syncthreads();
+  }
+}
+
+// backward solve of one box: x_r -= G_U x_c ; x_s -= T^T x_r
+__global__ void __launch_bounds__(256) solve_bwd_kernel(const BoxDev* __restrict__ boxes,
+                                                         const double* __restrict__ fpool,
+                                                         const int* __restrict__ ipool, double* __restrict__ x,
+                                                         i64 ldx, int nrhs) {
+  extern __shared__ double sm[];
+  const BoxDev b = boxes[blockIdx.x];
+  const int nr = b.nr, k = b.k, nc = b.nc;
+  if (nr <= 0) return;
+  const int ldn = (b.nb + 1) & ~1;
+  const int ldr = (b.r + 1) & ~1;
+  double* xc = sm;
+  double* xr = xc + nc;
+  const int* red = ipool + b.f_red;
+  const int* skel = ipool + b.f_skel;
+  const int* cc = ipool + b.f_c;
+  const double* T = fpool + b.f_T;
+  const double* GU = fpool + b.f_GU;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int col = 0; col < nrhs; ++col) {
+    for (int j = tid; j < nc; j += blockDim.x) xc[j] = x[(i64)cc[j] * ldx + col];
+    __syncthreads();
+    for (int i = warp; i < nr; i += blockDim.x / 32) {
+      double v = 0.0;
+      for (int j = lane; j < nc; j += 32) v += GU[(i64)i * ldr + j] * xc[j];
+      v = warp_sum(v);
+      if (lane == 0) {
+        const double nv = x[(i64)red[i] * ldx + col] - v;
+        x[(i64)red[i] * ldx + col] = nv;
+        xr[i] = nv;
+      }
+    }
+    __syncthreads();
+    for (int s = tid; s < k; s += blockDim.x) {
+      double v = 0.0;
+      for (int i = 0; i < nr; ++i) v += T[(i64)i * ldn + s] * xr[i];
+      x[(i64)skel[s] * ldx + col] -= v;
+    }
+    __syncthreads();
+  }
+}
+
+// apply, forward half of one box: x_s += T^T x_r ; x_r += G_U x_c ; x_r <- X_rr x_r
+__global__ void __launch_bounds__(256) apply_fwd_kernel(const BoxDev* __restrict__ boxes,
+                                                         const double* __restrict__ fpool,
+                                                         const int* __restrict__ ipool, double* __restrict__ x,
+                                                         i64 ldx, int nrhs) {
+  extern __shared__ double sm[];
+  const BoxDev b = boxes[blockIdx.x];
+  const int nr = b.nr, k = b.k, nc = b.nc;
+  if (nr <= 0) return;
+  const int ldn = (b.nb + 1) & ~1;
+  const int ldr = (b.r + 1) & ~1;
+  double* xc = sm;
+  double* xr = xc + nc;
+  double* xr2 = xr + nr;
+  const int* red = ipool + b.f_red;
+  const int* skel = ipool + b.f_skel;
+  const int* cc = ipool + b.f_c;
+  const double* T = fpool + b.f_T;
+  const double* GU = fpool + b.f_GU;
+  const double* Xrr = fpool + b.f_Xrr;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int col = 0; col < nrhs; ++col) {
+    for (int i = tid; i < nr; i += blockDim.x) xr[i] = x[(i64)red[i] * ldx + col];
+    __syncthreads();
+    for (int s = tid; s < k; s += blockDim.x) {
+      double v = 0.0;
+      for (int i = 0; i < nr; ++i) v += T[(i64)i * ldn + s] * xr[i];
+      x[(i64)skel[s] * ldx + col] += v;
+    }
+    __syncthreads();
+    for (int j = tid; j < nc; j += blockDim.x) xc[j] = x[(i64)cc[j] * ldx + col];
+    __syncthreads();
+    for (int i = warp; i < nr; i += blockDim.x / 32) {
+      double v = 0.0;
+      for (int j = lane; j < nc; j += 32) v += GU[(i64)i * ldr + j] * xc[j];
+      v = warp_sum(v);
+      if (lane == 0) xr[i] += v;
+    }
+    __syncthreads();
+    for (int i = warp; i < nr; i += blockDim.x / 32) {
+      double v = 0.0;
+      for (int j = lane; j < nr; j += 32) v += Xrr[(i64)i * ldn + j] * xr[j];
+      v = warp_sum(v);
+      if (lane == 0) xr2[i] = v;
+    }
+    __syncthreads();
+    for (int i = tid; i < nr; i += blockDim.x) x[(i64)red[i] * ldx + col] = xr2[i];
+    __syncthreads();
+  }
+}
+
+// apply, backward half of one box: x_c += G_L x_r ; x_r += T x_s
+__global__ void __launch_bounds__(256) apply_bwd_kernel(const BoxDev* __restrict__ boxes,
+                                                         const double* __restrict__ fpool,
+                                                         const int* __restrict__ ipool, double* __restrict__ x,
+                                                         i64 ldx, int nrhs) {
+  extern __shared__ double sm[];
+  const BoxDev b = boxes[blockIdx.x];
+  const int nr = b.nr, k = b.k, nc = b.nc;
+  if (nr <= 0) return;
+  const int ldn = (b.nb + 1) & ~1;
+  double* xs = sm;
+  double* xr = xs + k;
+  const int* red = ipool + b.f_red;
+  const int* skel = ipool + b.f_skel;
+  const int* cc = ipool + b.f_c;
+  const double* T = fpool + b.f_T;
+  const double* GL = fpool + b.f_GL;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int col = 0; col < nrhs; ++col) {
+    for (int i = tid; i < nr; i += blockDim.x) xr[i] = x[(i64)red[i] * ldx + col];
+    __syncthreads();
+    for (int ci = warp; ci < nc; ci += blockDim.x / 32) {
+      double v = 0.0;
+      for (int j = lane; j < nr; j += 32) v += GL[(i64)ci * ldn + j] * xr[j];
+      v = warp_sum(v);
+      if (lane == 0) x[(i64)cc[ci] * ldx + col] += v;
+    }
+    __syncthreads();
+    for (int s = tid; s < k; s += blockDim.x) xs[s] = x[(i64)skel[s] * ldx + col];
+    __syncthreads();
+    for (int i = tid; i < nr; i += blockDim.x) {
+      double v = xr[i];
+      for (int s = 0; s < k; ++s) v += T[(i64)i * ldn + s] * xs[s];
+      x[(i64)red[i] * ldx + col] = v;
+    }
+    __syncthreads();
+  }
+}
+
+// top block: x_S <- A~_SS^-1 x_S (LU with pivots) or x_S <- A~_SS x_S
+__global__ void __launch_bounds__(1024) top_solve_kernel(const double* __restrict__ LU, i64 lda, int n,
+                                                          const int* __restrict__ ipiv,
+                                                          const int* __restrict__ S, double* __restrict__ x,
+                                                          i64 ldx, int nrhs) {
+  extern __shared__ double xs[];
+  const int tid = threadIdx.x;
+  for (int col = 0; col < nrhs; ++col) {
+    for (int i = tid; i < n; i += blockDim.x) xs[i] = x[(i64)S[i] * ldx + col];
+    __syncthreads();
+    if (tid == 0)
+      for (int c = 0; c < n; ++c)
+        if (ipiv[c] != c) {
+          const double t = xs[c];
+          xs[c] = xs[ipiv[c]];
+          xs[ipiv[c]] = t;
+        }
+    __syncthreads();
+    for (int c = 0; c < n; ++c) {  // unit lower
+      const double xc = xs[c];
+      for (int i = c + 1 + tid; i < n; i += blockDim.x) xs[i] -= LU[(i64)i * lda + c] * xc;
+      __syncthreads();
+    }
+    for (int c = n - 1; c >= 0; --c) {  // upper
+      if (tid == 0) xs[c] /= LU[(i64)c * lda + c];
+      __syncthreads();
+      const double xc = xs[c];
+      for (int i = tid; i < c; i += blockDim.x) xs[i] -= LU[(i64)i * lda + c] * xc;
+      __syncthreads();
+    }
+    for (int i = tid; i < n; i += blockDim.x) x[(i64)S[i] * ldx + col] = xs[i];
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(1024) top_apply_kernel(const double* __restrict__ A, i64 lda, int n,
+                                                          const int* __restrict__ S, double* __restrict__ x,
+                                                          i64 ldx, int nrhs) {
+  extern __shared__ double xs[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int col = 0; col < nrhs; ++col) {
+    for (int i = tid; i < n; i += blockDim.x) xs[i] = x[(i64)S[i] * ldx + col];
+    __syncthreads();
+    for (int i = warp; i < n; i += blockDim.x / 32) {
+      double v = 0.0;
+      for (int j = lane; j < n; j += 32) v += A[(i64)i * lda + j] * xs[j];
+      v = warp_sum(v);
+      if (lane == 0) x[(i64)S[i] * ldx + col] = v;
+    }
+    __syncthreads();
+  }
+}
+
+// x_tree[t, :] = b[perm[t], :]  /  b[perm[t], :] = x_tree[t, :]
+__global__ void permute_rows_kernel(const double* __restrict__ src, i64 lds, double* __restrict__ dst, i64 ldd,
+                                    const int64_t* __restrict__ perm, int64_t N, int ncol, int inverse) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.y + threadIdx.y;
+  if (t >= N) return;
+  const int64_t o = perm[t];
+  for (int j = threadIdx.x; j < ncol; j += blockDim.x) {
+    if (!inverse)
+      dst[t * ldd + j] = src[o * lds + j];
+    else
+      dst[o * ldd + j] = src[t * lds + j];
+  }
+}
+
+}  // namespace rsrs

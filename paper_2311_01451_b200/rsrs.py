@@ -1,0 +1,251 @@
+"""Thin ctypes binding of librsrs.so (include/rsrs.h) -- argument marshalling only.
+
+Every step of the factorization, solve and apply runs in the library's own
+sm_100a kernels.  PyTorch supplies device memory and streams (tensors are
+passed by data_ptr()).  There is no CPU fallback: if librsrs.so is missing the
+import fails loudly, and without a GPU every compute call raises RSRSError
+(RSRS_ERR_CUDA).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librsrs.so")
+SAMPLER_PATH = os.path.join(_HERE, "libsampler.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `make -C paper_2311_01451_b200/csrc` "
+                      "(or __graft_entry__.build()); there is no fallback implementation")
+_lib = ctypes.CDLL(LIB_PATH)
+
+RSRS_OK, RSRS_ERR_INVALID, RSRS_ERR_SAMPLES, RSRS_ERR_SINGULAR = 0, 1, 2, 3
+RSRS_ERR_CUDA, RSRS_ERR_NCCL, RSRS_ERR_NOMEM, RSRS_ERR_STATE = 4, 5, 6, 7
+RSRS_F64, RSRS_C128 = 0, 1
+STATUS_NAMES = {0: "OK", 1: "INVALID", 2: "SAMPLES", 3: "SINGULAR", 4: "CUDA", 5: "NCCL", 6: "NOMEM", 7: "STATE"}
+
+# Every symbol include/rsrs.h declares (checked by tests/test_abi.py).
+EXPORTS = [
+    "rsrs_build_tree", "rsrs_tree_info", "rsrs_tree_perm", "rsrs_tree_level_size", "rsrs_tree_level",
+    "rsrs_plan_samples", "rsrs_tree_destroy", "rsrs_factor", "rsrs_solve", "rsrs_apply",
+    "rsrs_factor_stats", "rsrs_factor_ranks", "rsrs_factor_top", "rsrs_factor_destroy",
+    "rsrs_last_error", "rsrs_version",
+]
+
+
+class RSRSError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"RSRS_ERR_{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Opts(ctypes.Structure):
+    _fields_ = [("eps", ctypes.c_double), ("level_growth", ctypes.c_double), ("id_scale", ctypes.c_double),
+                ("oversample", ctypes.c_int), ("top_level", ctypes.c_int), ("rank", ctypes.c_int),
+                ("nranks", ctypes.c_int), ("nccl_comm", ctypes.c_void_p), ("stream", ctypes.c_void_p)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("N", ctypes.c_int64), ("p", ctypes.c_int64), ("L", ctypes.c_int), ("top_level", ctypes.c_int),
+                ("nlevels_compressed", ctypes.c_int), ("nsteps", ctypes.c_int64), ("top_size", ctypes.c_int64),
+                ("max_rank", ctypes.c_int64), ("memory_scalars", ctypes.c_int64), ("factor_ms", ctypes.c_double),
+                ("flops_model", ctypes.c_double), ("bytes_model", ctypes.c_double), ("launches", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_vp, _i64, _i32, _d = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+_lib.rsrs_last_error.restype = ctypes.c_char_p
+_lib.rsrs_version.restype = ctypes.c_char_p
+_lib.rsrs_build_tree.argtypes = [_vp, _i64, _i32, _i32, _vp, _d, _i32, ctypes.POINTER(_vp)]
+_lib.rsrs_tree_info.argtypes = [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i64)]
+_lib.rsrs_tree_perm.argtypes = [_vp, _vp]
+_lib.rsrs_tree_level_size.argtypes = [_vp, _i32, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]
+_lib.rsrs_tree_level.argtypes = [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp]
+_lib.rsrs_plan_samples.argtypes = [_vp, _i32, _i32, ctypes.POINTER(_i64)]
+_lib.rsrs_tree_destroy.argtypes = [_vp]
+_lib.rsrs_tree_destroy.restype = None
+_lib.rsrs_factor.argtypes = [_vp, _i32, _i64, _vp, _vp, _vp, _vp, _i64, ctypes.POINTER(Opts), ctypes.POINTER(_vp)]
+_lib.rsrs_solve.argtypes = [_vp, _vp, _i64, _i64, _vp]
+_lib.rsrs_apply.argtypes = [_vp, _vp, _i64, _i64, _vp]
+_lib.rsrs_factor_stats.argtypes = [_vp, ctypes.POINTER(Stats)]
+_lib.rsrs_factor_ranks.argtypes = [_vp, _i32, _vp, _i64]
+_lib.rsrs_factor_top.argtypes = [_vp, _vp, _i64, ctypes.POINTER(_i64)]
+_lib.rsrs_factor_destroy.argtypes = [_vp]
+_lib.rsrs_factor_destroy.restype = None
+for _n in ("rsrs_build_tree", "rsrs_tree_info", "rsrs_tree_perm", "rsrs_tree_level_size", "rsrs_tree_level",
+           "rsrs_plan_samples", "rsrs_factor", "rsrs_solve", "rsrs_apply", "rsrs_factor_stats",
+           "rsrs_factor_ranks", "rsrs_factor_top"):
+    getattr(_lib, _n).restype = ctypes.c_int
+
+
+def _check(st: int):
+    if st != RSRS_OK:
+        raise RSRSError(st, _lib.rsrs_last_error().decode())
+
+
+def version() -> str:
+    return _lib.rsrs_version().decode()
+
+
+def _ptr(t) -> int:
+    """Device pointer of a CUDA tensor (or host pointer of a numpy array)."""
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    return t.data_ptr()
+
+
+def _stream_ptr(stream) -> int | None:
+    if stream is None:
+        return None
+    return getattr(stream, "cuda_stream", stream)
+
+
+class Tree:
+    """Handle of rsrs_build_tree (host integer work)."""
+
+    def __init__(self, points: np.ndarray, leaf_max: int, root_lo=None, root_side: float = 0.0, nranks: int = 1):
+        pts = np.ascontiguousarray(points, dtype=np.float64)
+        N, d = pts.shape
+        lo = None if root_lo is None else np.ascontiguousarray(root_lo, dtype=np.float64)
+        h = _vp()
+        _check(_lib.rsrs_build_tree(pts.ctypes.data, N, d, int(leaf_max),
+                                    None if lo is None else lo.ctypes.data, float(root_side), int(nranks),
+                                    ctypes.byref(h)))
+        self._h = h
+        L, dd, NN = _i32(), _i32(), _i64()
+        _check(_lib.rsrs_tree_info(h, ctypes.byref(L), ctypes.byref(dd), ctypes.byref(NN)))
+        self.L, self.d, self.N = L.value, dd.value, NN.value
+
+    @property
+    def handle(self):
+        return self._h
+
+    def perm(self) -> np.ndarray:
+        out = np.empty(self.N, dtype=np.int64)
+        _check(_lib.rsrs_tree_perm(self._h, out.ctypes.data))
+        return out
+
+    def level(self, lev: int) -> dict:
+        nb, nn = _i64(), _i64()
+        _check(_lib.rsrs_tree_level_size(self._h, lev, ctypes.byref(nb), ctypes.byref(nn)))
+        n = nb.value
+        keys = np.empty(n, np.uint64)
+        start = np.empty(n + 1, np.int64)
+        parent = np.empty(n, np.int32)
+        colour = np.empty(n, np.int32)
+        off = np.empty(n + 1, np.int32)
+        nbr = np.empty(max(nn.value, 1), np.int32)
+        _check(_lib.rsrs_tree_level(self._h, lev, keys.ctypes.data, start.ctypes.data, parent.ctypes.data,
+                                    colour.ctypes.data, off.ctypes.data, nbr.ctypes.data))
+        return {"keys": keys, "start": start, "parent": parent, "colour": colour,
+                "neighbours": [nbr[off[i]:off[i + 1]] for i in range(n)]}
+
+    def plan_samples(self, kmax_guess: int = 20, oversample: int = 10) -> int:
+        p = _i64()
+        _check(_lib.rsrs_plan_samples(self._h, kmax_guess, oversample, ctypes.byref(p)))
+        return p.value
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _lib.rsrs_tree_destroy(h)
+            self._h = None
+
+
+class Factorization:
+    """Handle of rsrs_factor."""
+
+    def __init__(self, handle, tree: Tree):
+        self._h = handle
+        self.tree_L = tree.L
+
+    def stats(self) -> dict:
+        st = Stats()
+        _check(_lib.rsrs_factor_stats(self._h, ctypes.byref(st)))
+        return st.as_dict()
+
+    def ranks(self, level: int, nboxes: int) -> np.ndarray:
+        out = np.empty(max(nboxes, 1), np.int32)
+        _check(_lib.rsrs_factor_ranks(self._h, level, out.ctypes.data, out.shape[0]))
+        return out[:nboxes]
+
+    def top(self) -> np.ndarray:
+        n = _i64()
+        _check(_lib.rsrs_factor_top(self._h, None, 0, ctypes.byref(n)))
+        out = np.empty(max(n.value, 1), np.int64)
+        _check(_lib.rsrs_factor_top(self._h, out.ctypes.data, out.shape[0], ctypes.byref(n)))
+        return out[:n.value]
+
+    def solve(self, B, stream=None):
+        """B <- K^-1 B in place; B: CUDA float64 tensor (N,) or (N, nrhs) row-major, original order."""
+        nrhs = 1 if B.dim() == 1 else B.shape[1]
+        ldb = 1 if B.dim() == 1 else B.stride(0)
+        _check(_lib.rsrs_solve(self._h, _ptr(B), ldb, nrhs, _stream_ptr(stream)))
+        return B
+
+    def apply(self, X, stream=None):
+        """X <- K X in place (same layout as solve)."""
+        nrhs = 1 if X.dim() == 1 else X.shape[1]
+        ldx = 1 if X.dim() == 1 else X.stride(0)
+        _check(_lib.rsrs_apply(self._h, _ptr(X), ldx, nrhs, _stream_ptr(stream)))
+        return X
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _lib.rsrs_factor_destroy(h)
+            self._h = None
+
+
+def factor(tree: Tree, Y, Z, Omega, Psi, p: int, eps: float = 1e-6, level_growth: float = 1.0,
+           id_scale: float = 1.0, oversample: int = 10, top_level: int = 2, stream=None,
+           dtype: int = RSRS_F64) -> Factorization:
+    """rsrs_factor on CUDA tensors (N x ld, tree order); Y, Z, Omega, Psi are OVERWRITTEN."""
+    ld = Y.stride(0)
+    for t in (Z, Omega, Psi):
+        if t.stride(0) != ld:
+            raise ValueError("Y, Z, Omega, Psi must share the leading dimension")
+    o = Opts(eps, level_growth, id_scale, oversample, top_level, 0, 1, None, _stream_ptr(stream))
+    h = _vp()
+    _check(_lib.rsrs_factor(tree.handle, dtype, int(p), _ptr(Y), _ptr(Z), _ptr(Omega), _ptr(Psi), int(ld),
+                            ctypes.byref(o), ctypes.byref(h)))
+    return Factorization(h, tree)
+
+
+# ----------------------------------------------------------------------------
+# harness operator (libsampler.so, include/rsrs_sampler.h) -- not the factor path
+# ----------------------------------------------------------------------------
+_sampler = None
+KERNEL_KIND = {"log2d": 0, "lap3d": 1}
+
+
+def _sampler_lib():
+    global _sampler
+    if _sampler is None:
+        if not os.path.exists(SAMPLER_PATH):
+            raise ImportError(f"{SAMPLER_PATH} is missing (make -C paper_2311_01451_b200/csrc)")
+        s = ctypes.CDLL(SAMPLER_PATH)
+        s.rsrs_sample_matvec.argtypes = [_i32, _vp, _i64, _d, _vp, _i64, _vp, _i64, _i64, _i32, _vp]
+        s.rsrs_sample_matvec.restype = ctypes.c_int
+        s.rsrs_sampler_last_error.restype = ctypes.c_char_p
+        _sampler = s
+    return _sampler
+
+
+def sample_matvec(kind: str, pts3, weight: float, X, Y, adjoint: bool = False, stream=None):
+    """Y = A X with the on-the-fly kernel operator (device tensors; pts3 N x 3)."""
+    s = _sampler_lib()
+    N = pts3.shape[0]
+    ncol = 1 if X.dim() == 1 else X.shape[1]
+    ldx = 1 if X.dim() == 1 else X.stride(0)
+    ldy = 1 if Y.dim() == 1 else Y.stride(0)
+    st = s.rsrs_sample_matvec(KERNEL_KIND[kind], _ptr(pts3), N, float(weight), _ptr(X), ldx, _ptr(Y), ldy, ncol,
+                              int(adjoint), _stream_ptr(stream))
+    if st != 0:
+        raise RSRSError(st, s.rsrs_sampler_last_error().decode())
+    return Y
