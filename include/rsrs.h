@@ -61,6 +61,7 @@ typedef struct {
   int nranks;          /* number of ranks; must be 1 in this build (RSRS_ERR_STATE otherwise) */
   void* nccl_comm;     /* reserved (ncclComm_t), must be NULL */
   void* stream;        /* cudaStream_t the factorization runs on (NULL = legacy default stream) */
+  int profile;         /* 1: time every kernel class with CUDA events on `stream` (rsrs_factor_profile) */
 } rsrs_opts;
 
 /* Statistics of a factorization (Table 1). */
@@ -152,6 +153,16 @@ rsrs_status rsrs_factor(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, void* Z,
  * ------------------------------------------------------------------------- */
 rsrs_status rsrs_solve(rsrs_factorization f, void* B, int64_t ldb, int64_t nrhs, void* s);
 rsrs_status rsrs_apply(rsrs_factorization f, void* X, int64_t ldx, int64_t nrhs, void* s);
+
+/* Kernel classes of the sweep, for rsrs_factor_profile. */
+#define RSRS_NUM_KERNEL_CLASSES 11
+
+/* Per-kernel-class record of the last rsrs_factor: class name, summed device
+ * time (ms; only when opts.profile == 1, else 0), algorithmic FLOPs and HBM
+ * bytes of all its launches and the launch count.
+ * cls in [0, RSRS_NUM_KERNEL_CLASSES). */
+rsrs_status rsrs_factor_profile(rsrs_factorization f, int cls, const char** name, double* ms,
+                                double* flops, double* bytes, int64_t* launches);
 
 /* Statistics of the factorization (host struct). */
 rsrs_status rsrs_factor_stats(rsrs_factorization f, rsrs_stats* st);

@@ -162,16 +162,22 @@ def atol_schedule(eps: float, c_id: float, g: float, L: int, lev: int) -> float:
 
 
 def factor(tree: Tree, Y, Z, Om, Psi, eps: float, c_id: float = 1.0, g: float = 1.0,
-           l: int = 10, top_level: int = 2, on_step=None) -> Factorization:
+           l: int = 10, top_level: int = 2, on_step=None, max_boxes: int | None = None,
+           copy: bool = True) -> Factorization:
     """RSRS factorization from samples in TREE order (N x p each).
 
-    The inputs are copied; `on_step(step, Y, Z, Om, Psi)` (optional) sees the
-    updated samples after each step (used by the consistency tests).
+    The inputs are copied (unless copy=False); `on_step(step, Y, Z, Om, Psi)`
+    (optional) sees the updated samples after each step (consistency tests).
+    `max_boxes` stops after that many boxes in canonical order and returns the
+    partial record (ranks of the boxes processed so far; no top block) -- used
+    for sampled checks and bounded timing at full size.
     """
-    Y = np.array(Y, copy=True)
-    Z = np.array(Z, copy=True)
-    Om = np.array(Om, copy=True)
-    Psi = np.array(Psi, copy=True)
+    if copy:
+        Y = np.array(Y, copy=True)
+        Z = np.array(Z, copy=True)
+        Om = np.array(Om, copy=True)
+        Psi = np.array(Psi, copy=True)
+    nproc = 0
     N, p = Y.shape
     dt = np.result_type(Y.dtype, Om.dtype)
     L = tree.L
@@ -186,6 +192,11 @@ def factor(tree: Tree, Y, Z, Om, Psi, eps: float, c_id: float = 1.0, g: float = 
         atol = atol_schedule(eps, c_id, g, L, lev)
         fac.atol[lev] = atol
         for b in tree.canonical_order(lev):
+            if max_boxes is not None and nproc >= max_boxes:
+                fac.S = np.zeros(0, np.int64)
+                fac.A_SS = np.zeros((0, 0), dtype=dt)
+                return fac
+            nproc += 1
             Ib = act[b]
             nb = Ib.shape[0]
             fac.nb[(lev, b)] = nb

@@ -30,22 +30,27 @@ RSRS_DI void cp_async_wait() {
 }
 
 // Per-box record of one (level, colour) batch.  Static fields are written by
-// the host planner; k, nr, nc, status by the device (ID kernel).
+// the host planner; r, self_pos (near-list build) and k, nr, nc, status (ID)
+// by the device.
 struct BoxDev {
-  int nb, r, self_pos, row0;  // |I_b|, |near|, position of b inside near, first store row of b
-  int ldaug;                  // leading dimension of the augmented Gram (>= r, even)
+  int nb;                     // |I_b| (active rows of the box, static)
+  int rmax;                   // upper bound of |near| (every row of the neighbours)
+  int ldr, ldn;               // even leading dims >= rmax, >= nb
+  int row0;                   // first store row of b (its rows are contiguous)
   int level, box;             // for error messages
-  int pad0;
-  i64 off_aug;                // doubles: Omega-side [C; B] ((r+nb) x ldaug); Psi side follows
-  i64 off_yz;                 // doubles: [Y'' Z''] (nb x ldyz)
-  i64 off_h;                  // doubles: H (nb x nb)
-  i64 off_xy, off_xz;         // doubles: X_Y, X_Z (nb x r each, ld r)
-  i64 off_xrc, off_xcr;       // doubles: X_rc (nb x r, ld r), X_cr (r x nb, ld nb)
-  i64 off_rows;               // ints: [near rows (r); b rows (nb)]
-  i64 off_skelrow, off_redrow, off_crow, off_cpos;  // ints: nb, nb, r, r
-  i64 f_T, f_GL, f_GU, f_Xrr, f_Xinv;  // doubles in the level factor pool
+  int nnbr;                   // neighbour boxes (self included)
+  i64 off_nbr;                // ints: nnbr x {boxdev index or -1, row0, nb}
+  i64 off_aug;                // doubles: Omega side [C (rmax x ldr); u (nb x ldr)], Psi side follows
+  i64 off_yz;                 // doubles: [Y'' Z''] (nb x 2 nld)
+  i64 off_h;                  // doubles: H (nb x ldn)
+  i64 off_xy, off_xz;         // doubles: X_Y, X_Z (nb x ldr each)
+  i64 off_xrc, off_xcr;       // doubles: X_rc (nb x ldr), X_cr (rmax x ldn)
+  i64 off_rows;               // ints: near rows (capacity rmax) then b rows (nb)
+  i64 off_skelrow, off_redrow, off_crow, off_cpos;  // ints: nb, nb, rmax, rmax
+  i64 f_T, f_GL, f_GU, f_Xrr, f_Xinv;  // doubles in the level factor pool (lds ldn / ldr)
   i64 f_red, f_skel, f_c;              // ints (tree positions) in the level index pool
-  int k, nr, nc, status;               // dynamic
+  int r, self_pos;                     // dynamic: |near| and position of b inside near
+  int k, nr, nc, status;               // dynamic: ID results
 };
 
 // status codes in BoxDev::status (0 = ok)
@@ -67,6 +72,7 @@ struct NTDesc {
   double alpha;
   const int* pm;  // optional device size overrides
   const int* pn;
+  const int* psym;
 };
 
 // D[rowD(i), j] = beta * Cin[rowC(i), j] + alpha * sum_k opA(i, k) B[rowB(k), j]
@@ -91,10 +97,13 @@ struct NNDesc {
   const int* pK;
 };
 
-struct CholDesc {  // augmented Cholesky of [C; B] ((r + mextra) x r), see kernels.cuh
+// augmented Cholesky of [C; B]: C = rows [0, r) (r = *pr), B = rows
+// [uoff, uoff + mextra); see dense.cuh
+struct CholDesc {
   double* A;
   i64 lda;
-  int r, mextra;
+  const int* pr;
+  int mextra, uoff;
   int* status;
 };
 

@@ -19,9 +19,12 @@ __global__ void __launch_bounds__(256) chol_aug_kernel(const CholDesc* __restric
   constexpr int PS = NB + 4;
   __shared__ int bad;
   const CholDesc d = descs[blockIdx.x];
-  const int r = d.r, m = d.r + d.mextra;
+  if (d.status && *d.status != ST_OK) return;
+  const int r = *d.pr, me = d.mextra, m = r + me, uoff = d.uoff;
   double* A = d.A;
   const i64 lda = d.lda;
+  // logical row i (C rows [0, r), then the extra rows) -> physical row
+  auto prow = [&](int i) -> double* { return A + (i64)(i < r ? i : uoff + (i - r)) * lda; };
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
   if (tid == 0) bad = 0;
@@ -32,7 +35,7 @@ __global__ void __launch_bounds__(256) chol_aug_kernel(const CholDesc* __restric
     // 1. stage the panel A[j0:m, j0:j0+NB] (zero beyond jb)
     for (int idx = tid; idx < mp * NB; idx += 256) {
       const int i = idx / NB, c = idx % NB;
-      P[i * PS + c] = (c < jb) ? A[(i64)(j0 + i) * lda + j0 + c] : 0.0;
+      P[i * PS + c] = (c < jb) ? prow(j0 + i)[j0 + c] : 0.0;
     }
     __syncthreads();
     // 2. diagonal block (jb <= 32) by warp 0
@@ -81,9 +84,9 @@ __global__ void __launch_bounds__(256) chol_aug_kernel(const CholDesc* __restric
     // 4. write the finished column block back
     for (int idx = tid; idx < mp * jb; idx += 256) {
       const int i = idx / jb, c = idx % jb;
-      if (j0 + i >= j0 + c) A[(i64)(j0 + i) * lda + j0 + c] = P[i * PS + c];
+      if (i >= c) prow(j0 + i)[j0 + c] = P[i * PS + c];
     }
-    // 5. trailing update A[t0:m, t0:r] -= P P^T (lower part of C; all of B)
+    // 5. trailing update A[t0:m, t0:r] -= P P^T (lower part of C; all extra rows)
     const int t0 = j0 + jb;
     const int nrow = m - t0, ncol = r - t0;
     if (ncol > 0) {
@@ -95,14 +98,16 @@ __global__ void __launch_bounds__(256) chol_aug_kernel(const CholDesc* __restric
         if (rs + 32 <= r && tj > ti) continue;   // strictly upper tile of C
         const int cs = t0 + 32 * tj;
         double acc[4][4][2];
+        double* rp[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           const int gi = rs + t * 8 + gid;
+          rp[t] = gi < m ? prow(gi) : nullptr;
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int gj = cs + u * 8 + 2 * tig;
-            acc[t][u][0] = (gi < m && gj < r) ? A[(i64)gi * lda + gj] : 0.0;
-            acc[t][u][1] = (gi < m && gj + 1 < r) ? A[(i64)gi * lda + gj + 1] : 0.0;
+            acc[t][u][0] = (rp[t] && gj < r) ? rp[t][gj] : 0.0;
+            acc[t][u][1] = (rp[t] && gj + 1 < r) ? rp[t][gj + 1] : 0.0;
           }
         }
         for (int kk = 0; kk < nkk; ++kk) {
@@ -124,13 +129,12 @@ __global__ void __launch_bounds__(256) chol_aug_kernel(const CholDesc* __restric
         }
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
-          const int gi = rs + t * 8 + gid;
-          if (gi >= m) continue;
+          if (!rp[t]) continue;
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int gj = cs + u * 8 + 2 * tig;
-            if (gj < r) A[(i64)gi * lda + gj] = acc[t][u][0];
-            if (gj + 1 < r) A[(i64)gi * lda + gj + 1] = acc[t][u][1];
+            if (gj < r) rp[t][gj] = acc[t][u][0];
+            if (gj + 1 < r) rp[t][gj + 1] = acc[t][u][1];
           }
         }
       }
@@ -148,11 +152,11 @@ __global__ void __launch_bounds__(256) trsm_back_kernel(const CholDesc* __restri
   __shared__ double Ljj[32][33];
   __shared__ double V[64][33];
   const CholDesc d = descs[blockIdx.x];
-  const int r = d.r, me = d.mextra;
-  if (me <= 0 || r <= 0) return;
   if (d.status && *d.status != ST_OK) return;
+  const int r = *d.pr, me = d.mextra;
+  if (me <= 0 || r <= 0) return;
   const double* L = d.A;
-  double* U = d.A + (i64)r * d.lda;
+  double* U = d.A + (i64)d.uoff * d.lda;
   const i64 lda = d.lda;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
@@ -225,7 +229,18 @@ __global__ void __launch_bounds__(256) id_kernel(BoxDev* __restrict__ boxes, con
   extern __shared__ __align__(16) double Hs[];
   BoxDev& b = boxes[blockIdx.x];
   const int nb = b.nb, r = b.r;
+  if (b.status != ST_OK) {                 // e.g. too few samples for this near field
+    if (threadIdx.x == 0) {
+      b.k = nb;
+      b.nr = 0;
+      b.nc = r;
+    }
+    return;
+  }
   const int ldh = nb + 1;
+  // H = [Y'' Z''][Y'' Z'']^T is unnormalised: S = [Y' Z'] / sqrt(2w) => compare
+  // H_jj against 2 w atol^2 (T = (R11^-1 R12)^T is scale invariant)
+  const double thr = atol2 * 2.0 * (double)(p - r);
   int* perm = reinterpret_cast<int*>(Hs + nb * ldh);
   int* rank_of = perm + nb;        // sorted position of pivot-order entries
   int* is_red = rank_of + nb;
@@ -264,7 +279,7 @@ __global__ void __launch_bounds__(256) id_kernel(BoxDev* __restrict__ boxes, con
       }
     }
     __syncthreads();
-    if (!(pval > atol2)) {
+    if (!(pval > thr)) {
       if (tid == 0) kfinal = j;
       break;
     }
@@ -412,22 +427,23 @@ __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ bo
   if (tid == 0) singular = 0;
   __syncthreads();
   const double* T = fpool + b.f_T;
-  const double* WY = ws + b.off_aug + (i64)r * b.ldaug;
-  const double* WZ = ws + b.off_aug + (i64)(r + nb) * b.ldaug + (i64)r * b.ldaug;
+  const i64 ldr = b.ldr;
+  const double* WY = ws + b.off_aug + (i64)b.rmax * ldr;
+  const double* WZ = ws + b.off_aug + (i64)(b.rmax + nb) * ldr + (i64)b.rmax * ldr;
   double* XY = ws + b.off_xy;
   double* XZ = ws + b.off_xz;
   // 1. row combination X = W_r - T W_s
   for (int idx = tid; idx < nr * r; idx += 256) {
     const int i = idx / r, j = idx % r;
-    double vy = WY[(i64)redloc[i] * b.ldaug + j];
-    double vz = WZ[(i64)redloc[i] * b.ldaug + j];
+    double vy = WY[(i64)redloc[i] * ldr + j];
+    double vz = WZ[(i64)redloc[i] * ldr + j];
     for (int s = 0; s < k; ++s) {
       const double t = T[(i64)i * ldn + s];
-      vy -= t * WY[(i64)skelloc[s] * b.ldaug + j];
-      vz -= t * WZ[(i64)skelloc[s] * b.ldaug + j];
+      vy -= t * WY[(i64)skelloc[s] * ldr + j];
+      vz -= t * WZ[(i64)skelloc[s] * ldr + j];
     }
-    XY[(i64)i * r + j] = vy;
-    XZ[(i64)i * r + j] = vz;
+    XY[(i64)i * ldr + j] = vy;
+    XZ[(i64)i * ldr + j] = vz;
   }
   __syncthreads();
   // 2. column fix X[:, red] -= X[:, skel] T^T  (F_loc^-1 on b's own columns)
@@ -435,15 +451,15 @@ __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ bo
     for (int idx = tid; idx < nr * nr; idx += 256) {
       const int i = idx / nr, jj = idx % nr;
       const int col = b.self_pos + redloc[jj];
-      double vy = XY[(i64)i * r + col];
-      double vz = XZ[(i64)i * r + col];
+      double vy = XY[(i64)i * ldr + col];
+      double vz = XZ[(i64)i * ldr + col];
       for (int s = 0; s < k; ++s) {
         const double t = T[(i64)jj * ldn + s];
-        vy -= XY[(i64)i * r + b.self_pos + skelloc[s]] * t;
-        vz -= XZ[(i64)i * r + b.self_pos + skelloc[s]] * t;
+        vy -= XY[(i64)i * ldr + b.self_pos + skelloc[s]] * t;
+        vz -= XZ[(i64)i * ldr + b.self_pos + skelloc[s]] * t;
       }
-      XY[(i64)i * r + col] = vy;
-      XZ[(i64)i * r + col] = vz;
+      XY[(i64)i * ldr + col] = vy;
+      XZ[(i64)i * ldr + col] = vz;
     }
     __syncthreads();
   }
@@ -451,7 +467,7 @@ __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ bo
   double* Xrr = fpool + b.f_Xrr;
   for (int idx = tid; idx < nr * nr; idx += 256) {
     const int i = idx / nr, j = idx % nr;
-    const double v = XY[(i64)i * r + b.self_pos + redloc[j]];
+    const double v = XY[(i64)i * ldr + b.self_pos + redloc[j]];
     Xs[i * ldx + j] = v;
     Xrr[(i64)i * ldn + j] = v;
   }
@@ -459,11 +475,11 @@ __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ bo
   double* Xcr = ws + b.off_xcr;
   for (int idx = tid; idx < nr * nc; idx += 256) {
     const int i = idx / nc, j = idx % nc;
-    Xrc[(i64)i * ((r + 1) & ~1) + j] = XY[(i64)i * r + cpos[j]];
+    Xrc[(i64)i * ldr + j] = XY[(i64)i * ldr + cpos[j]];
   }
   for (int idx = tid; idx < nr * nc; idx += 256) {
     const int j = idx / nr, i = idx % nr;
-    Xcr[(i64)j * ldn + i] = XZ[(i64)i * r + cpos[j]];
+    Xcr[(i64)j * ldn + i] = XZ[(i64)i * ldr + cpos[j]];
   }
   __syncthreads();
   // 4. LU with partial pivoting
@@ -545,6 +561,44 @@ __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ bo
   for (int idx = tid; idx < nr * nr; idx += 256) {
     const int i = idx / nr, j = idx % nr;
     Xinv[(i64)i * ldn + j] = Is[i * ldx + j];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Near-field row list of every box of a colour batch, built on the device:
+// near = active(I_b u I_n) in Morton order of the neighbour boxes
+// (R2).  Neighbours processed by an earlier
+// colour contribute only their skeleton rows (their redundant rows are
+// decoupled); the others contribute all their rows.
+// ---------------------------------------------------------------------------
+__global__ void build_near_kernel(BoxDev* __restrict__ boxes, const BoxDev* __restrict__ level_boxes,
+                                  int* __restrict__ iws, int p, int oversample) {
+  BoxDev& b = boxes[blockIdx.x];
+  const int lane = threadIdx.x;
+  const int* nd = iws + b.off_nbr;
+  int* near = iws + b.off_rows;
+  int o = 0, selfp = 0;
+  for (int q = 0; q < b.nnbr; ++q) {
+    const int idx = nd[3 * q], r0 = nd[3 * q + 1];
+    int cnt = nd[3 * q + 2];
+    if (idx >= 0) {
+      const BoxDev& nbx = level_boxes[idx];
+      cnt = nbx.k;
+      const int* src = iws + nbx.off_skelrow;
+      for (int t = lane; t < cnt; t += 32) near[o + t] = src[t];
+    } else {
+      if (r0 == b.row0) selfp = o;
+      for (int t = lane; t < cnt; t += 32) near[o + t] = r0 + t;
+    }
+    o += cnt;
+  }
+  if (lane == 0) {
+    b.r = o;
+    b.self_pos = selfp;
+    b.status = (p - o < oversample + 1) ? ST_SAMPLES : ST_OK;
+    b.k = 0;
+    b.nr = 0;
+    b.nc = 0;
   }
 }
 

@@ -205,37 +205,30 @@ struct rsrs_factor_s {
   DBuf xtmp;
   rsrs_stats stats{};
   cudaStream_t stream = nullptr;
+  double kc_ms[RSRS_NUM_KERNEL_CLASSES] = {0};
+  double kc_flops[RSRS_NUM_KERNEL_CLASSES] = {0};
+  double kc_bytes[RSRS_NUM_KERNEL_CLASSES] = {0};
+  int64_t kc_launches[RSRS_NUM_KERNEL_CLASSES] = {0};
 };
 
+enum KC {
+  KC_GRAM = 0,   // gemm_nt: near-field Grams and Y_b M^T
+  KC_CHOL,       // chol_aug
+  KC_TRSM,       // trsm_back
+  KC_PROJ,       // gemm_nn: Y'' = Y_b - W M
+  KC_HGRAM,      // gemm_nt: H = S S^T
+  KC_ID,         // id_kernel
+  KC_EF,         // gemm_nn: E/F updates
+  KC_EXTRACT,    // extract_lu_kernel
+  KC_G,          // gemm_nn: G_U, G_L
+  KC_UPD,        // gemm_nn: L/U updates
+  KC_MISC        // compaction + top block
+};
+static const char* KC_NAMES[RSRS_NUM_KERNEL_CLASSES] = {
+    "gemm_nt_gram", "chol_aug", "trsm_back", "gemm_nn_proj", "gemm_nt_idgram", "id",
+    "gemm_nn_ef",   "extract_lu", "gemm_nn_g", "gemm_nn_lu_update", "compact_top"};
+
 namespace {
-
-// algorithmic real flops of one box
-double model_flops_box(double NB, double R, double K, double P) {
-  const double nr = NB - K, nc = R - nr;
-  double f = 0;
-  f += 2 * (R * (R + 1) * P);                       // near-field Grams (symmetric), both sides
-  f += 2 * (2 * NB * R * P);                        // B = Y_b M^T
-  f += 2 * (R * R * R / 3.0);                       // Cholesky
-  f += 2 * (2 * NB * R * R);                        // u = B L^-T, W = u L^-1
-  f += 2 * (2 * NB * R * P);                        // Y'' = Y_b - W M
-  f += NB * (NB + 1) * 2 * P;                       // H (symmetric)
-  if (nr > 0) {
-    f += 4 * (2 * nr * K * P);                      // E/F updates
-    f += 2 * (2 * nr * K * R + 2 * nr * nr * K);    // extraction combinations
-    f += 2.0 * nr * nr * nr;                        // LU + inverse
-    f += 2 * (2 * nr * nr * nc);                    // G_U, G_L
-    f += 2 * (2 * nc * nr * P);                     // L/U updates
-  }
-  return f;
-}
-
-// algorithmic HBM bytes of one box (samples read/written once; factors written once)
-double model_bytes_box(double NB, double R, double K, double P) {
-  const double nr = NB - K, nc = R - nr;
-  double b = 2 * R * P + 2 * NB * P;                // near Omega/Psi rows, own Y/Z rows
-  if (nr > 0) b += 2 * 2 * nc * P + 2 * NB * P + nr * K + 2 * nc * nr + 2 * nr * nr;
-  return 8.0 * b;
-}
 
 struct Planner {
   rsrs_factorization f;
@@ -245,8 +238,80 @@ struct Planner {
   int l = 10;
   int64_t launches = 0;
   double flops = 0, bytes = 0;
+  bool profile = false;
+  std::vector<cudaEvent_t> evpool;
+  struct Pend {
+    int cls;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pend> pend;
+  int cur_cls = 0;
+  cudaEvent_t cur_a = nullptr;
 
   Planner(rsrs_factorization f_, const rsrs::Tree& t, cudaStream_t st) : f(f_), T(t), s(st) {}
+  ~Planner() {
+    for (auto& p : pend) {
+      evpool.push_back(p.a);
+      evpool.push_back(p.b);
+    }
+    for (auto e : evpool) cudaEventDestroy(e);
+  }
+  cudaEvent_t ev() {
+    if (evpool.empty()) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      return e;
+    }
+    cudaEvent_t e = evpool.back();
+    evpool.pop_back();
+    return e;
+  }
+  void tic(int cls) {
+    cur_cls = cls;
+    f->kc_launches[cls]++;
+    if (!profile) return;
+    cur_a = ev();
+    CK(cudaEventRecord(cur_a, s));
+  }
+  void toc() {
+    if (!profile) return;
+    cudaEvent_t b = ev();
+    CK(cudaEventRecord(b, s));
+    pend.push_back(Pend{cur_cls, cur_a, b});
+  }
+  void flush_prof() {  // after a stream synchronize
+    for (auto& p : pend) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, p.a, p.b));
+      f->kc_ms[p.cls] += ms;
+      evpool.push_back(p.a);
+      evpool.push_back(p.b);
+    }
+    pend.clear();
+  }
+  void account(int cls, double fl, double by) {
+    f->kc_flops[cls] += fl;
+    f->kc_bytes[cls] += by;
+    flops += fl;
+    bytes += by;
+  }
+  // algorithmic FLOPs / HBM bytes of one box by kernel class
+  void account_box(double nb, double r, double k, double P) {
+    const double nr = nb - k, nc = r - nr, W8 = 8.0;
+    account(KC_GRAM, 2 * (r * (r + 1) * P + 2 * nb * r * P), W8 * (2 * (r * P + nb * P) + 2 * (r * (r + 1) / 2 + nb * r)));
+    account(KC_CHOL, 2 * (r * r * r / 3 + nb * r * r), W8 * 2 * 2 * (r * (r + 1) / 2 + nb * r));
+    account(KC_TRSM, 2 * (nb * r * r), W8 * 2 * (r * (r + 1) / 2 + 2 * nb * r));
+    account(KC_PROJ, 2 * (2 * nb * r * P), W8 * 2 * (nb * r + r * P + 2 * nb * P));
+    account(KC_HGRAM, 2 * nb * (nb + 1) * P, W8 * (2 * nb * P + nb * nb));
+    account(KC_ID, 2 * k * nb * nb + nr * k * k, W8 * (nb * nb + nr * k));
+    if (nr > 0) {
+      account(KC_EF, 4 * 2 * nr * k * P, W8 * 2 * ((k * P + 2 * nr * P) + (nr * P + 2 * k * P)));
+      account(KC_EXTRACT, 2 * (2 * nr * k * r + 2 * nr * nr * k) + 2 * nr * nr * nr,
+              W8 * (2 * nb * r + 2 * nr * r + 2 * nr * nc + 2 * nr * nr));
+      account(KC_G, 2 * 2 * nr * nr * nc, W8 * 2 * (2 * nr * nc + nr * nr));
+      account(KC_UPD, 2 * 2 * nc * nr * P, W8 * 2 * (nr * P + 2 * nc * P + nc * nr));
+    }
+  }
 
   DBuf* keep(size_t nbytes) {
     f->keep.emplace_back(new DBuf());
@@ -281,22 +346,12 @@ struct Planner {
       const rsrs::TreeLevel& lv = T.levels[lev];
       const int nbox = (int)lv.nboxes;
       const double atol = cid * eps * std::pow(g, (double)(L - lev));
-      std::vector<int> row0(nbox + 1, 0), rcount(nbox, 0), selfpos(nbox, 0);
+      std::vector<int> row0(nbox + 1, 0), rmaxv(nbox, 0);
       for (int b = 0; b < nbox; ++b) row0[b + 1] = row0[b] + nb_box[b];
       for (int b = 0; b < nbox; ++b) {
         int r = 0;
-        for (int q = lv.nbr_off[b]; q < lv.nbr_off[b + 1]; ++q) {
-          const int j = lv.nbr[q];
-          if (j == b) selfpos[b] = r;
-          r += nb_box[j];
-        }
-        rcount[b] = r;
-        if (nb_box[b] > 0 && p - r < l + 1) {
-          std::ostringstream os;
-          os << "level " << lev << " box " << b << ": p - r = " << p - r << " < l + 1 = " << l + 1
-             << " (deficit " << (l + 1) - (p - r) << " samples)";
-          throw StatusError{RSRS_ERR_SAMPLES, os.str()};
-        }
+        for (int q = lv.nbr_off[b]; q < lv.nbr_off[b + 1]; ++q) r += nb_box[lv.nbr[q]];
+        rmaxv[b] = r;
         if (nb_box[b] > 160) {
           std::ostringstream os;
           os << "level " << lev << " box " << b << ": |I_b| = " << nb_box[b] << " exceeds 160";
@@ -309,9 +364,10 @@ struct Planner {
       for (int b = 0; b < nbox; ++b)
         if (nb_box[b] > 0) bycol[lv.colour[b]].push_back(b);
 
-      // ---- host layout of the level --------------------------------------
+      // ---- host layout of the level (canonical order: colour-major, Morton inside)
       std::vector<BoxDev> hb;
       hb.reserve(nbox);
+      std::vector<int> hb_of(nbox, -1);
       struct BInfo {
         int first, count, max_nb, max_r, max_m;
       };
@@ -324,20 +380,21 @@ struct Planner {
         for (int b : bycol[c]) {
           BoxDev x;
           std::memset(&x, 0, sizeof(x));
-          const i64 nb = nb_box[b], r = rcount[b];
+          const i64 nb = nb_box[b], r = rmaxv[b];
           const i64 ldn = even(nb), ldr = even(r);
           x.nb = (int)nb;
-          x.r = (int)r;
-          x.self_pos = selfpos[b];
+          x.rmax = (int)r;
+          x.ldr = (int)ldr;
+          x.ldn = (int)ldn;
           x.row0 = row0[b];
-          x.ldaug = (int)ldr;
           x.level = lev;
           x.box = b;
+          x.nnbr = lv.nbr_off[b + 1] - lv.nbr_off[b];
           x.off_aug = wo;   wo += 2 * (r + nb) * ldr;
           x.off_yz = wo;    wo += nb * 2 * nld;
           x.off_h = wo;     wo += nb * ldn;
-          x.off_xy = wo;    wo += even(nb * r);
-          x.off_xz = wo;    wo += even(nb * r);
+          x.off_xy = wo;    wo += nb * ldr;
+          x.off_xz = wo;    wo += nb * ldr;
           x.off_xrc = wo;   wo += nb * ldr;
           x.off_xcr = wo;   wo += r * ldn;
           x.off_rows = ioff;    ioff += r + nb;
@@ -345,6 +402,7 @@ struct Planner {
           x.off_redrow = ioff;  ioff += nb;
           x.off_crow = ioff;    ioff += r;
           x.off_cpos = ioff;    ioff += r;
+          x.off_nbr = ioff;     ioff += 3 * x.nnbr;
           x.f_T = foff;     foff += nb * ldn;
           x.f_GL = foff;    foff += r * ldn;
           x.f_GU = foff;    foff += nb * ldr;
@@ -353,6 +411,7 @@ struct Planner {
           x.f_red = fioff;  fioff += nb;
           x.f_skel = fioff; fioff += nb;
           x.f_c = fioff;    fioff += r;
+          hb_of[b] = (int)hb.size();
           hb.push_back(x);
           bi.max_nb = std::max<int>(bi.max_nb, (int)nb);
           bi.max_r = std::max<int>(bi.max_r, (int)r);
@@ -372,62 +431,68 @@ struct Planner {
       double* dws = ws.as<double>();
       int* diws = iws.as<int>();
       {
-        std::vector<int> hrows(std::max<i64>(ioff, 1), 0);
+        // b rows (static) and neighbour records {boxdev index if processed earlier, row0, nb}
+        std::vector<int> hint(std::max<i64>(ioff, 1), 0);
         for (const BoxDev& x : hb) {
-          int o = (int)x.off_rows;
           const int b = x.box;
+          for (int t = 0; t < x.nb; ++t) hint[x.off_rows + x.rmax + t] = x.row0 + t;
+          int q3 = (int)x.off_nbr;
           for (int q = lv.nbr_off[b]; q < lv.nbr_off[b + 1]; ++q) {
             const int j = lv.nbr[q];
-            for (int t = 0; t < nb_box[j]; ++t) hrows[o++] = row0[j] + t;
+            const bool done = nb_box[j] > 0 && lv.colour[j] < lv.colour[b];
+            hint[q3++] = done ? hb_of[j] : -1;
+            hint[q3++] = row0[j];
+            hint[q3++] = nb_box[j];
           }
-          for (int t = 0; t < x.nb; ++t) hrows[o++] = x.row0 + t;
         }
-        CK(cudaMemcpyAsync(diws, hrows.data(), sizeof(int) * ioff, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(diws, hint.data(), sizeof(int) * ioff, cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(dboxes, hb.data(), sizeof(BoxDev) * hb.size(), cudaMemcpyHostToDevice, s));
         CK(cudaStreamSynchronize(s));
       }
 
-      // ---- descriptors --------------------------------------------------
+      // ---- descriptors (sizes that depend on the near set point at BoxDev::r / nr / nc / k)
       std::vector<NTDesc> nt_gram, nt_h;
       std::vector<NNDesc> nn_proj, nn_ef, nn_g, nn_upd;
       std::vector<CholDesc> chol;
       for (size_t q = 0; q < hb.size(); ++q) {
         const BoxDev& x = hb[q];
         BoxDev* dx = dboxes + q;
-        const int nb = x.nb, r = x.r;
-        const i64 ldr = x.ldaug, ldn = even(nb);
+        const int nb = x.nb, rm = x.rmax;
+        const i64 ldr = x.ldr, ldn = x.ldn;
         const int* near = diws + x.off_rows;
-        const int* brows = near + r;
+        const int* brows = near + rm;
         double* augO = dws + x.off_aug;
-        double* augP = augO + (i64)(r + nb) * ldr;
+        double* augP = augO + (i64)(rm + nb) * ldr;
         NTDesc a{};
         a.A = Om; a.rowA = near; a.lda = ld; a.B = Om; a.rowB = near; a.ldb = ld;
-        a.C = augO; a.ldc = ldr; a.m = r; a.n = r; a.K = p; a.sym_rows = r; a.alpha = 1.0;
+        a.C = augO; a.ldc = ldr; a.m = rm; a.n = rm; a.K = p; a.sym_rows = rm; a.alpha = 1.0;
+        a.pm = &dx->r; a.pn = &dx->r; a.psym = &dx->r;
         nt_gram.push_back(a);
         a.A = Ps; a.B = Ps; a.C = augP;
         nt_gram.push_back(a);
         NTDesc bq{};
         bq.A = Y; bq.rowA = brows; bq.lda = ld; bq.B = Om; bq.rowB = near; bq.ldb = ld;
-        bq.C = augO + (i64)r * ldr; bq.ldc = ldr; bq.m = nb; bq.n = r; bq.K = p; bq.sym_rows = 0; bq.alpha = 1.0;
+        bq.C = augO + (i64)rm * ldr; bq.ldc = ldr; bq.m = nb; bq.n = rm; bq.K = p; bq.sym_rows = 0;
+        bq.alpha = 1.0; bq.pn = &dx->r;
         nt_gram.push_back(bq);
-        bq.A = Z; bq.B = Ps; bq.C = augP + (i64)r * ldr;
+        bq.A = Z; bq.B = Ps; bq.C = augP + (i64)rm * ldr;
         nt_gram.push_back(bq);
-        chol.push_back(CholDesc{augO, ldr, r, nb, &dx->status});
-        chol.push_back(CholDesc{augP, ldr, r, nb, &dx->status});
+        chol.push_back(CholDesc{augO, ldr, &dx->r, nb, rm, &dx->status});
+        chol.push_back(CholDesc{augP, ldr, &dx->r, nb, rm, &dx->status});
         double* yz = dws + x.off_yz;
         NNDesc pr{};
-        pr.A = augO + (i64)r * ldr; pr.lda = ldr; pr.transA = 0;
+        pr.A = augO + (i64)rm * ldr; pr.lda = ldr; pr.transA = 0;
         pr.B = Om; pr.rowB = near; pr.ldb = ld;
         pr.D = yz; pr.rowD = nullptr; pr.ldd = 2 * nld;
         pr.Cin = Y + (i64)x.row0 * ld; pr.rowC = nullptr; pr.ldc = ld;
-        pr.m = nb; pr.n = p; pr.K = r; pr.alpha = -1.0; pr.beta = 1.0;
+        pr.m = nb; pr.n = p; pr.K = rm; pr.alpha = -1.0; pr.beta = 1.0; pr.pK = &dx->r;
         nn_proj.push_back(pr);
-        pr.A = augP + (i64)r * ldr; pr.B = Ps; pr.D = yz + nld; pr.Cin = Z + (i64)x.row0 * ld;
+        pr.A = augP + (i64)rm * ldr; pr.B = Ps; pr.D = yz + nld; pr.Cin = Z + (i64)x.row0 * ld;
         nn_proj.push_back(pr);
         NTDesc h{};
         h.A = yz; h.rowA = nullptr; h.lda = 2 * nld; h.B = yz; h.rowB = nullptr; h.ldb = 2 * nld;
         h.C = dws + x.off_h; h.ldc = ldn; h.m = nb; h.n = nb; h.K = (int)(2 * nld); h.sym_rows = 0;
-        h.alpha = 1.0 / (2.0 * (double)(p - r));
+        h.alpha = 1.0;
         nt_h.push_back(h);
         const int* skelrow = diws + x.off_skelrow;
         const int* redrow = diws + x.off_redrow;
@@ -448,18 +513,18 @@ struct Planner {
         nn_ef.push_back(fo);
         NNDesc gu{};
         gu.A = fpool + x.f_Xinv; gu.lda = ldn; gu.B = dws + x.off_xrc; gu.rowB = nullptr; gu.ldb = ldr;
-        gu.D = fpool + x.f_GU; gu.ldd = ldr; gu.Cin = nullptr; gu.m = nb; gu.n = r; gu.K = nb;
+        gu.D = fpool + x.f_GU; gu.ldd = ldr; gu.Cin = nullptr; gu.m = nb; gu.n = rm; gu.K = nb;
         gu.alpha = 1.0; gu.beta = 0.0; gu.pm = &dx->nr; gu.pn = &dx->nc; gu.pK = &dx->nr;
         nn_g.push_back(gu);
         NNDesc gl{};
         gl.A = dws + x.off_xcr; gl.lda = ldn; gl.B = fpool + x.f_Xinv; gl.rowB = nullptr; gl.ldb = ldn;
-        gl.D = fpool + x.f_GL; gl.ldd = ldn; gl.Cin = nullptr; gl.m = r; gl.n = nb; gl.K = nb;
+        gl.D = fpool + x.f_GL; gl.ldd = ldn; gl.Cin = nullptr; gl.m = rm; gl.n = nb; gl.K = nb;
         gl.alpha = 1.0; gl.beta = 0.0; gl.pm = &dx->nc; gl.pn = &dx->nr; gl.pK = &dx->nr;
         nn_g.push_back(gl);
         const int* crow = diws + x.off_crow;
         NNDesc u{};
         u.A = fpool + x.f_GL; u.lda = ldn; u.transA = 0; u.B = Y; u.rowB = redrow; u.ldb = ld;
-        u.D = Y; u.rowD = crow; u.ldd = ld; u.Cin = nullptr; u.m = r; u.n = p; u.K = nb;
+        u.D = Y; u.rowD = crow; u.ldd = ld; u.Cin = nullptr; u.m = rm; u.n = p; u.K = nb;
         u.alpha = -1.0; u.beta = 1.0; u.pm = &dx->nc; u.pK = &dx->nr;
         nn_upd.push_back(u);
         NNDesc uz = u;
@@ -496,28 +561,53 @@ struct Planner {
       for (const BInfo& bi : binfo) {
         const int n = bi.count, q0 = bi.first;
         BoxDev* dbx = dboxes + q0;
+        tic(KC_MISC);
+        rsrs::build_near_kernel<<<n, 32, 0, s>>>(dbx, dboxes, diws, p, l);
+        post("build_near_kernel", s, launches);
+        toc();
+        tic(KC_GRAM);
         launch_nt(Dgram + 4 * q0, 4 * n, bi.max_r, bi.max_r, s, launches);
+        toc();
+        tic(KC_CHOL);
         launch_chol(Dchol + 2 * q0, 2 * n, bi.max_m, s, launches);
+        toc();
+        tic(KC_TRSM);
         rsrs::trsm_back_kernel<<<2 * n, 256, 0, s>>>(Dchol + 2 * q0);
         post("trsm_back_kernel", s, launches);
+        toc();
+        tic(KC_PROJ);
         launch_nn(Dproj + 2 * q0, 2 * n, bi.max_nb, p, s, launches);
+        toc();
+        tic(KC_HGRAM);
         launch_nt(Dh + q0, n, bi.max_nb, bi.max_nb, s, launches);
+        toc();
         {
           const size_t sm = (size_t)bi.max_nb * (bi.max_nb + 1) * 8 + 3 * (size_t)bi.max_nb * 4 + 64;
+          tic(KC_ID);
           rsrs::id_kernel<<<n, 256, sm, s>>>(dbx, dws, diws, fpool, ipool, gidx, atol * atol, p, l);
           post("id_kernel", s, launches);
+          toc();
         }
+        tic(KC_EF);
         launch_nn(Def + 4 * q0, 4 * n, bi.max_nb, p, s, launches);
+        toc();
         {
           const size_t sm = 2 * (size_t)bi.max_nb * (bi.max_nb + 1) * 8 + 3 * (size_t)bi.max_nb * 4 + 64;
+          tic(KC_EXTRACT);
           rsrs::extract_lu_kernel<<<n, 256, sm, s>>>(dbx, dws, diws, fpool);
           post("extract_lu_kernel", s, launches);
+          toc();
         }
+        tic(KC_G);
         launch_nn(Dg + 2 * q0, 2 * n, bi.max_r, bi.max_r, s, launches);
+        toc();
+        tic(KC_UPD);
         launch_nn(Dupd + 2 * q0, 2 * n, bi.max_r, p, s, launches);
+        toc();
       }
       CK(cudaMemcpyAsync(hb.data(), dboxes, sizeof(BoxDev) * hb.size(), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
+      flush_prof();
       std::vector<int> newk(nbox, 0);
       f->ranks[lev].assign(nbox, -1);
       for (const BoxDev& x : hb) {
@@ -526,8 +616,12 @@ struct Planner {
           rsrs_status st = RSRS_ERR_SINGULAR;
           if (x.status == rsrs::ST_SAMPLES) {
             st = RSRS_ERR_SAMPLES;
-            os << "level " << x.level << " box " << x.box << ": rank " << x.k << " > p - r - l = "
-               << (p - x.r - l) << " (deficit " << x.k - (p - x.r - l) << " samples)";
+            if (p - x.r < l + 1)
+              os << "level " << x.level << " box " << x.box << ": p - r = " << p - x.r << " < l + 1 = " << l + 1
+                 << " (deficit " << (l + 1) - (p - x.r) << " samples)";
+            else
+              os << "level " << x.level << " box " << x.box << ": rank " << x.k << " > p - r - l = "
+                 << (p - x.r - l) << " (deficit " << x.k - (p - x.r - l) << " samples)";
           } else if (x.status == rsrs::ST_SINGULAR_GRAM) {
             os << "level " << x.level << " box " << x.box << ": near-field Gram not positive definite";
           } else {
@@ -542,8 +636,7 @@ struct Planner {
           f->stats.nsteps++;
           f->stats.memory_scalars += (int64_t)x.nr * x.k + 2LL * x.nr * x.nc + (int64_t)x.nr * x.nr;
         }
-        flops += model_flops_box(x.nb, x.r, x.k, p);
-        bytes += model_bytes_box(x.nb, x.r, x.k, p);
+        account_box(x.nb, x.r, x.k, p);
       }
       for (const BInfo& bi : binfo) {
         Batch B;
@@ -579,11 +672,14 @@ struct Planner {
         dstbuf.ensure(sizeof(int) * dst0.size(), s);
         CK(cudaMemcpyAsync(dstbuf.p, dst0.data(), sizeof(int) * dst0.size(), cudaMemcpyHostToDevice, s));
         dim3 grid((unsigned)hb.size(), 4);
+        tic(KC_MISC);
         rsrs::compact_kernel<<<grid, 128, 0, s>>>(dboxes, diws, dstbuf.as<int>(), Y, Z, Om, Ps, ld, gidx, nY, nZ,
                                                  nO, nP, nld, ng, p);
         post("compact_kernel", s, launches);
-        bytes += 2.0 * 4 * nnew * p * 8;
+        toc();
+        account(KC_MISC, 0.0, 2.0 * 4 * nnew * p * 8);
         CK(cudaStreamSynchronize(s));
+        flush_prof();
       }
       Y = nY; Z = nZ; Om = nO; Ps = nP; ld = nld;
       gidx = ng;
@@ -630,9 +726,12 @@ struct Planner {
     hd[0].A = Om; hd[0].rowA = nullptr; hd[0].lda = ld; hd[0].B = Om; hd[0].rowB = nullptr; hd[0].ldb = ld;
     hd[0].C = aug.as<double>(); hd[0].ldc = ldS; hd[0].m = nS; hd[0].n = nS; hd[0].K = p; hd[0].sym_rows = nS;
     hd[0].alpha = 1.0;
+    hd[0].pm = hd[0].pn = hd[0].psym = nullptr;
     hd[1] = hd[0];
     hd[1].A = Y; hd[1].C = aug.as<double>() + (i64)nS * ldS; hd[1].sym_rows = 0;
-    CholDesc cd{aug.as<double>(), ldS, nS, nS, dstat};
+    DBuf* nsb = keep(sizeof(int));
+    CK(cudaMemcpyAsync(nsb->p, &nS, sizeof(int), cudaMemcpyHostToDevice, s));
+    CholDesc cd{aug.as<double>(), ldS, nsb->as<int>(), nS, nS, dstat};
     DBuf dbuf;
     dbuf.alloc(sizeof(hd) + sizeof(cd) + 64, s);
     std::vector<char> h(sizeof(hd) + 16 + sizeof(cd));
@@ -643,6 +742,7 @@ struct Planner {
     CK(cudaStreamSynchronize(s));
     const NTDesc* dnt = dbuf.as<NTDesc>();
     const CholDesc* dch = reinterpret_cast<const CholDesc*>(dbuf.as<char>() + oc);
+    tic(KC_MISC);
     launch_nt(dnt, 2, nS, nS, s, launches);
     launch_chol(dch, 1, 2 * nS, s, launches);
     rsrs::trsm_back_kernel<<<1, 256, 0, s>>>(dch);
@@ -653,9 +753,11 @@ struct Planner {
                          cudaMemcpyDeviceToDevice, s));
     rsrs::top_lu_kernel<<<1, 1024, 0, s>>>(f->d_LU, ldS, nS, f->d_piv, dstat);
     post("top_lu_kernel", s, launches);
+    toc();
     int hst[4];
     CK(cudaMemcpyAsync(hst, dstat, sizeof(hst), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    flush_prof();
     if (hst[0] != 0)
       throw StatusError{RSRS_ERR_SINGULAR, hst[0] == rsrs::ST_SINGULAR_GRAM ? "top block: Gram of Omega_S not positive definite"
                                                                             : "top block A~_SS singular"};
@@ -665,7 +767,8 @@ struct Planner {
     for (int i = 0; i < nS; ++i) f->S_host[i] = tmp[i];
     f->stats.memory_scalars += (int64_t)nS * nS;
     const double n = nS;
-    flops += n * (n + 1) * p + 2 * n * n * p + n * n * n / 3 + 2 * n * n * n + 2 * n * n * n / 3;
+    account(KC_MISC, n * (n + 1) * p + 2 * n * n * p + n * n * n / 3 + 2 * n * n * n + 2 * n * n * n / 3,
+            8.0 * (2 * n * p + 3 * n * n));
   }
 };
 
@@ -686,7 +789,7 @@ rsrs_status rsrs_factor(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, void* Z,
   if (!t || !Y || !Z || !Omega || !Psi) return fail(RSRS_ERR_INVALID, "rsrs_factor: null argument");
   if (p < 1 || ld < p || (ld & 1)) return fail(RSRS_ERR_INVALID, "rsrs_factor: need 1 <= p <= ld and ld even");
   if (dt != RSRS_F64) return fail(RSRS_ERR_STATE, "rsrs_factor: RSRS_C128 is not built in this version");
-  rsrs_opts o{1e-6, 1.0, 1.0, 10, 2, 0, 1, nullptr, nullptr};
+  rsrs_opts o{1e-6, 1.0, 1.0, 10, 2, 0, 1, nullptr, nullptr, 0};
   if (opts) o = *opts;
   if (o.nranks != 1 || o.rank != 0 || o.nccl_comm)
     return fail(RSRS_ERR_STATE, "rsrs_factor: only nranks == 1 is supported by this build");
@@ -726,6 +829,7 @@ rsrs_status rsrs_factor(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, void* Z,
     P.g = o.level_growth;
     P.cid = o.id_scale;
     P.l = o.oversample;
+    P.profile = o.profile != 0;
     P.run((double*)Y, (double*)Z, (double*)Omega, (double*)Psi, ld);
     CK(cudaEventRecord(e1, s));
     CK(cudaEventSynchronize(e1));
@@ -819,6 +923,17 @@ rsrs_status rsrs_solve(rsrs_factorization f, void* B, int64_t ldb, int64_t nrhs,
 
 rsrs_status rsrs_apply(rsrs_factorization f, void* X, int64_t ldx, int64_t nrhs, void* s) {
   return sweep(f, X, ldx, nrhs, s, false);
+}
+
+rsrs_status rsrs_factor_profile(rsrs_factorization f, int cls, const char** name, double* ms, double* flops,
+                                double* bytes, int64_t* launches) {
+  if (!f || cls < 0 || cls >= RSRS_NUM_KERNEL_CLASSES) return fail(RSRS_ERR_INVALID, "rsrs_factor_profile: invalid argument");
+  if (name) *name = KC_NAMES[cls];
+  if (ms) *ms = f->kc_ms[cls];
+  if (flops) *flops = f->kc_flops[cls];
+  if (bytes) *bytes = f->kc_bytes[cls];
+  if (launches) *launches = f->kc_launches[cls];
+  return RSRS_OK;
 }
 
 rsrs_status rsrs_factor_stats(rsrs_factorization f, rsrs_stats* st) {

@@ -29,7 +29,8 @@ __global__ void __launch_bounds__(128) gemm_nt_kernel(const NTDesc* __restrict__
   const int n = d.pn ? *d.pn : d.n;
   const int i0 = blockIdx.y * GT, j0 = blockIdx.x * GT;
   if (i0 >= m || j0 >= n) return;
-  if (i0 + GT <= d.sym_rows && j0 >= i0 + GT) return;  // strictly upper tile of the Gram
+  const int sym = d.psym ? *d.psym : d.sym_rows;
+  if (i0 + GT <= sym && j0 >= i0 + GT) return;  // strictly upper tile of the Gram
   const int K = d.K;
   double* As = smem;
   double* Bs = smem + 2 * GT * GPA;

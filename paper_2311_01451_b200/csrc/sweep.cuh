@@ -21,7 +21,7 @@ __global__ void __launch_bounds__(256) solve_fwd_kernel(const BoxDev* __restrict
   const BoxDev b = boxes[blockIdx.x];
   const int nr = b.nr, k = b.k, nc = b.nc;
   if (nr <= 0) return;
-  const int ldn = (b.nb + 1) & ~1;
+  const int ldn = b.ldn;
   double* xs = sm;
   double* xr = xs + k;
   const int* red = ipool + b.f_red;
@@ -65,8 +65,8 @@ __global__ void __launch_bounds__(256) solve_bwd_kernel(const BoxDev* __restrict
   const BoxDev b = boxes[blockIdx.x];
   const int nr = b.nr, k = b.k, nc = b.nc;
   if (nr <= 0) return;
-  const int ldn = (b.nb + 1) & ~1;
-  const int ldr = (b.r + 1) & ~1;
+  const int ldn = b.ldn;
+  const int ldr = b.ldr;
   double* xc = sm;
   double* xr = xc + nc;
   const int* red = ipool + b.f_red;
@@ -107,8 +107,8 @@ __global__ void __launch_bounds__(256) apply_fwd_kernel(const BoxDev* __restrict
   const BoxDev b = boxes[blockIdx.x];
   const int nr = b.nr, k = b.k, nc = b.nc;
   if (nr <= 0) return;
-  const int ldn = (b.nb + 1) & ~1;
-  const int ldr = (b.r + 1) & ~1;
+  const int ldn = b.ldn;
+  const int ldr = b.ldr;
   double* xc = sm;
   double* xr = xc + nc;
   double* xr2 = xr + nr;
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(256) apply_bwd_kernel(const BoxDev* __restrict
   const BoxDev b = boxes[blockIdx.x];
   const int nr = b.nr, k = b.k, nc = b.nc;
   if (nr <= 0) return;
-  const int ldn = (b.nb + 1) & ~1;
+  const int ldn = b.ldn;
   double* xs = sm;
   double* xr = xs + k;
   const int* red = ipool + b.f_red;

@@ -31,7 +31,7 @@ STATUS_NAMES = {0: "OK", 1: "INVALID", 2: "SAMPLES", 3: "SINGULAR", 4: "CUDA", 5
 EXPORTS = [
     "rsrs_build_tree", "rsrs_tree_info", "rsrs_tree_perm", "rsrs_tree_level_size", "rsrs_tree_level",
     "rsrs_plan_samples", "rsrs_tree_destroy", "rsrs_factor", "rsrs_solve", "rsrs_apply",
-    "rsrs_factor_stats", "rsrs_factor_ranks", "rsrs_factor_top", "rsrs_factor_destroy",
+    "rsrs_factor_stats", "rsrs_factor_ranks", "rsrs_factor_top", "rsrs_factor_destroy", "rsrs_factor_profile",
     "rsrs_last_error", "rsrs_version",
 ]
 
@@ -45,7 +45,8 @@ class RSRSError(RuntimeError):
 class Opts(ctypes.Structure):
     _fields_ = [("eps", ctypes.c_double), ("level_growth", ctypes.c_double), ("id_scale", ctypes.c_double),
                 ("oversample", ctypes.c_int), ("top_level", ctypes.c_int), ("rank", ctypes.c_int),
-                ("nranks", ctypes.c_int), ("nccl_comm", ctypes.c_void_p), ("stream", ctypes.c_void_p)]
+                ("nranks", ctypes.c_int), ("nccl_comm", ctypes.c_void_p), ("stream", ctypes.c_void_p),
+                ("profile", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):
@@ -75,6 +76,10 @@ _lib.rsrs_apply.argtypes = [_vp, _vp, _i64, _i64, _vp]
 _lib.rsrs_factor_stats.argtypes = [_vp, ctypes.POINTER(Stats)]
 _lib.rsrs_factor_ranks.argtypes = [_vp, _i32, _vp, _i64]
 _lib.rsrs_factor_top.argtypes = [_vp, _vp, _i64, ctypes.POINTER(_i64)]
+_lib.rsrs_factor_profile.argtypes = [_vp, _i32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(_d),
+                                     ctypes.POINTER(_d), ctypes.POINTER(_d), ctypes.POINTER(_i64)]
+_lib.rsrs_factor_profile.restype = ctypes.c_int
+NUM_KERNEL_CLASSES = 11
 _lib.rsrs_factor_destroy.argtypes = [_vp]
 _lib.rsrs_factor_destroy.restype = None
 for _n in ("rsrs_build_tree", "rsrs_tree_info", "rsrs_tree_perm", "rsrs_tree_level_size", "rsrs_tree_level",
@@ -169,6 +174,17 @@ class Factorization:
         _check(_lib.rsrs_factor_stats(self._h, ctypes.byref(st)))
         return st.as_dict()
 
+    def profile(self) -> list:
+        """Per kernel class: name, device ms (opts.profile), algorithmic flops / bytes, launches."""
+        out = []
+        for c in range(NUM_KERNEL_CLASSES):
+            nm, ms, fl, by, nl = ctypes.c_char_p(), _d(), _d(), _d(), _i64()
+            _check(_lib.rsrs_factor_profile(self._h, c, ctypes.byref(nm), ctypes.byref(ms), ctypes.byref(fl),
+                                            ctypes.byref(by), ctypes.byref(nl)))
+            out.append({"name": nm.value.decode(), "ms": ms.value, "flops": fl.value, "bytes": by.value,
+                        "launches": nl.value})
+        return out
+
     def ranks(self, level: int, nboxes: int) -> np.ndarray:
         out = np.empty(max(nboxes, 1), np.int32)
         _check(_lib.rsrs_factor_ranks(self._h, level, out.ctypes.data, out.shape[0]))
@@ -204,13 +220,13 @@ class Factorization:
 
 def factor(tree: Tree, Y, Z, Omega, Psi, p: int, eps: float = 1e-6, level_growth: float = 1.0,
            id_scale: float = 1.0, oversample: int = 10, top_level: int = 2, stream=None,
-           dtype: int = RSRS_F64) -> Factorization:
+           dtype: int = RSRS_F64, profile: bool = False) -> Factorization:
     """rsrs_factor on CUDA tensors (N x ld, tree order); Y, Z, Omega, Psi are OVERWRITTEN."""
     ld = Y.stride(0)
     for t in (Z, Omega, Psi):
         if t.stride(0) != ld:
             raise ValueError("Y, Z, Omega, Psi must share the leading dimension")
-    o = Opts(eps, level_growth, id_scale, oversample, top_level, 0, 1, None, _stream_ptr(stream))
+    o = Opts(eps, level_growth, id_scale, oversample, top_level, 0, 1, None, _stream_ptr(stream), int(profile))
     h = _vp()
     _check(_lib.rsrs_factor(tree.handle, dtype, int(p), _ptr(Y), _ptr(Z), _ptr(Omega), _ptr(Psi), int(ld),
                             ctypes.byref(o), ctypes.byref(h)))

@@ -1,0 +1,148 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same
+seeded inputs.  Bar (BASELINE.json north_star): ||x_gpu - x_oracle|| / ||x_oracle||
+<= 10 eps, both solve residuals <= 10 eps, per-box ranks within +-2."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as W
+from gpu_common import dense_problem, gpu_apply, gpu_solve, rank_diffs, run_gpu, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+def _parity(cfg, X, root, p=None, check_apply=True):
+    X, A, Y, Z, Om, Ps, b = dense_problem(cfg, X, p)
+    t_or, f_or = run_oracle(cfg, X, Y, Z, Om, Ps, root)
+    t_g, f_g = run_gpu(cfg, X, Y, Z, Om, Ps, root, p=p)
+    x_or = O.solve(f_or, b)
+    x_g = gpu_solve(f_g, b)
+    eps = cfg.eps
+    err = np.linalg.norm(x_g - x_or) / np.linalg.norm(x_or)
+    res_g = np.linalg.norm(A @ x_g - b) / np.linalg.norm(b)
+    res_or = np.linalg.norm(A @ x_or - b) / np.linalg.norm(b)
+    assert err <= 10 * eps, err
+    assert res_g <= 10 * eps and res_or <= 10 * eps, (res_g, res_or)
+    levels = [lev for lev in range(t_or.L, 1, -1)]
+    d = rank_diffs(t_g, f_g, t_or, f_or, levels)
+    assert all(v <= 2 for v in d.values()), d
+    st = f_g.stats()
+    # |S| and the step count follow from the ranks
+    assert abs(st["top_size"] - f_or.S.shape[0]) <= 2 * len(t_or.levels[2].keys)
+    if check_apply:
+        v = W.gaussian(X.shape[0], 99, 7)
+        y_g = gpu_apply(f_g, v)
+        y_or = O.apply(f_or, v)
+        assert np.linalg.norm(y_g - y_or) / np.linalg.norm(y_or) <= 10 * eps
+        assert np.linalg.norm(y_g - A @ v) / np.linalg.norm(A @ v) <= 10 * eps
+        z = gpu_solve(f_g, y_g)
+        assert np.linalg.norm(z - v) / np.linalg.norm(v) <= 1e-11      # solve(apply(v)) = v
+    return dict(err=err, res_g=res_g, res_or=res_or, ranks=d, stats=st, f_or=f_or, t_or=t_or, f_g=f_g)
+
+
+def test_c1_parity():
+    """configs[0] (c1): 64x64 grid, 2D log kernel, N = 4096, every level."""
+    cfg = W.CONFIGS["c1"]
+    out = _parity(cfg, None, cfg.root())
+    st = out["stats"]
+    assert st["L"] == 3 and st["nlevels_compressed"] == 2
+    # identical ranks -> identical stored-scalar count (Table 1 'M')
+    if all(v == 0 for v in out["ranks"].values()) and st["top_size"] == out["f_or"].S.shape[0]:
+        assert st["memory_scalars"] == out["f_or"].memory()
+
+
+def test_ragged_clustered_points():
+    """Non-uniform points (ragged leaves, empty boxes, boxes of 1 point)."""
+    rng = np.random.default_rng(21)
+    X = rng.random((3000, 2)) ** 2
+    cfg = W.Config("ragged", "grid2d", 55, "log2d", "f64", leaf=40, p=640, seed=21, g=1.0)
+    _parity(cfg, X, (np.zeros(2), 1.0))
+
+
+def test_sphere_small():
+    """3D surface (c3/c5 family) at N = 8192 with the sphere sample count."""
+    cfg = W.CONFIGS["c3"].scaled(8192)
+    _parity(cfg, None, cfg.root())
+
+
+def test_tail_sizes_not_tile_multiples():
+    """p and box sizes that are not multiples of the 64-wide tiles / 32-wide chunks."""
+    cfg = W.Config("tail", "grid2d", 50, "log2d", "f64", leaf=37, p=650, seed=5, g=2.0)
+    _parity(cfg, None, cfg.root())
+
+
+def test_diagonal_operator_exact():
+    """Zero off-diagonal rank: every k = 0; K = A and K^-1 exact (special case)."""
+    import torch
+
+    import paper_2311_01451_b200 as R
+    rng = np.random.default_rng(8)
+    X = rng.random((2000, 2))
+    d = 1.0 + rng.random(2000)
+    t = R.Tree(X, 32, np.zeros(2), 1.0)
+    perm = t.perm()
+    Om = rng.standard_normal((2000, 512))
+    Ps = rng.standard_normal((2000, 512))
+    Om_t, Ps_t = Om[perm], Ps[perm]
+    dev = "cuda:0"
+    T = [torch.from_numpy(np.ascontiguousarray(M)).to(dev) for M in
+         (d[perm][:, None] * Om_t, d[perm][:, None] * Ps_t, Om_t, Ps_t)]
+    f = R.factor(t, *T, p=512, eps=1e-6)
+    for lev in range(t.L, 1, -1):
+        k = f.ranks(lev, len(t.level(lev)["keys"]))
+        assert (k[k >= 0] == 0).all()
+    v = rng.standard_normal(2000)
+    # extraction through the near-field Gram (CholeskyQR): error ~ cond(Omega_near)^2 eps,
+    # cond <= (sqrt p + sqrt r)/(sqrt p - sqrt r) ~ 12 at r <= 9*32, p = 512
+    assert np.allclose(gpu_apply(f, v), d * v, rtol=1e-11, atol=0)
+    assert np.allclose(gpu_solve(f, v), v / d, rtol=1e-11, atol=0)
+
+
+def test_insufficient_samples_reports_level_and_deficit():
+    import paper_2311_01451_b200 as R
+    cfg = W.CONFIGS["c1"]
+    X, A, Y, Z, Om, Ps, b = dense_problem(cfg, None, 560)
+    with pytest.raises(R.RSRSError) as e:
+        run_gpu(cfg, X, Y, Z, Om, Ps, cfg.root(), p=560)
+    assert e.value.status == 2
+    assert "level 3" in str(e.value) and "deficit" in str(e.value)
+
+
+def test_multiple_rhs():
+    cfg = W.CONFIGS["c1"]
+    X, A, Y, Z, Om, Ps, b = dense_problem(cfg)
+    t_g, f_g = run_gpu(cfg, X, Y, Z, Om, Ps, cfg.root())
+    B = W.rhs(cfg, nrhs=3)
+    Xs = gpu_solve(f_g, B)
+    for j in range(3):
+        assert np.allclose(Xs[:, j], gpu_solve(f_g, B[:, j]), rtol=0, atol=1e-13 * np.abs(Xs).max())
+        assert np.linalg.norm(A @ Xs[:, j] - B[:, j]) / np.linalg.norm(B[:, j]) <= 10 * cfg.eps
+
+
+def test_sampler_rows_match_direct_sum():
+    """Harness operator: GPU kernel matvec vs CPU direct sums on random rows."""
+    import torch
+
+    import paper_2311_01451_b200 as R
+    for cfg in (W.CONFIGS["c1"], W.CONFIGS["c3"].scaled(5000)):
+        X = W.points(cfg)
+        N = X.shape[0]
+        pts = np.zeros((N, 3))
+        pts[:, :X.shape[1]] = X
+        V = W.gaussian((N, 70), 3, 0)
+        Yd = torch.empty((N, 70), dtype=torch.float64, device="cuda:0")
+        R.sample_matvec(cfg.kernel, torch.from_numpy(pts).cuda(), W.kernel_weight(cfg),
+                        torch.from_numpy(V).cuda(), Yd)
+        rows = np.random.default_rng(1).choice(N, 64, replace=False)
+        ref = W.kernel_block(cfg, X, rows, np.arange(N)) @ V
+        got = Yd.cpu().numpy()[rows]
+        assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max() * math.sqrt(N)

@@ -20,7 +20,7 @@ def small_problem(kernel="log2d", n_side=32, leaf=16, p=416, seed=7, geometry="g
     X = W.points(cfg)
     t = O.build_tree(X, cfg.leaf, *cfg.root())
     A = W.dense_matrix(cfg, X)
-    Om, Ps = W.test_matrices(cfg)
+    Om, Ps = W.omega_psi(cfg)
     Y, Z = W.dense_samples(A, Om, Ps)
     P = t.perm
     At = A[np.ix_(P, P)]                              # operator in tree order
@@ -240,7 +240,7 @@ def test_c1_against_dense_lu():
     X = W.points(cfg)
     t = O.build_tree(X, cfg.leaf, *cfg.root())
     A = W.dense_matrix(cfg, X)
-    Om, Ps = W.test_matrices(cfg)
+    Om, Ps = W.omega_psi(cfg)
     Y, Z = W.dense_samples(A, Om, Ps)
     P = t.perm
     f = O.factor(t, Y[P], Z[P], Om[P], Ps[P], cfg.eps)

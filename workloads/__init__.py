@@ -45,8 +45,11 @@ class Config:
     dtype: str             # "f64" | "c128"
     leaf: int = 64
     eps: float = 1e-6
-    p: int = 640           # sample count (frozen per config)
+    p: int = 768           # sample count (frozen per config)
     seed: int = 1
+    g: float = 2.0         # per-level tolerance relaxation atol(l) = c_id eps g^(L-l)
+    c_id: float = 1.0
+    l: int = 10            # oversampling
     kappa: float = 25.0
     extra: dict = field(default_factory=dict)
 
@@ -78,11 +81,11 @@ class Config:
 
 
 CONFIGS = {
-    "c1": Config("c1", "grid2d", 64, "log2d", "f64", p=640, seed=1),
-    "c2": Config("c2", "grid2d", 512, "log2d", "f64", p=640, seed=2),
-    "c3": Config("c3", "sphere", 262144, "lap3d", "f64", p=1216, seed=3),
-    "c4": Config("c4", "grid2d", 512, "helm2d", "c128", p=640, seed=4),
-    "c5": Config("c5", "sphere", 1048576, "lap3d", "f64", p=1216, seed=5),
+    "c1": Config("c1", "grid2d", 64, "log2d", "f64", p=768, seed=1, g=2.0),
+    "c2": Config("c2", "grid2d", 512, "log2d", "f64", p=768, seed=2, g=2.0),
+    "c3": Config("c3", "sphere", 262144, "lap3d", "f64", p=1216, seed=3, g=2.0),
+    "c4": Config("c4", "grid2d", 512, "helm2d", "c128", p=768, seed=4, g=2.0),
+    "c5": Config("c5", "sphere", 1048576, "lap3d", "f64", p=1216, seed=5, g=2.0),
 }
 
 
@@ -174,7 +177,7 @@ def gaussian(shape, seed: int, stream: int, is_complex: bool = False) -> np.ndar
     return (re + 1j * im) * (1.0 / math.sqrt(2.0))
 
 
-def test_matrices(cfg: Config, N: int | None = None, p: int | None = None):
+def omega_psi(cfg: Config, N: int | None = None, p: int | None = None):
     """(Omega, Psi) of shape N x p in ORIGINAL point order."""
     N = cfg.N if N is None else N
     p = cfg.p if p is None else p
