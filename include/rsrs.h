@@ -76,6 +76,7 @@ typedef struct {
   double flops_model;        /* algorithmic flop count (SURVEY 8(d) model, real-equivalent) */
   double bytes_model;        /* algorithmic HBM bytes of the sweep */
   int64_t launches;          /* kernels launched by the last rsrs_factor */
+  int64_t solve_launches;    /* kernels one rsrs_solve / rsrs_apply call launches */
 } rsrs_stats;
 
 /* ---------------------------------------------------------------------------

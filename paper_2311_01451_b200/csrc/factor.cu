@@ -838,6 +838,7 @@ rsrs_status rsrs_factor(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, void* Z,
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     f->stats.factor_ms = ms;
+    f->stats.solve_launches = 2 + 2 * (int64_t)f->batches.size() + (f->nS > 0 ? 1 : 0);
     *out = f;
     return RSRS_OK;
   } catch (const StatusError& e) {

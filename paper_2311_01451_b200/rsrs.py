@@ -53,7 +53,8 @@ class Stats(ctypes.Structure):
     _fields_ = [("N", ctypes.c_int64), ("p", ctypes.c_int64), ("L", ctypes.c_int), ("top_level", ctypes.c_int),
                 ("nlevels_compressed", ctypes.c_int), ("nsteps", ctypes.c_int64), ("top_size", ctypes.c_int64),
                 ("max_rank", ctypes.c_int64), ("memory_scalars", ctypes.c_int64), ("factor_ms", ctypes.c_double),
-                ("flops_model", ctypes.c_double), ("bytes_model", ctypes.c_double), ("launches", ctypes.c_int64)]
+                ("flops_model", ctypes.c_double), ("bytes_model", ctypes.c_double), ("launches", ctypes.c_int64),
+                ("solve_launches", ctypes.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
