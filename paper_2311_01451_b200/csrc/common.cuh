@@ -45,6 +45,7 @@ struct BoxDev {
   i64 off_h;                  // doubles: H (nb x ldn)
   i64 off_xy, off_xz;         // doubles: X_Y, X_Z (nb x ldr each)
   i64 off_xrc, off_xcr;       // doubles: X_rc (nb x ldr), X_cr (rmax x ldn)
+  i64 off_linv;               // doubles: inverse diagonal blocks of the two Cholesky factors
   i64 off_rows;               // ints: near rows (capacity rmax) then b rows (nb)
   i64 off_skelrow, off_redrow, off_crow, off_cpos;  // ints: nb, nb, rmax, rmax
   i64 f_T, f_GL, f_GU, f_Xrr, f_Xinv;  // doubles in the level factor pool (lds ldn / ldr)
@@ -69,7 +70,7 @@ struct NTDesc {
   double* C;
   i64 ldc;
   int m, n, K, sym_rows;
-  double alpha;
+  double alpha, beta;
   const int* pm;  // optional device size overrides
   const int* pn;
   const int* psym;
@@ -105,6 +106,7 @@ struct CholDesc {
   const int* pr;
   int mextra, uoff;
   int* status;
+  double* linv;  // workspace: one 64 x 64 inverse diagonal block per panel
 };
 
 }  // namespace rsrs

@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "chol.cuh"
 #include "dense.cuh"
 #include "gemm.cuh"
 #include "internal.h"
@@ -83,6 +84,11 @@ void init_kernels() {
   set_smem(rsrs::chol_aug_kernel<32>, -1);
   set_smem(rsrs::chol_aug_kernel<16>, -1);
   set_smem(rsrs::chol_aug_kernel<8>, -1);
+  set_smem(rsrs::chol_update_kernel, rsrs::NT_SMEM);
+  set_smem(rsrs::chol_trsm_kernel, rsrs::NT_SMEM);
+  set_smem(rsrs::chol_back_a_kernel, rsrs::NN_SMEM);
+  set_smem(rsrs::chol_back_b_kernel, rsrs::NN_SMEM);
+  set_smem(rsrs::chol_diag_kernel, rsrs::CHOL_DIAG_SMEM);
   set_smem(rsrs::id_kernel, -1);
   set_smem(rsrs::extract_lu_kernel, -1);
   set_smem(rsrs::solve_fwd_kernel, -1);
@@ -159,6 +165,42 @@ void launch_chol(const CholDesc* d, int n, int mmax, cudaStream_t s, int64_t& la
   else if (nb == 16) rsrs::chol_aug_kernel<16><<<n, 256, sm, s>>>(d);
   else rsrs::chol_aug_kernel<8><<<n, 256, sm, s>>>(d);
   post("chol_aug", s, launches);
+}
+
+// blocked Cholesky + u = B L^-T of nmat matrices (panel width 64), see chol.cuh
+void launch_chol_blocked(const CholDesc* d, int nmat, int rmax, int mext, cudaStream_t s, int64_t& launches) {
+  const int CB = rsrs::CB;
+  const int np = (rmax + CB - 1) / CB;
+  const int gext = (mext + 63) / 64;
+  for (int q = 0; q < np; ++q) {
+    const int j0 = q * CB;
+    if (j0 > 0) {
+      dim3 g(1, std::max((rmax - j0 + 63) / 64, gext), 2 * nmat);
+      rsrs::chol_update_kernel<<<g, 128, rsrs::NT_SMEM, s>>>(d, j0);
+      post("chol_update", s, launches);
+    }
+    rsrs::chol_diag_kernel<<<nmat, 256, rsrs::CHOL_DIAG_SMEM, s>>>(d, j0);
+    post("chol_diag", s, launches);
+    dim3 g(1, std::max((rmax - j0 - CB + 63) / 64, gext), 2 * nmat);
+    rsrs::chol_trsm_kernel<<<g, 128, rsrs::NT_SMEM, s>>>(d, j0);
+    post("chol_trsm", s, launches);
+  }
+}
+
+// W = u L^-1 (back substitution by 64-column blocks, descending)
+void launch_back_blocked(const CholDesc* d, int nmat, int rmax, int mext, cudaStream_t s, int64_t& launches) {
+  const int CB = rsrs::CB;
+  const int np = (rmax + CB - 1) / CB;
+  dim3 g(1, (mext + 63) / 64, nmat);
+  for (int q = np - 1; q >= 0; --q) {
+    const int j0 = q * CB;
+    if (j0 + CB < rmax) {
+      rsrs::chol_back_a_kernel<<<g, 128, rsrs::NN_SMEM, s>>>(d, j0);
+      post("chol_back_a", s, launches);
+    }
+    rsrs::chol_back_b_kernel<<<g, 128, rsrs::NN_SMEM, s>>>(d, j0);
+    post("chol_back_b", s, launches);
+  }
 }
 
 void launch_nt(const NTDesc* d, int n, int mmax, int nmax, cudaStream_t s, int64_t& launches) {
@@ -397,6 +439,7 @@ struct Planner {
           x.off_xz = wo;    wo += nb * ldr;
           x.off_xrc = wo;   wo += nb * ldr;
           x.off_xcr = wo;   wo += r * ldn;
+          x.off_linv = wo;  wo += 2 * ((r + 63) / 64) * 64 * 64;
           x.off_rows = ioff;    ioff += r + nb;
           x.off_skelrow = ioff; ioff += nb;
           x.off_redrow = ioff;  ioff += nb;
@@ -477,8 +520,9 @@ struct Planner {
         nt_gram.push_back(bq);
         bq.A = Z; bq.B = Ps; bq.C = augP + (i64)rm * ldr;
         nt_gram.push_back(bq);
-        chol.push_back(CholDesc{augO, ldr, &dx->r, nb, rm, &dx->status});
-        chol.push_back(CholDesc{augP, ldr, &dx->r, nb, rm, &dx->status});
+        const i64 nlv = (i64)((rm + 63) / 64) * 64 * 64;
+        chol.push_back(CholDesc{augO, ldr, &dx->r, nb, rm, &dx->status, dws + x.off_linv});
+        chol.push_back(CholDesc{augP, ldr, &dx->r, nb, rm, &dx->status, dws + x.off_linv + nlv});
         double* yz = dws + x.off_yz;
         NNDesc pr{};
         pr.A = augO + (i64)rm * ldr; pr.lda = ldr; pr.transA = 0;
@@ -569,11 +613,10 @@ struct Planner {
         launch_nt(Dgram + 4 * q0, 4 * n, bi.max_r, bi.max_r, s, launches);
         toc();
         tic(KC_CHOL);
-        launch_chol(Dchol + 2 * q0, 2 * n, bi.max_m, s, launches);
+        launch_chol_blocked(Dchol + 2 * q0, 2 * n, bi.max_r, bi.max_nb, s, launches);
         toc();
         tic(KC_TRSM);
-        rsrs::trsm_back_kernel<<<2 * n, 256, 0, s>>>(Dchol + 2 * q0);
-        post("trsm_back_kernel", s, launches);
+        launch_back_blocked(Dchol + 2 * q0, 2 * n, bi.max_r, bi.max_nb, s, launches);
         toc();
         tic(KC_PROJ);
         launch_nn(Dproj + 2 * q0, 2 * n, bi.max_nb, p, s, launches);
@@ -708,8 +751,9 @@ struct Planner {
     }
     const i64 ldS = even(nS);
     f->ldS = (int)ldS;
-    DBuf aug;
+    DBuf aug, linv;
     aug.alloc(sizeof(double) * 2 * nS * ldS, s);
+    linv.alloc(sizeof(double) * ((nS + 63) / 64) * 64 * 64, s);
     DBuf* Sb = keep(sizeof(int) * nS);
     DBuf* Ab = keep(sizeof(double) * nS * ldS);
     DBuf* LUb = keep(sizeof(double) * nS * ldS);
@@ -731,7 +775,7 @@ struct Planner {
     hd[1].A = Y; hd[1].C = aug.as<double>() + (i64)nS * ldS; hd[1].sym_rows = 0;
     DBuf* nsb = keep(sizeof(int));
     CK(cudaMemcpyAsync(nsb->p, &nS, sizeof(int), cudaMemcpyHostToDevice, s));
-    CholDesc cd{aug.as<double>(), ldS, nsb->as<int>(), nS, nS, dstat};
+    CholDesc cd{aug.as<double>(), ldS, nsb->as<int>(), nS, nS, dstat, linv.as<double>()};
     DBuf dbuf;
     dbuf.alloc(sizeof(hd) + sizeof(cd) + 64, s);
     std::vector<char> h(sizeof(hd) + 16 + sizeof(cd));
@@ -744,9 +788,8 @@ struct Planner {
     const CholDesc* dch = reinterpret_cast<const CholDesc*>(dbuf.as<char>() + oc);
     tic(KC_MISC);
     launch_nt(dnt, 2, nS, nS, s, launches);
-    launch_chol(dch, 1, 2 * nS, s, launches);
-    rsrs::trsm_back_kernel<<<1, 256, 0, s>>>(dch);
-    post("trsm_back_kernel", s, launches);
+    launch_chol_blocked(dch, 1, nS, nS, s, launches);
+    launch_back_blocked(dch, 1, nS, nS, s, launches);
     CK(cudaMemcpy2DAsync(f->d_ASS, sizeof(double) * ldS, aug.as<double>() + (i64)nS * ldS, sizeof(double) * ldS,
                          sizeof(double) * nS, nS, cudaMemcpyDeviceToDevice, s));
     CK(cudaMemcpy2DAsync(f->d_LU, sizeof(double) * ldS, f->d_ASS, sizeof(double) * ldS, sizeof(double) * nS, nS,

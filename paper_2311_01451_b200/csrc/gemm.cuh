@@ -22,16 +22,11 @@ constexpr int GPB = 68;      // smem row stride of [32][64] tiles
 constexpr int NT_SMEM = 2 * 2 * GT * GPA * 8;              // 73,728 B
 constexpr int NN_SMEM = 2 * (GT * GPA + GBK * GPB) * 8;    // 71,680 B
 
-__global__ void __launch_bounds__(128) gemm_nt_kernel(const NTDesc* __restrict__ descs) {
-  extern __shared__ __align__(16) double smem[];
-  const NTDesc d = descs[blockIdx.z];
-  const int m = d.pm ? *d.pm : d.m;
-  const int n = d.pn ? *d.pn : d.n;
-  const int i0 = blockIdx.y * GT, j0 = blockIdx.x * GT;
-  if (i0 >= m || j0 >= n) return;
-  const int sym = d.psym ? *d.psym : d.sym_rows;
-  if (i0 + GT <= sym && j0 >= i0 + GT) return;  // strictly upper tile of the Gram
-  const int K = d.K;
+// dynamic size: min(cap, *p - off) when p is set, else cap
+RSRS_DI int dyn(const int* p, int off, int cap) { return p ? min(cap, *p - off) : cap; }
+
+// One 64x64 output tile of C = alpha A_rows B_rows^T + beta C (K columns).
+RSRS_DI void nt_tile(const NTDesc& d, int m, int n, int K, int i0, int j0, double* smem) {
   double* As = smem;
   double* Bs = smem + 2 * GT * GPA;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -109,22 +104,33 @@ __global__ void __launch_bounds__(128) gemm_nt_kernel(const NTDesc* __restrict__
     for (int u = 0; u < 4; ++u) {
       const int j = j0 + wc * 32 + u * 8 + 2 * tig;
       if (j + 1 < n) {
-        *reinterpret_cast<double2*>(crow + j) = make_double2(d.alpha * acc[t][u][0], d.alpha * acc[t][u][1]);
+        double2 c = make_double2(0.0, 0.0);
+        if (d.beta != 0.0) c = *reinterpret_cast<const double2*>(crow + j);
+        *reinterpret_cast<double2*>(crow + j) =
+            make_double2(d.beta * c.x + d.alpha * acc[t][u][0], d.beta * c.y + d.alpha * acc[t][u][1]);
       } else if (j < n) {
-        crow[j] = d.alpha * acc[t][u][0];
+        const double c = d.beta != 0.0 ? crow[j] : 0.0;
+        crow[j] = d.beta * c + d.alpha * acc[t][u][0];
       }
     }
   }
 }
 
-__global__ void __launch_bounds__(128) gemm_nn_kernel(const NNDesc* __restrict__ descs) {
+__global__ void __launch_bounds__(128) gemm_nt_kernel(const NTDesc* __restrict__ descs) {
   extern __shared__ __align__(16) double smem[];
-  const NNDesc d = descs[blockIdx.z];
-  const int m = d.pm ? *d.pm : d.m;
-  const int n = d.pn ? *d.pn : d.n;
-  const int K = d.pK ? *d.pK : d.K;
+  const NTDesc& d = descs[blockIdx.z];
+  const int m = dyn(d.pm, 0, d.m);
+  const int n = dyn(d.pn, 0, d.n);
   const int i0 = blockIdx.y * GT, j0 = blockIdx.x * GT;
   if (i0 >= m || j0 >= n) return;
+  const int sym = d.psym ? *d.psym : d.sym_rows;
+  if (i0 + GT <= sym && j0 >= i0 + GT) return;  // strictly upper tile of the Gram
+  const NTDesc dl = d;
+  nt_tile(dl, m, n, d.K, i0, j0, smem);
+}
+
+// One 64x64 output tile of D_rows = beta C_rows + alpha opA B_rows.
+RSRS_DI void nn_tile(const NNDesc& d, int m, int n, int K, int i0, int j0, double* smem) {
   const bool inplace = (d.Cin == nullptr);
   if (K <= 0 && inplace && d.beta == 1.0) return;
   double* As = smem;                       // [2][64][GPA]  (i, k)
@@ -252,6 +258,18 @@ __global__ void __launch_bounds__(128) gemm_nn_kernel(const NNDesc* __restrict__
       }
     }
   }
+}
+
+__global__ void __launch_bounds__(128) gemm_nn_kernel(const NNDesc* __restrict__ descs) {
+  extern __shared__ __align__(16) double smem[];
+  const NNDesc& d = descs[blockIdx.z];
+  const int m = dyn(d.pm, 0, d.m);
+  const int n = dyn(d.pn, 0, d.n);
+  const int K = dyn(d.pK, 0, d.K);
+  const int i0 = blockIdx.y * GT, j0 = blockIdx.x * GT;
+  if (i0 >= m || j0 >= n) return;
+  const NNDesc dl = d;
+  nn_tile(dl, m, n, K, i0, j0, smem);
 }
 
 }  // namespace rsrs
