@@ -166,8 +166,8 @@ def setup_problem(cfg, dev, seed_offset=0):
     Z_d = torch.empty_like(Ps_d)
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
-    R.sample_matvec(cfg.kernel, pts_d, W.kernel_weight(cfg), Om_d, Y_d)
-    R.sample_matvec(cfg.kernel, pts_d, W.kernel_weight(cfg), Ps_d, Z_d, adjoint=True)
+    R.sample_matvec(cfg.kernel, pts_d, W.kernel_weight(cfg), Om_d, Y_d, kappa=cfg.kappa)
+    R.sample_matvec(cfg.kernel, pts_d, W.kernel_weight(cfg), Ps_d, Z_d, adjoint=True, kappa=cfg.kappa)
     torch.cuda.synchronize(dev)
     t_sample = time.perf_counter() - t0
     b = torch.from_numpy(W.rhs(cfg)).to(dev)
@@ -245,7 +245,7 @@ def run_reference(args, rank, world, pg):
     val = dofs * len(timed) / tot
     line = {"metric": METRIC, "value": val, "unit": "DOF/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(timed), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic", "impl": "reference",
             "config": {"workload": cfg.name, "N": cfg.N, "p": cfg.p, "eps": cfg.eps, "sample": desc},
             "cpu_baseline": {"value": val, "unit": "DOF/s", "cores": 1, "kind": "oracle", "sample": desc},
             "e2e": {"value": val, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -315,7 +315,7 @@ def run_native(args, rank, world, local, pg):
     import paper_2311_01451_b200 as R
     ax = torch.empty_like(x)
     xt = x[pb["P"]].contiguous()
-    R.sample_matvec(cfg.kernel, pb["pts"], W.kernel_weight(cfg), xt.view(N, 1), ax.view(N, 1))
+    R.sample_matvec(cfg.kernel, pb["pts"], W.kernel_weight(cfg), xt.view(N, 1), ax.view(N, 1), kappa=cfg.kappa)
     resid = float((ax - pb["b"][pb["P"]]).norm() / pb["b"].norm())
     # ---- e2e: host (pinned) inputs, H2D + factor + solve + D2H inside the timed region
     e2e = None
@@ -376,7 +376,7 @@ def run_native(args, rank, world, local, pg):
     sweep_tf = st["flops_model"] / (st["factor_ms"] * 1e-3) / 1e12
     line = {"metric": METRIC, "value": world * N * args.steps / (ms * 1e-3), "unit": "DOF/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
             "config": {"workload": cfg.name, "N": N, "p": cfg.p, "eps": cfg.eps, "g": cfg.g, "leaf": cfg.leaf,
                        "kernel": cfg.kernel, "L": st["L"], "l2": "inputs 6.4 GB > 126 MB L2 (no flush needed)",
                        "step": "restore samples + rsrs_factor + rsrs_solve(1 rhs)", "parallelism": f"replicas{world}"},

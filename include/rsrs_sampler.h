@@ -25,6 +25,14 @@ extern "C" {
 
 int rsrs_sample_matvec(int kind, const double* pts, int64_t N, double weight, const void* X, int64_t ldx,
                        void* Y, int64_t ldy, int64_t ncol, int adjoint, void* stream);
+
+/* Complex 2D Helmholtz operator (config c4):
+ *     A_ij = delta_ij + weight * (i/4) H0^(1)(kappa |x_i - x_j|)   (i != j), A_ii = 1
+ * (complex symmetric: A^* = conj(A)).  X, Y are DEVICE complex128 arrays
+ * (interleaved {re, im} doubles), N x ldx / N x ldy complex elements, ncol
+ * columns used; adjoint 1 computes A^* X.  Same return codes. */
+int rsrs_sample_matvec_c128(const double* pts, int64_t N, double weight, double kappa, const void* X,
+                            int64_t ldx, void* Y, int64_t ldy, int64_t ncol, int adjoint, void* stream);
 const char* rsrs_sampler_last_error(void);
 
 #ifdef __cplusplus

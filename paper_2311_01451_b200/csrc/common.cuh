@@ -29,6 +29,44 @@ RSRS_DI void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// Scalar arithmetic shared by the real (double) and complex128 (double2 =
+// {re, im}) instantiations of the per-box kernels.
+RSRS_DI double s_zero(double) { return 0.0; }
+RSRS_DI double2 s_zero(double2) { return make_double2(0.0, 0.0); }
+RSRS_DI double s_one(double) { return 1.0; }
+RSRS_DI double2 s_one(double2) { return make_double2(1.0, 0.0); }
+RSRS_DI double s_add(double a, double b) { return a + b; }
+RSRS_DI double2 s_add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+RSRS_DI double s_sub(double a, double b) { return a - b; }
+RSRS_DI double2 s_sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+RSRS_DI double s_neg(double a) { return -a; }
+RSRS_DI double2 s_neg(double2 a) { return make_double2(-a.x, -a.y); }
+RSRS_DI double s_mul(double a, double b) { return a * b; }
+RSRS_DI double2 s_mul(double2 a, double2 b) { return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+RSRS_DI double s_conj(double a) { return a; }
+RSRS_DI double2 s_conj(double2 a) { return make_double2(a.x, -a.y); }
+// a * conj(b)
+RSRS_DI double s_mulc(double a, double b) { return a * b; }
+RSRS_DI double2 s_mulc(double2 a, double2 b) { return make_double2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y); }
+RSRS_DI double s_scale(double a, double t) { return a * t; }
+RSRS_DI double2 s_scale(double2 a, double t) { return make_double2(a.x * t, a.y * t); }
+RSRS_DI double s_real(double a) { return a; }
+RSRS_DI double s_real(double2 a) { return a.x; }
+RSRS_DI double s_abs(double a) { return fabs(a); }
+RSRS_DI double s_abs(double2 a) { return hypot(a.x, a.y); }
+RSRS_DI double s_div(double a, double b) { return a / b; }
+RSRS_DI double2 s_div(double2 a, double2 b) {
+  // Smith's algorithm
+  if (fabs(b.x) >= fabs(b.y)) {
+    const double r = b.y / b.x, den = b.x + b.y * r;
+    return make_double2((a.x + a.y * r) / den, (a.y - a.x * r) / den);
+  }
+  const double r = b.x / b.y, den = b.x * r + b.y;
+  return make_double2((a.x * r + a.y) / den, (a.y * r - a.x) / den);
+}
+template <bool C> struct ScalarOf { typedef double T; };
+template <> struct ScalarOf<true> { typedef double2 T; };
+
 // Per-box record of one (level, colour) batch.  Static fields are written by
 // the host planner; r, self_pos (near-list build) and k, nr, nc, status (ID)
 // by the device.

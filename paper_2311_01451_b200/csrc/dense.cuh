@@ -5,228 +5,21 @@
 namespace rsrs {
 
 // ---------------------------------------------------------------------------
-// Augmented Cholesky.  A is (r + mextra) x r row-major: rows 0..r-1 hold the
-// lower triangle of the SPD near-field Gram C = M M^T, rows r.. hold
-// B = Y_b M^T.  On exit rows 0..r-1 hold L (C = L L^T) and rows r.. hold
-// u = B L^-T.  This is the CholeskyQR form of the thin QR of M^T = Q R
-// (R = L^T), used for the nullspace projection and for the
-// right pseudo-inverse M^dagger = M^T C^-1.
-// Right-looking, panel width NB kept in shared memory, trailing update on DMMA.
-// ---------------------------------------------------------------------------
-template <int NB>
-__global__ void __launch_bounds__(256) chol_aug_kernel(const CholDesc* __restrict__ descs) {
-  extern __shared__ __align__(16) double P[];
-  constexpr int PS = NB + 4;
-  __shared__ int bad;
-  const CholDesc d = descs[blockIdx.x];
-  if (d.status && *d.status != ST_OK) return;
-  const int r = *d.pr, me = d.mextra, m = r + me, uoff = d.uoff;
-  double* A = d.A;
-  const i64 lda = d.lda;
-  // logical row i (C rows [0, r), then the extra rows) -> physical row
-  auto prow = [&](int i) -> double* { return A + (i64)(i < r ? i : uoff + (i - r)) * lda; };
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int gid = lane >> 2, tig = lane & 3;
-  if (tid == 0) bad = 0;
-  __syncthreads();
-  for (int j0 = 0; j0 < r; j0 += NB) {
-    const int jb = min(NB, r - j0);
-    const int mp = m - j0;
-    // 1. stage the panel A[j0:m, j0:j0+NB] (zero beyond jb)
-    for (int idx = tid; idx < mp * NB; idx += 256) {
-      const int i = idx / NB, c = idx % NB;
-      P[i * PS + c] = (c < jb) ? prow(j0 + i)[j0 + c] : 0.0;
-    }
-    __syncthreads();
-    // 2. diagonal block (jb <= 32) by warp 0
-    if (warp == 0) {
-      for (int c = 0; c < jb; ++c) {
-        const double dcc = P[c * PS + c];
-        if (!(dcc > 0.0)) {
-          if (lane == 0) bad = 1;
-          break;
-        }
-        const double lcc = sqrt(dcc);
-        __syncwarp();
-        if (lane == c) P[c * PS + c] = lcc;
-        if (lane > c && lane < jb) P[lane * PS + c] /= lcc;
-        __syncwarp();
-        if (lane > c && lane < jb) {
-          const double lic = P[lane * PS + c];
-          for (int j = c + 1; j <= lane; ++j) P[lane * PS + j] -= lic * P[j * PS + c];
-        }
-        __syncwarp();
-      }
-    }
-    __syncthreads();
-    if (bad) {
-      if (tid == 0 && d.status) *d.status = ST_SINGULAR_GRAM;
-      return;
-    }
-    // 3. panel rows below the diagonal block: x L11^T = a
-    for (int i = jb + tid; i < mp; i += 256) {
-      double x[NB];
-#pragma unroll
-      for (int c = 0; c < NB; ++c) x[c] = P[i * PS + c];
-#pragma unroll
-      for (int c = 0; c < NB; ++c) {
-        if (c < jb) {
-          double s = x[c];
-#pragma unroll
-          for (int q = 0; q < c; ++q) s -= x[q] * P[c * PS + q];
-          x[c] = s / P[c * PS + c];
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < NB; ++c) P[i * PS + c] = x[c];
-    }
-    __syncthreads();
-    // 4. write the finished column block back
-    for (int idx = tid; idx < mp * jb; idx += 256) {
-      const int i = idx / jb, c = idx % jb;
-      if (i >= c) prow(j0 + i)[j0 + c] = P[i * PS + c];
-    }
-    // 5. trailing update A[t0:m, t0:r] -= P P^T (lower part of C; all extra rows)
-    const int t0 = j0 + jb;
-    const int nrow = m - t0, ncol = r - t0;
-    if (ncol > 0) {
-      const int nti = (nrow + 31) / 32, ntj = (ncol + 31) / 32;
-      const int nkk = (jb + 3) / 4;
-      for (int u0 = warp; u0 < nti * ntj; u0 += 8) {
-        const int ti = u0 / ntj, tj = u0 % ntj;
-        const int rs = t0 + 32 * ti;
-        if (rs + 32 <= r && tj > ti) continue;   // strictly upper tile of C
-        const int cs = t0 + 32 * tj;
-        double acc[4][4][2];
-        double* rp[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int gi = rs + t * 8 + gid;
-          rp[t] = gi < m ? prow(gi) : nullptr;
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int gj = cs + u * 8 + 2 * tig;
-            acc[t][u][0] = (rp[t] && gj < r) ? rp[t][gj] : 0.0;
-            acc[t][u][1] = (rp[t] && gj + 1 < r) ? rp[t][gj + 1] : 0.0;
-          }
-        }
-        for (int kk = 0; kk < nkk; ++kk) {
-          double a[4], b[4];
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int gi = rs + t * 8 + gid;
-            a[t] = gi < m ? -P[(gi - j0) * PS + kk * 4 + tig] : 0.0;
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int gj = cs + u * 8 + gid;
-            b[u] = gj < r ? P[(gj - j0) * PS + kk * 4 + tig] : 0.0;
-          }
-#pragma unroll
-          for (int t = 0; t < 4; ++t)
-#pragma unroll
-            for (int u = 0; u < 4; ++u) dmma884(acc[t][u][0], acc[t][u][1], a[t], b[u]);
-        }
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          if (!rp[t]) continue;
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int gj = cs + u * 8 + 2 * tig;
-            if (gj < r) rp[t][gj] = acc[t][u][0];
-            if (gj + 1 < r) rp[t][gj + 1] = acc[t][u][1];
-          }
-        }
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// ---------------------------------------------------------------------------
-// W = u L^-1 (solve W L = u) in place over the extra rows of the augmented
-// matrix: W = B C^-1 = Y_b M^T (M M^T)^-1 = Y_b M^dagger.
-// Column blocks of 32, descending; the block GEMM runs on DMMA.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) trsm_back_kernel(const CholDesc* __restrict__ descs) {
-  __shared__ double Ljj[32][33];
-  __shared__ double V[64][33];
-  const CholDesc d = descs[blockIdx.x];
-  if (d.status && *d.status != ST_OK) return;
-  const int r = *d.pr, me = d.mextra;
-  if (me <= 0 || r <= 0) return;
-  const double* L = d.A;
-  double* U = d.A + (i64)d.uoff * d.lda;
-  const i64 lda = d.lda;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int gid = lane >> 2, tig = lane & 3;
-  const int nblk = (r + 31) / 32;
-  for (int jbk = nblk - 1; jbk >= 0; --jbk) {
-    const int j0 = jbk * 32;
-    const int nc = min(32, r - j0);
-    for (int idx = tid; idx < 32 * 32; idx += 256) {
-      const int i = idx / 32, j = idx % 32;
-      Ljj[i][j] = (i < nc && j < nc) ? L[(i64)(j0 + i) * lda + j0 + j] : 0.0;
-    }
-    for (int rg = 0; rg < me; rg += 64) {
-      // V = u[rg:rg+64, J] - W[rg:rg+64, j0+32:r] L[j0+32:r, J]
-      const int row = rg + warp * 8 + gid;
-      double acc[4][2];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int gj = j0 + u * 8 + 2 * tig;
-        acc[u][0] = (row < me && gj < r) ? U[(i64)row * lda + gj] : 0.0;
-        acc[u][1] = (row < me && gj + 1 < r) ? U[(i64)row * lda + gj + 1] : 0.0;
-      }
-      for (int kq = j0 + 32; kq < r; kq += 4) {
-        const int kk = kq + tig;
-        const double a = (row < me && kk < r) ? -U[(i64)row * lda + kk] : 0.0;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int gj = j0 + u * 8 + gid;
-          const double b = (kk < r && gj < r) ? L[(i64)kk * lda + gj] : 0.0;
-          dmma884(acc[u][0], acc[u][1], a, b);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        V[warp * 8 + gid][u * 8 + 2 * tig] = acc[u][0];
-        V[warp * 8 + gid][u * 8 + 2 * tig + 1] = acc[u][1];
-      }
-      __syncthreads();
-      // x L_JJ = v (back substitution over the block's columns)
-      if (tid < 64 && rg + tid < me) {
-        double x[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) x[j] = V[tid][j];
-#pragma unroll
-        for (int j = 31; j >= 0; --j) {
-          if (j < nc) {
-            double s = x[j];
-#pragma unroll
-            for (int q = j + 1; q < 32; ++q)
-              if (q < nc) s -= x[q] * Ljj[q][j];
-            x[j] = s / Ljj[j][j];
-          }
-        }
-        for (int j = 0; j < nc; ++j) U[(i64)(rg + tid) * lda + j0 + j] = x[j];
-      }
-      __syncthreads();
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Interpolative decomposition of S = [Y'', Z''] / sqrt(2w)
-// through its Gram H = S S^T: greedy max-residual-norm pivoting (the pivots and
+// through its Gram H = S S^* (Hermitian for complex128): greedy max-residual-norm pivoting (the pivots and
 // R of column-pivoted QR of S^T), stop at R_jj <= atol(l), T = (R11^-1 R12)^T.
 // Also writes the skeleton / redundant / coupled index lists of the box.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) id_kernel(BoxDev* __restrict__ boxes, const double* __restrict__ ws,
-                                                 int* __restrict__ iws, double* __restrict__ fpool,
+template <bool C>
+__global__ void __launch_bounds__(256) id_kernel(BoxDev* __restrict__ boxes, const double* __restrict__ wsd,
+                                                 int* __restrict__ iws, double* __restrict__ fpoold,
                                                  int* __restrict__ ipool, const int* __restrict__ gidx,
                                                  double atol2, int p, int oversample) {
-  extern __shared__ __align__(16) double Hs[];
+  typedef typename ScalarOf<C>::T S;
+  extern __shared__ __align__(16) double Hsd[];
+  S* Hs = reinterpret_cast<S*>(Hsd);
+  const S* ws = reinterpret_cast<const S*>(wsd);
+  S* fpool = reinterpret_cast<S*>(fpoold);
   BoxDev& b = boxes[blockIdx.x];
   const int nb = b.nb, r = b.r;
   if (b.status != ST_OK) {                 // e.g. too few samples for this near field
@@ -247,9 +40,14 @@ __global__ void __launch_bounds__(256) id_kernel(BoxDev* __restrict__ boxes, con
   __shared__ double pval;
   __shared__ int pidx, kfinal;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const double* H = ws + b.off_h;
-  const int ldhg = (nb + 1) & ~1;
-  for (int idx = tid; idx < nb * nb; idx += 256) Hs[(idx / nb) * ldh + idx % nb] = H[(idx / nb) * ldhg + idx % nb];
+  const S* H = ws + b.off_h;
+  const int ldhg = b.ldn;
+  // H = H_Y + H_Z = Y'' Y''^* + Z'' Z''^* (the two halves of S S^*, written by gemm_nt)
+  const S* H2 = H + (i64)nb * ldhg;
+  for (int idx = tid; idx < nb * nb; idx += 256) {
+    const i64 g = (i64)(idx / nb) * ldhg + idx % nb;
+    Hs[(idx / nb) * ldh + idx % nb] = s_add(H[g], H2[g]);
+  }
   for (int i = tid; i < nb; i += 256) perm[i] = i;
   if (tid == 0) kfinal = nb;
   __syncthreads();
@@ -258,7 +56,7 @@ __global__ void __launch_bounds__(256) id_kernel(BoxDev* __restrict__ boxes, con
       double bv = -1.0;
       int bi = nb;
       for (int i = j + lane; i < nb; i += 32) {
-        const double v = Hs[i * ldh + i];
+        const double v = s_real(Hs[i * ldh + i]);
         if (v > bv || (v == bv && i < bi)) {
           bv = v;
           bi = i;
@@ -286,13 +84,13 @@ __global__ void __launch_bounds__(256) id_kernel(BoxDev* __restrict__ boxes, con
     const int q = pidx;
     if (q != j) {
       for (int c = tid; c < nb; c += 256) {
-        const double t = Hs[j * ldh + c];
+        const S t = Hs[j * ldh + c];
         Hs[j * ldh + c] = Hs[q * ldh + c];
         Hs[q * ldh + c] = t;
       }
       __syncthreads();
       for (int c = tid; c < nb; c += 256) {
-        const double t = Hs[c * ldh + j];
+        const S t = Hs[c * ldh + j];
         Hs[c * ldh + j] = Hs[c * ldh + q];
         Hs[c * ldh + q] = t;
       }
@@ -303,15 +101,16 @@ __global__ void __launch_bounds__(256) id_kernel(BoxDev* __restrict__ boxes, con
       }
       __syncthreads();
     }
-    const double rjj = sqrt(Hs[j * ldh + j]);
+    const double rjj = sqrt(s_real(Hs[j * ldh + j]));
     __syncthreads();
-    for (int c = j + 1 + tid; c < nb; c += 256) Hs[j * ldh + c] /= rjj;
-    if (tid == 0) Hs[j * ldh + j] = rjj;
+    for (int c = j + 1 + tid; c < nb; c += 256) Hs[j * ldh + c] = s_scale(Hs[j * ldh + c], 1.0 / rjj);
+    if (tid == 0) Hs[j * ldh + j] = s_scale(s_one(S()), rjj);
     __syncthreads();
+    // Schur complement H_il -= conj(R_ji) R_jl  (H = R^* R)
     const int nt = nb - j - 1;
     for (int idx = tid; idx < nt * nt; idx += 256) {
       const int i = j + 1 + idx / nt, l = j + 1 + idx % nt;
-      Hs[i * ldh + l] -= Hs[j * ldh + i] * Hs[j * ldh + l];
+      Hs[i * ldh + l] = s_sub(Hs[i * ldh + l], s_mul(s_conj(Hs[j * ldh + i]), Hs[j * ldh + l]));
     }
     __syncthreads();
   }
@@ -343,20 +142,20 @@ __global__ void __launch_bounds__(256) id_kernel(BoxDev* __restrict__ boxes, con
       red_tp[rank_of[s]] = gidx[row];
     }
   }
-  // T = (R11^-1 R12)^T, rows = redundant (sorted), cols = skeleton (sorted)
+  // T = (R11^-1 R12)^*, rows = redundant (sorted), cols = skeleton (sorted)
   if (nr > 0 && k > 0) {
-    double* T = fpool + b.f_T;
-    const int ldn = (nb + 1) & ~1;
+    S* T = fpool + b.f_T;
+    const int ldn = b.ldn;
     for (int c = tid; c < nr; c += 256) {
       // back substitution R11 x = R12[:, c]  (x kept in the R12 column of Hs)
       const int col = k + c;
       for (int s = k - 1; s >= 0; --s) {
-        double v = Hs[s * ldh + col];
-        for (int q2 = s + 1; q2 < k; ++q2) v -= Hs[s * ldh + q2] * Hs[q2 * ldh + col];
-        Hs[s * ldh + col] = v / Hs[s * ldh + s];
+        S v = Hs[s * ldh + col];
+        for (int q2 = s + 1; q2 < k; ++q2) v = s_sub(v, s_mul(Hs[s * ldh + q2], Hs[q2 * ldh + col]));
+        Hs[s * ldh + col] = s_div(v, Hs[s * ldh + s]);
       }
       const int ri = rank_of[col];
-      for (int s = 0; s < k; ++s) T[(i64)ri * ldn + rank_of[s]] = Hs[s * ldh + col];
+      for (int s = 0; s < k; ++s) T[(i64)ri * ldn + rank_of[s]] = s_conj(Hs[s * ldh + col]);
     }
   }
   // coupled set c = near \ red in near order (ballot compaction by warp 0)
@@ -402,16 +201,22 @@ __global__ void __launch_bounds__(256) id_kernel(BoxDev* __restrict__ boxes, con
 // Then LU(X_rr) with partial pivoting and X_rr^-1; X_rc and X_cr are written
 // densely for the G_U / G_L GEMMs.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ boxes, double* __restrict__ ws,
+template <bool C>
+__global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ boxes, double* __restrict__ wsd,
                                                          const int* __restrict__ iws,
-                                                         double* __restrict__ fpool) {
-  extern __shared__ __align__(16) double Xs[];
+                                                         double* __restrict__ fpoold) {
+  typedef typename ScalarOf<C>::T S;
+  extern __shared__ __align__(16) double Xsd[];
+  S* Xs = reinterpret_cast<S*>(Xsd);
+  S* ws = reinterpret_cast<S*>(wsd);
+  S* fpool = reinterpret_cast<S*>(fpoold);
+  const S zero = s_zero(S());
   BoxDev& b = boxes[blockIdx.x];
   const int nr = b.nr, k = b.k, r = b.r, nb = b.nb, nc = b.nc;
   if (nr <= 0 || b.status != ST_OK) return;
-  const int ldn = (nb + 1) & ~1;
+  const int ldn = b.ldn;
   const int ldx = nr + 1;
-  double* Is = Xs + nr * ldx;
+  S* Is = Xs + nr * ldx;
   int* ipiv = reinterpret_cast<int*>(Is + nr * ldx);
   int* redloc = ipiv + nr;
   int* skelloc = redloc + nb;
@@ -426,37 +231,37 @@ __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ bo
   for (int s = tid; s < k; s += 256) skelloc[s] = skelrow[s] - b.row0;
   if (tid == 0) singular = 0;
   __syncthreads();
-  const double* T = fpool + b.f_T;
+  const S* T = fpool + b.f_T;
   const i64 ldr = b.ldr;
-  const double* WY = ws + b.off_aug + (i64)b.rmax * ldr;
-  const double* WZ = ws + b.off_aug + (i64)(b.rmax + nb) * ldr + (i64)b.rmax * ldr;
-  double* XY = ws + b.off_xy;
-  double* XZ = ws + b.off_xz;
+  const S* WY = ws + b.off_aug + (i64)b.rmax * ldr;
+  const S* WZ = ws + b.off_aug + (i64)(b.rmax + nb) * ldr + (i64)b.rmax * ldr;
+  S* XY = ws + b.off_xy;
+  S* XZ = ws + b.off_xz;
   // 1. row combination X = W_r - T W_s
   for (int idx = tid; idx < nr * r; idx += 256) {
     const int i = idx / r, j = idx % r;
-    double vy = WY[(i64)redloc[i] * ldr + j];
-    double vz = WZ[(i64)redloc[i] * ldr + j];
+    S vy = WY[(i64)redloc[i] * ldr + j];
+    S vz = WZ[(i64)redloc[i] * ldr + j];
     for (int s = 0; s < k; ++s) {
-      const double t = T[(i64)i * ldn + s];
-      vy -= t * WY[(i64)skelloc[s] * ldr + j];
-      vz -= t * WZ[(i64)skelloc[s] * ldr + j];
+      const S t = T[(i64)i * ldn + s];
+      vy = s_sub(vy, s_mul(t, WY[(i64)skelloc[s] * ldr + j]));
+      vz = s_sub(vz, s_mul(t, WZ[(i64)skelloc[s] * ldr + j]));
     }
     XY[(i64)i * ldr + j] = vy;
     XZ[(i64)i * ldr + j] = vz;
   }
   __syncthreads();
-  // 2. column fix X[:, red] -= X[:, skel] T^T  (F_loc^-1 on b's own columns)
+  // 2. column fix X[:, red] -= X[:, skel] T^*  (F_loc^-1 on b's own columns)
   if (k > 0) {
     for (int idx = tid; idx < nr * nr; idx += 256) {
       const int i = idx / nr, jj = idx % nr;
       const int col = b.self_pos + redloc[jj];
-      double vy = XY[(i64)i * ldr + col];
-      double vz = XZ[(i64)i * ldr + col];
+      S vy = XY[(i64)i * ldr + col];
+      S vz = XZ[(i64)i * ldr + col];
       for (int s = 0; s < k; ++s) {
-        const double t = T[(i64)jj * ldn + s];
-        vy -= XY[(i64)i * ldr + b.self_pos + skelloc[s]] * t;
-        vz -= XZ[(i64)i * ldr + b.self_pos + skelloc[s]] * t;
+        const S t = T[(i64)jj * ldn + s];
+        vy = s_sub(vy, s_mulc(XY[(i64)i * ldr + b.self_pos + skelloc[s]], t));
+        vz = s_sub(vz, s_mulc(XZ[(i64)i * ldr + b.self_pos + skelloc[s]], t));
       }
       XY[(i64)i * ldr + col] = vy;
       XZ[(i64)i * ldr + col] = vz;
@@ -464,22 +269,22 @@ __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ bo
     __syncthreads();
   }
   // 3. gather X_rr (shared + factor), X_rc (nr x nc), X_cr (nc x nr)
-  double* Xrr = fpool + b.f_Xrr;
+  S* Xrr = fpool + b.f_Xrr;
   for (int idx = tid; idx < nr * nr; idx += 256) {
     const int i = idx / nr, j = idx % nr;
-    const double v = XY[(i64)i * ldr + b.self_pos + redloc[j]];
+    const S v = XY[(i64)i * ldr + b.self_pos + redloc[j]];
     Xs[i * ldx + j] = v;
     Xrr[(i64)i * ldn + j] = v;
   }
-  double* Xrc = ws + b.off_xrc;
-  double* Xcr = ws + b.off_xcr;
+  S* Xrc = ws + b.off_xrc;
+  S* Xcr = ws + b.off_xcr;
   for (int idx = tid; idx < nr * nc; idx += 256) {
     const int i = idx / nc, j = idx % nc;
     Xrc[(i64)i * ldr + j] = XY[(i64)i * ldr + cpos[j]];
   }
   for (int idx = tid; idx < nr * nc; idx += 256) {
     const int j = idx / nr, i = idx % nr;
-    Xcr[(i64)j * ldn + i] = XZ[(i64)i * ldr + cpos[j]];
+    Xcr[(i64)j * ldn + i] = s_conj(XZ[(i64)i * ldr + cpos[j]]);   // X_cr = (X_Z)^*
   }
   __syncthreads();
   // 4. LU with partial pivoting
@@ -488,7 +293,7 @@ __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ bo
       double bv = -1.0;
       int bi = nr;
       for (int i = c + lane; i < nr; i += 32) {
-        const double v = fabs(Xs[i * ldx + c]);
+        const double v = s_abs(Xs[i * ldx + c]);
         if (v > bv || (v == bv && i < bi)) {
           bv = v;
           bi = i;
@@ -514,19 +319,19 @@ __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ bo
     if (singular) break;
     if (pi != c) {
       for (int j = tid; j < nr; j += 256) {
-        const double t = Xs[c * ldx + j];
+        const S t = Xs[c * ldx + j];
         Xs[c * ldx + j] = Xs[pi * ldx + j];
         Xs[pi * ldx + j] = t;
       }
       __syncthreads();
     }
-    const double piv = Xs[c * ldx + c];
-    for (int i = c + 1 + tid; i < nr; i += 256) Xs[i * ldx + c] /= piv;
+    const S piv = Xs[c * ldx + c];
+    for (int i = c + 1 + tid; i < nr; i += 256) Xs[i * ldx + c] = s_div(Xs[i * ldx + c], piv);
     __syncthreads();
     const int nt = nr - c - 1;
     for (int idx = tid; idx < nt * nt; idx += 256) {
       const int i = c + 1 + idx / nt, j = c + 1 + idx % nt;
-      Xs[i * ldx + j] -= Xs[i * ldx + c] * Xs[c * ldx + j];
+      Xs[i * ldx + j] = s_sub(Xs[i * ldx + j], s_mul(Xs[i * ldx + c], Xs[c * ldx + j]));
     }
     __syncthreads();
   }
@@ -536,28 +341,28 @@ __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ bo
   }
   // 5. X_rr^-1 = U^-1 L^-1 P, column by column
   for (int j = tid; j < nr; j += 256) {
-    for (int i = 0; i < nr; ++i) Is[i * ldx + j] = (i == j) ? 1.0 : 0.0;
+    for (int i = 0; i < nr; ++i) Is[i * ldx + j] = (i == j) ? s_one(S()) : zero;
     for (int c = 0; c < nr; ++c) {
       const int q = ipiv[c];
       if (q != c) {
-        const double t = Is[c * ldx + j];
+        const S t = Is[c * ldx + j];
         Is[c * ldx + j] = Is[q * ldx + j];
         Is[q * ldx + j] = t;
       }
     }
     for (int i = 0; i < nr; ++i) {
-      double s = Is[i * ldx + j];
-      for (int q = 0; q < i; ++q) s -= Xs[i * ldx + q] * Is[q * ldx + j];
+      S s = Is[i * ldx + j];
+      for (int q = 0; q < i; ++q) s = s_sub(s, s_mul(Xs[i * ldx + q], Is[q * ldx + j]));
       Is[i * ldx + j] = s;
     }
     for (int i = nr - 1; i >= 0; --i) {
-      double s = Is[i * ldx + j];
-      for (int q = i + 1; q < nr; ++q) s -= Xs[i * ldx + q] * Is[q * ldx + j];
-      Is[i * ldx + j] = s / Xs[i * ldx + i];
+      S s = Is[i * ldx + j];
+      for (int q = i + 1; q < nr; ++q) s = s_sub(s, s_mul(Xs[i * ldx + q], Is[q * ldx + j]));
+      Is[i * ldx + j] = s_div(s, Xs[i * ldx + i]);
     }
   }
   __syncthreads();
-  double* Xinv = fpool + b.f_Xinv;
+  S* Xinv = fpool + b.f_Xinv;
   for (int idx = tid; idx < nr * nr; idx += 256) {
     const int i = idx / nr, j = idx % nr;
     Xinv[(i64)i * ldn + j] = Is[i * ldx + j];
@@ -636,8 +441,11 @@ __global__ void compact_kernel(const BoxDev* __restrict__ boxes, const int* __re
 // ---------------------------------------------------------------------------
 // Top block: LU with partial pivoting of A~_SS (single CTA, in global memory).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) top_lu_kernel(double* __restrict__ A, i64 lda, int n,
+template <bool C>
+__global__ void __launch_bounds__(1024) top_lu_kernel(double* __restrict__ Ad, i64 lda, int n,
                                                        int* __restrict__ ipiv, int* __restrict__ status) {
+  typedef typename ScalarOf<C>::T S;
+  S* A = reinterpret_cast<S*>(Ad);
   __shared__ double rv[32];
   __shared__ int ri[32];
   __shared__ int pidx;
@@ -647,7 +455,7 @@ __global__ void __launch_bounds__(1024) top_lu_kernel(double* __restrict__ A, i6
     double bv = -1.0;
     int bi = n;
     for (int i = c + tid; i < n; i += 1024) {
-      const double v = fabs(A[(i64)i * lda + c]);
+      const double v = s_abs(A[(i64)i * lda + c]);
       if (v > bv || (v == bv && i < bi)) {
         bv = v;
         bi = i;
@@ -693,19 +501,19 @@ __global__ void __launch_bounds__(1024) top_lu_kernel(double* __restrict__ A, i6
     const int q = pidx;
     if (q != c) {
       for (int j = tid; j < n; j += 1024) {
-        const double t = A[(i64)c * lda + j];
+        const S t = A[(i64)c * lda + j];
         A[(i64)c * lda + j] = A[(i64)q * lda + j];
         A[(i64)q * lda + j] = t;
       }
       __syncthreads();
     }
-    const double piv = A[(i64)c * lda + c];
-    for (int i = c + 1 + tid; i < n; i += 1024) A[(i64)i * lda + c] /= piv;
+    const S piv = A[(i64)c * lda + c];
+    for (int i = c + 1 + tid; i < n; i += 1024) A[(i64)i * lda + c] = s_div(A[(i64)i * lda + c], piv);
     __syncthreads();
     const int nt = n - c - 1;
     for (int idx = tid; idx < nt * nt; idx += 1024) {
       const int i = c + 1 + idx / nt, j = c + 1 + idx % nt;
-      A[(i64)i * lda + j] -= A[(i64)i * lda + c] * A[(i64)c * lda + j];
+      A[(i64)i * lda + j] = s_sub(A[(i64)i * lda + j], s_mul(A[(i64)i * lda + c], A[(i64)c * lda + j]));
     }
     __syncthreads();
   }

@@ -5,17 +5,19 @@
 // one launch of each per-box kernel (boxes of one colour are >= 3 apart, so
 // their near sets are disjoint and the batch equals the sequential order,
 // DESIGN.md R10).  Per colour batch:
-//   gemm_nt      [Omega_near; Y_b] Omega_near^T, [Psi_near; Z_b] Psi_near^T
-//   chol_aug     L L^T = Gram, u = B L^-T
-//   trsm_back    W = u L^-1 = Y_b Omega_near^dagger
+//   gemm_nt      [Omega_near; Y_b] Omega_near^*, [Psi_near; Z_b] Psi_near^*
+//   chol_*       blocked Cholesky L L^* = Gram, u = B L^-*            (chol.cuh)
+//   chol_back_*  W = u L^-1 = Y_b Omega_near^dagger                  (chol.cuh)
 //   gemm_nn      Y'' = Y_b - W Omega_near (= Y_b null(Omega_near) null^T)
-//   gemm_nt      H = [Y'' Z''][Y'' Z'']^T / (2w)
+//   gemm_nt      H = Y'' Y''^* + Z'' Z''^*  (two halves, summed by id_kernel)
 //   id_kernel    skeletons, T
 //   gemm_nn      E/F sample updates
 //   extract_lu   X_{r,near}, X_{near,r}, LU(X_rr), X_rr^-1
 //   gemm_nn      G_U = X_rr^-1 X_rc, G_L = X_cr X_rr^-1
 //   gemm_nn      L/U sample updates
 // then compaction of the skeleton rows into the next level's store.
+// Real (RSRS_F64) and complex128 (RSRS_C128) share this driver: every offset
+// below is in SCALAR units and the kernels are instantiated for both types.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -71,6 +73,23 @@ void set_smem(K kern, int want) {
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, want < 0 ? mx : std::min(want, mx)));
 }
 
+template <bool C>
+void set_smem_both() {
+  set_smem(rsrs::chol_update_kernel<C>, rsrs::NT_SMEM);
+  set_smem(rsrs::chol_trsm_kernel<C>, rsrs::NT_SMEM);
+  set_smem(rsrs::chol_back_a_kernel<C>, rsrs::NN_SMEM);
+  set_smem(rsrs::chol_back_b_kernel<C>, rsrs::NN_SMEM);
+  set_smem(rsrs::chol_diag_kernel<C>, rsrs::CHOL_DIAG_SMEM);
+  set_smem(rsrs::id_kernel<C>, -1);
+  set_smem(rsrs::extract_lu_kernel<C>, -1);
+  set_smem(rsrs::solve_fwd_kernel<C>, -1);
+  set_smem(rsrs::solve_bwd_kernel<C>, -1);
+  set_smem(rsrs::apply_fwd_kernel<C>, -1);
+  set_smem(rsrs::apply_bwd_kernel<C>, -1);
+  set_smem(rsrs::top_solve_kernel<C>, -1);
+  set_smem(rsrs::top_apply_kernel<C>, -1);
+}
+
 void init_kernels() {
   static bool done = false;
   if (done) return;
@@ -81,22 +100,10 @@ void init_kernels() {
   CK(cudaDeviceGetAttribute(&g_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   set_smem(rsrs::gemm_nt_kernel, rsrs::NT_SMEM);
   set_smem(rsrs::gemm_nn_kernel, rsrs::NN_SMEM);
-  set_smem(rsrs::chol_aug_kernel<32>, -1);
-  set_smem(rsrs::chol_aug_kernel<16>, -1);
-  set_smem(rsrs::chol_aug_kernel<8>, -1);
-  set_smem(rsrs::chol_update_kernel, rsrs::NT_SMEM);
-  set_smem(rsrs::chol_trsm_kernel, rsrs::NT_SMEM);
-  set_smem(rsrs::chol_back_a_kernel, rsrs::NN_SMEM);
-  set_smem(rsrs::chol_back_b_kernel, rsrs::NN_SMEM);
-  set_smem(rsrs::chol_diag_kernel, rsrs::CHOL_DIAG_SMEM);
-  set_smem(rsrs::id_kernel, -1);
-  set_smem(rsrs::extract_lu_kernel, -1);
-  set_smem(rsrs::solve_fwd_kernel, -1);
-  set_smem(rsrs::solve_bwd_kernel, -1);
-  set_smem(rsrs::apply_fwd_kernel, -1);
-  set_smem(rsrs::apply_bwd_kernel, -1);
-  set_smem(rsrs::top_solve_kernel, -1);
-  set_smem(rsrs::top_apply_kernel, -1);
+  set_smem(rsrs::gemm_nt_kernel_c, rsrs::NT_SMEM);
+  set_smem(rsrs::gemm_nn_kernel_c, rsrs::NN_SMEM);
+  set_smem_both<false>();
+  set_smem_both<true>();
   // keep freed stream-ordered memory in the pool (repeated factorizations reuse it)
   cudaMemPool_t pool;
   CK(cudaDeviceGetDefaultMemPool(&pool, dev));
@@ -149,72 +156,72 @@ void post(const char* name, cudaStream_t s, int64_t& launches) {
   }
 }
 
-int chol_nb(int m) {
-  if ((size_t)m * 36 * 8 <= (size_t)SMEM_MAX - 1024) return 32;
-  if ((size_t)m * 20 * 8 <= (size_t)SMEM_MAX - 1024) return 16;
-  if ((size_t)m * 12 * 8 <= (size_t)SMEM_MAX - 1024) return 8;
-  return 0;
-}
-
-void launch_chol(const CholDesc* d, int n, int mmax, cudaStream_t s, int64_t& launches) {
-  const int nb = chol_nb(mmax);
-  if (nb == 0) throw StatusError{RSRS_ERR_INVALID, "near field too large for the Cholesky panel (r + n_b = " +
-                                                       std::to_string(mmax) + ")"};
-  const size_t sm = (size_t)mmax * (nb + 4) * 8;
-  if (nb == 32) rsrs::chol_aug_kernel<32><<<n, 256, sm, s>>>(d);
-  else if (nb == 16) rsrs::chol_aug_kernel<16><<<n, 256, sm, s>>>(d);
-  else rsrs::chol_aug_kernel<8><<<n, 256, sm, s>>>(d);
-  post("chol_aug", s, launches);
-}
-
-// blocked Cholesky + u = B L^-T of nmat matrices (panel width 64), see chol.cuh
+// blocked Cholesky + u = B L^-* of nmat matrices (panel width cbw<C>), see chol.cuh
+template <bool C>
 void launch_chol_blocked(const CholDesc* d, int nmat, int rmax, int mext, cudaStream_t s, int64_t& launches) {
-  const int CB = rsrs::CB;
+  const int CB = rsrs::cbw<C>();
+  const int TN = rsrs::tile_n<C>();
   const int np = (rmax + CB - 1) / CB;
   const int gext = (mext + 63) / 64;
+  const int gx = (CB + TN - 1) / TN;
   for (int q = 0; q < np; ++q) {
     const int j0 = q * CB;
     if (j0 > 0) {
-      dim3 g(1, std::max((rmax - j0 + 63) / 64, gext), 2 * nmat);
-      rsrs::chol_update_kernel<<<g, 128, rsrs::NT_SMEM, s>>>(d, j0);
+      dim3 g(gx, std::max((rmax - j0 + 63) / 64, gext), 2 * nmat);
+      rsrs::chol_update_kernel<C><<<g, 128, rsrs::NT_SMEM, s>>>(d, j0);
       post("chol_update", s, launches);
     }
-    rsrs::chol_diag_kernel<<<nmat, 256, rsrs::CHOL_DIAG_SMEM, s>>>(d, j0);
+    rsrs::chol_diag_kernel<C><<<nmat, 256, rsrs::CHOL_DIAG_SMEM, s>>>(d, j0);
     post("chol_diag", s, launches);
-    dim3 g(1, std::max((rmax - j0 - CB + 63) / 64, gext), 2 * nmat);
-    rsrs::chol_trsm_kernel<<<g, 128, rsrs::NT_SMEM, s>>>(d, j0);
+    dim3 g(gx, std::max((rmax - j0 - CB + 63) / 64, gext), 2 * nmat);
+    rsrs::chol_trsm_kernel<C><<<g, 128, rsrs::NT_SMEM, s>>>(d, j0);
     post("chol_trsm", s, launches);
   }
 }
 
-// W = u L^-1 (back substitution by 64-column blocks, descending)
+// W = u L^-1 (back substitution by panel-width column blocks, descending)
+template <bool C>
 void launch_back_blocked(const CholDesc* d, int nmat, int rmax, int mext, cudaStream_t s, int64_t& launches) {
-  const int CB = rsrs::CB;
+  const int CB = rsrs::cbw<C>();
+  const int TN = rsrs::tile_n<C>();
   const int np = (rmax + CB - 1) / CB;
-  dim3 g(1, (mext + 63) / 64, nmat);
+  dim3 g((CB + TN - 1) / TN, (mext + 63) / 64, nmat);
   for (int q = np - 1; q >= 0; --q) {
     const int j0 = q * CB;
     if (j0 + CB < rmax) {
-      rsrs::chol_back_a_kernel<<<g, 128, rsrs::NN_SMEM, s>>>(d, j0);
+      rsrs::chol_back_a_kernel<C><<<g, 128, rsrs::NN_SMEM, s>>>(d, j0);
       post("chol_back_a", s, launches);
     }
-    rsrs::chol_back_b_kernel<<<g, 128, rsrs::NN_SMEM, s>>>(d, j0);
+    rsrs::chol_back_b_kernel<C><<<g, 128, rsrs::NN_SMEM, s>>>(d, j0);
     post("chol_back_b", s, launches);
   }
 }
 
-void launch_nt(const NTDesc* d, int n, int mmax, int nmax, cudaStream_t s, int64_t& launches) {
+void launch_nt(bool cplx, const NTDesc* d, int n, int mmax, int nmax, cudaStream_t s, int64_t& launches) {
   if (n <= 0 || mmax <= 0 || nmax <= 0) return;
-  dim3 grid((nmax + 63) / 64, (mmax + 63) / 64, n);
-  rsrs::gemm_nt_kernel<<<grid, 128, rsrs::NT_SMEM, s>>>(d);
+  const int TN = cplx ? rsrs::GTC : rsrs::GT;
+  dim3 grid((nmax + TN - 1) / TN, (mmax + 63) / 64, n);
+  if (cplx) rsrs::gemm_nt_kernel_c<<<grid, 128, rsrs::NT_SMEM, s>>>(d);
+  else rsrs::gemm_nt_kernel<<<grid, 128, rsrs::NT_SMEM, s>>>(d);
   post("gemm_nt", s, launches);
 }
 
-void launch_nn(const NNDesc* d, int n, int mmax, int nmax, cudaStream_t s, int64_t& launches) {
+void launch_nn(bool cplx, const NNDesc* d, int n, int mmax, int nmax, cudaStream_t s, int64_t& launches) {
   if (n <= 0 || mmax <= 0 || nmax <= 0) return;
-  dim3 grid((nmax + 63) / 64, (mmax + 63) / 64, n);
-  rsrs::gemm_nn_kernel<<<grid, 128, rsrs::NN_SMEM, s>>>(d);
+  const int TN = cplx ? rsrs::GTC : rsrs::GT;
+  dim3 grid((nmax + TN - 1) / TN, (mmax + 63) / 64, n);
+  if (cplx) rsrs::gemm_nn_kernel_c<<<grid, 128, rsrs::NN_SMEM, s>>>(d);
+  else rsrs::gemm_nn_kernel<<<grid, 128, rsrs::NN_SMEM, s>>>(d);
   post("gemm_nn", s, launches);
+}
+
+void launch_chol_any(bool cplx, const CholDesc* d, int nmat, int rmax, int mext, cudaStream_t s, int64_t& l) {
+  if (cplx) launch_chol_blocked<true>(d, nmat, rmax, mext, s, l);
+  else launch_chol_blocked<false>(d, nmat, rmax, mext, s, l);
+}
+void launch_back_any(bool cplx, const CholDesc* d, int nmat, int rmax, int mext, cudaStream_t s, int64_t& l) {
+  if (cplx) launch_back_blocked<true>(d, nmat, rmax, mext, s, l);
+  else launch_back_blocked<false>(d, nmat, rmax, mext, s, l);
 }
 
 }  // namespace
@@ -231,6 +238,8 @@ struct Batch {
 
 struct rsrs_factor_s {
   rsrs_dtype dt = RSRS_F64;
+  bool cplx = false;                              // RSRS_C128
+  int sc = 1;                                     // doubles per scalar
   int64_t N = 0, p = 0;
   int L = 0, top_level = 2, d = 2;
   std::vector<Batch> batches;
@@ -281,6 +290,8 @@ struct Planner {
   int64_t launches = 0;
   double flops = 0, bytes = 0;
   bool profile = false;
+  bool cplx = false;
+  int SC = 1;          // doubles per scalar (1 real, 2 complex); all offsets below are in scalars
   std::vector<cudaEvent_t> evpool;
   struct Pend {
     int cls;
@@ -339,7 +350,9 @@ struct Planner {
   }
   // algorithmic FLOPs / HBM bytes of one box by kernel class
   void account_box(double nb, double r, double k, double P) {
-    const double nr = nb - k, nc = r - nr, W8 = 8.0;
+    const double nr = nb - k, nc = r - nr, W8 = 8.0 * SC;
+    const double F = cplx ? 4.0 : 1.0;   // real-equivalent flops of a complex multiply-add
+    auto account = [&](int cls, double fl, double by) { this->account(cls, F * fl, by); };
     account(KC_GRAM, 2 * (r * (r + 1) * P + 2 * nb * r * P), W8 * (2 * (r * P + nb * P) + 2 * (r * (r + 1) / 2 + nb * r)));
     account(KC_CHOL, 2 * (r * r * r / 3 + nb * r * r), W8 * 2 * 2 * (r * (r + 1) / 2 + nb * r));
     account(KC_TRSM, 2 * (nb * r * r), W8 * 2 * (r * (r + 1) / 2 + 2 * nb * r));
@@ -362,6 +375,7 @@ struct Planner {
   }
 
   void run(double* Y, double* Z, double* Om, double* Ps, i64 ld) {
+    const int sS = (int)(SC * sizeof(double));   // bytes per scalar
     const int L = T.L;
     const int p = (int)f->p;
     const int top = f->top_level;
@@ -394,9 +408,13 @@ struct Planner {
         int r = 0;
         for (int q = lv.nbr_off[b]; q < lv.nbr_off[b + 1]; ++q) r += nb_box[lv.nbr[q]];
         rmaxv[b] = r;
-        if (nb_box[b] > 160) {
+        // per-box dense kernels keep H (n_b x n_b) and X_rr, X_rr^-1 in shared memory
+        const size_t nbz = nb_box[b];
+        if (nbz * (nbz + 1) * sS + 3 * nbz * 4 + 64 > (size_t)SMEM_MAX ||
+            2 * nbz * (nbz + 1) * sS + 3 * nbz * 4 + 64 > (size_t)SMEM_MAX) {
           std::ostringstream os;
-          os << "level " << lev << " box " << b << ": |I_b| = " << nb_box[b] << " exceeds 160";
+          os << "level " << lev << " box " << b << ": |I_b| = " << nb_box[b]
+             << " exceeds the shared-memory capacity of the per-box ID / LU kernels";
           throw StatusError{RSRS_ERR_INVALID, os.str()};
         }
       }
@@ -434,7 +452,7 @@ struct Planner {
           x.nnbr = lv.nbr_off[b + 1] - lv.nbr_off[b];
           x.off_aug = wo;   wo += 2 * (r + nb) * ldr;
           x.off_yz = wo;    wo += nb * 2 * nld;
-          x.off_h = wo;     wo += nb * ldn;
+          x.off_h = wo;     wo += 2 * nb * ldn;   // H_Y = Y'' Y''^*, H_Z = Z'' Z''^*
           x.off_xy = wo;    wo += nb * ldr;
           x.off_xz = wo;    wo += nb * ldr;
           x.off_xrc = wo;   wo += nb * ldr;
@@ -463,13 +481,13 @@ struct Planner {
         ws_need = std::max(ws_need, wo);
         binfo.push_back(bi);
       }
-      DBuf* fpool_b = keep(sizeof(double) * std::max<i64>(foff, 2));
+      DBuf* fpool_b = keep((size_t)sS * std::max<i64>(foff, 2));
       DBuf* ipool_b = keep(sizeof(int) * std::max<i64>(fioff, 2));
       DBuf* boxes_b = keep(sizeof(BoxDev) * std::max<size_t>(hb.size(), 1));
       double* fpool = fpool_b->as<double>();
       int* ipool = ipool_b->as<int>();
       BoxDev* dboxes = boxes_b->as<BoxDev>();
-      ws.ensure(sizeof(double) * std::max<i64>(ws_need, 2), s);
+      ws.ensure((size_t)sS * std::max<i64>(ws_need, 2), s);
       iws.ensure(sizeof(int) * std::max<i64>(ioff, 2), s);
       double* dws = ws.as<double>();
       int* diws = iws.as<int>();
@@ -504,8 +522,8 @@ struct Planner {
         const i64 ldr = x.ldr, ldn = x.ldn;
         const int* near = diws + x.off_rows;
         const int* brows = near + rm;
-        double* augO = dws + x.off_aug;
-        double* augP = augO + (i64)(rm + nb) * ldr;
+        double* augO = dws + SC * x.off_aug;
+        double* augP = augO + SC * (i64)(rm + nb) * ldr;
         NTDesc a{};
         a.A = Om; a.rowA = near; a.lda = ld; a.B = Om; a.rowB = near; a.ldb = ld;
         a.C = augO; a.ldc = ldr; a.m = rm; a.n = rm; a.K = p; a.sym_rows = rm; a.alpha = 1.0;
@@ -515,32 +533,34 @@ struct Planner {
         nt_gram.push_back(a);
         NTDesc bq{};
         bq.A = Y; bq.rowA = brows; bq.lda = ld; bq.B = Om; bq.rowB = near; bq.ldb = ld;
-        bq.C = augO + (i64)rm * ldr; bq.ldc = ldr; bq.m = nb; bq.n = rm; bq.K = p; bq.sym_rows = 0;
+        bq.C = augO + SC * (i64)rm * ldr; bq.ldc = ldr; bq.m = nb; bq.n = rm; bq.K = p; bq.sym_rows = 0;
         bq.alpha = 1.0; bq.pn = &dx->r;
         nt_gram.push_back(bq);
-        bq.A = Z; bq.B = Ps; bq.C = augP + (i64)rm * ldr;
+        bq.A = Z; bq.B = Ps; bq.C = augP + SC * (i64)rm * ldr;
         nt_gram.push_back(bq);
         const i64 nlv = (i64)((rm + 63) / 64) * 64 * 64;
-        chol.push_back(CholDesc{augO, ldr, &dx->r, nb, rm, &dx->status, dws + x.off_linv});
-        chol.push_back(CholDesc{augP, ldr, &dx->r, nb, rm, &dx->status, dws + x.off_linv + nlv});
-        double* yz = dws + x.off_yz;
+        chol.push_back(CholDesc{augO, ldr, &dx->r, nb, rm, &dx->status, dws + SC * x.off_linv});
+        chol.push_back(CholDesc{augP, ldr, &dx->r, nb, rm, &dx->status, dws + SC * (x.off_linv + nlv)});
+        double* yz = dws + SC * x.off_yz;
         NNDesc pr{};
-        pr.A = augO + (i64)rm * ldr; pr.lda = ldr; pr.transA = 0;
+        pr.A = augO + SC * (i64)rm * ldr; pr.lda = ldr; pr.transA = 0;
         pr.B = Om; pr.rowB = near; pr.ldb = ld;
         pr.D = yz; pr.rowD = nullptr; pr.ldd = 2 * nld;
-        pr.Cin = Y + (i64)x.row0 * ld; pr.rowC = nullptr; pr.ldc = ld;
+        pr.Cin = Y + SC * (i64)x.row0 * ld; pr.rowC = nullptr; pr.ldc = ld;
         pr.m = nb; pr.n = p; pr.K = rm; pr.alpha = -1.0; pr.beta = 1.0; pr.pK = &dx->r;
         nn_proj.push_back(pr);
-        pr.A = augP + (i64)rm * ldr; pr.B = Ps; pr.D = yz + nld; pr.Cin = Z + (i64)x.row0 * ld;
+        pr.A = augP + SC * (i64)rm * ldr; pr.B = Ps; pr.D = yz + SC * nld; pr.Cin = Z + SC * (i64)x.row0 * ld;
         nn_proj.push_back(pr);
         NTDesc h{};
         h.A = yz; h.rowA = nullptr; h.lda = 2 * nld; h.B = yz; h.rowB = nullptr; h.ldb = 2 * nld;
-        h.C = dws + x.off_h; h.ldc = ldn; h.m = nb; h.n = nb; h.K = (int)(2 * nld); h.sym_rows = 0;
+        h.C = dws + SC * x.off_h; h.ldc = ldn; h.m = nb; h.n = nb; h.K = p; h.sym_rows = 0;
         h.alpha = 1.0;
+        nt_h.push_back(h);
+        h.A = yz + SC * nld; h.B = yz + SC * nld; h.C = dws + SC * (x.off_h + (i64)nb * ldn);
         nt_h.push_back(h);
         const int* skelrow = diws + x.off_skelrow;
         const int* redrow = diws + x.off_redrow;
-        double* Tm = fpool + x.f_T;
+        double* Tm = fpool + SC * x.f_T;
         NNDesc e{};
         e.A = Tm; e.lda = ldn; e.transA = 0; e.B = Y; e.rowB = skelrow; e.ldb = ld;
         e.D = Y; e.rowD = redrow; e.ldd = ld; e.Cin = nullptr;
@@ -556,23 +576,23 @@ struct Planner {
         fo.B = Ps; fo.D = Ps;
         nn_ef.push_back(fo);
         NNDesc gu{};
-        gu.A = fpool + x.f_Xinv; gu.lda = ldn; gu.B = dws + x.off_xrc; gu.rowB = nullptr; gu.ldb = ldr;
-        gu.D = fpool + x.f_GU; gu.ldd = ldr; gu.Cin = nullptr; gu.m = nb; gu.n = rm; gu.K = nb;
+        gu.A = fpool + SC * x.f_Xinv; gu.lda = ldn; gu.B = dws + SC * x.off_xrc; gu.rowB = nullptr; gu.ldb = ldr;
+        gu.D = fpool + SC * x.f_GU; gu.ldd = ldr; gu.Cin = nullptr; gu.m = nb; gu.n = rm; gu.K = nb;
         gu.alpha = 1.0; gu.beta = 0.0; gu.pm = &dx->nr; gu.pn = &dx->nc; gu.pK = &dx->nr;
         nn_g.push_back(gu);
         NNDesc gl{};
-        gl.A = dws + x.off_xcr; gl.lda = ldn; gl.B = fpool + x.f_Xinv; gl.rowB = nullptr; gl.ldb = ldn;
-        gl.D = fpool + x.f_GL; gl.ldd = ldn; gl.Cin = nullptr; gl.m = rm; gl.n = nb; gl.K = nb;
+        gl.A = dws + SC * x.off_xcr; gl.lda = ldn; gl.B = fpool + SC * x.f_Xinv; gl.rowB = nullptr; gl.ldb = ldn;
+        gl.D = fpool + SC * x.f_GL; gl.ldd = ldn; gl.Cin = nullptr; gl.m = rm; gl.n = nb; gl.K = nb;
         gl.alpha = 1.0; gl.beta = 0.0; gl.pm = &dx->nc; gl.pn = &dx->nr; gl.pK = &dx->nr;
         nn_g.push_back(gl);
         const int* crow = diws + x.off_crow;
         NNDesc u{};
-        u.A = fpool + x.f_GL; u.lda = ldn; u.transA = 0; u.B = Y; u.rowB = redrow; u.ldb = ld;
+        u.A = fpool + SC * x.f_GL; u.lda = ldn; u.transA = 0; u.B = Y; u.rowB = redrow; u.ldb = ld;
         u.D = Y; u.rowD = crow; u.ldd = ld; u.Cin = nullptr; u.m = rm; u.n = p; u.K = nb;
         u.alpha = -1.0; u.beta = 1.0; u.pm = &dx->nc; u.pK = &dx->nr;
         nn_upd.push_back(u);
         NNDesc uz = u;
-        uz.A = fpool + x.f_GU; uz.lda = ldr; uz.transA = 1; uz.B = Z; uz.D = Z;
+        uz.A = fpool + SC * x.f_GU; uz.lda = ldr; uz.transA = 1; uz.B = Z; uz.D = Z;
         nn_upd.push_back(uz);
       }
       std::vector<char> hdesc;
@@ -610,42 +630,44 @@ struct Planner {
         post("build_near_kernel", s, launches);
         toc();
         tic(KC_GRAM);
-        launch_nt(Dgram + 4 * q0, 4 * n, bi.max_r, bi.max_r, s, launches);
+        launch_nt(cplx, Dgram + 4 * q0, 4 * n, bi.max_r, bi.max_r, s, launches);
         toc();
         tic(KC_CHOL);
-        launch_chol_blocked(Dchol + 2 * q0, 2 * n, bi.max_r, bi.max_nb, s, launches);
+        launch_chol_any(cplx, Dchol + 2 * q0, 2 * n, bi.max_r, bi.max_nb, s, launches);
         toc();
         tic(KC_TRSM);
-        launch_back_blocked(Dchol + 2 * q0, 2 * n, bi.max_r, bi.max_nb, s, launches);
+        launch_back_any(cplx, Dchol + 2 * q0, 2 * n, bi.max_r, bi.max_nb, s, launches);
         toc();
         tic(KC_PROJ);
-        launch_nn(Dproj + 2 * q0, 2 * n, bi.max_nb, p, s, launches);
+        launch_nn(cplx, Dproj + 2 * q0, 2 * n, bi.max_nb, p, s, launches);
         toc();
         tic(KC_HGRAM);
-        launch_nt(Dh + q0, n, bi.max_nb, bi.max_nb, s, launches);
+        launch_nt(cplx, Dh + 2 * q0, 2 * n, bi.max_nb, bi.max_nb, s, launches);
         toc();
         {
-          const size_t sm = (size_t)bi.max_nb * (bi.max_nb + 1) * 8 + 3 * (size_t)bi.max_nb * 4 + 64;
+          const size_t sm = (size_t)bi.max_nb * (bi.max_nb + 1) * sS + 3 * (size_t)bi.max_nb * 4 + 64;
           tic(KC_ID);
-          rsrs::id_kernel<<<n, 256, sm, s>>>(dbx, dws, diws, fpool, ipool, gidx, atol * atol, p, l);
+          if (cplx) rsrs::id_kernel<true><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, ipool, gidx, atol * atol, p, l);
+          else rsrs::id_kernel<false><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, ipool, gidx, atol * atol, p, l);
           post("id_kernel", s, launches);
           toc();
         }
         tic(KC_EF);
-        launch_nn(Def + 4 * q0, 4 * n, bi.max_nb, p, s, launches);
+        launch_nn(cplx, Def + 4 * q0, 4 * n, bi.max_nb, p, s, launches);
         toc();
         {
-          const size_t sm = 2 * (size_t)bi.max_nb * (bi.max_nb + 1) * 8 + 3 * (size_t)bi.max_nb * 4 + 64;
+          const size_t sm = 2 * (size_t)bi.max_nb * (bi.max_nb + 1) * sS + 3 * (size_t)bi.max_nb * 4 + 64;
           tic(KC_EXTRACT);
-          rsrs::extract_lu_kernel<<<n, 256, sm, s>>>(dbx, dws, diws, fpool);
+          if (cplx) rsrs::extract_lu_kernel<true><<<n, 256, sm, s>>>(dbx, dws, diws, fpool);
+          else rsrs::extract_lu_kernel<false><<<n, 256, sm, s>>>(dbx, dws, diws, fpool);
           post("extract_lu_kernel", s, launches);
           toc();
         }
         tic(KC_G);
-        launch_nn(Dg + 2 * q0, 2 * n, bi.max_r, bi.max_r, s, launches);
+        launch_nn(cplx, Dg + 2 * q0, 2 * n, bi.max_r, bi.max_r, s, launches);
         toc();
         tic(KC_UPD);
-        launch_nn(Dupd + 2 * q0, 2 * n, bi.max_r, p, s, launches);
+        launch_nn(cplx, Dupd + 2 * q0, 2 * n, bi.max_r, p, s, launches);
         toc();
       }
       CK(cudaMemcpyAsync(hb.data(), dboxes, sizeof(BoxDev) * hb.size(), cudaMemcpyDeviceToHost, s));
@@ -704,23 +726,23 @@ struct Planner {
       std::vector<int> dst0(hb.size());
       for (size_t q = 0; q < hb.size(); ++q) dst0[q] = pref[hb[q].box];
       const int nxt = (cur == 0) ? 1 : 0;
-      store[nxt].ensure(sizeof(double) * std::max<i64>(2, 4 * nnew * nld), s);
+      store[nxt].ensure((size_t)sS * std::max<i64>(2, 4 * nnew * nld), s);
       gidx_buf[nxt].ensure(sizeof(int) * std::max<int64_t>(2, nnew), s);
       double* nY = store[nxt].as<double>();
-      double* nZ = nY + nnew * nld;
-      double* nO = nZ + nnew * nld;
-      double* nP = nO + nnew * nld;
+      double* nZ = nY + SC * nnew * nld;
+      double* nO = nZ + SC * nnew * nld;
+      double* nP = nO + SC * nnew * nld;
       int* ng = gidx_buf[nxt].as<int>();
       if (nnew > 0) {
         dstbuf.ensure(sizeof(int) * dst0.size(), s);
         CK(cudaMemcpyAsync(dstbuf.p, dst0.data(), sizeof(int) * dst0.size(), cudaMemcpyHostToDevice, s));
         dim3 grid((unsigned)hb.size(), 4);
         tic(KC_MISC);
-        rsrs::compact_kernel<<<grid, 128, 0, s>>>(dboxes, diws, dstbuf.as<int>(), Y, Z, Om, Ps, ld, gidx, nY, nZ,
-                                                 nO, nP, nld, ng, p);
+        rsrs::compact_kernel<<<grid, 128, 0, s>>>(dboxes, diws, dstbuf.as<int>(), Y, Z, Om, Ps, SC * ld, gidx, nY,
+                                                 nZ, nO, nP, SC * nld, ng, SC * p);
         post("compact_kernel", s, launches);
         toc();
-        account(KC_MISC, 0.0, 2.0 * 4 * nnew * p * 8);
+        account(KC_MISC, 0.0, 2.0 * 4 * nnew * p * sS);
         CK(cudaStreamSynchronize(s));
         flush_prof();
       }
@@ -752,11 +774,12 @@ struct Planner {
     const i64 ldS = even(nS);
     f->ldS = (int)ldS;
     DBuf aug, linv;
-    aug.alloc(sizeof(double) * 2 * nS * ldS, s);
-    linv.alloc(sizeof(double) * ((nS + 63) / 64) * 64 * 64, s);
+    const size_t sS = SC * sizeof(double);
+    aug.alloc(sS * 2 * nS * ldS, s);
+    linv.alloc(sS * ((nS + 63) / 64) * 64 * 64, s);
     DBuf* Sb = keep(sizeof(int) * nS);
-    DBuf* Ab = keep(sizeof(double) * nS * ldS);
-    DBuf* LUb = keep(sizeof(double) * nS * ldS);
+    DBuf* Ab = keep(sS * nS * ldS);
+    DBuf* LUb = keep(sS * nS * ldS);
     DBuf* pv = keep(sizeof(int) * nS);
     DBuf* st = keep(sizeof(int) * 4);
     f->d_S = Sb->as<int>();
@@ -772,7 +795,7 @@ struct Planner {
     hd[0].alpha = 1.0;
     hd[0].pm = hd[0].pn = hd[0].psym = nullptr;
     hd[1] = hd[0];
-    hd[1].A = Y; hd[1].C = aug.as<double>() + (i64)nS * ldS; hd[1].sym_rows = 0;
+    hd[1].A = Y; hd[1].C = aug.as<double>() + SC * (i64)nS * ldS; hd[1].sym_rows = 0;
     DBuf* nsb = keep(sizeof(int));
     CK(cudaMemcpyAsync(nsb->p, &nS, sizeof(int), cudaMemcpyHostToDevice, s));
     CholDesc cd{aug.as<double>(), ldS, nsb->as<int>(), nS, nS, dstat, linv.as<double>()};
@@ -787,14 +810,14 @@ struct Planner {
     const NTDesc* dnt = dbuf.as<NTDesc>();
     const CholDesc* dch = reinterpret_cast<const CholDesc*>(dbuf.as<char>() + oc);
     tic(KC_MISC);
-    launch_nt(dnt, 2, nS, nS, s, launches);
-    launch_chol_blocked(dch, 1, nS, nS, s, launches);
-    launch_back_blocked(dch, 1, nS, nS, s, launches);
-    CK(cudaMemcpy2DAsync(f->d_ASS, sizeof(double) * ldS, aug.as<double>() + (i64)nS * ldS, sizeof(double) * ldS,
-                         sizeof(double) * nS, nS, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpy2DAsync(f->d_LU, sizeof(double) * ldS, f->d_ASS, sizeof(double) * ldS, sizeof(double) * nS, nS,
+    launch_nt(cplx, dnt, 2, nS, nS, s, launches);
+    launch_chol_any(cplx, dch, 1, nS, nS, s, launches);
+    launch_back_any(cplx, dch, 1, nS, nS, s, launches);
+    CK(cudaMemcpy2DAsync(f->d_ASS, sS * ldS, aug.as<double>() + SC * (i64)nS * ldS, sS * ldS, sS * nS, nS,
                          cudaMemcpyDeviceToDevice, s));
-    rsrs::top_lu_kernel<<<1, 1024, 0, s>>>(f->d_LU, ldS, nS, f->d_piv, dstat);
+    CK(cudaMemcpy2DAsync(f->d_LU, sS * ldS, f->d_ASS, sS * ldS, sS * nS, nS, cudaMemcpyDeviceToDevice, s));
+    if (cplx) rsrs::top_lu_kernel<true><<<1, 1024, 0, s>>>(f->d_LU, ldS, nS, f->d_piv, dstat);
+    else rsrs::top_lu_kernel<false><<<1, 1024, 0, s>>>(f->d_LU, ldS, nS, f->d_piv, dstat);
     post("top_lu_kernel", s, launches);
     toc();
     int hst[4];
@@ -810,8 +833,9 @@ struct Planner {
     for (int i = 0; i < nS; ++i) f->S_host[i] = tmp[i];
     f->stats.memory_scalars += (int64_t)nS * nS;
     const double n = nS;
-    account(KC_MISC, n * (n + 1) * p + 2 * n * n * p + n * n * n / 3 + 2 * n * n * n + 2 * n * n * n / 3,
-            8.0 * (2 * n * p + 3 * n * n));
+    account(KC_MISC, (cplx ? 4.0 : 1.0) * (n * (n + 1) * p + 2 * n * n * p + n * n * n / 3 + 2 * n * n * n +
+                                         2 * n * n * n / 3),
+            sS * (2 * n * p + 3 * n * n));
   }
 };
 
@@ -831,7 +855,7 @@ rsrs_status rsrs_factor(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, void* Z,
   *out = nullptr;
   if (!t || !Y || !Z || !Omega || !Psi) return fail(RSRS_ERR_INVALID, "rsrs_factor: null argument");
   if (p < 1 || ld < p || (ld & 1)) return fail(RSRS_ERR_INVALID, "rsrs_factor: need 1 <= p <= ld and ld even");
-  if (dt != RSRS_F64) return fail(RSRS_ERR_STATE, "rsrs_factor: RSRS_C128 is not built in this version");
+  if (dt != RSRS_F64 && dt != RSRS_C128) return fail(RSRS_ERR_INVALID, "rsrs_factor: unknown dtype");
   rsrs_opts o{1e-6, 1.0, 1.0, 10, 2, 0, 1, nullptr, nullptr, 0};
   if (opts) o = *opts;
   if (o.nranks != 1 || o.rank != 0 || o.nccl_comm)
@@ -847,6 +871,8 @@ rsrs_status rsrs_factor(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, void* Z,
     f = new rsrs_factor_s();
     const rsrs::Tree& T = t->t;
     f->dt = dt;
+    f->cplx = (dt == RSRS_C128);
+    f->sc = f->cplx ? 2 : 1;
     f->N = T.N;
     f->p = p;
     f->L = T.L;
@@ -873,6 +899,8 @@ rsrs_status rsrs_factor(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, void* Z,
     P.cid = o.id_scale;
     P.l = o.oversample;
     P.profile = o.profile != 0;
+    P.cplx = f->cplx;
+    P.SC = f->sc;
     P.run((double*)Y, (double*)Z, (double*)Omega, (double*)Psi, ld);
     CK(cudaEventRecord(e1, s));
     CK(cudaEventSynchronize(e1));
@@ -896,6 +924,48 @@ rsrs_status rsrs_factor(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, void* Z,
   }
 }
 
+}  // extern "C"
+
+// solve / apply sweeps over the recorded colour batches
+template <bool C>
+static void run_sweep(rsrs_factorization f, double* x, int64_t nrhs, bool solve, cudaStream_t s) {
+  const size_t sS = (C ? 2 : 1) * sizeof(double);
+  const int nr = (int)nrhs;
+  if (solve) {
+    for (const Batch& b : f->batches) {
+      const size_t sm = sS * 2 * (b.max_nb + 2);
+      rsrs::solve_fwd_kernel<C><<<b.nbox, 256, sm, s>>>(b.d_boxes, b.fpool, b.ipool, x, nrhs, nr);
+      CK(cudaGetLastError());
+    }
+    if (f->nS > 0) {
+      rsrs::top_solve_kernel<C><<<1, 1024, sS * f->nS, s>>>(f->d_LU, f->ldS, f->nS, f->d_piv, f->d_S, x, nrhs, nr);
+      CK(cudaGetLastError());
+    }
+    for (auto it = f->batches.rbegin(); it != f->batches.rend(); ++it) {
+      const size_t sm = sS * (it->max_r + it->max_nb + 4);
+      rsrs::solve_bwd_kernel<C><<<it->nbox, 256, sm, s>>>(it->d_boxes, it->fpool, it->ipool, x, nrhs, nr);
+      CK(cudaGetLastError());
+    }
+  } else {
+    for (const Batch& b : f->batches) {
+      const size_t sm = sS * (b.max_r + 2 * b.max_nb + 4);
+      rsrs::apply_fwd_kernel<C><<<b.nbox, 256, sm, s>>>(b.d_boxes, b.fpool, b.ipool, x, nrhs, nr);
+      CK(cudaGetLastError());
+    }
+    if (f->nS > 0) {
+      rsrs::top_apply_kernel<C><<<1, 1024, sS * f->nS, s>>>(f->d_ASS, f->ldS, f->nS, f->d_S, x, nrhs, nr);
+      CK(cudaGetLastError());
+    }
+    for (auto it = f->batches.rbegin(); it != f->batches.rend(); ++it) {
+      const size_t sm = sS * (2 * it->max_nb + 4);
+      rsrs::apply_bwd_kernel<C><<<it->nbox, 256, sm, s>>>(it->d_boxes, it->fpool, it->ipool, x, nrhs, nr);
+      CK(cudaGetLastError());
+    }
+  }
+}
+
+extern "C" {
+
 static rsrs_status sweep(rsrs_factorization f, void* Bv, int64_t ldb, int64_t nrhs, void* sv, bool solve) {
   rsrs::clear_error();
   const char* who = solve ? "rsrs_solve" : "rsrs_apply";
@@ -905,52 +975,22 @@ static rsrs_status sweep(rsrs_factorization f, void* Bv, int64_t ldb, int64_t nr
   try {
     double* B = (double*)Bv;
     const int64_t N = f->N;
-    f->xtmp.ensure(sizeof(double) * N * nrhs, s);
+    const int SC = f->sc;
+    f->xtmp.ensure(sizeof(double) * SC * N * nrhs, s);
     double* x = f->xtmp.as<double>();
     const int nr = (int)nrhs;
     {
       dim3 blk(32, 8);
       dim3 grid((unsigned)((N + 7) / 8));
-      rsrs::permute_rows_kernel<<<grid, blk, 0, s>>>(B, ldb, x, nrhs, f->d_perm, N, nr, 0);
+      rsrs::permute_rows_kernel<<<grid, blk, 0, s>>>(B, SC * ldb, x, SC * nrhs, f->d_perm, N, SC * nr, 0);
       CK(cudaGetLastError());
     }
-    if (solve) {
-      for (const Batch& b : f->batches) {
-        const size_t sm = sizeof(double) * 2 * (b.max_nb + 2);
-        rsrs::solve_fwd_kernel<<<b.nbox, 256, sm, s>>>(b.d_boxes, b.fpool, b.ipool, x, nrhs, nr);
-        CK(cudaGetLastError());
-      }
-      if (f->nS > 0) {
-        rsrs::top_solve_kernel<<<1, 1024, sizeof(double) * f->nS, s>>>(f->d_LU, f->ldS, f->nS, f->d_piv, f->d_S,
-                                                                       x, nrhs, nr);
-        CK(cudaGetLastError());
-      }
-      for (auto it = f->batches.rbegin(); it != f->batches.rend(); ++it) {
-        const size_t sm = sizeof(double) * (it->max_r + it->max_nb + 4);
-        rsrs::solve_bwd_kernel<<<it->nbox, 256, sm, s>>>(it->d_boxes, it->fpool, it->ipool, x, nrhs, nr);
-        CK(cudaGetLastError());
-      }
-    } else {
-      for (const Batch& b : f->batches) {
-        const size_t sm = sizeof(double) * (b.max_r + 2 * b.max_nb + 4);
-        rsrs::apply_fwd_kernel<<<b.nbox, 256, sm, s>>>(b.d_boxes, b.fpool, b.ipool, x, nrhs, nr);
-        CK(cudaGetLastError());
-      }
-      if (f->nS > 0) {
-        rsrs::top_apply_kernel<<<1, 1024, sizeof(double) * f->nS, s>>>(f->d_ASS, f->ldS, f->nS, f->d_S, x, nrhs,
-                                                                       nr);
-        CK(cudaGetLastError());
-      }
-      for (auto it = f->batches.rbegin(); it != f->batches.rend(); ++it) {
-        const size_t sm = sizeof(double) * (2 * it->max_nb + 4);
-        rsrs::apply_bwd_kernel<<<it->nbox, 256, sm, s>>>(it->d_boxes, it->fpool, it->ipool, x, nrhs, nr);
-        CK(cudaGetLastError());
-      }
-    }
+    if (f->cplx) run_sweep<true>(f, x, nrhs, solve, s);
+    else run_sweep<false>(f, x, nrhs, solve, s);
     {
       dim3 blk(32, 8);
       dim3 grid((unsigned)((N + 7) / 8));
-      rsrs::permute_rows_kernel<<<grid, blk, 0, s>>>(x, nrhs, B, ldb, f->d_perm, N, nr, 1);
+      rsrs::permute_rows_kernel<<<grid, blk, 0, s>>>(x, SC * nrhs, B, SC * ldb, f->d_perm, N, SC * nr, 1);
       CK(cudaGetLastError());
     }
     return RSRS_OK;

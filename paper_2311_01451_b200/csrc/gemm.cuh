@@ -272,4 +272,286 @@ __global__ void __launch_bounds__(128) gemm_nn_kernel(const NNDesc* __restrict__
   nn_tile(dl, m, n, K, i0, j0, smem);
 }
 
+
+// ---------------------------------------------------------------------------
+// complex128 variants (RSRS_C128; interleaved {re, im} doubles).  Leading
+// dimensions and sizes in the descriptors are in COMPLEX units.  Both shapes
+// run as real DMMA GEMMs over the interleaved data (K_real = 2K):
+//   NT  C = A B^H:  Re = A_r B_r^T, Im = A_r (B')^T with B'_q = sign(q) B_{q^1}
+//                   (sign = -1 for an even real index q): Im(a conj b) = sum ai br - ar bi
+//   NN  D = opA B:  B''_{2k} = B_k, B''_{2k+1} = rot(B_k), rot(br, bi) = (-bi, br)
+//                   opA = conj(A)^T when transA (A^* in the sample updates)
+// ---------------------------------------------------------------------------
+constexpr int GTC = 32;      // complex output columns of the NT tile (64 rows x 32 complex)
+
+RSRS_DI void nt_tile_c(const NTDesc& d, int m, int n, int K, int i0, int j0, double* smem) {
+  double* As = smem;                      // [2][64][GPA]
+  double* Bs = smem + 2 * GT * GPA;       // [2][32][GPA]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int wr = warp >> 1, wc = warp & 1;
+  const int K2 = 2 * K;
+  const i64 lda2 = 2 * d.lda, ldb2 = 2 * d.ldb;
+  const double* aptr[8];
+  const double* bptr[4];
+  bool aval[8], bval[4];
+  const int lrow = tid >> 4, kc = (tid & 15) * 2;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int gi = i0 + lrow + 8 * q;
+    aval[q] = gi < m;
+    const i64 ar = aval[q] ? (d.rowA ? (i64)d.rowA[gi] : (i64)gi) : 0;
+    aptr[q] = d.A + ar * lda2;
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int gj = j0 + lrow + 8 * q;
+    bval[q] = gj < n;
+    const i64 br = bval[q] ? (d.rowB ? (i64)d.rowB[gj] : (i64)gj) : 0;
+    bptr[q] = d.B + br * ldb2;
+  }
+  auto load_stage = [&](int s, int kt) {
+    const int k = kt * GBK + kc;
+    const int bytes = k < K2 ? 16 : 0;
+    const int koff = bytes ? k : 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      cp_async16(&As[(s * GT + lrow + 8 * q) * GPA + kc], aptr[q] + koff, aval[q] ? bytes : 0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      cp_async16(&Bs[(s * GTC + lrow + 8 * q) * GPA + kc], bptr[q] + koff, bval[q] ? bytes : 0);
+  };
+  double ar_[4][2][2], ai_[4][2][2];
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+#pragma unroll
+    for (int u = 0; u < 2; ++u) ar_[t][u][0] = ar_[t][u][1] = ai_[t][u][0] = ai_[t][u][1] = 0.0;
+  const double sgn = (tig & 1) ? 1.0 : -1.0;
+  const int nk = (K2 + GBK - 1) / GBK;
+  if (nk > 0) {
+    load_stage(0, 0);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    if (kt + 1 < nk) {
+      load_stage((kt + 1) & 1, kt + 1);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* as = As + ((kt & 1) * GT + wr * 32) * GPA;
+    const double* bs = Bs + ((kt & 1) * GTC + wc * 16) * GPA;
+#pragma unroll
+    for (int kk = 0; kk < GBK / 4; ++kk) {
+      double a[4], b[2], b2[2];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) a[t] = as[(t * 8 + gid) * GPA + kk * 4 + tig];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        b[u] = bs[(u * 8 + gid) * GPA + kk * 4 + tig];
+        b2[u] = sgn * bs[(u * 8 + gid) * GPA + kk * 4 + (tig ^ 1)];
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          dmma884(ar_[t][u][0], ar_[t][u][1], a[t], b[u]);
+          dmma884(ai_[t][u][0], ai_[t][u][1], a[t], b2[u]);
+        }
+    }
+    __syncthreads();
+  }
+  const i64 ldc2 = 2 * d.ldc;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int i = i0 + wr * 32 + t * 8 + gid;
+    if (i >= m) continue;
+    double* crow = d.C + (i64)i * ldc2;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = j0 + wc * 16 + u * 8 + 2 * tig + e;
+        if (j < n) {
+          double2 c = make_double2(0.0, 0.0);
+          if (d.beta != 0.0) c = *reinterpret_cast<const double2*>(crow + 2 * j);
+          *reinterpret_cast<double2*>(crow + 2 * j) =
+              make_double2(d.beta * c.x + d.alpha * ar_[t][u][e], d.beta * c.y + d.alpha * ai_[t][u][e]);
+        }
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128) gemm_nt_kernel_c(const NTDesc* __restrict__ descs) {
+  extern __shared__ __align__(16) double smem[];
+  const NTDesc& d = descs[blockIdx.z];
+  const int m = dyn(d.pm, 0, d.m);
+  const int n = dyn(d.pn, 0, d.n);
+  const int i0 = blockIdx.y * GT, j0 = blockIdx.x * GTC;
+  if (i0 >= m || j0 >= n) return;
+  const int sym = d.psym ? *d.psym : d.sym_rows;
+  if (i0 + GT <= sym && j0 >= i0 + GT) return;  // strictly upper part of the Hermitian Gram
+  const NTDesc dl = d;
+  nt_tile_c(dl, m, n, d.K, i0, j0, smem);
+}
+
+// One tile (64 rows x 32 complex columns) of D_rows = beta C_rows + alpha opA B_rows.
+RSRS_DI void nn_tile_c(const NNDesc& d, int m, int n, int K, int i0, int j0, double* smem) {
+  const bool inplace = (d.Cin == nullptr);
+  if (K <= 0 && inplace && d.beta == 1.0) return;
+  double* As = smem;                       // [2][64][GPA]   (i, real k)
+  double* Bs = smem + 2 * GT * GPA;        // [2][16][GPB]   (complex k, real j)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int wr = warp >> 1, wc = warp & 1;
+  const int K2 = 2 * K, n2 = 2 * n, j02 = 2 * j0;
+  const i64 lda2 = 2 * d.lda, ldb2 = 2 * d.ldb;
+  auto load_stage = [&](int s, int kt) {
+    const int k0 = kt * GBK;               // real k
+    if (!d.transA) {
+      const int lrow = tid >> 4, kc = (tid & 15) * 2;
+      const int k = k0 + kc;
+      const int bytes = k < K2 ? 16 : 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int row = lrow + 8 * q;
+        const int gi = i0 + row;
+        const bool v = gi < m && bytes > 0;
+        const double* src = v ? d.A + (i64)gi * lda2 + k : d.A;
+        cp_async16(&As[(s * GT + row) * GPA + kc], src, v ? bytes : 0);
+      }
+    } else {
+      // opA(i, k) = conj(A[k][i]), A stored K x m (complex)
+      const int kr = tid >> 5, ic = (tid & 31) * 2;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int kl = kr + 4 * q;          // complex k (local, 0..15)
+        const int k = (k0 >> 1) + kl;
+        const int gi = i0 + ic;
+        double2 v0 = make_double2(0.0, 0.0), v1 = v0;
+        if (k < K) {
+          const double* src = d.A + (i64)k * lda2 + 2 * (i64)gi;
+          if (gi < m) v0 = *reinterpret_cast<const double2*>(src);
+          if (gi + 1 < m) v1 = *reinterpret_cast<const double2*>(src + 2);
+        }
+        As[(s * GT + ic) * GPA + 2 * kl] = v0.x;
+        As[(s * GT + ic) * GPA + 2 * kl + 1] = -v0.y;
+        As[(s * GT + ic + 1) * GPA + 2 * kl] = v1.x;
+        As[(s * GT + ic + 1) * GPA + 2 * kl + 1] = -v1.y;
+      }
+    }
+    {
+      const int kr = tid >> 5, jc = (tid & 31) * 2;
+      const int gj = j02 + jc;
+      const int cb = (gj < n2) ? 16 : 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int kl = kr + 4 * q;            // complex k (local)
+        const int k = (k0 >> 1) + kl;
+        const bool v = k < K && cb > 0;
+        const double* src = d.B;
+        if (v) {
+          const i64 br = d.rowB ? (i64)d.rowB[k] : (i64)k;
+          src = d.B + br * ldb2 + gj;
+        }
+        cp_async16(&Bs[(s * (GBK / 2) + kl) * GPB + jc], src, v ? cb : 0);
+      }
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
+  const bool odd_k = tig & 1;
+  const double sgn = (gid & 1) ? 1.0 : -1.0;
+  const int nk = K2 > 0 ? (K2 + GBK - 1) / GBK : 0;
+  if (nk > 0) {
+    load_stage(0, 0);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    if (kt + 1 < nk) {
+      load_stage((kt + 1) & 1, kt + 1);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* as = As + ((kt & 1) * GT + wr * 32) * GPA;
+    const double* bs = Bs + (kt & 1) * (GBK / 2) * GPB + wc * 32;
+#pragma unroll
+    for (int kk = 0; kk < GBK / 4; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) a[t] = as[(t * 8 + gid) * GPA + kk * 4 + tig];
+      const double* brow = bs + (kk * 2 + (tig >> 1)) * GPB;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int col = u * 8 + gid;
+        b[u] = odd_k ? sgn * brow[col ^ 1] : brow[col];
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) dmma884(acc[t][u][0], acc[t][u][1], a[t], b[u]);
+    }
+    __syncthreads();
+  }
+  const i64 ldd2 = 2 * d.ldd, ldc2 = 2 * d.ldc;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int i = i0 + wr * 32 + t * 8 + gid;
+    if (i >= m) continue;
+    const i64 dr = d.rowD ? (i64)d.rowD[i] : (i64)i;
+    double* drow = d.D + dr * ldd2;
+    const double* crow;
+    if (inplace) {
+      crow = drow;
+    } else {
+      const i64 cr = d.rowC ? (i64)d.rowC[i] : (i64)i;
+      crow = d.Cin + cr * ldc2;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = j02 + wc * 32 + u * 8 + 2 * tig;     // real column (even: one complex entry)
+      if (j < n2) {
+        double2 c = make_double2(0.0, 0.0);
+        if (d.beta != 0.0) c = *reinterpret_cast<const double2*>(crow + j);
+        *reinterpret_cast<double2*>(drow + j) =
+            make_double2(d.beta * c.x + d.alpha * acc[t][u][0], d.beta * c.y + d.alpha * acc[t][u][1]);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128) gemm_nn_kernel_c(const NNDesc* __restrict__ descs) {
+  extern __shared__ __align__(16) double smem[];
+  const NNDesc& d = descs[blockIdx.z];
+  const int m = dyn(d.pm, 0, d.m);
+  const int n = dyn(d.pn, 0, d.n);
+  const int K = dyn(d.pK, 0, d.K);
+  const int i0 = blockIdx.y * GT, j0 = blockIdx.x * GTC;
+  if (i0 >= m || j0 >= n) return;
+  const NNDesc dl = d;
+  nn_tile_c(dl, m, n, K, i0, j0, smem);
+}
+
+// scalar-type dispatch used by the templated per-box kernels
+template <bool C>
+RSRS_DI void nt_tile_t(const NTDesc& d, int m, int n, int K, int i0, int j0, double* smem) {
+  if constexpr (C) nt_tile_c(d, m, n, K, i0, j0, smem);
+  else nt_tile(d, m, n, K, i0, j0, smem);
+}
+template <bool C>
+RSRS_DI void nn_tile_t(const NNDesc& d, int m, int n, int K, int i0, int j0, double* smem) {
+  if constexpr (C) nn_tile_c(d, m, n, K, i0, j0, smem);
+  else nn_tile(d, m, n, K, i0, j0, smem);
+}
+template <bool C> constexpr int tile_n() { return C ? GTC : GT; }
+
 }  // namespace rsrs

@@ -99,6 +99,107 @@ __global__ void __launch_bounds__(128) matvec_real_kernel(const double* __restri
   }
 }
 
+// Complex operator (kind 2, config c4): A_ij = delta_ij + w (i/4) H0^(1)(kappa r)
+// = delta_ij + w (-Y0(kappa r) + i J0(kappa r)) / 4, complex symmetric, so
+// A^* = conj(A).  X, Y are complex128 (interleaved doubles).  Y = A X runs as
+// Y_real = A_r X_real + A_i rot(X_real) with rot(xr, xi) = (-xi, xr) per
+// entry, i.e. two real DMMAs per step.  64 rows x 64 complex columns per CTA.
+constexpr int CTN = 128;          // real columns of the X tile (64 complex)
+constexpr int CSB = CTN + 4;
+constexpr int CPLX_SMEM = (2 * TM * SA + TK * CSB + TM * 3) * 8;
+
+__global__ void __launch_bounds__(256) matvec_cplx_kernel(const double* __restrict__ pts, int64_t N,
+                                                          const double* __restrict__ X, int64_t ldx,
+                                                          double* __restrict__ Y, int64_t ldy, int ncol,
+                                                          double w, double kappa, int adjoint) {
+  extern __shared__ __align__(16) double csm[];
+  double* Ar = csm;
+  double* Ai = Ar + TM * SA;
+  double* Bs = Ai + TM * SA;
+  double* Pi = Bs + TK * CSB;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int wr = warp >> 2, wc = warp & 3;
+  const int64_t i0 = (int64_t)blockIdx.y * TM;
+  const int c0 = blockIdx.x * (CTN / 2);            // complex column
+  const int ncol2 = 2 * ncol;
+  const double sgn_im = adjoint ? -1.0 : 1.0;
+  for (int t = tid; t < TM * 3; t += 256) {
+    const int64_t gi = i0 + t / 3;
+    Pi[t] = gi < N ? pts[gi * 3 + t % 3] : 0.0;
+  }
+  double acc[4][4][2];
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
+  __syncthreads();
+  for (int64_t k0 = 0; k0 < N; k0 += TK) {
+    for (int t = tid; t < TM * TK; t += 256) {
+      const int ii = t / TK, kk = t % TK;
+      const int64_t gi = i0 + ii, gk = k0 + kk;
+      double vr = 0.0, vi = 0.0;
+      if (gi < N && gk < N) {
+        if (gi == gk) {
+          vr = 1.0;
+        } else {
+          const double dx = Pi[ii * 3] - pts[gk * 3];
+          const double dy = Pi[ii * 3 + 1] - pts[gk * 3 + 1];
+          const double dz = Pi[ii * 3 + 2] - pts[gk * 3 + 2];
+          const double kr = kappa * sqrt(dx * dx + dy * dy + dz * dz);
+          vr = -0.25 * w * ::y0(kr);
+          vi = sgn_im * 0.25 * w * ::j0(kr);
+        }
+      }
+      Ar[ii * SA + kk] = vr;
+      Ai[ii * SA + kk] = vi;
+    }
+    for (int t = tid; t < TK * CTN; t += 256) {
+      const int kk = t / CTN, jj = t % CTN;
+      const int64_t gk = k0 + kk;
+      Bs[kk * CSB + jj] = (gk < N && 2 * c0 + jj < ncol2) ? X[gk * 2 * ldx + 2 * c0 + jj] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < TK / 4; ++kk) {
+      double ar[4], ai[4], b[4], br[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        ar[t] = Ar[(wr * 32 + t * 8 + gid) * SA + kk * 4 + tig];
+        ai[t] = Ai[(wr * 32 + t * 8 + gid) * SA + kk * 4 + tig];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int col = wc * 32 + u * 8 + gid;
+        const double* brow = Bs + (kk * 4 + tig) * CSB;
+        b[u] = brow[col];
+        br[u] = (gid & 1) ? brow[col - 1] : -brow[col + 1];
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          rsrs::dmma884(acc[t][u][0], acc[t][u][1], ar[t], b[u]);
+          rsrs::dmma884(acc[t][u][0], acc[t][u][1], ai[t], br[u]);
+        }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int64_t i = i0 + wr * 32 + t * 8 + gid;
+    if (i >= N) continue;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = 2 * c0 + wc * 32 + u * 8 + 2 * tig;   // real column (even)
+      if (j < ncol2) {
+        Y[i * 2 * ldy + j] = acc[t][u][0];
+        Y[i * 2 * ldy + j + 1] = acc[t][u][1];
+      }
+    }
+  }
+}
+
 thread_local std::string g_err;
 
 }  // namespace
@@ -120,6 +221,24 @@ int rsrs_sample_matvec(int kind, const double* pts, int64_t N, double weight, co
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     g_err = std::string("rsrs_sample_matvec: ") + cudaGetErrorString(e);
+    return 4;
+  }
+  return 0;
+}
+
+int rsrs_sample_matvec_c128(const double* pts, int64_t N, double weight, double kappa, const void* X,
+                            int64_t ldx, void* Y, int64_t ldy, int64_t ncol, int adjoint, void* stream) {
+  if (!pts || !X || !Y || N < 1 || ncol < 1 || ldx < ncol || ldy < ncol) {
+    g_err = "rsrs_sample_matvec_c128: invalid argument";
+    return 1;
+  }
+  dim3 grid((unsigned)((ncol + CTN / 2 - 1) / (CTN / 2)), (unsigned)((N + TM - 1) / TM));
+  cudaFuncSetAttribute(matvec_cplx_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, CPLX_SMEM);
+  matvec_cplx_kernel<<<grid, 256, CPLX_SMEM, (cudaStream_t)stream>>>(pts, N, (const double*)X, ldx, (double*)Y, ldy,
+                                                             (int)ncol, weight, kappa, adjoint);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    g_err = std::string("rsrs_sample_matvec_c128: ") + cudaGetErrorString(e);
     return 4;
   }
   return 0;

@@ -11,44 +11,58 @@ RSRS_DI double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
+RSRS_DI double2 warp_sum(double2 v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+  }
+  return v;
+}
 
 // forward solve of one box: x_r -= T x_s ; x_c -= G_L x_r ; x_r <- X_rr^-1 x_r
+template <bool C>
 __global__ void __launch_bounds__(256) solve_fwd_kernel(const BoxDev* __restrict__ boxes,
-                                                         const double* __restrict__ fpool,
-                                                         const int* __restrict__ ipool, double* __restrict__ x,
+                                                         const double* __restrict__ fpoold,
+                                                         const int* __restrict__ ipool, double* __restrict__ xd,
                                                          i64 ldx, int nrhs) {
-  extern __shared__ double sm[];
+  typedef typename ScalarOf<C>::T S;
+  extern __shared__ __align__(16) double smd[];
+  S* sm = reinterpret_cast<S*>(smd);
+  const S* fpool = reinterpret_cast<const S*>(fpoold);
+  S* x = reinterpret_cast<S*>(xd);
+  const S zero = s_zero(S());
   const BoxDev b = boxes[blockIdx.x];
   const int nr = b.nr, k = b.k, nc = b.nc;
   if (nr <= 0) return;
   const int ldn = b.ldn;
-  double* xs = sm;
-  double* xr = xs + k;
+  S* xs = sm;
+  S* xr = xs + k;
   const int* red = ipool + b.f_red;
   const int* skel = ipool + b.f_skel;
   const int* cc = ipool + b.f_c;
-  const double* T = fpool + b.f_T;
-  const double* GL = fpool + b.f_GL;
-  const double* Xi = fpool + b.f_Xinv;
+  const S* T = fpool + b.f_T;
+  const S* GL = fpool + b.f_GL;
+  const S* Xi = fpool + b.f_Xinv;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int col = 0; col < nrhs; ++col) {
     for (int s = tid; s < k; s += blockDim.x) xs[s] = x[(i64)skel[s] * ldx + col];
     __syncthreads();
     for (int i = tid; i < nr; i += blockDim.x) {
-      double v = x[(i64)red[i] * ldx + col];
-      for (int s = 0; s < k; ++s) v -= T[(i64)i * ldn + s] * xs[s];
+      S v = x[(i64)red[i] * ldx + col];
+      for (int s = 0; s < k; ++s) v = s_sub(v, s_mul(T[(i64)i * ldn + s], xs[s]));
       xr[i] = v;
     }
     __syncthreads();
     for (int ci = warp; ci < nc; ci += blockDim.x / 32) {
-      double v = 0.0;
-      for (int j = lane; j < nr; j += 32) v += GL[(i64)ci * ldn + j] * xr[j];
+      S v = zero;
+      for (int j = lane; j < nr; j += 32) v = s_add(v, s_mul(GL[(i64)ci * ldn + j], xr[j]));
       v = warp_sum(v);
-      if (lane == 0) x[(i64)cc[ci] * ldx + col] -= v;
+      if (lane == 0) x[(i64)cc[ci] * ldx + col] = s_sub(x[(i64)cc[ci] * ldx + col], v);
     }
     for (int i = warp; i < nr; i += blockDim.x / 32) {
-      double v = 0.0;
-      for (int j = lane; j < nr; j += 32) v += Xi[(i64)i * ldn + j] * xr[j];
+      S v = zero;
+      for (int j = lane; j < nr; j += 32) v = s_add(v, s_mul(Xi[(i64)i * ldn + j], xr[j]));
       v = warp_sum(v);
       if (lane == 0) x[(i64)red[i] * ldx + col] = v;
     }
@@ -57,89 +71,101 @@ __global__ void __launch_bounds__(256) solve_fwd_kernel(const BoxDev* __restrict
 }
 
 // backward solve of one box: x_r -= G_U x_c ; x_s -= T^T x_r
+template <bool C>
 __global__ void __launch_bounds__(256) solve_bwd_kernel(const BoxDev* __restrict__ boxes,
-                                                         const double* __restrict__ fpool,
-                                                         const int* __restrict__ ipool, double* __restrict__ x,
+                                                         const double* __restrict__ fpoold,
+                                                         const int* __restrict__ ipool, double* __restrict__ xd,
                                                          i64 ldx, int nrhs) {
-  extern __shared__ double sm[];
+  typedef typename ScalarOf<C>::T S;
+  extern __shared__ __align__(16) double smd[];
+  S* sm = reinterpret_cast<S*>(smd);
+  const S* fpool = reinterpret_cast<const S*>(fpoold);
+  S* x = reinterpret_cast<S*>(xd);
+  const S zero = s_zero(S());
   const BoxDev b = boxes[blockIdx.x];
   const int nr = b.nr, k = b.k, nc = b.nc;
   if (nr <= 0) return;
   const int ldn = b.ldn;
   const int ldr = b.ldr;
-  double* xc = sm;
-  double* xr = xc + nc;
+  S* xc = sm;
+  S* xr = xc + nc;
   const int* red = ipool + b.f_red;
   const int* skel = ipool + b.f_skel;
   const int* cc = ipool + b.f_c;
-  const double* T = fpool + b.f_T;
-  const double* GU = fpool + b.f_GU;
+  const S* T = fpool + b.f_T;
+  const S* GU = fpool + b.f_GU;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int col = 0; col < nrhs; ++col) {
     for (int j = tid; j < nc; j += blockDim.x) xc[j] = x[(i64)cc[j] * ldx + col];
     __syncthreads();
     for (int i = warp; i < nr; i += blockDim.x / 32) {
-      double v = 0.0;
-      for (int j = lane; j < nc; j += 32) v += GU[(i64)i * ldr + j] * xc[j];
+      S v = zero;
+      for (int j = lane; j < nc; j += 32) v = s_add(v, s_mul(GU[(i64)i * ldr + j], xc[j]));
       v = warp_sum(v);
       if (lane == 0) {
-        const double nv = x[(i64)red[i] * ldx + col] - v;
+        const S nv = s_sub(x[(i64)red[i] * ldx + col], v);
         x[(i64)red[i] * ldx + col] = nv;
         xr[i] = nv;
       }
     }
     __syncthreads();
-    for (int s = tid; s < k; s += blockDim.x) {
-      double v = 0.0;
-      for (int i = 0; i < nr; ++i) v += T[(i64)i * ldn + s] * xr[i];
-      x[(i64)skel[s] * ldx + col] -= v;
+    for (int s = tid; s < k; s += blockDim.x) {   // x_s -= T^* x_r
+      S v = zero;
+      for (int i = 0; i < nr; ++i) v = s_add(v, s_mul(s_conj(T[(i64)i * ldn + s]), xr[i]));
+      x[(i64)skel[s] * ldx + col] = s_sub(x[(i64)skel[s] * ldx + col], v);
     }
     __syncthreads();
   }
 }
 
 // apply, forward half of one box: x_s += T^T x_r ; x_r += G_U x_c ; x_r <- X_rr x_r
+template <bool C>
 __global__ void __launch_bounds__(256) apply_fwd_kernel(const BoxDev* __restrict__ boxes,
-                                                         const double* __restrict__ fpool,
-                                                         const int* __restrict__ ipool, double* __restrict__ x,
+                                                         const double* __restrict__ fpoold,
+                                                         const int* __restrict__ ipool, double* __restrict__ xd,
                                                          i64 ldx, int nrhs) {
-  extern __shared__ double sm[];
+  typedef typename ScalarOf<C>::T S;
+  extern __shared__ __align__(16) double smd[];
+  S* sm = reinterpret_cast<S*>(smd);
+  const S* fpool = reinterpret_cast<const S*>(fpoold);
+  S* x = reinterpret_cast<S*>(xd);
+  const S zero = s_zero(S());
   const BoxDev b = boxes[blockIdx.x];
   const int nr = b.nr, k = b.k, nc = b.nc;
   if (nr <= 0) return;
   const int ldn = b.ldn;
   const int ldr = b.ldr;
-  double* xc = sm;
-  double* xr = xc + nc;
-  double* xr2 = xr + nr;
+  S* xc = sm;
+  S* xr = xc + nc;
+  S* xr2 = xr + nr;
   const int* red = ipool + b.f_red;
   const int* skel = ipool + b.f_skel;
   const int* cc = ipool + b.f_c;
-  const double* T = fpool + b.f_T;
-  const double* GU = fpool + b.f_GU;
-  const double* Xrr = fpool + b.f_Xrr;
+  const S* T = fpool + b.f_T;
+  const S* GU = fpool + b.f_GU;
+  const S* Xrr = fpool + b.f_Xrr;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int col = 0; col < nrhs; ++col) {
     for (int i = tid; i < nr; i += blockDim.x) xr[i] = x[(i64)red[i] * ldx + col];
     __syncthreads();
-    for (int s = tid; s < k; s += blockDim.x) {
-      double v = 0.0;
-      for (int i = 0; i < nr; ++i) v += T[(i64)i * ldn + s] * xr[i];
-      x[(i64)skel[s] * ldx + col] += v;
+    for (int s = tid; s < k; s += blockDim.x) {   // x_s += T^* x_r
+      S v = zero;
+      for (int i = 0; i < nr; ++i) v = s_add(v, s_mul(s_conj(T[(i64)i * ldn + s]), xr[i]));
+      x[(i64)skel[s] * ldx + col] = s_add(x[(i64)skel[s] * ldx + col], v);
     }
     __syncthreads();
     for (int j = tid; j < nc; j += blockDim.x) xc[j] = x[(i64)cc[j] * ldx + col];
     __syncthreads();
     for (int i = warp; i < nr; i += blockDim.x / 32) {
-      double v = 0.0;
-      for (int j = lane; j < nc; j += 32) v += GU[(i64)i * ldr + j] * xc[j];
+      S v = zero;
+      for (int j = lane; j < nc; j += 32) v = s_add(v, s_mul(GU[(i64)i * ldr + j], xc[j]));
       v = warp_sum(v);
-      if (lane == 0) xr[i] += v;
+      if (lane == 0) xr[i] = s_add(xr[i], v);
     }
     __syncthreads();
     for (int i = warp; i < nr; i += blockDim.x / 32) {
-      double v = 0.0;
-      for (int j = lane; j < nr; j += 32) v += Xrr[(i64)i * ldn + j] * xr[j];
+      S v = zero;
+      for (int j = lane; j < nr; j += 32) v = s_add(v, s_mul(Xrr[(i64)i * ldn + j], xr[j]));
       v = warp_sum(v);
       if (lane == 0) xr2[i] = v;
     }
@@ -150,38 +176,44 @@ __global__ void __launch_bounds__(256) apply_fwd_kernel(const BoxDev* __restrict
 }
 
 // apply, backward half of one box: x_c += G_L x_r ; x_r += T x_s
+template <bool C>
 __global__ void __launch_bounds__(256) apply_bwd_kernel(const BoxDev* __restrict__ boxes,
-                                                         const double* __restrict__ fpool,
-                                                         const int* __restrict__ ipool, double* __restrict__ x,
+                                                         const double* __restrict__ fpoold,
+                                                         const int* __restrict__ ipool, double* __restrict__ xd,
                                                          i64 ldx, int nrhs) {
-  extern __shared__ double sm[];
+  typedef typename ScalarOf<C>::T S;
+  extern __shared__ __align__(16) double smd[];
+  S* sm = reinterpret_cast<S*>(smd);
+  const S* fpool = reinterpret_cast<const S*>(fpoold);
+  S* x = reinterpret_cast<S*>(xd);
+  const S zero = s_zero(S());
   const BoxDev b = boxes[blockIdx.x];
   const int nr = b.nr, k = b.k, nc = b.nc;
   if (nr <= 0) return;
   const int ldn = b.ldn;
-  double* xs = sm;
-  double* xr = xs + k;
+  S* xs = sm;
+  S* xr = xs + k;
   const int* red = ipool + b.f_red;
   const int* skel = ipool + b.f_skel;
   const int* cc = ipool + b.f_c;
-  const double* T = fpool + b.f_T;
-  const double* GL = fpool + b.f_GL;
+  const S* T = fpool + b.f_T;
+  const S* GL = fpool + b.f_GL;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int col = 0; col < nrhs; ++col) {
     for (int i = tid; i < nr; i += blockDim.x) xr[i] = x[(i64)red[i] * ldx + col];
     __syncthreads();
     for (int ci = warp; ci < nc; ci += blockDim.x / 32) {
-      double v = 0.0;
-      for (int j = lane; j < nr; j += 32) v += GL[(i64)ci * ldn + j] * xr[j];
+      S v = zero;
+      for (int j = lane; j < nr; j += 32) v = s_add(v, s_mul(GL[(i64)ci * ldn + j], xr[j]));
       v = warp_sum(v);
-      if (lane == 0) x[(i64)cc[ci] * ldx + col] += v;
+      if (lane == 0) x[(i64)cc[ci] * ldx + col] = s_add(x[(i64)cc[ci] * ldx + col], v);
     }
     __syncthreads();
     for (int s = tid; s < k; s += blockDim.x) xs[s] = x[(i64)skel[s] * ldx + col];
     __syncthreads();
     for (int i = tid; i < nr; i += blockDim.x) {
-      double v = xr[i];
-      for (int s = 0; s < k; ++s) v += T[(i64)i * ldn + s] * xs[s];
+      S v = xr[i];
+      for (int s = 0; s < k; ++s) v = s_add(v, s_mul(T[(i64)i * ldn + s], xs[s]));
       x[(i64)red[i] * ldx + col] = v;
     }
     __syncthreads();
@@ -189,53 +221,63 @@ __global__ void __launch_bounds__(256) apply_bwd_kernel(const BoxDev* __restrict
 }
 
 // top block: x_S <- A~_SS^-1 x_S (LU with pivots) or x_S <- A~_SS x_S
-__global__ void __launch_bounds__(1024) top_solve_kernel(const double* __restrict__ LU, i64 lda, int n,
+template <bool C>
+__global__ void __launch_bounds__(1024) top_solve_kernel(const double* __restrict__ LUd, i64 lda, int n,
                                                           const int* __restrict__ ipiv,
-                                                          const int* __restrict__ S, double* __restrict__ x,
+                                                          const int* __restrict__ Sidx, double* __restrict__ xd,
                                                           i64 ldx, int nrhs) {
-  extern __shared__ double xs[];
+  typedef typename ScalarOf<C>::T S;
+  extern __shared__ __align__(16) double xsd[];
+  S* xs = reinterpret_cast<S*>(xsd);
+  const S* LU = reinterpret_cast<const S*>(LUd);
+  S* x = reinterpret_cast<S*>(xd);
   const int tid = threadIdx.x;
   for (int col = 0; col < nrhs; ++col) {
-    for (int i = tid; i < n; i += blockDim.x) xs[i] = x[(i64)S[i] * ldx + col];
+    for (int i = tid; i < n; i += blockDim.x) xs[i] = x[(i64)Sidx[i] * ldx + col];
     __syncthreads();
     if (tid == 0)
       for (int c = 0; c < n; ++c)
         if (ipiv[c] != c) {
-          const double t = xs[c];
+          const S t = xs[c];
           xs[c] = xs[ipiv[c]];
           xs[ipiv[c]] = t;
         }
     __syncthreads();
     for (int c = 0; c < n; ++c) {  // unit lower
-      const double xc = xs[c];
-      for (int i = c + 1 + tid; i < n; i += blockDim.x) xs[i] -= LU[(i64)i * lda + c] * xc;
+      const S xc = xs[c];
+      for (int i = c + 1 + tid; i < n; i += blockDim.x) xs[i] = s_sub(xs[i], s_mul(LU[(i64)i * lda + c], xc));
       __syncthreads();
     }
     for (int c = n - 1; c >= 0; --c) {  // upper
-      if (tid == 0) xs[c] /= LU[(i64)c * lda + c];
+      if (tid == 0) xs[c] = s_div(xs[c], LU[(i64)c * lda + c]);
       __syncthreads();
-      const double xc = xs[c];
-      for (int i = tid; i < c; i += blockDim.x) xs[i] -= LU[(i64)i * lda + c] * xc;
+      const S xc = xs[c];
+      for (int i = tid; i < c; i += blockDim.x) xs[i] = s_sub(xs[i], s_mul(LU[(i64)i * lda + c], xc));
       __syncthreads();
     }
-    for (int i = tid; i < n; i += blockDim.x) x[(i64)S[i] * ldx + col] = xs[i];
+    for (int i = tid; i < n; i += blockDim.x) x[(i64)Sidx[i] * ldx + col] = xs[i];
     __syncthreads();
   }
 }
 
-__global__ void __launch_bounds__(1024) top_apply_kernel(const double* __restrict__ A, i64 lda, int n,
-                                                          const int* __restrict__ S, double* __restrict__ x,
+template <bool C>
+__global__ void __launch_bounds__(1024) top_apply_kernel(const double* __restrict__ Ad, i64 lda, int n,
+                                                          const int* __restrict__ Sidx, double* __restrict__ xd,
                                                           i64 ldx, int nrhs) {
-  extern __shared__ double xs[];
+  typedef typename ScalarOf<C>::T S;
+  extern __shared__ __align__(16) double xsd[];
+  S* xs = reinterpret_cast<S*>(xsd);
+  const S* A = reinterpret_cast<const S*>(Ad);
+  S* x = reinterpret_cast<S*>(xd);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int col = 0; col < nrhs; ++col) {
-    for (int i = tid; i < n; i += blockDim.x) xs[i] = x[(i64)S[i] * ldx + col];
+    for (int i = tid; i < n; i += blockDim.x) xs[i] = x[(i64)Sidx[i] * ldx + col];
     __syncthreads();
     for (int i = warp; i < n; i += blockDim.x / 32) {
-      double v = 0.0;
-      for (int j = lane; j < n; j += 32) v += A[(i64)i * lda + j] * xs[j];
+      S v = s_zero(S());
+      for (int j = lane; j < n; j += 32) v = s_add(v, s_mul(A[(i64)i * lda + j], xs[j]));
       v = warp_sum(v);
-      if (lane == 0) x[(i64)S[i] * ldx + col] = v;
+      if (lane == 0) x[(i64)Sidx[i] * ldx + col] = v;
     }
     __syncthreads();
   }

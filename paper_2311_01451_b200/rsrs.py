@@ -219,14 +219,29 @@ class Factorization:
             self._h = None
 
 
+def _dtype_code(t) -> int:
+    import torch
+    if t.dtype == torch.float64:
+        return RSRS_F64
+    if t.dtype == torch.complex128:
+        return RSRS_C128
+    raise ValueError(f"unsupported dtype {t.dtype} (float64 or complex128)")
+
+
 def factor(tree: Tree, Y, Z, Omega, Psi, p: int, eps: float = 1e-6, level_growth: float = 1.0,
            id_scale: float = 1.0, oversample: int = 10, top_level: int = 2, stream=None,
-           dtype: int = RSRS_F64, profile: bool = False) -> Factorization:
-    """rsrs_factor on CUDA tensors (N x ld, tree order); Y, Z, Omega, Psi are OVERWRITTEN."""
+           dtype: int | None = None, profile: bool = False) -> Factorization:
+    """rsrs_factor on CUDA tensors (N x ld, tree order); Y, Z, Omega, Psi are OVERWRITTEN.
+
+    float64 tensors -> RSRS_F64, complex128 -> RSRS_C128 (ld in elements)."""
     ld = Y.stride(0)
+    code = _dtype_code(Y)
     for t in (Z, Omega, Psi):
-        if t.stride(0) != ld:
-            raise ValueError("Y, Z, Omega, Psi must share the leading dimension")
+        if t.stride(0) != ld or t.dtype != Y.dtype:
+            raise ValueError("Y, Z, Omega, Psi must share dtype and leading dimension")
+    if dtype is not None and dtype != code:
+        raise ValueError("dtype does not match the tensors")
+    dtype = code
     o = Opts(eps, level_growth, id_scale, oversample, top_level, 0, 1, None, _stream_ptr(stream), int(profile))
     h = _vp()
     _check(_lib.rsrs_factor(tree.handle, dtype, int(p), _ptr(Y), _ptr(Z), _ptr(Omega), _ptr(Psi), int(ld),
@@ -238,7 +253,7 @@ def factor(tree: Tree, Y, Z, Omega, Psi, p: int, eps: float = 1e-6, level_growth
 # harness operator (libsampler.so, include/rsrs_sampler.h) -- not the factor path
 # ----------------------------------------------------------------------------
 _sampler = None
-KERNEL_KIND = {"log2d": 0, "lap3d": 1}
+KERNEL_KIND = {"log2d": 0, "lap3d": 1, "helm2d": 2}
 
 
 def _sampler_lib():
@@ -250,19 +265,27 @@ def _sampler_lib():
         s.rsrs_sample_matvec.argtypes = [_i32, _vp, _i64, _d, _vp, _i64, _vp, _i64, _i64, _i32, _vp]
         s.rsrs_sample_matvec.restype = ctypes.c_int
         s.rsrs_sampler_last_error.restype = ctypes.c_char_p
+        s.rsrs_sample_matvec_c128.argtypes = [_vp, _i64, _d, _d, _vp, _i64, _vp, _i64, _i64, _i32, _vp]
+        s.rsrs_sample_matvec_c128.restype = ctypes.c_int
         _sampler = s
     return _sampler
 
 
-def sample_matvec(kind: str, pts3, weight: float, X, Y, adjoint: bool = False, stream=None):
-    """Y = A X with the on-the-fly kernel operator (device tensors; pts3 N x 3)."""
+def sample_matvec(kind: str, pts3, weight: float, X, Y, adjoint: bool = False, stream=None, kappa: float = 25.0):
+    """Y = A X with the on-the-fly kernel operator (device tensors; pts3 N x 3).
+
+    helm2d is complex (X, Y complex128); the others are real (float64)."""
     s = _sampler_lib()
     N = pts3.shape[0]
     ncol = 1 if X.dim() == 1 else X.shape[1]
     ldx = 1 if X.dim() == 1 else X.stride(0)
     ldy = 1 if Y.dim() == 1 else Y.stride(0)
-    st = s.rsrs_sample_matvec(KERNEL_KIND[kind], _ptr(pts3), N, float(weight), _ptr(X), ldx, _ptr(Y), ldy, ncol,
-                              int(adjoint), _stream_ptr(stream))
+    if kind == "helm2d":
+        st = s.rsrs_sample_matvec_c128(_ptr(pts3), N, float(weight), float(kappa), _ptr(X), ldx, _ptr(Y), ldy,
+                                       ncol, int(adjoint), _stream_ptr(stream))
+    else:
+        st = s.rsrs_sample_matvec(KERNEL_KIND[kind], _ptr(pts3), N, float(weight), _ptr(X), ldx, _ptr(Y), ldy,
+                                  ncol, int(adjoint), _stream_ptr(stream))
     if st != 0:
         raise RSRSError(st, s.rsrs_sampler_last_error().decode())
     return Y

@@ -39,7 +39,7 @@ def _parity(cfg, X, root, p=None, check_apply=True):
     # |S| and the step count follow from the ranks
     assert abs(st["top_size"] - f_or.S.shape[0]) <= 2 * len(t_or.levels[2].keys)
     if check_apply:
-        v = W.gaussian(X.shape[0], 99, 7)
+        v = W.gaussian(X.shape[0], 99, 7, cfg.is_complex)
         y_g = gpu_apply(f_g, v)
         y_or = O.apply(f_or, v)
         assert np.linalg.norm(y_g - y_or) / np.linalg.norm(y_or) <= 10 * eps
@@ -58,6 +58,21 @@ def test_c1_parity():
     # identical ranks -> identical stored-scalar count (Table 1 'M')
     if all(v == 0 for v in out["ranks"].values()) and st["top_size"] == out["f_or"].S.shape[0]:
         assert st["memory_scalars"] == out["f_or"].memory()
+
+
+def test_c4_family_parity_complex128():
+    """c4's complex Helmholtz operator (kappa = 25, complex128) on the c1-size grid (N = 4096):
+    complex DMMA GEMMs, Hermitian Cholesky / pivoted Gram ID, complex LU, conjugate
+    sample updates (RSRS_C128 path)."""
+    cfg = W.CONFIGS["c4"].scaled(64)
+    out = _parity(cfg, None, cfg.root())
+    assert out["stats"]["L"] == 3
+
+
+def test_c4_family_tails_complex128():
+    """complex128 with p and box sizes off the tile multiples."""
+    cfg = W.Config("tail_c", "grid2d", 50, "helm2d", "c128", leaf=37, p=650, seed=15, g=2.0)
+    _parity(cfg, None, cfg.root())
 
 
 def test_ragged_clustered_points():
@@ -133,16 +148,22 @@ def test_sampler_rows_match_direct_sum():
     import torch
 
     import paper_2311_01451_b200 as R
-    for cfg in (W.CONFIGS["c1"], W.CONFIGS["c3"].scaled(5000)):
+    for cfg in (W.CONFIGS["c1"], W.CONFIGS["c3"].scaled(5000), W.CONFIGS["c4"].scaled(70)):
         X = W.points(cfg)
         N = X.shape[0]
         pts = np.zeros((N, 3))
         pts[:, :X.shape[1]] = X
-        V = W.gaussian((N, 70), 3, 0)
-        Yd = torch.empty((N, 70), dtype=torch.float64, device="cuda:0")
-        R.sample_matvec(cfg.kernel, torch.from_numpy(pts).cuda(), W.kernel_weight(cfg),
-                        torch.from_numpy(V).cuda(), Yd)
-        rows = np.random.default_rng(1).choice(N, 64, replace=False)
-        ref = W.kernel_block(cfg, X, rows, np.arange(N)) @ V
-        got = Yd.cpu().numpy()[rows]
-        assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max() * math.sqrt(N)
+        V = W.gaussian((N, 70), 3, 0, cfg.is_complex)
+        dt = torch.complex128 if cfg.is_complex else torch.float64
+        for adjoint in (False, True):
+            Yd = torch.empty((N, 70), dtype=dt, device="cuda:0")
+            R.sample_matvec(cfg.kernel, torch.from_numpy(pts).cuda(), W.kernel_weight(cfg),
+                            torch.from_numpy(V).cuda(), Yd, adjoint=adjoint, kappa=cfg.kappa)
+            rows = np.random.default_rng(1).choice(N, 64, replace=False)
+            Ab = W.kernel_block(cfg, X, rows, np.arange(N))
+            # A^* rows = conj(A) rows for these symmetric kernels
+            ref = (Ab.conj() if adjoint else Ab) @ V
+            got = Yd.cpu().numpy()[rows]
+            # CUDA's j0/y0 are accurate to a few ulp; log / rsqrt to ~1 ulp
+            tol = (1e-12 if cfg.is_complex else 1e-13) * np.abs(ref).max() * math.sqrt(N)
+            assert np.abs(got - ref).max() <= tol, (cfg.name, adjoint)

@@ -1,0 +1,10 @@
+set -x
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?"
+tail -5 gpurun_out/pytest_gpu.log
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench exit $?"
+tail -c 3000 gpurun_out/bench.json
+CFG=c3 RUNS=1216:2 ITERS=2 timeout 900 python tools/quick_c2.py > gpurun_out/c3.log 2>&1; echo "c3 exit $?"
+tail -30 gpurun_out/c3.log

@@ -24,8 +24,8 @@ pts = np.zeros((N, 3)); pts[:, :X.shape[1]] = X
 pts_d = torch.from_numpy(pts[perm]).to(dev)
 Y_d = torch.empty_like(Om_d); Z_d = torch.empty_like(Ps_d)
 torch.cuda.synchronize(); t0 = time.time()
-R.sample_matvec(cfg.kernel, pts_d, W.kernel_weight(cfg), Om_d, Y_d)
-R.sample_matvec(cfg.kernel, pts_d, W.kernel_weight(cfg), Ps_d, Z_d, adjoint=True)
+R.sample_matvec(cfg.kernel, pts_d, W.kernel_weight(cfg), Om_d, Y_d, kappa=cfg.kappa)
+R.sample_matvec(cfg.kernel, pts_d, W.kernel_weight(cfg), Ps_d, Z_d, adjoint=True, kappa=cfg.kappa)
 torch.cuda.synchronize(); print("sample", time.time() - t0, flush=True)
 src = [Y_d, Z_d, Om_d, Ps_d]
 work = [x.clone() for x in src]
@@ -46,7 +46,7 @@ for (pf, g) in runs:
               f"DOF/s {N/(t1-t0):.3e}, model {st['flops_model']/1e12:.2f} TF, {st['flops_model']/(st['factor_ms']*1e-3)/1e12:.2f} TF/s", flush=True)
     else:
         ax = torch.empty_like(x)
-        R.sample_matvec(cfg.kernel, pts_d, W.kernel_weight(cfg), x[P].contiguous().view(N, 1), ax.view(N, 1))
+        R.sample_matvec(cfg.kernel, pts_d, W.kernel_weight(cfg), x[P].contiguous().view(N, 1), ax.view(N, 1), kappa=cfg.kappa)
         res = (ax - b[P]).norm() / b.norm()
         ks = []
         for lev in range(t.L, 1, -1):
