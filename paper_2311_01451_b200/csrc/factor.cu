@@ -21,13 +21,16 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <sstream>
 #include <string>
 #include <vector>
 
+#include "arena.h"
 #include "common.cuh"
 #include "chol.cuh"
 #include "dense.cuh"
@@ -64,6 +67,24 @@ constexpr int SMEM_MAX = 227 * 1024 - 1024;  // dynamic-smem budget of the large
 
 int g_optin = 0;
 bool g_debug = false;  // RSRS_DEBUG_SYNC=1: synchronize and check after every launch
+bool g_trace = false;  // RSRS_TRACE=1: host-side time split of rsrs_factor on stderr
+
+// host-side time split of one rsrs_factor (RSRS_TRACE)
+struct HostTrace {
+  double alloc = 0, sync = 0;
+  int nalloc = 0, nsync = 0;
+  size_t alloc_bytes = 0;
+};
+HostTrace g_ht;
+inline double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+void stream_sync(cudaStream_t s) {
+  const double t0 = now_s();
+  CK(cudaStreamSynchronize(s));
+  g_ht.sync += now_s() - t0;
+  g_ht.nsync++;
+}
 
 template <class K>
 void set_smem(K kern, int want) {
@@ -95,6 +116,8 @@ void init_kernels() {
   if (done) return;
   const char* dbg = getenv("RSRS_DEBUG_SYNC");
   g_debug = dbg && dbg[0] == '1';
+  const char* tr = getenv("RSRS_TRACE");
+  g_trace = tr && tr[0] == '1';
   int dev = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&g_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
@@ -104,15 +127,12 @@ void init_kernels() {
   set_smem(rsrs::gemm_nn_kernel_c, rsrs::NN_SMEM);
   set_smem_both<false>();
   set_smem_both<true>();
-  // keep freed stream-ordered memory in the pool (repeated factorizations reuse it)
-  cudaMemPool_t pool;
-  CK(cudaDeviceGetDefaultMemPool(&pool, dev));
-  uint64_t thr = UINT64_MAX;
-  CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
   done = true;
 }
 
-// device buffer, stream-ordered
+// device buffer from the library arena (arena.h).  release() first waits for
+// the stream the buffer was used on, so a freed block is never reused while a
+// queued kernel still touches it (also on the exception path).
 struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
@@ -122,12 +142,14 @@ struct DBuf {
     s = st;
     bytes = b;
     if (b) {
-      cudaError_t e = cudaMallocAsync(&p, b, st);
-      if (e != cudaSuccess) {
-        p = nullptr;
+      const double t0 = now_s();
+      p = rsrs::Arena::get().alloc(b);
+      g_ht.alloc += now_s() - t0;
+      g_ht.nalloc++;
+      g_ht.alloc_bytes += b;
+      if (!p) {
         bytes = 0;
-        throw StatusError{RSRS_ERR_NOMEM, std::string("device allocation of ") + std::to_string(b) +
-                                              " bytes failed: " + cudaGetErrorString(e)};
+        throw StatusError{RSRS_ERR_NOMEM, std::string("device allocation of ") + std::to_string(b) + " bytes failed"};
       }
     }
   }
@@ -135,7 +157,10 @@ struct DBuf {
     if (b > bytes) alloc(b, st);
   }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p) {
+      cudaStreamSynchronize(s);
+      rsrs::Arena::get().free(p);
+    }
     p = nullptr;
     bytes = 0;
   }
@@ -391,7 +416,7 @@ struct Planner {
       for (int64_t i = 0; i < T.N; ++i) h[i] = (int)i;
       leaf_gidx.alloc(sizeof(int) * T.N, s);
       CK(cudaMemcpyAsync(leaf_gidx.p, h.data(), sizeof(int) * T.N, cudaMemcpyHostToDevice, s));
-      CK(cudaStreamSynchronize(s));
+      stream_sync(s);
     }
     int* gidx = leaf_gidx.as<int>();
     int64_t nrows = T.N;
@@ -508,7 +533,7 @@ struct Planner {
         }
         CK(cudaMemcpyAsync(diws, hint.data(), sizeof(int) * ioff, cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(dboxes, hb.data(), sizeof(BoxDev) * hb.size(), cudaMemcpyHostToDevice, s));
-        CK(cudaStreamSynchronize(s));
+        stream_sync(s);
       }
 
       // ---- descriptors (sizes that depend on the near set point at BoxDev::r / nr / nc / k)
@@ -611,7 +636,7 @@ struct Planner {
       const size_t o_chol = put(chol.data(), sizeof(CholDesc) * chol.size());
       descbuf.ensure(hdesc.size() + 16, s);
       CK(cudaMemcpyAsync(descbuf.p, hdesc.data(), hdesc.size(), cudaMemcpyHostToDevice, s));
-      CK(cudaStreamSynchronize(s));
+      stream_sync(s);
       const char* dd = descbuf.as<char>();
       const NTDesc* Dgram = reinterpret_cast<const NTDesc*>(dd + o_gram);
       const NTDesc* Dh = reinterpret_cast<const NTDesc*>(dd + o_h);
@@ -671,7 +696,7 @@ struct Planner {
         toc();
       }
       CK(cudaMemcpyAsync(hb.data(), dboxes, sizeof(BoxDev) * hb.size(), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
+      stream_sync(s);
       flush_prof();
       std::vector<int> newk(nbox, 0);
       f->ranks[lev].assign(nbox, -1);
@@ -743,7 +768,7 @@ struct Planner {
         post("compact_kernel", s, launches);
         toc();
         account(KC_MISC, 0.0, 2.0 * 4 * nnew * p * sS);
-        CK(cudaStreamSynchronize(s));
+        stream_sync(s);
         flush_prof();
       }
       Y = nY; Z = nZ; Om = nO; Ps = nP; ld = nld;
@@ -806,7 +831,7 @@ struct Planner {
     const size_t oc = (sizeof(hd) + 15) & ~size_t(15);
     std::memcpy(h.data() + oc, &cd, sizeof(cd));
     CK(cudaMemcpyAsync(dbuf.p, h.data(), oc + sizeof(cd), cudaMemcpyHostToDevice, s));
-    CK(cudaStreamSynchronize(s));
+    stream_sync(s);
     const NTDesc* dnt = dbuf.as<NTDesc>();
     const CholDesc* dch = reinterpret_cast<const CholDesc*>(dbuf.as<char>() + oc);
     tic(KC_MISC);
@@ -822,7 +847,7 @@ struct Planner {
     toc();
     int hst[4];
     CK(cudaMemcpyAsync(hst, dstat, sizeof(hst), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    stream_sync(s);
     flush_prof();
     if (hst[0] != 0)
       throw StatusError{RSRS_ERR_SINGULAR, hst[0] == rsrs::ST_SINGULAR_GRAM ? "top block: Gram of Omega_S not positive definite"
@@ -889,6 +914,8 @@ rsrs_status rsrs_factor(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, void* Z,
     f->keep.back()->alloc(sizeof(int64_t) * T.N, s);
     f->d_perm = f->keep.back()->as<int64_t>();
     CK(cudaMemcpyAsync(f->d_perm, T.perm.data(), sizeof(int64_t) * T.N, cudaMemcpyHostToDevice, s));
+    g_ht = HostTrace();
+    const double th0 = now_s();
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
@@ -909,6 +936,10 @@ rsrs_status rsrs_factor(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, void* Z,
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     f->stats.factor_ms = ms;
+    if (g_trace)
+      fprintf(stderr, "[rsrs trace] factor: host %.1f ms, device %.1f ms, alloc %.1f ms (%d calls, %.2f GB), sync-wait %.1f ms (%d), launches %lld\n",
+              1e3 * (now_s() - th0), ms, 1e3 * g_ht.alloc, g_ht.nalloc, g_ht.alloc_bytes / 1e9, 1e3 * g_ht.sync,
+              g_ht.nsync, (long long)P.launches);
     f->stats.solve_launches = 2 + 2 * (int64_t)f->batches.size() + (f->nS > 0 ? 1 : 0);
     *out = f;
     return RSRS_OK;
@@ -1049,8 +1080,19 @@ rsrs_status rsrs_factor_top(rsrs_factorization f, int64_t* S, int64_t cap, int64
 
 void rsrs_factor_destroy(rsrs_factorization f) {
   if (!f) return;
-  cudaStreamSynchronize(f->stream);
+  cudaDeviceSynchronize();   // solves may run on any stream; the arena reuses freed blocks at once
   delete f;
+}
+
+void rsrs_release_memory(void) {
+  cudaDeviceSynchronize();
+  rsrs::Arena::get().release_idle();
+}
+
+rsrs_status rsrs_memory_info(int64_t* reserved, int64_t* in_use) {
+  if (reserved) *reserved = (int64_t)rsrs::Arena::get().reserved();
+  if (in_use) *in_use = (int64_t)rsrs::Arena::get().in_use();
+  return RSRS_OK;
 }
 
 }  // extern "C"

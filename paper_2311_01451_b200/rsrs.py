@@ -32,7 +32,7 @@ EXPORTS = [
     "rsrs_build_tree", "rsrs_tree_info", "rsrs_tree_perm", "rsrs_tree_level_size", "rsrs_tree_level",
     "rsrs_plan_samples", "rsrs_tree_destroy", "rsrs_factor", "rsrs_solve", "rsrs_apply",
     "rsrs_factor_stats", "rsrs_factor_ranks", "rsrs_factor_top", "rsrs_factor_destroy", "rsrs_factor_profile",
-    "rsrs_last_error", "rsrs_version",
+    "rsrs_last_error", "rsrs_version", "rsrs_memory_info", "rsrs_release_memory",
 ]
 
 
@@ -96,6 +96,24 @@ def _check(st: int):
 
 def version() -> str:
     return _lib.rsrs_version().decode()
+
+
+_lib.rsrs_memory_info.argtypes = [ctypes.POINTER(_i64), ctypes.POINTER(_i64)]
+_lib.rsrs_memory_info.restype = ctypes.c_int
+_lib.rsrs_release_memory.argtypes = []
+_lib.rsrs_release_memory.restype = None
+
+
+def memory_info() -> dict:
+    """Bytes of device memory the library's arena holds (reserved) and uses."""
+    r, u = _i64(), _i64()
+    _check(_lib.rsrs_memory_info(ctypes.byref(r), ctypes.byref(u)))
+    return {"reserved": r.value, "in_use": u.value}
+
+
+def release_memory() -> None:
+    """Return the arena's idle chunks to the driver (synchronises the device)."""
+    _lib.rsrs_release_memory()
 
 
 def _ptr(t) -> int:

@@ -36,7 +36,9 @@ for (pf, g) in runs:
         for w_, s_ in zip(work, src): w_.copy_(s_)
         torch.cuda.synchronize(); t0 = time.time()
         try:
-            f = R.factor(t, *work, p=p, eps=cfg.eps, level_growth=g, profile=(it == ITERS - 1))
+            prof = os.environ.get("PROF", "last")
+            f = R.factor(t, *work, p=p, eps=cfg.eps, level_growth=g,
+                         profile=(prof == "all" or (prof == "last" and it == ITERS - 1)))
         except R.RSRSError as e:
             print(f"p={p} g={g}: {e}", flush=True); break
         torch.cuda.synchronize(); t1 = time.time()
