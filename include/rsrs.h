@@ -57,11 +57,13 @@ typedef struct {
   double id_scale;     /* c_id (default 1.0) */
   int oversample;      /* l: require p - r >= k + l (default 10) */
   int top_level;       /* last compressed level ("typically on level 2") */
-  int rank;            /* this process's rank; must be 0 in this build */
-  int nranks;          /* number of ranks; must be 1 in this build (RSRS_ERR_STATE otherwise) */
-  void* nccl_comm;     /* reserved (ncclComm_t), must be NULL */
+  int rank;            /* this process's rank (0 .. nranks-1) */
+  int nranks;          /* number of ranks (one process per GPU); 1 = single GPU */
+  void* nccl_comm;     /* ncclComm_t from rsrs_comm_init when nranks > 1, else NULL */
   void* stream;        /* cudaStream_t the factorization runs on (NULL = legacy default stream) */
   int profile;         /* 1: time every kernel class with CUDA events on `stream` (rsrs_factor_profile) */
+  int gather_level;    /* multi-GPU: boxes on levels <= gather_level are gathered on rank 0 (-1: auto,
+                          the largest level with <= 16 * nranks boxes; always >= top_level - 1) */
 } rsrs_opts;
 
 /* Statistics of a factorization (Table 1). */
@@ -176,6 +178,63 @@ rsrs_status rsrs_factor_ranks(rsrs_factorization f, int level, int32_t* k, int64
 rsrs_status rsrs_factor_top(rsrs_factorization f, int64_t* S, int64_t cap, int64_t* size);
 
 void rsrs_factor_destroy(rsrs_factorization f);
+
+/* ---------------------------------------------------------------------------
+ * Multi-GPU (BASELINE.json north_star): one process per GPU.
+ * Leaves are split into nranks Morton-contiguous ranges of about equal work
+ * (rsrs_tree_partition); rank q owns the boxes whose first point lies in its
+ * range, and boxes on levels <= gather_level belong to rank 0 (the coarse
+ * levels and the top block A~_SS run there).  Per (level, colour) the sweep
+ * fetches the active Y, Z, Omega, Psi rows of foreign neighbour boxes, updates
+ * the foreign Y/Z rows in place and returns them (one writer per row: boxes of
+ * one colour have disjoint near sets, R10); skeleton rows move to the
+ * owner of their parent between levels.  Transport: NCCL point-to-point and
+ * all-reduce on the communicator passed in rsrs_opts.nccl_comm.
+ *
+ * With nranks > 1, rsrs_factor takes THIS RANK's rows: Y, Z, Omega, Psi hold
+ * tree positions [first[rank], first[rank+1]) (N_loc x ld).  rsrs_solve /
+ * rsrs_apply take the FULL right-hand side, replicated on every rank, and leave
+ * the full result on every rank (touched rows merged by an all-reduce after each
+ * colour batch).  Every rank must make the same calls.
+ * ------------------------------------------------------------------------- */
+
+/* Partition of the leaves for nranks ranks: first[nranks + 1] tree positions
+ * (host int64), and the gather level actually used (gather_level < 0: auto). */
+rsrs_status rsrs_tree_partition(rsrs_tree t, int nranks, int gather_level, int top_level, int64_t* first,
+                                int* gather_out);
+
+/* Owner rank of every box of `level` (host int32[nboxes]). */
+rsrs_status rsrs_dist_owner(rsrs_tree t, int nranks, int gather_level, int top_level, int level, int32_t* owner);
+
+/* Host views of the exchange plans (what rsrs_factor executes), for tests and
+ * tooling.  Records of 4 int32 {kind (0 send, 1 recv), peer, box, rows}, in the
+ * order the rows travel; cap = record capacity of out, *len = records needed.
+ *   halo plan of (level, colour) on `rank`: nb[box] = active rows of every box of
+ *     the level, cnt[box] = rows a neighbour sees (skeletons once processed);
+ *   move plan of `level` -> level-1 on `rank`: k[box] = skeleton count. */
+rsrs_status rsrs_dist_halo_plan(rsrs_tree t, int nranks, int gather_level, int top_level, int level, int colour,
+                                const int32_t* nb, const int32_t* cnt, int rank, int32_t* out, int64_t cap,
+                                int64_t* len);
+rsrs_status rsrs_dist_move_plan(rsrs_tree t, int nranks, int gather_level, int top_level, int level,
+                                const int32_t* k, int rank, int32_t* out, int64_t cap, int64_t* len);
+
+/* NCCL communicator: rank 0 calls rsrs_comm_unique_id (128 bytes, host), the
+ * caller broadcasts it (e.g. over torch.distributed), every rank calls
+ * rsrs_comm_init.  NCCL is loaded at run time (libnccl.so.2); RSRS_ERR_NCCL if absent. */
+rsrs_status rsrs_comm_unique_id(void* id128);
+rsrs_status rsrs_comm_init(int nranks, int rank, const void* id128, void** comm);
+void rsrs_comm_destroy(void* comm);
+
+/* Single-GPU emulation of a G-rank run (validation of the multi-GPU path on one
+ * device): G host threads, one per rank, each with its own stream, exchanging
+ * through device-to-device copies; no kernel waits on another.  Y, Z, Omega, Psi
+ * are the FULL tree-ordered arrays (N x ld; overwritten); out receives G handles
+ * (rank order).  rsrs_solve_emulated / rsrs_apply_emulated run the distributed
+ * sweep over the G handles on the full B (original order, overwritten). */
+rsrs_status rsrs_factor_emulated(rsrs_tree t, rsrs_dtype dt, int64_t p, int G, void* Y, void* Z, void* Omega,
+                                 void* Psi, int64_t ld, const rsrs_opts* opts, rsrs_factorization* out);
+rsrs_status rsrs_solve_emulated(rsrs_factorization* fs, int G, void* B, int64_t ldb, int64_t nrhs);
+rsrs_status rsrs_apply_emulated(rsrs_factorization* fs, int G, void* X, int64_t ldx, int64_t nrhs);
 
 /* Device memory of the library: rsrs_factor draws its workspace and the factor
  * storage from a process-wide arena of cudaMalloc'ed chunks that is kept between

@@ -5,5 +5,5 @@ sweep -- lives in librsrs.so (hand-written sm_100a CUDA behind the C ABI
 include/rsrs.h).  This package is a thin ctypes binding over it.
 """
 from .rsrs import (Tree, Factorization, factor, RSRSError, version, sample_matvec, memory_info,  # noqa: F401
-                   release_memory,
+                   release_memory, NcclComm, factor_emulated, solve_emulated, apply_emulated,
                    RSRS_F64, RSRS_C128, EXPORTS, LIB_PATH, SAMPLER_PATH)

@@ -375,12 +375,14 @@ __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ bo
 // (R2).  Neighbours processed by an earlier
 // colour contribute only their skeleton rows (their redundant rows are
 // decoupled); the others contribute all their rows.
+// Records {boxdev index or -1, first row, count}: a foreign neighbour on the
+// multi-GPU path is a contiguous halo block holding exactly its active rows.
 // ---------------------------------------------------------------------------
 __global__ void build_near_kernel(BoxDev* __restrict__ boxes, const BoxDev* __restrict__ level_boxes,
-                                  int* __restrict__ iws, int p, int oversample) {
+                                  int* __restrict__ iws, const int* __restrict__ nbrrec, int p, int oversample) {
   BoxDev& b = boxes[blockIdx.x];
   const int lane = threadIdx.x;
-  const int* nd = iws + b.off_nbr;
+  const int* nd = nbrrec + b.off_nbr;
   int* near = iws + b.off_rows;
   int o = 0, selfp = 0;
   for (int q = 0; q < b.nnbr; ++q) {
@@ -421,6 +423,7 @@ __global__ void compact_kernel(const BoxDev* __restrict__ boxes, const int* __re
   const int k = b.k;
   const int* skelrow = iws + b.off_skelrow;
   const int base = dst_row0[blockIdx.x];
+  if (base < 0) return;                    // skeletons move to another rank (dist.h plan_moves)
   for (int s = blockIdx.y; s < k; s += gridDim.y) {
     const int src = skelrow[s];
     const int dst = base + s;
@@ -517,6 +520,113 @@ __global__ void __launch_bounds__(1024) top_lu_kernel(double* __restrict__ Ad, i
     }
     __syncthreads();
   }
+}
+
+}  // namespace rsrs
+
+// ---------------------------------------------------------------------------
+// Multi-GPU data movement (dist.h plans): flat row lists, row gathers into
+// message buffers and scatters back.  A message holds `narr` sections of n rows
+// x w doubles (Y, Z[, Omega, Psi]) followed, optionally, by the n tree
+// positions (as doubles, exact below 2^53).
+// ---------------------------------------------------------------------------
+namespace rsrs {
+
+// recs[i] = {boxdev index (>= 0: the box's skeleton rows) or -1 (rows row0 ..), row0, count, out offset}
+__global__ void rowlist_kernel(const BoxDev* __restrict__ boxes, const int* __restrict__ iws,
+                               const int4* __restrict__ recs, int* __restrict__ out) {
+  const int4 r = recs[blockIdx.x];
+  if (r.x >= 0) {
+    const int* src = iws + boxes[r.x].off_skelrow;
+    for (int t = threadIdx.x; t < r.z; t += blockDim.x) out[r.w + t] = src[t];
+  } else {
+    for (int t = threadIdx.x; t < r.z; t += blockDim.x) out[r.w + t] = r.y + t;
+  }
+}
+
+// out[a][i][:] = A_a[rows[i]][:w] ; out_g[i] = gidx[rows[i]]   (rows == nullptr: row0 + i)
+__global__ void gather_rows_kernel(const double* __restrict__ A0, const double* __restrict__ A1,
+                                   const double* __restrict__ A2, const double* __restrict__ A3, i64 ldd,
+                                   const int* __restrict__ gidx, const int* __restrict__ rows, int row0, int n,
+                                   int w, int narr, int with_gidx, double* __restrict__ out) {
+  const int i = blockIdx.x, a = blockIdx.y;
+  if (i >= n) return;
+  const int row = rows ? rows[i] : row0 + i;
+  if (a < narr) {
+    const double* A = a == 0 ? A0 : a == 1 ? A1 : a == 2 ? A2 : A3;
+    const double* src = A + (i64)row * ldd;
+    double* dst = out + ((i64)a * n + i) * w;
+    for (int j = threadIdx.x; j < w; j += blockDim.x) dst[j] = src[j];
+  } else if (with_gidx && threadIdx.x == 0) {
+    out[(i64)narr * n * w + i] = (double)gidx[row];
+  }
+}
+
+// A_a[rows[i]][:w] = in[a][i][:] ; gidx[rows[i]] = in_g[i]
+__global__ void scatter_rows_kernel(const double* __restrict__ in, double* __restrict__ A0, double* __restrict__ A1,
+                                    double* __restrict__ A2, double* __restrict__ A3, i64 ldd,
+                                    int* __restrict__ gidx, const int* __restrict__ rows, int row0, int n, int w,
+                                    int narr, int with_gidx) {
+  const int i = blockIdx.x, a = blockIdx.y;
+  if (i >= n) return;
+  const int row = rows ? rows[i] : row0 + i;
+  if (a < narr) {
+    double* A = a == 0 ? A0 : a == 1 ? A1 : a == 2 ? A2 : A3;
+    double* dst = A + (i64)row * ldd;
+    const double* src = in + ((i64)a * n + i) * w;
+    for (int j = threadIdx.x; j < w; j += blockDim.x) dst[j] = src[j];
+  } else if (with_gidx && threadIdx.x == 0) {
+    gidx[row] = (int)in[(i64)narr * n * w + i];
+  }
+}
+
+// solve merge: rows a box touched (lists of tree positions in the factor's index
+// pool) -> contrib[pos] = x[pos], mask[pos] = 1.  which: 0 = red and c
+// (forward / apply-backward), 1 = red and skel (backward / apply-forward).
+__global__ void mark_rows_kernel(const BoxDev* __restrict__ boxes, const int* __restrict__ ipool,
+                                 const double* __restrict__ x, i64 ldx, int w, double* __restrict__ contrib,
+                                 double* __restrict__ mask, int which) {
+  const BoxDev& b = boxes[blockIdx.x];
+  if (b.nr <= 0) return;
+  const int* l1 = ipool + b.f_red;
+  const int n1 = b.nr;
+  const int* l2 = ipool + (which == 0 ? b.f_c : b.f_skel);
+  const int n2 = which == 0 ? b.nc : b.k;
+  for (int t = threadIdx.x; t < (n1 + n2) * w; t += blockDim.x) {
+    const int i = t / w, j = t % w;
+    const int pos = i < n1 ? l1[i] : l2[i - n1];
+    contrib[(i64)pos * w + j] = x[(i64)pos * ldx + j];
+    if (j == 0) mask[pos] = 1.0;
+  }
+}
+
+__global__ void mark_list_kernel(const int* __restrict__ list, int n, const double* __restrict__ x, i64 ldx, int w,
+                                 double* __restrict__ contrib, double* __restrict__ mask) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n * w; t += gridDim.x * blockDim.x) {
+    const int i = t / w, j = t % w;
+    const int pos = list[i];
+    contrib[(i64)pos * w + j] = x[(i64)pos * ldx + j];
+    if (j == 0) mask[pos] = 1.0;
+  }
+}
+
+// after the sum over ranks: x[pos] = contrib[pos] where some rank touched pos (exactly one did)
+__global__ void merge_finalize_kernel(int64_t N, double* __restrict__ x, i64 ldx, int w, double* __restrict__ contrib,
+                                      double* __restrict__ mask) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    if (mask[i] != 0.0) {
+      for (int j = 0; j < w; ++j) {
+        x[i * ldx + j] = contrib[i * w + j];
+        contrib[i * w + j] = 0.0;
+      }
+      mask[i] = 0.0;
+    }
+  }
+}
+
+__global__ void add_into_kernel(double* __restrict__ dst, const double* __restrict__ src, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] += src[i];
 }
 
 }  // namespace rsrs

@@ -27,12 +27,15 @@
 #include <cstring>
 #include <memory>
 #include <sstream>
+#include <thread>
 #include <string>
 #include <vector>
 
 #include "arena.h"
+#include "comm.h"
 #include "common.cuh"
 #include "chol.cuh"
+#include "dist.h"
 #include "dense.cuh"
 #include "gemm.cuh"
 #include "internal.h"
@@ -75,7 +78,7 @@ struct HostTrace {
   int nalloc = 0, nsync = 0;
   size_t alloc_bytes = 0;
 };
-HostTrace g_ht;
+thread_local HostTrace g_ht;
 inline double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -137,6 +140,7 @@ struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
   cudaStream_t s = nullptr;
+  bool devsync = false;   // factor-lifetime buffers: the stream they were last used on may be gone
   void alloc(size_t b, cudaStream_t st) {
     release();
     s = st;
@@ -158,7 +162,8 @@ struct DBuf {
   }
   void release() {
     if (p) {
-      cudaStreamSynchronize(s);
+      if (devsync) cudaDeviceSynchronize();
+      else cudaStreamSynchronize(s);
       rsrs::Arena::get().free(p);
     }
     p = nullptr;
@@ -251,6 +256,21 @@ void launch_back_any(bool cplx, const CholDesc* d, int nmat, int rmax, int mext,
 
 }  // namespace
 
+// in-process sum over the emulated ranks, in rank order (identical on every rank)
+void rsrs::InProcComm::allreduce_sum_f64(double* dev, size_t n, cudaStream_t s) {
+  hub_->dbuf(rank) = dev;
+  cudaStreamSynchronize(s);
+  hub_->barrier();
+  double* t = tmp(n);
+  cudaMemcpyAsync(t, hub_->dbuf(0), n * sizeof(double), cudaMemcpyDeviceToDevice, s);
+  for (int q = 1; q < nranks; ++q)
+    rsrs::add_into_kernel<<<592, 256, 0, s>>>(t, hub_->dbuf(q), (int64_t)n);
+  cudaStreamSynchronize(s);
+  hub_->barrier();
+  cudaMemcpyAsync(dev, t, n * sizeof(double), cudaMemcpyDeviceToDevice, s);
+  cudaStreamSynchronize(s);
+}
+
 // ---------------------------------------------------------------------------
 struct Batch {
   int level = 0, colour = 0, nbox = 0;
@@ -259,6 +279,7 @@ struct Batch {
   double* fpool = nullptr;         // the level's factor pools
   int* ipool = nullptr;
   int max_nb = 0, max_r = 0;
+  bool dist = false;               // multi-rank: merge x across ranks after the batch (solve / apply)
 };
 
 struct rsrs_factor_s {
@@ -278,7 +299,10 @@ struct rsrs_factor_s {
   int* d_piv = nullptr;
   std::vector<int64_t> S_host;
   int64_t* d_perm = nullptr;
-  DBuf xtmp;
+  DBuf xtmp, mergebuf;
+  int nranks = 1, rank = 0;                       // multi-GPU: this factor holds rank's boxes only
+  void* nccl_comm = nullptr;                      // NCCL communicator of the factorization (borrowed)
+  bool own_stream = false;                        // emulated ranks: the library created `stream`
   rsrs_stats stats{};
   cudaStream_t stream = nullptr;
   double kc_ms[RSRS_NUM_KERNEL_CLASSES] = {0};
@@ -395,77 +419,181 @@ struct Planner {
 
   DBuf* keep(size_t nbytes) {
     f->keep.emplace_back(new DBuf());
+    f->keep.back()->devsync = true;
     f->keep.back()->alloc(nbytes, s);
     return f->keep.back().get();
   }
 
-  void run(double* Y, double* Z, double* Om, double* Ps, i64 ld) {
+  // ---- multi-GPU helpers (dist.h plans; no-ops on one rank) ------------------
+  rsrs::Comm* comm = nullptr;     // nullptr: single rank
+  rsrs::Partition part;
+  int R = 1, me = 0;
+  DBuf mv_rows, mv_recs, mv_send, mv_recv;
+
+  // gather rows described by records into one message per peer (narr sections + gidx)
+  // recs: {boxdev index or -1, row0, count, offset}; returns the flat device row list (kept in `rows_out`)
+  void build_rowlist(const std::vector<int4>& recs, int nrows, const BoxDev* dboxes, const int* diws, DBuf& rows_out) {
+    rows_out.ensure(sizeof(int) * std::max(nrows, 1), s);
+    if (recs.empty() || nrows == 0) return;
+    mv_recs.ensure(sizeof(int4) * recs.size(), s);
+    CK(cudaMemcpyAsync(mv_recs.p, recs.data(), sizeof(int4) * recs.size(), cudaMemcpyHostToDevice, s));
+    rsrs::rowlist_kernel<<<(unsigned)recs.size(), 64, 0, s>>>(dboxes, diws, mv_recs.as<int4>(), rows_out.as<int>());
+    post("rowlist_kernel", s, launches);
+  }
+  void gather_rows(double* const A[4], i64 ldd, const int* gidx, const int* rows, int row0, int n, int w, int narr,
+                   bool with_g, double* out) {
+    if (n <= 0) return;
+    dim3 grid((unsigned)n, narr + (with_g ? 1 : 0));
+    rsrs::gather_rows_kernel<<<grid, 128, 0, s>>>(A[0], A[1], A[2], A[3], ldd, gidx, rows, row0, n, w, narr,
+                                                  with_g ? 1 : 0, out);
+    post("gather_rows_kernel", s, launches);
+  }
+  void scatter_rows(const double* in, double* const A[4], i64 ldd, int* gidx, const int* rows, int row0, int n,
+                    int w, int narr, bool with_g) {
+    if (n <= 0) return;
+    dim3 grid((unsigned)n, narr + (with_g ? 1 : 0));
+    rsrs::scatter_rows_kernel<<<grid, 128, 0, s>>>(in, A[0], A[1], A[2], A[3], ldd, gidx, rows, row0, n, w, narr,
+                                                   with_g ? 1 : 0);
+    post("scatter_rows_kernel", s, launches);
+  }
+  // upper bound of the halo rows of `level` over its colours (a foreign box neighbours
+  // at most one same-colour box, so no deduplication is needed)
+  int64_t halo_capacity(int level, const std::vector<int>& nb) {
+    if (R == 1 || level <= part.gather_level) return 0;
+    const rsrs::TreeLevel& lv = T.levels[level];
+    int ncol = 1;
+    for (int i = 0; i < T.d; ++i) ncol *= 3;
+    std::vector<int64_t> cap(ncol, 0);
+    for (int64_t b = 0; b < lv.nboxes; ++b) {
+      if (nb[b] <= 0 || part.owner(T, level, b) != me) continue;
+      for (int32_t q = lv.nbr_off[b]; q < lv.nbr_off[b + 1]; ++q) {
+        const int j = lv.nbr[q];
+        if (part.owner(T, level, j) != me) cap[lv.colour[b]] += nb[j];
+      }
+    }
+    return *std::max_element(cap.begin(), cap.end());
+  }
+
+  void run(double* Yu, double* Zu, double* Omu, double* Psu, i64 ldu) {
     const int sS = (int)(SC * sizeof(double));   // bytes per scalar
     const int L = T.L;
     const int p = (int)f->p;
     const int top = f->top_level;
     const i64 nld = even(p);
+    const int W = SC * p;                        // doubles per sample row
+    if (comm) {
+      R = comm->nranks;
+      me = comm->rank;
+    }
     DBuf store[2], gidx_buf[2];
     int cur = -1;
-    std::vector<int> nb_box(T.levels[L].nboxes);
+    // global active counts of the current level's boxes
+    std::vector<int> nb_all(T.levels[L].nboxes);
     for (int64_t b = 0; b < T.levels[L].nboxes; ++b)
-      nb_box[b] = (int)(T.levels[L].start[b + 1] - T.levels[L].start[b]);
+      nb_all[b] = (int)(T.levels[L].start[b + 1] - T.levels[L].start[b]);
+    // the leaf store: the caller's arrays (one rank) or a copy with halo room
+    double *Y = Yu, *Z = Zu, *Om = Omu, *Ps = Psu;
+    i64 ld = ldu;
+    int64_t nloc = T.N;
+    int64_t gfirst = 0;
+    int64_t leaf_cap = T.N;
+    if (R > 1) {
+      gfirst = part.first[me];
+      nloc = part.first[me + 1] - part.first[me];
+      leaf_cap = nloc;
+      if (L > part.gather_level) {
+        const int64_t cap = nloc + halo_capacity(L, nb_all);
+        leaf_cap = cap;
+        cur = 0;
+        store[0].ensure((size_t)sS * std::max<i64>(2, 4 * cap * nld), s);
+        double* base = store[0].as<double>();
+        double* dst[4] = {base, base + SC * cap * nld, base + 2 * SC * cap * nld, base + 3 * SC * cap * nld};
+        double* src[4] = {Yu, Zu, Omu, Psu};
+        for (int a = 0; a < 4; ++a)
+          if (nloc)
+            CK(cudaMemcpy2DAsync(dst[a], sS * nld, src[a], sS * ldu, sS * p, nloc, cudaMemcpyDeviceToDevice, s));
+        Y = dst[0]; Z = dst[1]; Om = dst[2]; Ps = dst[3];
+        ld = nld;
+      }
+    }
     DBuf leaf_gidx;
     {
-      std::vector<int> h(T.N);
-      for (int64_t i = 0; i < T.N; ++i) h[i] = (int)i;
-      leaf_gidx.alloc(sizeof(int) * T.N, s);
-      CK(cudaMemcpyAsync(leaf_gidx.p, h.data(), sizeof(int) * T.N, cudaMemcpyHostToDevice, s));
+      std::vector<int> h(std::max<int64_t>(leaf_cap, 1), 0);   // room for the halo rows' tree positions
+      for (int64_t i = 0; i < nloc; ++i) h[i] = (int)(gfirst + i);
+      leaf_gidx.alloc(sizeof(int) * h.size(), s);
+      CK(cudaMemcpyAsync(leaf_gidx.p, h.data(), sizeof(int) * nloc, cudaMemcpyHostToDevice, s));
       stream_sync(s);
     }
     int* gidx = leaf_gidx.as<int>();
-    int64_t nrows = T.N;
-    DBuf ws, iws, descbuf, dstbuf;
+    DBuf ws, iws, nbrbuf, descbuf, dstbuf, rl_send, rl_recv;
     f->ranks.assign(L + 1, std::vector<int32_t>());
+    int ncol = 1;
+    for (int i = 0; i < T.d; ++i) ncol *= 3;
 
     for (int lev = L; lev >= top && lev >= 1; --lev) {
       const rsrs::TreeLevel& lv = T.levels[lev];
       const int nbox = (int)lv.nboxes;
       const double atol = cid * eps * std::pow(g, (double)(L - lev));
-      std::vector<int> row0(nbox + 1, 0), rmaxv(nbox, 0);
-      for (int b = 0; b < nbox; ++b) row0[b + 1] = row0[b] + nb_box[b];
+      const bool dist = R > 1 && lev > part.gather_level;
+      std::vector<int> own(nbox, 0);
+      for (int b = 0; b < nbox; ++b) own[b] = part.owner(T, lev, b);
+      // local rows of my boxes (Morton order)
+      std::vector<int> row0(nbox, -1), rmaxv(nbox, 0);
+      {
+        int64_t acc = 0;
+        for (int b = 0; b < nbox; ++b)
+          if (own[b] == me) {
+            row0[b] = (int)acc;
+            acc += nb_all[b];
+          }
+        if (acc != nloc) {
+          std::ostringstream os;
+          os << "internal: level " << lev << " holds " << nloc << " rows, boxes need " << acc;
+          throw StatusError{RSRS_ERR_STATE, os.str()};
+        }
+      }
       for (int b = 0; b < nbox; ++b) {
+        if (own[b] != me) continue;
         int r = 0;
-        for (int q = lv.nbr_off[b]; q < lv.nbr_off[b + 1]; ++q) r += nb_box[lv.nbr[q]];
+        for (int q = lv.nbr_off[b]; q < lv.nbr_off[b + 1]; ++q) r += nb_all[lv.nbr[q]];
         rmaxv[b] = r;
         // per-box dense kernels keep H (n_b x n_b) and X_rr, X_rr^-1 in shared memory
-        const size_t nbz = nb_box[b];
+        const size_t nbz = nb_all[b];
         if (nbz * (nbz + 1) * sS + 3 * nbz * 4 + 64 > (size_t)SMEM_MAX ||
             2 * nbz * (nbz + 1) * sS + 3 * nbz * 4 + 64 > (size_t)SMEM_MAX) {
           std::ostringstream os;
-          os << "level " << lev << " box " << b << ": |I_b| = " << nb_box[b]
+          os << "level " << lev << " box " << b << ": |I_b| = " << nb_all[b]
              << " exceeds the shared-memory capacity of the per-box ID / LU kernels";
           throw StatusError{RSRS_ERR_INVALID, os.str()};
         }
       }
-      int ncol = 1;
-      for (int i = 0; i < T.d; ++i) ncol *= 3;
+      // colours present on the level (globally: every rank walks the same colour sequence)
+      std::vector<char> present(ncol, 0);
       std::vector<std::vector<int>> bycol(ncol);
       for (int b = 0; b < nbox; ++b)
-        if (nb_box[b] > 0) bycol[lv.colour[b]].push_back(b);
+        if (nb_all[b] > 0) {
+          present[lv.colour[b]] = 1;
+          if (own[b] == me) bycol[lv.colour[b]].push_back(b);
+        }
 
-      // ---- host layout of the level (canonical order: colour-major, Morton inside)
+      // ---- host layout of my boxes (canonical order: colour-major, Morton inside)
       std::vector<BoxDev> hb;
       hb.reserve(nbox);
       std::vector<int> hb_of(nbox, -1);
       struct BInfo {
-        int first, count, max_nb, max_r, max_m;
+        int colour, first, count, max_nb, max_r, max_m;
+        int64_t rec0, rec1;     // range of the colour's neighbour records
       };
       std::vector<BInfo> binfo;
-      i64 foff = 0, fioff = 0, ioff = 0, ws_need = 0;
+      i64 foff = 0, fioff = 0, ioff = 0, ws_need = 0, noff = 0;
       for (int c = 0; c < ncol; ++c) {
-        if (bycol[c].empty()) continue;
-        BInfo bi{(int)hb.size(), (int)bycol[c].size(), 0, 0, 0};
+        if (!present[c]) continue;
+        BInfo bi{c, (int)hb.size(), (int)bycol[c].size(), 0, 0, 0, noff, noff};
         i64 wo = 0;
         for (int b : bycol[c]) {
           BoxDev x;
           std::memset(&x, 0, sizeof(x));
-          const i64 nb = nb_box[b], r = rmaxv[b];
+          const i64 nb = nb_all[b], r = rmaxv[b];
           const i64 ldn = even(nb), ldr = even(r);
           x.nb = (int)nb;
           x.rmax = (int)r;
@@ -488,7 +616,7 @@ struct Planner {
           x.off_redrow = ioff;  ioff += nb;
           x.off_crow = ioff;    ioff += r;
           x.off_cpos = ioff;    ioff += r;
-          x.off_nbr = ioff;     ioff += 3 * x.nnbr;
+          x.off_nbr = noff;     noff += 3 * x.nnbr;
           x.f_T = foff;     foff += nb * ldn;
           x.f_GL = foff;    foff += r * ldn;
           x.f_GU = foff;    foff += nb * ldr;
@@ -503,6 +631,7 @@ struct Planner {
           bi.max_r = std::max<int>(bi.max_r, (int)r);
           bi.max_m = std::max<int>(bi.max_m, (int)(r + nb));
         }
+        bi.rec1 = noff;
         ws_need = std::max(ws_need, wo);
         binfo.push_back(bi);
       }
@@ -514,25 +643,42 @@ struct Planner {
       BoxDev* dboxes = boxes_b->as<BoxDev>();
       ws.ensure((size_t)sS * std::max<i64>(ws_need, 2), s);
       iws.ensure(sizeof(int) * std::max<i64>(ioff, 2), s);
+      nbrbuf.ensure(sizeof(int) * std::max<i64>(noff, 2), s);
       double* dws = ws.as<double>();
       int* diws = iws.as<int>();
+      int* dnbr = nbrbuf.as<int>();
+      // neighbour records {boxdev index if processed earlier, row0, nb}; foreign
+      // neighbours are filled per colour with their halo block
+      std::vector<int> hnbr(std::max<i64>(noff, 1), 0);
+      std::vector<std::pair<int, int>> foreign_slot;   // (record index, box) per my box
+      std::vector<int> fs_first(hb.size() + 1, 0);
       {
-        // b rows (static) and neighbour records {boxdev index if processed earlier, row0, nb}
         std::vector<int> hint(std::max<i64>(ioff, 1), 0);
-        for (const BoxDev& x : hb) {
+        for (size_t q = 0; q < hb.size(); ++q) {
+          const BoxDev& x = hb[q];
           const int b = x.box;
+          fs_first[q] = (int)foreign_slot.size();
           for (int t = 0; t < x.nb; ++t) hint[x.off_rows + x.rmax + t] = x.row0 + t;
           int q3 = (int)x.off_nbr;
-          for (int q = lv.nbr_off[b]; q < lv.nbr_off[b + 1]; ++q) {
-            const int j = lv.nbr[q];
-            const bool done = nb_box[j] > 0 && lv.colour[j] < lv.colour[b];
-            hint[q3++] = done ? hb_of[j] : -1;
-            hint[q3++] = row0[j];
-            hint[q3++] = nb_box[j];
+          for (int qq = lv.nbr_off[b]; qq < lv.nbr_off[b + 1]; ++qq) {
+            const int j = lv.nbr[qq];
+            if (own[j] != me) {
+              foreign_slot.push_back({q3, j});
+              hnbr[q3++] = -1;
+              hnbr[q3++] = 0;
+              hnbr[q3++] = 0;
+              continue;
+            }
+            const bool done = nb_all[j] > 0 && lv.colour[j] < lv.colour[b];
+            hnbr[q3++] = done ? hb_of[j] : -1;
+            hnbr[q3++] = row0[j];
+            hnbr[q3++] = nb_all[j];
           }
         }
+        fs_first[hb.size()] = (int)foreign_slot.size();
         CK(cudaMemcpyAsync(diws, hint.data(), sizeof(int) * ioff, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(dboxes, hb.data(), sizeof(BoxDev) * hb.size(), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(dnbr, hnbr.data(), sizeof(int) * noff, cudaMemcpyHostToDevice, s));
+        if (!hb.empty()) CK(cudaMemcpyAsync(dboxes, hb.data(), sizeof(BoxDev) * hb.size(), cudaMemcpyHostToDevice, s));
         stream_sync(s);
       }
 
@@ -635,7 +781,7 @@ struct Planner {
       const size_t o_upd = put(nn_upd.data(), sizeof(NNDesc) * nn_upd.size());
       const size_t o_chol = put(chol.data(), sizeof(CholDesc) * chol.size());
       descbuf.ensure(hdesc.size() + 16, s);
-      CK(cudaMemcpyAsync(descbuf.p, hdesc.data(), hdesc.size(), cudaMemcpyHostToDevice, s));
+      if (!hdesc.empty()) CK(cudaMemcpyAsync(descbuf.p, hdesc.data(), hdesc.size(), cudaMemcpyHostToDevice, s));
       stream_sync(s);
       const char* dd = descbuf.as<char>();
       const NTDesc* Dgram = reinterpret_cast<const NTDesc*>(dd + o_gram);
@@ -646,59 +792,174 @@ struct Planner {
       const NNDesc* Dupd = reinterpret_cast<const NNDesc*>(dd + o_upd);
       const CholDesc* Dchol = reinterpret_cast<const CholDesc*>(dd + o_chol);
 
+      // global skeleton counts of the level (-1 = not processed yet)
+      std::vector<int> k_all(nbox, -1);
+      double* const store4[4] = {Y, Z, Om, Ps};
+
       // ---- colour batches --------------------------------------------------
       for (const BInfo& bi : binfo) {
         const int n = bi.count, q0 = bi.first;
         BoxDev* dbx = dboxes + q0;
-        tic(KC_MISC);
-        rsrs::build_near_kernel<<<n, 32, 0, s>>>(dbx, dboxes, diws, p, l);
-        post("build_near_kernel", s, launches);
-        toc();
-        tic(KC_GRAM);
-        launch_nt(cplx, Dgram + 4 * q0, 4 * n, bi.max_r, bi.max_r, s, launches);
-        toc();
-        tic(KC_CHOL);
-        launch_chol_any(cplx, Dchol + 2 * q0, 2 * n, bi.max_r, bi.max_nb, s, launches);
-        toc();
-        tic(KC_TRSM);
-        launch_back_any(cplx, Dchol + 2 * q0, 2 * n, bi.max_r, bi.max_nb, s, launches);
-        toc();
-        tic(KC_PROJ);
-        launch_nn(cplx, Dproj + 2 * q0, 2 * n, bi.max_nb, p, s, launches);
-        toc();
-        tic(KC_HGRAM);
-        launch_nt(cplx, Dh + 2 * q0, 2 * n, bi.max_nb, bi.max_nb, s, launches);
-        toc();
-        {
-          const size_t sm = (size_t)bi.max_nb * (bi.max_nb + 1) * sS + 3 * (size_t)bi.max_nb * 4 + 64;
-          tic(KC_ID);
-          if (cplx) rsrs::id_kernel<true><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, ipool, gidx, atol * atol, p, l);
-          else rsrs::id_kernel<false><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, ipool, gidx, atol * atol, p, l);
-          post("id_kernel", s, launches);
+        rsrs::HaloPlan H;
+        std::vector<int4> srecs;
+        int64_t nsend = 0;
+        std::vector<int64_t> recv_off(R + 1, 0), send_off(R + 1, 0);
+        if (dist) {
+          // active counts: processed boxes contribute their skeletons (R15)
+          std::vector<int> cnt(nbox);
+          for (int j = 0; j < nbox; ++j)
+            cnt[j] = (nb_all[j] > 0 && lv.colour[j] < bi.colour) ? k_all[j] : nb_all[j];
+          H = rsrs::plan_halo(T, part, lev, bi.colour, nb_all, cnt, me);
+          // halo rows after my rows, grouped by owner in Morton order
+          std::vector<int> halo0(nbox, -1);
+          int64_t hr = nloc;
+          for (int q = 0; q < R; ++q) {
+            recv_off[q] = hr - nloc;
+            for (const auto& bc : H.recv[q]) {
+              halo0[bc.box] = (int)hr;
+              hr += bc.count;
+            }
+          }
+          recv_off[R] = hr - nloc;
+          for (int qb = q0; qb < q0 + n; ++qb)
+            for (int t = fs_first[qb]; t < fs_first[qb + 1]; ++t) {
+              const int rec = foreign_slot[t].first, j = foreign_slot[t].second;
+              hnbr[rec] = -1;
+              hnbr[rec + 1] = halo0[j] >= 0 ? halo0[j] : 0;
+              hnbr[rec + 2] = halo0[j] >= 0 ? cnt[j] : 0;
+            }
+          if (bi.rec1 > bi.rec0)
+            CK(cudaMemcpyAsync(dnbr + bi.rec0, hnbr.data() + bi.rec0, sizeof(int) * (bi.rec1 - bi.rec0),
+                               cudaMemcpyHostToDevice, s));
+          // my rows requested by each peer
+          for (int q = 0; q < R; ++q) {
+            send_off[q] = nsend;
+            for (const auto& bc : H.send[q]) {
+              const bool done = lv.colour[bc.box] < bi.colour;
+              srecs.push_back(make_int4(done ? hb_of[bc.box] : -1, row0[bc.box], bc.count, (int)nsend));
+              nsend += bc.count;
+            }
+          }
+          send_off[R] = nsend;
+          build_rowlist(srecs, (int)nsend, dboxes, diws, rl_send);
+          const int64_t nrecv = recv_off[R];
+          const size_t rowbytes = sizeof(double) * (4 * (size_t)W + 1);
+          mv_send.ensure(std::max<size_t>(16, nsend * rowbytes), s);
+          mv_recv.ensure(std::max<size_t>(16, nrecv * rowbytes), s);
+          std::vector<rsrs::Msg> sends, recvs;
+          for (int q = 0; q < R; ++q) {
+            const int64_t ns = send_off[q + 1] - send_off[q], nr_ = recv_off[q + 1] - recv_off[q];
+            double* sb = mv_send.as<double>() + send_off[q] * (4 * W + 1);
+            if (ns) {
+              gather_rows(store4, SC * ld, gidx, rl_send.as<int>() + send_off[q], 0, (int)ns, W, 4, true, sb);
+              sends.push_back({q, sb, (size_t)ns * rowbytes});
+            }
+            if (nr_) recvs.push_back({q, mv_recv.as<double>() + recv_off[q] * (4 * W + 1), (size_t)nr_ * rowbytes});
+          }
+          comm->exchange(sends, recvs, s);
+          for (int q = 0; q < R; ++q) {
+            const int64_t nr_ = recv_off[q + 1] - recv_off[q];
+            if (nr_)
+              scatter_rows(mv_recv.as<double>() + recv_off[q] * (4 * W + 1), store4, SC * ld, gidx, nullptr,
+                           (int)(nloc + recv_off[q]), (int)nr_, W, 4, true);
+          }
+        }
+        if (n > 0) {
+          tic(KC_MISC);
+          rsrs::build_near_kernel<<<n, 32, 0, s>>>(dbx, dboxes, diws, dnbr, p, l);
+          post("build_near_kernel", s, launches);
+          toc();
+          tic(KC_GRAM);
+          launch_nt(cplx, Dgram + 4 * q0, 4 * n, bi.max_r, bi.max_r, s, launches);
+          toc();
+          tic(KC_CHOL);
+          launch_chol_any(cplx, Dchol + 2 * q0, 2 * n, bi.max_r, bi.max_nb, s, launches);
+          toc();
+          tic(KC_TRSM);
+          launch_back_any(cplx, Dchol + 2 * q0, 2 * n, bi.max_r, bi.max_nb, s, launches);
+          toc();
+          tic(KC_PROJ);
+          launch_nn(cplx, Dproj + 2 * q0, 2 * n, bi.max_nb, p, s, launches);
+          toc();
+          tic(KC_HGRAM);
+          launch_nt(cplx, Dh + 2 * q0, 2 * n, bi.max_nb, bi.max_nb, s, launches);
+          toc();
+          {
+            const size_t sm = (size_t)bi.max_nb * (bi.max_nb + 1) * sS + 3 * (size_t)bi.max_nb * 4 + 64;
+            tic(KC_ID);
+            if (cplx) rsrs::id_kernel<true><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, ipool, gidx, atol * atol, p, l);
+            else rsrs::id_kernel<false><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, ipool, gidx, atol * atol, p, l);
+            post("id_kernel", s, launches);
+            toc();
+          }
+          tic(KC_EF);
+          launch_nn(cplx, Def + 4 * q0, 4 * n, bi.max_nb, p, s, launches);
+          toc();
+          {
+            const size_t sm = 2 * (size_t)bi.max_nb * (bi.max_nb + 1) * sS + 3 * (size_t)bi.max_nb * 4 + 64;
+            tic(KC_EXTRACT);
+            if (cplx) rsrs::extract_lu_kernel<true><<<n, 256, sm, s>>>(dbx, dws, diws, fpool);
+            else rsrs::extract_lu_kernel<false><<<n, 256, sm, s>>>(dbx, dws, diws, fpool);
+            post("extract_lu_kernel", s, launches);
+            toc();
+          }
+          tic(KC_G);
+          launch_nn(cplx, Dg + 2 * q0, 2 * n, bi.max_r, bi.max_r, s, launches);
+          toc();
+          tic(KC_UPD);
+          launch_nn(cplx, Dupd + 2 * q0, 2 * n, bi.max_r, p, s, launches);
           toc();
         }
-        tic(KC_EF);
-        launch_nn(cplx, Def + 4 * q0, 4 * n, bi.max_nb, p, s, launches);
-        toc();
-        {
-          const size_t sm = 2 * (size_t)bi.max_nb * (bi.max_nb + 1) * sS + 3 * (size_t)bi.max_nb * 4 + 64;
-          tic(KC_EXTRACT);
-          if (cplx) rsrs::extract_lu_kernel<true><<<n, 256, sm, s>>>(dbx, dws, diws, fpool);
-          else rsrs::extract_lu_kernel<false><<<n, 256, sm, s>>>(dbx, dws, diws, fpool);
-          post("extract_lu_kernel", s, launches);
-          toc();
+        if (dist) {
+          // return the updated Y/Z halo rows to their owners (each row has one writer per colour)
+          const size_t rowbytes2 = sizeof(double) * 2 * (size_t)W;
+          std::vector<rsrs::Msg> sends, recvs;
+          for (int q = 0; q < R; ++q) {
+            const int64_t nr_ = recv_off[q + 1] - recv_off[q], ns = send_off[q + 1] - send_off[q];
+            double* rb = mv_recv.as<double>() + recv_off[q] * 2 * W;
+            if (nr_) {
+              gather_rows(store4, SC * ld, gidx, nullptr, (int)(nloc + recv_off[q]), (int)nr_, W, 2, false, rb);
+              sends.push_back({q, rb, (size_t)nr_ * rowbytes2});
+            }
+            if (ns) recvs.push_back({q, mv_send.as<double>() + send_off[q] * 2 * W, (size_t)ns * rowbytes2});
+          }
+          comm->exchange(sends, recvs, s);
+          for (int q = 0; q < R; ++q) {
+            const int64_t ns = send_off[q + 1] - send_off[q];
+            if (ns)
+              scatter_rows(mv_send.as<double>() + send_off[q] * 2 * W, store4, SC * ld, gidx,
+                           rl_send.as<int>() + send_off[q], 0, (int)ns, W, 2, false);
+          }
         }
-        tic(KC_G);
-        launch_nn(cplx, Dg + 2 * q0, 2 * n, bi.max_r, bi.max_r, s, launches);
-        toc();
-        tic(KC_UPD);
-        launch_nn(cplx, Dupd + 2 * q0, 2 * n, bi.max_r, p, s, launches);
-        toc();
+        if (R > 1) {
+          // skeleton counts and failures of this colour, known to every rank
+          std::vector<BoxDev> hc(n);
+          if (n) CK(cudaMemcpyAsync(hc.data(), dbx, sizeof(BoxDev) * n, cudaMemcpyDeviceToHost, s));
+          stream_sync(s);
+          std::vector<int> kv(2 * (size_t)nbox, -1);
+          for (int b = 0; b < nbox; ++b) kv[nbox + b] = 0;
+          for (const BoxDev& x : hc) {
+            kv[x.box] = x.k;
+            kv[nbox + x.box] = x.status;
+          }
+          comm->allreduce_max_i32(kv.data(), kv.size(), s);
+          for (int b = 0; b < nbox; ++b) {
+            if (lv.colour[b] != bi.colour || nb_all[b] <= 0) continue;
+            k_all[b] = kv[b];
+            if (kv[nbox + b] != rsrs::ST_OK) {
+              std::ostringstream os;
+              os << "level " << lev << " box " << b << " (rank " << own[b] << "): "
+                 << (kv[nbox + b] == rsrs::ST_SAMPLES ? "too few samples (p - r < k + l)"
+                     : kv[nbox + b] == rsrs::ST_SINGULAR_GRAM ? "near-field Gram not positive definite"
+                                                            : "X_rr singular");
+              throw StatusError{kv[nbox + b] == rsrs::ST_SAMPLES ? RSRS_ERR_SAMPLES : RSRS_ERR_SINGULAR, os.str()};
+            }
+          }
+        }
       }
-      CK(cudaMemcpyAsync(hb.data(), dboxes, sizeof(BoxDev) * hb.size(), cudaMemcpyDeviceToHost, s));
+      if (!hb.empty()) CK(cudaMemcpyAsync(hb.data(), dboxes, sizeof(BoxDev) * hb.size(), cudaMemcpyDeviceToHost, s));
       stream_sync(s);
       flush_prof();
-      std::vector<int> newk(nbox, 0);
       f->ranks[lev].assign(nbox, -1);
       for (const BoxDev& x : hb) {
         if (x.status != rsrs::ST_OK) {
@@ -719,8 +980,7 @@ struct Planner {
           }
           throw StatusError{st, os.str()};
         }
-        newk[x.box] = x.k;
-        f->ranks[lev][x.box] = x.k;
+        k_all[x.box] = x.k;
         f->stats.max_rank = std::max<int64_t>(f->stats.max_rank, x.k);
         if (x.nr > 0) {
           f->stats.nsteps++;
@@ -728,10 +988,14 @@ struct Planner {
         }
         account_box(x.nb, x.r, x.k, p);
       }
+      for (int b = 0; b < nbox; ++b) {
+        if (nb_all[b] <= 0) k_all[b] = 0;
+        f->ranks[lev][b] = nb_all[b] > 0 ? k_all[b] : -1;
+      }
       for (const BInfo& bi : binfo) {
         Batch B;
         B.level = lev;
-        B.colour = T.levels[lev].colour[hb[bi.first].box];
+        B.colour = bi.colour;
         B.nbox = bi.count;
         B.d_boxes = dboxes + bi.first;
         B.h.assign(hb.begin() + bi.first, hb.begin() + bi.first + bi.count);
@@ -739,26 +1003,39 @@ struct Planner {
         B.ipool = ipool;
         B.max_nb = bi.max_nb;
         B.max_r = bi.max_r;
+        B.dist = R > 1;
         f->batches.push_back(std::move(B));
       }
       // ---- merge: skeleton rows into the parent level's store
       const rsrs::TreeLevel& pl = T.levels[lev - 1];
-      std::vector<int> pnb(pl.nboxes, 0);
-      for (int b = 0; b < nbox; ++b) pnb[lv.parent[b]] += newk[b];
-      std::vector<int> pref(nbox + 1, 0);
-      for (int b = 0; b < nbox; ++b) pref[b + 1] = pref[b] + newk[b];
-      const int64_t nnew = pref[nbox];
+      std::vector<int> pnb(pl.nboxes, 0), coff(nbox, 0);
+      for (int b = 0; b < nbox; ++b) {          // children in Morton order inside a parent
+        coff[b] = pnb[lv.parent[b]];
+        pnb[lv.parent[b]] += k_all[b];
+      }
+      std::vector<int> prow0(pl.nboxes, -1);
+      int64_t nnew = 0;
+      for (int64_t P = 0; P < pl.nboxes; ++P)
+        if (part.owner(T, lev - 1, P) == me) {
+          prow0[P] = (int)nnew;
+          nnew += pnb[P];
+        }
+      const int64_t cap = nnew + (lev - 1 >= top ? halo_capacity(lev - 1, pnb) : 0);
       std::vector<int> dst0(hb.size());
-      for (size_t q = 0; q < hb.size(); ++q) dst0[q] = pref[hb[q].box];
+      for (size_t q = 0; q < hb.size(); ++q) {
+        const int b = hb[q].box;
+        const int P = lv.parent[b];
+        dst0[q] = (prow0[P] >= 0) ? prow0[P] + coff[b] : -1;
+      }
       const int nxt = (cur == 0) ? 1 : 0;
-      store[nxt].ensure((size_t)sS * std::max<i64>(2, 4 * nnew * nld), s);
-      gidx_buf[nxt].ensure(sizeof(int) * std::max<int64_t>(2, nnew), s);
+      store[nxt].ensure((size_t)sS * std::max<i64>(2, 4 * cap * nld), s);
+      gidx_buf[nxt].ensure(sizeof(int) * std::max<int64_t>(2, cap), s);
       double* nY = store[nxt].as<double>();
-      double* nZ = nY + SC * nnew * nld;
-      double* nO = nZ + SC * nnew * nld;
-      double* nP = nO + SC * nnew * nld;
+      double* nZ = nY + SC * cap * nld;
+      double* nO = nZ + SC * cap * nld;
+      double* nP = nO + SC * cap * nld;
       int* ng = gidx_buf[nxt].as<int>();
-      if (nnew > 0) {
+      if (!hb.empty()) {
         dstbuf.ensure(sizeof(int) * dst0.size(), s);
         CK(cudaMemcpyAsync(dstbuf.p, dst0.data(), sizeof(int) * dst0.size(), cudaMemcpyHostToDevice, s));
         dim3 grid((unsigned)hb.size(), 4);
@@ -767,18 +1044,65 @@ struct Planner {
                                                  nZ, nO, nP, SC * nld, ng, SC * p);
         post("compact_kernel", s, launches);
         toc();
-        account(KC_MISC, 0.0, 2.0 * 4 * nnew * p * sS);
-        stream_sync(s);
-        flush_prof();
       }
+      account(KC_MISC, 0.0, 2.0 * 4 * nnew * p * sS);
+      if (R > 1) {
+        // skeletons whose parent lives on another rank (Morton-range boundary or the gather level)
+        rsrs::MovePlan M = rsrs::plan_moves(T, part, lev, k_all, me);
+        std::vector<int4> recs;
+        std::vector<int64_t> so(R + 1, 0), ro(R + 1, 0);
+        int64_t ns = 0, nr_ = 0;
+        std::vector<int> rdst;
+        for (int q = 0; q < R; ++q) {
+          so[q] = ns;
+          for (const auto& bc : M.send[q]) {
+            recs.push_back(make_int4(hb_of[bc.box], 0, bc.count, (int)ns));
+            ns += bc.count;
+          }
+          ro[q] = nr_;
+          for (const auto& bc : M.recv[q]) {
+            const int P = lv.parent[bc.box];
+            for (int t = 0; t < bc.count; ++t) rdst.push_back(prow0[P] + coff[bc.box] + t);
+            nr_ += bc.count;
+          }
+        }
+        so[R] = ns;
+        ro[R] = nr_;
+        build_rowlist(recs, (int)ns, dboxes, diws, rl_send);
+        rl_recv.ensure(sizeof(int) * std::max<int64_t>(nr_, 1), s);
+        if (nr_) CK(cudaMemcpyAsync(rl_recv.p, rdst.data(), sizeof(int) * nr_, cudaMemcpyHostToDevice, s));
+        const size_t rowbytes = sizeof(double) * (4 * (size_t)W + 1);
+        mv_send.ensure(std::max<size_t>(16, ns * rowbytes), s);
+        mv_recv.ensure(std::max<size_t>(16, nr_ * rowbytes), s);
+        std::vector<rsrs::Msg> sends, recvs;
+        for (int q = 0; q < R; ++q) {
+          const int64_t a = so[q + 1] - so[q], b2 = ro[q + 1] - ro[q];
+          double* sb = mv_send.as<double>() + so[q] * (4 * W + 1);
+          if (a) {
+            gather_rows(store4, SC * ld, gidx, rl_send.as<int>() + so[q], 0, (int)a, W, 4, true, sb);
+            sends.push_back({q, sb, (size_t)a * rowbytes});
+          }
+          if (b2) recvs.push_back({q, mv_recv.as<double>() + ro[q] * (4 * W + 1), (size_t)b2 * rowbytes});
+        }
+        comm->exchange(sends, recvs, s);
+        double* const nstore4[4] = {nY, nZ, nO, nP};
+        for (int q = 0; q < R; ++q) {
+          const int64_t b2 = ro[q + 1] - ro[q];
+          if (b2)
+            scatter_rows(mv_recv.as<double>() + ro[q] * (4 * W + 1), nstore4, SC * nld, ng,
+                         rl_recv.as<int>() + ro[q], 0, (int)b2, W, 4, true);
+        }
+      }
+      stream_sync(s);
+      flush_prof();
       Y = nY; Z = nZ; Om = nO; Ps = nP; ld = nld;
       gidx = ng;
       cur = nxt;
-      nrows = nnew;
-      nb_box = pnb;
+      nloc = nnew;
+      nb_all = pnb;
       f->stats.nlevels_compressed++;
     }
-    finish_top(Y, Om, ld, gidx, (int)nrows);
+    finish_top(Y, Om, ld, gidx, (int)nloc);
     f->stats.flops_model = flops;
     f->stats.bytes_model = bytes;
     f->stats.launches = launches;
@@ -873,27 +1197,14 @@ rsrs_status fail(rsrs_status st, const std::string& msg) {
 
 extern "C" {
 
-rsrs_status rsrs_factor(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, void* Z, void* Omega, void* Psi,
-                        int64_t ld, const rsrs_opts* opts, rsrs_factorization* out) {
-  rsrs::clear_error();
-  if (!out) return fail(RSRS_ERR_INVALID, "rsrs_factor: out is NULL");
-  *out = nullptr;
-  if (!t || !Y || !Z || !Omega || !Psi) return fail(RSRS_ERR_INVALID, "rsrs_factor: null argument");
-  if (p < 1 || ld < p || (ld & 1)) return fail(RSRS_ERR_INVALID, "rsrs_factor: need 1 <= p <= ld and ld even");
-  if (dt != RSRS_F64 && dt != RSRS_C128) return fail(RSRS_ERR_INVALID, "rsrs_factor: unknown dtype");
-  rsrs_opts o{1e-6, 1.0, 1.0, 10, 2, 0, 1, nullptr, nullptr, 0};
-  if (opts) o = *opts;
-  if (o.nranks != 1 || o.rank != 0 || o.nccl_comm)
-    return fail(RSRS_ERR_STATE, "rsrs_factor: only nranks == 1 is supported by this build");
-  if (!(o.eps > 0) || !(o.level_growth > 0) || !(o.id_scale > 0) || o.oversample < 0 || o.top_level < 1)
-    return fail(RSRS_ERR_INVALID, "rsrs_factor: invalid options");
-  int ndev = 0;
-  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
-    return fail(RSRS_ERR_CUDA, "rsrs_factor: no CUDA device (there is no CPU fallback)");
+// Shared implementation of rsrs_factor (one rank or one rank of a multi-GPU run).
+static rsrs_status factor_impl(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, void* Z, void* Omega, void* Psi,
+                               int64_t ld, const rsrs_opts& o, rsrs::Comm* comm, rsrs_factorization* out) {
   rsrs_factorization f = nullptr;
   try {
     init_kernels();
     f = new rsrs_factor_s();
+    f->xtmp.devsync = f->mergebuf.devsync = true;
     const rsrs::Tree& T = t->t;
     f->dt = dt;
     f->cplx = (dt == RSRS_C128);
@@ -904,6 +1215,9 @@ rsrs_status rsrs_factor(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, void* Z,
     f->d = T.d;
     f->top_level = o.top_level;
     f->stream = (cudaStream_t)o.stream;
+    f->nranks = comm ? comm->nranks : 1;
+    f->rank = comm ? comm->rank : 0;
+    f->nccl_comm = o.nccl_comm;
     cudaStream_t s = f->stream;
     f->stats.N = T.N;
     f->stats.p = p;
@@ -911,6 +1225,7 @@ rsrs_status rsrs_factor(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, void* Z,
     f->stats.top_level = o.top_level;
     // tree -> original permutation on the device (solve / apply)
     f->keep.emplace_back(new DBuf());
+    f->keep.back()->devsync = true;
     f->keep.back()->alloc(sizeof(int64_t) * T.N, s);
     f->d_perm = f->keep.back()->as<int64_t>();
     CK(cudaMemcpyAsync(f->d_perm, T.perm.data(), sizeof(int64_t) * T.N, cudaMemcpyHostToDevice, s));
@@ -928,6 +1243,8 @@ rsrs_status rsrs_factor(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, void* Z,
     P.profile = o.profile != 0;
     P.cplx = f->cplx;
     P.SC = f->sc;
+    P.comm = (comm && comm->nranks > 1) ? comm : nullptr;
+    P.part = rsrs::make_partition(T, comm ? comm->nranks : 1, o.gather_level, o.top_level);
     P.run((double*)Y, (double*)Z, (double*)Omega, (double*)Psi, ld);
     CK(cudaEventRecord(e1, s));
     CK(cudaEventSynchronize(e1));
@@ -937,67 +1254,221 @@ rsrs_status rsrs_factor(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, void* Z,
     cudaEventDestroy(e1);
     f->stats.factor_ms = ms;
     if (g_trace)
-      fprintf(stderr, "[rsrs trace] factor: host %.1f ms, device %.1f ms, alloc %.1f ms (%d calls, %.2f GB), sync-wait %.1f ms (%d), launches %lld\n",
-              1e3 * (now_s() - th0), ms, 1e3 * g_ht.alloc, g_ht.nalloc, g_ht.alloc_bytes / 1e9, 1e3 * g_ht.sync,
-              g_ht.nsync, (long long)P.launches);
+      fprintf(stderr, "[rsrs trace] factor (rank %d/%d): host %.1f ms, device %.1f ms, alloc %.1f ms (%d calls, %.2f GB), sync-wait %.1f ms (%d), launches %lld\n",
+              f->rank, f->nranks, 1e3 * (now_s() - th0), ms, 1e3 * g_ht.alloc, g_ht.nalloc, g_ht.alloc_bytes / 1e9,
+              1e3 * g_ht.sync, g_ht.nsync, (long long)P.launches);
     f->stats.solve_launches = 2 + 2 * (int64_t)f->batches.size() + (f->nS > 0 ? 1 : 0);
     *out = f;
     return RSRS_OK;
   } catch (const StatusError& e) {
+    if (f) cudaStreamSynchronize(f->stream);
     delete f;
     return fail(e.st, "rsrs_factor: " + e.msg);
   } catch (const CudaError& e) {
     delete f;
     return fail(RSRS_ERR_CUDA, "rsrs_factor: " + e.msg);
+  } catch (const rsrs::CommError& e) {
+    if (f) cudaStreamSynchronize(f->stream);
+    delete f;
+    return fail(RSRS_ERR_NCCL, "rsrs_factor: " + e.msg);
   } catch (const std::bad_alloc&) {
     delete f;
     return fail(RSRS_ERR_NOMEM, "rsrs_factor: out of host memory");
   }
 }
 
+static rsrs_status check_args(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, void* Z, void* Omega, void* Psi,
+                              int64_t ld, const rsrs_opts* opts, rsrs_opts& o) {
+  if (!t || !Y || !Z || !Omega || !Psi) return fail(RSRS_ERR_INVALID, "rsrs_factor: null argument");
+  if (p < 1 || ld < p || (ld & 1)) return fail(RSRS_ERR_INVALID, "rsrs_factor: need 1 <= p <= ld and ld even");
+  if (dt != RSRS_F64 && dt != RSRS_C128) return fail(RSRS_ERR_INVALID, "rsrs_factor: unknown dtype");
+  o = rsrs_opts{1e-6, 1.0, 1.0, 10, 2, 0, 1, nullptr, nullptr, 0, -1};
+  if (opts) o = *opts;
+  if (!(o.eps > 0) || !(o.level_growth > 0) || !(o.id_scale > 0) || o.oversample < 0 || o.top_level < 1 ||
+      o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks)
+    return fail(RSRS_ERR_INVALID, "rsrs_factor: invalid options");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(RSRS_ERR_CUDA, "rsrs_factor: no CUDA device (there is no CPU fallback)");
+  return RSRS_OK;
+}
+
+rsrs_status rsrs_factor(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, void* Z, void* Omega, void* Psi,
+                        int64_t ld, const rsrs_opts* opts, rsrs_factorization* out) {
+  rsrs::clear_error();
+  if (!out) return fail(RSRS_ERR_INVALID, "rsrs_factor: out is NULL");
+  *out = nullptr;
+  rsrs_opts o;
+  rsrs_status st = check_args(t, dt, p, Y, Z, Omega, Psi, ld, opts, o);
+  if (st != RSRS_OK) return st;
+  if (o.nranks == 1) return factor_impl(t, dt, p, Y, Z, Omega, Psi, ld, o, nullptr, out);
+  if (!o.nccl_comm) return fail(RSRS_ERR_INVALID, "rsrs_factor: nranks > 1 needs opts.nccl_comm (rsrs_comm_init)");
+  if (!rsrs::NcclApi::get().ok()) return fail(RSRS_ERR_NCCL, "rsrs_factor: libnccl.so.2 not loadable");
+  rsrs::NcclComm c(o.nccl_comm, o.rank, o.nranks);
+  return factor_impl(t, dt, p, Y, Z, Omega, Psi, ld, o, &c, out);
+}
+
+// G ranks emulated by G host threads on the current GPU (tests / validation of the
+// multi-GPU path on one device): Y, Z, Omega, Psi are the FULL tree-ordered arrays;
+// rank q works on its leaf rows [first_q, first_q+1) like a real rank would.
+rsrs_status rsrs_factor_emulated(rsrs_tree t, rsrs_dtype dt, int64_t p, int G, void* Y, void* Z, void* Omega,
+                                 void* Psi, int64_t ld, const rsrs_opts* opts, rsrs_factorization* out) {
+  rsrs::clear_error();
+  if (!out || G < 1) return fail(RSRS_ERR_INVALID, "rsrs_factor_emulated: invalid argument");
+  for (int q = 0; q < G; ++q) out[q] = nullptr;
+  rsrs_opts o;
+  rsrs_status st = check_args(t, dt, p, Y, Z, Omega, Psi, ld, opts, o);
+  if (st != RSRS_OK) return st;
+  try {
+    init_kernels();
+  } catch (const CudaError& e) {
+    return fail(RSRS_ERR_CUDA, "rsrs_factor_emulated: " + e.msg);
+  }
+  const rsrs::Partition P = rsrs::make_partition(t->t, G, o.gather_level, o.top_level);
+  rsrs::InProcHub hub(G);
+  std::vector<rsrs_status> sts(G, RSRS_OK);
+  std::vector<std::string> msgs(G);
+  std::vector<cudaStream_t> streams(G, nullptr);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const size_t esz = (dt == RSRS_C128 ? 16 : 8);
+  std::vector<std::thread> th;
+  for (int q = 0; q < G; ++q)
+    th.emplace_back([&, q] {
+      cudaSetDevice(dev);
+      cudaStreamCreateWithFlags(&streams[q], cudaStreamNonBlocking);
+      rsrs::InProcComm c(&hub, q);
+      rsrs_opts oq = o;
+      oq.rank = q;
+      oq.nranks = G;
+      oq.stream = streams[q];
+      const size_t off = (size_t)P.first[q] * ld * esz;
+      sts[q] = factor_impl(t, dt, p, (char*)Y + off, (char*)Z + off, (char*)Omega + off, (char*)Psi + off, ld, oq,
+                           &c, &out[q]);
+      if (sts[q] != RSRS_OK) {
+        msgs[q] = rsrs_last_error();
+        hub.abort();
+      }
+    });
+  for (auto& x : th) x.join();
+  for (int q = 0; q < G; ++q)
+    if (out[q]) out[q]->own_stream = true;
+    else if (streams[q]) cudaStreamDestroy(streams[q]);
+  rsrs_status first = RSRS_OK;
+  std::string msg;
+  // the rank that failed first names the error; the others only saw the abort
+  for (int pass = 0; pass < 2 && first == RSRS_OK; ++pass)
+    for (int q = 0; q < G; ++q)
+      if (sts[q] != RSRS_OK && (pass == 1 || msgs[q].find("another emulated rank failed") == std::string::npos)) {
+        first = sts[q];
+        msg = "rank " + std::to_string(q) + ": " + msgs[q];
+        break;
+      }
+  if (first != RSRS_OK) {
+    for (int r = 0; r < G; ++r) {
+      rsrs_factor_destroy(out[r]);
+      out[r] = nullptr;
+    }
+    return fail(first, msg);
+  }
+  return RSRS_OK;
+}
+
 }  // extern "C"
 
 // solve / apply sweeps over the recorded colour batches
+// Multi-GPU: x (N x nrhs, tree order) is replicated on every rank; after each
+// colour batch the rows the batch touched (one writer per row, since same-colour
+// near sets are disjoint) are merged: contrib = x on touched rows, mask = 1, sum
+// over ranks, x = contrib where mask != 0 (exact: exactly one nonzero term).
+struct Merger {
+  rsrs_factorization f;
+  rsrs::Comm* comm;
+  double* x;
+  int64_t N;
+  int w;            // doubles per x row
+  cudaStream_t s;
+  double* contrib = nullptr;
+  double* mask = nullptr;
+  void init() {
+    if (!comm) return;
+    f->mergebuf.ensure(sizeof(double) * N * (w + 1), s);
+    contrib = f->mergebuf.as<double>();
+    mask = contrib + N * w;
+    CK(cudaMemsetAsync(contrib, 0, sizeof(double) * N * (w + 1), s));
+  }
+  void batch(const Batch& b, int which) {
+    if (!comm) return;
+    if (b.nbox > 0) {
+      rsrs::mark_rows_kernel<<<b.nbox, 128, 0, s>>>(b.d_boxes, b.ipool, x, w, w, contrib, mask, which);
+      CK(cudaGetLastError());
+    }
+    finish();
+  }
+  void list(const int* l, int n) {
+    if (!comm) return;
+    if (n > 0) {
+      rsrs::mark_list_kernel<<<std::min(1024, (n * w + 255) / 256), 256, 0, s>>>(l, n, x, w, w, contrib, mask);
+      CK(cudaGetLastError());
+    }
+    finish();
+  }
+  void finish() {
+    comm->allreduce_sum_f64(contrib, (size_t)N * (w + 1), s);
+    rsrs::merge_finalize_kernel<<<592, 256, 0, s>>>(N, x, w, w, contrib, mask);
+    CK(cudaGetLastError());
+  }
+};
+
 template <bool C>
-static void run_sweep(rsrs_factorization f, double* x, int64_t nrhs, bool solve, cudaStream_t s) {
+static void run_sweep(rsrs_factorization f, double* x, int64_t nrhs, bool solve, cudaStream_t s, rsrs::Comm* comm) {
   const size_t sS = (C ? 2 : 1) * sizeof(double);
   const int nr = (int)nrhs;
+  Merger M{f, comm, x, f->N, (int)((C ? 2 : 1) * nrhs), s};
+  M.init();
   if (solve) {
     for (const Batch& b : f->batches) {
       const size_t sm = sS * 2 * (b.max_nb + 2);
-      rsrs::solve_fwd_kernel<C><<<b.nbox, 256, sm, s>>>(b.d_boxes, b.fpool, b.ipool, x, nrhs, nr);
+      if (b.nbox) rsrs::solve_fwd_kernel<C><<<b.nbox, 256, sm, s>>>(b.d_boxes, b.fpool, b.ipool, x, nrhs, nr);
       CK(cudaGetLastError());
+      M.batch(b, 0);
     }
     if (f->nS > 0) {
       rsrs::top_solve_kernel<C><<<1, 1024, sS * f->nS, s>>>(f->d_LU, f->ldS, f->nS, f->d_piv, f->d_S, x, nrhs, nr);
       CK(cudaGetLastError());
     }
+    M.list(f->d_S, f->nS);
     for (auto it = f->batches.rbegin(); it != f->batches.rend(); ++it) {
       const size_t sm = sS * (it->max_r + it->max_nb + 4);
-      rsrs::solve_bwd_kernel<C><<<it->nbox, 256, sm, s>>>(it->d_boxes, it->fpool, it->ipool, x, nrhs, nr);
+      if (it->nbox) rsrs::solve_bwd_kernel<C><<<it->nbox, 256, sm, s>>>(it->d_boxes, it->fpool, it->ipool, x, nrhs, nr);
       CK(cudaGetLastError());
+      M.batch(*it, 1);
     }
   } else {
     for (const Batch& b : f->batches) {
       const size_t sm = sS * (b.max_r + 2 * b.max_nb + 4);
-      rsrs::apply_fwd_kernel<C><<<b.nbox, 256, sm, s>>>(b.d_boxes, b.fpool, b.ipool, x, nrhs, nr);
+      if (b.nbox) rsrs::apply_fwd_kernel<C><<<b.nbox, 256, sm, s>>>(b.d_boxes, b.fpool, b.ipool, x, nrhs, nr);
       CK(cudaGetLastError());
+      M.batch(b, 1);
     }
     if (f->nS > 0) {
       rsrs::top_apply_kernel<C><<<1, 1024, sS * f->nS, s>>>(f->d_ASS, f->ldS, f->nS, f->d_S, x, nrhs, nr);
       CK(cudaGetLastError());
     }
+    M.list(f->d_S, f->nS);
     for (auto it = f->batches.rbegin(); it != f->batches.rend(); ++it) {
       const size_t sm = sS * (2 * it->max_nb + 4);
-      rsrs::apply_bwd_kernel<C><<<it->nbox, 256, sm, s>>>(it->d_boxes, it->fpool, it->ipool, x, nrhs, nr);
+      if (it->nbox) rsrs::apply_bwd_kernel<C><<<it->nbox, 256, sm, s>>>(it->d_boxes, it->fpool, it->ipool, x, nrhs, nr);
       CK(cudaGetLastError());
+      M.batch(*it, 0);
     }
   }
 }
 
 extern "C" {
 
-static rsrs_status sweep(rsrs_factorization f, void* Bv, int64_t ldb, int64_t nrhs, void* sv, bool solve) {
+static rsrs_status sweep_comm(rsrs_factorization f, void* Bv, int64_t ldb, int64_t nrhs, void* sv, bool solve,
+                              rsrs::Comm* comm) {
   rsrs::clear_error();
   const char* who = solve ? "rsrs_solve" : "rsrs_apply";
   if (!f || !Bv) return fail(RSRS_ERR_INVALID, std::string(who) + ": null argument");
@@ -1016,8 +1487,8 @@ static rsrs_status sweep(rsrs_factorization f, void* Bv, int64_t ldb, int64_t nr
       rsrs::permute_rows_kernel<<<grid, blk, 0, s>>>(B, SC * ldb, x, SC * nrhs, f->d_perm, N, SC * nr, 0);
       CK(cudaGetLastError());
     }
-    if (f->cplx) run_sweep<true>(f, x, nrhs, solve, s);
-    else run_sweep<false>(f, x, nrhs, solve, s);
+    if (f->cplx) run_sweep<true>(f, x, nrhs, solve, s, comm);
+    else run_sweep<false>(f, x, nrhs, solve, s, comm);
     {
       dim3 blk(32, 8);
       dim3 grid((unsigned)((N + 7) / 8));
@@ -1029,7 +1500,18 @@ static rsrs_status sweep(rsrs_factorization f, void* Bv, int64_t ldb, int64_t nr
     return fail(e.st, std::string(who) + ": " + e.msg);
   } catch (const CudaError& e) {
     return fail(RSRS_ERR_CUDA, std::string(who) + ": " + e.msg);
+  } catch (const rsrs::CommError& e) {
+    return fail(RSRS_ERR_NCCL, std::string(who) + ": " + e.msg);
   }
+}
+
+static rsrs_status sweep(rsrs_factorization f, void* Bv, int64_t ldb, int64_t nrhs, void* sv, bool solve) {
+  if (f && f->nranks > 1) {
+    if (!rsrs::NcclApi::get().ok()) return fail(RSRS_ERR_NCCL, "multi-rank solve: libnccl.so.2 not loadable");
+    rsrs::NcclComm c(f->nccl_comm, f->rank, f->nranks);
+    return sweep_comm(f, Bv, ldb, nrhs, sv, solve, &c);
+  }
+  return sweep_comm(f, Bv, ldb, nrhs, sv, solve, nullptr);
 }
 
 rsrs_status rsrs_solve(rsrs_factorization f, void* B, int64_t ldb, int64_t nrhs, void* s) {
@@ -1081,8 +1563,97 @@ rsrs_status rsrs_factor_top(rsrs_factorization f, int64_t* S, int64_t cap, int64
 void rsrs_factor_destroy(rsrs_factorization f) {
   if (!f) return;
   cudaDeviceSynchronize();   // solves may run on any stream; the arena reuses freed blocks at once
+  cudaStream_t s = f->own_stream ? f->stream : nullptr;
   delete f;
+  if (s) cudaStreamDestroy(s);
 }
+
+// G emulated ranks: B (full, original order) is copied to every rank, the
+// distributed sweep runs with in-process merges, rank 0's result is written back.
+static rsrs_status sweep_emulated(rsrs_factorization* fs, int G, void* B, int64_t ldb, int64_t nrhs, bool solve) {
+  rsrs::clear_error();
+  if (!fs || G < 1 || !B || nrhs < 1 || ldb < nrhs) return fail(RSRS_ERR_INVALID, "emulated sweep: invalid argument");
+  for (int q = 0; q < G; ++q)
+    if (!fs[q] || fs[q]->nranks != G || fs[q]->rank != q)
+      return fail(RSRS_ERR_INVALID, "emulated sweep: factors do not form ranks 0..G-1");
+  const size_t bytes = sizeof(double) * fs[0]->sc * fs[0]->N * ldb;
+  std::vector<void*> xs(G, nullptr);
+  for (int q = 0; q < G; ++q) {
+    xs[q] = rsrs::Arena::get().alloc(bytes);
+    if (!xs[q]) return fail(RSRS_ERR_NOMEM, "emulated sweep: allocation failed");
+    cudaMemcpy(xs[q], B, bytes, cudaMemcpyDeviceToDevice);
+  }
+  rsrs::InProcHub hub(G);
+  std::vector<rsrs_status> sts(G, RSRS_OK);
+  std::vector<std::string> msgs(G);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::vector<std::thread> th;
+  for (int q = 0; q < G; ++q)
+    th.emplace_back([&, q] {
+      cudaSetDevice(dev);
+      cudaStream_t s;
+      cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+      rsrs::InProcComm c(&hub, q);
+      sts[q] = sweep_comm(fs[q], xs[q], ldb, nrhs, s, solve, &c);
+      cudaStreamSynchronize(s);
+      if (sts[q] != RSRS_OK) {
+        msgs[q] = rsrs_last_error();
+        hub.abort();
+      }
+      cudaStreamDestroy(s);
+    });
+  for (auto& x : th) x.join();
+  rsrs_status st = RSRS_OK;
+  std::string msg;
+  for (int q = 0; q < G; ++q)
+    if (sts[q] != RSRS_OK && st == RSRS_OK) {
+      st = sts[q];
+      msg = msgs[q];
+    }
+  if (st == RSRS_OK) cudaMemcpy(B, xs[0], bytes, cudaMemcpyDeviceToDevice);
+  cudaDeviceSynchronize();
+  for (int q = 0; q < G; ++q) rsrs::Arena::get().free(xs[q]);
+  if (st != RSRS_OK) return fail(st, msg);
+  return RSRS_OK;
+}
+
+rsrs_status rsrs_solve_emulated(rsrs_factorization* fs, int G, void* B, int64_t ldb, int64_t nrhs) {
+  return sweep_emulated(fs, G, B, ldb, nrhs, true);
+}
+rsrs_status rsrs_apply_emulated(rsrs_factorization* fs, int G, void* X, int64_t ldx, int64_t nrhs) {
+  return sweep_emulated(fs, G, X, ldx, nrhs, false);
+}
+
+// NCCL communicator of the library (multi-GPU rsrs_factor / rsrs_solve)
+rsrs_status rsrs_comm_unique_id(void* id128) {
+  rsrs::clear_error();
+  if (!id128) return fail(RSRS_ERR_INVALID, "rsrs_comm_unique_id: null argument");
+  rsrs::NcclApi& A = rsrs::NcclApi::get();
+  if (!A.ok()) return fail(RSRS_ERR_NCCL, "rsrs_comm_unique_id: libnccl.so.2 not loadable");
+  const int r = A.getUniqueId(id128);
+  if (r != 0) return fail(RSRS_ERR_NCCL, std::string("ncclGetUniqueId: ") + (A.errStr ? A.errStr(r) : "error"));
+  return RSRS_OK;
+}
+
+rsrs_status rsrs_comm_init(int nranks, int rank, const void* id128, void** comm) {
+  rsrs::clear_error();
+  if (!id128 || !comm || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(RSRS_ERR_INVALID, "rsrs_comm_init: invalid argument");
+  rsrs::NcclApi& A = rsrs::NcclApi::get();
+  if (!A.ok()) return fail(RSRS_ERR_NCCL, "rsrs_comm_init: libnccl.so.2 not loadable");
+  rsrs::NcclUid id;
+  std::memcpy(id.internal, id128, sizeof(id.internal));
+  const int r = A.commInitRank(comm, nranks, id, rank);
+  if (r != 0) return fail(RSRS_ERR_NCCL, std::string("ncclCommInitRank: ") + (A.errStr ? A.errStr(r) : "error"));
+  return RSRS_OK;
+}
+
+void rsrs_comm_destroy(void* comm) {
+  rsrs::NcclApi& A = rsrs::NcclApi::get();
+  if (comm && A.commDestroy) A.commDestroy(comm);
+}
+
 
 void rsrs_release_memory(void) {
   cudaDeviceSynchronize();

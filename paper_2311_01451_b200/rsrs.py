@@ -33,6 +33,9 @@ EXPORTS = [
     "rsrs_plan_samples", "rsrs_tree_destroy", "rsrs_factor", "rsrs_solve", "rsrs_apply",
     "rsrs_factor_stats", "rsrs_factor_ranks", "rsrs_factor_top", "rsrs_factor_destroy", "rsrs_factor_profile",
     "rsrs_last_error", "rsrs_version", "rsrs_memory_info", "rsrs_release_memory",
+    "rsrs_tree_partition", "rsrs_dist_owner", "rsrs_dist_halo_plan", "rsrs_dist_move_plan",
+    "rsrs_comm_unique_id", "rsrs_comm_init", "rsrs_comm_destroy",
+    "rsrs_factor_emulated", "rsrs_solve_emulated", "rsrs_apply_emulated",
 ]
 
 
@@ -46,7 +49,7 @@ class Opts(ctypes.Structure):
     _fields_ = [("eps", ctypes.c_double), ("level_growth", ctypes.c_double), ("id_scale", ctypes.c_double),
                 ("oversample", ctypes.c_int), ("top_level", ctypes.c_int), ("rank", ctypes.c_int),
                 ("nranks", ctypes.c_int), ("nccl_comm", ctypes.c_void_p), ("stream", ctypes.c_void_p),
-                ("profile", ctypes.c_int)]
+                ("profile", ctypes.c_int), ("gather_level", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):
@@ -81,6 +84,22 @@ _lib.rsrs_factor_profile.argtypes = [_vp, _i32, ctypes.POINTER(ctypes.c_char_p),
                                      ctypes.POINTER(_d), ctypes.POINTER(_d), ctypes.POINTER(_i64)]
 _lib.rsrs_factor_profile.restype = ctypes.c_int
 NUM_KERNEL_CLASSES = 11
+_lib.rsrs_tree_partition.argtypes = [_vp, _i32, _i32, _i32, _vp, ctypes.POINTER(_i32)]
+_lib.rsrs_dist_owner.argtypes = [_vp, _i32, _i32, _i32, _i32, _vp]
+_lib.rsrs_dist_halo_plan.argtypes = [_vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _i32, _vp, _i64,
+                                     ctypes.POINTER(_i64)]
+_lib.rsrs_dist_move_plan.argtypes = [_vp, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _i64, ctypes.POINTER(_i64)]
+_lib.rsrs_comm_unique_id.argtypes = [_vp]
+_lib.rsrs_comm_init.argtypes = [_i32, _i32, _vp, ctypes.POINTER(_vp)]
+_lib.rsrs_comm_destroy.argtypes = [_vp]
+_lib.rsrs_comm_destroy.restype = None
+_lib.rsrs_factor_emulated.argtypes = [_vp, _i32, _i64, _i32, _vp, _vp, _vp, _vp, _i64, ctypes.POINTER(Opts), _vp]
+_lib.rsrs_solve_emulated.argtypes = [_vp, _i32, _vp, _i64, _i64]
+_lib.rsrs_apply_emulated.argtypes = [_vp, _i32, _vp, _i64, _i64]
+for _n in ("rsrs_tree_partition", "rsrs_dist_owner", "rsrs_dist_halo_plan", "rsrs_dist_move_plan",
+           "rsrs_comm_unique_id", "rsrs_comm_init", "rsrs_factor_emulated", "rsrs_solve_emulated",
+           "rsrs_apply_emulated"):
+    getattr(_lib, _n).restype = ctypes.c_int
 _lib.rsrs_factor_destroy.argtypes = [_vp]
 _lib.rsrs_factor_destroy.restype = None
 for _n in ("rsrs_build_tree", "rsrs_tree_info", "rsrs_tree_perm", "rsrs_tree_level_size", "rsrs_tree_level",
@@ -169,6 +188,40 @@ class Tree:
         return {"keys": keys, "start": start, "parent": parent, "colour": colour,
                 "neighbours": [nbr[off[i]:off[i + 1]] for i in range(n)]}
 
+    def partition(self, nranks: int, gather_level: int = -1, top_level: int = 2):
+        """(first[nranks+1] tree positions of the ranks' leaf ranges, gather level used)."""
+        first = np.empty(nranks + 1, np.int64)
+        g = _i32()
+        _check(_lib.rsrs_tree_partition(self._h, nranks, gather_level, top_level, first.ctypes.data, ctypes.byref(g)))
+        return first, g.value
+
+    def owner(self, level: int, nranks: int, gather_level: int = -1, top_level: int = 2) -> np.ndarray:
+        nb, nn = _i64(), _i64()
+        _check(_lib.rsrs_tree_level_size(self._h, level, ctypes.byref(nb), ctypes.byref(nn)))
+        out = np.empty(max(nb.value, 1), np.int32)
+        _check(_lib.rsrs_dist_owner(self._h, nranks, gather_level, top_level, level, out.ctypes.data))
+        return out[:nb.value]
+
+    def _plan(self, fn, args):
+        n = _i64()
+        _check(fn(*args, None, 0, ctypes.byref(n)))
+        out = np.zeros((max(n.value, 1), 4), np.int32)
+        _check(fn(*args, out.ctypes.data, out.shape[0], ctypes.byref(n)))
+        return out[:n.value]
+
+    def halo_plan(self, nranks, level, colour, nb, cnt, rank, gather_level=-1, top_level=2) -> np.ndarray:
+        """Records {kind (0 send, 1 recv), peer, box, rows} of the (level, colour) halo exchange."""
+        nb = np.ascontiguousarray(nb, np.int32)
+        cnt = np.ascontiguousarray(cnt, np.int32)
+        return self._plan(_lib.rsrs_dist_halo_plan, (self._h, nranks, gather_level, top_level, level, colour,
+                                                     nb.ctypes.data, cnt.ctypes.data, rank))
+
+    def move_plan(self, nranks, level, k, rank, gather_level=-1, top_level=2) -> np.ndarray:
+        """Records {kind, peer, box, rows} of the skeleton-row moves level -> level-1."""
+        k = np.ascontiguousarray(k, np.int32)
+        return self._plan(_lib.rsrs_dist_move_plan, (self._h, nranks, gather_level, top_level, level,
+                                                     k.ctypes.data, rank))
+
     def plan_samples(self, kmax_guess: int = 20, oversample: int = 10) -> int:
         p = _i64()
         _check(_lib.rsrs_plan_samples(self._h, kmax_guess, oversample, ctypes.byref(p)))
@@ -248,10 +301,13 @@ def _dtype_code(t) -> int:
 
 def factor(tree: Tree, Y, Z, Omega, Psi, p: int, eps: float = 1e-6, level_growth: float = 1.0,
            id_scale: float = 1.0, oversample: int = 10, top_level: int = 2, stream=None,
-           dtype: int | None = None, profile: bool = False) -> Factorization:
+           dtype: int | None = None, profile: bool = False, comm=None, rank: int = 0, nranks: int = 1,
+           gather_level: int = -1) -> Factorization:
     """rsrs_factor on CUDA tensors (N x ld, tree order); Y, Z, Omega, Psi are OVERWRITTEN.
 
-    float64 tensors -> RSRS_F64, complex128 -> RSRS_C128 (ld in elements)."""
+    float64 tensors -> RSRS_F64, complex128 -> RSRS_C128 (ld in elements).
+    Multi-GPU (nranks > 1): this rank's rows only (Tree.partition()) and the
+    NcclComm of this rank in `comm`."""
     ld = Y.stride(0)
     code = _dtype_code(Y)
     for t in (Z, Omega, Psi):
@@ -260,11 +316,67 @@ def factor(tree: Tree, Y, Z, Omega, Psi, p: int, eps: float = 1e-6, level_growth
     if dtype is not None and dtype != code:
         raise ValueError("dtype does not match the tensors")
     dtype = code
-    o = Opts(eps, level_growth, id_scale, oversample, top_level, 0, 1, None, _stream_ptr(stream), int(profile))
+    o = Opts(eps, level_growth, id_scale, oversample, top_level, int(rank), int(nranks),
+             None if comm is None else comm.handle, _stream_ptr(stream), int(profile), int(gather_level))
     h = _vp()
     _check(_lib.rsrs_factor(tree.handle, dtype, int(p), _ptr(Y), _ptr(Z), _ptr(Omega), _ptr(Psi), int(ld),
                             ctypes.byref(o), ctypes.byref(h)))
     return Factorization(h, tree)
+
+
+class NcclComm:
+    """The library's NCCL communicator (rsrs_comm_init).  Rank 0 draws the unique
+    id; `bcast(bytes) -> bytes` ships it to the other ranks (e.g. torch.distributed)."""
+
+    def __init__(self, nranks: int, rank: int, bcast):
+        uid = ctypes.create_string_buffer(128)
+        if rank == 0:
+            _check(_lib.rsrs_comm_unique_id(uid))
+        raw = bcast(uid.raw if rank == 0 else None)
+        uid = ctypes.create_string_buffer(bytes(raw), 128)
+        h = _vp()
+        _check(_lib.rsrs_comm_init(nranks, rank, uid, ctypes.byref(h)))
+        self._h, self.nranks, self.rank = h, nranks, rank
+
+    @property
+    def handle(self):
+        return self._h
+
+    def destroy(self):
+        if self._h is not None and self._h.value:
+            _lib.rsrs_comm_destroy(self._h)
+            self._h = None
+
+
+def factor_emulated(tree: Tree, G: int, Y, Z, Omega, Psi, p: int, eps: float = 1e-6, level_growth: float = 1.0,
+                    id_scale: float = 1.0, oversample: int = 10, top_level: int = 2, gather_level: int = -1) -> list:
+    """G-rank run of the multi-GPU sweep emulated on this GPU (one host thread per rank);
+    full tree-ordered Y, Z, Omega, Psi (overwritten).  Returns the G rank factorizations."""
+    ld = Y.stride(0)
+    code = _dtype_code(Y)
+    o = Opts(eps, level_growth, id_scale, oversample, top_level, 0, G, None, None, 0, int(gather_level))
+    hs = (_vp * G)()
+    _check(_lib.rsrs_factor_emulated(tree.handle, code, int(p), int(G), _ptr(Y), _ptr(Z), _ptr(Omega), _ptr(Psi),
+                                     int(ld), ctypes.byref(o), hs))
+    return [Factorization(_vp(hs[q]), tree) for q in range(G)]
+
+
+def _emul_sweep(fn, fs, B):
+    G = len(fs)
+    hs = (_vp * G)(*[f._h.value for f in fs])
+    nrhs = 1 if B.dim() == 1 else B.shape[1]
+    ld = 1 if B.dim() == 1 else B.stride(0)
+    _check(fn(hs, G, _ptr(B), ld, nrhs))
+    return B
+
+
+def solve_emulated(fs: list, B):
+    """B <- K^-1 B through the G emulated ranks' distributed solve (full B, original order)."""
+    return _emul_sweep(_lib.rsrs_solve_emulated, fs, B)
+
+
+def apply_emulated(fs: list, X):
+    return _emul_sweep(_lib.rsrs_apply_emulated, fs, X)
 
 
 # ----------------------------------------------------------------------------

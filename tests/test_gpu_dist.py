@@ -1,0 +1,119 @@
+"""Multi-GPU sweep validated on one B200: G ranks emulated as G
+host threads (rsrs_factor_emulated), each owning a Morton range, exchanging halo
+rows / skeleton moves / solve merges through device copies.  The partitioned
+factorization must reproduce the single-GPU one bit for bit (same per-box
+arithmetic, exact exchanges) and stay within the oracle parity bar."""
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as W
+from gpu_common import dense_problem, run_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+def _emulated(cfg, X, Y, Z, Om, Ps, G, gather_level=-1):
+    import torch
+
+    import paper_2311_01451_b200 as R
+    t = R.Tree(X, cfg.leaf, *cfg.root())
+    perm = t.perm()
+    T = [torch.from_numpy(np.ascontiguousarray(M[perm])).to("cuda:0") for M in (Y, Z, Om, Ps)]
+    fs = R.factor_emulated(t, G, *T, p=cfg.p, eps=cfg.eps, level_growth=cfg.g, id_scale=cfg.c_id,
+                           oversample=cfg.l, gather_level=gather_level)
+    return t, fs
+
+
+def _solve_emul(fs, b):
+    import torch
+
+    import paper_2311_01451_b200 as R
+    x = torch.from_numpy(np.array(b, copy=True)).to("cuda:0")
+    R.solve_emulated(fs, x)
+    return x.cpu().numpy()
+
+
+def _apply_emul(fs, v):
+    import torch
+
+    import paper_2311_01451_b200 as R
+    x = torch.from_numpy(np.array(v, copy=True)).to("cuda:0")
+    R.apply_emulated(fs, x)
+    return x.cpu().numpy()
+
+
+def _single(cfg, X, Y, Z, Om, Ps):
+    import torch
+    t, f = run_gpu(cfg, X, Y, Z, Om, Ps, cfg.root())
+    return t, f
+
+
+def _check(cfg, G, gather_level=-1, X=None):
+    import torch
+    X, A, Y, Z, Om, Ps, b = dense_problem(cfg, X)
+    t1, f1 = _single(cfg, X, Y, Z, Om, Ps)
+    x1 = torch.from_numpy(b.copy()).to("cuda:0")
+    f1.solve(x1)
+    x1 = x1.cpu().numpy()
+    tg, fs = _emulated(cfg, X, Y, Z, Om, Ps, G, gather_level)
+    # ranks per box identical on every level, reported identically by every rank
+    for lev in range(tg.L, 1, -1):
+        nb = len(tg.level(lev)["keys"])
+        k1 = f1.ranks(lev, nb)
+        for f in fs:
+            assert np.array_equal(f.ranks(lev, nb), k1), lev
+    xg = _solve_emul(fs, b)
+    assert np.array_equal(xg, x1)                       # bit-exact: same per-box arithmetic
+    v = W.gaussian(X.shape[0], 5, 9, cfg.is_complex)
+    y1 = torch.from_numpy(v.copy()).to("cuda:0")
+    f1.apply(y1)
+    assert np.array_equal(_apply_emul(fs, v), y1.cpu().numpy())
+    res = np.linalg.norm(A @ xg - b) / np.linalg.norm(b)
+    assert res <= 10 * cfg.eps
+    # stored factors are split across ranks, not duplicated
+    m = sum(f.stats()["memory_scalars"] for f in fs)
+    assert m == f1.stats()["memory_scalars"]
+    return fs
+
+
+@pytest.mark.parametrize("G", [2, 3, 4])
+def test_emulated_ranks_c1_bit_exact(G):
+    """configs[0] (c1) on G emulated ranks; level 3 distributed, level 2 + top on rank 0."""
+    _check(W.CONFIGS["c1"], G)
+
+
+def test_emulated_ranks_deeper_tree_two_distributed_levels():
+    """96 x 96 grid, leaf 16: several distributed levels, straddling parents, gather above."""
+    cfg = W.Config("g96", "grid2d", 96, "log2d", "f64", leaf=16, p=544, seed=31, g=2.0)
+    _check(cfg, 3, gather_level=2)
+
+
+def test_emulated_ranks_sphere():
+    """3D sphere family (c3/c5 kernel), 27 colours, ragged leaves, on 4 emulated ranks."""
+    cfg = W.CONFIGS["c3"].scaled(8192)
+    _check(cfg, 4, gather_level=2)
+
+
+def test_emulated_ranks_complex128():
+    """c4 family (complex Helmholtz) on 2 emulated ranks."""
+    cfg = W.CONFIGS["c4"].scaled(64)
+    _check(cfg, 2)
+
+
+def test_emulated_rank_failure_is_reported_by_all():
+    """Too few samples on one rank: every rank stops and the error names level and box."""
+    import paper_2311_01451_b200 as R
+    cfg = W.CONFIGS["c1"]
+    X, A, Y, Z, Om, Ps, b = dense_problem(cfg, None, 560)
+    cfg2 = W.Config("c1_p560", "grid2d", 64, "log2d", "f64", p=560, seed=1, g=2.0)
+    with pytest.raises(R.RSRSError) as e:
+        _emulated(cfg2, X, Y, Z, Om, Ps, 2)
+    assert e.value.status == 2 and "level 3" in str(e.value)
