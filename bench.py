@@ -13,8 +13,11 @@ Workload: configs[1] of BASELINE.json (c2: 512 x 512 grid, 2D log kernel, FP64,
 N = 262144, eps = 1e-6) -- inputs (Y, Z, Omega, Psi: 6.4 GB) are larger than L2, so
 no explicit L2 flush is needed.  Sampling (Y = A Omega, Z = A^* Psi through the
 harness kernel matvec) is done once before timing (excluded, BASELINE.json
-north_star).  N > 1 (torchrun): every rank factors its own seeded instance
-(weak scaling, no data-path collective -- DESIGN.md section 7).
+north_star).  N > 1 (torchrun): ONE problem sharded over the ranks (strong scaling): each rank
+owns a Morton range of leaves, draws its own sample rows, and the sweep exchanges
+near-field halo rows per colour and skeleton rows per level over NCCL
+(include/rsrs.h multi-GPU section); the solve takes the
+replicated right-hand side.
 """
 from __future__ import annotations
 
@@ -138,22 +141,22 @@ def fp64_peak() -> dict:
 # ---------------------------------------------------------------------------
 # problem setup (seeded, synthetic; sampling excluded from timing)
 # ---------------------------------------------------------------------------
-def setup_problem(cfg, dev, seed_offset=0):
-    import dataclasses
-
+def setup_problem(cfg, dev, rank=0, world=1, pg=None):
+    """Seeded problem; with world > 1 this rank keeps only its Morton range of rows
+    (rsrs_tree_partition) and draws its own sample rows Y = A[rows, :] Omega."""
     import numpy as np
     import torch
 
     import paper_2311_01451_b200 as R
     import workloads as W
-    if seed_offset:
-        cfg = dataclasses.replace(cfg, seed=cfg.seed + seed_offset)
     X = W.points(cfg)
     t_tree = time.perf_counter()
-    tree = R.Tree(X, cfg.leaf, *cfg.root())
+    tree = R.Tree(X, cfg.leaf, *cfg.root(), nranks=world)
     t_tree = time.perf_counter() - t_tree
     perm = tree.perm()
     N = cfg.N
+    first, gather = tree.partition(world)
+    r0, r1 = int(first[rank]), int(first[rank + 1])
     Om, Ps = W.omega_psi(cfg)
     P = torch.from_numpy(perm).to(dev)
     Om_d = torch.from_numpy(Om).to(dev)[P].contiguous()
@@ -162,24 +165,37 @@ def setup_problem(cfg, dev, seed_offset=0):
     pts = np.zeros((N, 3))
     pts[:, :X.shape[1]] = X
     pts_d = torch.from_numpy(pts[perm]).to(dev)
-    Y_d = torch.empty_like(Om_d)
-    Z_d = torch.empty_like(Ps_d)
+    Y_d = torch.empty((r1 - r0, cfg.p), dtype=Om_d.dtype, device=dev)
+    Z_d = torch.empty_like(Y_d)
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
-    R.sample_matvec(cfg.kernel, pts_d, W.kernel_weight(cfg), Om_d, Y_d, kappa=cfg.kappa)
-    R.sample_matvec(cfg.kernel, pts_d, W.kernel_weight(cfg), Ps_d, Z_d, adjoint=True, kappa=cfg.kappa)
+    R.sample_matvec_rows(cfg.kernel, pts_d, W.kernel_weight(cfg), Om_d, Y_d, r0, kappa=cfg.kappa)
+    R.sample_matvec_rows(cfg.kernel, pts_d, W.kernel_weight(cfg), Ps_d, Z_d, r0, adjoint=True, kappa=cfg.kappa)
     torch.cuda.synchronize(dev)
     t_sample = time.perf_counter() - t0
+    if world > 1:
+        Om_d = Om_d[r0:r1].contiguous()
+        Ps_d = Ps_d[r0:r1].contiguous()
+        torch.cuda.empty_cache()
     b = torch.from_numpy(W.rhs(cfg)).to(dev)
+    comm = None
+    if world > 1:
+        def bcast(raw):
+            obj = [raw]
+            pg.broadcast_object_list(obj, src=0)
+            return obj[0]
+        comm = R.NcclComm(world, rank, bcast)
     return dict(cfg=cfg, X=X, tree=tree, perm=perm, P=P, pts=pts_d, src=[Y_d, Z_d, Om_d, Ps_d], b=b,
-                t_sample=t_sample, t_tree=t_tree)
+                t_sample=t_sample, t_tree=t_tree, comm=comm, rank=rank, world=world, rows=(r0, r1),
+                gather_level=gather)
 
 
 def factor_solve(pb, work, x, stream, profile=False, solve_events=None):
     import paper_2311_01451_b200 as R
     cfg = pb["cfg"]
     f = R.factor(pb["tree"], *work, p=cfg.p, eps=cfg.eps, level_growth=cfg.g, id_scale=cfg.c_id,
-                 oversample=cfg.l, stream=stream, profile=profile)
+                 oversample=cfg.l, stream=stream, profile=profile, comm=pb["comm"], rank=pb["rank"],
+                 nranks=pb["world"])
     if solve_events is not None:
         solve_events[0].record(stream)
     f.solve(x, stream=stream)
@@ -260,7 +276,7 @@ def run_native(args, rank, world, local, pg):
     dev = torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
     cfg = W.CONFIGS[args.config]
-    pb = setup_problem(cfg, dev, seed_offset=rank)
+    pb = setup_problem(cfg, dev, rank, world, pg)
     stream = torch.cuda.Stream(device=dev)
     work = [t.clone() for t in pb["src"]]
     x = pb["b"].clone()
@@ -323,8 +339,8 @@ def run_native(args, rank, world, local, pg):
         host = [t.cpu().pin_memory() for t in pb["src"]]
         hb = pb["b"].cpu().pin_memory()
         hx = torch.empty_like(hb).pin_memory()
-        h2d = sum(t.numel() * t.element_size() for t in host) + hb.numel() * 8
-        d2h = hx.numel() * 8
+        h2d = sum(t.numel() * t.element_size() for t in host) + hb.numel() * hb.element_size()
+        d2h = hx.numel() * hx.element_size()
         barrier(pg, dev)
         torch.cuda.synchronize(dev)
         g0 = torch.cuda.Event(enable_timing=True)
@@ -343,7 +359,7 @@ def run_native(args, rank, world, local, pg):
         torch.cuda.synchronize(dev)
         barrier(pg, dev)
         gms = max_over_ranks(g0.elapsed_time(g1), pg, dev)
-        e2e = {"value": world * N * args.e2e_steps / (gms * 1e-3), "unit": "DOF/s", "h2d_bytes_per_step": int(h2d),
+        e2e = {"value": N * args.e2e_steps / (gms * 1e-3), "unit": "DOF/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": gms / args.e2e_steps}
     if rank != 0:
         return
@@ -368,18 +384,19 @@ def run_native(args, rank, world, local, pg):
     breakdown = {k: {"ms_per_step": v["ms"] / args.steps, "tflops": v["flops"] / max(v["ms"], 1e-9) / 1e9,
                      "gbs": v["bytes"] / max(v["ms"], 1e-9) / 1e6} for k, v in prof.items() if v["launches"]}
     cpu = None
-    if not args.no_cpu:
+    if not args.no_cpu and world == 1:
         nbx = args.cpu_boxes or 96
         dofs, times, desc = oracle_sample(cfg, nbx, reps=1)
         cpu = {"value": dofs / times[0], "unit": "DOF/s", "cores": 1, "kind": "oracle", "sample": desc,
                "seconds": times[0]}
     sweep_tf = st["flops_model"] / (st["factor_ms"] * 1e-3) / 1e12
-    line = {"metric": METRIC, "value": world * N * args.steps / (ms * 1e-3), "unit": "DOF/s", "n_gpus": world,
+    line = {"metric": METRIC, "value": N * args.steps / (ms * 1e-3), "unit": "DOF/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
             "config": {"workload": cfg.name, "N": N, "p": cfg.p, "eps": cfg.eps, "g": cfg.g, "leaf": cfg.leaf,
                        "kernel": cfg.kernel, "L": st["L"], "l2": "inputs 6.4 GB > 126 MB L2 (no flush needed)",
-                       "step": "restore samples + rsrs_factor + rsrs_solve(1 rhs)", "parallelism": f"replicas{world}"},
+                       "step": "restore samples + rsrs_factor + rsrs_solve(1 rhs)", "parallelism": (f"morton-range x{world}, halo exchange, gather at level {pb['gather_level']}"
+                                       if world > 1 else "single GPU")},
             "factor_ms": st["factor_ms"], "solve_ms": statistics.median(solve_ms), "sample_s": pb["t_sample"], "tree_s": pb["t_tree"],
             "residual": resid, "top_size": st["top_size"], "max_rank": st["max_rank"],
             "memory_scalars": st["memory_scalars"], "sweep_tflops": sweep_tf,

@@ -224,6 +224,8 @@ rsrs_status rsrs_dist_move_plan(rsrs_tree t, int nranks, int gather_level, int t
 rsrs_status rsrs_comm_unique_id(void* id128);
 rsrs_status rsrs_comm_init(int nranks, int rank, const void* id128, void** comm);
 void rsrs_comm_destroy(void* comm);
+/* Transport self-test (all ranks call it): all-reduces and a ring exchange. */
+rsrs_status rsrs_comm_selftest(void* comm, int nranks, int rank);
 
 /* Single-GPU emulation of a G-rank run (validation of the multi-GPU path on one
  * device): G host threads, one per rank, each with its own stream, exchanging

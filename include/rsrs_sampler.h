@@ -33,6 +33,12 @@ int rsrs_sample_matvec(int kind, const double* pts, int64_t N, double weight, co
  * columns used; adjoint 1 computes A^* X.  Same return codes. */
 int rsrs_sample_matvec_c128(const double* pts, int64_t N, double weight, double kappa, const void* X,
                             int64_t ldx, void* Y, int64_t ldy, int64_t ncol, int adjoint, void* stream);
+/* Rows [row0, row0 + nrows) of Y = A X (or A^* X) for any kind (0 log2d, 1
+ * lap3d real; 2 helm2d complex128 with kappa): Y holds nrows rows (ldy), X all N
+ * rows.  Used by each rank of a multi-GPU run to draw its own sample rows. */
+int rsrs_sample_matvec_rows(int kind, const double* pts, int64_t N, int64_t row0, int64_t nrows, double weight,
+                            double kappa, const void* X, int64_t ldx, void* Y, int64_t ldy, int64_t ncol,
+                            int adjoint, void* stream);
 const char* rsrs_sampler_last_error(void);
 
 #ifdef __cplusplus

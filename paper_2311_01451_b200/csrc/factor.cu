@@ -1649,6 +1649,50 @@ rsrs_status rsrs_comm_init(int nranks, int rank, const void* id128, void** comm)
   return RSRS_OK;
 }
 
+// Transport self-test on a live communicator (every rank calls it): max and sum
+// all-reduces and a ring exchange (rank -> rank+1; a self-exchange on one rank).
+rsrs_status rsrs_comm_selftest(void* comm, int nranks, int rank) {
+  rsrs::clear_error();
+  if (!comm || nranks < 1 || rank < 0 || rank >= nranks) return fail(RSRS_ERR_INVALID, "rsrs_comm_selftest: invalid argument");
+  if (!rsrs::NcclApi::get().ok()) return fail(RSRS_ERR_NCCL, "rsrs_comm_selftest: libnccl.so.2 not loadable");
+  try {
+    rsrs::NcclComm c(comm, rank, nranks);
+    cudaStream_t s;
+    CK(cudaStreamCreate(&s));
+    std::vector<int> v = {rank, -rank, 7};
+    c.allreduce_max_i32(v.data(), v.size(), s);
+    if (v[0] != nranks - 1 || v[1] != 0 || v[2] != 7) throw StatusError{RSRS_ERR_NCCL, "allreduce max mismatch"};
+    const int n = 1000;
+    double *a, *b;
+    CK(cudaMalloc(&a, sizeof(double) * n));
+    CK(cudaMalloc(&b, sizeof(double) * n));
+    std::vector<double> h(n);
+    for (int i = 0; i < n; ++i) h[i] = rank + 0.5 * i;
+    CK(cudaMemcpy(a, h.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+    c.exchange({{(rank + 1) % nranks, a, sizeof(double) * n}}, {{(rank + nranks - 1) % nranks, b, sizeof(double) * n}}, s);
+    c.allreduce_sum_f64(a, n, s);
+    CK(cudaStreamSynchronize(s));
+    std::vector<double> ha(n), hb(n);
+    CK(cudaMemcpy(ha.data(), a, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hb.data(), b, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    cudaFree(a);
+    cudaFree(b);
+    cudaStreamDestroy(s);
+    const int src = (rank + nranks - 1) % nranks;
+    for (int i = 0; i < n; ++i) {
+      if (hb[i] != src + 0.5 * i) throw StatusError{RSRS_ERR_NCCL, "exchange mismatch"};
+      if (ha[i] != nranks * (nranks - 1) / 2.0 + nranks * 0.5 * i) throw StatusError{RSRS_ERR_NCCL, "allreduce sum mismatch"};
+    }
+    return RSRS_OK;
+  } catch (const StatusError& e) {
+    return fail(e.st, "rsrs_comm_selftest: " + e.msg);
+  } catch (const CudaError& e) {
+    return fail(RSRS_ERR_CUDA, "rsrs_comm_selftest: " + e.msg);
+  } catch (const rsrs::CommError& e) {
+    return fail(RSRS_ERR_NCCL, "rsrs_comm_selftest: " + e.msg);
+  }
+}
+
 void rsrs_comm_destroy(void* comm) {
   rsrs::NcclApi& A = rsrs::NcclApi::get();
   if (comm && A.commDestroy) A.commDestroy(comm);

@@ -26,8 +26,9 @@ __device__ __forceinline__ double kval(int kind, double r, double w) {
   return w / r;                            // 3D Laplace single layer
 }
 
-__global__ void __launch_bounds__(128) matvec_real_kernel(const double* __restrict__ pts, int64_t N,
-                                                          const double* __restrict__ X, int64_t ldx,
+// rows [row0, row0 + nrows) of Y = A X (Y holds only those rows)
+__global__ void __launch_bounds__(128) matvec_real_kernel(const double* __restrict__ pts, int64_t N, int64_t row0,
+                                                          int64_t nrows, const double* __restrict__ X, int64_t ldx,
                                                           double* __restrict__ Y, int64_t ldy, int ncol,
                                                           int kind, double w) {
   __shared__ double As[TM * SA];
@@ -36,11 +37,12 @@ __global__ void __launch_bounds__(128) matvec_real_kernel(const double* __restri
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const int wr = warp >> 1, wc = warp & 1;
-  const int64_t i0 = (int64_t)blockIdx.y * TM;
+  const int64_t i0 = row0 + (int64_t)blockIdx.y * TM;
+  const int64_t iend = row0 + nrows;
   const int j0 = blockIdx.x * TN;
   for (int t = tid; t < TM * 3; t += 128) {
     const int64_t gi = i0 + t / 3;
-    Pi[t] = gi < N ? pts[gi * 3 + t % 3] : 0.0;
+    Pi[t] = gi < iend ? pts[gi * 3 + t % 3] : 0.0;
   }
   double acc[4][4][2];
 #pragma unroll
@@ -54,7 +56,7 @@ __global__ void __launch_bounds__(128) matvec_real_kernel(const double* __restri
       const int ii = t / TK, kk = t % TK;
       const int64_t gi = i0 + ii, gk = k0 + kk;
       double v = 0.0;
-      if (gi < N && gk < N) {
+      if (gi < iend && gk < N) {
         if (gi == gk) {
           v = 1.0;
         } else {
@@ -89,12 +91,12 @@ __global__ void __launch_bounds__(128) matvec_real_kernel(const double* __restri
 #pragma unroll
   for (int t = 0; t < 4; ++t) {
     const int64_t i = i0 + wr * 32 + t * 8 + gid;
-    if (i >= N) continue;
+    if (i >= iend) continue;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int j = j0 + wc * 32 + u * 8 + 2 * tig;
-      if (j < ncol) Y[i * ldy + j] = acc[t][u][0];
-      if (j + 1 < ncol) Y[i * ldy + j + 1] = acc[t][u][1];
+      if (j < ncol) Y[(i - row0) * ldy + j] = acc[t][u][0];
+      if (j + 1 < ncol) Y[(i - row0) * ldy + j + 1] = acc[t][u][1];
     }
   }
 }
@@ -109,6 +111,7 @@ constexpr int CSB = CTN + 4;
 constexpr int CPLX_SMEM = (2 * TM * SA + TK * CSB + TM * 3) * 8;
 
 __global__ void __launch_bounds__(256) matvec_cplx_kernel(const double* __restrict__ pts, int64_t N,
+                                                          int64_t row0, int64_t nrows,
                                                           const double* __restrict__ X, int64_t ldx,
                                                           double* __restrict__ Y, int64_t ldy, int ncol,
                                                           double w, double kappa, int adjoint) {
@@ -120,13 +123,14 @@ __global__ void __launch_bounds__(256) matvec_cplx_kernel(const double* __restri
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const int wr = warp >> 2, wc = warp & 3;
-  const int64_t i0 = (int64_t)blockIdx.y * TM;
+  const int64_t i0 = row0 + (int64_t)blockIdx.y * TM;
+  const int64_t iend = row0 + nrows;
   const int c0 = blockIdx.x * (CTN / 2);            // complex column
   const int ncol2 = 2 * ncol;
   const double sgn_im = adjoint ? -1.0 : 1.0;
   for (int t = tid; t < TM * 3; t += 256) {
     const int64_t gi = i0 + t / 3;
-    Pi[t] = gi < N ? pts[gi * 3 + t % 3] : 0.0;
+    Pi[t] = gi < iend ? pts[gi * 3 + t % 3] : 0.0;
   }
   double acc[4][4][2];
 #pragma unroll
@@ -139,7 +143,7 @@ __global__ void __launch_bounds__(256) matvec_cplx_kernel(const double* __restri
       const int ii = t / TK, kk = t % TK;
       const int64_t gi = i0 + ii, gk = k0 + kk;
       double vr = 0.0, vi = 0.0;
-      if (gi < N && gk < N) {
+      if (gi < iend && gk < N) {
         if (gi == gk) {
           vr = 1.0;
         } else {
@@ -188,13 +192,13 @@ __global__ void __launch_bounds__(256) matvec_cplx_kernel(const double* __restri
 #pragma unroll
   for (int t = 0; t < 4; ++t) {
     const int64_t i = i0 + wr * 32 + t * 8 + gid;
-    if (i >= N) continue;
+    if (i >= iend) continue;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int j = 2 * c0 + wc * 32 + u * 8 + 2 * tig;   // real column (even)
       if (j < ncol2) {
-        Y[i * 2 * ldy + j] = acc[t][u][0];
-        Y[i * 2 * ldy + j + 1] = acc[t][u][1];
+        Y[(i - row0) * 2 * ldy + j] = acc[t][u][0];
+        Y[(i - row0) * 2 * ldy + j + 1] = acc[t][u][1];
       }
     }
   }
@@ -208,40 +212,47 @@ extern "C" {
 
 const char* rsrs_sampler_last_error(void) { return g_err.c_str(); }
 
-int rsrs_sample_matvec(int kind, const double* pts, int64_t N, double weight, const void* X, int64_t ldx,
-                       void* Y, int64_t ldy, int64_t ncol, int adjoint, void* stream) {
-  (void)adjoint;  // real kernels here are symmetric: A^* = A
-  if (kind < 0 || kind > 1 || !pts || !X || !Y || N < 1 || ncol < 1 || ldx < ncol || ldy < ncol) {
-    g_err = "rsrs_sample_matvec: invalid argument";
+int rsrs_sample_matvec_rows(int kind, const double* pts, int64_t N, int64_t row0, int64_t nrows, double weight,
+                            double kappa, const void* X, int64_t ldx, void* Y, int64_t ldy, int64_t ncol,
+                            int adjoint, void* stream) {
+  if (kind < 0 || kind > 2 || !pts || !X || !Y || N < 1 || row0 < 0 || nrows < 0 || row0 + nrows > N ||
+      ncol < 1 || ldx < ncol || ldy < ncol) {
+    g_err = "rsrs_sample_matvec_rows: invalid argument";
     return 1;
   }
-  dim3 grid((unsigned)((ncol + TN - 1) / TN), (unsigned)((N + TM - 1) / TM));
-  matvec_real_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(pts, N, (const double*)X, ldx, (double*)Y, ldy,
-                                                             (int)ncol, kind, weight);
+  if (nrows == 0) return 0;
+  if (kind == 2) {
+    dim3 grid((unsigned)((ncol + CTN / 2 - 1) / (CTN / 2)), (unsigned)((nrows + TM - 1) / TM));
+    cudaFuncSetAttribute(matvec_cplx_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, CPLX_SMEM);
+    matvec_cplx_kernel<<<grid, 256, CPLX_SMEM, (cudaStream_t)stream>>>(pts, N, row0, nrows, (const double*)X, ldx,
+                                                                       (double*)Y, ldy, (int)ncol, weight, kappa,
+                                                                       adjoint);
+  } else {
+    // the real kernels here are symmetric: A^* = A
+    dim3 grid((unsigned)((ncol + TN - 1) / TN), (unsigned)((nrows + TM - 1) / TM));
+    matvec_real_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(pts, N, row0, nrows, (const double*)X, ldx,
+                                                               (double*)Y, ldy, (int)ncol, kind, weight);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
-    g_err = std::string("rsrs_sample_matvec: ") + cudaGetErrorString(e);
+    g_err = std::string("rsrs_sample_matvec_rows: ") + cudaGetErrorString(e);
     return 4;
   }
   return 0;
 }
 
-int rsrs_sample_matvec_c128(const double* pts, int64_t N, double weight, double kappa, const void* X,
-                            int64_t ldx, void* Y, int64_t ldy, int64_t ncol, int adjoint, void* stream) {
-  if (!pts || !X || !Y || N < 1 || ncol < 1 || ldx < ncol || ldy < ncol) {
-    g_err = "rsrs_sample_matvec_c128: invalid argument";
+int rsrs_sample_matvec(int kind, const double* pts, int64_t N, double weight, const void* X, int64_t ldx,
+                       void* Y, int64_t ldy, int64_t ncol, int adjoint, void* stream) {
+  if (kind < 0 || kind > 1) {
+    g_err = "rsrs_sample_matvec: invalid kind (0 log2d, 1 lap3d; complex kinds: rsrs_sample_matvec_c128)";
     return 1;
   }
-  dim3 grid((unsigned)((ncol + CTN / 2 - 1) / (CTN / 2)), (unsigned)((N + TM - 1) / TM));
-  cudaFuncSetAttribute(matvec_cplx_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, CPLX_SMEM);
-  matvec_cplx_kernel<<<grid, 256, CPLX_SMEM, (cudaStream_t)stream>>>(pts, N, (const double*)X, ldx, (double*)Y, ldy,
-                                                             (int)ncol, weight, kappa, adjoint);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) {
-    g_err = std::string("rsrs_sample_matvec_c128: ") + cudaGetErrorString(e);
-    return 4;
-  }
-  return 0;
+  return rsrs_sample_matvec_rows(kind, pts, N, 0, N, weight, 0.0, X, ldx, Y, ldy, ncol, adjoint, stream);
+}
+
+int rsrs_sample_matvec_c128(const double* pts, int64_t N, double weight, double kappa, const void* X,
+                            int64_t ldx, void* Y, int64_t ldy, int64_t ncol, int adjoint, void* stream) {
+  return rsrs_sample_matvec_rows(2, pts, N, 0, N, weight, kappa, X, ldx, Y, ldy, ncol, adjoint, stream);
 }
 
 }  // extern "C"

@@ -34,7 +34,7 @@ EXPORTS = [
     "rsrs_factor_stats", "rsrs_factor_ranks", "rsrs_factor_top", "rsrs_factor_destroy", "rsrs_factor_profile",
     "rsrs_last_error", "rsrs_version", "rsrs_memory_info", "rsrs_release_memory",
     "rsrs_tree_partition", "rsrs_dist_owner", "rsrs_dist_halo_plan", "rsrs_dist_move_plan",
-    "rsrs_comm_unique_id", "rsrs_comm_init", "rsrs_comm_destroy",
+    "rsrs_comm_unique_id", "rsrs_comm_init", "rsrs_comm_destroy", "rsrs_comm_selftest",
     "rsrs_factor_emulated", "rsrs_solve_emulated", "rsrs_apply_emulated",
 ]
 
@@ -93,6 +93,8 @@ _lib.rsrs_comm_unique_id.argtypes = [_vp]
 _lib.rsrs_comm_init.argtypes = [_i32, _i32, _vp, ctypes.POINTER(_vp)]
 _lib.rsrs_comm_destroy.argtypes = [_vp]
 _lib.rsrs_comm_destroy.restype = None
+_lib.rsrs_comm_selftest.argtypes = [_vp, _i32, _i32]
+_lib.rsrs_comm_selftest.restype = ctypes.c_int
 _lib.rsrs_factor_emulated.argtypes = [_vp, _i32, _i64, _i32, _vp, _vp, _vp, _vp, _i64, ctypes.POINTER(Opts), _vp]
 _lib.rsrs_solve_emulated.argtypes = [_vp, _i32, _vp, _i64, _i64]
 _lib.rsrs_apply_emulated.argtypes = [_vp, _i32, _vp, _i64, _i64]
@@ -342,6 +344,10 @@ class NcclComm:
     def handle(self):
         return self._h
 
+    def selftest(self):
+        """All-reduces and a ring exchange through the library's NCCL transport."""
+        _check(_lib.rsrs_comm_selftest(self._h, self.nranks, self.rank))
+
     def destroy(self):
         if self._h is not None and self._h.value:
             _lib.rsrs_comm_destroy(self._h)
@@ -397,6 +403,9 @@ def _sampler_lib():
         s.rsrs_sampler_last_error.restype = ctypes.c_char_p
         s.rsrs_sample_matvec_c128.argtypes = [_vp, _i64, _d, _d, _vp, _i64, _vp, _i64, _i64, _i32, _vp]
         s.rsrs_sample_matvec_c128.restype = ctypes.c_int
+        s.rsrs_sample_matvec_rows.argtypes = [_i32, _vp, _i64, _i64, _i64, _d, _d, _vp, _i64, _vp, _i64, _i64, _i32,
+                                              _vp]
+        s.rsrs_sample_matvec_rows.restype = ctypes.c_int
         _sampler = s
     return _sampler
 
@@ -416,6 +425,22 @@ def sample_matvec(kind: str, pts3, weight: float, X, Y, adjoint: bool = False, s
     else:
         st = s.rsrs_sample_matvec(KERNEL_KIND[kind], _ptr(pts3), N, float(weight), _ptr(X), ldx, _ptr(Y), ldy,
                                   ncol, int(adjoint), _stream_ptr(stream))
+    if st != 0:
+        raise RSRSError(st, s.rsrs_sampler_last_error().decode())
+    return Y
+
+
+def sample_matvec_rows(kind: str, pts3, weight: float, X, Y, row0: int, adjoint: bool = False, stream=None,
+                       kappa: float = 25.0):
+    """Rows [row0, row0 + Y.shape[0]) of A X (multi-GPU sampling of a rank's own rows)."""
+    s = _sampler_lib()
+    N = pts3.shape[0]
+    nrows = Y.shape[0]
+    ncol = 1 if X.dim() == 1 else X.shape[1]
+    ldx = 1 if X.dim() == 1 else X.stride(0)
+    ldy = 1 if Y.dim() == 1 else Y.stride(0)
+    st = s.rsrs_sample_matvec_rows(KERNEL_KIND[kind], _ptr(pts3), N, int(row0), int(nrows), float(weight),
+                                   float(kappa), _ptr(X), ldx, _ptr(Y), ldy, ncol, int(adjoint), _stream_ptr(stream))
     if st != 0:
         raise RSRSError(st, s.rsrs_sampler_last_error().decode())
     return Y

@@ -117,3 +117,12 @@ def test_emulated_rank_failure_is_reported_by_all():
     with pytest.raises(R.RSRSError) as e:
         _emulated(cfg2, X, Y, Z, Om, Ps, 2)
     assert e.value.status == 2 and "level 3" in str(e.value)
+
+
+def test_nccl_transport_single_rank():
+    """The library's NCCL transport (dlopen'ed libnccl.so.2, ncclCommInitRank with the
+    id passed by value, grouped send/recv, all-reduce) on a one-rank communicator."""
+    import paper_2311_01451_b200 as R
+    c = R.NcclComm(1, 0, lambda raw: raw)
+    c.selftest()
+    c.destroy()
