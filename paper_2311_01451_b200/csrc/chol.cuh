@@ -49,73 +49,104 @@ __global__ void __launch_bounds__(128) chol_update_kernel(const CholDesc* __rest
   nt_tile_t<C>(d, m, n, j0, i0, jt, smem);
 }
 
-// Cholesky of the diagonal block P[J, J] (in place) and L_JJ^-1 (to linv[J])
-constexpr int CHOL_DIAG_SMEM = 2 * CB * (CB + 1) * 8;   // >= the complex 32 x 32 case
+// Cholesky of the diagonal block P[J, J] (in place) and L_JJ^-1 (to linv[J]).
+// Gaussian elimination without pivoting on the augmented [C_JJ | I] held in
+// REGISTERS (thread t owns rows t/16 + 16a, columns t%16 + 16b): after step c,
+// C = Lt D Lt^* gives L[:, c] = a[:, c] / sqrt(d_c) and the I part becomes
+// Lt^-1, so L^-1 = D^-1/2 Lt^-1 comes out of the same sweep (no serial
+// triangular inverse).  One barrier per column (column c and row c are
+// broadcast through double-buffered shared memory).
+constexpr int CHOL_DIAG_SMEM = 2 * CB * (CB + 1) * 8;   // dynamic smem reserved (kernel uses static smem)
 
 template <bool C>
 __global__ void __launch_bounds__(256) chol_diag_kernel(const CholDesc* __restrict__ cds, int j0) {
   constexpr int CBW = cbw<C>();
   typedef typename ScalarOf<C>::T S;
-  extern __shared__ __align__(16) double dsm[];
-  S (*Ls)[CBW + 1] = reinterpret_cast<S (*)[CBW + 1]>(dsm);
-  S (*Is)[CBW + 1] = reinterpret_cast<S (*)[CBW + 1]>(reinterpret_cast<S*>(dsm) + CBW * (CBW + 1));
-  __shared__ int bad;
+  constexpr int RA = CBW / 16, CA = 2 * CBW / 16;      // owned rows / columns per thread
+  __shared__ S colbuf[2][CBW];
+  __shared__ S rowbuf[2][2 * CBW];
+  __shared__ double pivs[CBW];
   const CholDesc& cd = cds[blockIdx.x];
   if (cd.status && *cd.status != ST_OK) return;
   const int r = *cd.pr;
   if (j0 >= r) return;
   const int jb = min(CBW, r - j0);
   const int tid = threadIdx.x;
-  const S zero = s_zero(S());
+  const int tr = tid >> 4, tc = tid & 15;
+  const S zero = s_zero(S()), one = s_one(S());
   S* A = reinterpret_cast<S*>(cd.A) + (i64)j0 * cd.lda + j0;
-  for (int idx = tid; idx < CBW * CBW; idx += 256) {
-    const int i = idx / CBW, j = idx % CBW;
-    Ls[i][j] = (i < jb && j <= i) ? A[(i64)i * cd.lda + j] : zero;
-  }
-  if (tid == 0) bad = 0;
-  __syncthreads();
-  for (int c = 0; c < jb; ++c) {
-    const double dcc = s_real(Ls[c][c]);
-    if (!(dcc > 0.0)) {
-      if (tid == 0) bad = 1;
-      break;
+  S a[RA][CA];
+#pragma unroll
+  for (int ra = 0; ra < RA; ++ra) {
+    const int i = tr + 16 * ra;
+#pragma unroll
+    for (int cb = 0; cb < CA; ++cb) {
+      const int j = tc + 16 * cb;
+      S v;
+      if (j < CBW) {   // C part: Hermitian from the lower triangle; identity on padding rows
+        if (i < jb && j < jb) v = (j <= i) ? A[(i64)i * cd.lda + j] : s_conj(A[(i64)j * cd.lda + i]);
+        else v = (i == j) ? one : zero;
+      } else {
+        v = (j - CBW == i) ? one : zero;
+      }
+      a[ra][cb] = v;
     }
-    const double lcc = sqrt(dcc);
-    __syncthreads();
-    for (int i = c + 1 + tid; i < jb; i += 256) Ls[i][c] = s_scale(Ls[i][c], 1.0 / lcc);
-    if (tid == 0) Ls[c][c] = s_scale(s_one(S()), lcc);
-    __syncthreads();
-    const int nt = jb - c - 1;
-    for (int idx = tid; idx < nt * nt; idx += 256) {
-      const int i = c + 1 + idx / nt, j = c + 1 + idx % nt;
-      if (j <= i) Ls[i][j] = s_sub(Ls[i][j], s_mulc(Ls[i][c], Ls[j][c]));
-    }
-    __syncthreads();
   }
-  __syncthreads();
+  bool bad = false;
+  // c = 16 * cblk + cc: the owned slot of column / row c is the compile-time cblk
+#pragma unroll
+  for (int cblk = 0; cblk < CBW / 16; ++cblk) {
+    for (int cc = 0; cc < 16 && !bad; ++cc) {
+      const int c = 16 * cblk + cc;
+      if (c >= jb) break;
+      const int buf = c & 1;
+      if (tc == cc)                       // owners of column c (C part)
+#pragma unroll
+        for (int ra = 0; ra < RA; ++ra) colbuf[buf][tr + 16 * ra] = a[ra][cblk];
+      if (tr == cc)                       // owners of row c
+#pragma unroll
+        for (int cb = 0; cb < CA; ++cb) rowbuf[buf][tc + 16 * cb] = a[cblk][cb];
+      __syncthreads();
+      const double piv = s_real(colbuf[buf][c]);
+      if (!(piv > 0.0)) {
+        bad = true;
+        break;
+      }
+      const double rs = 1.0 / sqrt(piv), rp = 1.0 / piv;
+      if (tid < jb && tid >= c) A[(i64)tid * cd.lda + c] = s_scale(colbuf[buf][tid], rs);   // L[:, c]
+      if (tid == 0) pivs[c] = piv;
+      // rows i > c: a[i, :] -= (a[i, c] / piv) a[c, :] over ALL owned columns: the I part of
+      // row c is exactly zero right of c, and the C part left of the diagonal (never read
+      // again) just collects rounding residue -- no per-element predicates
+      S rb[CA];
+#pragma unroll
+      for (int cb = 0; cb < CA; ++cb) rb[cb] = rowbuf[buf][tc + 16 * cb];
+#pragma unroll
+      for (int ra = 0; ra < RA; ++ra) {
+        const int i = tr + 16 * ra;
+        const S m = (i > c) ? s_scale(colbuf[buf][i], rp) : zero;
+#pragma unroll
+        for (int cb = 0; cb < CA; ++cb) a[ra][cb] = s_sub(a[ra][cb], s_mul(m, rb[cb]));
+      }
+    }
+  }
   if (bad) {
     if (tid == 0 && cd.status) *cd.status = ST_SINGULAR_GRAM;
     return;
   }
-  // L^-1 column by column (lower triangular), zero padded to 64 x 64
-  if (tid < CBW) {
-    const int j = tid;
-    for (int i = 0; i < CBW; ++i) Is[i][j] = zero;
-    if (j < jb) {
-      Is[j][j] = s_div(s_one(S()), Ls[j][j]);
-      for (int i = j + 1; i < jb; ++i) {
-        S s = zero;
-        for (int q = j; q < i; ++q) s = s_add(s, s_mul(Ls[i][q], Is[q][j]));
-        Is[i][j] = s_neg(s_div(s, Ls[i][i]));
-      }
-    }
-  }
   __syncthreads();
+  // L^-1 = D^-1/2 Lt^-1 (zero padded beyond jb)
   S* linv = reinterpret_cast<S*>(cd.linv) + (i64)(j0 / CBW) * CBW * CBW;
-  for (int idx = tid; idx < CBW * CBW; idx += 256) {
-    const int i = idx / CBW, j = idx % CBW;
-    linv[idx] = Is[i][j];
-    if (i < jb && j <= i) A[(i64)i * cd.lda + j] = Ls[i][j];
+#pragma unroll
+  for (int ra = 0; ra < RA; ++ra) {
+    const int i = tr + 16 * ra;
+#pragma unroll
+    for (int cb = 0; cb < CA; ++cb) {
+      const int j = tc + 16 * cb;
+      if (j < CBW) continue;
+      const int jj = j - CBW;
+      linv[i * CBW + jj] = (i < jb && jj < jb) ? s_scale(a[ra][cb], 1.0 / sqrt(pivs[i])) : zero;
+    }
   }
 }
 

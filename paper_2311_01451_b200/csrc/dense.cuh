@@ -193,6 +193,125 @@ __global__ void __launch_bounds__(256) id_kernel(BoxDev* __restrict__ boxes, con
 }
 
 // ---------------------------------------------------------------------------
+// X^-1 of an n x n matrix (n <= 64) by Gauss-Jordan elimination with partial
+// pivoting on the augmented [X | I] held in REGISTERS (256 threads; thread t
+// owns rows t/16 + 16a, columns t%16 + 16b of the 64 x 128 block).  Pivot rows
+// are not swapped: step c eliminates column c from every other row with the
+// largest remaining |x_ic| (argmax computed redundantly by every warp with
+// shuffles), so the left half ends as a permutation and X^-1[c, :] is the
+// right half of the step-c pivot row.  Two barriers per column.
+// Returns false (on every thread) if a pivot is exactly zero.
+// ---------------------------------------------------------------------------
+template <class S>
+__device__ bool gj_inverse_reg(const S* __restrict__ Xs, int ldx, int n, S* __restrict__ Xinv, int ldo,
+                               S* colbuf /* smem [2][64] */, S* rowbuf /* smem [2][128] */, int* prow /* smem [64] */) {
+  constexpr int RA = 4, CA = 8;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int tr = tid >> 4, tc = tid & 15;
+  const S zero = s_zero(S()), one = s_one(S());
+  S a[RA][CA];
+#pragma unroll
+  for (int ra = 0; ra < RA; ++ra) {
+    const int i = tr + 16 * ra;
+#pragma unroll
+    for (int cb = 0; cb < CA; ++cb) {
+      const int j = tc + 16 * cb;
+      S v;
+      if (j < 64) v = (i < n && j < n) ? Xs[i * ldx + j] : (i == j ? one : zero);
+      else v = (j - 64 == i) ? one : zero;
+      a[ra][cb] = v;
+    }
+  }
+  unsigned long long used = 0;           // rows already used as pivots (same on every thread)
+  bool ok = true;
+#pragma unroll
+  for (int cblk = 0; cblk < 4; ++cblk) {
+    for (int cc = 0; cc < 16 && ok; ++cc) {
+      const int c = 16 * cblk + cc;
+      if (c >= n) break;
+      const int buf = c & 1;
+      if (tc == cc)
+#pragma unroll
+        for (int ra = 0; ra < RA; ++ra) colbuf[buf * 64 + tr + 16 * ra] = a[ra][cblk];
+      __syncthreads();
+      // argmax |x_ic| over unused rows i < n (lowest index on ties), in every warp
+      double bv = -1.0;
+      int bi = 64;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = lane + 32 * h;
+        if (i < n && !((used >> i) & 1ull)) {
+          const double v = s_abs(colbuf[buf * 64 + i]);
+          if (v > bv || (v == bv && i < bi)) {
+            bv = v;
+            bi = i;
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if (!(bv > 0.0)) {
+        ok = false;
+        break;
+      }
+      const int pr = bi;
+      used |= 1ull << pr;
+      if (tid == 0) prow[c] = pr;
+      if (tr == (pr & 15)) {              // owners of the pivot row publish it (select chain:
+        const int sel = pr >> 4;          // no dynamic register indexing)
+#pragma unroll
+        for (int cb = 0; cb < CA; ++cb) {
+          S v = a[0][cb];
+#pragma unroll
+          for (int ra = 1; ra < RA; ++ra) v = (ra == sel) ? a[ra][cb] : v;
+          rowbuf[buf * 128 + tc + 16 * cb] = v;
+        }
+      }
+      __syncthreads();
+      const S piv = colbuf[buf * 64 + pr];
+      const S rpiv = s_div(one, piv);
+#pragma unroll
+      for (int ra = 0; ra < RA; ++ra) {
+        const int i = tr + 16 * ra;
+        if (i == pr) {
+#pragma unroll
+          for (int cb = 0; cb < CA; ++cb) a[ra][cb] = s_mul(a[ra][cb], rpiv);
+        } else {
+          const S m = s_mul(colbuf[buf * 64 + i], rpiv);
+#pragma unroll
+          for (int cb = 0; cb < CA; ++cb) a[ra][cb] = s_sub(a[ra][cb], s_mul(m, rowbuf[buf * 128 + tc + 16 * cb]));
+        }
+      }
+    }
+  }
+  if (!ok) return false;
+  __syncthreads();
+  // X^-1[c, :] = right half of pivot row prow[c]; invert the map through colbuf's int view
+  int* pos = reinterpret_cast<int*>(rowbuf);   // row -> step
+  if (tid < n) pos[prow[tid]] = tid;
+  __syncthreads();
+#pragma unroll
+  for (int ra = 0; ra < RA; ++ra) {
+    const int i = tr + 16 * ra;
+    if (i >= n) continue;
+    const int c = pos[i];
+#pragma unroll
+    for (int cb = 4; cb < CA; ++cb) {
+      const int j = tc + 16 * cb - 64;
+      if (j < n) Xinv[(i64)c * ldo + j] = a[ra][cb];
+    }
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------------------
 // Block extraction + elimination factors of one box (PAPER.md:1213-1218,
 // 934-955).  X_Y = Yhat_r Omegahat_near^dagger evaluated through the
 // pre-update pseudo-inverse: Omegahat_near = F_loc Omega_near =>
@@ -287,6 +406,16 @@ __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ bo
     Xcr[(i64)j * ldn + i] = s_conj(XZ[(i64)i * ldr + cpos[j]]);   // X_cr = (X_Z)^*
   }
   __syncthreads();
+  if (nr <= 64) {
+    // 4-5. X_rr^-1 by register Gauss-Jordan (the LU factors themselves are not stored)
+    __shared__ S gj_col[2 * 64];
+    __shared__ S gj_row[2 * 128];
+    __shared__ int gj_prow[64];
+    if (!gj_inverse_reg<S>(Xs, ldx, nr, fpool + b.f_Xinv, ldn, gj_col, gj_row, gj_prow)) {
+      if (threadIdx.x == 0) b.status = ST_SINGULAR_XRR;
+    }
+    return;
+  }
   // 4. LU with partial pivoting
   for (int c = 0; c < nr; ++c) {
     if (warp == 0) {

@@ -95,6 +95,8 @@ void set_smem(K kern, int want) {
   CK(cudaFuncGetAttributes(&fa, kern));
   const int mx = g_optin - (int)fa.sharedSizeBytes;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, want < 0 ? mx : std::min(want, mx)));
+  // prefer the largest shared-memory carveout so that several tile CTAs fit per SM
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
 }
 
 template <bool C>
@@ -103,7 +105,6 @@ void set_smem_both() {
   set_smem(rsrs::chol_trsm_kernel<C>, rsrs::NT_SMEM);
   set_smem(rsrs::chol_back_a_kernel<C>, rsrs::NN_SMEM);
   set_smem(rsrs::chol_back_b_kernel<C>, rsrs::NN_SMEM);
-  set_smem(rsrs::chol_diag_kernel<C>, rsrs::CHOL_DIAG_SMEM);
   set_smem(rsrs::id_kernel<C>, -1);
   set_smem(rsrs::extract_lu_kernel<C>, -1);
   set_smem(rsrs::solve_fwd_kernel<C>, -1);
@@ -201,7 +202,7 @@ void launch_chol_blocked(const CholDesc* d, int nmat, int rmax, int mext, cudaSt
       rsrs::chol_update_kernel<C><<<g, 128, rsrs::NT_SMEM, s>>>(d, j0);
       post("chol_update", s, launches);
     }
-    rsrs::chol_diag_kernel<C><<<nmat, 256, rsrs::CHOL_DIAG_SMEM, s>>>(d, j0);
+    rsrs::chol_diag_kernel<C><<<nmat, 256, 0, s>>>(d, j0);
     post("chol_diag", s, launches);
     dim3 g(gx, std::max((rmax - j0 - CB + 63) / 64, gext), 2 * nmat);
     rsrs::chol_trsm_kernel<C><<<g, 128, rsrs::NT_SMEM, s>>>(d, j0);
