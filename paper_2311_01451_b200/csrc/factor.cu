@@ -125,10 +125,14 @@ void init_kernels() {
   int dev = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&g_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  set_smem(rsrs::gemm_nt_kernel, rsrs::NT_SMEM);
-  set_smem(rsrs::gemm_nn_kernel, rsrs::NN_SMEM);
-  set_smem(rsrs::gemm_nt_kernel_c, rsrs::NT_SMEM);
-  set_smem(rsrs::gemm_nn_kernel_c, rsrs::NN_SMEM);
+  set_smem(rsrs::gemm_nt_kernel<64>, rsrs::NT_SMEM);
+  set_smem(rsrs::gemm_nn_kernel<64>, rsrs::NN_SMEM);
+  set_smem(rsrs::gemm_nt_kernel_c<64>, rsrs::NT_SMEM);
+  set_smem(rsrs::gemm_nn_kernel_c<64>, rsrs::NN_SMEM);
+  set_smem(rsrs::gemm_nt_kernel<32>, rsrs::NT_SMEM);
+  set_smem(rsrs::gemm_nn_kernel<32>, rsrs::NN_SMEM);
+  set_smem(rsrs::gemm_nt_kernel_c<32>, rsrs::NT_SMEM);
+  set_smem(rsrs::gemm_nn_kernel_c<32>, rsrs::NN_SMEM);
   set_smem_both<false>();
   set_smem_both<true>();
   done = true;
@@ -228,21 +232,35 @@ void launch_back_blocked(const CholDesc* d, int nmat, int rmax, int mext, cudaSt
   }
 }
 
+// Row tile 32 when every descriptor of the launch has at most 32 rows (small boxes:
+// the sphere's leaves hold ~15 points), else 64.
 void launch_nt(bool cplx, const NTDesc* d, int n, int mmax, int nmax, cudaStream_t s, int64_t& launches) {
   if (n <= 0 || mmax <= 0 || nmax <= 0) return;
   const int TN = cplx ? rsrs::GTC : rsrs::GT;
-  dim3 grid((nmax + TN - 1) / TN, (mmax + 63) / 64, n);
-  if (cplx) rsrs::gemm_nt_kernel_c<<<grid, 128, rsrs::NT_SMEM, s>>>(d);
-  else rsrs::gemm_nt_kernel<<<grid, 128, rsrs::NT_SMEM, s>>>(d);
+  const int TM = mmax <= 32 ? 32 : 64;
+  dim3 grid((nmax + TN - 1) / TN, (mmax + TM - 1) / TM, n);
+  if (cplx) {
+    if (TM == 32) rsrs::gemm_nt_kernel_c<32><<<grid, 128, rsrs::nt_smem(32, true), s>>>(d);
+    else rsrs::gemm_nt_kernel_c<64><<<grid, 128, rsrs::nt_smem(64, true), s>>>(d);
+  } else {
+    if (TM == 32) rsrs::gemm_nt_kernel<32><<<grid, 128, rsrs::nt_smem(32, false), s>>>(d);
+    else rsrs::gemm_nt_kernel<64><<<grid, 128, rsrs::NT_SMEM, s>>>(d);
+  }
   post("gemm_nt", s, launches);
 }
 
 void launch_nn(bool cplx, const NNDesc* d, int n, int mmax, int nmax, cudaStream_t s, int64_t& launches) {
   if (n <= 0 || mmax <= 0 || nmax <= 0) return;
   const int TN = cplx ? rsrs::GTC : rsrs::GT;
-  dim3 grid((nmax + TN - 1) / TN, (mmax + 63) / 64, n);
-  if (cplx) rsrs::gemm_nn_kernel_c<<<grid, 128, rsrs::NN_SMEM, s>>>(d);
-  else rsrs::gemm_nn_kernel<<<grid, 128, rsrs::NN_SMEM, s>>>(d);
+  const int TM = mmax <= 32 ? 32 : 64;
+  dim3 grid((nmax + TN - 1) / TN, (mmax + TM - 1) / TM, n);
+  if (cplx) {
+    if (TM == 32) rsrs::gemm_nn_kernel_c<32><<<grid, 128, rsrs::nn_smem(32, true), s>>>(d);
+    else rsrs::gemm_nn_kernel_c<64><<<grid, 128, rsrs::nn_smem(64, true), s>>>(d);
+  } else {
+    if (TM == 32) rsrs::gemm_nn_kernel<32><<<grid, 128, rsrs::nn_smem(32, false), s>>>(d);
+    else rsrs::gemm_nn_kernel<64><<<grid, 128, rsrs::NN_SMEM, s>>>(d);
+  }
   post("gemm_nn", s, launches);
 }
 

@@ -21,28 +21,36 @@ constexpr int GPA = 36;      // smem row stride (doubles) of [64][32] tiles: con
 constexpr int GPB = 68;      // smem row stride of [32][64] tiles
 constexpr int NT_SMEM = 2 * 2 * GT * GPA * 8;              // 73,728 B
 constexpr int NN_SMEM = 2 * (GT * GPA + GBK * GPB) * 8;    // 71,680 B
+// shared memory of a TM-row tile (C: complex variants)
+constexpr int nt_smem(int TM, bool C) { return 2 * (TM + (C ? 32 : GT)) * GPA * 8; }
+constexpr int nn_smem(int TM, bool C) { return 2 * (TM * GPA + (C ? GBK / 2 : GBK) * GPB) * 8; }
 
 // dynamic size: min(cap, *p - off) when p is set, else cap
 RSRS_DI int dyn(const int* p, int off, int cap) { return p ? min(cap, *p - off) : cap; }
 
-// One 64x64 output tile of C = alpha A_rows B_rows^T + beta C (K columns).
+// One TM x 64 output tile (TM = 64 or 32 rows) of C = alpha A_rows B_rows^T + beta C (K columns).
+template <int TM = GT>
 RSRS_DI void nt_tile(const NTDesc& d, int m, int n, int K, int i0, int j0, double* smem) {
+  constexpr int MT = TM / 16, QA = TM / 8;
   double* As = smem;
-  double* Bs = smem + 2 * GT * GPA;
+  double* Bs = smem + 2 * TM * GPA;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const int wr = warp >> 1, wc = warp & 1;
 
-  const double* aptr[8];
+  const double* aptr[QA];
   const double* bptr[8];
-  bool aval[8], bval[8];
+  bool aval[QA], bval[8];
   const int lrow = tid >> 4, kc = (tid & 15) * 2;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
+  for (int q = 0; q < QA; ++q) {
     const int gi = i0 + lrow + 8 * q;
     aval[q] = gi < m;
     const i64 ar = aval[q] ? (d.rowA ? (i64)d.rowA[gi] : (i64)gi) : 0;
     aptr[q] = d.A + ar * d.lda;
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
     const int gj = j0 + lrow + 8 * q;
     bval[q] = gj < n;
     const i64 br = bval[q] ? (d.rowB ? (i64)d.rowB[gj] : (i64)gj) : 0;
@@ -53,15 +61,15 @@ RSRS_DI void nt_tile(const NTDesc& d, int m, int n, int K, int i0, int j0, doubl
     const int bytes = (k + 2 <= K) ? 16 : (k < K ? 8 : 0);
     const int koff = bytes ? k : 0;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int row = lrow + 8 * q;
-      cp_async16(&As[(s * GT + row) * GPA + kc], aptr[q] + koff, aval[q] ? bytes : 0);
-      cp_async16(&Bs[(s * GT + row) * GPA + kc], bptr[q] + koff, bval[q] ? bytes : 0);
-    }
-  };
-  double acc[4][4][2];
+    for (int q = 0; q < QA; ++q)
+      cp_async16(&As[(s * TM + lrow + 8 * q) * GPA + kc], aptr[q] + koff, aval[q] ? bytes : 0);
 #pragma unroll
-  for (int t = 0; t < 4; ++t)
+    for (int q = 0; q < 8; ++q)
+      cp_async16(&Bs[(s * GT + lrow + 8 * q) * GPA + kc], bptr[q] + koff, bval[q] ? bytes : 0);
+  };
+  double acc[MT][4][2];
+#pragma unroll
+  for (int t = 0; t < MT; ++t)
 #pragma unroll
     for (int u = 0; u < 4; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
 
@@ -79,25 +87,25 @@ RSRS_DI void nt_tile(const NTDesc& d, int m, int n, int K, int i0, int j0, doubl
       cp_async_wait<0>();
     }
     __syncthreads();
-    const double* as = As + ((kt & 1) * GT + wr * 32) * GPA;
+    const double* as = As + ((kt & 1) * TM + wr * (TM / 2)) * GPA;
     const double* bs = Bs + ((kt & 1) * GT + wc * 32) * GPA;
 #pragma unroll
     for (int kk = 0; kk < GBK / 4; ++kk) {
-      double a[4], b[4];
+      double a[MT], b[4];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) a[t] = as[(t * 8 + gid) * GPA + kk * 4 + tig];
+      for (int t = 0; t < MT; ++t) a[t] = as[(t * 8 + gid) * GPA + kk * 4 + tig];
 #pragma unroll
       for (int u = 0; u < 4; ++u) b[u] = bs[(u * 8 + gid) * GPA + kk * 4 + tig];
 #pragma unroll
-      for (int t = 0; t < 4; ++t)
+      for (int t = 0; t < MT; ++t)
 #pragma unroll
         for (int u = 0; u < 4; ++u) dmma884(acc[t][u][0], acc[t][u][1], a[t], b[u]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    const int i = i0 + wr * 32 + t * 8 + gid;
+  for (int t = 0; t < MT; ++t) {
+    const int i = i0 + wr * (TM / 2) + t * 8 + gid;
     if (i >= m) continue;
     double* crow = d.C + (i64)i * d.ldc;
 #pragma unroll
@@ -116,25 +124,28 @@ RSRS_DI void nt_tile(const NTDesc& d, int m, int n, int K, int i0, int j0, doubl
   }
 }
 
+template <int TM>
 __global__ void __launch_bounds__(128) gemm_nt_kernel(const NTDesc* __restrict__ descs) {
   extern __shared__ __align__(16) double smem[];
   const NTDesc& d = descs[blockIdx.z];
   const int m = dyn(d.pm, 0, d.m);
   const int n = dyn(d.pn, 0, d.n);
-  const int i0 = blockIdx.y * GT, j0 = blockIdx.x * GT;
+  const int i0 = blockIdx.y * TM, j0 = blockIdx.x * GT;
   if (i0 >= m || j0 >= n) return;
   const int sym = d.psym ? *d.psym : d.sym_rows;
-  if (i0 + GT <= sym && j0 >= i0 + GT) return;  // strictly upper tile of the Gram
+  if (i0 + TM <= sym && j0 >= i0 + TM) return;  // strictly upper tile of the Gram
   const NTDesc dl = d;
-  nt_tile(dl, m, n, d.K, i0, j0, smem);
+  nt_tile<TM>(dl, m, n, d.K, i0, j0, smem);
 }
 
-// One 64x64 output tile of D_rows = beta C_rows + alpha opA B_rows.
+// One TM x 64 output tile (TM = 64 or 32 rows) of D_rows = beta C_rows + alpha opA B_rows.
+template <int TM = GT>
 RSRS_DI void nn_tile(const NNDesc& d, int m, int n, int K, int i0, int j0, double* smem) {
+  constexpr int MT = TM / 16, QA = TM / 8, RP = TM / 2;
   const bool inplace = (d.Cin == nullptr);
   if (K <= 0 && inplace && d.beta == 1.0) return;
-  double* As = smem;                       // [2][64][GPA]  (i, k)
-  double* Bs = smem + 2 * GT * GPA;        // [2][32][GPB]  (k, j)
+  double* As = smem;                       // [2][TM][GPA]  (i, k)
+  double* Bs = smem + 2 * TM * GPA;        // [2][32][GPB]  (k, j)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const int wr = warp >> 1, wc = warp & 1;
@@ -146,19 +157,19 @@ RSRS_DI void nn_tile(const NNDesc& d, int m, int n, int K, int i0, int j0, doubl
       const int k = k0 + kc;
       const int bytes = (k + 2 <= K) ? 16 : (k < K ? 8 : 0);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < QA; ++q) {
         const int row = lrow + 8 * q;
         const int gi = i0 + row;
         const bool v = gi < m && bytes > 0;
         const double* src = v ? d.A + (i64)gi * d.lda + k : d.A;
-        cp_async16(&As[(s * GT + row) * GPA + kc], src, v ? bytes : 0);
+        cp_async16(&As[(s * TM + row) * GPA + kc], src, v ? bytes : 0);
       }
     } else {
       // A stored (K x m): opA(i, k) = A[k*lda + i]; transpose through registers
-      const int kr = tid >> 5, ic = (tid & 31) * 2;
+      const int kr = tid / RP, ic = (tid % RP) * 2;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int kl = kr + 4 * q;
+      for (int q = 0; q < RP / 4; ++q) {
+        const int kl = kr + (128 / RP) * q;
         const int k = k0 + kl;
         const int gi = i0 + ic;
         double v0 = 0.0, v1 = 0.0;
@@ -172,8 +183,8 @@ RSRS_DI void nn_tile(const NNDesc& d, int m, int n, int K, int i0, int j0, doubl
             v0 = src[0];
           }
         }
-        As[(s * GT + ic) * GPA + kl] = v0;
-        As[(s * GT + ic + 1) * GPA + kl] = v1;
+        As[(s * TM + ic) * GPA + kl] = v0;
+        As[(s * TM + ic + 1) * GPA + kl] = v1;
       }
     }
     {
@@ -194,9 +205,9 @@ RSRS_DI void nn_tile(const NNDesc& d, int m, int n, int K, int i0, int j0, doubl
       }
     }
   };
-  double acc[4][4][2];
+  double acc[MT][4][2];
 #pragma unroll
-  for (int t = 0; t < 4; ++t)
+  for (int t = 0; t < MT; ++t)
 #pragma unroll
     for (int u = 0; u < 4; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
 
@@ -214,17 +225,17 @@ RSRS_DI void nn_tile(const NNDesc& d, int m, int n, int K, int i0, int j0, doubl
       cp_async_wait<0>();
     }
     __syncthreads();
-    const double* as = As + ((kt & 1) * GT + wr * 32) * GPA;
+    const double* as = As + ((kt & 1) * TM + wr * (TM / 2)) * GPA;
     const double* bs = Bs + (kt & 1) * GBK * GPB + wc * 32;
 #pragma unroll
     for (int kk = 0; kk < GBK / 4; ++kk) {
-      double a[4], b[4];
+      double a[MT], b[4];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) a[t] = as[(t * 8 + gid) * GPA + kk * 4 + tig];
+      for (int t = 0; t < MT; ++t) a[t] = as[(t * 8 + gid) * GPA + kk * 4 + tig];
 #pragma unroll
       for (int u = 0; u < 4; ++u) b[u] = bs[(kk * 4 + tig) * GPB + u * 8 + gid];
 #pragma unroll
-      for (int t = 0; t < 4; ++t)
+      for (int t = 0; t < MT; ++t)
 #pragma unroll
         for (int u = 0; u < 4; ++u) dmma884(acc[t][u][0], acc[t][u][1], a[t], b[u]);
     }
@@ -232,8 +243,8 @@ RSRS_DI void nn_tile(const NNDesc& d, int m, int n, int K, int i0, int j0, doubl
   }
   // epilogue
 #pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    const int i = i0 + wr * 32 + t * 8 + gid;
+  for (int t = 0; t < MT; ++t) {
+    const int i = i0 + wr * (TM / 2) + t * 8 + gid;
     if (i >= m) continue;
     const i64 dr = d.rowD ? (i64)d.rowD[i] : (i64)i;
     double* drow = d.D + dr * d.ldd;
@@ -260,16 +271,17 @@ RSRS_DI void nn_tile(const NNDesc& d, int m, int n, int K, int i0, int j0, doubl
   }
 }
 
+template <int TM>
 __global__ void __launch_bounds__(128) gemm_nn_kernel(const NNDesc* __restrict__ descs) {
   extern __shared__ __align__(16) double smem[];
   const NNDesc& d = descs[blockIdx.z];
   const int m = dyn(d.pm, 0, d.m);
   const int n = dyn(d.pn, 0, d.n);
   const int K = dyn(d.pK, 0, d.K);
-  const int i0 = blockIdx.y * GT, j0 = blockIdx.x * GT;
+  const int i0 = blockIdx.y * TM, j0 = blockIdx.x * GT;
   if (i0 >= m || j0 >= n) return;
   const NNDesc dl = d;
-  nn_tile(dl, m, n, K, i0, j0, smem);
+  nn_tile<TM>(dl, m, n, K, i0, j0, smem);
 }
 
 
@@ -284,20 +296,22 @@ __global__ void __launch_bounds__(128) gemm_nn_kernel(const NNDesc* __restrict__
 // ---------------------------------------------------------------------------
 constexpr int GTC = 32;      // complex output columns of the NT tile (64 rows x 32 complex)
 
+template <int TM = GT>
 RSRS_DI void nt_tile_c(const NTDesc& d, int m, int n, int K, int i0, int j0, double* smem) {
-  double* As = smem;                      // [2][64][GPA]
-  double* Bs = smem + 2 * GT * GPA;       // [2][32][GPA]
+  constexpr int MT = TM / 16, QA = TM / 8;
+  double* As = smem;                      // [2][TM][GPA]
+  double* Bs = smem + 2 * TM * GPA;       // [2][32][GPA]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const int wr = warp >> 1, wc = warp & 1;
   const int K2 = 2 * K;
   const i64 lda2 = 2 * d.lda, ldb2 = 2 * d.ldb;
-  const double* aptr[8];
+  const double* aptr[QA];
   const double* bptr[4];
-  bool aval[8], bval[4];
+  bool aval[QA], bval[4];
   const int lrow = tid >> 4, kc = (tid & 15) * 2;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
+  for (int q = 0; q < QA; ++q) {
     const int gi = i0 + lrow + 8 * q;
     aval[q] = gi < m;
     const i64 ar = aval[q] ? (d.rowA ? (i64)d.rowA[gi] : (i64)gi) : 0;
@@ -315,15 +329,15 @@ RSRS_DI void nt_tile_c(const NTDesc& d, int m, int n, int K, int i0, int j0, dou
     const int bytes = k < K2 ? 16 : 0;
     const int koff = bytes ? k : 0;
 #pragma unroll
-    for (int q = 0; q < 8; ++q)
-      cp_async16(&As[(s * GT + lrow + 8 * q) * GPA + kc], aptr[q] + koff, aval[q] ? bytes : 0);
+    for (int q = 0; q < QA; ++q)
+      cp_async16(&As[(s * TM + lrow + 8 * q) * GPA + kc], aptr[q] + koff, aval[q] ? bytes : 0);
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       cp_async16(&Bs[(s * GTC + lrow + 8 * q) * GPA + kc], bptr[q] + koff, bval[q] ? bytes : 0);
   };
-  double ar_[4][2][2], ai_[4][2][2];
+  double ar_[MT][2][2], ai_[MT][2][2];
 #pragma unroll
-  for (int t = 0; t < 4; ++t)
+  for (int t = 0; t < MT; ++t)
 #pragma unroll
     for (int u = 0; u < 2; ++u) ar_[t][u][0] = ar_[t][u][1] = ai_[t][u][0] = ai_[t][u][1] = 0.0;
   const double sgn = (tig & 1) ? 1.0 : -1.0;
@@ -341,20 +355,20 @@ RSRS_DI void nt_tile_c(const NTDesc& d, int m, int n, int K, int i0, int j0, dou
       cp_async_wait<0>();
     }
     __syncthreads();
-    const double* as = As + ((kt & 1) * GT + wr * 32) * GPA;
+    const double* as = As + ((kt & 1) * TM + wr * (TM / 2)) * GPA;
     const double* bs = Bs + ((kt & 1) * GTC + wc * 16) * GPA;
 #pragma unroll
     for (int kk = 0; kk < GBK / 4; ++kk) {
-      double a[4], b[2], b2[2];
+      double a[MT], b[2], b2[2];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) a[t] = as[(t * 8 + gid) * GPA + kk * 4 + tig];
+      for (int t = 0; t < MT; ++t) a[t] = as[(t * 8 + gid) * GPA + kk * 4 + tig];
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         b[u] = bs[(u * 8 + gid) * GPA + kk * 4 + tig];
         b2[u] = sgn * bs[(u * 8 + gid) * GPA + kk * 4 + (tig ^ 1)];
       }
 #pragma unroll
-      for (int t = 0; t < 4; ++t)
+      for (int t = 0; t < MT; ++t)
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           dmma884(ar_[t][u][0], ar_[t][u][1], a[t], b[u]);
@@ -365,8 +379,8 @@ RSRS_DI void nt_tile_c(const NTDesc& d, int m, int n, int K, int i0, int j0, dou
   }
   const i64 ldc2 = 2 * d.ldc;
 #pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    const int i = i0 + wr * 32 + t * 8 + gid;
+  for (int t = 0; t < MT; ++t) {
+    const int i = i0 + wr * (TM / 2) + t * 8 + gid;
     if (i >= m) continue;
     double* crow = d.C + (i64)i * ldc2;
 #pragma unroll
@@ -385,25 +399,28 @@ RSRS_DI void nt_tile_c(const NTDesc& d, int m, int n, int K, int i0, int j0, dou
   }
 }
 
+template <int TM>
 __global__ void __launch_bounds__(128) gemm_nt_kernel_c(const NTDesc* __restrict__ descs) {
   extern __shared__ __align__(16) double smem[];
   const NTDesc& d = descs[blockIdx.z];
   const int m = dyn(d.pm, 0, d.m);
   const int n = dyn(d.pn, 0, d.n);
-  const int i0 = blockIdx.y * GT, j0 = blockIdx.x * GTC;
+  const int i0 = blockIdx.y * TM, j0 = blockIdx.x * GTC;
   if (i0 >= m || j0 >= n) return;
   const int sym = d.psym ? *d.psym : d.sym_rows;
-  if (i0 + GT <= sym && j0 >= i0 + GT) return;  // strictly upper part of the Hermitian Gram
+  if (i0 + TM <= sym && j0 >= i0 + TM) return;  // strictly upper part of the Hermitian Gram
   const NTDesc dl = d;
-  nt_tile_c(dl, m, n, d.K, i0, j0, smem);
+  nt_tile_c<TM>(dl, m, n, d.K, i0, j0, smem);
 }
 
 // One tile (64 rows x 32 complex columns) of D_rows = beta C_rows + alpha opA B_rows.
+template <int TM = GT>
 RSRS_DI void nn_tile_c(const NNDesc& d, int m, int n, int K, int i0, int j0, double* smem) {
+  constexpr int MT = TM / 16, QA = TM / 8, RP = TM / 2;
   const bool inplace = (d.Cin == nullptr);
   if (K <= 0 && inplace && d.beta == 1.0) return;
-  double* As = smem;                       // [2][64][GPA]   (i, real k)
-  double* Bs = smem + 2 * GT * GPA;        // [2][16][GPB]   (complex k, real j)
+  double* As = smem;                       // [2][TM][GPA]   (i, real k)
+  double* Bs = smem + 2 * TM * GPA;        // [2][16][GPB]   (complex k, real j)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const int wr = warp >> 1, wc = warp & 1;
@@ -416,19 +433,19 @@ RSRS_DI void nn_tile_c(const NNDesc& d, int m, int n, int K, int i0, int j0, dou
       const int k = k0 + kc;
       const int bytes = k < K2 ? 16 : 0;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < QA; ++q) {
         const int row = lrow + 8 * q;
         const int gi = i0 + row;
         const bool v = gi < m && bytes > 0;
         const double* src = v ? d.A + (i64)gi * lda2 + k : d.A;
-        cp_async16(&As[(s * GT + row) * GPA + kc], src, v ? bytes : 0);
+        cp_async16(&As[(s * TM + row) * GPA + kc], src, v ? bytes : 0);
       }
     } else {
       // opA(i, k) = conj(A[k][i]), A stored K x m (complex)
-      const int kr = tid >> 5, ic = (tid & 31) * 2;
+      const int kr = tid / RP, ic = (tid % RP) * 2;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int kl = kr + 4 * q;          // complex k (local, 0..15)
+      for (int q = 0; q < RP / 8; ++q) {
+        const int kl = kr + (128 / RP) * q;   // complex k (local, 0..15)
         const int k = (k0 >> 1) + kl;
         const int gi = i0 + ic;
         double2 v0 = make_double2(0.0, 0.0), v1 = v0;
@@ -437,10 +454,10 @@ RSRS_DI void nn_tile_c(const NNDesc& d, int m, int n, int K, int i0, int j0, dou
           if (gi < m) v0 = *reinterpret_cast<const double2*>(src);
           if (gi + 1 < m) v1 = *reinterpret_cast<const double2*>(src + 2);
         }
-        As[(s * GT + ic) * GPA + 2 * kl] = v0.x;
-        As[(s * GT + ic) * GPA + 2 * kl + 1] = -v0.y;
-        As[(s * GT + ic + 1) * GPA + 2 * kl] = v1.x;
-        As[(s * GT + ic + 1) * GPA + 2 * kl + 1] = -v1.y;
+        As[(s * TM + ic) * GPA + 2 * kl] = v0.x;
+        As[(s * TM + ic) * GPA + 2 * kl + 1] = -v0.y;
+        As[(s * TM + ic + 1) * GPA + 2 * kl] = v1.x;
+        As[(s * TM + ic + 1) * GPA + 2 * kl + 1] = -v1.y;
       }
     }
     {
@@ -461,9 +478,9 @@ RSRS_DI void nn_tile_c(const NNDesc& d, int m, int n, int K, int i0, int j0, dou
       }
     }
   };
-  double acc[4][4][2];
+  double acc[MT][4][2];
 #pragma unroll
-  for (int t = 0; t < 4; ++t)
+  for (int t = 0; t < MT; ++t)
 #pragma unroll
     for (int u = 0; u < 4; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
   const bool odd_k = tig & 1;
@@ -482,13 +499,13 @@ RSRS_DI void nn_tile_c(const NNDesc& d, int m, int n, int K, int i0, int j0, dou
       cp_async_wait<0>();
     }
     __syncthreads();
-    const double* as = As + ((kt & 1) * GT + wr * 32) * GPA;
+    const double* as = As + ((kt & 1) * TM + wr * (TM / 2)) * GPA;
     const double* bs = Bs + (kt & 1) * (GBK / 2) * GPB + wc * 32;
 #pragma unroll
     for (int kk = 0; kk < GBK / 4; ++kk) {
-      double a[4], b[4];
+      double a[MT], b[4];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) a[t] = as[(t * 8 + gid) * GPA + kk * 4 + tig];
+      for (int t = 0; t < MT; ++t) a[t] = as[(t * 8 + gid) * GPA + kk * 4 + tig];
       const double* brow = bs + (kk * 2 + (tig >> 1)) * GPB;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -496,7 +513,7 @@ RSRS_DI void nn_tile_c(const NNDesc& d, int m, int n, int K, int i0, int j0, dou
         b[u] = odd_k ? sgn * brow[col ^ 1] : brow[col];
       }
 #pragma unroll
-      for (int t = 0; t < 4; ++t)
+      for (int t = 0; t < MT; ++t)
 #pragma unroll
         for (int u = 0; u < 4; ++u) dmma884(acc[t][u][0], acc[t][u][1], a[t], b[u]);
     }
@@ -504,8 +521,8 @@ RSRS_DI void nn_tile_c(const NNDesc& d, int m, int n, int K, int i0, int j0, dou
   }
   const i64 ldd2 = 2 * d.ldd, ldc2 = 2 * d.ldc;
 #pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    const int i = i0 + wr * 32 + t * 8 + gid;
+  for (int t = 0; t < MT; ++t) {
+    const int i = i0 + wr * (TM / 2) + t * 8 + gid;
     if (i >= m) continue;
     const i64 dr = d.rowD ? (i64)d.rowD[i] : (i64)i;
     double* drow = d.D + dr * ldd2;
@@ -529,16 +546,17 @@ RSRS_DI void nn_tile_c(const NNDesc& d, int m, int n, int K, int i0, int j0, dou
   }
 }
 
+template <int TM>
 __global__ void __launch_bounds__(128) gemm_nn_kernel_c(const NNDesc* __restrict__ descs) {
   extern __shared__ __align__(16) double smem[];
   const NNDesc& d = descs[blockIdx.z];
   const int m = dyn(d.pm, 0, d.m);
   const int n = dyn(d.pn, 0, d.n);
   const int K = dyn(d.pK, 0, d.K);
-  const int i0 = blockIdx.y * GT, j0 = blockIdx.x * GTC;
+  const int i0 = blockIdx.y * TM, j0 = blockIdx.x * GTC;
   if (i0 >= m || j0 >= n) return;
   const NNDesc dl = d;
-  nn_tile_c(dl, m, n, K, i0, j0, smem);
+  nn_tile_c<TM>(dl, m, n, K, i0, j0, smem);
 }
 
 // scalar-type dispatch used by the templated per-box kernels
