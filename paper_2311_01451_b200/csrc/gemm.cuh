@@ -72,6 +72,14 @@ RSRS_DI void nt_tile(const NTDesc& d, int m, int n, int K, int i0, int j0, doubl
   for (int t = 0; t < MT; ++t)
 #pragma unroll
     for (int u = 0; u < 4; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
+  // a warp whose sub-tile lies wholly outside C (ragged near fields) or strictly above
+  // the diagonal of the symmetric Gram (never consumed) skips its MMAs
+  bool wact;
+  {
+    const int sym = d.psym ? *d.psym : d.sym_rows;
+    const int rb = i0 + wr * (TM / 2), cb = j0 + wc * 32;
+    wact = rb < m && cb < n && !(rb < sym && cb >= rb + TM / 2);
+  }
 
   const int nk = (K + GBK - 1) / GBK;
   if (nk > 0) {
@@ -89,17 +97,19 @@ RSRS_DI void nt_tile(const NTDesc& d, int m, int n, int K, int i0, int j0, doubl
     __syncthreads();
     const double* as = As + ((kt & 1) * TM + wr * (TM / 2)) * GPA;
     const double* bs = Bs + ((kt & 1) * GT + wc * 32) * GPA;
+    if (wact) {
 #pragma unroll
-    for (int kk = 0; kk < GBK / 4; ++kk) {
-      double a[MT], b[4];
+      for (int kk = 0; kk < GBK / 4; ++kk) {
+        double a[MT], b[4];
 #pragma unroll
-      for (int t = 0; t < MT; ++t) a[t] = as[(t * 8 + gid) * GPA + kk * 4 + tig];
+        for (int t = 0; t < MT; ++t) a[t] = as[(t * 8 + gid) * GPA + kk * 4 + tig];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) b[u] = bs[(u * 8 + gid) * GPA + kk * 4 + tig];
+        for (int u = 0; u < 4; ++u) b[u] = bs[(u * 8 + gid) * GPA + kk * 4 + tig];
 #pragma unroll
-      for (int t = 0; t < MT; ++t)
+        for (int t = 0; t < MT; ++t)
 #pragma unroll
-        for (int u = 0; u < 4; ++u) dmma884(acc[t][u][0], acc[t][u][1], a[t], b[u]);
+          for (int u = 0; u < 4; ++u) dmma884(acc[t][u][0], acc[t][u][1], a[t], b[u]);
+      }
     }
     __syncthreads();
   }
