@@ -71,6 +71,7 @@ constexpr int SMEM_MAX = 227 * 1024 - 1024;  // dynamic-smem budget of the large
 int g_optin = 0;
 bool g_debug = false;  // RSRS_DEBUG_SYNC=1: synchronize and check after every launch
 bool g_trace = false;  // RSRS_TRACE=1: host-side time split of rsrs_factor on stderr
+int g_upd_tm = 0;      // RSRS_UPD_TM=32|64: row tile of the L/U sample-update GEMMs (0: auto)
 
 // host-side time split of one rsrs_factor (RSRS_TRACE)
 struct HostTrace {
@@ -122,6 +123,9 @@ void init_kernels() {
   g_debug = dbg && dbg[0] == '1';
   const char* tr = getenv("RSRS_TRACE");
   g_trace = tr && tr[0] == '1';
+  const char* ut = getenv("RSRS_UPD_TM");
+  g_upd_tm = ut ? atoi(ut) : 0;
+  if (g_upd_tm != 32 && g_upd_tm != 64) g_upd_tm = 0;
   int dev = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&g_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
@@ -249,10 +253,11 @@ void launch_nt(bool cplx, const NTDesc* d, int n, int mmax, int nmax, cudaStream
   post("gemm_nt", s, launches);
 }
 
-void launch_nn(bool cplx, const NNDesc* d, int n, int mmax, int nmax, cudaStream_t s, int64_t& launches) {
+void launch_nn(bool cplx, const NNDesc* d, int n, int mmax, int nmax, cudaStream_t s, int64_t& launches,
+               int force_tm = 0) {
   if (n <= 0 || mmax <= 0 || nmax <= 0) return;
   const int TN = cplx ? rsrs::GTC : rsrs::GT;
-  const int TM = mmax <= 32 ? 32 : 64;
+  const int TM = force_tm ? force_tm : (mmax <= 32 ? 32 : 64);
   dim3 grid((nmax + TN - 1) / TN, (mmax + TM - 1) / TM, n);
   if (cplx) {
     if (TM == 32) rsrs::gemm_nn_kernel_c<32><<<grid, 128, rsrs::nn_smem(32, true), s>>>(d);
@@ -926,7 +931,7 @@ struct Planner {
           launch_nn(cplx, Dg + 2 * q0, 2 * n, bi.max_r, bi.max_r, s, launches);
           toc();
           tic(KC_UPD);
-          launch_nn(cplx, Dupd + 2 * q0, 2 * n, bi.max_r, p, s, launches);
+          launch_nn(cplx, Dupd + 2 * q0, 2 * n, bi.max_r, p, s, launches, g_upd_tm);
           toc();
         }
         if (dist) {
