@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-boxes", type=int, default=0, help="oracle sample size (leaf boxes); 0 = auto")
+    ap.add_argument("--variant", default="paper", choices=["paper", "symmetric"],
+                    help="paper: two independent sketches (PAPER.md:1180-1183, the headline); symmetric: the "
+                         "SURVEY 8(f) f2 shortcut Psi = Omega, Z = Y for real symmetric A")
     return ap.parse_args()
 
 
@@ -141,7 +144,7 @@ def fp64_peak() -> dict:
 # ---------------------------------------------------------------------------
 # problem setup (seeded, synthetic; sampling excluded from timing)
 # ---------------------------------------------------------------------------
-def setup_problem(cfg, dev, rank=0, world=1, pg=None):
+def setup_problem(cfg, dev, rank=0, world=1, pg=None, symmetric=False):
     """Seeded problem; with world > 1 this rank keeps only its Morton range of rows
     (rsrs_tree_partition) and draws its own sample rows Y = A[rows, :] Omega."""
     import numpy as np
@@ -170,7 +173,11 @@ def setup_problem(cfg, dev, rank=0, world=1, pg=None):
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
     R.sample_matvec_rows(cfg.kernel, pts_d, W.kernel_weight(cfg), Om_d, Y_d, r0, kappa=cfg.kappa)
-    R.sample_matvec_rows(cfg.kernel, pts_d, W.kernel_weight(cfg), Ps_d, Z_d, r0, adjoint=True, kappa=cfg.kappa)
+    if symmetric:            # f2: Psi = Omega => Z = A^T Omega = Y; only Y / Omega are used
+        Ps_d, Z_d = Om_d, Y_d
+    else:
+        R.sample_matvec_rows(cfg.kernel, pts_d, W.kernel_weight(cfg), Ps_d, Z_d, r0, adjoint=True,
+                             kappa=cfg.kappa)
     torch.cuda.synchronize(dev)
     t_sample = time.perf_counter() - t0
     if world > 1:
@@ -185,7 +192,8 @@ def setup_problem(cfg, dev, rank=0, world=1, pg=None):
             pg.broadcast_object_list(obj, src=0)
             return obj[0]
         comm = R.NcclComm(world, rank, bcast)
-    return dict(cfg=cfg, X=X, tree=tree, perm=perm, P=P, pts=pts_d, src=[Y_d, Z_d, Om_d, Ps_d], b=b,
+    src = [Y_d, Om_d] if symmetric else [Y_d, Z_d, Om_d, Ps_d]
+    return dict(cfg=cfg, X=X, tree=tree, perm=perm, P=P, pts=pts_d, src=src, b=b, symmetric=symmetric,
                 t_sample=t_sample, t_tree=t_tree, comm=comm, rank=rank, world=world, rows=(r0, r1),
                 gather_level=gather)
 
@@ -193,9 +201,10 @@ def setup_problem(cfg, dev, rank=0, world=1, pg=None):
 def factor_solve(pb, work, x, stream, profile=False, solve_events=None):
     import paper_2311_01451_b200 as R
     cfg = pb["cfg"]
-    f = R.factor(pb["tree"], *work, p=cfg.p, eps=cfg.eps, level_growth=cfg.g, id_scale=cfg.c_id,
+    arrays = (work[0], None, work[1], None) if pb["symmetric"] else tuple(work)
+    f = R.factor(pb["tree"], *arrays, p=cfg.p, eps=cfg.eps, level_growth=cfg.g, id_scale=cfg.c_id,
                  oversample=cfg.l, stream=stream, profile=profile, comm=pb["comm"], rank=pb["rank"],
-                 nranks=pb["world"])
+                 nranks=pb["world"], symmetric=pb["symmetric"])
     if solve_events is not None:
         solve_events[0].record(stream)
     f.solve(x, stream=stream)
@@ -276,7 +285,9 @@ def run_native(args, rank, world, local, pg):
     dev = torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
     cfg = W.CONFIGS[args.config]
-    pb = setup_problem(cfg, dev, rank, world, pg)
+    if args.variant == "symmetric" and cfg.is_complex:
+        raise SystemExit("--variant symmetric needs a real symmetric operator (not c4)")
+    pb = setup_problem(cfg, dev, rank, world, pg, symmetric=args.variant == "symmetric")
     stream = torch.cuda.Stream(device=dev)
     work = [t.clone() for t in pb["src"]]
     x = pb["b"].clone()
@@ -394,8 +405,8 @@ def run_native(args, rank, world, local, pg):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
             "config": {"workload": cfg.name, "N": N, "p": cfg.p, "eps": cfg.eps, "g": cfg.g, "leaf": cfg.leaf,
-                       "kernel": cfg.kernel, "L": st["L"], "l2": "inputs 6.4 GB > 126 MB L2 (no flush needed)",
-                       "step": "restore samples + rsrs_factor + rsrs_solve(1 rhs)", "parallelism": (f"morton-range x{world}, halo exchange, gather at level {pb['gather_level']}"
+                       "kernel": cfg.kernel, "L": st["L"], "l2": f"inputs {sum(t.numel() * t.element_size() for t in pb['src']) / 1e9:.1f} GB > 126 MB L2 (no flush needed)",
+                       "step": "restore samples + rsrs_factor + rsrs_solve(1 rhs)", "variant": args.variant, "parallelism": (f"morton-range x{world}, halo exchange, gather at level {pb['gather_level']}"
                                        if world > 1 else "single GPU")},
             "factor_ms": st["factor_ms"], "solve_ms": statistics.median(solve_ms), "sample_s": pb["t_sample"], "tree_s": pb["t_tree"],
             "residual": resid, "top_size": st["top_size"], "max_rank": st["max_rank"],

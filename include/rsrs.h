@@ -64,6 +64,10 @@ typedef struct {
   int profile;         /* 1: time every kernel class with CUDA events on `stream` (rsrs_factor_profile) */
   int gather_level;    /* multi-GPU: boxes on levels <= gather_level are gathered on rank 0 (-1: auto,
                           the largest level with <= 16 * nranks boxes; always >= top_level - 1) */
+  int symmetric;       /* 1: symmetric shortcut (not in the paper, which always draws two
+                          independent sketches): A real symmetric, Psi = Omega hence
+                          Z = Y; only the Y / Omega side of the sweep runs, X_rr is symmetrised so that
+                          G_L = G_U^T.  Z and Psi are ignored (may be NULL).  RSRS_F64 only. */
 } rsrs_opts;
 
 /* Statistics of a factorization (Table 1). */

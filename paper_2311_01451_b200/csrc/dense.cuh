@@ -14,7 +14,7 @@ template <bool C>
 __global__ void __launch_bounds__(256) id_kernel(BoxDev* __restrict__ boxes, const double* __restrict__ wsd,
                                                  int* __restrict__ iws, double* __restrict__ fpoold,
                                                  int* __restrict__ ipool, const int* __restrict__ gidx,
-                                                 double atol2, int p, int oversample) {
+                                                 double atol2, int p, int oversample, int hsame) {
   typedef typename ScalarOf<C>::T S;
   extern __shared__ __align__(16) double Hsd[];
   S* Hs = reinterpret_cast<S*>(Hsd);
@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(256) id_kernel(BoxDev* __restrict__ boxes, con
   const S* H = ws + b.off_h;
   const int ldhg = b.ldn;
   // H = H_Y + H_Z = Y'' Y''^* + Z'' Z''^* (the two halves of S S^*, written by gemm_nt)
-  const S* H2 = H + (i64)nb * ldhg;
+  const S* H2 = hsame ? H : H + (i64)nb * ldhg;   // symmetric shortcut: Z'' = Y'', H = 2 H_Y
   for (int idx = tid; idx < nb * nb; idx += 256) {
     const i64 g = (i64)(idx / nb) * ldhg + idx % nb;
     Hs[(idx / nb) * ldh + idx % nb] = s_add(H[g], H2[g]);
@@ -323,7 +323,7 @@ __device__ bool gj_inverse_reg(const S* __restrict__ Xs, int ldx, int n, S* __re
 template <bool C>
 __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ boxes, double* __restrict__ wsd,
                                                          const int* __restrict__ iws,
-                                                         double* __restrict__ fpoold) {
+                                                         double* __restrict__ fpoold, int sym) {
   typedef typename ScalarOf<C>::T S;
   extern __shared__ __align__(16) double Xsd[];
   S* Xs = reinterpret_cast<S*>(Xsd);
@@ -353,7 +353,8 @@ __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ bo
   const S* T = fpool + b.f_T;
   const i64 ldr = b.ldr;
   const S* WY = ws + b.off_aug + (i64)b.rmax * ldr;
-  const S* WZ = ws + b.off_aug + (i64)(b.rmax + nb) * ldr + (i64)b.rmax * ldr;
+  // symmetric shortcut (Psi = Omega, Z = Y): the Z side equals the Y side
+  const S* WZ = sym ? WY : ws + b.off_aug + (i64)(b.rmax + nb) * ldr + (i64)b.rmax * ldr;
   S* XY = ws + b.off_xy;
   S* XZ = ws + b.off_xz;
   // 1. row combination X = W_r - T W_s
@@ -391,9 +392,25 @@ __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ bo
   S* Xrr = fpool + b.f_Xrr;
   for (int idx = tid; idx < nr * nr; idx += 256) {
     const int i = idx / nr, j = idx % nr;
-    const S v = XY[(i64)i * ldr + b.self_pos + redloc[j]];
-    Xs[i * ldx + j] = v;
-    Xrr[(i64)i * ldn + j] = v;
+    Xs[i * ldx + j] = XY[(i64)i * ldr + b.self_pos + redloc[j]];
+  }
+  if (sym) {
+    // symmetric shortcut: X_rr := (X_rr + X_rr^T) / 2, so G_L = G_U^T and the Z-side
+    // update equals the Y-side one (Z stays equal to Y)
+    __syncthreads();
+    for (int idx = tid; idx < nr * nr; idx += 256) {
+      const int i = idx / nr, j = idx % nr;
+      if (i < j) {
+        const S v = s_scale(s_add(Xs[i * ldx + j], Xs[j * ldx + i]), 0.5);
+        Xs[i * ldx + j] = v;
+        Xs[j * ldx + i] = v;
+      }
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < nr * nr; idx += 256) {
+    const int i = idx / nr, j = idx % nr;
+    Xrr[(i64)i * ldn + j] = Xs[i * ldx + j];
   }
   S* Xrc = ws + b.off_xrc;
   S* Xcr = ws + b.off_xcr;
@@ -561,11 +578,14 @@ __global__ void compact_kernel(const BoxDev* __restrict__ boxes, const int* __re
     const double* z = Z + (i64)src * ld;
     const double* o = Om + (i64)src * ld;
     const double* q = Ps + (i64)src * ld;
+    const bool zs = nZ != nullptr;      // symmetric shortcut: no Z / Psi stores
     for (int j = threadIdx.x; j < p; j += blockDim.x) {
       nY[(i64)dst * nld + j] = y[j];
-      nZ[(i64)dst * nld + j] = z[j];
       nOm[(i64)dst * nld + j] = o[j];
-      nPs[(i64)dst * nld + j] = q[j];
+      if (zs) {
+        nZ[(i64)dst * nld + j] = z[j];
+        nPs[(i64)dst * nld + j] = q[j];
+      }
     }
   }
 }

@@ -364,6 +364,7 @@ struct Planner {
   double flops = 0, bytes = 0;
   bool profile = false;
   bool cplx = false;
+  bool sym = false;    // symmetric shortcut: Psi = Omega, Z = Y, only the Y / Omega side runs
   int SC = 1;          // doubles per scalar (1 real, 2 complex); all offsets below are in scalars
   std::vector<cudaEvent_t> evpool;
   struct Pend {
@@ -425,7 +426,11 @@ struct Planner {
   void account_box(double nb, double r, double k, double P) {
     const double nr = nb - k, nc = r - nr, W8 = 8.0 * SC;
     const double F = cplx ? 4.0 : 1.0;   // real-equivalent flops of a complex multiply-add
-    auto account = [&](int cls, double fl, double by) { this->account(cls, F * fl, by); };
+    // symmetric shortcut: the two-sided classes run on one side only
+    auto account = [&](int cls, double fl, double by) {
+      const double h = (sym && cls != KC_ID && cls != KC_EXTRACT && cls != KC_G) ? 0.5 : 1.0;
+      this->account(cls, F * fl * h, by * h);
+    };
     account(KC_GRAM, 2 * (r * (r + 1) * P + 2 * nb * r * P), W8 * (2 * (r * P + nb * P) + 2 * (r * (r + 1) / 2 + nb * r)));
     account(KC_CHOL, 2 * (r * r * r / 3 + nb * r * r), W8 * 2 * 2 * (r * (r + 1) / 2 + nb * r));
     account(KC_TRSM, 2 * (nb * r * r), W8 * 2 * (r * (r + 1) / 2 + 2 * nb * r));
@@ -508,6 +513,10 @@ struct Planner {
     if (comm) {
       R = comm->nranks;
       me = comm->rank;
+    }
+    if (sym) {          // Z and Psi are never read: alias them to Y and Omega
+      Zu = Yu;
+      Psu = Omu;
     }
     DBuf store[2], gidx_buf[2];
     int cur = -1;
@@ -725,17 +734,17 @@ struct Planner {
         a.pm = &dx->r; a.pn = &dx->r; a.psym = &dx->r;
         nt_gram.push_back(a);
         a.A = Ps; a.B = Ps; a.C = augP;
-        nt_gram.push_back(a);
+        if (!sym) nt_gram.push_back(a);
         NTDesc bq{};
         bq.A = Y; bq.rowA = brows; bq.lda = ld; bq.B = Om; bq.rowB = near; bq.ldb = ld;
         bq.C = augO + SC * (i64)rm * ldr; bq.ldc = ldr; bq.m = nb; bq.n = rm; bq.K = p; bq.sym_rows = 0;
         bq.alpha = 1.0; bq.pn = &dx->r;
         nt_gram.push_back(bq);
         bq.A = Z; bq.B = Ps; bq.C = augP + SC * (i64)rm * ldr;
-        nt_gram.push_back(bq);
+        if (!sym) nt_gram.push_back(bq);
         const i64 nlv = (i64)((rm + 63) / 64) * 64 * 64;
         chol.push_back(CholDesc{augO, ldr, &dx->r, nb, rm, &dx->status, dws + SC * x.off_linv});
-        chol.push_back(CholDesc{augP, ldr, &dx->r, nb, rm, &dx->status, dws + SC * (x.off_linv + nlv)});
+        if (!sym) chol.push_back(CholDesc{augP, ldr, &dx->r, nb, rm, &dx->status, dws + SC * (x.off_linv + nlv)});
         double* yz = dws + SC * x.off_yz;
         NNDesc pr{};
         pr.A = augO + SC * (i64)rm * ldr; pr.lda = ldr; pr.transA = 0;
@@ -745,14 +754,14 @@ struct Planner {
         pr.m = nb; pr.n = p; pr.K = rm; pr.alpha = -1.0; pr.beta = 1.0; pr.pK = &dx->r;
         nn_proj.push_back(pr);
         pr.A = augP + SC * (i64)rm * ldr; pr.B = Ps; pr.D = yz + SC * nld; pr.Cin = Z + SC * (i64)x.row0 * ld;
-        nn_proj.push_back(pr);
+        if (!sym) nn_proj.push_back(pr);
         NTDesc h{};
         h.A = yz; h.rowA = nullptr; h.lda = 2 * nld; h.B = yz; h.rowB = nullptr; h.ldb = 2 * nld;
         h.C = dws + SC * x.off_h; h.ldc = ldn; h.m = nb; h.n = nb; h.K = p; h.sym_rows = 0;
         h.alpha = 1.0;
         nt_h.push_back(h);
         h.A = yz + SC * nld; h.B = yz + SC * nld; h.C = dws + SC * (x.off_h + (i64)nb * ldn);
-        nt_h.push_back(h);
+        if (!sym) nt_h.push_back(h);
         const int* skelrow = diws + x.off_skelrow;
         const int* redrow = diws + x.off_redrow;
         double* Tm = fpool + SC * x.f_T;
@@ -762,14 +771,14 @@ struct Planner {
         e.m = nb; e.n = p; e.K = nb; e.alpha = -1.0; e.beta = 1.0; e.pm = &dx->nr; e.pK = &dx->k;
         nn_ef.push_back(e);
         e.B = Z; e.D = Z;
-        nn_ef.push_back(e);
+        if (!sym) nn_ef.push_back(e);
         NNDesc fo{};
         fo.A = Tm; fo.lda = ldn; fo.transA = 1; fo.B = Om; fo.rowB = redrow; fo.ldb = ld;
         fo.D = Om; fo.rowD = skelrow; fo.ldd = ld; fo.Cin = nullptr;
         fo.m = nb; fo.n = p; fo.K = nb; fo.alpha = 1.0; fo.beta = 1.0; fo.pm = &dx->k; fo.pK = &dx->nr;
         nn_ef.push_back(fo);
         fo.B = Ps; fo.D = Ps;
-        nn_ef.push_back(fo);
+        if (!sym) nn_ef.push_back(fo);
         NNDesc gu{};
         gu.A = fpool + SC * x.f_Xinv; gu.lda = ldn; gu.B = dws + SC * x.off_xrc; gu.rowB = nullptr; gu.ldb = ldr;
         gu.D = fpool + SC * x.f_GU; gu.ldd = ldr; gu.Cin = nullptr; gu.m = nb; gu.n = rm; gu.K = nb;
@@ -788,7 +797,7 @@ struct Planner {
         nn_upd.push_back(u);
         NNDesc uz = u;
         uz.A = fpool + SC * x.f_GU; uz.lda = ldr; uz.transA = 1; uz.B = Z; uz.D = Z;
-        nn_upd.push_back(uz);
+        if (!sym) nn_upd.push_back(uz);
       }
       std::vector<char> hdesc;
       auto put = [&](const void* src, size_t n) {
@@ -893,37 +902,40 @@ struct Planner {
           rsrs::build_near_kernel<<<n, 32, 0, s>>>(dbx, dboxes, diws, dnbr, p, l);
           post("build_near_kernel", s, launches);
           toc();
+          // descriptors per box: 4 Gram / 2 Cholesky / 2 projection / 2 H / 4 E-F / 2 L-U,
+          // halved by the symmetric shortcut (Y / Omega side only)
+          const int ns = sym ? 1 : 2;
           tic(KC_GRAM);
-          launch_nt(cplx, Dgram + 4 * q0, 4 * n, bi.max_r, bi.max_r, s, launches);
+          launch_nt(cplx, Dgram + 2 * ns * q0, 2 * ns * n, bi.max_r, bi.max_r, s, launches);
           toc();
           tic(KC_CHOL);
-          launch_chol_any(cplx, Dchol + 2 * q0, 2 * n, bi.max_r, bi.max_nb, s, launches);
+          launch_chol_any(cplx, Dchol + ns * q0, ns * n, bi.max_r, bi.max_nb, s, launches);
           toc();
           tic(KC_TRSM);
-          launch_back_any(cplx, Dchol + 2 * q0, 2 * n, bi.max_r, bi.max_nb, s, launches);
+          launch_back_any(cplx, Dchol + ns * q0, ns * n, bi.max_r, bi.max_nb, s, launches);
           toc();
           tic(KC_PROJ);
-          launch_nn(cplx, Dproj + 2 * q0, 2 * n, bi.max_nb, p, s, launches);
+          launch_nn(cplx, Dproj + ns * q0, ns * n, bi.max_nb, p, s, launches);
           toc();
           tic(KC_HGRAM);
-          launch_nt(cplx, Dh + 2 * q0, 2 * n, bi.max_nb, bi.max_nb, s, launches);
+          launch_nt(cplx, Dh + ns * q0, ns * n, bi.max_nb, bi.max_nb, s, launches);
           toc();
           {
             const size_t sm = (size_t)bi.max_nb * (bi.max_nb + 1) * sS + 3 * (size_t)bi.max_nb * 4 + 64;
             tic(KC_ID);
-            if (cplx) rsrs::id_kernel<true><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, ipool, gidx, atol * atol, p, l);
-            else rsrs::id_kernel<false><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, ipool, gidx, atol * atol, p, l);
+            if (cplx) rsrs::id_kernel<true><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, ipool, gidx, atol * atol, p, l, sym);
+            else rsrs::id_kernel<false><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, ipool, gidx, atol * atol, p, l, sym);
             post("id_kernel", s, launches);
             toc();
           }
           tic(KC_EF);
-          launch_nn(cplx, Def + 4 * q0, 4 * n, bi.max_nb, p, s, launches);
+          launch_nn(cplx, Def + 2 * ns * q0, 2 * ns * n, bi.max_nb, p, s, launches);
           toc();
           {
             const size_t sm = 2 * (size_t)bi.max_nb * (bi.max_nb + 1) * sS + 3 * (size_t)bi.max_nb * 4 + 64;
             tic(KC_EXTRACT);
-            if (cplx) rsrs::extract_lu_kernel<true><<<n, 256, sm, s>>>(dbx, dws, diws, fpool);
-            else rsrs::extract_lu_kernel<false><<<n, 256, sm, s>>>(dbx, dws, diws, fpool);
+            if (cplx) rsrs::extract_lu_kernel<true><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, sym);
+            else rsrs::extract_lu_kernel<false><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, sym);
             post("extract_lu_kernel", s, launches);
             toc();
           }
@@ -931,7 +943,7 @@ struct Planner {
           launch_nn(cplx, Dg + 2 * q0, 2 * n, bi.max_r, bi.max_r, s, launches);
           toc();
           tic(KC_UPD);
-          launch_nn(cplx, Dupd + 2 * q0, 2 * n, bi.max_r, p, s, launches, g_upd_tm);
+          launch_nn(cplx, Dupd + ns * q0, ns * n, bi.max_r, p, s, launches, g_upd_tm);
           toc();
         }
         if (dist) {
@@ -1065,7 +1077,8 @@ struct Planner {
         dim3 grid((unsigned)hb.size(), 4);
         tic(KC_MISC);
         rsrs::compact_kernel<<<grid, 128, 0, s>>>(dboxes, diws, dstbuf.as<int>(), Y, Z, Om, Ps, SC * ld, gidx, nY,
-                                                 nZ, nO, nP, SC * nld, ng, SC * p);
+                                                 (sym && R == 1) ? nullptr : nZ, nO,
+                                                 (sym && R == 1) ? nullptr : nP, SC * nld, ng, SC * p);
         post("compact_kernel", s, launches);
         toc();
       }
@@ -1267,6 +1280,7 @@ static rsrs_status factor_impl(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, v
     P.profile = o.profile != 0;
     P.cplx = f->cplx;
     P.SC = f->sc;
+    P.sym = o.symmetric != 0;
     P.comm = (comm && comm->nranks > 1) ? comm : nullptr;
     P.part = rsrs::make_partition(T, comm ? comm->nranks : 1, o.gather_level, o.top_level);
     P.run((double*)Y, (double*)Z, (double*)Omega, (double*)Psi, ld);
@@ -1303,10 +1317,13 @@ static rsrs_status factor_impl(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, v
 
 static rsrs_status check_args(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, void* Z, void* Omega, void* Psi,
                               int64_t ld, const rsrs_opts* opts, rsrs_opts& o) {
-  if (!t || !Y || !Z || !Omega || !Psi) return fail(RSRS_ERR_INVALID, "rsrs_factor: null argument");
+  const bool symm = opts && opts->symmetric;
+  if (!t || !Y || !Omega || (!symm && (!Z || !Psi))) return fail(RSRS_ERR_INVALID, "rsrs_factor: null argument");
+  if (symm && dt != RSRS_F64)
+    return fail(RSRS_ERR_INVALID, "rsrs_factor: the symmetric shortcut is for real symmetric operators (RSRS_F64)");
   if (p < 1 || ld < p || (ld & 1)) return fail(RSRS_ERR_INVALID, "rsrs_factor: need 1 <= p <= ld and ld even");
   if (dt != RSRS_F64 && dt != RSRS_C128) return fail(RSRS_ERR_INVALID, "rsrs_factor: unknown dtype");
-  o = rsrs_opts{1e-6, 1.0, 1.0, 10, 2, 0, 1, nullptr, nullptr, 0, -1};
+  o = rsrs_opts{1e-6, 1.0, 1.0, 10, 2, 0, 1, nullptr, nullptr, 0, -1, 0};
   if (opts) o = *opts;
   if (!(o.eps > 0) || !(o.level_growth > 0) || !(o.id_scale > 0) || o.oversample < 0 || o.top_level < 1 ||
       o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks)
@@ -1325,6 +1342,10 @@ rsrs_status rsrs_factor(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, void* Z,
   rsrs_opts o;
   rsrs_status st = check_args(t, dt, p, Y, Z, Omega, Psi, ld, opts, o);
   if (st != RSRS_OK) return st;
+  if (o.symmetric) {
+    Z = Y;
+    Psi = Omega;
+  }
   if (o.nranks == 1) return factor_impl(t, dt, p, Y, Z, Omega, Psi, ld, o, nullptr, out);
   if (!o.nccl_comm) return fail(RSRS_ERR_INVALID, "rsrs_factor: nranks > 1 needs opts.nccl_comm (rsrs_comm_init)");
   if (!rsrs::NcclApi::get().ok()) return fail(RSRS_ERR_NCCL, "rsrs_factor: libnccl.so.2 not loadable");
@@ -1347,6 +1368,10 @@ rsrs_status rsrs_factor_emulated(rsrs_tree t, rsrs_dtype dt, int64_t p, int G, v
     init_kernels();
   } catch (const CudaError& e) {
     return fail(RSRS_ERR_CUDA, "rsrs_factor_emulated: " + e.msg);
+  }
+  if (o.symmetric) {
+    Z = Y;
+    Psi = Omega;
   }
   const rsrs::Partition P = rsrs::make_partition(t->t, G, o.gather_level, o.top_level);
   rsrs::InProcHub hub(G);

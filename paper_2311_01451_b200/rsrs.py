@@ -49,7 +49,7 @@ class Opts(ctypes.Structure):
     _fields_ = [("eps", ctypes.c_double), ("level_growth", ctypes.c_double), ("id_scale", ctypes.c_double),
                 ("oversample", ctypes.c_int), ("top_level", ctypes.c_int), ("rank", ctypes.c_int),
                 ("nranks", ctypes.c_int), ("nccl_comm", ctypes.c_void_p), ("stream", ctypes.c_void_p),
-                ("profile", ctypes.c_int), ("gather_level", ctypes.c_int)]
+                ("profile", ctypes.c_int), ("gather_level", ctypes.c_int), ("symmetric", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):
@@ -304,14 +304,17 @@ def _dtype_code(t) -> int:
 def factor(tree: Tree, Y, Z, Omega, Psi, p: int, eps: float = 1e-6, level_growth: float = 1.0,
            id_scale: float = 1.0, oversample: int = 10, top_level: int = 2, stream=None,
            dtype: int | None = None, profile: bool = False, comm=None, rank: int = 0, nranks: int = 1,
-           gather_level: int = -1) -> Factorization:
+           gather_level: int = -1, symmetric: bool = False) -> Factorization:
     """rsrs_factor on CUDA tensors (N x ld, tree order); Y, Z, Omega, Psi are OVERWRITTEN.
 
     float64 tensors -> RSRS_F64, complex128 -> RSRS_C128 (ld in elements).
     Multi-GPU (nranks > 1): this rank's rows only (Tree.partition()) and the
-    NcclComm of this rank in `comm`."""
+    NcclComm of this rank in `comm`.
+    symmetric=True: the f2 shortcut for real symmetric A (Psi = Omega, Z = Y); Z and Psi may be None."""
     ld = Y.stride(0)
     code = _dtype_code(Y)
+    if symmetric:
+        Z, Psi = Y, Omega
     for t in (Z, Omega, Psi):
         if t.stride(0) != ld or t.dtype != Y.dtype:
             raise ValueError("Y, Z, Omega, Psi must share dtype and leading dimension")
@@ -319,7 +322,8 @@ def factor(tree: Tree, Y, Z, Omega, Psi, p: int, eps: float = 1e-6, level_growth
         raise ValueError("dtype does not match the tensors")
     dtype = code
     o = Opts(eps, level_growth, id_scale, oversample, top_level, int(rank), int(nranks),
-             None if comm is None else comm.handle, _stream_ptr(stream), int(profile), int(gather_level))
+             None if comm is None else comm.handle, _stream_ptr(stream), int(profile), int(gather_level),
+             int(symmetric))
     h = _vp()
     _check(_lib.rsrs_factor(tree.handle, dtype, int(p), _ptr(Y), _ptr(Z), _ptr(Omega), _ptr(Psi), int(ld),
                             ctypes.byref(o), ctypes.byref(h)))
@@ -355,12 +359,16 @@ class NcclComm:
 
 
 def factor_emulated(tree: Tree, G: int, Y, Z, Omega, Psi, p: int, eps: float = 1e-6, level_growth: float = 1.0,
-                    id_scale: float = 1.0, oversample: int = 10, top_level: int = 2, gather_level: int = -1) -> list:
+                    id_scale: float = 1.0, oversample: int = 10, top_level: int = 2, gather_level: int = -1,
+                    symmetric: bool = False) -> list:
     """G-rank run of the multi-GPU sweep emulated on this GPU (one host thread per rank);
     full tree-ordered Y, Z, Omega, Psi (overwritten).  Returns the G rank factorizations."""
     ld = Y.stride(0)
     code = _dtype_code(Y)
-    o = Opts(eps, level_growth, id_scale, oversample, top_level, 0, G, None, None, 0, int(gather_level))
+    if symmetric:
+        Z, Psi = Y, Omega
+    o = Opts(eps, level_growth, id_scale, oversample, top_level, 0, G, None, None, 0, int(gather_level),
+             int(symmetric))
     hs = (_vp * G)()
     _check(_lib.rsrs_factor_emulated(tree.handle, code, int(p), int(G), _ptr(Y), _ptr(Z), _ptr(Omega), _ptr(Psi),
                                      int(ld), ctypes.byref(o), hs))
