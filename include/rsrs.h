@@ -68,6 +68,8 @@ typedef struct {
                           independent sketches): A real symmetric, Psi = Omega hence
                           Z = Y; only the Y / Omega side of the sweep runs, X_rr is symmetrised so that
                           G_L = G_U^T.  Z and Psi are ignored (may be NULL).  RSRS_F64 only. */
+  int direct_gram;     /* 1: compute every near-field Gram directly (r x r x p per box) instead of
+                          assembling it from the level-wide box-pair blocks (single rank) */
 } rsrs_opts;
 
 /* Statistics of a factorization (Table 1). */

@@ -77,7 +77,7 @@ struct BoxDev {
   int row0;                   // first store row of b (its rows are contiguous)
   int level, box;             // for error messages
   int nnbr;                   // neighbour boxes (self included)
-  i64 off_nbr;                // ints in the level's record array: nnbr x {boxdev index or -1, row0, count}
+  i64 off_nbr;                // ints in the level's record array: nnbr x {boxdev index or -1, row0, count, box}
   i64 off_aug;                // doubles: Omega side [C (rmax x ldr); u (nb x ldr)], Psi side follows
   i64 off_yz;                 // doubles: [Y'' Z''] (nb x 2 nld)
   i64 off_h;                  // doubles: H (nb x ldn)

@@ -23,6 +23,15 @@ __global__ void __launch_bounds__(256) id_kernel(BoxDev* __restrict__ boxes, con
   BoxDev& b = boxes[blockIdx.x];
   const int nb = b.nb, r = b.r;
   if (b.status != ST_OK) {                 // e.g. too few samples for this near field
+    // keep every row as a skeleton so that later near lists / compaction stay in range
+    // (the factorization is abandoned at the end of the level)
+    int* skelrow = iws + b.off_skelrow;
+    const int* near = iws + b.off_rows;
+    for (int t = threadIdx.x; t < nb; t += blockDim.x) skelrow[t] = b.row0 + t;
+    for (int t = threadIdx.x; t < r; t += blockDim.x) {
+      iws[b.off_crow + t] = near[t];
+      iws[b.off_cpos + t] = t;
+    }
     if (threadIdx.x == 0) {
       b.k = nb;
       b.nr = 0;
@@ -521,7 +530,7 @@ __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ bo
 // (R2).  Neighbours processed by an earlier
 // colour contribute only their skeleton rows (their redundant rows are
 // decoupled); the others contribute all their rows.
-// Records {boxdev index or -1, first row, count}: a foreign neighbour on the
+// Records {boxdev index or -1, first row, count, box}: a foreign neighbour on the
 // multi-GPU path is a contiguous halo block holding exactly its active rows.
 // ---------------------------------------------------------------------------
 __global__ void build_near_kernel(BoxDev* __restrict__ boxes, const BoxDev* __restrict__ level_boxes,
@@ -530,10 +539,11 @@ __global__ void build_near_kernel(BoxDev* __restrict__ boxes, const BoxDev* __re
   const int lane = threadIdx.x;
   const int* nd = nbrrec + b.off_nbr;
   int* near = iws + b.off_rows;
+  for (int t = lane; t < b.nb; t += 32) near[b.rmax + t] = b.row0 + t;   // the box's own rows (cross product)
   int o = 0, selfp = 0;
   for (int q = 0; q < b.nnbr; ++q) {
-    const int idx = nd[3 * q], r0 = nd[3 * q + 1];
-    int cnt = nd[3 * q + 2];
+    const int idx = nd[4 * q], r0 = nd[4 * q + 1];
+    int cnt = nd[4 * q + 2];
     if (idx >= 0) {
       const BoxDev& nbx = level_boxes[idx];
       cnt = nbx.k;

@@ -1,0 +1,161 @@
+// Per-box GEMM / Cholesky descriptors of a level, built on the device from the
+// box records (one thread per box) -- the host used to build and upload ~2 KB of
+// descriptors per box per level (40 MB at the sphere's leaf level), which left
+// the GPU idle.  Same contents and order as the launch code expects:
+//   Gram   [Omega Gram, Psi Gram]* (omitted with the level's Gram blocks), [Y cross, Z cross]
+//   Chol   [Omega side, Psi side]     proj [Y, Z]     H [H_Y, H_Z]
+//   E/F    [Y, Z, Omega, Psi]         G [G_U, G_L]    L/U [Y, Z]
+// with every Z / Psi entry dropped by the symmetric shortcut.
+#pragma once
+#include "common.cuh"
+
+namespace rsrs {
+
+struct DescParams {
+  double *Y, *Z, *Om, *Ps;       // current store
+  i64 ld, nld;
+  int p, SC, sym, blocks, nbox, pad;
+  double* dws;                   // level workspace
+  double* fpool;                 // level factor pool
+  int* diws;                     // level int workspace
+  BoxDev* boxes;
+  NTDesc* gram;
+  NTDesc* h;
+  NNDesc* proj;
+  NNDesc* ef;
+  NNDesc* g;
+  NNDesc* upd;
+  CholDesc* chol;
+};
+
+__global__ void make_desc_kernel(const DescParams P) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= P.nbox) return;
+  BoxDev* dx = P.boxes + q;
+  const BoxDev x = *dx;
+  const int SC = P.SC, p = P.p;
+  const int ns = P.sym ? 1 : 2;
+  const i64 ld = P.ld, nld = P.nld;
+  const int nb = x.nb, rm = x.rmax;
+  const i64 ldr = x.ldr, ldn = x.ldn;
+  const int* near = P.diws + x.off_rows;
+  const int* brows = near + rm;
+  double* augO = P.dws + SC * x.off_aug;
+  double* augP = augO + SC * (i64)(rm + nb) * ldr;
+  // ---- Gram + cross
+  {
+    NTDesc* o = P.gram + (i64)q * (P.blocks ? 1 : 2) * ns;
+    if (!P.blocks) {
+      NTDesc a{};
+      a.A = P.Om; a.rowA = near; a.lda = ld; a.B = P.Om; a.rowB = near; a.ldb = ld;
+      a.C = augO; a.ldc = ldr; a.m = rm; a.n = rm; a.K = p; a.sym_rows = rm; a.alpha = 1.0;
+      a.pm = &dx->r; a.pn = &dx->r; a.psym = &dx->r;
+      *o++ = a;
+      if (!P.sym) {
+        a.A = P.Ps; a.B = P.Ps; a.C = augP;
+        *o++ = a;
+      }
+    }
+    NTDesc bq{};
+    bq.A = P.Y; bq.rowA = brows; bq.lda = ld; bq.B = P.Om; bq.rowB = near; bq.ldb = ld;
+    bq.C = augO + SC * (i64)rm * ldr; bq.ldc = ldr; bq.m = nb; bq.n = rm; bq.K = p; bq.sym_rows = 0;
+    bq.alpha = 1.0; bq.pn = &dx->r;
+    *o++ = bq;
+    if (!P.sym) {
+      bq.A = P.Z; bq.B = P.Ps; bq.C = augP + SC * (i64)rm * ldr;
+      *o++ = bq;
+    }
+  }
+  // ---- Cholesky
+  {
+    const i64 nlv = (i64)((rm + 63) / 64) * 64 * 64;
+    CholDesc* o = P.chol + (i64)q * ns;
+    o[0] = CholDesc{augO, ldr, &dx->r, nb, rm, &dx->status, P.dws + SC * x.off_linv};
+    if (!P.sym) o[1] = CholDesc{augP, ldr, &dx->r, nb, rm, &dx->status, P.dws + SC * (x.off_linv + nlv)};
+  }
+  double* yz = P.dws + SC * x.off_yz;
+  // ---- projection
+  {
+    NNDesc* o = P.proj + (i64)q * ns;
+    NNDesc pr{};
+    pr.A = augO + SC * (i64)rm * ldr; pr.lda = ldr; pr.transA = 0;
+    pr.B = P.Om; pr.rowB = near; pr.ldb = ld;
+    pr.D = yz; pr.rowD = nullptr; pr.ldd = 2 * nld;
+    pr.Cin = P.Y + SC * (i64)x.row0 * ld; pr.rowC = nullptr; pr.ldc = ld;
+    pr.m = nb; pr.n = p; pr.K = rm; pr.alpha = -1.0; pr.beta = 1.0; pr.pK = &dx->r;
+    o[0] = pr;
+    if (!P.sym) {
+      pr.A = augP + SC * (i64)rm * ldr; pr.B = P.Ps; pr.D = yz + SC * nld; pr.Cin = P.Z + SC * (i64)x.row0 * ld;
+      o[1] = pr;
+    }
+  }
+  // ---- H
+  {
+    NTDesc* o = P.h + (i64)q * ns;
+    NTDesc h{};
+    h.A = yz; h.rowA = nullptr; h.lda = 2 * nld; h.B = yz; h.rowB = nullptr; h.ldb = 2 * nld;
+    h.C = P.dws + SC * x.off_h; h.ldc = ldn; h.m = nb; h.n = nb; h.K = p; h.sym_rows = 0;
+    h.alpha = 1.0;
+    o[0] = h;
+    if (!P.sym) {
+      h.A = yz + SC * nld; h.B = yz + SC * nld; h.C = P.dws + SC * (x.off_h + (i64)nb * ldn);
+      o[1] = h;
+    }
+  }
+  const int* skelrow = P.diws + x.off_skelrow;
+  const int* redrow = P.diws + x.off_redrow;
+  double* Tm = P.fpool + SC * x.f_T;
+  // ---- E/F
+  {
+    NNDesc* o = P.ef + (i64)q * 2 * ns;
+    NNDesc e{};
+    e.A = Tm; e.lda = ldn; e.transA = 0; e.B = P.Y; e.rowB = skelrow; e.ldb = ld;
+    e.D = P.Y; e.rowD = redrow; e.ldd = ld; e.Cin = nullptr;
+    e.m = nb; e.n = p; e.K = nb; e.alpha = -1.0; e.beta = 1.0; e.pm = &dx->nr; e.pK = &dx->k;
+    *o++ = e;
+    if (!P.sym) {
+      e.B = P.Z; e.D = P.Z;
+      *o++ = e;
+    }
+    NNDesc fo{};
+    fo.A = Tm; fo.lda = ldn; fo.transA = 1; fo.B = P.Om; fo.rowB = redrow; fo.ldb = ld;
+    fo.D = P.Om; fo.rowD = skelrow; fo.ldd = ld; fo.Cin = nullptr;
+    fo.m = nb; fo.n = p; fo.K = nb; fo.alpha = 1.0; fo.beta = 1.0; fo.pm = &dx->k; fo.pK = &dx->nr;
+    *o++ = fo;
+    if (!P.sym) {
+      fo.B = P.Ps; fo.D = P.Ps;
+      *o++ = fo;
+    }
+  }
+  // ---- G_U, G_L
+  {
+    NNDesc* o = P.g + (i64)q * 2;
+    NNDesc gu{};
+    gu.A = P.fpool + SC * x.f_Xinv; gu.lda = ldn; gu.B = P.dws + SC * x.off_xrc; gu.rowB = nullptr; gu.ldb = ldr;
+    gu.D = P.fpool + SC * x.f_GU; gu.ldd = ldr; gu.Cin = nullptr; gu.m = nb; gu.n = rm; gu.K = nb;
+    gu.alpha = 1.0; gu.beta = 0.0; gu.pm = &dx->nr; gu.pn = &dx->nc; gu.pK = &dx->nr;
+    o[0] = gu;
+    NNDesc gl{};
+    gl.A = P.dws + SC * x.off_xcr; gl.lda = ldn; gl.B = P.fpool + SC * x.f_Xinv; gl.rowB = nullptr; gl.ldb = ldn;
+    gl.D = P.fpool + SC * x.f_GL; gl.ldd = ldn; gl.Cin = nullptr; gl.m = rm; gl.n = nb; gl.K = nb;
+    gl.alpha = 1.0; gl.beta = 0.0; gl.pm = &dx->nc; gl.pn = &dx->nr; gl.pK = &dx->nr;
+    o[1] = gl;
+  }
+  // ---- L/U updates
+  {
+    NNDesc* o = P.upd + (i64)q * ns;
+    const int* crow = P.diws + x.off_crow;
+    NNDesc u{};
+    u.A = P.fpool + SC * x.f_GL; u.lda = ldn; u.transA = 0; u.B = P.Y; u.rowB = redrow; u.ldb = ld;
+    u.D = P.Y; u.rowD = crow; u.ldd = ld; u.Cin = nullptr; u.m = rm; u.n = p; u.K = nb;
+    u.alpha = -1.0; u.beta = 1.0; u.pm = &dx->nc; u.pK = &dx->nr;
+    o[0] = u;
+    if (!P.sym) {
+      NNDesc uz = u;
+      uz.A = P.fpool + SC * x.f_GU; uz.lda = ldr; uz.transA = 1; uz.B = P.Z; uz.D = P.Z;
+      o[1] = uz;
+    }
+  }
+}
+
+}  // namespace rsrs

@@ -37,7 +37,9 @@
 #include "chol.cuh"
 #include "dist.h"
 #include "dense.cuh"
+#include "descs.cuh"
 #include "gemm.cuh"
+#include "gram.cuh"
 #include "internal.h"
 #include "sweep.cuh"
 
@@ -114,6 +116,7 @@ void set_smem_both() {
   set_smem(rsrs::apply_bwd_kernel<C>, -1);
   set_smem(rsrs::top_solve_kernel<C>, -1);
   set_smem(rsrs::top_apply_kernel<C>, -1);
+  set_smem(rsrs::gblk_update_kernel<C>, rsrs::gblk_smem<C>());
 }
 
 void init_kernels() {
@@ -240,6 +243,11 @@ void launch_back_blocked(const CholDesc* d, int nmat, int rmax, int mext, cudaSt
 // the sphere's leaves hold ~15 points), else 64.
 void launch_nt(bool cplx, const NTDesc* d, int n, int mmax, int nmax, cudaStream_t s, int64_t& launches) {
   if (n <= 0 || mmax <= 0 || nmax <= 0) return;
+  constexpr int ZMAX = 65535;          // gridDim.z limit: split large descriptor batches
+  if (n > ZMAX) {
+    for (int i = 0; i < n; i += ZMAX) launch_nt(cplx, d + i, std::min(ZMAX, n - i), mmax, nmax, s, launches);
+    return;
+  }
   const int TN = cplx ? rsrs::GTC : rsrs::GT;
   const int TM = mmax <= 32 ? 32 : 64;
   dim3 grid((nmax + TN - 1) / TN, (mmax + TM - 1) / TM, n);
@@ -256,6 +264,12 @@ void launch_nt(bool cplx, const NTDesc* d, int n, int mmax, int nmax, cudaStream
 void launch_nn(bool cplx, const NNDesc* d, int n, int mmax, int nmax, cudaStream_t s, int64_t& launches,
                int force_tm = 0) {
   if (n <= 0 || mmax <= 0 || nmax <= 0) return;
+  constexpr int ZMAX = 65535;
+  if (n > ZMAX) {
+    for (int i = 0; i < n; i += ZMAX)
+      launch_nn(cplx, d + i, std::min(ZMAX, n - i), mmax, nmax, s, launches, force_tm);
+    return;
+  }
   const int TN = cplx ? rsrs::GTC : rsrs::GT;
   const int TM = force_tm ? force_tm : (mmax <= 32 ? 32 : 64);
   dim3 grid((nmax + TN - 1) / TN, (mmax + TM - 1) / TM, n);
@@ -365,6 +379,8 @@ struct Planner {
   bool profile = false;
   bool cplx = false;
   bool sym = false;    // symmetric shortcut: Psi = Omega, Z = Y, only the Y / Omega side runs
+  bool gram_blocks = true;   // level-wide near-field Gram blocks (gram.cuh; single rank)
+  bool level_blocks = false; // the current level uses them (account_box counts the cross products only)
   int SC = 1;          // doubles per scalar (1 real, 2 complex); all offsets below are in scalars
   std::vector<cudaEvent_t> evpool;
   struct Pend {
@@ -431,7 +447,10 @@ struct Planner {
       const double h = (sym && cls != KC_ID && cls != KC_EXTRACT && cls != KC_G) ? 0.5 : 1.0;
       this->account(cls, F * fl * h, by * h);
     };
-    account(KC_GRAM, 2 * (r * (r + 1) * P + 2 * nb * r * P), W8 * (2 * (r * P + nb * P) + 2 * (r * (r + 1) / 2 + nb * r)));
+    if (level_blocks)   // near-field Gram assembled from the level's blocks (bytes: assembly); cross product computed
+      account(KC_GRAM, 2 * (2 * nb * r * P), W8 * (2 * (r * P + nb * P) + 2 * (r * (r + 1) + nb * r)));
+    else
+      account(KC_GRAM, 2 * (r * (r + 1) * P + 2 * nb * r * P), W8 * (2 * (r * P + nb * P) + 2 * (r * (r + 1) / 2 + nb * r)));
     account(KC_CHOL, 2 * (r * r * r / 3 + nb * r * r), W8 * 2 * 2 * (r * (r + 1) / 2 + nb * r));
     account(KC_TRSM, 2 * (nb * r * r), W8 * 2 * (r * (r + 1) / 2 + 2 * nb * r));
     account(KC_PROJ, 2 * (2 * nb * r * P), W8 * 2 * (nb * r + r * P + 2 * nb * P));
@@ -649,7 +668,7 @@ struct Planner {
           x.off_redrow = ioff;  ioff += nb;
           x.off_crow = ioff;    ioff += r;
           x.off_cpos = ioff;    ioff += r;
-          x.off_nbr = noff;     noff += 3 * x.nnbr;
+          x.off_nbr = noff;     noff += 4 * x.nnbr;
           x.f_T = foff;     foff += nb * ldn;
           x.f_GL = foff;    foff += r * ldn;
           x.f_GU = foff;    foff += nb * ldr;
@@ -686,12 +705,12 @@ struct Planner {
       std::vector<std::pair<int, int>> foreign_slot;   // (record index, box) per my box
       std::vector<int> fs_first(hb.size() + 1, 0);
       {
-        std::vector<int> hint(std::max<i64>(ioff, 1), 0);
+
         for (size_t q = 0; q < hb.size(); ++q) {
           const BoxDev& x = hb[q];
           const int b = x.box;
           fs_first[q] = (int)foreign_slot.size();
-          for (int t = 0; t < x.nb; ++t) hint[x.off_rows + x.rmax + t] = x.row0 + t;
+
           int q3 = (int)x.off_nbr;
           for (int qq = lv.nbr_off[b]; qq < lv.nbr_off[b + 1]; ++qq) {
             const int j = lv.nbr[qq];
@@ -700,123 +719,199 @@ struct Planner {
               hnbr[q3++] = -1;
               hnbr[q3++] = 0;
               hnbr[q3++] = 0;
+              hnbr[q3++] = j;
               continue;
             }
             const bool done = nb_all[j] > 0 && lv.colour[j] < lv.colour[b];
             hnbr[q3++] = done ? hb_of[j] : -1;
             hnbr[q3++] = row0[j];
             hnbr[q3++] = nb_all[j];
+            hnbr[q3++] = j;
           }
         }
         fs_first[hb.size()] = (int)foreign_slot.size();
-        CK(cudaMemcpyAsync(diws, hint.data(), sizeof(int) * ioff, cudaMemcpyHostToDevice, s));
+
         CK(cudaMemcpyAsync(dnbr, hnbr.data(), sizeof(int) * noff, cudaMemcpyHostToDevice, s));
         if (!hb.empty()) CK(cudaMemcpyAsync(dboxes, hb.data(), sizeof(BoxDev) * hb.size(), cudaMemcpyHostToDevice, s));
         stream_sync(s);
       }
 
       // ---- descriptors (sizes that depend on the near set point at BoxDev::r / nr / nc / k)
-      std::vector<NTDesc> nt_gram, nt_h;
-      std::vector<NNDesc> nn_proj, nn_ef, nn_g, nn_upd;
-      std::vector<CholDesc> chol;
-      for (size_t q = 0; q < hb.size(); ++q) {
-        const BoxDev& x = hb[q];
-        BoxDev* dx = dboxes + q;
-        const int nb = x.nb, rm = x.rmax;
-        const i64 ldr = x.ldr, ldn = x.ldn;
-        const int* near = diws + x.off_rows;
-        const int* brows = near + rm;
-        double* augO = dws + SC * x.off_aug;
-        double* augP = augO + SC * (i64)(rm + nb) * ldr;
-        NTDesc a{};
-        a.A = Om; a.rowA = near; a.lda = ld; a.B = Om; a.rowB = near; a.ldb = ld;
-        a.C = augO; a.ldc = ldr; a.m = rm; a.n = rm; a.K = p; a.sym_rows = rm; a.alpha = 1.0;
-        a.pm = &dx->r; a.pn = &dx->r; a.psym = &dx->r;
-        nt_gram.push_back(a);
-        a.A = Ps; a.B = Ps; a.C = augP;
-        if (!sym) nt_gram.push_back(a);
-        NTDesc bq{};
-        bq.A = Y; bq.rowA = brows; bq.lda = ld; bq.B = Om; bq.rowB = near; bq.ldb = ld;
-        bq.C = augO + SC * (i64)rm * ldr; bq.ldc = ldr; bq.m = nb; bq.n = rm; bq.K = p; bq.sym_rows = 0;
-        bq.alpha = 1.0; bq.pn = &dx->r;
-        nt_gram.push_back(bq);
-        bq.A = Z; bq.B = Ps; bq.C = augP + SC * (i64)rm * ldr;
-        if (!sym) nt_gram.push_back(bq);
-        const i64 nlv = (i64)((rm + 63) / 64) * 64 * 64;
-        chol.push_back(CholDesc{augO, ldr, &dx->r, nb, rm, &dx->status, dws + SC * x.off_linv});
-        if (!sym) chol.push_back(CholDesc{augP, ldr, &dx->r, nb, rm, &dx->status, dws + SC * (x.off_linv + nlv)});
-        double* yz = dws + SC * x.off_yz;
-        NNDesc pr{};
-        pr.A = augO + SC * (i64)rm * ldr; pr.lda = ldr; pr.transA = 0;
-        pr.B = Om; pr.rowB = near; pr.ldb = ld;
-        pr.D = yz; pr.rowD = nullptr; pr.ldd = 2 * nld;
-        pr.Cin = Y + SC * (i64)x.row0 * ld; pr.rowC = nullptr; pr.ldc = ld;
-        pr.m = nb; pr.n = p; pr.K = rm; pr.alpha = -1.0; pr.beta = 1.0; pr.pK = &dx->r;
-        nn_proj.push_back(pr);
-        pr.A = augP + SC * (i64)rm * ldr; pr.B = Ps; pr.D = yz + SC * nld; pr.Cin = Z + SC * (i64)x.row0 * ld;
-        if (!sym) nn_proj.push_back(pr);
-        NTDesc h{};
-        h.A = yz; h.rowA = nullptr; h.lda = 2 * nld; h.B = yz; h.rowB = nullptr; h.ldb = 2 * nld;
-        h.C = dws + SC * x.off_h; h.ldc = ldn; h.m = nb; h.n = nb; h.K = p; h.sym_rows = 0;
-        h.alpha = 1.0;
-        nt_h.push_back(h);
-        h.A = yz + SC * nld; h.B = yz + SC * nld; h.C = dws + SC * (x.off_h + (i64)nb * ldn);
-        if (!sym) nt_h.push_back(h);
-        const int* skelrow = diws + x.off_skelrow;
-        const int* redrow = diws + x.off_redrow;
-        double* Tm = fpool + SC * x.f_T;
-        NNDesc e{};
-        e.A = Tm; e.lda = ldn; e.transA = 0; e.B = Y; e.rowB = skelrow; e.ldb = ld;
-        e.D = Y; e.rowD = redrow; e.ldd = ld; e.Cin = nullptr;
-        e.m = nb; e.n = p; e.K = nb; e.alpha = -1.0; e.beta = 1.0; e.pm = &dx->nr; e.pK = &dx->k;
-        nn_ef.push_back(e);
-        e.B = Z; e.D = Z;
-        if (!sym) nn_ef.push_back(e);
-        NNDesc fo{};
-        fo.A = Tm; fo.lda = ldn; fo.transA = 1; fo.B = Om; fo.rowB = redrow; fo.ldb = ld;
-        fo.D = Om; fo.rowD = skelrow; fo.ldd = ld; fo.Cin = nullptr;
-        fo.m = nb; fo.n = p; fo.K = nb; fo.alpha = 1.0; fo.beta = 1.0; fo.pm = &dx->k; fo.pK = &dx->nr;
-        nn_ef.push_back(fo);
-        fo.B = Ps; fo.D = Ps;
-        if (!sym) nn_ef.push_back(fo);
-        NNDesc gu{};
-        gu.A = fpool + SC * x.f_Xinv; gu.lda = ldn; gu.B = dws + SC * x.off_xrc; gu.rowB = nullptr; gu.ldb = ldr;
-        gu.D = fpool + SC * x.f_GU; gu.ldd = ldr; gu.Cin = nullptr; gu.m = nb; gu.n = rm; gu.K = nb;
-        gu.alpha = 1.0; gu.beta = 0.0; gu.pm = &dx->nr; gu.pn = &dx->nc; gu.pK = &dx->nr;
-        nn_g.push_back(gu);
-        NNDesc gl{};
-        gl.A = dws + SC * x.off_xcr; gl.lda = ldn; gl.B = fpool + SC * x.f_Xinv; gl.rowB = nullptr; gl.ldb = ldn;
-        gl.D = fpool + SC * x.f_GL; gl.ldd = ldn; gl.Cin = nullptr; gl.m = rm; gl.n = nb; gl.K = nb;
-        gl.alpha = 1.0; gl.beta = 0.0; gl.pm = &dx->nc; gl.pn = &dx->nr; gl.pK = &dx->nr;
-        nn_g.push_back(gl);
-        const int* crow = diws + x.off_crow;
-        NNDesc u{};
-        u.A = fpool + SC * x.f_GL; u.lda = ldn; u.transA = 0; u.B = Y; u.rowB = redrow; u.ldb = ld;
-        u.D = Y; u.rowD = crow; u.ldd = ld; u.Cin = nullptr; u.m = rm; u.n = p; u.K = nb;
-        u.alpha = -1.0; u.beta = 1.0; u.pm = &dx->nc; u.pK = &dx->nr;
-        nn_upd.push_back(u);
-        NNDesc uz = u;
-        uz.A = fpool + SC * x.f_GU; uz.lda = ldr; uz.transA = 1; uz.B = Z; uz.D = Z;
-        if (!sym) nn_upd.push_back(uz);
+      // level-wide Gram blocks (gram.cuh): single rank, boxes small enough for the kernels' tables
+      bool use_blocks = gram_blocks && R == 1;
+      int max_nnbr = 1;
+      for (int b = 0; b < nbox; ++b) {
+        max_nnbr = std::max(max_nnbr, lv.nbr_off[b + 1] - lv.nbr_off[b]);
+        if (nb_all[b] > rsrs::GB_MAX || (lv.nbr_off[b + 1] - lv.nbr_off[b]) > 64) use_blocks = false;
       }
-      std::vector<char> hdesc;
-      auto put = [&](const void* src, size_t n) {
-        const size_t at = hdesc.size();
-        hdesc.resize(at + ((n + 15) & ~size_t(15)));
-        if (n) std::memcpy(hdesc.data() + at, src, n);
+      level_blocks = use_blocks;
+      DBuf gpool_buf, gtab_b, gps_b, growl_b, gwork_b;
+      std::vector<int64_t> gwork_off(binfo.size() + 1, 0);
+      DBuf* gpool = &gpool_buf;
+      i64 gpool_side = 0;
+      const int sides = sym ? 1 : 2;
+      if (use_blocks) {
+        // partners of box i: every box that shares a near field with it (neighbours of its
+        // nonempty neighbours), ascending; flat CSR built with a stamp array
+        std::vector<int> gpstart(nbox + 1, 0), plist, stamp(nbox, -1);
+        plist.reserve((size_t)nbox * 16);
+        for (int i = 0; i < nbox; ++i) {
+          const size_t at = plist.size();
+          if (nb_all[i] > 0)
+            for (int q = lv.nbr_off[i]; q < lv.nbr_off[i + 1]; ++q) {
+              const int m = lv.nbr[q];
+              if (nb_all[m] <= 0) continue;
+              for (int q2 = lv.nbr_off[m]; q2 < lv.nbr_off[m + 1]; ++q2) {
+                const int j = lv.nbr[q2];
+                if (nb_all[j] > 0 && stamp[j] != i) {
+                  stamp[j] = i;
+                  plist.push_back(j);
+                }
+              }
+            }
+          std::sort(plist.begin() + at, plist.end());
+          gpstart[i + 1] = (int)plist.size();
+        }
+        // row-block storage: box i keeps [G(i, j) for partners j >= i] side by side
+        // (nb_i x sum nb_j, leading dimension even(sum)), so one NT GEMM per box fills it
+        std::vector<i64> roff(nbox, 0), coloff(std::max<size_t>(plist.size(), 1), -1);
+        std::vector<int> rld(nbox, 0);
+        i64 poff = 0;
+        int64_t nrowl = 0;
+        for (int i = 0; i < nbox; ++i) {
+          int cols = 0;
+          for (int t = gpstart[i]; t < gpstart[i + 1]; ++t)
+            if (plist[t] >= i) {
+              coloff[t] = cols;
+              cols += nb_all[plist[t]];
+            }
+          rld[i] = (int)even(cols);
+          roff[i] = poff;
+          poff += (i64)nb_all[i] * rld[i];
+          nrowl += cols;
+        }
+        std::vector<rsrs::GBlk> gtab(std::max<size_t>(plist.size(), 1));
+        for (int i = 0; i < nbox; ++i)
+          for (int t = gpstart[i]; t < gpstart[i + 1]; ++t) {
+            const int j = plist[t];
+            rsrs::GBlk e{};
+            e.j = j;
+            if (j >= i) {
+              e.mode = (j == i) ? 2 : 0;
+              e.off = roff[i] + coloff[t];
+              e.ld = rld[i];
+              e.nrow = nb_all[i];
+              e.ncol = nb_all[j];
+            } else {
+              const int tj = (int)(std::lower_bound(plist.begin() + gpstart[j], plist.begin() + gpstart[j + 1], i) -
+                                   plist.begin());
+              e.mode = 1;
+              e.off = roff[j] + coloff[tj];
+              e.ld = rld[j];
+              e.nrow = nb_all[j];
+              e.ncol = nb_all[i];
+            }
+            gtab[t] = e;
+          }
+        gpool_side = poff;
+        gpool_buf.alloc((size_t)sS * std::max<i64>(2, sides * poff), s);
+        double* poolO = gpool_buf.as<double>();
+        // B-row lists of the per-box GEMMs (store rows of the partners j >= i)
+        std::vector<int> rowl(std::max<int64_t>(nrowl, 1));
+        std::vector<int64_t> rowl_at(nbox, 0);
+        {
+          int64_t o = 0;
+          for (int i = 0; i < nbox; ++i) {
+            rowl_at[i] = o;
+            for (int t = gpstart[i]; t < gpstart[i + 1]; ++t)
+              if (plist[t] >= i)
+                for (int r = 0; r < nb_all[plist[t]]; ++r) rowl[o++] = row0[plist[t]] + r;
+          }
+        }
+        growl_b.alloc(sizeof(int) * rowl.size(), s);
+        CK(cudaMemcpyAsync(growl_b.p, rowl.data(), sizeof(int) * rowl.size(), cudaMemcpyHostToDevice, s));
+        std::vector<NTDesc> pre;
+        double fl = 0;
+        int maxnb = 0, maxcols = 0;
+        for (int i = 0; i < nbox; ++i) {
+          if (nb_all[i] <= 0) continue;
+          const int cols = (int)((i + 1 < nbox ? rowl_at[i + 1] : nrowl) - rowl_at[i]);
+          maxnb = std::max(maxnb, nb_all[i]);
+          maxcols = std::max(maxcols, cols);
+          for (int side = 0; side < sides; ++side) {
+            const double* M = side ? Ps : Om;
+            NTDesc d{};
+            d.A = M + SC * (i64)row0[i] * ld; d.rowA = nullptr; d.lda = ld;
+            d.B = M; d.rowB = growl_b.as<int>() + rowl_at[i]; d.ldb = ld;
+            d.C = poolO + SC * (side * poff + roff[i]); d.ldc = rld[i];
+            d.m = nb_all[i]; d.n = cols; d.K = p; d.sym_rows = 0; d.alpha = 1.0;
+            pre.push_back(d);
+            fl += 2.0 * nb_all[i] * cols * p;
+          }
+        }
+        // per colour batch: (box, block) work items of the block update
+        std::vector<int2> gwork;
+        for (size_t bi2 = 0; bi2 < binfo.size(); ++bi2) {
+          gwork_off[bi2] = (int64_t)gwork.size();
+          for (int q = binfo[bi2].first; q < binfo[bi2].first + binfo[bi2].count; ++q) {
+            const int i = hb[q].box;
+            for (int t = gpstart[i]; t < gpstart[i + 1]; ++t) gwork.push_back(make_int2(q, t));
+          }
+        }
+        gwork_off[binfo.size()] = (int64_t)gwork.size();
+        gwork_b.alloc(sizeof(int2) * std::max<size_t>(gwork.size(), 1), s);
+        if (!gwork.empty())
+          CK(cudaMemcpyAsync(gwork_b.p, gwork.data(), sizeof(int2) * gwork.size(), cudaMemcpyHostToDevice, s));
+        gtab_b.alloc(sizeof(rsrs::GBlk) * gtab.size(), s);
+        gps_b.alloc(sizeof(int) * gpstart.size(), s);
+        CK(cudaMemcpyAsync(gtab_b.p, gtab.data(), sizeof(rsrs::GBlk) * gtab.size(), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(gps_b.p, gpstart.data(), sizeof(int) * gpstart.size(), cudaMemcpyHostToDevice, s));
+        DBuf pre_b;
+        pre_b.alloc(sizeof(NTDesc) * std::max<size_t>(pre.size(), 1), s);
+        if (!pre.empty()) {
+          CK(cudaMemcpyAsync(pre_b.p, pre.data(), sizeof(NTDesc) * pre.size(), cudaMemcpyHostToDevice, s));
+          tic(KC_GRAM);
+          launch_nt(cplx, pre_b.as<NTDesc>(), (int)pre.size(), maxnb, maxcols, s, launches);
+          toc();
+          double rows = 0;
+          for (int i = 0; i < nbox; ++i) rows += nb_all[i];
+          account(KC_GRAM, (cplx ? 4.0 : 1.0) * fl, (double)sS * (sides * rows * p + sides * poff));
+        }
+        stream_sync(s);   // pre_b is released at scope end
+      }
+      // ---- descriptors, built on the device from the box records (descs.cuh)
+      const int nsd = sym ? 1 : 2;
+      const size_t nbx = hb.size();
+      size_t dsz = 0;
+      auto slot = [&](size_t bytes) {
+        const size_t at = dsz;
+        dsz += (bytes + 15) & ~size_t(15);
         return at;
       };
-      const size_t o_gram = put(nt_gram.data(), sizeof(NTDesc) * nt_gram.size());
-      const size_t o_h = put(nt_h.data(), sizeof(NTDesc) * nt_h.size());
-      const size_t o_proj = put(nn_proj.data(), sizeof(NNDesc) * nn_proj.size());
-      const size_t o_ef = put(nn_ef.data(), sizeof(NNDesc) * nn_ef.size());
-      const size_t o_g = put(nn_g.data(), sizeof(NNDesc) * nn_g.size());
-      const size_t o_upd = put(nn_upd.data(), sizeof(NNDesc) * nn_upd.size());
-      const size_t o_chol = put(chol.data(), sizeof(CholDesc) * chol.size());
-      descbuf.ensure(hdesc.size() + 16, s);
-      if (!hdesc.empty()) CK(cudaMemcpyAsync(descbuf.p, hdesc.data(), hdesc.size(), cudaMemcpyHostToDevice, s));
-      stream_sync(s);
-      const char* dd = descbuf.as<char>();
+      const size_t o_gram = slot(sizeof(NTDesc) * nbx * (use_blocks ? 1 : 2) * nsd);
+      const size_t o_h = slot(sizeof(NTDesc) * nbx * nsd);
+      const size_t o_proj = slot(sizeof(NNDesc) * nbx * nsd);
+      const size_t o_ef = slot(sizeof(NNDesc) * nbx * 2 * nsd);
+      const size_t o_g = slot(sizeof(NNDesc) * nbx * 2);
+      const size_t o_upd = slot(sizeof(NNDesc) * nbx * nsd);
+      const size_t o_chol = slot(sizeof(CholDesc) * nbx * nsd);
+      descbuf.ensure(dsz + 16, s);
+      char* dd = descbuf.as<char>();
+      if (nbx) {
+        rsrs::DescParams dp{};
+        dp.Y = Y; dp.Z = Z; dp.Om = Om; dp.Ps = Ps; dp.ld = ld; dp.nld = nld; dp.p = p; dp.SC = SC;
+        dp.sym = sym; dp.blocks = use_blocks; dp.nbox = (int)nbx; dp.dws = dws; dp.fpool = fpool; dp.diws = diws;
+        dp.boxes = dboxes;
+        dp.gram = reinterpret_cast<NTDesc*>(dd + o_gram);
+        dp.h = reinterpret_cast<NTDesc*>(dd + o_h);
+        dp.proj = reinterpret_cast<NNDesc*>(dd + o_proj);
+        dp.ef = reinterpret_cast<NNDesc*>(dd + o_ef);
+        dp.g = reinterpret_cast<NNDesc*>(dd + o_g);
+        dp.upd = reinterpret_cast<NNDesc*>(dd + o_upd);
+        dp.chol = reinterpret_cast<CholDesc*>(dd + o_chol);
+        rsrs::make_desc_kernel<<<(unsigned)((nbx + 127) / 128), 128, 0, s>>>(dp);
+        post("make_desc_kernel", s, launches);
+      }
       const NTDesc* Dgram = reinterpret_cast<const NTDesc*>(dd + o_gram);
       const NTDesc* Dh = reinterpret_cast<const NTDesc*>(dd + o_h);
       const NNDesc* Dproj = reinterpret_cast<const NNDesc*>(dd + o_proj);
@@ -905,8 +1000,23 @@ struct Planner {
           // descriptors per box: 4 Gram / 2 Cholesky / 2 projection / 2 H / 4 E-F / 2 L-U,
           // halved by the symmetric shortcut (Y / Omega side only)
           const int ns = sym ? 1 : 2;
+          const int gpb = (use_blocks ? 1 : 2) * ns;   // Gram descriptors per box (cross products only with blocks)
           tic(KC_GRAM);
-          launch_nt(cplx, Dgram + 2 * ns * q0, 2 * ns * n, bi.max_r, bi.max_r, s, launches);
+          if (use_blocks) {
+            launch_nt(cplx, Dgram + gpb * q0, gpb * n, bi.max_nb, bi.max_r, s, launches);
+            dim3 ga(n, max_nnbr);
+            double* pO = gpool->as<double>();
+            double* pP = pO + SC * gpool_side;
+            if (cplx)
+              rsrs::gram_assemble_kernel<true><<<ga, 256, 0, s>>>(dbx, dboxes, diws, dnbr, gtab_b.as<rsrs::GBlk>(),
+                                                                  gps_b.as<int>(), pO, pP, dws, sides);
+            else
+              rsrs::gram_assemble_kernel<false><<<ga, 256, 0, s>>>(dbx, dboxes, diws, dnbr, gtab_b.as<rsrs::GBlk>(),
+                                                                   gps_b.as<int>(), pO, pP, dws, sides);
+            post("gram_assemble_kernel", s, launches);
+          } else {
+            launch_nt(cplx, Dgram + gpb * q0, gpb * n, bi.max_r, bi.max_r, s, launches);
+          }
           toc();
           tic(KC_CHOL);
           launch_chol_any(cplx, Dchol + ns * q0, ns * n, bi.max_r, bi.max_nb, s, launches);
@@ -930,6 +1040,23 @@ struct Planner {
           }
           tic(KC_EF);
           launch_nn(cplx, Def + 2 * ns * q0, 2 * ns * n, bi.max_nb, p, s, launches);
+          if (use_blocks) {      // keep the Gram blocks equal to F Omega Omega^* F^* (the E/F on Omega_s)
+            const size_t bi_idx = &bi - &binfo[0];
+            const int nw = (int)(gwork_off[bi_idx + 1] - gwork_off[bi_idx]);
+            if (nw > 0) {
+              double* pO = gpool->as<double>();
+              double* pP = pO + SC * gpool_side;
+              const int2* wk = gwork_b.as<int2>() + gwork_off[bi_idx];
+              dim3 gu(nw, sides);
+              if (cplx)
+                rsrs::gblk_update_kernel<true><<<gu, 256, rsrs::gblk_smem<true>(), s>>>(dboxes, wk, gtab_b.as<rsrs::GBlk>(), pO, pP, fpool,
+                                                                   diws);
+              else
+                rsrs::gblk_update_kernel<false><<<gu, 256, rsrs::gblk_smem<false>(), s>>>(dboxes, wk, gtab_b.as<rsrs::GBlk>(), pO, pP, fpool,
+                                                                    diws);
+              post("gblk_update_kernel", s, launches);
+            }
+          }
           toc();
           {
             const size_t sm = 2 * (size_t)bi.max_nb * (bi.max_nb + 1) * sS + 3 * (size_t)bi.max_nb * 4 + 64;
@@ -1281,6 +1408,7 @@ static rsrs_status factor_impl(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, v
     P.cplx = f->cplx;
     P.SC = f->sc;
     P.sym = o.symmetric != 0;
+    P.gram_blocks = o.direct_gram == 0;
     P.comm = (comm && comm->nranks > 1) ? comm : nullptr;
     P.part = rsrs::make_partition(T, comm ? comm->nranks : 1, o.gather_level, o.top_level);
     P.run((double*)Y, (double*)Z, (double*)Omega, (double*)Psi, ld);
@@ -1323,7 +1451,7 @@ static rsrs_status check_args(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, vo
     return fail(RSRS_ERR_INVALID, "rsrs_factor: the symmetric shortcut is for real symmetric operators (RSRS_F64)");
   if (p < 1 || ld < p || (ld & 1)) return fail(RSRS_ERR_INVALID, "rsrs_factor: need 1 <= p <= ld and ld even");
   if (dt != RSRS_F64 && dt != RSRS_C128) return fail(RSRS_ERR_INVALID, "rsrs_factor: unknown dtype");
-  o = rsrs_opts{1e-6, 1.0, 1.0, 10, 2, 0, 1, nullptr, nullptr, 0, -1, 0};
+  o = rsrs_opts{1e-6, 1.0, 1.0, 10, 2, 0, 1, nullptr, nullptr, 0, -1, 0, 0};
   if (opts) o = *opts;
   if (!(o.eps > 0) || !(o.level_growth > 0) || !(o.id_scale > 0) || o.oversample < 0 || o.top_level < 1 ||
       o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks)

@@ -1,0 +1,155 @@
+// Level-wide near-field Gram blocks (single GPU).
+//
+// Every near field of a level is a concatenation of whole neighbour boxes, and
+// the Omega / Psi rows of a box change exactly once during the level: when the
+// box is eliminated, its skeleton rows take the E/F update Omega_s += T^* Omega_r
+// (the Omega_r rows are dead afterwards, R15).
+// So the near-field Gram of box b, C_b = Omega_near Omega_near^*, is a matrix of
+// blocks G(i, j) = Omega_i Omega_j^* over pairs of boxes i, j that meet in some
+// near field (both neighbours of one nonempty box).  The blocks are computed once
+// per level (one batched DMMA GEMM over the box pairs instead of one r x r x p
+// GEMM per box), kept current by applying F (rows) / F^* (columns) when a box
+// is eliminated, and each C_b is assembled from them by a gather.
+#pragma once
+#include "common.cuh"
+
+namespace rsrs {
+
+// One partner entry of a box (entries of a box sorted by partner).
+struct GBlk {
+  int j;       // partner box
+  int mode;    // 0: stored block is (this, j) -- rows are this box; 1: stored (j, this) -- columns; 2: (this, this)
+  int nrow, ncol;   // shape of the stored block
+  i64 off;     // scalar offset of the stored block in the pool (row-major, leading dimension ld)
+  int ld, pad;
+};
+
+// After the colour batch's E/F updates: for every (eliminated box, block) work item
+// (grid x; grid y = side), stage the block (<= 64 x 64) and T in shared memory,
+// apply F = [rows s += T^* rows r] to the box's rows and / or F^* to its columns,
+// and write the block back.  Boxes of one colour never share a block.
+constexpr int GB_MAX = 64;
+constexpr int GB_LD = GB_MAX + 1;
+template <bool C> constexpr int gblk_smem() { return 2 * GB_MAX * GB_LD * (C ? 16 : 8) + 2 * GB_MAX * 4; }
+template <bool C>
+__global__ void __launch_bounds__(256) gblk_update_kernel(const BoxDev* __restrict__ level_boxes,
+                                                          const int2* __restrict__ work,
+                                                          const GBlk* __restrict__ tab, double* __restrict__ poolO,
+                                                          double* __restrict__ poolP, const double* __restrict__ fpoold,
+                                                          const int* __restrict__ iws) {
+  typedef typename ScalarOf<C>::T S;
+  extern __shared__ __align__(16) double gsm[];
+  S* Bs = reinterpret_cast<S*>(gsm);        // block (nrow x ncol), ld GB_LD
+  S* Ts = Bs + GB_MAX * GB_LD;              // T (n_r x k), ld GB_LD
+  int* skl = reinterpret_cast<int*>(Ts + GB_MAX * GB_LD);
+  int* red = skl + GB_MAX;
+  const int2 w = work[blockIdx.x];
+  const BoxDev& b = level_boxes[w.x];
+  const int k = b.k, nr = b.nr;
+  if (b.status != ST_OK || nr <= 0 || k <= 0) return;
+  const GBlk e = tab[w.y];
+  const int tid = threadIdx.x;
+  const S* T = reinterpret_cast<const S*>(fpoold) + b.f_T;
+  for (int idx = tid; idx < nr * k; idx += 256) Ts[(idx / k) * GB_LD + idx % k] = T[(i64)(idx / k) * b.ldn + idx % k];
+  for (int q = tid; q < k; q += 256) skl[q] = iws[b.off_skelrow + q] - b.row0;
+  for (int i = tid; i < nr; i += 256) red[i] = iws[b.off_redrow + i] - b.row0;
+  S* B = reinterpret_cast<S*>(blockIdx.y ? poolP : poolO) + e.off;
+  for (int idx = tid; idx < e.nrow * e.ncol; idx += 256) {
+    const int r = idx / e.ncol, c = idx % e.ncol;
+    Bs[r * GB_LD + c] = B[(i64)r * e.ld + c];
+  }
+  __syncthreads();
+  if (e.mode != 1) {   // rows: B[s, :] += T^* B[r, :]   (red and skel rows are disjoint)
+    for (int idx = tid; idx < k * e.ncol; idx += 256) {
+      const int q = idx / e.ncol, c = idx % e.ncol;
+      S acc = Bs[skl[q] * GB_LD + c];
+      for (int i = 0; i < nr; ++i) acc = s_add(acc, s_mul(s_conj(Ts[i * GB_LD + q]), Bs[red[i] * GB_LD + c]));
+      Bs[skl[q] * GB_LD + c] = acc;
+    }
+    __syncthreads();
+  }
+  if (e.mode != 0) {   // columns: B[:, s] += B[:, r] T
+    for (int idx = tid; idx < e.nrow * k; idx += 256) {
+      const int r = idx / k, q = idx % k;
+      S acc = Bs[r * GB_LD + skl[q]];
+      for (int i = 0; i < nr; ++i) acc = s_add(acc, s_mul(Bs[r * GB_LD + red[i]], Ts[i * GB_LD + q]));
+      Bs[r * GB_LD + skl[q]] = acc;
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < e.nrow * e.ncol; idx += 256) {
+    const int r = idx / e.ncol, c = idx % e.ncol;
+    B[(i64)r * e.ld + c] = Bs[r * GB_LD + c];
+  }
+}
+
+// C_b[pos(q1) + a, pos(q2) + c] = G(n_q1, n_q2)[act_q1[a], act_q2[c]] for slots q2 <= q1
+// of b's neighbour list (the lower block triangle of the near-field Gram).
+// Grid (boxes of the batch, neighbour slots q1).
+template <bool C>
+__global__ void __launch_bounds__(256) gram_assemble_kernel(const BoxDev* __restrict__ boxes,
+                                                            const BoxDev* __restrict__ level_boxes,
+                                                            const int* __restrict__ iws, const int* __restrict__ nbrrec,
+                                                            const GBlk* __restrict__ tab, const int* __restrict__ pstart,
+                                                            const double* __restrict__ poolO,
+                                                            const double* __restrict__ poolP,
+                                                            double* __restrict__ wsd, int sides) {
+  typedef typename ScalarOf<C>::T S;
+  __shared__ int pos[64], cnt[64], bx[64], idxs[64];
+  __shared__ int act1[192];
+  const BoxDev& b = boxes[blockIdx.x];
+  const int q1 = blockIdx.y;
+  if (q1 >= b.nnbr || b.status != ST_OK) return;
+  const int* nd = nbrrec + b.off_nbr;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    int o = 0;
+    for (int q = 0; q < b.nnbr; ++q) {
+      const int idx = nd[4 * q];
+      const int c = idx >= 0 ? level_boxes[idx].k : nd[4 * q + 2];
+      pos[q] = o;
+      cnt[q] = c;
+      bx[q] = nd[4 * q + 3];
+      idxs[q] = idx;
+      o += c;
+    }
+  }
+  __syncthreads();
+  const int n1 = cnt[q1];
+  if (n1 == 0) return;
+  const int i1 = idxs[q1];
+  if (i1 >= 0) {
+    const BoxDev& nb1 = level_boxes[i1];
+    for (int a = tid; a < n1; a += 256) act1[a] = iws[nb1.off_skelrow + a] - nb1.row0;
+  } else {
+    for (int a = tid; a < n1; a += 256) act1[a] = a;
+  }
+  __syncthreads();
+  const int box1 = bx[q1];
+  const GBlk* t1 = tab + pstart[box1];
+  const i64 ldr = b.ldr;
+  for (int q2 = 0; q2 <= q1; ++q2) {
+    const int n2 = cnt[q2];
+    if (n2 == 0) continue;
+    const int box2 = bx[q2];
+    int ei = 0;
+    while (t1[ei].j != box2) ++ei;        // the partner table holds every pair that meets in a near field
+    const GBlk e = t1[ei];
+    const int i2 = idxs[q2];
+    const int* sk2 = i2 >= 0 ? iws + level_boxes[i2].off_skelrow : nullptr;
+    const int r02 = i2 >= 0 ? level_boxes[i2].row0 : 0;
+    for (int side = 0; side < sides; ++side) {
+      const S* B = reinterpret_cast<const S*>(side ? poolP : poolO) + e.off;
+      S* Cb = reinterpret_cast<S*>(wsd) + b.off_aug + (side ? (i64)(b.rmax + b.nb) * ldr : 0);
+      for (int idx = tid; idx < n1 * n2; idx += 256) {
+        const int a = idx / n2, c = idx % n2;
+        const int ra = act1[a];
+        const int rc = sk2 ? sk2[c] - r02 : c;
+        const S v = (e.mode == 1) ? s_conj(B[(i64)rc * e.ld + ra]) : B[(i64)ra * e.ld + rc];
+        Cb[(i64)(pos[q1] + a) * ldr + pos[q2] + c] = v;
+      }
+    }
+  }
+}
+
+}  // namespace rsrs

@@ -24,7 +24,7 @@ def run_oracle(cfg, X, Y, Z, Om, Ps, root, **kw):
     return t, f
 
 
-def run_gpu(cfg, X, Y, Z, Om, Ps, root, p=None, profile=False):
+def run_gpu(cfg, X, Y, Z, Om, Ps, root, p=None, profile=False, **kw):
     import torch
 
     import paper_2311_01451_b200 as R
@@ -34,7 +34,7 @@ def run_gpu(cfg, X, Y, Z, Om, Ps, root, p=None, profile=False):
     dev = torch.device("cuda:0")
     T = [torch.from_numpy(np.ascontiguousarray(M[perm][:, :p])).to(dev) for M in (Y, Z, Om, Ps)]
     f = R.factor(t, *T, p=p, eps=cfg.eps, level_growth=cfg.g, id_scale=cfg.c_id, oversample=cfg.l,
-                 profile=profile)
+                 profile=profile, **kw)
     return t, f
 
 

@@ -51,8 +51,8 @@ def _apply_emul(fs, v):
 
 
 def _single(cfg, X, Y, Z, Om, Ps):
-    import torch
-    t, f = run_gpu(cfg, X, Y, Z, Om, Ps, cfg.root())
+    # the ranks compute each near-field Gram directly; so does this single-GPU reference
+    t, f = run_gpu(cfg, X, Y, Z, Om, Ps, cfg.root(), direct_gram=True)
     return t, f
 
 

@@ -29,7 +29,7 @@ def _sym_problem(cfg):
     return X, A, Y, Om, b
 
 
-def _gpu_sym(cfg, X, Y, Om, emulate=0):
+def _gpu_sym(cfg, X, Y, Om, emulate=0, **kw):
     import torch
 
     import paper_2311_01451_b200 as R
@@ -42,7 +42,7 @@ def _gpu_sym(cfg, X, Y, Om, emulate=0):
                                id_scale=cfg.c_id, oversample=cfg.l, symmetric=True)
         return t, fs
     f = R.factor(t, Yd, None, Od, None, p=cfg.p, eps=cfg.eps, level_growth=cfg.g, id_scale=cfg.c_id,
-                 oversample=cfg.l, symmetric=True)
+                 oversample=cfg.l, symmetric=True, **kw)
     return t, f
 
 
@@ -97,7 +97,7 @@ def test_symmetric_shortcut_emulated_ranks_bit_exact():
     import paper_2311_01451_b200 as R
     cfg = W.CONFIGS["c1"]
     X, A, Y, Om, b = _sym_problem(cfg)
-    t, f = _gpu_sym(cfg, X, Y, Om)
+    t, f = _gpu_sym(cfg, X, Y, Om, direct_gram=True)
     _, fs = _gpu_sym(cfg, X, Y, Om, emulate=3)
     x1 = torch.from_numpy(b.copy()).cuda()
     f.solve(x1)
