@@ -70,6 +70,9 @@ typedef struct {
                           G_L = G_U^T.  Z and Psi are ignored (may be NULL).  RSRS_F64 only. */
   int direct_gram;     /* 1: compute every near-field Gram directly (r x r x p per box) instead of
                           assembling it from the level-wide box-pair blocks (single rank) */
+  int push_updates;    /* 1: apply every L/U sample update when its box is eliminated (push, as the
+                          multi-GPU ranks do) instead of pulling the updates of a box's rows when the
+                          box comes up (single rank) */
 } rsrs_opts;
 
 /* Statistics of a factorization (Table 1). */

@@ -90,6 +90,11 @@ struct BoxDev {
   i64 f_red, f_skel, f_c;              // ints (tree positions) in the level index pool
   int r, self_pos;                     // dynamic: |near| and position of b inside near
   int k, nr, nc, status;               // dynamic: ID results
+  int ncp;                             // dynamic: leading entries of c outside unprocessed neighbours
+  int kpull;                           // dynamic: inner dimension of the pulled L/U update (sum of n_r)
+  i64 off_nflag;                       // ints: per near position, 1 = row of an unprocessed neighbour
+  i64 off_prow;                        // ints: store rows of the pulled Y_r / Z_r (capacity rmax)
+  i64 off_pull;                        // scalars: pulled update operands A_Y, A_Z (nb x ldr each)
 };
 
 // status codes in BoxDev::status (0 = ok)

@@ -36,6 +36,7 @@ __global__ void __launch_bounds__(256) id_kernel(BoxDev* __restrict__ boxes, con
       b.k = nb;
       b.nr = 0;
       b.nc = r;
+      b.ncp = r;
     }
     return;
   }
@@ -167,36 +168,46 @@ __global__ void __launch_bounds__(256) id_kernel(BoxDev* __restrict__ boxes, con
       for (int s = 0; s < k; ++s) T[(i64)ri * ldn + rank_of[s]] = s_conj(Hs[s * ldh + col]);
     }
   }
-  // coupled set c = near \ red in near order (ballot compaction by warp 0)
+  // coupled set c = near \ red, as two groups in near order (ballot compaction by warp 0):
+  // rows that will not be eliminated later on this level (own skeletons, skeletons of
+  // eliminated neighbours) first, then the rows of not-yet-eliminated neighbours -- those
+  // take their L/U update by a pull when their own box comes up (single GPU)
+  __shared__ int ncp_s;
   if (warp == 0) {
     const int* near = iws + b.off_rows;
+    const int* nflag = iws + b.off_nflag;
     int* crow = iws + b.off_crow;
     int* cpos = iws + b.off_cpos;
     int* c_tp = ipool + b.f_c;
     int base = 0;
-    for (int p0 = 0; p0 < r; p0 += 32) {
-      const int pp = p0 + lane;
-      bool keep = false;
-      int row = 0;
-      if (pp < r) {
-        row = near[pp];
-        const int loc = pp - b.self_pos;
-        keep = !(loc >= 0 && loc < nb && is_red[loc]);
+    for (int grp = 0; grp < 2; ++grp) {
+      if (grp == 1 && lane == 0) ncp_s = base;
+      for (int p0 = 0; p0 < r; p0 += 32) {
+        const int pp = p0 + lane;
+        bool keep = false;
+        int row = 0;
+        if (pp < r) {
+          row = near[pp];
+          const int loc = pp - b.self_pos;
+          keep = !(loc >= 0 && loc < nb && is_red[loc]) && nflag[pp] == grp;
+        }
+        const unsigned mask = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+          const int o = base + __popc(mask & ((1u << lane) - 1u));
+          crow[o] = row;
+          cpos[o] = pp;
+          c_tp[o] = gidx[row];
+        }
+        base += __popc(mask);
       }
-      const unsigned mask = __ballot_sync(0xffffffffu, keep);
-      if (keep) {
-        const int o = base + __popc(mask & ((1u << lane) - 1u));
-        crow[o] = row;
-        cpos[o] = pp;
-        c_tp[o] = gidx[row];
-      }
-      base += __popc(mask);
     }
   }
+  __syncthreads();
   if (tid == 0) {
     b.k = k;
     b.nr = nr;
     b.nc = r - nr;
+    b.ncp = ncp_s;
     if (k > w - oversample) b.status = ST_SAMPLES;   // rank not resolvable with p samples
   }
 }
@@ -525,6 +536,67 @@ __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ bo
 }
 
 // ---------------------------------------------------------------------------
+// Pulled L/U update (single GPU).  When a box j comes up, the eliminated
+// neighbours n have not pushed Y_c -= G_L Y_r into j's rows (they only updated
+// rows that are never eliminated later on the level); j applies all of them at
+// once:  Y_j -= [G_L^(n1)[j, :] G_L^(n2)[j, :] ..] [Y_r(n1); Y_r(n2); ..]  and
+// Z_j -= [G_U^(n1)[:, j]^* ..] [Z_r(n1); ..]  -- one GEMM with K = sum n_r instead
+// of up to 3^d - 1 read-modify-write passes over j's rows.  This kernel gathers
+// the operands (A_Y, A_Z: n_b x K into ws at off_pull; the Y_r row list at off_prow).
+// j's rows are one contiguous, ascending run in the second group of c(n).
+// ---------------------------------------------------------------------------
+template <bool C>
+__global__ void __launch_bounds__(256) pull_assemble_kernel(BoxDev* __restrict__ boxes,
+                                                            const BoxDev* __restrict__ level_boxes,
+                                                            int* __restrict__ iws, const int* __restrict__ nbrrec,
+                                                            const double* __restrict__ fpoold, double* __restrict__ wsd,
+                                                            int zside) {
+  typedef typename ScalarOf<C>::T S;
+  BoxDev& b = boxes[blockIdx.x];
+  const int nb = b.nb;
+  const int* nd = nbrrec + b.off_nbr;
+  const S* fpool = reinterpret_cast<const S*>(fpoold);
+  S* AY = reinterpret_cast<S*>(wsd) + b.off_pull;
+  S* AZ = AY + (i64)nb * b.ldr;
+  int* prow = iws + b.off_prow;
+  __shared__ int K0s, offs;
+  const int tid = threadIdx.x;
+  if (tid == 0) K0s = 0;
+  __syncthreads();
+  for (int q = 0; q < b.nnbr; ++q) {
+    const int idx = nd[4 * q];
+    if (idx < 0) continue;                              // not eliminated (or the box itself)
+    const BoxDev& n = level_boxes[idx];
+    const int nr = n.nr;
+    if (nr <= 0 || n.status != ST_OK) continue;
+    if (tid == 0) {                                     // first row of b in the second group of c(n)
+      const int* crow = iws + n.off_crow;
+      int lo = n.ncp, hi = n.nc;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (crow[mid] < b.row0) lo = mid + 1;
+        else hi = mid;
+      }
+      offs = lo;
+    }
+    __syncthreads();
+    const int o = offs, K0 = K0s;
+    const S* GL = fpool + n.f_GL;      // nc x nr, ld ldn(n)
+    const S* GU = fpool + n.f_GU;      // nr x nc, ld ldr(n)
+    for (int idx2 = tid; idx2 < nb * nr; idx2 += 256) {
+      const int a = idx2 / nr, i = idx2 % nr;
+      AY[(i64)a * b.ldr + K0 + i] = GL[(i64)(o + a) * n.ldn + i];
+      if (zside) AZ[(i64)a * b.ldr + K0 + i] = s_conj(GU[(i64)i * n.ldr + o + a]);
+    }
+    for (int i = tid; i < nr; i += 256) prow[K0 + i] = iws[n.off_redrow + i];
+    __syncthreads();
+    if (tid == 0) K0s = K0 + nr;
+    __syncthreads();
+  }
+  if (tid == 0) b.kpull = K0s;
+}
+
+// ---------------------------------------------------------------------------
 // Near-field row list of every box of a colour batch, built on the device:
 // near = active(I_b u I_n) in Morton order of the neighbour boxes
 // (R2).  Neighbours processed by an earlier
@@ -540,6 +612,7 @@ __global__ void build_near_kernel(BoxDev* __restrict__ boxes, const BoxDev* __re
   const int* nd = nbrrec + b.off_nbr;
   int* near = iws + b.off_rows;
   for (int t = lane; t < b.nb; t += 32) near[b.rmax + t] = b.row0 + t;   // the box's own rows (cross product)
+  int* nflag = iws + b.off_nflag;
   int o = 0, selfp = 0;
   for (int q = 0; q < b.nnbr; ++q) {
     const int idx = nd[4 * q], r0 = nd[4 * q + 1];
@@ -548,10 +621,18 @@ __global__ void build_near_kernel(BoxDev* __restrict__ boxes, const BoxDev* __re
       const BoxDev& nbx = level_boxes[idx];
       cnt = nbx.k;
       const int* src = iws + nbx.off_skelrow;
-      for (int t = lane; t < cnt; t += 32) near[o + t] = src[t];
+      for (int t = lane; t < cnt; t += 32) {
+        near[o + t] = src[t];
+        nflag[o + t] = 0;
+      }
     } else {
-      if (r0 == b.row0) selfp = o;
-      for (int t = lane; t < cnt; t += 32) near[o + t] = r0 + t;
+      const bool self = (r0 == b.row0);
+      if (self) selfp = o;
+      const int fl = (self || idx == -2) ? 0 : 1;   // 1: rows of a not-yet-eliminated neighbour
+      for (int t = lane; t < cnt; t += 32) {
+        near[o + t] = r0 + t;
+        nflag[o + t] = fl;
+      }
     }
     o += cnt;
   }

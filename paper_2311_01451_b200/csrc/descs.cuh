@@ -14,7 +14,7 @@ namespace rsrs {
 struct DescParams {
   double *Y, *Z, *Om, *Ps;       // current store
   i64 ld, nld;
-  int p, SC, sym, blocks, nbox, pad;
+  int p, SC, sym, blocks, nbox, pull;   // pull: L/U updates of not-yet-eliminated rows are pulled
   double* dws;                   // level workspace
   double* fpool;                 // level factor pool
   int* diws;                     // level int workspace
@@ -25,6 +25,7 @@ struct DescParams {
   NNDesc* ef;
   NNDesc* g;
   NNDesc* upd;
+  NNDesc* pullD;                 // [Y, Z] per box (pull mode)
   CholDesc* chol;
 };
 
@@ -148,12 +149,26 @@ __global__ void make_desc_kernel(const DescParams P) {
     NNDesc u{};
     u.A = P.fpool + SC * x.f_GL; u.lda = ldn; u.transA = 0; u.B = P.Y; u.rowB = redrow; u.ldb = ld;
     u.D = P.Y; u.rowD = crow; u.ldd = ld; u.Cin = nullptr; u.m = rm; u.n = p; u.K = nb;
-    u.alpha = -1.0; u.beta = 1.0; u.pm = &dx->nc; u.pK = &dx->nr;
+    u.alpha = -1.0; u.beta = 1.0; u.pm = P.pull ? &dx->ncp : &dx->nc; u.pK = &dx->nr;
     o[0] = u;
     if (!P.sym) {
       NNDesc uz = u;
       uz.A = P.fpool + SC * x.f_GU; uz.lda = ldr; uz.transA = 1; uz.B = P.Z; uz.D = P.Z;
       o[1] = uz;
+    }
+  }
+  // ---- pulled L/U update into the box's own rows (pull_assemble_kernel gathers A and the rows)
+  if (P.pull) {
+    NNDesc* o = P.pullD + (i64)q * ns;
+    double* AY = P.dws + SC * x.off_pull;
+    NNDesc v{};
+    v.A = AY; v.lda = ldr; v.transA = 0; v.B = P.Y; v.rowB = P.diws + x.off_prow; v.ldb = ld;
+    v.D = P.Y + SC * (i64)x.row0 * ld; v.rowD = nullptr; v.ldd = ld; v.Cin = nullptr;
+    v.m = nb; v.n = p; v.K = rm; v.alpha = -1.0; v.beta = 1.0; v.pK = &dx->kpull;
+    o[0] = v;
+    if (!P.sym) {
+      v.A = AY + SC * (i64)nb * ldr; v.B = P.Z; v.D = P.Z + SC * (i64)x.row0 * ld;
+      o[1] = v;
     }
   }
 }

@@ -381,6 +381,7 @@ struct Planner {
   bool sym = false;    // symmetric shortcut: Psi = Omega, Z = Y, only the Y / Omega side runs
   bool gram_blocks = true;   // level-wide near-field Gram blocks (gram.cuh; single rank)
   bool level_blocks = false; // the current level uses them (account_box counts the cross products only)
+  bool push_updates = false; // push every L/U update (as the multi-GPU ranks do) instead of pulling
   int SC = 1;          // doubles per scalar (1 real, 2 complex); all offsets below are in scalars
   std::vector<cudaEvent_t> evpool;
   struct Pend {
@@ -663,11 +664,14 @@ struct Planner {
           x.off_xrc = wo;   wo += nb * ldr;
           x.off_xcr = wo;   wo += r * ldn;
           x.off_linv = wo;  wo += 2 * ((r + 63) / 64) * 64 * 64;
+          x.off_pull = wo;  wo += 2 * nb * ldr;
           x.off_rows = ioff;    ioff += r + nb;
           x.off_skelrow = ioff; ioff += nb;
           x.off_redrow = ioff;  ioff += nb;
           x.off_crow = ioff;    ioff += r;
           x.off_cpos = ioff;    ioff += r;
+          x.off_nflag = ioff;   ioff += r;
+          x.off_prow = ioff;    ioff += r;
           x.off_nbr = noff;     noff += 4 * x.nnbr;
           x.f_T = foff;     foff += nb * ldn;
           x.f_GL = foff;    foff += r * ldn;
@@ -895,6 +899,8 @@ struct Planner {
       const size_t o_g = slot(sizeof(NNDesc) * nbx * 2);
       const size_t o_upd = slot(sizeof(NNDesc) * nbx * nsd);
       const size_t o_chol = slot(sizeof(CholDesc) * nbx * nsd);
+      const bool pull = R == 1 && !push_updates;
+      const size_t o_pull = slot(sizeof(NNDesc) * nbx * nsd);
       descbuf.ensure(dsz + 16, s);
       char* dd = descbuf.as<char>();
       if (nbx) {
@@ -909,6 +915,8 @@ struct Planner {
         dp.g = reinterpret_cast<NNDesc*>(dd + o_g);
         dp.upd = reinterpret_cast<NNDesc*>(dd + o_upd);
         dp.chol = reinterpret_cast<CholDesc*>(dd + o_chol);
+        dp.pull = pull;
+        dp.pullD = reinterpret_cast<NNDesc*>(dd + o_pull);
         rsrs::make_desc_kernel<<<(unsigned)((nbx + 127) / 128), 128, 0, s>>>(dp);
         post("make_desc_kernel", s, launches);
       }
@@ -919,6 +927,7 @@ struct Planner {
       const NNDesc* Dg = reinterpret_cast<const NNDesc*>(dd + o_g);
       const NNDesc* Dupd = reinterpret_cast<const NNDesc*>(dd + o_upd);
       const CholDesc* Dchol = reinterpret_cast<const CholDesc*>(dd + o_chol);
+      const NNDesc* Dpull = reinterpret_cast<const NNDesc*>(dd + o_pull);
 
       // global skeleton counts of the level (-1 = not processed yet)
       std::vector<int> k_all(nbox, -1);
@@ -952,7 +961,8 @@ struct Planner {
           for (int qb = q0; qb < q0 + n; ++qb)
             for (int t = fs_first[qb]; t < fs_first[qb + 1]; ++t) {
               const int rec = foreign_slot[t].first, j = foreign_slot[t].second;
-              hnbr[rec] = -1;
+              // -2: halo block of a foreign box eliminated in an earlier colour (its skeletons)
+              hnbr[rec] = (nb_all[j] > 0 && lv.colour[j] < bi.colour) ? -2 : -1;
               hnbr[rec + 1] = halo0[j] >= 0 ? halo0[j] : 0;
               hnbr[rec + 2] = halo0[j] >= 0 ? cnt[j] : 0;
             }
@@ -1001,6 +1011,14 @@ struct Planner {
           // halved by the symmetric shortcut (Y / Omega side only)
           const int ns = sym ? 1 : 2;
           const int gpb = (use_blocks ? 1 : 2) * ns;   // Gram descriptors per box (cross products only with blocks)
+          if (pull) {            // L/U updates of the eliminated neighbours into this batch's rows
+            tic(KC_UPD);
+            if (cplx) rsrs::pull_assemble_kernel<true><<<n, 256, 0, s>>>(dbx, dboxes, diws, dnbr, fpool, dws, !sym);
+            else rsrs::pull_assemble_kernel<false><<<n, 256, 0, s>>>(dbx, dboxes, diws, dnbr, fpool, dws, !sym);
+            post("pull_assemble_kernel", s, launches);
+            launch_nn(cplx, Dpull + ns * q0, ns * n, bi.max_nb, p, s, launches);
+            toc();
+          }
           tic(KC_GRAM);
           if (use_blocks) {
             launch_nt(cplx, Dgram + gpb * q0, gpb * n, bi.max_nb, bi.max_r, s, launches);
@@ -1409,6 +1427,7 @@ static rsrs_status factor_impl(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, v
     P.SC = f->sc;
     P.sym = o.symmetric != 0;
     P.gram_blocks = o.direct_gram == 0;
+    P.push_updates = o.push_updates != 0;
     P.comm = (comm && comm->nranks > 1) ? comm : nullptr;
     P.part = rsrs::make_partition(T, comm ? comm->nranks : 1, o.gather_level, o.top_level);
     P.run((double*)Y, (double*)Z, (double*)Omega, (double*)Psi, ld);
@@ -1451,7 +1470,7 @@ static rsrs_status check_args(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, vo
     return fail(RSRS_ERR_INVALID, "rsrs_factor: the symmetric shortcut is for real symmetric operators (RSRS_F64)");
   if (p < 1 || ld < p || (ld & 1)) return fail(RSRS_ERR_INVALID, "rsrs_factor: need 1 <= p <= ld and ld even");
   if (dt != RSRS_F64 && dt != RSRS_C128) return fail(RSRS_ERR_INVALID, "rsrs_factor: unknown dtype");
-  o = rsrs_opts{1e-6, 1.0, 1.0, 10, 2, 0, 1, nullptr, nullptr, 0, -1, 0, 0};
+  o = rsrs_opts{1e-6, 1.0, 1.0, 10, 2, 0, 1, nullptr, nullptr, 0, -1, 0, 0, 0};
   if (opts) o = *opts;
   if (!(o.eps > 0) || !(o.level_growth > 0) || !(o.id_scale > 0) || o.oversample < 0 || o.top_level < 1 ||
       o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks)

@@ -50,7 +50,7 @@ class Opts(ctypes.Structure):
                 ("oversample", ctypes.c_int), ("top_level", ctypes.c_int), ("rank", ctypes.c_int),
                 ("nranks", ctypes.c_int), ("nccl_comm", ctypes.c_void_p), ("stream", ctypes.c_void_p),
                 ("profile", ctypes.c_int), ("gather_level", ctypes.c_int), ("symmetric", ctypes.c_int),
-                ("direct_gram", ctypes.c_int)]
+                ("direct_gram", ctypes.c_int), ("push_updates", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):
@@ -305,7 +305,8 @@ def _dtype_code(t) -> int:
 def factor(tree: Tree, Y, Z, Omega, Psi, p: int, eps: float = 1e-6, level_growth: float = 1.0,
            id_scale: float = 1.0, oversample: int = 10, top_level: int = 2, stream=None,
            dtype: int | None = None, profile: bool = False, comm=None, rank: int = 0, nranks: int = 1,
-           gather_level: int = -1, symmetric: bool = False, direct_gram: bool = False) -> Factorization:
+           gather_level: int = -1, symmetric: bool = False, direct_gram: bool = False,
+           push_updates: bool = False) -> Factorization:
     """rsrs_factor on CUDA tensors (N x ld, tree order); Y, Z, Omega, Psi are OVERWRITTEN.
 
     float64 tensors -> RSRS_F64, complex128 -> RSRS_C128 (ld in elements).
@@ -324,7 +325,7 @@ def factor(tree: Tree, Y, Z, Omega, Psi, p: int, eps: float = 1e-6, level_growth
     dtype = code
     o = Opts(eps, level_growth, id_scale, oversample, top_level, int(rank), int(nranks),
              None if comm is None else comm.handle, _stream_ptr(stream), int(profile), int(gather_level),
-             int(symmetric), int(direct_gram))
+             int(symmetric), int(direct_gram), int(push_updates))
     h = _vp()
     _check(_lib.rsrs_factor(tree.handle, dtype, int(p), _ptr(Y), _ptr(Z), _ptr(Omega), _ptr(Psi), int(ld),
                             ctypes.byref(o), ctypes.byref(h)))
@@ -369,7 +370,7 @@ def factor_emulated(tree: Tree, G: int, Y, Z, Omega, Psi, p: int, eps: float = 1
     if symmetric:
         Z, Psi = Y, Omega
     o = Opts(eps, level_growth, id_scale, oversample, top_level, 0, G, None, None, 0, int(gather_level),
-             int(symmetric), 0)
+             int(symmetric), 0, 0)
     hs = (_vp * G)()
     _check(_lib.rsrs_factor_emulated(tree.handle, code, int(p), int(G), _ptr(Y), _ptr(Z), _ptr(Omega), _ptr(Psi),
                                      int(ld), ctypes.byref(o), hs))

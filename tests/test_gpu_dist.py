@@ -51,8 +51,8 @@ def _apply_emul(fs, v):
 
 
 def _single(cfg, X, Y, Z, Om, Ps):
-    # the ranks compute each near-field Gram directly; so does this single-GPU reference
-    t, f = run_gpu(cfg, X, Y, Z, Om, Ps, cfg.root(), direct_gram=True)
+    # the ranks compute each near-field Gram directly and push the L/U updates; so does this reference
+    t, f = run_gpu(cfg, X, Y, Z, Om, Ps, cfg.root(), direct_gram=True, push_updates=True)
     return t, f
 
 

@@ -97,7 +97,7 @@ def test_symmetric_shortcut_emulated_ranks_bit_exact():
     import paper_2311_01451_b200 as R
     cfg = W.CONFIGS["c1"]
     X, A, Y, Om, b = _sym_problem(cfg)
-    t, f = _gpu_sym(cfg, X, Y, Om, direct_gram=True)
+    t, f = _gpu_sym(cfg, X, Y, Om, direct_gram=True, push_updates=True)
     _, fs = _gpu_sym(cfg, X, Y, Om, emulate=3)
     x1 = torch.from_numpy(b.copy()).cuda()
     f.solve(x1)
