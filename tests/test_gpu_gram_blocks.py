@@ -48,3 +48,19 @@ def test_gram_blocks_match_direct(name, cfg, X):
     assert np.linalg.norm(xb - x_or) / np.linalg.norm(x_or) <= 10 * cfg.eps
     # fewer algorithmic Gram flops than the per-box Grams
     assert fb.stats()["flops_model"] < fd.stats()["flops_model"]
+
+
+@pytest.mark.parametrize("name,cfg,X", CASES, ids=[c[0] for c in CASES])
+def test_pulled_updates_match_pushed(name, cfg, X):
+    """Pulled L/U updates (default on one GPU) vs pushing every update when its box is
+    eliminated (opts.push_updates, the multi-GPU ranks' scheme): same sums regrouped."""
+    X, A, Y, Z, Om, Ps, b = dense_problem(cfg, X)
+    t1, fp = run_gpu(cfg, X, Y, Z, Om, Ps, cfg.root())
+    t2, fq = run_gpu(cfg, X, Y, Z, Om, Ps, cfg.root(), push_updates=True)
+    for lev in range(t1.L, 1, -1):
+        nb = len(t1.level(lev)["keys"])
+        assert np.array_equal(fp.ranks(lev, nb), fq.ranks(lev, nb)), lev
+    xp = gpu_solve(fp, b)
+    xq = gpu_solve(fq, b)
+    assert np.linalg.norm(xp - xq) / np.linalg.norm(xq) <= 1e-10
+    assert np.linalg.norm(A @ xp - b) / np.linalg.norm(b) <= 10 * cfg.eps
