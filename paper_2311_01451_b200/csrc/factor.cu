@@ -78,6 +78,7 @@ int g_upd_tm = 0;      // RSRS_UPD_TM=32|64: row tile of the L/U sample-update G
 // host-side time split of one rsrs_factor (RSRS_TRACE)
 struct HostTrace {
   double alloc = 0, sync = 0;
+  double ph[6] = {0, 0, 0, 0, 0, 0};   // level setup, Gram-block setup, descriptors, batch launches, level end, merge
   int nalloc = 0, nsync = 0;
   size_t alloc_bytes = 0;
 };
@@ -584,6 +585,12 @@ struct Planner {
     for (int i = 0; i < T.d; ++i) ncol *= 3;
 
     for (int lev = L; lev >= top && lev >= 1; --lev) {
+      double tph = now_s();
+      auto phase = [&](int i) {
+        const double t = now_s();
+        g_ht.ph[i] += t - tph;
+        tph = t;
+      };
       const rsrs::TreeLevel& lv = T.levels[lev];
       const int nbox = (int)lv.nboxes;
       const double atol = cid * eps * std::pow(g, (double)(L - lev));
@@ -741,6 +748,7 @@ struct Planner {
       }
 
       // ---- descriptors (sizes that depend on the near set point at BoxDev::r / nr / nc / k)
+      phase(0);
       // level-wide Gram blocks (gram.cuh): single rank, boxes small enough for the kernels' tables
       bool use_blocks = gram_blocks && R == 1;
       int max_nnbr = 1;
@@ -755,25 +763,14 @@ struct Planner {
       i64 gpool_side = 0;
       const int sides = sym ? 1 : 2;
       if (use_blocks) {
-        // partners of box i: every box that shares a near field with it (neighbours of its
-        // nonempty neighbours), ascending; flat CSR built with a stamp array
-        std::vector<int> gpstart(nbox + 1, 0), plist, stamp(nbox, -1);
-        plist.reserve((size_t)nbox * 16);
+        // partners of box i: boxes that share a near field with it (tree planner, tree.cpp),
+        // restricted to boxes with active rows on this level
+        std::vector<int> gpstart(nbox + 1, 0), plist;
+        plist.reserve(lv.part.size());
         for (int i = 0; i < nbox; ++i) {
-          const size_t at = plist.size();
           if (nb_all[i] > 0)
-            for (int q = lv.nbr_off[i]; q < lv.nbr_off[i + 1]; ++q) {
-              const int m = lv.nbr[q];
-              if (nb_all[m] <= 0) continue;
-              for (int q2 = lv.nbr_off[m]; q2 < lv.nbr_off[m + 1]; ++q2) {
-                const int j = lv.nbr[q2];
-                if (nb_all[j] > 0 && stamp[j] != i) {
-                  stamp[j] = i;
-                  plist.push_back(j);
-                }
-              }
-            }
-          std::sort(plist.begin() + at, plist.end());
+            for (int32_t q = lv.part_off[i]; q < lv.part_off[i + 1]; ++q)
+              if (nb_all[lv.part[q]] > 0) plist.push_back(lv.part[q]);
           gpstart[i + 1] = (int)plist.size();
         }
         // row-block storage: box i keeps [G(i, j) for partners j >= i] side by side
@@ -883,6 +880,7 @@ struct Planner {
         }
         stream_sync(s);   // pre_b is released at scope end
       }
+      phase(1);
       // ---- descriptors, built on the device from the box records (descs.cuh)
       const int nsd = sym ? 1 : 2;
       const size_t nbx = hb.size();
@@ -933,6 +931,7 @@ struct Planner {
       std::vector<int> k_all(nbox, -1);
       double* const store4[4] = {Y, Z, Om, Ps};
 
+      phase(2);
       // ---- colour batches --------------------------------------------------
       for (const BInfo& bi : binfo) {
         const int n = bi.count, q0 = bi.first;
@@ -1138,6 +1137,7 @@ struct Planner {
           }
         }
       }
+      phase(3);
       if (!hb.empty()) CK(cudaMemcpyAsync(hb.data(), dboxes, sizeof(BoxDev) * hb.size(), cudaMemcpyDeviceToHost, s));
       stream_sync(s);
       flush_prof();
@@ -1187,6 +1187,7 @@ struct Planner {
         B.dist = R > 1;
         f->batches.push_back(std::move(B));
       }
+      phase(4);
       // ---- merge: skeleton rows into the parent level's store
       const rsrs::TreeLevel& pl = T.levels[lev - 1];
       std::vector<int> pnb(pl.nboxes, 0), coff(nbox, 0);
@@ -1283,6 +1284,7 @@ struct Planner {
       nloc = nnew;
       nb_all = pnb;
       f->stats.nlevels_compressed++;
+      phase(5);
     }
     finish_top(Y, Om, ld, gidx, (int)nloc);
     f->stats.flops_model = flops;
@@ -1442,6 +1444,10 @@ static rsrs_status factor_impl(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, v
       fprintf(stderr, "[rsrs trace] factor (rank %d/%d): host %.1f ms, device %.1f ms, alloc %.1f ms (%d calls, %.2f GB), sync-wait %.1f ms (%d), launches %lld\n",
               f->rank, f->nranks, 1e3 * (now_s() - th0), ms, 1e3 * g_ht.alloc, g_ht.nalloc, g_ht.alloc_bytes / 1e9,
               1e3 * g_ht.sync, g_ht.nsync, (long long)P.launches);
+    if (g_trace)
+      fprintf(stderr, "[rsrs trace]   host phases ms: level setup %.1f, Gram blocks %.1f, descriptors %.1f, batches %.1f, "
+              "level end %.1f, merge %.1f\n", 1e3 * g_ht.ph[0], 1e3 * g_ht.ph[1], 1e3 * g_ht.ph[2], 1e3 * g_ht.ph[3],
+              1e3 * g_ht.ph[4], 1e3 * g_ht.ph[5]);
     f->stats.solve_launches = 2 + 2 * (int64_t)f->batches.size() + (f->nS > 0 ? 1 : 0);
     *out = f;
     return RSRS_OK;

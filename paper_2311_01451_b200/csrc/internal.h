@@ -23,6 +23,8 @@ struct TreeLevel {
   std::vector<int32_t> nbr;        // neighbour lists (self included, ascending)
   std::vector<int32_t> child_off;  // nboxes + 1 (children on level + 1)
   std::vector<int32_t> child;
+  std::vector<int32_t> part_off;   // nboxes + 1: boxes sharing a near field (neighbours of neighbours)
+  std::vector<int32_t> part;       // ascending per box (Gram blocks, gram.cuh)
 };
 
 struct Tree {

@@ -157,6 +157,28 @@ static rsrs_status build(const double* pts, int64_t N, int d, int leaf_max, cons
       }
     }
   }
+  // partners: boxes that meet in some near field (neighbours of a common box)
+  for (int lev = 0; lev <= L; ++lev) {
+    TreeLevel& lv = T.levels[lev];
+    lv.part_off.assign(lv.nboxes + 1, 0);
+    lv.part.clear();
+    std::vector<int32_t> stamp(lv.nboxes, -1);
+    for (int64_t i = 0; i < lv.nboxes; ++i) {
+      const size_t at = lv.part.size();
+      for (int32_t q = lv.nbr_off[i]; q < lv.nbr_off[i + 1]; ++q) {
+        const int32_t m = lv.nbr[q];
+        for (int32_t q2 = lv.nbr_off[m]; q2 < lv.nbr_off[m + 1]; ++q2) {
+          const int32_t j = lv.nbr[q2];
+          if (stamp[j] != (int32_t)i) {
+            stamp[j] = (int32_t)i;
+            lv.part.push_back(j);
+          }
+        }
+      }
+      std::sort(lv.part.begin() + at, lv.part.end());
+      lv.part_off[i + 1] = (int32_t)lv.part.size();
+    }
+  }
   for (int lev = 0; lev <= L; ++lev) {
     TreeLevel& lv = T.levels[lev];
     lv.child_off.assign(lv.nboxes + 1, 0);
