@@ -37,7 +37,7 @@ for (pf, g) in runs:
         torch.cuda.synchronize(); t0 = time.time()
         try:
             prof = os.environ.get("PROF", "last")
-            f = R.factor(t, *work, p=p, eps=cfg.eps, level_growth=g,
+            f = R.factor(t, *work, p=p, eps=cfg.eps, level_growth=g, id_scale=cfg.c_id, oversample=cfg.l,
                          profile=(prof == "all" or (prof == "last" and it == ITERS - 1)))
         except R.RSRSError as e:
             print(f"p={p} g={g}: {e}", flush=True); break
