@@ -77,10 +77,17 @@ __global__ void __launch_bounds__(256) gblk_update_kernel(const BoxDev* __restri
     }
     __syncthreads();
   }
-  for (int idx = tid; idx < e.nrow * e.ncol; idx += 256) {
-    const int r = idx / e.ncol, c = idx % e.ncol;
-    B[(i64)r * e.ld + c] = Bs[r * GB_LD + c];
-  }
+  // write back only what changed: the box's rows (mode 0, 2) and columns (mode 1, 2)
+  if (e.mode != 1)
+    for (int idx = tid; idx < k * e.ncol; idx += 256) {
+      const int q = idx / e.ncol, c = idx % e.ncol;
+      B[(i64)skl[q] * e.ld + c] = Bs[skl[q] * GB_LD + c];
+    }
+  if (e.mode != 0)
+    for (int idx = tid; idx < e.nrow * k; idx += 256) {
+      const int r = idx / k, q = idx % k;
+      B[(i64)r * e.ld + skl[q]] = Bs[r * GB_LD + skl[q]];
+    }
 }
 
 // C_b[pos(q1) + a, pos(q2) + c] = G(n_q1, n_q2)[act_q1[a], act_q2[c]] for slots q2 <= q1
@@ -96,7 +103,8 @@ __global__ void __launch_bounds__(256) gram_assemble_kernel(const BoxDev* __rest
                                                             double* __restrict__ wsd, int sides) {
   typedef typename ScalarOf<C>::T S;
   __shared__ int pos[64], cnt[64], bx[64], idxs[64];
-  __shared__ int act1[192];
+  __shared__ int act1[192], act2[192];
+  __shared__ S tile[32][33];
   const BoxDev& b = boxes[blockIdx.x];
   const int q1 = blockIdx.y;
   if (q1 >= b.nnbr || b.status != ST_OK) return;
@@ -136,17 +144,35 @@ __global__ void __launch_bounds__(256) gram_assemble_kernel(const BoxDev* __rest
     while (t1[ei].j != box2) ++ei;        // the partner table holds every pair that meets in a near field
     const GBlk e = t1[ei];
     const int i2 = idxs[q2];
-    const int* sk2 = i2 >= 0 ? iws + level_boxes[i2].off_skelrow : nullptr;
-    const int r02 = i2 >= 0 ? level_boxes[i2].row0 : 0;
+    __syncthreads();
+    if (i2 >= 0) {
+      const BoxDev& nb2 = level_boxes[i2];
+      for (int c = tid; c < n2; c += 256) act2[c] = iws[nb2.off_skelrow + c] - nb2.row0;
+    } else {
+      for (int c = tid; c < n2; c += 256) act2[c] = c;
+    }
+    __syncthreads();
     for (int side = 0; side < sides; ++side) {
       const S* B = reinterpret_cast<const S*>(side ? poolP : poolO) + e.off;
       S* Cb = reinterpret_cast<S*>(wsd) + b.off_aug + (side ? (i64)(b.rmax + b.nb) * ldr : 0);
-      for (int idx = tid; idx < n1 * n2; idx += 256) {
-        const int a = idx / n2, c = idx % n2;
-        const int ra = act1[a];
-        const int rc = sk2 ? sk2[c] - r02 : c;
-        const S v = (e.mode == 1) ? s_conj(B[(i64)rc * e.ld + ra]) : B[(i64)ra * e.ld + rc];
-        Cb[(i64)(pos[q1] + a) * ldr + pos[q2] + c] = v;
+      if (e.mode != 1) {
+        for (int idx = tid; idx < n1 * n2; idx += 256) {
+          const int a = idx / n2, c = idx % n2;
+          Cb[(i64)(pos[q1] + a) * ldr + pos[q2] + c] = B[(i64)act1[a] * e.ld + act2[c]];
+        }
+      } else {
+        // stored transposed: 32 x 32 tiles through shared memory (coalesced both ways)
+        const int tx = tid & 31, ty = tid >> 5;
+        for (int a0 = 0; a0 < n1; a0 += 32)
+          for (int c0 = 0; c0 < n2; c0 += 32) {
+            for (int cc = ty; cc < 32; cc += 8)
+              if (c0 + cc < n2 && a0 + tx < n1) tile[cc][tx] = B[(i64)act2[c0 + cc] * e.ld + act1[a0 + tx]];
+            __syncthreads();
+            for (int aa = ty; aa < 32; aa += 8)
+              if (a0 + aa < n1 && c0 + tx < n2)
+                Cb[(i64)(pos[q1] + a0 + aa) * ldr + pos[q2] + c0 + tx] = s_conj(tile[tx][aa]);
+            __syncthreads();
+          }
       }
     }
   }
