@@ -146,6 +146,7 @@ class Factorization:
     near: dict = field(default_factory=dict)      # (level, box) -> r
     atol: dict = field(default_factory=dict)      # level -> atol
     xrr_mismatch: list = field(default_factory=list)
+    coupling: dict = field(default_factory=dict)  # (level, box) -> (est of |A~_{r,f}|_F, est of |A~_{f,r}|_F)
     dtype: object = np.float64
 
     def memory(self) -> int:
@@ -161,9 +162,26 @@ def atol_schedule(eps: float, c_id: float, g: float, L: int, lev: int) -> float:
     return c_id * eps * g ** (L - lev)
 
 
+def coupling_estimate(Y_r, Om_r):
+    """Randomized estimate of |A~(r, f)|_F, f = (1:N) minus r, after box b's elimination.
+
+    PAPER.md:1232-1235 (section 5): "we use randomized sampling techniques (e.g. block
+    nullification) to estimate the extent to which A~_{r,f} and A~_{f,r} deviate from
+    desired compression tolerance, where in this case I_f = (1:N) minus I_r, for every box".
+    With the current samples Y = A~ Omega (master invariant), Y_r null(Omega_r) =
+    A~(r, f) Omega_f null(Omega_r), a Gaussian sketch of A~(r, f) with w = p - |r|
+    columns, so its Frobenius norm / sqrt(w) estimates |A~(r, f)|_F (block nullification,
+    PAPER.md:259-298).  The adjoint side uses Z, Psi for A~(f, r)^*.
+    """
+    nr, p = Y_r.shape
+    if nr == 0:
+        return 0.0
+    return float(np.linalg.norm(Y_r @ null_basis(Om_r)) / math.sqrt(p - nr))
+
+
 def factor(tree: Tree, Y, Z, Om, Psi, eps: float, c_id: float = 1.0, g: float = 1.0,
            l: int = 10, top_level: int = 2, on_step=None, max_boxes: int | None = None,
-           copy: bool = True) -> Factorization:
+           copy: bool = True, estimate_coupling: bool = False) -> Factorization:
     """RSRS factorization from samples in TREE order (N x p each).
 
     The inputs are copied (unless copy=False); `on_step(step, Y, Z, Om, Psi)`
@@ -256,6 +274,8 @@ def factor(tree: Tree, Y, Z, Om, Psi, eps: float, c_id: float = 1.0, g: float = 
             Z[c] -= G_U.conj().T @ Zr
             Om[red] += G_U @ Om[c]
             Psi[red] += G_L.conj().T @ Psi[c]
+            if estimate_coupling:
+                fac.coupling[(lev, b)] = (coupling_estimate(Y[red], Om[red]), coupling_estimate(Z[red], Psi[red]))
             st = Step(level=lev, box=b, skel=skel, red=red, c=c, T=T, G_L=G_L, G_U=G_U,
                       X_rr=X_rr, lu=lu)
             steps.append(st)

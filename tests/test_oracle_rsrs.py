@@ -261,3 +261,53 @@ def test_c1_against_dense_lu():
         sv = np.linalg.svd(np.hstack([At[np.ix_(Ib, far)], At[np.ix_(far, Ib)].T]), compute_uv=False)
         srank = int((sv / math.sqrt(2) > cfg.eps).sum())
         assert srank - 1 <= f.ranks[(t.L, b)] <= srank + 3
+
+
+# ---------------------------------------------------------------------------
+# coupling estimator
+# ---------------------------------------------------------------------------
+def test_coupling_estimate_tracks_explicit_coupling():
+    """The per-box estimate of |A~(r, f)|_F / |A~(f, r)|_F (block nullification of the red
+    rows of the current samples) against the explicitly tracked operator A_g of the
+    master-invariant test: within a factor 3 where the coupling is above the noise floor."""
+    cfg, X, t, A, At, Y, Z, Om, Ps = small_problem()
+    Ag = At.copy()
+    exact = {}
+
+    def on_step(s, Yc, Zc, Omc, Psc):
+        _apply_step_dense(Ag, s)
+        other = np.setdiff1d(np.arange(cfg.N), s.red)
+        exact[(s.level, s.box)] = (np.linalg.norm(Ag[np.ix_(s.red, other)]),
+                                   np.linalg.norm(Ag[np.ix_(other, s.red)]))
+
+    f = O.factor(t, Y, Z, Om, Ps, eps=1e-6, on_step=on_step, estimate_coupling=True)
+    assert set(exact) <= set(f.coupling)
+    checked = 0
+    for key, (ey, ez) in exact.items():
+        gy, gz = f.coupling[key]
+        for e, g in ((ey, gy), (ez, gz)):
+            if e > 1e-9:
+                assert e / 3 <= g <= 3 * e, (key, e, g)
+                checked += 1
+            else:
+                assert g <= 1e-8
+    assert checked > 10
+
+
+def test_coupling_estimate_zero_for_block_diagonal():
+    """Exactly block-diagonal operator: nothing couples the eliminated rows -> estimates ~ 0."""
+    cfg, X, t, A, At, Y, Z, Om, Ps = small_problem()
+    Ab = _masked(At, t, 0)
+    f = O.factor(t, Ab @ Om, Ab.T @ Ps, Om, Ps, eps=1e-6, estimate_coupling=True)
+    assert len(f.coupling) > 0
+    assert max(max(v) for v in f.coupling.values()) <= 1e-12
+
+
+def test_coupling_estimate_decreases_with_tolerance():
+    """Tighter atol -> smaller residual coupling (log kernel, max over boxes per level)."""
+    cfg, X, t, A, At, Y, Z, Om, Ps = small_problem()
+    worst = []
+    for eps in (1e-3, 1e-5, 1e-7):
+        f = O.factor(t, Y, Z, Om, Ps, eps=eps, estimate_coupling=True)
+        worst.append(max(max(v) for k, v in f.coupling.items() if k[0] == t.L))
+    assert worst[0] > worst[1] > worst[2]
