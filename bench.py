@@ -198,13 +198,13 @@ def setup_problem(cfg, dev, rank=0, world=1, pg=None, symmetric=False):
                 gather_level=gather)
 
 
-def factor_solve(pb, work, x, stream, profile=False, solve_events=None):
+def factor_solve(pb, work, x, stream, profile=False, solve_events=None, estimate=False):
     import paper_2311_01451_b200 as R
     cfg = pb["cfg"]
     arrays = (work[0], None, work[1], None) if pb["symmetric"] else tuple(work)
     f = R.factor(pb["tree"], *arrays, p=cfg.p, eps=cfg.eps, level_growth=cfg.g, id_scale=cfg.c_id,
                  oversample=cfg.l, stream=stream, profile=profile, comm=pb["comm"], rank=pb["rank"],
-                 nranks=pb["world"], symmetric=pb["symmetric"])
+                 nranks=pb["world"], symmetric=pb["symmetric"], estimate_coupling=estimate)
     if solve_events is not None:
         solve_events[0].record(stream)
     f.solve(x, stream=stream)
@@ -344,6 +344,24 @@ def run_native(args, rank, world, local, pg):
     xt = x[pb["P"]].contiguous()
     R.sample_matvec(cfg.kernel, pb["pts"], W.kernel_weight(cfg), xt.view(N, 1), ax.view(N, 1), kappa=cfg.kappa)
     resid = float((ax - pb["b"][pb["P"]]).norm() / pb["b"].norm())
+    # ---- coupling estimates, one extra factorization outside the timed region
+    coupling = None
+    if world == 1:
+        with torch.cuda.stream(stream):
+            for w_, s_ in zip(work, pb["src"]):
+                w_.copy_(s_)
+            x.copy_(pb["b"])
+        fe = factor_solve(pb, work, x, stream, estimate=True)
+        coupling = {}
+        tr = pb["tree"]
+        for lev in range(st["L"], st["top_level"] - 1, -1):
+            nbx = len(tr.level(lev)["keys"])
+            e = fe.coupling(lev, nbx)
+            e = e[e[:, 0] >= 0]
+            if e.size:
+                coupling[str(lev)] = {"max": float(e.max()), "median": float(np.median(e)),
+                                      "atol": cfg.c_id * cfg.eps * cfg.g ** (st["L"] - lev)}
+        del fe
     # ---- e2e: host (pinned) inputs, H2D + factor + solve + D2H inside the timed region
     e2e = None
     if not args.no_e2e:
@@ -412,7 +430,7 @@ def run_native(args, rank, world, local, pg):
             "residual": resid, "top_size": st["top_size"], "max_rank": st["max_rank"],
             "memory_scalars": st["memory_scalars"], "sweep_tflops": sweep_tf,
             "roofline": roof, "kernels": breakdown, "fp64_peaks": peaks, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": int(launches), "clocks": clk}
+            "gpu_launches": int(launches), "clocks": clk, "coupling_estimate": coupling}
     print(json.dumps(line), flush=True)
 
 

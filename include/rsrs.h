@@ -73,6 +73,9 @@ typedef struct {
   int push_updates;    /* 1: apply every L/U sample update when its box is eliminated (push, as the
                           multi-GPU ranks do) instead of pulling the updates of a box's rows when the
                           box comes up (single rank) */
+  int estimate_coupling; /* 1: after each box's elimination, estimate |A~(r, f)|_F and |A~(f, r)|_F by
+                          block nullification of its redundant sample rows (PAPER.md:1232-1235,
+                          SURVEY 8(f) f1); read them with rsrs_factor_coupling */
 } rsrs_opts;
 
 /* Statistics of a factorization (Table 1). */
@@ -167,7 +170,7 @@ rsrs_status rsrs_solve(rsrs_factorization f, void* B, int64_t ldb, int64_t nrhs,
 rsrs_status rsrs_apply(rsrs_factorization f, void* X, int64_t ldx, int64_t nrhs, void* s);
 
 /* Kernel classes of the sweep, for rsrs_factor_profile. */
-#define RSRS_NUM_KERNEL_CLASSES 11
+#define RSRS_NUM_KERNEL_CLASSES 12
 
 /* Per-kernel-class record of the last rsrs_factor: class name, summed device
  * time (ms; only when opts.profile == 1, else 0), algorithmic FLOPs and HBM
@@ -182,6 +185,13 @@ rsrs_status rsrs_factor_stats(rsrs_factorization f, rsrs_stats* st);
 /* Per-box ranks of a level (host, int32 per box of that level in Morton order):
  * k = skeleton count, or -1 for an empty box; cap = capacity of k[]. */
 rsrs_status rsrs_factor_ranks(rsrs_factorization f, int level, int32_t* k, int64_t cap);
+
+/* Coupling estimates of a level (opts.estimate_coupling): est[2 b] ~ |A~(r_b, f)|_F,
+ * est[2 b + 1] ~ |A~(f, r_b)|_F after box b's elimination ("estimate the
+ * extent to which A~_{r,f} and A~_{f,r} deviate from desired compression tolerance", f = all
+ * indices but r_b), -1 for boxes with nothing eliminated; cap >= 2 * nboxes.
+ * RSRS_ERR_STATE if the factorization ran without the estimator. */
+rsrs_status rsrs_factor_coupling(rsrs_factorization f, int level, double* est, int64_t cap);
 
 /* Final skeleton set S (tree positions, host int64, ascending) and its size. */
 rsrs_status rsrs_factor_top(rsrs_factorization f, int64_t* S, int64_t cap, int64_t* size);

@@ -95,6 +95,8 @@ struct BoxDev {
   i64 off_nflag;                       // ints: per near position, 1 = row of an unprocessed neighbour
   i64 off_prow;                        // ints: store rows of the pulled Y_r / Z_r (capacity rmax)
   i64 off_pull;                        // scalars: pulled update operands A_Y, A_Z (nb x ldr each)
+  i64 off_est;                         // scalars: coupling estimator, Omega^_r and Psi^_r (nb x nld each)
+  double est_y, est_z;                 // dynamic: estimates of |A~(r, f)|_F and |A~(f, r)|_F
 };
 
 // status codes in BoxDev::status (0 = ok)

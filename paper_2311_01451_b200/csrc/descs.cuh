@@ -173,4 +173,104 @@ __global__ void make_desc_kernel(const DescParams P) {
   }
 }
 
+// Coupling estimator: after the box's elimination,
+//   Omega^_r = Omega_r + G_U Omega_c,  Psi^_r = Psi_r + G_L^* Psi_c   (the U / L^-* updates of
+//   the red rows, skipped by the sweep because eliminated rows are dead)
+//   R_Y = Y_r (I - Omega^_r^dagger Omega^_r) = A~(r, f) Omega^_f null(Omega^_r),  same for Z
+// through the same Gram / Cholesky / projection kernels as the nullification.
+struct EstParams {
+  double *Y, *Z, *Om, *Ps;
+  i64 ld, nld;
+  int p, SC, sym, nbox;
+  double* dws;
+  double* fpool;
+  int* diws;
+  BoxDev* boxes;
+  NNDesc* form;      // [Omega^, Psi^] per box
+  NTDesc* gram;      // [Omega^ Gram, Psi^ Gram, Y_r cross, Z_r cross]
+  CholDesc* chol;    // [Omega side, Psi side]
+  NNDesc* proj;      // [R_Y, R_Z]
+};
+
+__global__ void make_est_desc_kernel(const EstParams P) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= P.nbox) return;
+  BoxDev* dx = P.boxes + q;
+  const BoxDev x = *dx;
+  const int SC = P.SC, p = P.p;
+  const int ns = P.sym ? 1 : 2;
+  const i64 ld = P.ld, nld = P.nld, ldr = x.ldr, ldn = x.ldn;
+  const int nb = x.nb, rm = x.rmax;
+  const int* redrow = P.diws + x.off_redrow;
+  const int* crow = P.diws + x.off_crow;
+  double* est = P.dws + SC * x.off_est;                 // [Omega^_r ; Psi^_r], nb x nld each
+  double* augO = P.dws + SC * x.off_aug;
+  double* augP = augO + SC * (i64)(rm + nb) * ldr;
+  double* yz = P.dws + SC * x.off_yz;                   // [R_Y | R_Z], ld 2 nld
+  for (int side = 0; side < ns; ++side) {
+    double* eh = est + SC * (i64)side * nb * nld;
+    double* aug = side ? augP : augO;
+    NNDesc f{};
+    f.A = side ? P.fpool + SC * x.f_GL : P.fpool + SC * x.f_GU;
+    f.lda = side ? ldn : ldr;
+    f.transA = side;                                    // G_L^* for Psi
+    f.B = side ? P.Ps : P.Om; f.rowB = crow; f.ldb = ld;
+    f.D = eh; f.rowD = nullptr; f.ldd = nld;
+    f.Cin = side ? P.Ps : P.Om; f.rowC = redrow; f.ldc = ld;
+    f.m = nb; f.n = p; f.K = rm; f.alpha = 1.0; f.beta = 1.0; f.pm = &dx->nr; f.pK = &dx->nc;
+    P.form[(i64)q * ns + side] = f;
+    NTDesc a{};
+    a.A = eh; a.rowA = nullptr; a.lda = nld; a.B = eh; a.rowB = nullptr; a.ldb = nld;
+    a.C = aug; a.ldc = ldr; a.m = nb; a.n = nb; a.K = p; a.sym_rows = nb; a.alpha = 1.0;
+    a.pm = &dx->nr; a.pn = &dx->nr; a.psym = &dx->nr;
+    P.gram[(i64)q * 2 * ns + side] = a;
+    NTDesc c{};
+    c.A = side ? P.Z : P.Y; c.rowA = redrow; c.lda = ld; c.B = eh; c.rowB = nullptr; c.ldb = nld;
+    c.C = aug + SC * (i64)rm * ldr; c.ldc = ldr; c.m = nb; c.n = nb; c.K = p; c.sym_rows = 0; c.alpha = 1.0;
+    c.pm = &dx->nr; c.pn = &dx->nr;
+    P.gram[(i64)q * 2 * ns + ns + side] = c;
+    P.chol[(i64)q * ns + side] =
+        CholDesc{aug, ldr, &dx->nr, nb, rm, &dx->status, P.dws + SC * (x.off_linv + side * (i64)((rm + 63) / 64) * 64 * 64)};
+    NNDesc pr{};
+    pr.A = aug + SC * (i64)rm * ldr; pr.lda = ldr; pr.transA = 0;
+    pr.B = eh; pr.rowB = nullptr; pr.ldb = nld;
+    pr.D = yz + SC * (i64)side * nld; pr.rowD = nullptr; pr.ldd = 2 * nld;
+    pr.Cin = side ? P.Z : P.Y; pr.rowC = redrow; pr.ldc = ld;
+    pr.m = nb; pr.n = p; pr.K = nb; pr.alpha = -1.0; pr.beta = 1.0; pr.pm = &dx->nr; pr.pK = &dx->nr;
+    P.proj[(i64)q * ns + side] = pr;
+  }
+}
+
+// est = |R|_F / sqrt(p - n_r) per side (one CTA per box)
+template <bool C>
+__global__ void __launch_bounds__(256) est_norm_kernel(BoxDev* __restrict__ boxes, const double* __restrict__ wsd,
+                                                       i64 nld, int p, int sides) {
+  typedef typename ScalarOf<C>::T S;
+  BoxDev& b = boxes[blockIdx.x];
+  const int nr = b.nr;
+  __shared__ double red[2][256];
+  const S* R = reinterpret_cast<const S*>(wsd) + b.off_yz;
+  for (int side = 0; side < sides; ++side) {
+    double acc = 0.0;
+    if (b.status == ST_OK)
+      for (int idx = threadIdx.x; idx < nr * p; idx += 256) {
+        const S v = R[(i64)(idx / p) * 2 * nld + (i64)side * nld + idx % p];
+        const double a = s_abs(v);
+        acc += a * a;
+      }
+    red[side][threadIdx.x] = acc;
+  }
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o)
+      for (int side = 0; side < sides; ++side) red[side][threadIdx.x] += red[side][threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double w = (double)(p - nr);
+    b.est_y = (nr > 0 && w > 0) ? sqrt(red[0][0] / w) : 0.0;
+    b.est_z = sides > 1 ? ((nr > 0 && w > 0) ? sqrt(red[1][0] / w) : 0.0) : b.est_y;
+  }
+}
+
 }  // namespace rsrs

@@ -330,6 +330,7 @@ struct rsrs_factor_s {
   std::vector<Batch> batches;
   std::vector<std::unique_ptr<DBuf>> keep;        // factor-lifetime device buffers
   std::vector<std::vector<int32_t>> ranks;        // [level][box] (-1 empty)
+  std::vector<std::vector<double>> coupling;      // [level][2 box + side] coupling estimates (-1: none)
   int nS = 0;
   int ldS = 0;
   int* d_S = nullptr;                             // tree positions of S
@@ -361,11 +362,12 @@ enum KC {
   KC_EXTRACT,    // extract_lu_kernel
   KC_G,          // gemm_nn: G_U, G_L
   KC_UPD,        // gemm_nn: L/U updates
-  KC_MISC        // compaction + top block
+  KC_MISC,       // compaction + top block
+  KC_EST         // coupling estimator (opts.estimate_coupling)
 };
 static const char* KC_NAMES[RSRS_NUM_KERNEL_CLASSES] = {
     "gemm_nt_gram", "chol_aug", "trsm_back", "gemm_nn_proj", "gemm_nt_idgram", "id",
-    "gemm_nn_ef",   "extract_lu", "gemm_nn_g", "gemm_nn_lu_update", "compact_top"};
+    "gemm_nn_ef",   "extract_lu", "gemm_nn_g", "gemm_nn_lu_update", "compact_top", "coupling_est"};
 
 namespace {
 
@@ -383,6 +385,7 @@ struct Planner {
   bool gram_blocks = true;   // level-wide near-field Gram blocks (gram.cuh; single rank)
   bool level_blocks = false; // the current level uses them (account_box counts the cross products only)
   bool push_updates = false; // push every L/U update (as the multi-GPU ranks do) instead of pulling
+  bool estimate = false;     // per-box coupling estimator
   int SC = 1;          // doubles per scalar (1 real, 2 complex); all offsets below are in scalars
   std::vector<cudaEvent_t> evpool;
   struct Pend {
@@ -579,8 +582,13 @@ struct Planner {
       stream_sync(s);
     }
     int* gidx = leaf_gidx.as<int>();
-    DBuf ws, iws, nbrbuf, descbuf, dstbuf, rl_send, rl_recv;
+    DBuf ws, iws, nbrbuf, descbuf, dstbuf, rl_send, rl_recv, estdesc;
+    const NNDesc* Eform = nullptr;
+    const NTDesc* Egram = nullptr;
+    const CholDesc* Echol = nullptr;
+    const NNDesc* Eproj = nullptr;
     f->ranks.assign(L + 1, std::vector<int32_t>());
+    f->coupling.assign(L + 1, std::vector<double>());
     int ncol = 1;
     for (int i = 0; i < T.d; ++i) ncol *= 3;
 
@@ -672,6 +680,7 @@ struct Planner {
           x.off_xcr = wo;   wo += r * ldn;
           x.off_linv = wo;  wo += 2 * ((r + 63) / 64) * 64 * 64;
           x.off_pull = wo;  wo += 2 * nb * ldr;
+          x.off_est = wo;   if (estimate) wo += 2 * nb * nld;
           x.off_rows = ioff;    ioff += r + nb;
           x.off_skelrow = ioff; ioff += nb;
           x.off_redrow = ioff;  ioff += nb;
@@ -926,6 +935,30 @@ struct Planner {
       const NNDesc* Dupd = reinterpret_cast<const NNDesc*>(dd + o_upd);
       const CholDesc* Dchol = reinterpret_cast<const CholDesc*>(dd + o_chol);
       const NNDesc* Dpull = reinterpret_cast<const NNDesc*>(dd + o_pull);
+      // coupling-estimator descriptors
+      if (estimate) {
+        const size_t o_ef = 0, o_eg = (sizeof(NNDesc) * nbx * nsd + 15) & ~size_t(15);
+        const size_t o_ec = o_eg + ((sizeof(NTDesc) * nbx * 2 * nsd + 15) & ~size_t(15));
+        const size_t o_ep = o_ec + ((sizeof(CholDesc) * nbx * nsd + 15) & ~size_t(15));
+        const size_t esz = o_ep + sizeof(NNDesc) * nbx * nsd + 16;
+        estdesc.ensure(esz, s);
+        char* ed = estdesc.as<char>();
+        if (nbx) {
+          rsrs::EstParams ep{};
+          ep.Y = Y; ep.Z = Z; ep.Om = Om; ep.Ps = Ps; ep.ld = ld; ep.nld = nld; ep.p = p; ep.SC = SC; ep.sym = sym;
+          ep.nbox = (int)nbx; ep.dws = dws; ep.fpool = fpool; ep.diws = diws; ep.boxes = dboxes;
+          ep.form = reinterpret_cast<NNDesc*>(ed + o_ef);
+          ep.gram = reinterpret_cast<NTDesc*>(ed + o_eg);
+          ep.chol = reinterpret_cast<CholDesc*>(ed + o_ec);
+          ep.proj = reinterpret_cast<NNDesc*>(ed + o_ep);
+          rsrs::make_est_desc_kernel<<<(unsigned)((nbx + 127) / 128), 128, 0, s>>>(ep);
+          post("make_est_desc_kernel", s, launches);
+        }
+        Eform = reinterpret_cast<const NNDesc*>(ed + o_ef);
+        Egram = reinterpret_cast<const NTDesc*>(ed + o_eg);
+        Echol = reinterpret_cast<const CholDesc*>(ed + o_ec);
+        Eproj = reinterpret_cast<const NNDesc*>(ed + o_ep);
+      }
 
       // global skeleton counts of the level (-1 = not processed yet)
       std::vector<int> k_all(nbox, -1);
@@ -1089,6 +1122,18 @@ struct Planner {
           tic(KC_UPD);
           launch_nn(cplx, Dupd + ns * q0, ns * n, bi.max_r, p, s, launches, g_upd_tm);
           toc();
+          if (estimate) {        // coupling estimator of the boxes just eliminated
+            tic(KC_EST);
+            launch_nn(cplx, Eform + ns * q0, ns * n, bi.max_nb, p, s, launches);
+            launch_nt(cplx, Egram + 2 * ns * q0, 2 * ns * n, bi.max_nb, bi.max_nb, s, launches);
+            launch_chol_any(cplx, Echol + ns * q0, ns * n, bi.max_nb, bi.max_nb, s, launches);
+            launch_back_any(cplx, Echol + ns * q0, ns * n, bi.max_nb, bi.max_nb, s, launches);
+            launch_nn(cplx, Eproj + ns * q0, ns * n, bi.max_nb, p, s, launches);
+            if (cplx) rsrs::est_norm_kernel<true><<<n, 256, 0, s>>>(dbx, dws, nld, p, ns);
+            else rsrs::est_norm_kernel<false><<<n, 256, 0, s>>>(dbx, dws, nld, p, ns);
+            post("est_norm_kernel", s, launches);
+            toc();
+          }
         }
         if (dist) {
           // return the updated Y/Z halo rows to their owners (each row has one writer per colour)
@@ -1172,6 +1217,14 @@ struct Planner {
       for (int b = 0; b < nbox; ++b) {
         if (nb_all[b] <= 0) k_all[b] = 0;
         f->ranks[lev][b] = nb_all[b] > 0 ? k_all[b] : -1;
+      }
+      if (estimate) {
+        f->coupling[lev].assign(2 * (size_t)nbox, -1.0);
+        for (const BoxDev& x : hb)
+          if (x.nr > 0) {
+            f->coupling[lev][2 * x.box] = x.est_y;
+            f->coupling[lev][2 * x.box + 1] = x.est_z;
+          }
       }
       for (const BInfo& bi : binfo) {
         Batch B;
@@ -1430,6 +1483,7 @@ static rsrs_status factor_impl(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, v
     P.sym = o.symmetric != 0;
     P.gram_blocks = o.direct_gram == 0;
     P.push_updates = o.push_updates != 0;
+    P.estimate = o.estimate_coupling != 0;
     P.comm = (comm && comm->nranks > 1) ? comm : nullptr;
     P.part = rsrs::make_partition(T, comm ? comm->nranks : 1, o.gather_level, o.top_level);
     P.run((double*)Y, (double*)Z, (double*)Omega, (double*)Psi, ld);
@@ -1476,7 +1530,7 @@ static rsrs_status check_args(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, vo
     return fail(RSRS_ERR_INVALID, "rsrs_factor: the symmetric shortcut is for real symmetric operators (RSRS_F64)");
   if (p < 1 || ld < p || (ld & 1)) return fail(RSRS_ERR_INVALID, "rsrs_factor: need 1 <= p <= ld and ld even");
   if (dt != RSRS_F64 && dt != RSRS_C128) return fail(RSRS_ERR_INVALID, "rsrs_factor: unknown dtype");
-  o = rsrs_opts{1e-6, 1.0, 1.0, 10, 2, 0, 1, nullptr, nullptr, 0, -1, 0, 0, 0};
+  o = rsrs_opts{1e-6, 1.0, 1.0, 10, 2, 0, 1, nullptr, nullptr, 0, -1, 0, 0, 0, 0};
   if (opts) o = *opts;
   if (!(o.eps > 0) || !(o.level_growth > 0) || !(o.id_scale > 0) || o.oversample < 0 || o.top_level < 1 ||
       o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks)
@@ -1747,6 +1801,15 @@ rsrs_status rsrs_factor_ranks(rsrs_factorization f, int level, int32_t* k, int64
   if ((int64_t)v.size() > cap) return fail(RSRS_ERR_INVALID, "rsrs_factor_ranks: capacity too small");
   for (size_t i = 0; i < v.size(); ++i) k[i] = v[i];
   for (int64_t i = (int64_t)v.size(); i < cap; ++i) k[i] = -1;
+  return RSRS_OK;
+}
+
+rsrs_status rsrs_factor_coupling(rsrs_factorization f, int level, double* est, int64_t cap) {
+  if (!f || !est || level < 0 || level > f->L) return fail(RSRS_ERR_INVALID, "rsrs_factor_coupling: invalid argument");
+  const auto& v = f->coupling[level];
+  if (v.empty()) return fail(RSRS_ERR_STATE, "rsrs_factor_coupling: factor without opts.estimate_coupling");
+  if ((int64_t)v.size() > cap) return fail(RSRS_ERR_INVALID, "rsrs_factor_coupling: capacity too small");
+  for (size_t i = 0; i < v.size(); ++i) est[i] = v[i];
   return RSRS_OK;
 }
 

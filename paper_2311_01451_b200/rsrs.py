@@ -35,7 +35,7 @@ EXPORTS = [
     "rsrs_last_error", "rsrs_version", "rsrs_memory_info", "rsrs_release_memory",
     "rsrs_tree_partition", "rsrs_dist_owner", "rsrs_dist_halo_plan", "rsrs_dist_move_plan",
     "rsrs_comm_unique_id", "rsrs_comm_init", "rsrs_comm_destroy", "rsrs_comm_selftest",
-    "rsrs_factor_emulated", "rsrs_solve_emulated", "rsrs_apply_emulated",
+    "rsrs_factor_emulated", "rsrs_solve_emulated", "rsrs_apply_emulated", "rsrs_factor_coupling",
 ]
 
 
@@ -50,7 +50,8 @@ class Opts(ctypes.Structure):
                 ("oversample", ctypes.c_int), ("top_level", ctypes.c_int), ("rank", ctypes.c_int),
                 ("nranks", ctypes.c_int), ("nccl_comm", ctypes.c_void_p), ("stream", ctypes.c_void_p),
                 ("profile", ctypes.c_int), ("gather_level", ctypes.c_int), ("symmetric", ctypes.c_int),
-                ("direct_gram", ctypes.c_int), ("push_updates", ctypes.c_int)]
+                ("direct_gram", ctypes.c_int), ("push_updates", ctypes.c_int),
+                ("estimate_coupling", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):
@@ -81,10 +82,12 @@ _lib.rsrs_apply.argtypes = [_vp, _vp, _i64, _i64, _vp]
 _lib.rsrs_factor_stats.argtypes = [_vp, ctypes.POINTER(Stats)]
 _lib.rsrs_factor_ranks.argtypes = [_vp, _i32, _vp, _i64]
 _lib.rsrs_factor_top.argtypes = [_vp, _vp, _i64, ctypes.POINTER(_i64)]
+_lib.rsrs_factor_coupling.argtypes = [_vp, _i32, _vp, _i64]
+_lib.rsrs_factor_coupling.restype = ctypes.c_int
 _lib.rsrs_factor_profile.argtypes = [_vp, _i32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(_d),
                                      ctypes.POINTER(_d), ctypes.POINTER(_d), ctypes.POINTER(_i64)]
 _lib.rsrs_factor_profile.restype = ctypes.c_int
-NUM_KERNEL_CLASSES = 11
+NUM_KERNEL_CLASSES = 12
 _lib.rsrs_tree_partition.argtypes = [_vp, _i32, _i32, _i32, _vp, ctypes.POINTER(_i32)]
 _lib.rsrs_dist_owner.argtypes = [_vp, _i32, _i32, _i32, _i32, _vp]
 _lib.rsrs_dist_halo_plan.argtypes = [_vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _i32, _vp, _i64,
@@ -265,6 +268,12 @@ class Factorization:
         _check(_lib.rsrs_factor_ranks(self._h, level, out.ctypes.data, out.shape[0]))
         return out[:nboxes]
 
+    def coupling(self, level: int, nboxes: int) -> np.ndarray:
+        """(nboxes, 2) estimates of |A~(r_b, f)|_F, |A~(f, r_b)|_F (opts.estimate_coupling); -1: none."""
+        out = np.empty(2 * max(nboxes, 1), np.float64)
+        _check(_lib.rsrs_factor_coupling(self._h, level, out.ctypes.data, out.shape[0]))
+        return out[:2 * nboxes].reshape(nboxes, 2)
+
     def top(self) -> np.ndarray:
         n = _i64()
         _check(_lib.rsrs_factor_top(self._h, None, 0, ctypes.byref(n)))
@@ -306,7 +315,7 @@ def factor(tree: Tree, Y, Z, Omega, Psi, p: int, eps: float = 1e-6, level_growth
            id_scale: float = 1.0, oversample: int = 10, top_level: int = 2, stream=None,
            dtype: int | None = None, profile: bool = False, comm=None, rank: int = 0, nranks: int = 1,
            gather_level: int = -1, symmetric: bool = False, direct_gram: bool = False,
-           push_updates: bool = False) -> Factorization:
+           push_updates: bool = False, estimate_coupling: bool = False) -> Factorization:
     """rsrs_factor on CUDA tensors (N x ld, tree order); Y, Z, Omega, Psi are OVERWRITTEN.
 
     float64 tensors -> RSRS_F64, complex128 -> RSRS_C128 (ld in elements).
@@ -325,7 +334,7 @@ def factor(tree: Tree, Y, Z, Omega, Psi, p: int, eps: float = 1e-6, level_growth
     dtype = code
     o = Opts(eps, level_growth, id_scale, oversample, top_level, int(rank), int(nranks),
              None if comm is None else comm.handle, _stream_ptr(stream), int(profile), int(gather_level),
-             int(symmetric), int(direct_gram), int(push_updates))
+             int(symmetric), int(direct_gram), int(push_updates), int(estimate_coupling))
     h = _vp()
     _check(_lib.rsrs_factor(tree.handle, dtype, int(p), _ptr(Y), _ptr(Z), _ptr(Omega), _ptr(Psi), int(ld),
                             ctypes.byref(o), ctypes.byref(h)))
@@ -370,7 +379,7 @@ def factor_emulated(tree: Tree, G: int, Y, Z, Omega, Psi, p: int, eps: float = 1
     if symmetric:
         Z, Psi = Y, Omega
     o = Opts(eps, level_growth, id_scale, oversample, top_level, 0, G, None, None, 0, int(gather_level),
-             int(symmetric), 0, 0)
+             int(symmetric), 0, 0, 0)
     hs = (_vp * G)()
     _check(_lib.rsrs_factor_emulated(tree.handle, code, int(p), int(G), _ptr(Y), _ptr(Z), _ptr(Omega), _ptr(Psi),
                                      int(ld), ctypes.byref(o), hs))

@@ -1,0 +1,55 @@
+"""Coupling estimator on the GPU against the
+oracle's (tests/test_oracle_rsrs.py pins the oracle's estimator to the explicitly
+tracked operator)."""
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as W
+from gpu_common import dense_problem, run_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+CASES = [("c1", W.CONFIGS["c1"]), ("sphere8k", W.CONFIGS["c3"].scaled(8192)), ("c4_64", W.CONFIGS["c4"].scaled(64))]
+
+
+@pytest.mark.parametrize("name,cfg", CASES, ids=[c[0] for c in CASES])
+def test_coupling_estimate_matches_oracle(name, cfg):
+    X, A, Y, Z, Om, Ps, b = dense_problem(cfg)
+    t, f = run_gpu(cfg, X, Y, Z, Om, Ps, cfg.root(), estimate_coupling=True)
+    to = O.build_tree(X, cfg.leaf, *cfg.root())
+    P = to.perm
+    fo = O.factor(to, Y[P], Z[P], Om[P], Ps[P], cfg.eps, c_id=cfg.c_id, g=cfg.g, l=cfg.l, estimate_coupling=True)
+    L = to.L
+    lv = to.levels[L]
+    est = f.coupling(L, lv.nboxes)
+    checked = 0
+    for bx in range(lv.nboxes):
+        if lv.colour[bx] != 0 or (L, bx) not in fo.coupling:
+            continue
+        # colour-0 leaf boxes depend only on the initial samples: tight agreement
+        for side in range(2):
+            o = fo.coupling[(L, bx)][side]
+            g = est[bx, side]
+            assert abs(g - o) <= 1e-2 * o + 1e-12, (bx, side, g, o)
+            checked += 1
+    assert checked > 0
+    for lev in range(L, 1, -1):
+        nb = len(to.levels[lev].keys)
+        e = f.coupling(lev, nb)
+        og = max((max(v) for k, v in fo.coupling.items() if k[0] == lev), default=0.0)
+        gg = e.max()
+        assert (og <= 1e-12 and gg <= 1e-10) or og / 2 <= gg <= 2 * og, (lev, gg, og)
+    # the estimator does not change the factorization
+    t2, f2 = run_gpu(cfg, X, Y, Z, Om, Ps, cfg.root())
+    for lev in range(L, 1, -1):
+        nb = len(to.levels[lev].keys)
+        assert np.array_equal(f.ranks(lev, nb), f2.ranks(lev, nb))
