@@ -628,7 +628,9 @@ __global__ void build_near_kernel(BoxDev* __restrict__ boxes, const BoxDev* __re
     } else {
       const bool self = (r0 == b.row0);
       if (self) selfp = o;
-      const int fl = (self || idx == -2) ? 0 : 1;   // 1: rows of a not-yet-eliminated neighbour
+      // 1: rows of a not-yet-eliminated neighbour on this rank (pulled later); own rows and
+      // halo blocks (-2, -3: foreign, pushed and returned) are 0
+      const int fl = (self || idx <= -2) ? 0 : 1;
       for (int t = lane; t < cnt; t += 32) {
         near[o + t] = r0 + t;
         nflag[o + t] = fl;

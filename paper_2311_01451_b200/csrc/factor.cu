@@ -906,7 +906,9 @@ struct Planner {
       const size_t o_g = slot(sizeof(NNDesc) * nbx * 2);
       const size_t o_upd = slot(sizeof(NNDesc) * nbx * nsd);
       const size_t o_chol = slot(sizeof(CholDesc) * nbx * nsd);
-      const bool pull = R == 1 && !push_updates;
+      // pulled L/U updates: a rank pulls from its own eliminated neighbours; foreign rows
+      // (halo) are always pushed and returned with the halo
+      const bool pull = !push_updates;
       const size_t o_pull = slot(sizeof(NNDesc) * nbx * nsd);
       descbuf.ensure(dsz + 16, s);
       char* dd = descbuf.as<char>();
@@ -993,8 +995,9 @@ struct Planner {
           for (int qb = q0; qb < q0 + n; ++qb)
             for (int t = fs_first[qb]; t < fs_first[qb + 1]; ++t) {
               const int rec = foreign_slot[t].first, j = foreign_slot[t].second;
-              // -2: halo block of a foreign box eliminated in an earlier colour (its skeletons)
-              hnbr[rec] = (nb_all[j] > 0 && lv.colour[j] < bi.colour) ? -2 : -1;
+              // halo block of a foreign box: -2 eliminated in an earlier colour (its skeletons),
+              // -3 not yet eliminated (its L/U updates are pushed and returned to the owner)
+              hnbr[rec] = (nb_all[j] > 0 && lv.colour[j] < bi.colour) ? -2 : -3;
               hnbr[rec + 1] = halo0[j] >= 0 ? halo0[j] : 0;
               hnbr[rec + 2] = halo0[j] >= 0 ? cnt[j] : 0;
             }

@@ -371,7 +371,7 @@ class NcclComm:
 
 def factor_emulated(tree: Tree, G: int, Y, Z, Omega, Psi, p: int, eps: float = 1e-6, level_growth: float = 1.0,
                     id_scale: float = 1.0, oversample: int = 10, top_level: int = 2, gather_level: int = -1,
-                    symmetric: bool = False) -> list:
+                    symmetric: bool = False, push_updates: bool = False) -> list:
     """G-rank run of the multi-GPU sweep emulated on this GPU (one host thread per rank);
     full tree-ordered Y, Z, Omega, Psi (overwritten).  Returns the G rank factorizations."""
     ld = Y.stride(0)
@@ -379,7 +379,7 @@ def factor_emulated(tree: Tree, G: int, Y, Z, Omega, Psi, p: int, eps: float = 1
     if symmetric:
         Z, Psi = Y, Omega
     o = Opts(eps, level_growth, id_scale, oversample, top_level, 0, G, None, None, 0, int(gather_level),
-             int(symmetric), 0, 0, 0)
+             int(symmetric), 0, int(push_updates), 0)
     hs = (_vp * G)()
     _check(_lib.rsrs_factor_emulated(tree.handle, code, int(p), int(G), _ptr(Y), _ptr(Z), _ptr(Omega), _ptr(Psi),
                                      int(ld), ctypes.byref(o), hs))

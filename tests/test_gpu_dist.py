@@ -20,7 +20,7 @@ def _cuda():
         pytest.skip("needs a CUDA device")
 
 
-def _emulated(cfg, X, Y, Z, Om, Ps, G, gather_level=-1):
+def _emulated(cfg, X, Y, Z, Om, Ps, G, gather_level=-1, push_updates=True):
     import torch
 
     import paper_2311_01451_b200 as R
@@ -28,7 +28,7 @@ def _emulated(cfg, X, Y, Z, Om, Ps, G, gather_level=-1):
     perm = t.perm()
     T = [torch.from_numpy(np.ascontiguousarray(M[perm])).to("cuda:0") for M in (Y, Z, Om, Ps)]
     fs = R.factor_emulated(t, G, *T, p=cfg.p, eps=cfg.eps, level_growth=cfg.g, id_scale=cfg.c_id,
-                           oversample=cfg.l, gather_level=gather_level)
+                           oversample=cfg.l, gather_level=gather_level, push_updates=push_updates)
     return t, fs
 
 
@@ -126,3 +126,24 @@ def test_nccl_transport_single_rank():
     c = R.NcclComm(1, 0, lambda raw: raw)
     c.selftest()
     c.destroy()
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_emulated_ranks_default_mode(G):
+    """The ranks' default scheme (pull from own eliminated neighbours, push + return foreign
+    rows) against the single-GPU default (Gram blocks, pull everything): same ranks, same
+    solution to rounding, parity bar."""
+    import torch
+    cfg = W.CONFIGS["c1"]
+    X, A, Y, Z, Om, Ps, b = dense_problem(cfg)
+    t1, f1 = run_gpu(cfg, X, Y, Z, Om, Ps, cfg.root())
+    tg, fs = _emulated(cfg, X, Y, Z, Om, Ps, G, push_updates=False)
+    for lev in range(tg.L, 1, -1):
+        nb = len(tg.level(lev)["keys"])
+        for f in fs:
+            assert np.array_equal(f.ranks(lev, nb), f1.ranks(lev, nb)), lev
+    x1 = torch.from_numpy(b.copy()).to("cuda:0")
+    f1.solve(x1)
+    xg = _solve_emul(fs, b)
+    assert np.linalg.norm(xg - x1.cpu().numpy()) / np.linalg.norm(xg) <= 1e-10
+    assert np.linalg.norm(A @ xg - b) / np.linalg.norm(b) <= 10 * cfg.eps

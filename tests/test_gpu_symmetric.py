@@ -39,7 +39,7 @@ def _gpu_sym(cfg, X, Y, Om, emulate=0, **kw):
     Od = torch.from_numpy(np.ascontiguousarray(Om[perm])).cuda()
     if emulate:
         fs = R.factor_emulated(t, emulate, Yd, None, Od, None, p=cfg.p, eps=cfg.eps, level_growth=cfg.g,
-                               id_scale=cfg.c_id, oversample=cfg.l, symmetric=True)
+                               id_scale=cfg.c_id, oversample=cfg.l, symmetric=True, push_updates=True)
         return t, fs
     f = R.factor(t, Yd, None, Od, None, p=cfg.p, eps=cfg.eps, level_growth=cfg.g, id_scale=cfg.c_id,
                  oversample=cfg.l, symmetric=True, **kw)
