@@ -14,7 +14,8 @@ template <bool C>
 __global__ void __launch_bounds__(256) id_kernel(BoxDev* __restrict__ boxes, const double* __restrict__ wsd,
                                                  int* __restrict__ iws, double* __restrict__ fpoold,
                                                  int* __restrict__ ipool, const int* __restrict__ gidx,
-                                                 double atol2, int p, int oversample, int hsame) {
+                                                 double atol2, int p, int oversample, int hsame,
+                                                 int pullmode) {
   typedef typename ScalarOf<C>::T S;
   extern __shared__ __align__(16) double Hsd[];
   S* Hs = reinterpret_cast<S*>(Hsd);
@@ -189,7 +190,8 @@ __global__ void __launch_bounds__(256) id_kernel(BoxDev* __restrict__ boxes, con
         if (pp < r) {
           row = near[pp];
           const int loc = pp - b.self_pos;
-          keep = !(loc >= 0 && loc < nb && is_red[loc]) && nflag[pp] == grp;
+          // push mode: one group in near order (the order does not depend on rank ownership)
+          keep = !(loc >= 0 && loc < nb && is_red[loc]) && (pullmode ? nflag[pp] : 0) == grp;
         }
         const unsigned mask = __ballot_sync(0xffffffffu, keep);
         if (keep) {

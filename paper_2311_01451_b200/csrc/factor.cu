@@ -1086,8 +1086,8 @@ struct Planner {
           {
             const size_t sm = (size_t)bi.max_nb * (bi.max_nb + 1) * sS + 3 * (size_t)bi.max_nb * 4 + 64;
             tic(KC_ID);
-            if (cplx) rsrs::id_kernel<true><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, ipool, gidx, atol * atol, p, l, sym);
-            else rsrs::id_kernel<false><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, ipool, gidx, atol * atol, p, l, sym);
+            if (cplx) rsrs::id_kernel<true><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, ipool, gidx, atol * atol, p, l, sym, pull);
+            else rsrs::id_kernel<false><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, ipool, gidx, atol * atol, p, l, sym, pull);
             post("id_kernel", s, launches);
             toc();
           }
