@@ -270,7 +270,7 @@ def run_reference(args, rank, world, pg):
     val = dofs * len(timed) / tot
     line = {"metric": METRIC, "value": val, "unit": "DOF/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(timed), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic", "impl": "reference",
+            "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic", "impl": "reference",
             "config": {"workload": cfg.name, "N": cfg.N, "p": cfg.p, "eps": cfg.eps, "sample": desc},
             "cpu_baseline": {"value": val, "unit": "DOF/s", "cores": 1, "kind": "oracle", "sample": desc},
             "e2e": {"value": val, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
