@@ -56,7 +56,6 @@ __global__ void __launch_bounds__(128) chol_update_kernel(const CholDesc* __rest
 // Lt^-1, so L^-1 = D^-1/2 Lt^-1 comes out of the same sweep (no serial
 // triangular inverse).  One barrier per column (column c and row c are
 // broadcast through double-buffered shared memory).
-constexpr int CHOL_DIAG_SMEM = 2 * CB * (CB + 1) * 8;   // dynamic smem reserved (kernel uses static smem)
 
 template <bool C>
 __global__ void __launch_bounds__(256) chol_diag_kernel(const CholDesc* __restrict__ cds, int j0) {

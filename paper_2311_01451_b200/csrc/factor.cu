@@ -73,7 +73,6 @@ constexpr int SMEM_MAX = 227 * 1024 - 1024;  // dynamic-smem budget of the large
 int g_optin = 0;
 bool g_debug = false;  // RSRS_DEBUG_SYNC=1: synchronize and check after every launch
 bool g_trace = false;  // RSRS_TRACE=1: host-side time split of rsrs_factor on stderr
-int g_upd_tm = 0;      // RSRS_UPD_TM=32|64: row tile of the L/U sample-update GEMMs (0: auto)
 
 // host-side time split of one rsrs_factor (RSRS_TRACE)
 struct HostTrace {
@@ -127,9 +126,6 @@ void init_kernels() {
   g_debug = dbg && dbg[0] == '1';
   const char* tr = getenv("RSRS_TRACE");
   g_trace = tr && tr[0] == '1';
-  const char* ut = getenv("RSRS_UPD_TM");
-  g_upd_tm = ut ? atoi(ut) : 0;
-  if (g_upd_tm != 32 && g_upd_tm != 64) g_upd_tm = 0;
   int dev = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&g_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
@@ -318,7 +314,6 @@ struct Batch {
   double* fpool = nullptr;         // the level's factor pools
   int* ipool = nullptr;
   int max_nb = 0, max_r = 0;
-  bool dist = false;               // multi-rank: merge x across ranks after the batch (solve / apply)
 };
 
 struct rsrs_factor_s {
@@ -353,8 +348,8 @@ struct rsrs_factor_s {
 
 enum KC {
   KC_GRAM = 0,   // gemm_nt: near-field Grams and Y_b M^T
-  KC_CHOL,       // chol_aug
-  KC_TRSM,       // trsm_back
+  KC_CHOL,       // blocked Cholesky (chol_update / chol_diag / chol_trsm)
+  KC_TRSM,       // back substitution W = u L^-1 (chol_back_a / chol_back_b)
   KC_PROJ,       // gemm_nn: Y'' = Y_b - W M
   KC_HGRAM,      // gemm_nt: H = S S^T
   KC_ID,         // id_kernel
@@ -366,7 +361,7 @@ enum KC {
   KC_EST         // coupling estimator (opts.estimate_coupling)
 };
 static const char* KC_NAMES[RSRS_NUM_KERNEL_CLASSES] = {
-    "gemm_nt_gram", "chol_aug", "trsm_back", "gemm_nn_proj", "gemm_nt_idgram", "id",
+    "gemm_nt_gram", "cholesky", "back_substitution", "gemm_nn_proj", "gemm_nt_idgram", "id",
     "gemm_nn_ef",   "extract_lu", "gemm_nn_g", "gemm_nn_lu_update", "compact_top", "coupling_est"};
 
 namespace {
@@ -1123,7 +1118,7 @@ struct Planner {
           launch_nn(cplx, Dg + 2 * q0, 2 * n, bi.max_r, bi.max_r, s, launches);
           toc();
           tic(KC_UPD);
-          launch_nn(cplx, Dupd + ns * q0, ns * n, bi.max_r, p, s, launches, g_upd_tm);
+          launch_nn(cplx, Dupd + ns * q0, ns * n, bi.max_r, p, s, launches);
           toc();
           if (estimate) {        // coupling estimator of the boxes just eliminated
             tic(KC_EST);
@@ -1240,7 +1235,6 @@ struct Planner {
         B.ipool = ipool;
         B.max_nb = bi.max_nb;
         B.max_r = bi.max_r;
-        B.dist = R > 1;
         f->batches.push_back(std::move(B));
       }
       phase(4);
