@@ -761,7 +761,8 @@ struct Planner {
         if (nb_all[b] > rsrs::GB_MAX || (lv.nbr_off[b + 1] - lv.nbr_off[b]) > 64) use_blocks = false;
       }
       level_blocks = use_blocks;
-      DBuf gpool_buf, gtab_b, gps_b, growl_b, gwork_b;
+      DBuf gpool_buf, gtab_b, gup_b, growl_b, gwork_b, pre_b;
+      const int* gps_b_ptr = nullptr;
       std::vector<int64_t> gwork_off(binfo.size() + 1, 0);
       DBuf* gpool = &gpool_buf;
       i64 gpool_side = 0;
@@ -778,71 +779,81 @@ struct Planner {
           gpstart[i + 1] = (int)plist.size();
         }
         // row-block storage: box i keeps [G(i, j) for partners j >= i] side by side
-        // (nb_i x sum nb_j, leading dimension even(sum)), so one NT GEMM per box fills it
-        std::vector<i64> roff(nbox, 0), coloff(std::max<size_t>(plist.size(), 1), -1);
+        // (nb_i x sum nb_j, leading dimension even(sum)), so one NT GEMM per box fills it.
+        // The host keeps only per-box sizes; the partner table and the GEMMs' B-row lists
+        // are expanded on the device (gblk_tables_kernel).
+        std::vector<i64> roff(nbox, 0), rowl_at(nbox + 1, 0);
         std::vector<int> rld(nbox, 0);
         i64 poff = 0;
-        int64_t nrowl = 0;
+        int maxnb = 0, maxcols = 0;
         for (int i = 0; i < nbox; ++i) {
           int cols = 0;
           for (int t = gpstart[i]; t < gpstart[i + 1]; ++t)
-            if (plist[t] >= i) {
-              coloff[t] = cols;
-              cols += nb_all[plist[t]];
-            }
+            if (plist[t] >= i) cols += nb_all[plist[t]];
           rld[i] = (int)even(cols);
           roff[i] = poff;
           poff += (i64)nb_all[i] * rld[i];
-          nrowl += cols;
-        }
-        std::vector<rsrs::GBlk> gtab(std::max<size_t>(plist.size(), 1));
-        for (int i = 0; i < nbox; ++i)
-          for (int t = gpstart[i]; t < gpstart[i + 1]; ++t) {
-            const int j = plist[t];
-            rsrs::GBlk e{};
-            e.j = j;
-            if (j >= i) {
-              e.mode = (j == i) ? 2 : 0;
-              e.off = roff[i] + coloff[t];
-              e.ld = rld[i];
-              e.nrow = nb_all[i];
-              e.ncol = nb_all[j];
-            } else {
-              const int tj = (int)(std::lower_bound(plist.begin() + gpstart[j], plist.begin() + gpstart[j + 1], i) -
-                                   plist.begin());
-              e.mode = 1;
-              e.off = roff[j] + coloff[tj];
-              e.ld = rld[j];
-              e.nrow = nb_all[j];
-              e.ncol = nb_all[i];
-            }
-            gtab[t] = e;
+          rowl_at[i + 1] = rowl_at[i] + cols;
+          if (nb_all[i] > 0) {
+            maxnb = std::max(maxnb, nb_all[i]);
+            maxcols = std::max(maxcols, cols);
           }
+        }
+        const int64_t nrowl = rowl_at[nbox];
         gpool_side = poff;
         gpool_buf.alloc((size_t)sS * std::max<i64>(2, sides * poff), s);
         double* poolO = gpool_buf.as<double>();
-        // B-row lists of the per-box GEMMs (store rows of the partners j >= i)
-        std::vector<int> rowl(std::max<int64_t>(nrowl, 1));
-        std::vector<int64_t> rowl_at(nbox, 0);
+        // (box, block) work items of the block update, per colour batch: prefix over my boxes
+        std::vector<int64_t> wpre(hb.size() + 1, 0);
+        for (size_t q = 0; q < hb.size(); ++q) wpre[q + 1] = wpre[q] + gpstart[hb[q].box + 1] - gpstart[hb[q].box];
+        for (size_t bi2 = 0; bi2 < binfo.size(); ++bi2) gwork_off[bi2] = wpre[binfo[bi2].first];
+        gwork_off[binfo.size()] = wpre[hb.size()];
+        // one upload of the per-box arrays: gpstart | plist | nb | row0 | rld  (int), roff | rowl_at | wpre (i64)
+        const size_t ni = (size_t)(nbox + 1) + plist.size() + 3 * (size_t)nbox;
+        const size_t nl = (size_t)nbox + (size_t)(nbox + 1) + hb.size() + 1;
+        std::vector<int64_t> up((ni + 1) / 2 + nl);
         {
-          int64_t o = 0;
-          for (int i = 0; i < nbox; ++i) {
-            rowl_at[i] = o;
-            for (int t = gpstart[i]; t < gpstart[i + 1]; ++t)
-              if (plist[t] >= i)
-                for (int r = 0; r < nb_all[plist[t]]; ++r) rowl[o++] = row0[plist[t]] + r;
-          }
+          int* ip = reinterpret_cast<int*>(up.data());
+          size_t o = 0;
+          std::copy(gpstart.begin(), gpstart.end(), ip + o); o += nbox + 1;
+          std::copy(plist.begin(), plist.end(), ip + o);     o += plist.size();
+          std::copy(nb_all.begin(), nb_all.begin() + nbox, ip + o); o += nbox;
+          std::copy(row0.begin(), row0.begin() + nbox, ip + o);     o += nbox;
+          std::copy(rld.begin(), rld.end(), ip + o);
+          int64_t* lp = up.data() + (ni + 1) / 2;
+          std::copy(roff.begin(), roff.end(), lp);
+          std::copy(rowl_at.begin(), rowl_at.end(), lp + nbox);
+          std::copy(wpre.begin(), wpre.end(), lp + 2 * nbox + 1);
         }
-        growl_b.alloc(sizeof(int) * rowl.size(), s);
-        CK(cudaMemcpyAsync(growl_b.p, rowl.data(), sizeof(int) * rowl.size(), cudaMemcpyHostToDevice, s));
+        gup_b.alloc(sizeof(int64_t) * up.size(), s);
+        CK(cudaMemcpyAsync(gup_b.p, up.data(), sizeof(int64_t) * up.size(), cudaMemcpyHostToDevice, s));
+        const int* d_gps = gup_b.as<int>();
+        const int* d_pl = d_gps + nbox + 1;
+        const int* d_nb = d_pl + plist.size();
+        const int* d_row0 = d_nb + nbox;
+        const int* d_rld = d_row0 + nbox;
+        const i64* d_roff = gup_b.as<i64>() + (ni + 1) / 2;
+        const i64* d_rowlat = d_roff + nbox;
+        const i64* d_wpre = d_rowlat + nbox + 1;
+        growl_b.alloc(sizeof(int) * std::max<int64_t>(nrowl, 1), s);
+        gtab_b.alloc(sizeof(rsrs::GBlk) * std::max<size_t>(plist.size(), 1), s);
+        gwork_b.alloc(sizeof(int2) * std::max<int64_t>(wpre[hb.size()], 1), s);
+        if (nbox > 0) {
+          rsrs::gblk_tables_kernel<<<(nbox + 7) / 8, 256, 0, s>>>(nbox, d_gps, d_pl, d_nb, d_row0, d_roff, d_rld, d_rowlat,
+                                                                  gtab_b.as<rsrs::GBlk>(), growl_b.as<int>());
+          post("gblk_tables", s, launches);
+        }
+        if (!hb.empty()) {
+          rsrs::gblk_work_kernel<<<((int)hb.size() + 7) / 8, 256, 0, s>>>((int)hb.size(), dboxes, d_gps, d_wpre,
+                                                                         gwork_b.as<int2>());
+          post("gblk_work", s, launches);
+        }
+        gps_b_ptr = d_gps;
         std::vector<NTDesc> pre;
         double fl = 0;
-        int maxnb = 0, maxcols = 0;
         for (int i = 0; i < nbox; ++i) {
           if (nb_all[i] <= 0) continue;
-          const int cols = (int)((i + 1 < nbox ? rowl_at[i + 1] : nrowl) - rowl_at[i]);
-          maxnb = std::max(maxnb, nb_all[i]);
-          maxcols = std::max(maxcols, cols);
+          const int cols = (int)(rowl_at[i + 1] - rowl_at[i]);
           for (int side = 0; side < sides; ++side) {
             const double* M = side ? Ps : Om;
             NTDesc d{};
@@ -854,24 +865,6 @@ struct Planner {
             fl += 2.0 * nb_all[i] * cols * p;
           }
         }
-        // per colour batch: (box, block) work items of the block update
-        std::vector<int2> gwork;
-        for (size_t bi2 = 0; bi2 < binfo.size(); ++bi2) {
-          gwork_off[bi2] = (int64_t)gwork.size();
-          for (int q = binfo[bi2].first; q < binfo[bi2].first + binfo[bi2].count; ++q) {
-            const int i = hb[q].box;
-            for (int t = gpstart[i]; t < gpstart[i + 1]; ++t) gwork.push_back(make_int2(q, t));
-          }
-        }
-        gwork_off[binfo.size()] = (int64_t)gwork.size();
-        gwork_b.alloc(sizeof(int2) * std::max<size_t>(gwork.size(), 1), s);
-        if (!gwork.empty())
-          CK(cudaMemcpyAsync(gwork_b.p, gwork.data(), sizeof(int2) * gwork.size(), cudaMemcpyHostToDevice, s));
-        gtab_b.alloc(sizeof(rsrs::GBlk) * gtab.size(), s);
-        gps_b.alloc(sizeof(int) * gpstart.size(), s);
-        CK(cudaMemcpyAsync(gtab_b.p, gtab.data(), sizeof(rsrs::GBlk) * gtab.size(), cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(gps_b.p, gpstart.data(), sizeof(int) * gpstart.size(), cudaMemcpyHostToDevice, s));
-        DBuf pre_b;
         pre_b.alloc(sizeof(NTDesc) * std::max<size_t>(pre.size(), 1), s);
         if (!pre.empty()) {
           CK(cudaMemcpyAsync(pre_b.p, pre.data(), sizeof(NTDesc) * pre.size(), cudaMemcpyHostToDevice, s));
@@ -882,7 +875,6 @@ struct Planner {
           for (int i = 0; i < nbox; ++i) rows += nb_all[i];
           account(KC_GRAM, (cplx ? 4.0 : 1.0) * fl, (double)sS * (sides * rows * p + sides * poff));
         }
-        stream_sync(s);   // pre_b is released at scope end
       }
       phase(1);
       // ---- descriptors, built on the device from the box records (descs.cuh)
@@ -1057,10 +1049,10 @@ struct Planner {
             double* pP = pO + SC * gpool_side;
             if (cplx)
               rsrs::gram_assemble_kernel<true><<<ga, 256, 0, s>>>(dbx, dboxes, diws, dnbr, gtab_b.as<rsrs::GBlk>(),
-                                                                  gps_b.as<int>(), pO, pP, dws, sides);
+                                                                  gps_b_ptr, pO, pP, dws, sides);
             else
               rsrs::gram_assemble_kernel<false><<<ga, 256, 0, s>>>(dbx, dboxes, diws, dnbr, gtab_b.as<rsrs::GBlk>(),
-                                                                   gps_b.as<int>(), pO, pP, dws, sides);
+                                                                   gps_b_ptr, pO, pP, dws, sides);
             post("gram_assemble_kernel", s, launches);
           } else {
             launch_nt(cplx, Dgram + gpb * q0, gpb * n, bi.max_r, bi.max_r, s, launches);

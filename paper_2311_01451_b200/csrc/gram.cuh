@@ -24,6 +24,63 @@ struct GBlk {
   int ld, pad;
 };
 
+// Partner table and B-row lists of the level (one warp per box i; partner lists sorted).
+// Entry t of box i points at G(i, j) inside i's row block (j >= i: mode 0, or 2 on the
+// diagonal) or at G(j, i) inside j's row block (j < i: mode 1, columns offset by the
+// partners of j below i).  rowl[rowl_at[i] + ...] = store rows of i's partners j >= i.
+__global__ void __launch_bounds__(256) gblk_tables_kernel(int nbox, const int* __restrict__ gpstart,
+                                                          const int* __restrict__ plist, const int* __restrict__ nb,
+                                                          const int* __restrict__ row0, const i64* __restrict__ roff,
+                                                          const int* __restrict__ rld,
+                                                          const i64* __restrict__ rowl_at, GBlk* __restrict__ tab,
+                                                          int* __restrict__ rowl) {
+  const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= nbox) return;
+  int col = 0;
+  for (int t = gpstart[i]; t < gpstart[i + 1]; ++t) {
+    const int j = plist[t];
+    GBlk e;
+    e.j = j;
+    e.pad = 0;
+    if (j >= i) {
+      e.mode = j == i ? 2 : 0;
+      e.off = roff[i] + col;
+      e.ld = rld[i];
+      e.nrow = nb[i];
+      e.ncol = nb[j];
+      int* rl = rowl + rowl_at[i] + col;
+      for (int r = lane; r < nb[j]; r += 32) rl[r] = row0[j] + r;
+      col += nb[j];
+    } else {
+      int c = 0;
+      for (int u = gpstart[j]; u < gpstart[j + 1]; ++u) {
+        const int v = plist[u];
+        if (v >= i) break;
+        if (v >= j) c += nb[v];
+      }
+      e.mode = 1;
+      e.off = roff[j] + c;
+      e.ld = rld[j];
+      e.nrow = nb[j];
+      e.ncol = nb[i];
+    }
+    if (lane == 0) tab[t] = e;
+  }
+}
+
+// (box, block) work items of the block update: my box q (level order) -> its partner entries.
+__global__ void __launch_bounds__(256) gblk_work_kernel(int nq, const BoxDev* __restrict__ level_boxes,
+                                                        const int* __restrict__ gpstart,
+                                                        const i64* __restrict__ wpre, int2* __restrict__ work) {
+  const int q = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (q >= nq) return;
+  const int i = level_boxes[q].box;
+  const int t0 = gpstart[i], cnt = gpstart[i + 1] - t0;
+  for (int u = lane; u < cnt; u += 32) work[wpre[q] + u] = make_int2(q, t0 + u);
+}
+
 // After the colour batch's E/F updates: for every (eliminated box, block) work item
 // (grid x; grid y = side), stage the block (<= 64 x 64) and T in shared memory,
 // apply F = [rows s += T^* rows r] to the box's rows and / or F^* to its columns,
