@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(128) chol_update_kernel(const CholDesc* __rest
 // broadcast through double-buffered shared memory).
 
 template <bool C>
-__global__ void __launch_bounds__(256) chol_diag_kernel(const CholDesc* __restrict__ cds, int j0) {
+__global__ void __launch_bounds__(256, 3) chol_diag_kernel(const CholDesc* __restrict__ cds, int j0) {
   constexpr int CBW = cbw<C>();
   typedef typename ScalarOf<C>::T S;
   constexpr int RA = CBW / 16, CA = 2 * CBW / 16;      // owned rows / columns per thread
@@ -102,30 +102,38 @@ __global__ void __launch_bounds__(256) chol_diag_kernel(const CholDesc* __restri
       if (tc == cc)                       // owners of column c (C part)
 #pragma unroll
         for (int ra = 0; ra < RA; ++ra) colbuf[buf][tr + 16 * ra] = a[ra][cblk];
-      if (tr == cc)                       // owners of row c
+      if (tr == cc) {                     // owners of row c publish the multiplier row a[c, :] / piv
+        // (the pivot a[c, c] sits in the same thread row; its owner is (tr, tc) = (cc, cc))
+        const double pv = s_real(a[cblk][cblk]);
+        const double rp = 1.0 / __shfl_sync(0xffffu << (threadIdx.x & 16), pv, cc, 16);
 #pragma unroll
-        for (int cb = 0; cb < CA; ++cb) rowbuf[buf][tc + 16 * cb] = a[cblk][cb];
+        for (int cb = 0; cb < CA; ++cb) rowbuf[buf][tc + 16 * cb] = s_scale(a[cblk][cb], rp);
+      }
       __syncthreads();
       const double piv = s_real(colbuf[buf][c]);
       if (!(piv > 0.0)) {
         bad = true;
         break;
       }
-      const double rs = 1.0 / sqrt(piv), rp = 1.0 / piv;
-      if (tid < jb && tid >= c) A[(i64)tid * cd.lda + c] = s_scale(colbuf[buf][tid], rs);   // L[:, c]
+      if (tid < jb && tid >= c) A[(i64)tid * cd.lda + c] = colbuf[buf][tid];   // unscaled L[:, c] * sqrt(piv)
       if (tid == 0) pivs[c] = piv;
-      // rows i > c: a[i, :] -= (a[i, c] / piv) a[c, :] over ALL owned columns: the I part of
-      // row c is exactly zero right of c, and the C part left of the diagonal (never read
-      // again) just collects rounding residue -- no per-element predicates
+      // rows i > c: a[i, :] -= a[i, c] (a[c, :] / piv)
       S rb[CA];
 #pragma unroll
       for (int cb = 0; cb < CA; ++cb) rb[cb] = rowbuf[buf][tc + 16 * cb];
+      // compile-time skips (cblk is unrolled): owned rows below 16 cblk are finished, C columns
+      // below 16 cblk are never read again, I columns from 16 (cblk + 1) on are zero in row c
 #pragma unroll
       for (int ra = 0; ra < RA; ++ra) {
+        if (ra < cblk) continue;
         const int i = tr + 16 * ra;
-        const S m = (i > c) ? s_scale(colbuf[buf][i], rp) : zero;
+        const S m = (i > c) ? colbuf[buf][i] : zero;
 #pragma unroll
-        for (int cb = 0; cb < CA; ++cb) a[ra][cb] = s_sub(a[ra][cb], s_mul(m, rb[cb]));
+        for (int cb = 0; cb < CA; ++cb) {
+          if (cb < CA / 2 && cb < cblk) continue;
+          if (cb >= CA / 2 && cb - CA / 2 > cblk) continue;
+          a[ra][cb] = s_sub(a[ra][cb], s_mul(m, rb[cb]));
+        }
       }
     }
   }
@@ -134,6 +142,13 @@ __global__ void __launch_bounds__(256) chol_diag_kernel(const CholDesc* __restri
     return;
   }
   __syncthreads();
+  if (tid < jb) pivs[tid] = rsqrt(pivs[tid]);
+  __syncthreads();
+  // L[:, c] = column c at step c / sqrt(piv_c)
+  for (int idx = tid; idx < jb * jb; idx += 256) {
+    const int i = idx / jb, c = idx - i * jb;
+    if (i >= c) A[(i64)i * cd.lda + c] = s_scale(A[(i64)i * cd.lda + c], pivs[c]);
+  }
   // L^-1 = D^-1/2 Lt^-1 (zero padded beyond jb)
   S* linv = reinterpret_cast<S*>(cd.linv) + (i64)(j0 / CBW) * CBW * CBW;
 #pragma unroll
@@ -144,7 +159,7 @@ __global__ void __launch_bounds__(256) chol_diag_kernel(const CholDesc* __restri
       const int j = tc + 16 * cb;
       if (j < CBW) continue;
       const int jj = j - CBW;
-      linv[i * CBW + jj] = (i < jb && jj < jb) ? s_scale(a[ra][cb], 1.0 / sqrt(pivs[i])) : zero;
+      linv[i * CBW + jj] = (i < jb && jj < jb) ? s_scale(a[ra][cb], pivs[i]) : zero;
     }
   }
 }

@@ -1048,10 +1048,10 @@ struct Planner {
             double* pO = gpool->as<double>();
             double* pP = pO + SC * gpool_side;
             if (cplx)
-              rsrs::gram_assemble_kernel<true><<<ga, 256, 0, s>>>(dbx, dboxes, diws, dnbr, gtab_b.as<rsrs::GBlk>(),
+              rsrs::gram_assemble_kernel<true><<<ga, 256, rsrs::gram_assemble_smem(bi.max_r), s>>>(dbx, dboxes, diws, dnbr, gtab_b.as<rsrs::GBlk>(),
                                                                   gps_b_ptr, pO, pP, dws, sides);
             else
-              rsrs::gram_assemble_kernel<false><<<ga, 256, 0, s>>>(dbx, dboxes, diws, dnbr, gtab_b.as<rsrs::GBlk>(),
+              rsrs::gram_assemble_kernel<false><<<ga, 256, rsrs::gram_assemble_smem(bi.max_r), s>>>(dbx, dboxes, diws, dnbr, gtab_b.as<rsrs::GBlk>(),
                                                                    gps_b_ptr, pO, pP, dws, sides);
             post("gram_assemble_kernel", s, launches);
           } else {

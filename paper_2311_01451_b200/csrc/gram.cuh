@@ -149,7 +149,13 @@ __global__ void __launch_bounds__(256) gblk_update_kernel(const BoxDev* __restri
 
 // C_b[pos(q1) + a, pos(q2) + c] = G(n_q1, n_q2)[act_q1[a], act_q2[c]] for slots q2 <= q1
 // of b's neighbour list (the lower block triangle of the near-field Gram).
-// Grid (boxes of the batch, neighbour slots q1).
+// Grid (boxes of the batch, neighbour slots q1).  The slot table, the partner entries
+// and the active-row map of the whole row band are staged in shared memory by all
+// threads at once; the band is then copied in one flat pass (blocks stored as (this, j)
+// and small transposed blocks), with large transposed blocks (mode 1) going through a
+// 32 x 32 shared-memory tile so that both sides stay coalesced.
+// Dynamic shared memory: gram_assemble_smem(max r of the batch).
+inline size_t gram_assemble_smem(int rmax) { return sizeof(int) * 2 * (size_t)(rmax > 0 ? rmax : 1); }
 template <bool C>
 __global__ void __launch_bounds__(256) gram_assemble_kernel(const BoxDev* __restrict__ boxes,
                                                             const BoxDev* __restrict__ level_boxes,
@@ -159,78 +165,97 @@ __global__ void __launch_bounds__(256) gram_assemble_kernel(const BoxDev* __rest
                                                             const double* __restrict__ poolP,
                                                             double* __restrict__ wsd, int sides) {
   typedef typename ScalarOf<C>::T S;
-  __shared__ int pos[64], cnt[64], bx[64], idxs[64];
-  __shared__ int act1[192], act2[192];
+  extern __shared__ int gasm[];
+  __shared__ int pos[65], cnt[64], bx[64], idxs[64], ent[64];
+  __shared__ GBlk sE[64];
   __shared__ S tile[32][33];
   const BoxDev& b = boxes[blockIdx.x];
   const int q1 = blockIdx.y;
   if (q1 >= b.nnbr || b.status != ST_OK) return;
+  const int nn = b.nnbr;
   const int* nd = nbrrec + b.off_nbr;
   const int tid = threadIdx.x;
+  if (tid < nn) {
+    const int idx = nd[4 * tid];
+    cnt[tid] = idx >= 0 ? level_boxes[idx].k : nd[4 * tid + 2];
+    bx[tid] = nd[4 * tid + 3];
+    idxs[tid] = idx;
+    ent[tid] = 0;
+  }
+  __syncthreads();
+  if (cnt[q1] == 0) return;   // uniform
   if (tid == 0) {
     int o = 0;
-    for (int q = 0; q < b.nnbr; ++q) {
-      const int idx = nd[4 * q];
-      const int c = idx >= 0 ? level_boxes[idx].k : nd[4 * q + 2];
+    for (int q = 0; q < nn; ++q) {
       pos[q] = o;
-      cnt[q] = c;
-      bx[q] = nd[4 * q + 3];
-      idxs[q] = idx;
-      o += c;
+      o += cnt[q];
     }
+    pos[nn] = o;
   }
-  __syncthreads();
-  const int n1 = cnt[q1];
-  if (n1 == 0) return;
-  const int i1 = idxs[q1];
-  if (i1 >= 0) {
-    const BoxDev& nb1 = level_boxes[i1];
-    for (int a = tid; a < n1; a += 256) act1[a] = iws[nb1.off_skelrow + a] - nb1.row0;
-  } else {
-    for (int a = tid; a < n1; a += 256) act1[a] = a;
-  }
-  __syncthreads();
+  // partner entries of slot q1's box for every slot q2 <= q1 (each partner matches at most one slot)
   const int box1 = bx[q1];
   const GBlk* t1 = tab + pstart[box1];
-  const i64 ldr = b.ldr;
-  for (int q2 = 0; q2 <= q1; ++q2) {
-    const int n2 = cnt[q2];
-    if (n2 == 0) continue;
-    const int box2 = bx[q2];
-    int ei = 0;
-    while (t1[ei].j != box2) ++ei;        // the partner table holds every pair that meets in a near field
-    const GBlk e = t1[ei];
-    const int i2 = idxs[q2];
-    __syncthreads();
-    if (i2 >= 0) {
-      const BoxDev& nb2 = level_boxes[i2];
-      for (int c = tid; c < n2; c += 256) act2[c] = iws[nb2.off_skelrow + c] - nb2.row0;
-    } else {
-      for (int c = tid; c < n2; c += 256) act2[c] = c;
+  const int np1 = pstart[box1 + 1] - pstart[box1];
+  for (int u = tid; u < np1; u += 256) {
+    const int j = t1[u].j;
+    for (int q = 0; q <= q1; ++q)
+      if (bx[q] == j) ent[q] = u;
+  }
+  __syncthreads();
+  if (tid <= q1) sE[tid] = t1[ent[tid]];
+  // active local row of every column of the band, and its slot
+  int* act = gasm;
+  int* colq = gasm + b.rmax;
+  const int p1 = pos[q1], n1 = cnt[q1], ncols = p1 + n1;
+  for (int col = tid; col < ncols; col += 256) {
+    int lo = 0, hi = q1;   // last slot with pos <= col
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (pos[mid] <= col) lo = mid;
+      else hi = mid - 1;
     }
-    __syncthreads();
-    for (int side = 0; side < sides; ++side) {
-      const S* B = reinterpret_cast<const S*>(side ? poolP : poolO) + e.off;
-      S* Cb = reinterpret_cast<S*>(wsd) + b.off_aug + (side ? (i64)(b.rmax + b.nb) * ldr : 0);
+    const int a = col - pos[lo], idx = idxs[lo];
+    colq[col] = lo;
+    act[col] = idx >= 0 ? iws[level_boxes[idx].off_skelrow + a] - level_boxes[idx].row0 : a;
+  }
+  __syncthreads();
+  const int* act1 = act + p1;
+  const i64 ldr = b.ldr;
+  const bool big1 = n1 >= 16;
+  for (int side = 0; side < sides; ++side) {
+    const S* P = reinterpret_cast<const S*>(side ? poolP : poolO);
+    S* Cb = reinterpret_cast<S*>(wsd) + b.off_aug + (side ? (i64)(b.rmax + b.nb) * ldr : 0);
+    for (int idx = tid; idx < n1 * ncols; idx += 256) {
+      const int a = idx / ncols, col = idx - a * ncols;
+      const int q2 = colq[col];
+      const GBlk& e = sE[q2];
+      S v;
       if (e.mode != 1) {
-        for (int idx = tid; idx < n1 * n2; idx += 256) {
-          const int a = idx / n2, c = idx % n2;
-          Cb[(i64)(pos[q1] + a) * ldr + pos[q2] + c] = B[(i64)act1[a] * e.ld + act2[c]];
-        }
+        v = P[e.off + (i64)act1[a] * e.ld + act[col]];
       } else {
-        // stored transposed: 32 x 32 tiles through shared memory (coalesced both ways)
-        const int tx = tid & 31, ty = tid >> 5;
-        for (int a0 = 0; a0 < n1; a0 += 32)
-          for (int c0 = 0; c0 < n2; c0 += 32) {
-            for (int cc = ty; cc < 32; cc += 8)
-              if (c0 + cc < n2 && a0 + tx < n1) tile[cc][tx] = B[(i64)act2[c0 + cc] * e.ld + act1[a0 + tx]];
-            __syncthreads();
-            for (int aa = ty; aa < 32; aa += 8)
-              if (a0 + aa < n1 && c0 + tx < n2)
-                Cb[(i64)(pos[q1] + a0 + aa) * ldr + pos[q2] + c0 + tx] = s_conj(tile[tx][aa]);
-            __syncthreads();
-          }
+        if (big1 && cnt[q2] >= 16) continue;   // tiled below
+        v = s_conj(P[e.off + (i64)act[col] * e.ld + act1[a]]);
       }
+      Cb[(i64)(p1 + a) * ldr + col] = v;
+    }
+    if (!big1) continue;
+    // large blocks stored transposed: 32 x 32 tiles through shared memory
+    const int tx = tid & 31, ty = tid >> 5;
+    for (int q2 = 0; q2 < q1; ++q2) {
+      const GBlk e = sE[q2];
+      const int n2 = cnt[q2];
+      if (e.mode != 1 || n2 < 16) continue;
+      const S* B = P + e.off;
+      const int* act2 = act + pos[q2];
+      for (int a0 = 0; a0 < n1; a0 += 32)
+        for (int c0 = 0; c0 < n2; c0 += 32) {
+          for (int cc = ty; cc < 32; cc += 8)
+            if (c0 + cc < n2 && a0 + tx < n1) tile[cc][tx] = B[(i64)act2[c0 + cc] * e.ld + act1[a0 + tx]];
+          __syncthreads();
+          for (int aa = ty; aa < 32; aa += 8)
+            if (a0 + aa < n1 && c0 + tx < n2) Cb[(i64)(p1 + a0 + aa) * ldr + pos[q2] + c0 + tx] = s_conj(tile[tx][aa]);
+          __syncthreads();
+        }
     }
   }
 }

@@ -1,0 +1,10 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_gram_blocks.py tests/test_gpu_parity.py -x -q > gpurun_out/pytest_gb.log 2>&1; echo "pytest exit $?"
+tail -2 gpurun_out/pytest_gb.log; grep -E "FAILED|Error" gpurun_out/pytest_gb.log | head -5
+CFG=c2 RUNS=768:2 ITERS=3 PROF=last timeout 900 python tools/quick_c2.py > gpurun_out/c2_q.log 2>&1
+CFG=c3 RUNS=1216:2 ITERS=2 PROF=last timeout 900 python tools/quick_c2.py > gpurun_out/c3_q.log 2>&1
+cat gpurun_out/c2_q.log gpurun_out/c3_q.log | grep -v "^sample"
+export CFG=c3 RUNS=1216:2 ITERS=1 PROF=none
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"chol_diag|gram_assemble" -c 400 --csv --log-file gpurun_out/launches_c3_diag.csv python tools/quick_c2.py > gpurun_out/ncu_l.log 2>&1; echo "ncu launches exit $?"
+python tools/launch_summary.py gpurun_out/launches_c3_diag.csv | head -8
