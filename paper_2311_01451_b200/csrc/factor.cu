@@ -117,6 +117,7 @@ void set_smem_both() {
   set_smem(rsrs::top_solve_kernel<C>, -1);
   set_smem(rsrs::top_apply_kernel<C>, -1);
   set_smem(rsrs::gblk_update_kernel<C>, rsrs::gblk_smem<C>());
+  set_smem(rsrs::skinny_nn_kernel<C>, rsrs::skinny_smem<C>());
 }
 
 void init_kernels() {
@@ -278,6 +279,15 @@ void launch_nn(bool cplx, const NNDesc* d, int n, int mmax, int nmax, cudaStream
     else rsrs::gemm_nn_kernel<64><<<grid, 128, rsrs::NN_SMEM, s>>>(d);
   }
   post("gemm_nn", s, launches);
+}
+
+// in-place skinny updates (E/F), see gemm.cuh
+void launch_skinny(bool cplx, const NNDesc* d, int n, int ncols, cudaStream_t s, int64_t& launches) {
+  if (n <= 0 || ncols <= 0) return;
+  dim3 grid(n, (ncols + 127) / 128);
+  if (cplx) rsrs::skinny_nn_kernel<true><<<grid, 128, rsrs::skinny_smem<true>(), s>>>(d);
+  else rsrs::skinny_nn_kernel<false><<<grid, 128, rsrs::skinny_smem<false>(), s>>>(d);
+  post("skinny_nn", s, launches);
 }
 
 void launch_chol_any(bool cplx, const CholDesc* d, int nmat, int rmax, int mext, cudaStream_t s, int64_t& l) {
@@ -1079,7 +1089,8 @@ struct Planner {
             toc();
           }
           tic(KC_EF);
-          launch_nn(cplx, Def + 2 * ns * q0, 2 * ns * n, bi.max_nb, p, s, launches);
+          if (bi.max_nb <= rsrs::SK_MAX) launch_skinny(cplx, Def + 2 * ns * q0, 2 * ns * n, p, s, launches);
+          else launch_nn(cplx, Def + 2 * ns * q0, 2 * ns * n, bi.max_nb, p, s, launches);
           if (use_blocks) {      // keep the Gram blocks equal to F Omega Omega^* F^* (the E/F on Omega_s)
             const size_t bi_idx = &bi - &binfo[0];
             const int nw = (int)(gwork_off[bi_idx + 1] - gwork_off[bi_idx]);

@@ -582,4 +582,56 @@ RSRS_DI void nn_tile_t(const NNDesc& d, int m, int n, int K, int i0, int j0, dou
 }
 template <bool C> constexpr int tile_n() { return C ? GTC : GT; }
 
+// Skinny in-place update D_rows += alpha opA B_rows with m, K <= SK_MAX (the E/F
+// updates Y_r -= T Y_s, Omega_s += T^* Omega_r: a few rows times p columns, HBM-bound).
+// One CTA per (descriptor, 128-column chunk): opA is staged in shared memory as
+// [K][mp] (mp = m rounded up to 16, zero padded) and every thread streams one column,
+// 16 output rows per pass, reading each B row once per pass (coalesced over columns).
+// Grid (descriptors, column chunks); dynamic shared memory skinny_smem<C>().
+constexpr int SK_MAX = 64;
+template <bool C> constexpr int skinny_smem() { return SK_MAX * SK_MAX * (C ? 16 : 8); }
+template <bool C>
+__global__ void __launch_bounds__(128) skinny_nn_kernel(const NNDesc* __restrict__ descs) {
+  typedef typename ScalarOf<C>::T S;
+  extern __shared__ __align__(16) double ssm[];
+  S* As = reinterpret_cast<S*>(ssm);
+  const NNDesc& d = descs[blockIdx.x];
+  const int m = dyn(d.pm, 0, d.m), n = dyn(d.pn, 0, d.n), K = dyn(d.pK, 0, d.K);
+  if (m <= 0 || K <= 0 || (int)blockIdx.y * 128 >= n) return;
+  const int mp = (m + 15) & ~15;
+  const S* A = reinterpret_cast<const S*>(d.A);
+  const S zero = s_zero(S());
+  for (int idx = threadIdx.x; idx < K * mp; idx += 128) {
+    const int t = idx / mp, i = idx - t * mp;
+    S v = zero;
+    if (i < m) v = d.transA ? s_conj(A[(i64)t * d.lda + i]) : A[(i64)i * d.lda + t];
+    As[idx] = v;
+  }
+  __syncthreads();
+  const int j = blockIdx.y * 128 + threadIdx.x;
+  if (j >= n) return;
+  const S* B = reinterpret_cast<const S*>(d.B);
+  S* D = reinterpret_cast<S*>(d.D);
+  for (int i0 = 0; i0 < m; i0 += 16) {
+    S acc[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) acc[u] = zero;
+    for (int t = 0; t < K; ++t) {
+      const i64 br = d.rowB ? (i64)d.rowB[t] : (i64)t;
+      const S b = B[br * d.ldb + j];
+      const S* at = As + t * mp + i0;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) acc[u] = s_add(acc[u], s_mul(at[u], b));
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int i = i0 + u;
+      if (i < m) {
+        S* dp = D + (d.rowD ? (i64)d.rowD[i] : (i64)i) * d.ldd + j;
+        *dp = s_add(*dp, s_scale(acc[u], d.alpha));
+      }
+    }
+  }
+}
+
 }  // namespace rsrs

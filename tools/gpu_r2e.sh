@@ -1,6 +1,6 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_gram_blocks.py tests/test_gpu_parity.py tests/test_gpu_symmetric.py -x -q > gpurun_out/pytest_gb.log 2>&1; echo "pytest exit $?"
+timeout 900 python -m pytest tests/test_gpu_gram_blocks.py tests/test_gpu_parity.py tests/test_gpu_symmetric.py tests/test_gpu_dist.py -x -q > gpurun_out/pytest_gb.log 2>&1; echo "pytest exit $?"
 tail -2 gpurun_out/pytest_gb.log; grep -E "FAILED|Error" gpurun_out/pytest_gb.log | head -5
 CFG=c2 RUNS=768:2 ITERS=3 PROF=last timeout 900 python tools/quick_c2.py > gpurun_out/c2_q.log 2>&1
 CFG=c3 RUNS=1216:2 ITERS=2 PROF=last timeout 900 python tools/quick_c2.py > gpurun_out/c3_q.log 2>&1
