@@ -220,6 +220,8 @@ RSRS_DI void nn_tile(const NNDesc& d, int m, int n, int K, int i0, int j0, doubl
   for (int t = 0; t < MT; ++t)
 #pragma unroll
     for (int u = 0; u < 4; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
+  // a warp whose sub-tile lies wholly outside D (skinny or ragged rows) skips its MMAs
+  const bool wact = i0 + wr * (TM / 2) < m && j0 + wc * 32 < n;
 
   const int nk = K > 0 ? (K + GBK - 1) / GBK : 0;
   if (nk > 0) {
@@ -237,18 +239,19 @@ RSRS_DI void nn_tile(const NNDesc& d, int m, int n, int K, int i0, int j0, doubl
     __syncthreads();
     const double* as = As + ((kt & 1) * TM + wr * (TM / 2)) * GPA;
     const double* bs = Bs + (kt & 1) * GBK * GPB + wc * 32;
+    if (wact)
 #pragma unroll
-    for (int kk = 0; kk < GBK / 4; ++kk) {
-      double a[MT], b[4];
+      for (int kk = 0; kk < GBK / 4; ++kk) {
+        double a[MT], b[4];
 #pragma unroll
-      for (int t = 0; t < MT; ++t) a[t] = as[(t * 8 + gid) * GPA + kk * 4 + tig];
+        for (int t = 0; t < MT; ++t) a[t] = as[(t * 8 + gid) * GPA + kk * 4 + tig];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) b[u] = bs[(kk * 4 + tig) * GPB + u * 8 + gid];
+        for (int u = 0; u < 4; ++u) b[u] = bs[(kk * 4 + tig) * GPB + u * 8 + gid];
 #pragma unroll
-      for (int t = 0; t < MT; ++t)
+        for (int t = 0; t < MT; ++t)
 #pragma unroll
-        for (int u = 0; u < 4; ++u) dmma884(acc[t][u][0], acc[t][u][1], a[t], b[u]);
-    }
+          for (int u = 0; u < 4; ++u) dmma884(acc[t][u][0], acc[t][u][1], a[t], b[u]);
+      }
     __syncthreads();
   }
   // epilogue
@@ -495,6 +498,8 @@ RSRS_DI void nn_tile_c(const NNDesc& d, int m, int n, int K, int i0, int j0, dou
     for (int u = 0; u < 4; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
   const bool odd_k = tig & 1;
   const double sgn = (gid & 1) ? 1.0 : -1.0;
+  // a warp whose sub-tile lies wholly outside D (skinny or ragged rows) skips its MMAs
+  const bool wact = i0 + wr * (TM / 2) < m && 2 * j0 + wc * 32 < 2 * n;
   const int nk = K2 > 0 ? (K2 + GBK - 1) / GBK : 0;
   if (nk > 0) {
     load_stage(0, 0);
@@ -511,22 +516,23 @@ RSRS_DI void nn_tile_c(const NNDesc& d, int m, int n, int K, int i0, int j0, dou
     __syncthreads();
     const double* as = As + ((kt & 1) * TM + wr * (TM / 2)) * GPA;
     const double* bs = Bs + (kt & 1) * (GBK / 2) * GPB + wc * 32;
+    if (wact)
 #pragma unroll
-    for (int kk = 0; kk < GBK / 4; ++kk) {
-      double a[MT], b[4];
+      for (int kk = 0; kk < GBK / 4; ++kk) {
+        double a[MT], b[4];
 #pragma unroll
-      for (int t = 0; t < MT; ++t) a[t] = as[(t * 8 + gid) * GPA + kk * 4 + tig];
-      const double* brow = bs + (kk * 2 + (tig >> 1)) * GPB;
+        for (int t = 0; t < MT; ++t) a[t] = as[(t * 8 + gid) * GPA + kk * 4 + tig];
+        const double* brow = bs + (kk * 2 + (tig >> 1)) * GPB;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int col = u * 8 + gid;
-        b[u] = odd_k ? sgn * brow[col ^ 1] : brow[col];
+        for (int u = 0; u < 4; ++u) {
+          const int col = u * 8 + gid;
+          b[u] = odd_k ? sgn * brow[col ^ 1] : brow[col];
+        }
+#pragma unroll
+        for (int t = 0; t < MT; ++t)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) dmma884(acc[t][u][0], acc[t][u][1], a[t], b[u]);
       }
-#pragma unroll
-      for (int t = 0; t < MT; ++t)
-#pragma unroll
-        for (int u = 0; u < 4; ++u) dmma884(acc[t][u][0], acc[t][u][1], a[t], b[u]);
-    }
     __syncthreads();
   }
   const i64 ldd2 = 2 * d.ldd, ldc2 = 2 * d.ldc;
