@@ -160,6 +160,17 @@ RSRS_DI void nn_tile(const NNDesc& d, int m, int n, int K, int i0, int j0, doubl
   const int gid = lane >> 2, tig = lane & 3;
   const int wr = warp >> 1, wc = warp & 1;
 
+  // row indices of the B rows of the next stage to be loaded, fetched one stage ahead
+  // so that the dependent index loads overlap the MMAs instead of stalling the cp.async
+  int brow[8];
+  auto fetch_rows = [&](int kt) {
+    const int kr = tid >> 5;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int k = kt * GBK + kr + 4 * q;
+      brow[q] = k < K ? (d.rowB ? d.rowB[k] : k) : 0;
+    }
+  };
   auto load_stage = [&](int s, int kt) {
     const int k0 = kt * GBK;
     if (!d.transA) {
@@ -206,11 +217,7 @@ RSRS_DI void nn_tile(const NNDesc& d, int m, int n, int K, int i0, int j0, doubl
         const int kl = kr + 4 * q;
         const int k = k0 + kl;
         const bool v = k < K && cb > 0;
-        const double* src = d.B;
-        if (v) {
-          const i64 br = d.rowB ? (i64)d.rowB[k] : (i64)k;
-          src = d.B + br * d.ldb + gj;
-        }
+        const double* src = v ? d.B + (i64)brow[q] * d.ldb + gj : d.B;
         cp_async16(&Bs[(s * GBK + kl) * GPB + jc], src, v ? cb : 0);
       }
     }
@@ -225,13 +232,16 @@ RSRS_DI void nn_tile(const NNDesc& d, int m, int n, int K, int i0, int j0, doubl
 
   const int nk = K > 0 ? (K + GBK - 1) / GBK : 0;
   if (nk > 0) {
+    fetch_rows(0);
     load_stage(0, 0);
     cp_async_commit();
+    if (nk > 1) fetch_rows(1);
   }
   for (int kt = 0; kt < nk; ++kt) {
     if (kt + 1 < nk) {
       load_stage((kt + 1) & 1, kt + 1);
       cp_async_commit();
+      if (kt + 2 < nk) fetch_rows(kt + 2);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
@@ -439,6 +449,15 @@ RSRS_DI void nn_tile_c(const NNDesc& d, int m, int n, int K, int i0, int j0, dou
   const int wr = warp >> 1, wc = warp & 1;
   const int K2 = 2 * K, n2 = 2 * n, j02 = 2 * j0;
   const i64 lda2 = 2 * d.lda, ldb2 = 2 * d.ldb;
+  int brow[4];   // B row indices of the next stage (complex k), fetched one stage ahead
+  auto fetch_rows = [&](int kt) {
+    const int kr = tid >> 5;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = kt * (GBK / 2) + kr + 4 * q;
+      brow[q] = k < K ? (d.rowB ? d.rowB[k] : k) : 0;
+    }
+  };
   auto load_stage = [&](int s, int kt) {
     const int k0 = kt * GBK;               // real k
     if (!d.transA) {
@@ -482,11 +501,7 @@ RSRS_DI void nn_tile_c(const NNDesc& d, int m, int n, int K, int i0, int j0, dou
         const int kl = kr + 4 * q;            // complex k (local)
         const int k = (k0 >> 1) + kl;
         const bool v = k < K && cb > 0;
-        const double* src = d.B;
-        if (v) {
-          const i64 br = d.rowB ? (i64)d.rowB[k] : (i64)k;
-          src = d.B + br * ldb2 + gj;
-        }
+        const double* src = v ? d.B + (i64)brow[q] * ldb2 + gj : d.B;
         cp_async16(&Bs[(s * (GBK / 2) + kl) * GPB + jc], src, v ? cb : 0);
       }
     }
@@ -502,13 +517,16 @@ RSRS_DI void nn_tile_c(const NNDesc& d, int m, int n, int K, int i0, int j0, dou
   const bool wact = i0 + wr * (TM / 2) < m && 2 * j0 + wc * 32 < 2 * n;
   const int nk = K2 > 0 ? (K2 + GBK - 1) / GBK : 0;
   if (nk > 0) {
+    fetch_rows(0);
     load_stage(0, 0);
     cp_async_commit();
+    if (nk > 1) fetch_rows(1);
   }
   for (int kt = 0; kt < nk; ++kt) {
     if (kt + 1 < nk) {
       load_stage((kt + 1) & 1, kt + 1);
       cp_async_commit();
+      if (kt + 2 < nk) fetch_rows(kt + 2);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
