@@ -613,7 +613,7 @@ template <bool C> constexpr int tile_n() { return C ? GTC : GT; }
 // 16 output rows per pass, reading each B row once per pass (coalesced over columns).
 // Grid (descriptors, column chunks); dynamic shared memory skinny_smem<C>().
 constexpr int SK_MAX = 64;
-template <bool C> constexpr int skinny_smem() { return SK_MAX * SK_MAX * (C ? 16 : 8); }
+template <bool C> constexpr int skinny_smem() { return SK_MAX * SK_MAX * (C ? 16 : 8) + 2 * SK_MAX * 4; }
 template <bool C>
 __global__ void __launch_bounds__(128) skinny_nn_kernel(const NNDesc* __restrict__ descs) {
   typedef typename ScalarOf<C>::T S;
@@ -625,6 +625,10 @@ __global__ void __launch_bounds__(128) skinny_nn_kernel(const NNDesc* __restrict
   const int mp = (m + 15) & ~15;
   const S* A = reinterpret_cast<const S*>(d.A);
   const S zero = s_zero(S());
+  int* rB = reinterpret_cast<int*>(As + SK_MAX * SK_MAX);   // gathered row indices, staged once
+  int* rD = rB + SK_MAX;
+  for (int t = threadIdx.x; t < K; t += 128) rB[t] = d.rowB ? d.rowB[t] : t;
+  for (int i = threadIdx.x; i < m; i += 128) rD[i] = d.rowD ? d.rowD[i] : i;
   for (int idx = threadIdx.x; idx < K * mp; idx += 128) {
     const int t = idx / mp, i = idx - t * mp;
     S v = zero;
@@ -641,8 +645,7 @@ __global__ void __launch_bounds__(128) skinny_nn_kernel(const NNDesc* __restrict
 #pragma unroll
     for (int u = 0; u < 16; ++u) acc[u] = zero;
     for (int t = 0; t < K; ++t) {
-      const i64 br = d.rowB ? (i64)d.rowB[t] : (i64)t;
-      const S b = B[br * d.ldb + j];
+      const S b = B[(i64)rB[t] * d.ldb + j];
       const S* at = As + t * mp + i0;
 #pragma unroll
       for (int u = 0; u < 16; ++u) acc[u] = s_add(acc[u], s_mul(at[u], b));
@@ -651,7 +654,7 @@ __global__ void __launch_bounds__(128) skinny_nn_kernel(const NNDesc* __restrict
     for (int u = 0; u < 16; ++u) {
       const int i = i0 + u;
       if (i < m) {
-        S* dp = D + (d.rowD ? (i64)d.rowD[i] : (i64)i) * d.ldd + j;
+        S* dp = D + (i64)rD[i] * d.ldd + j;
         *dp = s_add(*dp, s_scale(acc[u], d.alpha));
       }
     }
