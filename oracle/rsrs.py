@@ -130,6 +130,7 @@ class Step:
     G_U: np.ndarray       # |red| x |c|
     X_rr: np.ndarray      # |red| x |red|
     lu: tuple             # scipy lu_factor(X_rr)
+    xrr_mismatch: float = 0.0   # ||X_rr^Y - X_rr^Z|| / ||X_rr^Y|| (SURVEY c.2 #9 diagnostic)
 
 
 @dataclass
@@ -181,7 +182,7 @@ def coupling_estimate(Y_r, Om_r):
 
 def factor(tree: Tree, Y, Z, Om, Psi, eps: float, c_id: float = 1.0, g: float = 1.0,
            l: int = 10, top_level: int = 2, on_step=None, max_boxes: int | None = None,
-           copy: bool = True, estimate_coupling: bool = False) -> Factorization:
+           copy: bool = True, estimate_coupling: bool = False, workers: int = 1) -> Factorization:
     """RSRS factorization from samples in TREE order (N x p each).
 
     The inputs are copied (unless copy=False); `on_step(step, Y, Z, Om, Psi)`
@@ -189,6 +190,13 @@ def factor(tree: Tree, Y, Z, Om, Psi, eps: float, c_id: float = 1.0, g: float = 
     `max_boxes` stops after that many boxes in canonical order and returns the
     partial record (ranks of the boxes processed so far; no top block) -- used
     for sampled checks and bounded timing at full size.
+
+    `workers` > 1 only changes WHEN boxes run, never what they compute: the boxes
+    of one colour are >= 3 boxes apart (R10), so their near sets -- every
+    row one box reads or writes -- are disjoint, and running them concurrently on a
+    thread pool (LAPACK releases the GIL) gives bit-for-bit the result of the
+    sequential canonical order (pinned by tests/test_oracle_rsrs.py).  Colours and
+    levels stay strictly sequential.  Ignored when on_step or max_boxes is given.
     """
     if copy:
         Y = np.array(Y, copy=True)
@@ -204,91 +212,123 @@ def factor(tree: Tree, Y, Z, Om, Psi, eps: float, c_id: float = 1.0, g: float = 
                         perm=tree.perm, dtype=dt)
     lv = tree.levels[L]
     act = [np.arange(lv.start[b], lv.start[b + 1], dtype=np.int64) for b in range(lv.nboxes)]
-    lev = L
-    while lev >= top_level and lev >= 1:
-        lv = tree.levels[lev]
-        atol = atol_schedule(eps, c_id, g, L, lev)
-        fac.atol[lev] = atol
-        for b in tree.canonical_order(lev):
-            if max_boxes is not None and nproc >= max_boxes:
-                fac.S = np.zeros(0, np.int64)
-                fac.A_SS = np.zeros((0, 0), dtype=dt)
-                return fac
-            nproc += 1
-            Ib = act[b]
-            nb = Ib.shape[0]
-            fac.nb[(lev, b)] = nb
-            if nb == 0:
-                fac.ranks[(lev, b)] = 0
-                continue
-            near = np.concatenate([act[j] for j in lv.neighbours[b]])
-            r = near.shape[0]
+    pool = None
+    if workers > 1 and on_step is None and max_boxes is None:
+        from concurrent.futures import ThreadPoolExecutor
+        pool = ThreadPoolExecutor(max_workers=workers)
+
+    def process_box(lev, lv, b, atol):
+        """O3-O9 for box b of level lev; returns (nb, r, k, coupling, Step or None)."""
+        Ib = act[b]
+        nb = Ib.shape[0]
+        if nb == 0:
+            return nb, None, 0, None, None
+        near = np.concatenate([act[j] for j in lv.neighbours[b]])
+        r = near.shape[0]
+        w = p - r
+        if w < l + 1:
+            raise RSRSError("samples", f"level {lev} box {b}: p - r = {w} < l + 1 = {l + 1}")
+        # O4 -- block nullification (PAPER.md:1195-1200)
+        Yp = Y[Ib] @ null_basis(Om[near])
+        Zp = Z[Ib] @ null_basis(Psi[near])
+        # O5 -- joint row ID (PAPER.md:613-666, 874-885)
+        S = np.hstack([Yp, Zp]) / math.sqrt(2.0 * w)
+        k, sk, rd, T, _ = row_id(S, atol)
+        if k > min(nb, w - l):
+            raise RSRSError("samples", f"level {lev} box {b}: rank {k} > w - l = {w - l}")
+        if k == nb:
+            return nb, r, k, None, None          # nothing to eliminate
+        skel = Ib[sk]
+        red = Ib[rd]
+        Th = T.conj().T
+        # O6 -- E/F sample updates
+        if k > 0:
+            Y[red] -= T @ Y[skel]
+            Z[red] -= T @ Z[skel]
+            Om[skel] += Th @ Om[red]
+            Psi[skel] += Th @ Psi[red]
+        # O7 -- block extraction (PAPER.md:1213-1218)
+        X_Y = Y[red] @ pinv_right(Om[near])          # X_{r,near}
+        X_Z = Z[red] @ pinv_right(Psi[near])         # (X_{near,r})^*
+        # O8 -- block Gaussian elimination (PAPER.md:934-955)
+        is_red = np.isin(near, red)
+        pos_red = np.flatnonzero(is_red)
+        pos_c = np.flatnonzero(~is_red)
+        # near lists I_b in ascending order, so pos_red follows `red`'s order
+        assert np.array_equal(near[pos_red], red)
+        c = near[pos_c]
+        X_rr = X_Y[:, pos_red]
+        X_rc = X_Y[:, pos_c]
+        X_cr = X_Z[:, pos_c].conj().T
+        mism = np.linalg.norm(X_rr - X_Z[:, pos_red].conj().T) / max(np.linalg.norm(X_rr), 1e-300)
+        lu = sla.lu_factor(X_rr, check_finite=True)
+        if np.min(np.abs(np.diag(lu[0]))) == 0.0:
+            raise RSRSError("singular", f"level {lev} box {b}: X_rr singular")
+        G_U = sla.lu_solve(lu, X_rc)                       # X_rr^-1 X_rc
+        G_L = sla.lu_solve(lu, X_cr.T, trans=1).T          # X_cr X_rr^-1
+        # O9 -- L/U sample updates (PAPER.md:1219-1227)
+        Yr = Y[red].copy()
+        Zr = Z[red].copy()
+        Y[c] -= G_L @ Yr
+        Z[c] -= G_U.conj().T @ Zr
+        Om[red] += G_U @ Om[c]
+        Psi[red] += G_L.conj().T @ Psi[c]
+        cpl = None
+        if estimate_coupling:     # PAPER.md:1232-1235
+            cpl = (coupling_estimate(Y[red], Om[red]), coupling_estimate(Z[red], Psi[red]))
+        st = Step(level=lev, box=b, skel=skel, red=red, c=c, T=T, G_L=G_L, G_U=G_U,
+                  X_rr=X_rr, lu=lu)
+        st.xrr_mismatch = mism
+        return nb, r, k, cpl, st
+
+    def record(lev, b, res):
+        nb, r, k, cpl, st = res
+        fac.nb[(lev, b)] = nb
+        fac.ranks[(lev, b)] = k
+        if r is not None:
             fac.near[(lev, b)] = r
-            w = p - r
-            if w < l + 1:
-                raise RSRSError("samples", f"level {lev} box {b}: p - r = {w} < l + 1 = {l + 1}")
-            # O4 -- block nullification
-            Yp = Y[Ib] @ null_basis(Om[near])
-            Zp = Z[Ib] @ null_basis(Psi[near])
-            # O5 -- joint row ID
-            S = np.hstack([Yp, Zp]) / math.sqrt(2.0 * w)
-            k, sk, rd, T, _ = row_id(S, atol)
-            fac.ranks[(lev, b)] = k
-            if k > min(nb, w - l):
-                raise RSRSError("samples", f"level {lev} box {b}: rank {k} > w - l = {w - l}")
-            if k == nb:
-                continue                      # nothing to eliminate
-            skel = Ib[sk]
-            red = Ib[rd]
-            Th = T.conj().T
-            # O6 -- E/F sample updates
-            if k > 0:
-                Y[red] -= T @ Y[skel]
-                Z[red] -= T @ Z[skel]
-                Om[skel] += Th @ Om[red]
-                Psi[skel] += Th @ Psi[red]
-            # O7 -- block extraction
-            X_Y = Y[red] @ pinv_right(Om[near])          # X_{r,near}
-            X_Z = Z[red] @ pinv_right(Psi[near])         # (X_{near,r})^*
-            # O8 -- block Gaussian elimination
-            is_red = np.isin(near, red)
-            pos_red = np.flatnonzero(is_red)
-            pos_c = np.flatnonzero(~is_red)
-            # near lists I_b in ascending order, so pos_red follows `red`'s order
-            assert np.array_equal(near[pos_red], red)
-            c = near[pos_c]
-            X_rr = X_Y[:, pos_red]
-            X_rc = X_Y[:, pos_c]
-            X_cr = X_Z[:, pos_c].conj().T
-            fac.xrr_mismatch.append(
-                np.linalg.norm(X_rr - X_Z[:, pos_red].conj().T) / max(np.linalg.norm(X_rr), 1e-300))
-            lu = sla.lu_factor(X_rr, check_finite=True)
-            if np.min(np.abs(np.diag(lu[0]))) == 0.0:
-                raise RSRSError("singular", f"level {lev} box {b}: X_rr singular")
-            G_U = sla.lu_solve(lu, X_rc)                       # X_rr^-1 X_rc
-            G_L = sla.lu_solve(lu, X_cr.T, trans=1).T          # X_cr X_rr^-1
-            # O9 -- L/U sample updates
-            Yr = Y[red].copy()
-            Zr = Z[red].copy()
-            Y[c] -= G_L @ Yr
-            Z[c] -= G_U.conj().T @ Zr
-            Om[red] += G_U @ Om[c]
-            Psi[red] += G_L.conj().T @ Psi[c]
-            if estimate_coupling:
-                fac.coupling[(lev, b)] = (coupling_estimate(Y[red], Om[red]), coupling_estimate(Z[red], Psi[red]))
-            st = Step(level=lev, box=b, skel=skel, red=red, c=c, T=T, G_L=G_L, G_U=G_U,
-                      X_rr=X_rr, lu=lu)
+        if st is not None:
+            fac.xrr_mismatch.append(st.xrr_mismatch)
+            if cpl is not None:
+                fac.coupling[(lev, b)] = cpl
             steps.append(st)
-            act[b] = skel
-            if on_step is not None:
-                on_step(st, Y, Z, Om, Psi)
-        # O10 -- merge children into parents
-        if lev - 1 >= 0:
-            parent_level = tree.levels[lev - 1]
-            kids = parent_level.children_of(lv)
-            act = [np.concatenate([act[j] for j in kids[q]]) if kids[q] else np.zeros(0, np.int64)
-                   for q in range(parent_level.nboxes)]
-        lev -= 1
+            act[b] = st.skel
+
+    try:
+        lev = L
+        while lev >= top_level and lev >= 1:
+            lv = tree.levels[lev]
+            atol = atol_schedule(eps, c_id, g, L, lev)
+            fac.atol[lev] = atol
+            order = tree.canonical_order(lev)
+            if pool is None:
+                for b in order:
+                    if max_boxes is not None and nproc >= max_boxes:
+                        fac.S = np.zeros(0, np.int64)
+                        fac.A_SS = np.zeros((0, 0), dtype=dt)
+                        return fac
+                    nproc += 1
+                    res = process_box(lev, lv, b, atol)
+                    record(lev, b, res)
+                    if res[4] is not None and on_step is not None:
+                        on_step(res[4], Y, Z, Om, Psi)
+            else:
+                # one colour at a time (canonical order); its boxes touch disjoint rows
+                for col in sorted(set(int(lv.colour[b]) for b in order)):
+                    group = [b for b in order if lv.colour[b] == col]
+                    results = list(pool.map(lambda b: process_box(lev, lv, b, atol), group))
+                    for b, res in zip(group, results):
+                        record(lev, b, res)
+            # O10 -- merge children into parents (PAPER.md:1004, 1071)
+            if lev - 1 >= 0:
+                parent_level = tree.levels[lev - 1]
+                kids = parent_level.children_of(lv)
+                act = [np.concatenate([act[j] for j in kids[q]]) if kids[q] else np.zeros(0, np.int64)
+                       for q in range(parent_level.nboxes)]
+            lev -= 1
+    finally:
+        if pool is not None:
+            pool.shutdown()
     # O11 -- top block A~_SS = Y_S pinv(Omega_S)
     S = np.concatenate(act) if act else np.zeros(0, np.int64)
     fac.S = S

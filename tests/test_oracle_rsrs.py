@@ -5,6 +5,7 @@ operators, closed-form identities of the paper, textbook routines (dense LU
 solve, SVD ranks) and special cases (zero far field, diagonal operator).
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -234,19 +235,30 @@ def test_small_relerr_errsolve_dense(kernel):
     assert np.linalg.norm(O.solve(f, O.apply(f, v)) - v) <= 1e-11 * np.linalg.norm(v)
 
 
-def test_c1_against_dense_lu():
-    """c1 end to end: ||x - A\\b|| / ||A\\b|| <= 10 eps, residual <= 10 eps, ranks vs SVD."""
-    cfg = W.CONFIGS["c1"]
+def _dense_lu_case(cfg, workers=None):
     X = W.points(cfg)
     t = O.build_tree(X, cfg.leaf, *cfg.root())
     A = W.dense_matrix(cfg, X)
     Om, Ps = W.omega_psi(cfg)
     Y, Z = W.dense_samples(A, Om, Ps)
     P = t.perm
-    f = O.factor(t, Y[P], Z[P], Om[P], Ps[P], cfg.eps)
+    f = O.factor(t, Y[P], Z[P], Om[P], Ps[P], cfg.eps, c_id=cfg.c_id, g=cfg.g, l=cfg.l,
+                 workers=workers or (os.cpu_count() or 1))
     b = W.rhs(cfg)
     x = O.solve(f, b)
     xd = sla.lu_solve(sla.lu_factor(A), b)                       # LAPACK getrf/getrs
+    return t, A, P, f, b, x, xd
+
+
+@pytest.mark.parametrize("frozen", [False, True], ids=["g1_cid1", "frozen_cfg"])
+def test_c1_against_dense_lu(frozen):
+    """c1 end to end: ||x - A\\b|| / ||A\\b|| <= 10 eps, residual <= 10 eps, ranks vs SVD --
+    with g = c_id = 1 and at the FROZEN configuration every GPU comparison and bench line
+    uses (workloads.CONFIGS['c1']: p = 768, l = 10, g = 2, c_id = 1)."""
+    cfg = W.CONFIGS["c1"]
+    if not frozen:
+        cfg = W.Config("c1_g1", cfg.geometry, cfg.n, cfg.kernel, cfg.dtype, p=cfg.p, seed=cfg.seed, g=1.0, c_id=1.0)
+    t, A, P, f, b, x, xd = _dense_lu_case(cfg)
     assert np.linalg.norm(x - xd) / np.linalg.norm(xd) <= 10 * cfg.eps
     assert np.linalg.norm(A @ x - b) / np.linalg.norm(b) <= 10 * cfg.eps
     # p independent of N (Fig. 6c) is exercised by c2 on the GPU; here: leaf ranks
@@ -259,8 +271,75 @@ def test_c1_against_dense_lu():
         near = np.concatenate([np.arange(lv.start[j], lv.start[j + 1]) for j in lv.neighbours[b]])
         far = np.setdiff1d(np.arange(cfg.N), near)
         sv = np.linalg.svd(np.hstack([At[np.ix_(Ib, far)], At[np.ix_(far, Ib)].T]), compute_uv=False)
-        srank = int((sv / math.sqrt(2) > cfg.eps).sum())
+        srank = int((sv / math.sqrt(2) > cfg.c_id * cfg.eps).sum())
         assert srank - 1 <= f.ranks[(t.L, b)] <= srank + 3
+
+
+def test_sphere_frozen_config_against_dense_lu():
+    """The sphere configurations' frozen parameters (p = 1216, g = 2, c5's c_id = 0.5; c3's
+    c_id = 1 with g = 2 is the c1 frozen case above) on the
+    same Fibonacci-sphere Laplace operator at N = 6000 (dense A, depth L = 3: levels 3 and 2
+    are compressed, so the relaxed tolerance atol(2) = g atol(3) is exercised):
+    solution vs LAPACK getrf/getrs and residual within 10 eps."""
+    cfg = W.CONFIGS["c5"].scaled(6000)
+    t, A, P, f, b, x, xd = _dense_lu_case(cfg)
+    assert t.L >= 3
+    assert np.linalg.norm(x - xd) / np.linalg.norm(xd) <= 10 * cfg.eps
+    assert np.linalg.norm(A @ x - b) / np.linalg.norm(b) <= 10 * cfg.eps
+
+
+def test_atol_schedule_pins():
+    """atol(l) at the frozen configuration ("the absolute tolerance at the leaf
+    level"; "successively relaxed at every level"):
+      * the leaf level uses c_id * eps exactly;
+      * g > 1 relaxes strictly at every coarser level (atol(l-1) > atol(l)); g = 1 keeps it;
+      * behaviour: relaxing only the coarse levels leaves every leaf rank unchanged and can
+        only lower the ranks of the next level (the CPQR rank count is monotone in atol for
+        identical inputs).  An exponent (l - L) instead of (L - l) fails the last two."""
+    cfg = W.CONFIGS["c1"].scaled(48, p=640)
+    X = W.points(cfg)
+    t = O.build_tree(X, 36, *cfg.root())
+    A = W.dense_matrix(cfg, X)
+    Om, Ps = W.omega_psi(cfg)
+    Y, Z = W.dense_samples(A, Om, Ps)
+    P = t.perm
+    assert t.L >= 3
+    fs = {}
+    for g in (1.0, 2.0, 4.0):
+        fs[g] = O.factor(t, Y[P], Z[P], Om[P], Ps[P], 1e-6, c_id=1.0, g=g, l=10, workers=os.cpu_count() or 1)
+    L = t.L
+    for g, f in fs.items():
+        assert f.atol[L] == 1e-6
+        levs = sorted(f.atol)
+        for lo, hi in zip(levs[:-1], levs[1:]):        # lo = coarser level
+            if g > 1:
+                assert f.atol[lo] > f.atol[hi]
+            else:
+                assert f.atol[lo] == f.atol[hi]
+    nbx = t.levels[L].nboxes
+    for g in (2.0, 4.0):
+        assert all(fs[g].ranks[(L, b)] == fs[1.0].ranks[(L, b)] for b in range(nbx))
+        n1 = t.levels[L - 1].nboxes
+        ks = [(fs[g].ranks[(L - 1, b)], fs[1.0].ranks[(L - 1, b)]) for b in range(n1)]
+        assert all(a <= c for a, c in ks)
+    # and the relaxation actually bites somewhere on the coarse level
+    assert sum(fs[4.0].ranks[(L - 1, b)] for b in range(t.levels[L - 1].nboxes)) < \
+        sum(fs[1.0].ranks[(L - 1, b)] for b in range(t.levels[L - 1].nboxes))
+
+
+def test_colour_parallel_oracle_is_bit_identical():
+    """workers > 1 runs the boxes of one colour concurrently (their near sets are disjoint,
+    DESIGN.md R10): every stored factor and the top block equal the sequential run bit for bit."""
+    cfg, X, t, A, At, Y, Z, Om, Ps = small_problem(kernel="helm2d")
+    f1 = O.factor(t, Y, Z, Om, Ps, eps=1e-6, g=2.0)
+    f4 = O.factor(t, Y, Z, Om, Ps, eps=1e-6, g=2.0, workers=4)
+    assert len(f1.steps) == len(f4.steps) > 0
+    for a, c in zip(f1.steps, f4.steps):
+        assert (a.level, a.box) == (c.level, c.box)
+        for nm in ("skel", "red", "c", "T", "G_L", "G_U", "X_rr"):
+            assert np.array_equal(getattr(a, nm), getattr(c, nm)), nm
+    assert np.array_equal(f1.A_SS, f4.A_SS)
+    assert f1.ranks == f4.ranks
 
 
 # ---------------------------------------------------------------------------
