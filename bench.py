@@ -7,17 +7,24 @@ whole hot path over one seeded synthetic problem.
 value = DOF / step time (N points per step, summed over ranks), CUDA events on the
 launching stream, barrier + synchronize on both sides, max over ranks.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl reference]
 
-Workload: configs[1] of BASELINE.json (c2: 512 x 512 grid, 2D log kernel, FP64,
-N = 262144, eps = 1e-6) -- inputs (Y, Z, Omega, Psi: 6.4 GB) are larger than L2, so
-no explicit L2 flush is needed.  Sampling (Y = A Omega, Z = A^* Psi through the
-harness kernel matvec) is done once before timing (excluded, BASELINE.json
-north_star).  N > 1 (torchrun): ONE problem sharded over the ranks (strong scaling): each rank
+Workload (default): c5 of BASELINE.json -- N = 1,048,576 Fibonacci-sphere points,
+3D Laplace second-kind kernel, FP64, octree leaf 64, eps = 1e-6 -- the largest
+configuration, and it fits one B200 (the 40.8 GB sample store twice: pristine +
+working copy).  Inputs are far larger than L2 (no flush needed).  Sampling
+(Y = A Omega, Z = A^* Psi through the harness kernel matvec) is done once before
+timing (excluded, BASELINE.json north_star) and reported as sample_s.
+N > 1 (torchrun): ONE problem sharded over the ranks (strong scaling): each rank
 owns a Morton range of leaves, draws its own sample rows, and the sweep exchanges
 near-field halo rows per colour and skeleton rows per level over NCCL
-(include/rsrs.h multi-GPU section); the solve takes the
-replicated right-hand side.
+(include/rsrs.h multi-GPU section).
+
+cpu_baseline / --impl reference: the CPU oracle (oracle/, test infrastructure) as it
+stands, timed on this host's cores: a full factor + solve of the same configuration
+family (kernel, p, eps, g, c_id, leaf) at a bounded N (default 8192 for the sphere),
+its samples formed on the CPU from the dense operator (untimed), boxes of one colour
+on nproc worker threads (one BLAS thread each).
 """
 from __future__ import annotations
 
@@ -40,15 +47,17 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c5")
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--cpu-boxes", type=int, default=0, help="oracle sample size (leaf boxes); 0 = auto")
+    ap.add_argument("--cpu-n", type=int, default=0,
+                    help="oracle sample size N (same config family); 0 = auto (sphere 8192, 2D grid 64x64)")
     ap.add_argument("--variant", default="paper", choices=["paper", "symmetric"],
                     help="paper: two independent sketches (PAPER.md:1180-1183, the headline); symmetric: the "
-                         "SURVEY 8(f) f2 shortcut Psi = Omega, Z = Y for real symmetric A")
+                         "SURVEY 8(f) f2 shortcut Psi = Omega, Z = Y for real symmetric A (c1-c3, c5) / "
+                         "Psi = conj(Omega), Z = conj(Y) for the complex-symmetric c4")
     return ap.parse_args()
 
 
@@ -173,7 +182,8 @@ def setup_problem(cfg, dev, rank=0, world=1, pg=None, symmetric=False):
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
     R.sample_matvec_rows(cfg.kernel, pts_d, W.kernel_weight(cfg), Om_d, Y_d, r0, kappa=cfg.kappa)
-    if symmetric:            # f2: Psi = Omega => Z = A^T Omega = Y; only Y / Omega are used
+    if symmetric:            # f2: Psi = Omega (real) / conj(Omega) (complex symmetric c4) => Z = Y / conj(Y);
+        #                      only Y / Omega are read by the library
         Ps_d, Z_d = Om_d, Y_d
     else:
         R.sample_matvec_rows(cfg.kernel, pts_d, W.kernel_weight(cfg), Ps_d, Z_d, r0, adjoint=True,
@@ -214,47 +224,88 @@ def factor_solve(pb, work, x, stream, profile=False, solve_events=None, estimate
 
 
 # ---------------------------------------------------------------------------
-# CPU oracle baseline on a bounded sample (leaf boxes of the same workload)
+# CPU oracle baseline: a full factor + solve of a bounded member of the workload family
 # ---------------------------------------------------------------------------
-def oracle_sample(cfg, nboxes: int, reps: int = 1, seed_offset: int = 0):
-    """Time the oracle on the first `nboxes` leaf boxes of the canonical order.
+def oracle_config(cfg, n: int = 0):
+    """Same kernel / p / eps / g / c_id / leaf as cfg at a bounded size."""
+    if cfg.geometry == "grid2d":
+        return cfg.scaled(n or 64)          # 64 x 64 grid (c1 size)
+    return cfg.scaled(n or 8192)
 
-    Those boxes (colour 0 of the leaf level) read only their own Y/Z rows and the
-    near-field Omega/Psi rows, so their samples are computed exactly on the CPU by
-    direct sums (no GPU involvement) and the oracle's per-box work is the full
-    O4-O9 sequence of the workload.  Returns DOF/s = (points eliminated or
-    skeletonised in the sample) / time, plus the sample description.
-    """
+
+def oracle_problem(cfg_s):
+    """Dense operator and seeded samples of the bounded oracle case (CPU, untimed)."""
     import numpy as np
     from threadpoolctl import threadpool_limits
 
     import oracle as O
     import workloads as W
-    X = W.points(cfg)
-    t = O.build_tree(X, cfg.leaf, *cfg.root())
-    N, p, L = cfg.N, cfg.p, t.L
-    lv = t.levels[L]
-    order = t.canonical_order(L)[:nboxes]
-    Om, Ps = W.omega_psi(cfg)
-    Om, Ps = Om[t.perm], Ps[t.perm]
-    Y = np.zeros_like(Om)
-    Z = np.zeros_like(Ps)
-    allidx = np.arange(N)
+    X = W.points(cfg_s)
+    t = O.build_tree(X, cfg_s.leaf, *cfg_s.root())
     with threadpool_limits(limits=os.cpu_count()):
-        for b in order:
-            rows = np.arange(lv.start[b], lv.start[b + 1])
-            Ab = W.kernel_block(cfg, X, t.perm[rows], t.perm[allidx])
-            Y[rows] = Ab @ Om
-            Z[rows] = Ab.conj() @ Ps        # A^* rows = conj(A)^T rows (symmetric kernels)
-    times = []
-    dofs = int(sum(lv.start[b + 1] - lv.start[b] for b in order))
-    with threadpool_limits(limits=1):
-        for _ in range(reps):
-            Yc, Zc, Oc, Pc = Y.copy(), Z.copy(), Om.copy(), Ps.copy()
-            t0 = time.perf_counter()
-            O.factor(t, Yc, Zc, Oc, Pc, cfg.eps, c_id=cfg.c_id, g=cfg.g, l=cfg.l, max_boxes=len(order), copy=False)
-            times.append(time.perf_counter() - t0)
-    return dofs, times, f"oracle O4-O9 on the first {len(order)} leaf boxes (colour 0, {dofs} points) of {cfg.name}"
+        A = W.dense_matrix(cfg_s, X)
+        Om, Ps = W.omega_psi(cfg_s)
+        Y, Z = W.dense_samples(A, Om, Ps)
+        P = t.perm
+        arrays = [np.ascontiguousarray(M[P]) for M in (Y, Z, Om, Ps)]
+    b = W.rhs(cfg_s)
+    return dict(cfg=cfg_s, X=X, A=A, tree=t, arrays=arrays, b=b)
+
+
+def oracle_run(pb, workers: int):
+    """One timed oracle factor + solve (the oracle as it stands; inputs copied outside the timing)."""
+    import numpy as np
+
+    import oracle as O
+    cfg_s = pb["cfg"]
+    Yc, Zc, Oc, Pc = (M.copy() for M in pb["arrays"])
+    t0 = time.perf_counter()
+    f = O.factor(pb["tree"], Yc, Zc, Oc, Pc, cfg_s.eps, c_id=cfg_s.c_id, g=cfg_s.g, l=cfg_s.l, copy=False,
+                 workers=workers)
+    t1 = time.perf_counter()
+    x = O.solve(f, pb["b"])
+    t2 = time.perf_counter()
+    res = float(np.linalg.norm(pb["A"] @ x - pb["b"]) / np.linalg.norm(pb["b"]))
+    return t2 - t0, t1 - t0, t2 - t1, res
+
+
+def host_desc():
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    blas = ""
+    try:
+        from threadpoolctl import threadpool_info
+        for d in threadpool_info():
+            if d.get("user_api") == "blas":
+                blas = f"{d.get('internal_api')} {d.get('version')}"
+                break
+    except Exception:  # noqa: BLE001
+        pass
+    return model, blas
+
+
+def oracle_baseline(cfg, n: int = 0, reps: int = 1, warm: int = 0):
+    """cpu_baseline record: the oracle's full factor + solve of the bounded case, DOF/s."""
+    pb = oracle_problem(oracle_config(cfg, n))
+    workers = os.cpu_count() or 1
+    times = [oracle_run(pb, workers) for _ in range(warm + reps)][warm:]
+    tot = sum(t[0] for t in times)
+    cfg_s = pb["cfg"]
+    model, blas = host_desc()
+    desc = (f"oracle factor + solve (every level, top block, 1-RHS solve) of {cfg_s.name}: {cfg.kernel}, "
+            f"N = {cfg_s.N}, L = {pb['tree'].L}, p = {cfg_s.p}, eps = {cfg_s.eps}, g = {cfg_s.g}, c_id = {cfg_s.c_id}; "
+            f"samples from the dense operator (untimed); {workers} worker threads x 1 BLAS thread ({blas}); "
+            f"CPU: {model}")
+    rec = {"value": cfg_s.N * len(times) / tot, "unit": "DOF/s", "cores": workers, "kind": "oracle",
+           "sample": desc, "seconds_per_run": tot / len(times), "factor_s": times[-1][1], "solve_s": times[-1][2],
+           "residual": times[-1][3], "N": cfg_s.N, "cpu_model": model, "blas": blas}
+    return rec, times
 
 
 # ---------------------------------------------------------------------------
@@ -263,16 +314,15 @@ def run_reference(args, rank, world, pg):
     if rank != 0:
         return
     cfg = W.CONFIGS[args.config]
-    nb = args.cpu_boxes or 24
-    dofs, times, desc = oracle_sample(cfg, nb, reps=args.warmup + args.steps)
-    timed = times[args.warmup:]
-    tot = sum(timed)
-    val = dofs * len(timed) / tot
+    rec, times = oracle_baseline(cfg, args.cpu_n, reps=args.steps, warm=args.warmup)
+    tot = sum(t[0] for t in times)
+    val = rec["value"]
     line = {"metric": METRIC, "value": val, "unit": "DOF/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(timed), "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic", "impl": "reference",
-            "config": {"workload": cfg.name, "N": cfg.N, "p": cfg.p, "eps": cfg.eps, "sample": desc},
-            "cpu_baseline": {"value": val, "unit": "DOF/s", "cores": 1, "kind": "oracle", "sample": desc},
+            "config": {"workload": cfg.name, "N": cfg.N, "p": cfg.p, "eps": cfg.eps,
+                       "sample": rec["sample"], "same_config": False},
+            "cpu_baseline": rec,
             "e2e": {"value": val, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -285,8 +335,6 @@ def run_native(args, rank, world, local, pg):
     dev = torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
     cfg = W.CONFIGS[args.config]
-    if args.variant == "symmetric" and cfg.is_complex:
-        raise SystemExit("--variant symmetric needs a real symmetric operator (not c4)")
     pb = setup_problem(cfg, dev, rank, world, pg, symmetric=args.variant == "symmetric")
     stream = torch.cuda.Stream(device=dev)
     work = [t.clone() for t in pb["src"]]
@@ -365,9 +413,13 @@ def run_native(args, rank, world, local, pg):
     # ---- e2e: host (pinned) inputs, H2D + factor + solve + D2H inside the timed region
     e2e = None
     if not args.no_e2e:
-        host = [t.cpu().pin_memory() for t in pb["src"]]
-        hb = pb["b"].cpu().pin_memory()
-        hx = torch.empty_like(hb).pin_memory()
+        def pinned_copy(t):        # pinned host buffer filled from the device (no pageable staging copy)
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t)
+            return h
+        host = [pinned_copy(t) for t in pb["src"]]
+        hb = pinned_copy(pb["b"])
+        hx = torch.empty(hb.shape, dtype=hb.dtype, pin_memory=True)
         h2d = sum(t.numel() * t.element_size() for t in host) + hb.numel() * hb.element_size()
         d2h = hx.numel() * hx.element_size()
         barrier(pg, dev)
@@ -398,27 +450,38 @@ def run_native(args, rank, world, local, pg):
     per_launch_ms = d["ms"] / max(d["launches"], 1)
     achieved = d["flops"] / (d["ms"] * 1e-3) / 1e12
     peak = peaks.get("dmma_tflops")
-    traffic = None
-    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    # DRAM bytes per class region (one NVTX range = one colour batch's launches of the class),
+    # dram__bytes_read.sum + dram__bytes_write.sum from an ncu capture of THIS config
+    # (tools/ncu_traffic.py -> profiles/ncu_traffic_r02.json); None if not captured.
+    traffic, traffic_src = None, None
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic_r02.json")
     if os.path.exists(tfile):
         try:
-            traffic = json.load(open(tfile)).get(name)
+            rec = json.load(open(tfile)).get(cfg.name, {}).get(name)
+            if rec:
+                traffic, traffic_src = rec["bytes_per_region"], rec.get("source")
         except Exception:  # noqa: BLE001
             traffic = None
+    nreg = max(d["launches"], 1)
     roof = {"bound": "tensor", "kernel": name, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-            "frac": (achieved / peak) if peak else None, "traffic": traffic,
+            "frac": (achieved / peak) if peak else None, "traffic": traffic, "traffic_source": traffic_src,
             "peak_source": "measured FP64 DMMA (tools/fp64_peak, this box; MEASURED_PEAKS.json has no FP64)",
-            "flops_per_launch": d["flops"] / max(d["launches"], 1), "ms_per_launch": per_launch_ms,
+            "launch_unit": "one class region = the launches of the class for one colour batch (an NVTX range)",
+            "flops_per_launch": d["flops"] / nreg, "bytes_model_per_launch": d["bytes"] / nreg,
+            "ms_per_launch": per_launch_ms, "launches": d["launches"] // max(args.steps, 1),
             "share_of_step": d["ms"] / ms}
     breakdown = {k: {"ms_per_step": v["ms"] / args.steps, "tflops": v["flops"] / max(v["ms"], 1e-9) / 1e9,
                      "gbs": v["bytes"] / max(v["ms"], 1e-9) / 1e6} for k, v in prof.items() if v["launches"]}
     cpu = None
     if not args.no_cpu and world == 1:
-        nbx = args.cpu_boxes or 96
-        dofs, times, desc = oracle_sample(cfg, nbx, reps=1)
-        cpu = {"value": dofs / times[0], "unit": "DOF/s", "cores": 1, "kind": "oracle", "sample": desc,
-               "seconds": times[0]}
+        cpu, _ = oracle_baseline(cfg, args.cpu_n, reps=1)
     sweep_tf = st["flops_model"] / (st["factor_ms"] * 1e-3) / 1e12
+    sweep_tf_s = st["flops_survey"] / (st["factor_ms"] * 1e-3) / 1e12
+    sweep = {"build_model_tflop": st["flops_model"] / 1e12, "build_model_tflops": sweep_tf,
+             "survey_model_tflop": st["flops_survey"] / 1e12, "survey_model_tflops": sweep_tf_s,
+             "survey_model_frac": (sweep_tf_s / peak) if peak else None,
+             "note": "whole factor sweep: build model = this build's formulation (CholeskyQR, Gram blocks); "
+                     "survey model = SURVEY 8(d) standard dense forms on the same (n_b, r, k)"}
     line = {"metric": METRIC, "value": N * args.steps / (ms * 1e-3), "unit": "DOF/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
@@ -428,7 +491,7 @@ def run_native(args, rank, world, local, pg):
                                        if world > 1 else "single GPU")},
             "factor_ms": st["factor_ms"], "solve_ms": statistics.median(solve_ms), "sample_s": pb["t_sample"], "tree_s": pb["t_tree"],
             "residual": resid, "top_size": st["top_size"], "max_rank": st["max_rank"],
-            "memory_scalars": st["memory_scalars"], "sweep_tflops": sweep_tf,
+            "memory_scalars": st["memory_scalars"], "sweep": sweep,
             "roofline": roof, "kernels": breakdown, "fp64_peaks": peaks, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clk, "coupling_estimate": coupling}
     print(json.dumps(line), flush=True)

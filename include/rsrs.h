@@ -64,10 +64,16 @@ typedef struct {
   int profile;         /* 1: time every kernel class with CUDA events on `stream` (rsrs_factor_profile) */
   int gather_level;    /* multi-GPU: boxes on levels <= gather_level are gathered on rank 0 (-1: auto,
                           the largest level with <= 16 * nranks boxes; always >= top_level - 1) */
-  int symmetric;       /* 1: symmetric shortcut (not in the paper, which always draws two
-                          independent sketches): A real symmetric, Psi = Omega hence
-                          Z = Y; only the Y / Omega side of the sweep runs, X_rr is symmetrised so that
-                          G_L = G_U^T.  Z and Psi are ignored (may be NULL).  RSRS_F64 only. */
+  int symmetric;       /* symmetric shortcuts (not in the paper, which always draws two
+                          independent sketches).  Only the Y / Omega side of the sweep
+                          runs; Z and Psi are ignored (may be NULL).
+                          RSRS_F64, symmetric = 1 (or 2): A real symmetric, Psi = Omega hence Z = Y;
+                            H = 2 Y''Y''^T, X_rr symmetrised so that G_L = G_U^T.
+                          RSRS_C128, symmetric = 2: A complex symmetric (A = A^T, e.g. the Helmholtz
+                            operator of config c4), Psi = conj(Omega) hence Z = A^* Psi = conj(Y); every
+                            Z-side quantity is the conjugate of its Y-side one: H = 2 Re(Y''Y''^*) (so T
+                            is real), X_cr = X_Y^T, X_rr := (X_rr + X_rr^T)/2 so that G_L = G_U^T.
+                          RSRS_C128 with symmetric = 1 (Hermitian) is rejected (RSRS_ERR_INVALID). */
   int direct_gram;     /* 1: compute every near-field Gram directly (r x r x p per box) instead of
                           assembling it from the level-wide box-pair blocks (single rank) */
   int push_updates;    /* 1: apply every L/U sample update when its box is eliminated (push, as the
@@ -87,10 +93,16 @@ typedef struct {
   int64_t max_rank;          /* max k over boxes */
   int64_t memory_scalars;    /* M: stored scalars of T, G_L, G_U, X_rr, A_SS */
   double factor_ms;          /* device time of the last rsrs_factor (CUDA events) */
-  double flops_model;        /* algorithmic flop count (SURVEY 8(d) model, real-equivalent) */
-  double bytes_model;        /* algorithmic HBM bytes of the sweep */
+  double flops_model;        /* flops of THIS BUILD's formulation (CholeskyQR nullification, level-wide
+                                Gram blocks, Gram-pivoted ID, explicit X_rr^-1),
+                                real-equivalent, from the recorded (n_b, r, k) of every box; the
+                                per-class split is rsrs_factor_profile */
+  double bytes_model;        /* algorithmic HBM bytes of the sweep (same formulation) */
   int64_t launches;          /* kernels launched by the last rsrs_factor */
   int64_t solve_launches;    /* kernels one rsrs_solve / rsrs_apply call launches */
+  double flops_survey;       /* flops of the method by SURVEY 8(d)'s standard dense forms (Householder QR
+                                of the near field, projection, truncated CPQR, extraction, LU, sample
+                                updates), real-equivalent, same (n_b, r, k) */
 } rsrs_stats;
 
 /* ---------------------------------------------------------------------------

@@ -213,9 +213,13 @@ def factor(tree: Tree, Y, Z, Om, Psi, eps: float, c_id: float = 1.0, g: float = 
     lv = tree.levels[L]
     act = [np.arange(lv.start[b], lv.start[b + 1], dtype=np.int64) for b in range(lv.nboxes)]
     pool = None
+    blas_limit = None
     if workers > 1 and on_step is None and max_boxes is None:
         from concurrent.futures import ThreadPoolExecutor
+
+        from threadpoolctl import threadpool_limits
         pool = ThreadPoolExecutor(max_workers=workers)
+        blas_limit = threadpool_limits(limits=1)     # one BLAS thread per worker (no oversubscription)
 
     def process_box(lev, lv, b, atol):
         """O3-O9 for box b of level lev; returns (nb, r, k, coupling, Step or None)."""
@@ -326,19 +330,20 @@ def factor(tree: Tree, Y, Z, Om, Psi, eps: float, c_id: float = 1.0, g: float = 
                 act = [np.concatenate([act[j] for j in kids[q]]) if kids[q] else np.zeros(0, np.int64)
                        for q in range(parent_level.nboxes)]
             lev -= 1
+        # O11 -- top block A~_SS = Y_S pinv(Omega_S)
+        S = np.concatenate(act) if act else np.zeros(0, np.int64)
+        fac.S = S
+        if S.shape[0] > 0:
+            if S.shape[0] + l > p:
+                raise RSRSError("samples", f"top block |S| = {S.shape[0]} needs p >= |S| + l = {S.shape[0] + l}")
+            fac.A_SS = Y[S] @ pinv_right(Om[S])
+            fac.lu_SS = sla.lu_factor(fac.A_SS)
+        else:
+            fac.A_SS = np.zeros((0, 0), dtype=dt)
     finally:
         if pool is not None:
             pool.shutdown()
-    # O11 -- top block A~_SS = Y_S pinv(Omega_S)
-    S = np.concatenate(act) if act else np.zeros(0, np.int64)
-    fac.S = S
-    if S.shape[0] > 0:
-        if S.shape[0] + l > p:
-            raise RSRSError("samples", f"top block |S| = {S.shape[0]} needs p >= |S| + l = {S.shape[0] + l}")
-        fac.A_SS = Y[S] @ pinv_right(Om[S])
-        fac.lu_SS = sla.lu_factor(fac.A_SS)
-    else:
-        fac.A_SS = np.zeros((0, 0), dtype=dt)
+            blas_limit.restore_original_limits()
     return fac
 
 

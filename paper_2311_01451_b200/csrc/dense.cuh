@@ -54,10 +54,12 @@ __global__ void __launch_bounds__(256) id_kernel(BoxDev* __restrict__ boxes, con
   const S* H = ws + b.off_h;
   const int ldhg = b.ldn;
   // H = H_Y + H_Z = Y'' Y''^* + Z'' Z''^* (the two halves of S S^*, written by gemm_nt)
-  const S* H2 = hsame ? H : H + (i64)nb * ldhg;   // symmetric shortcut: Z'' = Y'', H = 2 H_Y
+  // symmetric shortcuts (hsame): 1 = Z'' = Y'' (A = A^*, Psi = Omega): H = 2 H_Y;
+  // 2 = Z'' = conj(Y'') (complex symmetric A = A^T, Psi = conj(Omega)): H = H_Y + conj(H_Y) = 2 Re(H_Y)
+  const S* H2 = hsame ? H : H + (i64)nb * ldhg;
   for (int idx = tid; idx < nb * nb; idx += 256) {
     const i64 g = (i64)(idx / nb) * ldhg + idx % nb;
-    Hs[(idx / nb) * ldh + idx % nb] = s_add(H[g], H2[g]);
+    Hs[(idx / nb) * ldh + idx % nb] = s_add(H[g], hsame == 2 ? s_conj(H2[g]) : H2[g]);
   }
   for (int i = tid; i < nb; i += 256) perm[i] = i;
   if (tid == 0) kfinal = nb;
@@ -417,17 +419,22 @@ __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ bo
     Xs[i * ldx + j] = XY[(i64)i * ldr + b.self_pos + redloc[j]];
   }
   if (sym) {
-    // symmetric shortcut: X_rr := (X_rr + X_rr^T) / 2, so G_L = G_U^T and the Z-side
-    // update equals the Y-side one (Z stays equal to Y)
+    // symmetric shortcuts: sym = 1 (A = A^*, Z = Y): X_rr := (X_rr + X_rr^*) / 2, so
+    // G_L = G_U^* and the Z-side update equals the Y-side one (Z stays equal to Y);
+    // sym = 2 (complex symmetric A = A^T, Z = conj(Y)): X_rr := (X_rr + X_rr^T) / 2, so
+    // G_L = G_U^T and the Z-side update is the conjugate of the Y-side one
     __syncthreads();
     for (int idx = tid; idx < nr * nr; idx += 256) {
       const int i = idx / nr, j = idx % nr;
       if (i < j) {
-        const S v = s_scale(s_add(Xs[i * ldx + j], Xs[j * ldx + i]), 0.5);
+        const S xji = sym == 2 ? Xs[j * ldx + i] : s_conj(Xs[j * ldx + i]);
+        const S v = s_scale(s_add(Xs[i * ldx + j], xji), 0.5);
         Xs[i * ldx + j] = v;
-        Xs[j * ldx + i] = v;
+        Xs[j * ldx + i] = sym == 2 ? v : s_conj(v);
       }
     }
+    if (sym == 1 && C)
+      for (int i = tid; i < nr; i += 256) Xs[i * ldx + i] = s_scale(s_add(Xs[i * ldx + i], s_conj(Xs[i * ldx + i])), 0.5);
   }
   __syncthreads();
   for (int idx = tid; idx < nr * nr; idx += 256) {
@@ -442,7 +449,8 @@ __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ bo
   }
   for (int idx = tid; idx < nr * nc; idx += 256) {
     const int j = idx / nr, i = idx % nr;
-    Xcr[(i64)j * ldn + i] = s_conj(XZ[(i64)i * ldr + cpos[j]]);   // X_cr = (X_Z)^*
+    // X_cr = (X_Z)^*; complex-symmetric shortcut: X_Z = conj(X_Y) (held as X_Y), X_cr = X_Y^T
+    Xcr[(i64)j * ldn + i] = sym == 2 ? XZ[(i64)i * ldr + cpos[j]] : s_conj(XZ[(i64)i * ldr + cpos[j]]);
   }
   __syncthreads();
   if (nr <= 64) {

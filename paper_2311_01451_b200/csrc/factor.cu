@@ -19,6 +19,7 @@
 // Real (RSRS_F64) and complex128 (RSRS_C128) share this driver: every offset
 // below is in SCALAR units and the kernels are instantiated for both types.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -199,6 +200,11 @@ void post(const char* name, cudaStream_t s, int64_t& launches) {
 // blocked Cholesky + u = B L^-* of nmat matrices (panel width cbw<C>), see chol.cuh
 template <bool C>
 void launch_chol_blocked(const CholDesc* d, int nmat, int rmax, int mext, cudaStream_t s, int64_t& launches) {
+  constexpr int ZMAX = 32767;          // gridDim.z = 2 * nmat <= 65535: split large batches
+  if (nmat > ZMAX) {
+    for (int i = 0; i < nmat; i += ZMAX) launch_chol_blocked<C>(d + i, std::min(ZMAX, nmat - i), rmax, mext, s, launches);
+    return;
+  }
   const int CB = rsrs::cbw<C>();
   const int TN = rsrs::tile_n<C>();
   const int np = (rmax + CB - 1) / CB;
@@ -222,6 +228,11 @@ void launch_chol_blocked(const CholDesc* d, int nmat, int rmax, int mext, cudaSt
 // W = u L^-1 (back substitution by panel-width column blocks, descending)
 template <bool C>
 void launch_back_blocked(const CholDesc* d, int nmat, int rmax, int mext, cudaStream_t s, int64_t& launches) {
+  constexpr int ZMAX = 65535;          // gridDim.z = nmat
+  if (nmat > ZMAX) {
+    for (int i = 0; i < nmat; i += ZMAX) launch_back_blocked<C>(d + i, std::min(ZMAX, nmat - i), rmax, mext, s, launches);
+    return;
+  }
   const int CB = rsrs::cbw<C>();
   const int TN = rsrs::tile_n<C>();
   const int np = (rmax + CB - 1) / CB;
@@ -387,6 +398,7 @@ struct Planner {
   bool profile = false;
   bool cplx = false;
   bool sym = false;    // symmetric shortcut: Psi = Omega, Z = Y, only the Y / Omega side runs
+  int symmode = 0;     // 1: A = A^* (Z = Y); 2: complex symmetric A = A^T (Psi = conj Omega, Z = conj Y)
   bool gram_blocks = true;   // level-wide near-field Gram blocks (gram.cuh; single rank)
   bool level_blocks = false; // the current level uses them (account_box counts the cross products only)
   bool push_updates = false; // push every L/U update (as the multi-GPU ranks do) instead of pulling
@@ -419,24 +431,31 @@ struct Planner {
     evpool.pop_back();
     return e;
   }
+  // Every kernel-class region is also an NVTX range named after the class, so that
+  // `ncu --nvtx --nvtx-include "<class>/"` captures exactly the launches the live
+  // CUDA-event profile attributes to it (bench.py roofline traffic).
   void tic(int cls) {
     cur_cls = cls;
     f->kc_launches[cls]++;
+    nvtxRangePushA(KC_NAMES[cls]);
     if (!profile) return;
     cur_a = ev();
     CK(cudaEventRecord(cur_a, s));
   }
   void toc() {
+    nvtxRangePop();
     if (!profile) return;
     cudaEvent_t b = ev();
     CK(cudaEventRecord(b, s));
     pend.push_back(Pend{cur_cls, cur_a, b});
   }
+  double lev_ms[RSRS_NUM_KERNEL_CLASSES] = {0};   // RSRS_TRACE=1 with opts.profile: per-level class split
   void flush_prof() {  // after a stream synchronize
     for (auto& p : pend) {
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, p.a, p.b));
       f->kc_ms[p.cls] += ms;
+      lev_ms[p.cls] += ms;
       evpool.push_back(p.a);
       evpool.push_back(p.b);
     }
@@ -466,6 +485,19 @@ struct Planner {
     account(KC_PROJ, 2 * (2 * nb * r * P), W8 * 2 * (nb * r + r * P + 2 * nb * P));
     account(KC_HGRAM, 2 * nb * (nb + 1) * P, W8 * (2 * nb * P + nb * nb));
     account(KC_ID, 2 * k * nb * nb + nr * k * k, W8 * (nb * nb + nr * k));
+    // SURVEY 8(d) per-box formulas (standard dense algorithms: Householder QR of the near
+    // field, projection, truncated CPQR, extraction, LU + G, E/F and L/U updates), for
+    // the fraction of peak the method's own work reaches independent of this build's
+    // reformulation (CholeskyQR, Gram blocks, padding)
+    {
+      const double w = P - r, sides = sym ? 1.0 : 2.0;
+      double fs = sides * (2 * P * r * r - (2.0 / 3) * r * r * r) + sides * (4 * P * r * nb - 2 * r * r * nb) +
+                  4 * (2 * w) * nb * k;
+      if (nr > 0)
+        fs += 2 * (2 * nr * k * r + nr * r * r) + (2.0 / 3) * nr * nr * nr + 2 * (2 * nc * nr * nr) +
+              sides * 2 * (2 * nr * k * P) + sides * 2 * (2 * nc * nr * P);
+      f->stats.flops_survey += F * fs;
+    }
     if (nr > 0) {
       account(KC_EF, 4 * 2 * nr * k * P, W8 * 2 * ((k * P + 2 * nr * P) + (nr * P + 2 * k * P)));
       account(KC_EXTRACT, 2 * (2 * nr * k * r + 2 * nr * nr * k) + 2 * nr * nr * nr,
@@ -1083,8 +1115,8 @@ struct Planner {
           {
             const size_t sm = (size_t)bi.max_nb * (bi.max_nb + 1) * sS + 3 * (size_t)bi.max_nb * 4 + 64;
             tic(KC_ID);
-            if (cplx) rsrs::id_kernel<true><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, ipool, gidx, atol * atol, p, l, sym, pull);
-            else rsrs::id_kernel<false><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, ipool, gidx, atol * atol, p, l, sym, pull);
+            if (cplx) rsrs::id_kernel<true><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, ipool, gidx, atol * atol, p, l, symmode, pull);
+            else rsrs::id_kernel<false><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, ipool, gidx, atol * atol, p, l, symmode, pull);
             post("id_kernel", s, launches);
             toc();
           }
@@ -1112,8 +1144,8 @@ struct Planner {
           {
             const size_t sm = 2 * (size_t)bi.max_nb * (bi.max_nb + 1) * sS + 3 * (size_t)bi.max_nb * 4 + 64;
             tic(KC_EXTRACT);
-            if (cplx) rsrs::extract_lu_kernel<true><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, sym);
-            else rsrs::extract_lu_kernel<false><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, sym);
+            if (cplx) rsrs::extract_lu_kernel<true><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, symmode);
+            else rsrs::extract_lu_kernel<false><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, symmode);
             post("extract_lu_kernel", s, launches);
             toc();
           }
@@ -1331,6 +1363,13 @@ struct Planner {
       }
       stream_sync(s);
       flush_prof();
+      if (g_trace && profile) {
+        fprintf(stderr, "[rsrs trace] level %d (%d boxes, %zu colour batches):", lev, nbox, binfo.size());
+        for (int c = 0; c < RSRS_NUM_KERNEL_CLASSES; ++c)
+          if (lev_ms[c] > 0) fprintf(stderr, " %s %.2f", KC_NAMES[c], lev_ms[c]);
+        fprintf(stderr, " ms\n");
+        for (double& v : lev_ms) v = 0;
+      }
       Y = nY; Z = nZ; Om = nO; Ps = nP; ld = nld;
       gidx = ng;
       cur = nxt;
@@ -1419,6 +1458,9 @@ struct Planner {
     for (int i = 0; i < nS; ++i) f->S_host[i] = tmp[i];
     f->stats.memory_scalars += (int64_t)nS * nS;
     const double n = nS;
+    // top block by the SURVEY 8(d) standard forms: QR of Omega_S^*, Y_S Omega_S^dagger, LU
+    f->stats.flops_survey += (cplx ? 4.0 : 1.0) * (2 * p * n * n - (2.0 / 3) * n * n * n + 2 * n * n * p +
+                                                  (2.0 / 3) * n * n * n);
     account(KC_MISC, (cplx ? 4.0 : 1.0) * (n * (n + 1) * p + 2 * n * n * p + n * n * n / 3 + 2 * n * n * n +
                                          2 * n * n * n / 3),
             sS * (2 * n * p + 3 * n * n));
@@ -1481,6 +1523,7 @@ static rsrs_status factor_impl(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, v
     P.cplx = f->cplx;
     P.SC = f->sc;
     P.sym = o.symmetric != 0;
+    P.symmode = o.symmetric == 0 ? 0 : (f->cplx ? 2 : 1);   // real: symmetric = Hermitian (Z = Y)
     P.gram_blocks = o.direct_gram == 0;
     P.push_updates = o.push_updates != 0;
     P.estimate = o.estimate_coupling != 0;
@@ -1526,8 +1569,11 @@ static rsrs_status check_args(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, vo
                               int64_t ld, const rsrs_opts* opts, rsrs_opts& o) {
   const bool symm = opts && opts->symmetric;
   if (!t || !Y || !Omega || (!symm && (!Z || !Psi))) return fail(RSRS_ERR_INVALID, "rsrs_factor: null argument");
-  if (symm && dt != RSRS_F64)
-    return fail(RSRS_ERR_INVALID, "rsrs_factor: the symmetric shortcut is for real symmetric operators (RSRS_F64)");
+  if (opts && (opts->symmetric < 0 || opts->symmetric > 2))
+    return fail(RSRS_ERR_INVALID, "rsrs_factor: opts.symmetric must be 0, 1 or 2");
+  if (symm && dt == RSRS_C128 && opts->symmetric != 2)
+    return fail(RSRS_ERR_INVALID, "rsrs_factor: complex128 supports the complex-symmetric shortcut only "
+                                  "(opts.symmetric = 2: A = A^T, Psi = conj(Omega))");
   if (p < 1 || ld < p || (ld & 1)) return fail(RSRS_ERR_INVALID, "rsrs_factor: need 1 <= p <= ld and ld even");
   if (dt != RSRS_F64 && dt != RSRS_C128) return fail(RSRS_ERR_INVALID, "rsrs_factor: unknown dtype");
   o = rsrs_opts{1e-6, 1.0, 1.0, 10, 2, 0, 1, nullptr, nullptr, 0, -1, 0, 0, 0, 0};

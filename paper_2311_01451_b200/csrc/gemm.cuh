@@ -78,7 +78,8 @@ RSRS_DI void nt_tile(const NTDesc& d, int m, int n, int K, int i0, int j0, doubl
   {
     const int sym = d.psym ? *d.psym : d.sym_rows;
     const int rb = i0 + wr * (TM / 2), cb = j0 + wc * 32;
-    wact = rb < m && cb < n && !(rb < sym && cb >= rb + TM / 2);
+    // (same condition as the tile-level skip: every row of the warp's band below sym_rows)
+    wact = rb < m && cb < n && !(rb + TM / 2 <= sym && cb >= rb + TM / 2);
   }
 
   const int nk = (K + GBK - 1) / GBK;

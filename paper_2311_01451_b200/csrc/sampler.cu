@@ -101,6 +101,117 @@ __global__ void __launch_bounds__(128) matvec_real_kernel(const double* __restri
   }
 }
 
+// Real kernels, wide tile: 64 rows x 128 columns per CTA (256 threads, 8 warps of
+// 32 x 32), X tiles double-buffered with cp.async.  The kernel values of a 64 x 32
+// A tile are evaluated once per 128 output columns (twice the reuse of the 64-wide
+// tile above: the log / rsqrt evaluations and the scattered point loads were the
+// bound), so Y = A Omega, Z = A Psi of c5 need ~half the evaluations.
+constexpr int WTN = 128;
+constexpr int WSB = WTN + 4;
+constexpr int WIDE_SMEM = (TM * SA + 2 * TK * WSB + TM * 3) * 8;
+
+__global__ void __launch_bounds__(256, 2) matvec_real_wide_kernel(const double* __restrict__ pts, int64_t N,
+                                                                  int64_t row0, int64_t nrows,
+                                                                  const double* __restrict__ X, int64_t ldx,
+                                                                  double* __restrict__ Y, int64_t ldy, int ncol,
+                                                                  int kind, double w) {
+  extern __shared__ __align__(16) double wsm[];
+  double* As = wsm;                       // [TM][SA]
+  double* Bs = As + TM * SA;              // [2][TK][WSB]
+  double* Pi = Bs + 2 * TK * WSB;         // [TM][3]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int wr = warp >> 2, wc = warp & 3;
+  const int64_t i0 = row0 + (int64_t)blockIdx.y * TM;
+  const int64_t iend = row0 + nrows;
+  const int j0 = blockIdx.x * WTN;
+  for (int t = tid; t < TM * 3; t += 256) {
+    const int64_t gi = i0 + t / 3;
+    Pi[t] = gi < iend ? pts[gi * 3 + t % 3] : 0.0;
+  }
+  // X tile loader: 32 rows x 128 columns = 2048 16-byte chunks, 8 per thread
+  auto load_b = [&](int st, int64_t k0) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int c = tid + 256 * q;
+      const int kk = c >> 6, jj = 2 * (c & 63);
+      const int64_t gk = k0 + kk;
+      const int j = j0 + jj;
+      const int nb = (gk < N && j < ncol) ? ((j + 1 < ncol) ? 16 : 8) : 0;
+      rsrs::cp_async16(&Bs[(st * TK + kk) * WSB + jj], nb ? (const void*)(X + gk * ldx + j) : (const void*)X, nb);
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
+  const int nk = (int)((N + TK - 1) / TK);
+  load_b(0, 0);
+  rsrs::cp_async_commit();
+  __syncthreads();
+  for (int kt = 0; kt < nk; ++kt) {
+    const int64_t k0 = (int64_t)kt * TK;
+    if (kt + 1 < nk) load_b((kt + 1) & 1, k0 + TK);
+    rsrs::cp_async_commit();
+    // kernel tile A[i0:i0+64, k0:k0+32]: a warp evaluates one row against 32 consecutive points
+    {
+      const int kk = lane;
+      const int64_t gk = k0 + kk;
+      double px = 0.0, py = 0.0, pz = 0.0;
+      if (gk < N) {
+        px = pts[gk * 3];
+        py = pts[gk * 3 + 1];
+        pz = pts[gk * 3 + 2];
+      }
+#pragma unroll 2
+      for (int ii = warp; ii < TM; ii += 8) {
+        const int64_t gi = i0 + ii;
+        double v = 0.0;
+        if (gi < iend && gk < N) {
+          if (gi == gk) {
+            v = 1.0;
+          } else {
+            const double dx = Pi[ii * 3] - px;
+            const double dy = Pi[ii * 3 + 1] - py;
+            const double dz = Pi[ii * 3 + 2] - pz;
+            v = kval(kind, sqrt(dx * dx + dy * dy + dz * dz), w);
+          }
+        }
+        As[ii * SA + kk] = v;
+      }
+    }
+    rsrs::cp_async_wait<1>();
+    __syncthreads();
+    const double* bs = Bs + (kt & 1) * TK * WSB;
+#pragma unroll
+    for (int kk = 0; kk < TK / 4; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) a[t] = As[(wr * 32 + t * 8 + gid) * SA + kk * 4 + tig];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) b[u] = bs[(kk * 4 + tig) * WSB + wc * 32 + u * 8 + gid];
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) rsrs::dmma884(acc[t][u][0], acc[t][u][1], a[t], b[u]);
+    }
+    __syncthreads();
+  }
+  rsrs::cp_async_wait<0>();
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int64_t i = i0 + wr * 32 + t * 8 + gid;
+    if (i >= iend) continue;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = j0 + wc * 32 + u * 8 + 2 * tig;
+      if (j < ncol) Y[(i - row0) * ldy + j] = acc[t][u][0];
+      if (j + 1 < ncol) Y[(i - row0) * ldy + j + 1] = acc[t][u][1];
+    }
+  }
+}
+
 // Complex operator (kind 2, config c4): A_ij = delta_ij + w (i/4) H0^(1)(kappa r)
 // = delta_ij + w (-Y0(kappa r) + i J0(kappa r)) / 4, complex symmetric, so
 // A^* = conj(A).  X, Y are complex128 (interleaved doubles).  Y = A X runs as
@@ -229,9 +340,17 @@ int rsrs_sample_matvec_rows(int kind, const double* pts, int64_t N, int64_t row0
                                                                        adjoint);
   } else {
     // the real kernels here are symmetric: A^* = A
-    dim3 grid((unsigned)((ncol + TN - 1) / TN), (unsigned)((nrows + TM - 1) / TM));
-    matvec_real_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(pts, N, row0, nrows, (const double*)X, ldx,
-                                                               (double*)Y, ldy, (int)ncol, kind, weight);
+    if ((ldx & 1) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0) {   // 16-byte aligned X rows
+      dim3 grid((unsigned)((ncol + WTN - 1) / WTN), (unsigned)((nrows + TM - 1) / TM));
+      cudaFuncSetAttribute(matvec_real_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, WIDE_SMEM);
+      matvec_real_wide_kernel<<<grid, 256, WIDE_SMEM, (cudaStream_t)stream>>>(pts, N, row0, nrows, (const double*)X,
+                                                                             ldx, (double*)Y, ldy, (int)ncol, kind,
+                                                                             weight);
+    } else {
+      dim3 grid((unsigned)((ncol + TN - 1) / TN), (unsigned)((nrows + TM - 1) / TM));
+      matvec_real_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(pts, N, row0, nrows, (const double*)X, ldx,
+                                                                 (double*)Y, ldy, (int)ncol, kind, weight);
+    }
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

@@ -59,7 +59,7 @@ class Stats(ctypes.Structure):
                 ("nlevels_compressed", ctypes.c_int), ("nsteps", ctypes.c_int64), ("top_size", ctypes.c_int64),
                 ("max_rank", ctypes.c_int64), ("memory_scalars", ctypes.c_int64), ("factor_ms", ctypes.c_double),
                 ("flops_model", ctypes.c_double), ("bytes_model", ctypes.c_double), ("launches", ctypes.c_int64),
-                ("solve_launches", ctypes.c_int64)]
+                ("solve_launches", ctypes.c_int64), ("flops_survey", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -146,6 +146,34 @@ def _ptr(t) -> int:
     if isinstance(t, np.ndarray):
         return t.ctypes.data
     return t.data_ptr()
+
+
+def _check_tensor(name, t, rows, min_cols=None, dtype=None, allow_1d=False):
+    """Argument validation the C ABI cannot do (it only sees a pointer and a leading dimension):
+    a CUDA tensor of the factor's dtype with `rows` rows, unit column stride, 16-byte aligned
+    rows (the kernels stage rows with 16-byte cp.async)."""
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"{name} has dtype {t.dtype}, expected {dtype}")
+    if t.dtype not in (torch.float64, torch.complex128):
+        raise ValueError(f"{name}: unsupported dtype {t.dtype} (float64 or complex128)")
+    if t.dim() == 1 and allow_1d:
+        if t.stride(0) != 1:
+            raise ValueError(f"{name}: a 1-D right-hand side must be contiguous")
+    elif t.dim() != 2:
+        raise ValueError(f"{name} must be 2-D (rows x columns)" + (" or 1-D" if allow_1d else ""))
+    elif t.stride(1) != 1:
+        raise ValueError(f"{name}: column stride must be 1 (row-major rows)")
+    if t.shape[0] != rows:
+        raise ValueError(f"{name} has {t.shape[0]} rows, expected {rows}")
+    if min_cols is not None and (t.dim() != 2 or t.shape[1] < min_cols):
+        raise ValueError(f"{name} needs at least {min_cols} columns")
+    if t.data_ptr() % 16:
+        raise ValueError(f"{name}: data pointer not 16-byte aligned")
+    if t.dim() == 2 and (t.stride(0) * t.element_size()) % 16:
+        raise ValueError(f"{name}: row stride not a multiple of 16 bytes")
 
 
 def _stream_ptr(stream) -> int | None:
@@ -243,9 +271,11 @@ class Tree:
 class Factorization:
     """Handle of rsrs_factor."""
 
-    def __init__(self, handle, tree: Tree):
+    def __init__(self, handle, tree: Tree, dtype=None):
         self._h = handle
         self.tree_L = tree.L
+        self.N = tree.N
+        self.dtype = dtype
 
     def stats(self) -> dict:
         st = Stats()
@@ -282,7 +312,9 @@ class Factorization:
         return out[:n.value]
 
     def solve(self, B, stream=None):
-        """B <- K^-1 B in place; B: CUDA float64 tensor (N,) or (N, nrhs) row-major, original order."""
+        """B <- K^-1 B in place; B: CUDA tensor of the factor's dtype, (N,) or (N, nrhs) row-major,
+        original order."""
+        _check_tensor("B", B, self.N, dtype=self.dtype, allow_1d=True)
         nrhs = 1 if B.dim() == 1 else B.shape[1]
         ldb = 1 if B.dim() == 1 else B.stride(0)
         _check(_lib.rsrs_solve(self._h, _ptr(B), ldb, nrhs, _stream_ptr(stream)))
@@ -290,6 +322,7 @@ class Factorization:
 
     def apply(self, X, stream=None):
         """X <- K X in place (same layout as solve)."""
+        _check_tensor("X", X, self.N, dtype=self.dtype, allow_1d=True)
         nrhs = 1 if X.dim() == 1 else X.shape[1]
         ldx = 1 if X.dim() == 1 else X.stride(0)
         _check(_lib.rsrs_apply(self._h, _ptr(X), ldx, nrhs, _stream_ptr(stream)))
@@ -321,24 +354,32 @@ def factor(tree: Tree, Y, Z, Omega, Psi, p: int, eps: float = 1e-6, level_growth
     float64 tensors -> RSRS_F64, complex128 -> RSRS_C128 (ld in elements).
     Multi-GPU (nranks > 1): this rank's rows only (Tree.partition()) and the
     NcclComm of this rank in `comm`.
-    symmetric=True: the f2 shortcut for real symmetric A (Psi = Omega, Z = Y); Z and Psi may be None."""
-    ld = Y.stride(0)
-    code = _dtype_code(Y)
+    symmetric=True: the f2 shortcut -- float64: real symmetric A (Psi = Omega, Z = Y); complex128: complex
+    symmetric A = A^T (Psi = conj(Omega), Z = conj(Y)); Z and Psi may be None."""
+    rows = tree.N
+    if nranks > 1:
+        first, _ = tree.partition(nranks, gather_level, top_level)
+        rows = int(first[rank + 1] - first[rank])
     if symmetric:
         Z, Psi = Y, Omega
-    for t in (Z, Omega, Psi):
-        if t.stride(0) != ld or t.dtype != Y.dtype:
-            raise ValueError("Y, Z, Omega, Psi must share dtype and leading dimension")
+    _check_tensor("Y", Y, rows, min_cols=p)
+    ld = Y.stride(0)
+    code = _dtype_code(Y)
+    for nm, t in (("Z", Z), ("Omega", Omega), ("Psi", Psi)):
+        _check_tensor(nm, t, rows, min_cols=p, dtype=Y.dtype)
+        if t.stride(0) != ld:
+            raise ValueError("Y, Z, Omega, Psi must share the leading dimension")
     if dtype is not None and dtype != code:
         raise ValueError("dtype does not match the tensors")
     dtype = code
+    symmode = 0 if not symmetric else (2 if code == RSRS_C128 else 1)
     o = Opts(eps, level_growth, id_scale, oversample, top_level, int(rank), int(nranks),
              None if comm is None else comm.handle, _stream_ptr(stream), int(profile), int(gather_level),
-             int(symmetric), int(direct_gram), int(push_updates), int(estimate_coupling))
+             symmode, int(direct_gram), int(push_updates), int(estimate_coupling))
     h = _vp()
     _check(_lib.rsrs_factor(tree.handle, dtype, int(p), _ptr(Y), _ptr(Z), _ptr(Omega), _ptr(Psi), int(ld),
                             ctypes.byref(o), ctypes.byref(h)))
-    return Factorization(h, tree)
+    return Factorization(h, tree, Y.dtype)
 
 
 class NcclComm:
@@ -374,20 +415,26 @@ def factor_emulated(tree: Tree, G: int, Y, Z, Omega, Psi, p: int, eps: float = 1
                     symmetric: bool = False, push_updates: bool = False) -> list:
     """G-rank run of the multi-GPU sweep emulated on this GPU (one host thread per rank);
     full tree-ordered Y, Z, Omega, Psi (overwritten).  Returns the G rank factorizations."""
-    ld = Y.stride(0)
-    code = _dtype_code(Y)
     if symmetric:
         Z, Psi = Y, Omega
+    for nm, t in (("Y", Y), ("Z", Z), ("Omega", Omega), ("Psi", Psi)):
+        _check_tensor(nm, t, tree.N, min_cols=p, dtype=Y.dtype)
+        if t.stride(0) != Y.stride(0):
+            raise ValueError("Y, Z, Omega, Psi must share the leading dimension")
+    ld = Y.stride(0)
+    code = _dtype_code(Y)
+    symmode = 0 if not symmetric else (2 if code == RSRS_C128 else 1)
     o = Opts(eps, level_growth, id_scale, oversample, top_level, 0, G, None, None, 0, int(gather_level),
-             int(symmetric), 0, int(push_updates), 0)
+             symmode, 0, int(push_updates), 0)
     hs = (_vp * G)()
     _check(_lib.rsrs_factor_emulated(tree.handle, code, int(p), int(G), _ptr(Y), _ptr(Z), _ptr(Omega), _ptr(Psi),
                                      int(ld), ctypes.byref(o), hs))
-    return [Factorization(_vp(hs[q]), tree) for q in range(G)]
+    return [Factorization(_vp(hs[q]), tree, Y.dtype) for q in range(G)]
 
 
 def _emul_sweep(fn, fs, B):
     G = len(fs)
+    _check_tensor("B", B, fs[0].N, dtype=fs[0].dtype, allow_1d=True)
     hs = (_vp * G)(*[f._h.value for f in fs])
     nrhs = 1 if B.dim() == 1 else B.shape[1]
     ld = 1 if B.dim() == 1 else B.stride(0)

@@ -106,14 +106,67 @@ def test_symmetric_shortcut_emulated_ranks_bit_exact():
     assert np.array_equal(xg.cpu().numpy(), x1.cpu().numpy())
 
 
-def test_symmetric_shortcut_rejects_complex():
+def test_complex_symmetric_shortcut_parity():
+    """c4's complex-symmetric Helmholtz operator (A = A^T, complex128) on the c1-size grid:
+    Psi = conj(Omega) => Z = A^* Psi = conj(A Omega) = conj(Y), so only the Y / Omega side
+    runs (rsrs_opts.symmetric = 2).  Reference: the oracle's general two-sketch algorithm on
+    the same inputs (Y, Z = conj(Y), Omega, Psi = conj(Omega)), north_star bar."""
     import torch
 
     import paper_2311_01451_b200 as R
+    cfg = W.CONFIGS["c4"].scaled(64)
+    X = W.points(cfg)
+    A = W.dense_matrix(cfg, X)
+    assert np.allclose(A, A.T) and not np.allclose(A, A.conj().T)
+    Om, _ = W.omega_psi(cfg)
+    Y = A @ Om
+    b = W.rhs(cfg)
+    t = R.Tree(X, cfg.leaf, *cfg.root())
+    perm = t.perm()
+    Yd = torch.from_numpy(np.ascontiguousarray(Y[perm])).cuda()
+    Od = torch.from_numpy(np.ascontiguousarray(Om[perm])).cuda()
+    f = R.factor(t, Yd, None, Od, None, p=cfg.p, eps=cfg.eps, level_growth=cfg.g, id_scale=cfg.c_id,
+                 oversample=cfg.l, symmetric=True)
+    to = O.build_tree(X, cfg.leaf, *cfg.root())
+    P = to.perm
+    Yt, Ot = Y[P], Om[P]
+    fo = O.factor(to, Yt, Yt.conj(), Ot, Ot.conj(), cfg.eps, c_id=cfg.c_id, g=cfg.g, l=cfg.l)
+    x_or = O.solve(fo, b)
+    xd = torch.from_numpy(b.copy()).cuda()
+    f.solve(xd)
+    x = xd.cpu().numpy()
+    eps = cfg.eps
+    assert np.linalg.norm(x - x_or) / np.linalg.norm(x_or) <= 10 * eps
+    assert np.linalg.norm(A @ x - b) / np.linalg.norm(b) <= 10 * eps
+    assert np.linalg.norm(A @ x_or - b) / np.linalg.norm(b) <= 10 * eps
+    for lev in range(to.L, 1, -1):
+        nb = len(to.levels[lev].keys)
+        kg = f.ranks(lev, nb)
+        for bx in range(nb):
+            if fo.nb.get((lev, bx), 0) > 0:
+                assert abs(int(kg[bx]) - int(fo.ranks[(lev, bx)])) <= 2
+    v = W.gaussian(X.shape[0], 3, 9, True)
+    vd = torch.from_numpy(v.copy()).cuda()
+    f.apply(vd)
+    assert np.linalg.norm(vd.cpu().numpy() - A @ v) / np.linalg.norm(A @ v) <= 10 * eps
+    f.solve(vd)
+    assert np.linalg.norm(vd.cpu().numpy() - v) / np.linalg.norm(v) <= 1e-11
+
+
+def test_symmetric_shortcut_rejects_hermitian_complex():
+    """complex128 supports only the complex-symmetric form (opts.symmetric = 2) at the C ABI."""
+    import ctypes
+
+    import torch
+
+    import paper_2311_01451_b200 as R
+    from paper_2311_01451_b200 import rsrs as RR
     cfg = W.CONFIGS["c4"].scaled(32)
     X = W.points(cfg)
     t = R.Tree(X, cfg.leaf, *cfg.root())
     Y = torch.zeros((X.shape[0], 64), dtype=torch.complex128, device="cuda")
-    with pytest.raises(R.RSRSError) as e:
-        R.factor(t, Y, None, Y.clone(), None, p=64, symmetric=True)
-    assert e.value.status == 1
+    o = RR.Opts(1e-6, 1.0, 1.0, 10, 2, 0, 1, None, None, 0, -1, 1, 0, 0, 0)
+    h = ctypes.c_void_p()
+    st = RR._lib.rsrs_factor(t.handle, RR.RSRS_C128, 64, Y.data_ptr(), None, Y.data_ptr(), None, 64,
+                             ctypes.byref(o), ctypes.byref(h))
+    assert st == 1

@@ -331,7 +331,9 @@ def test_colour_parallel_oracle_is_bit_identical():
     """workers > 1 runs the boxes of one colour concurrently (their near sets are disjoint,
     DESIGN.md R10): every stored factor and the top block equal the sequential run bit for bit."""
     cfg, X, t, A, At, Y, Z, Om, Ps = small_problem(kernel="helm2d")
-    f1 = O.factor(t, Y, Z, Om, Ps, eps=1e-6, g=2.0)
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=1):        # the workers run one BLAS thread each
+        f1 = O.factor(t, Y, Z, Om, Ps, eps=1e-6, g=2.0)
     f4 = O.factor(t, Y, Z, Om, Ps, eps=1e-6, g=2.0, workers=4)
     assert len(f1.steps) == len(f4.steps) > 0
     for a, c in zip(f1.steps, f4.steps):
