@@ -82,6 +82,18 @@ typedef struct {
   int estimate_coupling; /* 1: after each box's elimination, estimate |A~(r, f)|_F and |A~(f, r)|_F by
                           block nullification of its redundant sample rows (PAPER.md:1232-1235,
                           SURVEY 8(f) f1); read them with rsrs_factor_coupling */
+  double noise_factor; /* theta > 0: noise-aware tolerance (reading R17) instead of
+                          the fixed schedule: the estimator runs on every box, nu(l) = median over the boxes
+                          eliminated on level l of max(est_Y, est_Z) / sqrt(|r_b|), and
+                          atol(L) = id_scale * eps, atol(l-1) = max(atol(l), theta * nu(l)); level_growth is
+                          ignored.  0 (default): atol(l) = id_scale * eps * level_growth^(L-l).
+                          Single rank only (RSRS_ERR_INVALID with nranks > 1). */
+  int triangular;      /* 1: triangular output form of the Remark PAPER.md:577-611 for a
+                          real symmetric positive definite A (needs RSRS_F64 and opts.symmetric):
+                          X_rr (symmetrised) = C C^T by Cholesky, stored C, C^-1 and M_U = C^-1 X_rc
+                          instead of X_rr, G_L, G_U; K = V_1..V_n A~ W_n..W_1 with V = E [C 0; M_U^T I],
+                          W = [C^T M_U; 0 I] F and identity blocks in the middle.  RSRS_ERR_SINGULAR if
+                          some X_rr is not positive definite. */
 } rsrs_opts;
 
 /* Statistics of a factorization (Table 1). */
@@ -204,6 +216,10 @@ rsrs_status rsrs_factor_ranks(rsrs_factorization f, int level, int32_t* k, int64
  * indices but r_b), -1 for boxes with nothing eliminated; cap >= 2 * nboxes.
  * RSRS_ERR_STATE if the factorization ran without the estimator. */
 rsrs_status rsrs_factor_coupling(rsrs_factorization f, int level, double* est, int64_t cap);
+
+/* ID tolerance atol(level) the factorization used on a compressed level (0 otherwise):
+ * the fixed schedule or the noise-aware one (rsrs_opts.noise_factor). */
+rsrs_status rsrs_factor_atol(rsrs_factorization f, int level, double* atol);
 
 /* Final skeleton set S (tree positions, host int64, ascending) and its size. */
 rsrs_status rsrs_factor_top(rsrs_factorization f, int64_t* S, int64_t cap, int64_t* size);

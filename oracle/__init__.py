@@ -18,4 +18,5 @@ the +-2 rank and 10 eps solution tolerances); see DESIGN.md.
 """
 from .tree import build_tree, Tree, Level, morton_encode, morton_decode  # noqa: F401
 from .rsrs import (factor, solve, apply, Factorization, Step, RSRSError,  # noqa: F401
-                   null_basis, pinv_right, row_id, atol_schedule, coupling_estimate)
+                   null_basis, pinv_right, row_id, atol_schedule, coupling_estimate,
+                   noise_level, noise_aware_atol)

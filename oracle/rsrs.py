@@ -131,6 +131,10 @@ class Step:
     X_rr: np.ndarray      # |red| x |red|
     lu: tuple             # scipy lu_factor(X_rr)
     xrr_mismatch: float = 0.0   # ||X_rr^Y - X_rr^Z|| / ||X_rr^Y|| (SURVEY c.2 #9 diagnostic)
+    # triangular form (Remark PAPER.md:577-611): X_rr = C C^* (Cholesky), M_L = X_cr C^-*, M_U = C^-1 X_rc
+    C: np.ndarray | None = None
+    M_L: np.ndarray | None = None
+    M_U: np.ndarray | None = None
 
 
 @dataclass
@@ -149,18 +153,42 @@ class Factorization:
     xrr_mismatch: list = field(default_factory=list)
     coupling: dict = field(default_factory=dict)  # (level, box) -> (est of |A~_{r,f}|_F, est of |A~_{f,r}|_F)
     dtype: object = np.float64
+    triangular: bool = False          # factors stored in the triangular form (Remark PAPER.md:577-611)
 
     def memory(self) -> int:
-        """Stored scalars (Table 1 'M')."""
+        """Stored scalars (Table 1 'M').  Triangular form: T, C (triangle), M_L, M_U."""
         m = 0
         for s in self.steps:
-            m += s.T.size + s.G_L.size + s.G_U.size + s.X_rr.size
+            if self.triangular:
+                nr = len(s.red)
+                m += s.T.size + nr * (nr + 1) // 2 + s.M_L.size + s.M_U.size
+            else:
+                m += s.T.size + s.G_L.size + s.G_U.size + s.X_rr.size
         return m + self.A_SS.size
 
 
 def atol_schedule(eps: float, c_id: float, g: float, L: int, lev: int) -> float:
     """atol(l) = c_id * eps * g^(L - l): relaxed at every level."""
     return c_id * eps * g ** (L - lev)
+
+
+def noise_level(coupling: dict, reds: dict, lev: int) -> float:
+    """nu(l): median over the boxes eliminated on level l of the per-row residual coupling
+    max(|A~(r,f)|_F, |A~(f,r)|_F) / sqrt(|r|) -- the estimates of PAPER.md:1232-1235 ("estimate
+    the extent to which A~_{r,f} and A~_{f,r} deviate from desired compression tolerance ...
+    for every box").  0 if nothing was eliminated (reading R17)."""
+    v = sorted(max(e) / math.sqrt(reds[key]) for key, e in coupling.items() if key[0] == lev and reds.get(key))
+    if not v:
+        return 0.0
+    n = len(v)
+    return v[n // 2] if n % 2 else 0.5 * (v[n // 2 - 1] + v[n // 2])
+
+
+def noise_aware_atol(atol_prev: float, nu: float, theta: float) -> float:
+    """Noise-aware relaxation (reading R17): the next coarser level
+    never resolves below theta x the coupling the finer level left behind, and never tightens:
+    atol(l - 1) = max(atol(l), theta * nu(l)); atol(L) = c_id * eps."""
+    return max(atol_prev, theta * nu)
 
 
 def coupling_estimate(Y_r, Om_r):
@@ -182,7 +210,8 @@ def coupling_estimate(Y_r, Om_r):
 
 def factor(tree: Tree, Y, Z, Om, Psi, eps: float, c_id: float = 1.0, g: float = 1.0,
            l: int = 10, top_level: int = 2, on_step=None, max_boxes: int | None = None,
-           copy: bool = True, estimate_coupling: bool = False, workers: int = 1) -> Factorization:
+           copy: bool = True, estimate_coupling: bool = False, workers: int = 1,
+           noise_factor: float = 0.0, triangular: bool = False) -> Factorization:
     """RSRS factorization from samples in TREE order (N x p each).
 
     The inputs are copied (unless copy=False); `on_step(step, Y, Z, Om, Psi)`
@@ -197,7 +226,16 @@ def factor(tree: Tree, Y, Z, Om, Psi, eps: float, c_id: float = 1.0, g: float = 
     thread pool (LAPACK releases the GIL) gives bit-for-bit the result of the
     sequential canonical order (pinned by tests/test_oracle_rsrs.py).  Colours and
     levels stay strictly sequential.  Ignored when on_step or max_boxes is given.
+
+    `noise_factor` theta > 0 replaces the fixed schedule by the noise-aware one (f1):
+    the coupling estimator runs on every box and atol(l - 1) = max(atol(l), theta nu(l)).
+
+    `triangular` stores the triangular form of the Remark for spd A:
+    Cholesky X_rr = C C^*, M_L = X_cr C^-*, M_U = C^-1 X_rc; the sample
+    updates are unchanged (with X_rr's Hermitian part).
     """
+    if noise_factor > 0:
+        estimate_coupling = True
     if copy:
         Y = np.array(Y, copy=True)
         Z = np.array(Z, copy=True)
@@ -209,7 +247,7 @@ def factor(tree: Tree, Y, Z, Om, Psi, eps: float, c_id: float = 1.0, g: float = 
     L = tree.L
     steps = []
     fac = Factorization(N=N, p=p, steps=steps, S=None, A_SS=None, lu_SS=None,
-                        perm=tree.perm, dtype=dt)
+                        perm=tree.perm, dtype=dt, triangular=triangular)
     lv = tree.levels[L]
     act = [np.arange(lv.start[b], lv.start[b + 1], dtype=np.int64) for b in range(lv.nboxes)]
     pool = None
@@ -265,6 +303,19 @@ def factor(tree: Tree, Y, Z, Om, Psi, eps: float, c_id: float = 1.0, g: float = 
         X_rc = X_Y[:, pos_c]
         X_cr = X_Z[:, pos_c].conj().T
         mism = np.linalg.norm(X_rr - X_Z[:, pos_red].conj().T) / max(np.linalg.norm(X_rr), 1e-300)
+        Cf = M_L = M_U = None
+        if triangular:
+            # Remark PAPER.md:577-611: for spd A, A_11 = C_11 C_11^* and the elimination factors
+            # become [C 0; A_21 C^-* I] and [C^* C^-1 A_12; 0 I] (no block-diagonal middle).  X_rr
+            # from the samples is Hermitian only to the compression error: take its Hermitian
+            # part (reading R18).
+            X_rr = 0.5 * (X_rr + X_rr.conj().T)
+            try:
+                Cf = sla.cholesky(X_rr, lower=True)
+            except np.linalg.LinAlgError:
+                raise RSRSError("singular", f"level {lev} box {b}: X_rr not positive definite") from None
+            M_U = sla.solve_triangular(Cf, X_rc, lower=True)                  # C^-1 X_rc
+            M_L = sla.solve_triangular(Cf, X_cr.conj().T, lower=True).conj().T  # X_cr C^-*
         lu = sla.lu_factor(X_rr, check_finite=True)
         if np.min(np.abs(np.diag(lu[0]))) == 0.0:
             raise RSRSError("singular", f"level {lev} box {b}: X_rr singular")
@@ -281,9 +332,11 @@ def factor(tree: Tree, Y, Z, Om, Psi, eps: float, c_id: float = 1.0, g: float = 
         if estimate_coupling:
             cpl = (coupling_estimate(Y[red], Om[red]), coupling_estimate(Z[red], Psi[red]))
         st = Step(level=lev, box=b, skel=skel, red=red, c=c, T=T, G_L=G_L, G_U=G_U,
-                  X_rr=X_rr, lu=lu)
+                  X_rr=X_rr, lu=lu, C=Cf, M_L=M_L, M_U=M_U)
         st.xrr_mismatch = mism
         return nb, r, k, cpl, st
+
+    reds = {}            # (level, box) -> |r| of the boxes with a coupling estimate
 
     def record(lev, b, res):
         nb, r, k, cpl, st = res
@@ -295,6 +348,7 @@ def factor(tree: Tree, Y, Z, Om, Psi, eps: float, c_id: float = 1.0, g: float = 
             fac.xrr_mismatch.append(st.xrr_mismatch)
             if cpl is not None:
                 fac.coupling[(lev, b)] = cpl
+                reds[(lev, b)] = len(st.red)
             steps.append(st)
             act[b] = st.skel
 
@@ -302,7 +356,11 @@ def factor(tree: Tree, Y, Z, Om, Psi, eps: float, c_id: float = 1.0, g: float = 
         lev = L
         while lev >= top_level and lev >= 1:
             lv = tree.levels[lev]
-            atol = atol_schedule(eps, c_id, g, L, lev)
+            if noise_factor > 0:
+                atol = c_id * eps if lev == L else noise_aware_atol(
+                    fac.atol[lev + 1], noise_level(fac.coupling, reds, lev + 1), noise_factor)
+            else:
+                atol = atol_schedule(eps, c_id, g, L, lev)
             fac.atol[lev] = atol
             order = tree.canonical_order(lev)
             if pool is None:
@@ -361,9 +419,39 @@ def _from_tree(fac: Factorization, x):
     return out
 
 
+def _solve_triangular_form(fac: Factorization, x):
+    """K = V_1 .. V_n A~_SS W_n .. W_1 with V = E [C 0; M_L I], W = [C^* M_U; 0 I] F (Remark
+    PAPER.md:577-611): the eliminated blocks of the middle factor are identities."""
+    for s in fac.steps:                      # V_i^-1: E^-1, then [C 0; M_L I]^-1
+        x[s.red] -= s.T @ x[s.skel]
+        x[s.red] = sla.solve_triangular(s.C, x[s.red], lower=True)
+        x[s.c] -= s.M_L @ x[s.red]
+    if fac.S.shape[0]:
+        x[fac.S] = sla.lu_solve(fac.lu_SS, x[fac.S])
+    for s in reversed(fac.steps):            # W_i^-1: [C^* M_U; 0 I]^-1, then F^-1
+        x[s.red] = sla.solve_triangular(s.C, x[s.red] - s.M_U @ x[s.c], lower=True, trans="C")
+        x[s.skel] -= s.T.conj().T @ x[s.red]
+    return _from_tree(fac, x)
+
+
+def _apply_triangular_form(fac: Factorization, x):
+    for s in fac.steps:                      # W_i = [C^* M_U; 0 I] F
+        x[s.skel] += s.T.conj().T @ x[s.red]
+        x[s.red] = s.C.conj().T @ x[s.red] + s.M_U @ x[s.c]
+    if fac.S.shape[0]:
+        x[fac.S] = fac.A_SS @ x[fac.S]
+    for s in reversed(fac.steps):            # V_i = E [C 0; M_L I]
+        x[s.c] += s.M_L @ x[s.red]
+        x[s.red] = s.C @ x[s.red]
+        x[s.red] += s.T @ x[s.skel]
+    return _from_tree(fac, x)
+
+
 def solve(fac: Factorization, b) -> np.ndarray:
     """x = K^-1 b = W_1^-1 ... W_n^-1 A~_diag^-1 V_n^-1 ... V_1^-1 b (original order)."""
     x = _to_tree(fac, b)
+    if fac.triangular:
+        return _solve_triangular_form(fac, x)
     for s in fac.steps:                      # V_i^-1 = L_i^-1 E_i^-1
         x[s.red] -= s.T @ x[s.skel]
         x[s.c] -= s.G_L @ x[s.red]
@@ -380,6 +468,8 @@ def solve(fac: Factorization, b) -> np.ndarray:
 def apply(fac: Factorization, v) -> np.ndarray:
     """K v = V_1 ... V_n A~_diag W_n ... W_1 v (original order)."""
     x = _to_tree(fac, v)
+    if fac.triangular:
+        return _apply_triangular_form(fac, x)
     for s in fac.steps:                      # W_i = U_i F_i
         x[s.skel] += s.T.conj().T @ x[s.red]
         x[s.red] += s.G_U @ x[s.c]

@@ -347,7 +347,7 @@ __device__ bool gj_inverse_reg(const S* __restrict__ Xs, int ldx, int n, S* __re
 template <bool C>
 __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ boxes, double* __restrict__ wsd,
                                                          const int* __restrict__ iws,
-                                                         double* __restrict__ fpoold, int sym) {
+                                                         double* __restrict__ fpoold, int sym, int tri) {
   typedef typename ScalarOf<C>::T S;
   extern __shared__ __align__(16) double Xsd[];
   S* Xs = reinterpret_cast<S*>(Xsd);
@@ -453,6 +453,51 @@ __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ bo
     Xcr[(i64)j * ldn + i] = sym == 2 ? XZ[(i64)i * ldr + cpos[j]] : s_conj(XZ[(i64)i * ldr + cpos[j]]);
   }
   __syncthreads();
+  if (tri) {
+    // triangular form (Remark PAPER.md:577-611): X_rr (symmetrised above) = C C^T
+    // by a right-looking Cholesky in shared memory; C -> f_Xrr (apply), C^-1 -> f_Xinv (solve,
+    // and M_U = C^-1 X_rc by the G-stage GEMM).  Real symmetric shortcut only.
+    for (int c = 0; c < nr; ++c) {
+      const S d = Xs[c * ldx + c];
+      if (!(s_real(d) > 0.0)) {            // not positive definite
+        if (tid == 0) singular = 1;
+        break;
+      }
+      const double dc = sqrt(s_real(d));
+      __syncthreads();
+      for (int i = c + 1 + tid; i < nr; i += 256) Xs[i * ldx + c] = s_scale(Xs[i * ldx + c], 1.0 / dc);
+      if (tid == 0) Xs[c * ldx + c] = s_scale(s_one(S()), dc);
+      __syncthreads();
+      const int nt = nr - c - 1;
+      for (int idx = tid; idx < nt * nt; idx += 256) {
+        const int i = c + 1 + idx / nt, j = c + 1 + idx % nt;
+        if (j <= i) Xs[i * ldx + j] = s_sub(Xs[i * ldx + j], s_mul(Xs[i * ldx + c], s_conj(Xs[j * ldx + c])));
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    if (singular) {
+      if (tid == 0) b.status = ST_SINGULAR_XRR;
+      return;
+    }
+    // C^-1 (lower) column by column: C z = e_j
+    for (int j = tid; j < nr; j += 256) {
+      for (int i = 0; i < nr; ++i) {
+        S v = (i == j) ? s_one(S()) : zero;
+        for (int q = j; q < i; ++q) v = s_sub(v, s_mul(Xs[i * ldx + q], Is[q * ldx + j]));
+        Is[i * ldx + j] = (i < j) ? zero : s_div(v, Xs[i * ldx + i]);
+      }
+    }
+    __syncthreads();
+    S* Cf = fpool + b.f_Xrr;
+    S* Ci = fpool + b.f_Xinv;
+    for (int idx = tid; idx < nr * nr; idx += 256) {
+      const int i = idx / nr, j = idx % nr;
+      Cf[(i64)i * ldn + j] = j <= i ? Xs[i * ldx + j] : zero;
+      Ci[(i64)i * ldn + j] = Is[i * ldx + j];
+    }
+    return;
+  }
   if (nr <= 64) {
     // 4-5. X_rr^-1 by register Gauss-Jordan (the LU factors themselves are not stored)
     __shared__ S gj_col[2 * 64];

@@ -27,6 +27,8 @@ struct DescParams {
   NNDesc* upd;
   NNDesc* pullD;                 // [Y, Z] per box (pull mode)
   CholDesc* chol;
+  int tri;                       // triangular form (f4): g[2q] = M_U = C^-1 X_rc, g[2q+1] empty,
+  NNDesc* g2;                    //   g2[q] = G_L = M_U^T C^-1 (a second launch: it reads M_U)
 };
 
 __global__ void make_desc_kernel(const DescParams P) {
@@ -140,6 +142,17 @@ __global__ void make_desc_kernel(const DescParams P) {
     gl.A = P.dws + SC * x.off_xcr; gl.lda = ldn; gl.B = P.fpool + SC * x.f_Xinv; gl.rowB = nullptr; gl.ldb = ldn;
     gl.D = P.fpool + SC * x.f_GL; gl.ldd = ldn; gl.Cin = nullptr; gl.m = rm; gl.n = nb; gl.K = nb;
     gl.alpha = 1.0; gl.beta = 0.0; gl.pm = &dx->nc; gl.pn = &dx->nr; gl.pK = &dx->nr;
+    if (P.tri) {
+      // f_Xinv holds C^-1, so gu computes M_U = C^-1 X_rc (stored in f_GU for the solve);
+      // G_L = X_cr X_rr^-1 = M_U^T C^-1 (real symmetric: X_cr = X_rc^T) for the L/U updates
+      NNDesc g2{};
+      g2.A = P.fpool + SC * x.f_GU; g2.lda = ldr; g2.transA = 1;
+      g2.B = P.fpool + SC * x.f_Xinv; g2.rowB = nullptr; g2.ldb = ldn;
+      g2.D = P.fpool + SC * x.f_GL; g2.ldd = ldn; g2.Cin = nullptr; g2.m = rm; g2.n = nb; g2.K = nb;
+      g2.alpha = 1.0; g2.beta = 0.0; g2.pm = &dx->nc; g2.pn = &dx->nr; g2.pK = &dx->nr;
+      P.g2[q] = g2;
+      gl = NNDesc{};          // empty (m = 0)
+    }
     o[1] = gl;
   }
   // ---- L/U updates

@@ -141,6 +141,10 @@ void init_kernels() {
   set_smem(rsrs::gemm_nn_kernel_c<32>, rsrs::NN_SMEM);
   set_smem_both<false>();
   set_smem_both<true>();
+  set_smem(rsrs::solve_fwd_tri_kernel, -1);
+  set_smem(rsrs::solve_bwd_tri_kernel, -1);
+  set_smem(rsrs::apply_fwd_tri_kernel, -1);
+  set_smem(rsrs::apply_bwd_tri_kernel, -1);
   done = true;
 }
 
@@ -335,6 +339,7 @@ struct Batch {
   double* fpool = nullptr;         // the level's factor pools
   int* ipool = nullptr;
   int max_nb = 0, max_r = 0;
+  bool tri = false;                // factors in the triangular form (C, C^-1, M_U)
 };
 
 struct rsrs_factor_s {
@@ -347,6 +352,7 @@ struct rsrs_factor_s {
   std::vector<std::unique_ptr<DBuf>> keep;        // factor-lifetime device buffers
   std::vector<std::vector<int32_t>> ranks;        // [level][box] (-1 empty)
   std::vector<std::vector<double>> coupling;      // [level][2 box + side] coupling estimates (-1: none)
+  std::vector<double> atol;                       // [level] ID tolerance used (0: level not compressed)
   int nS = 0;
   int ldS = 0;
   int* d_S = nullptr;                             // tree positions of S
@@ -399,10 +405,13 @@ struct Planner {
   bool cplx = false;
   bool sym = false;    // symmetric shortcut: Psi = Omega, Z = Y, only the Y / Omega side runs
   int symmode = 0;     // 1: A = A^* (Z = Y); 2: complex symmetric A = A^T (Psi = conj Omega, Z = conj Y)
+  bool tri = false;    // triangular form (Remark PAPER.md:577-611): Cholesky X_rr = C C^T
   bool gram_blocks = true;   // level-wide near-field Gram blocks (gram.cuh; single rank)
   bool level_blocks = false; // the current level uses them (account_box counts the cross products only)
   bool push_updates = false; // push every L/U update (as the multi-GPU ranks do) instead of pulling
   bool estimate = false;     // per-box coupling estimator
+  double theta = 0.0;        // > 0: noise-aware tolerance atol(l-1) = max(atol(l), theta nu(l)) (f1, DESIGN R17)
+  double atol_next = 0.0;    // noise-aware schedule: tolerance of the next (coarser) level
   int SC = 1;          // doubles per scalar (1 real, 2 complex); all offsets below are in scalars
   std::vector<cudaEvent_t> evpool;
   struct Pend {
@@ -625,6 +634,7 @@ struct Planner {
     const CholDesc* Echol = nullptr;
     const NNDesc* Eproj = nullptr;
     f->ranks.assign(L + 1, std::vector<int32_t>());
+    f->atol.assign(L + 1, 0.0);
     f->coupling.assign(L + 1, std::vector<double>());
     int ncol = 1;
     for (int i = 0; i < T.d; ++i) ncol *= 3;
@@ -638,7 +648,8 @@ struct Planner {
       };
       const rsrs::TreeLevel& lv = T.levels[lev];
       const int nbox = (int)lv.nboxes;
-      const double atol = cid * eps * std::pow(g, (double)(L - lev));
+      const double atol = theta > 0 ? (lev == L ? cid * eps : atol_next) : cid * eps * std::pow(g, (double)(L - lev));
+      f->atol[lev] = atol;
       const bool dist = R > 1 && lev > part.gather_level;
       std::vector<int> own(nbox, 0);
       for (int b = 0; b < nbox; ++b) own[b] = part.owner(T, lev, b);
@@ -939,6 +950,7 @@ struct Planner {
       // (halo) are always pushed and returned with the halo
       const bool pull = !push_updates;
       const size_t o_pull = slot(sizeof(NNDesc) * nbx * nsd);
+      const size_t o_g2 = slot(sizeof(NNDesc) * (tri ? nbx : 1));
       descbuf.ensure(dsz + 16, s);
       char* dd = descbuf.as<char>();
       if (nbx) {
@@ -955,6 +967,8 @@ struct Planner {
         dp.chol = reinterpret_cast<CholDesc*>(dd + o_chol);
         dp.pull = pull;
         dp.pullD = reinterpret_cast<NNDesc*>(dd + o_pull);
+        dp.tri = tri;
+        dp.g2 = reinterpret_cast<NNDesc*>(dd + o_g2);
         rsrs::make_desc_kernel<<<(unsigned)((nbx + 127) / 128), 128, 0, s>>>(dp);
         post("make_desc_kernel", s, launches);
       }
@@ -966,6 +980,7 @@ struct Planner {
       const NNDesc* Dupd = reinterpret_cast<const NNDesc*>(dd + o_upd);
       const CholDesc* Dchol = reinterpret_cast<const CholDesc*>(dd + o_chol);
       const NNDesc* Dpull = reinterpret_cast<const NNDesc*>(dd + o_pull);
+      const NNDesc* Dg2 = reinterpret_cast<const NNDesc*>(dd + o_g2);
       // coupling-estimator descriptors
       if (estimate) {
         const size_t o_ef = 0, o_eg = (sizeof(NNDesc) * nbx * nsd + 15) & ~size_t(15);
@@ -1144,13 +1159,14 @@ struct Planner {
           {
             const size_t sm = 2 * (size_t)bi.max_nb * (bi.max_nb + 1) * sS + 3 * (size_t)bi.max_nb * 4 + 64;
             tic(KC_EXTRACT);
-            if (cplx) rsrs::extract_lu_kernel<true><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, symmode);
-            else rsrs::extract_lu_kernel<false><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, symmode);
+            if (cplx) rsrs::extract_lu_kernel<true><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, symmode, tri);
+            else rsrs::extract_lu_kernel<false><<<n, 256, sm, s>>>(dbx, dws, diws, fpool, symmode, tri);
             post("extract_lu_kernel", s, launches);
             toc();
           }
           tic(KC_G);
           launch_nn(cplx, Dg + 2 * q0, 2 * n, bi.max_r, bi.max_r, s, launches);
+          if (tri) launch_nn(cplx, Dg2 + q0, n, bi.max_r, bi.max_nb, s, launches);   // G_L = M_U^T C^-1
           toc();
           tic(KC_UPD);
           launch_nn(cplx, Dupd + ns * q0, ns * n, bi.max_r, p, s, launches);
@@ -1243,7 +1259,9 @@ struct Planner {
         f->stats.max_rank = std::max<int64_t>(f->stats.max_rank, x.k);
         if (x.nr > 0) {
           f->stats.nsteps++;
-          f->stats.memory_scalars += (int64_t)x.nr * x.k + 2LL * x.nr * x.nc + (int64_t)x.nr * x.nr;
+          // block-diagonal form: T, G_L, G_U, X_rr; triangular form: T, M_U (= M_L^T), C and C^-1 triangles
+          f->stats.memory_scalars += tri ? (int64_t)x.nr * x.k + (int64_t)x.nr * x.nc + (int64_t)x.nr * (x.nr + 1)
+                                         : (int64_t)x.nr * x.k + 2LL * x.nr * x.nc + (int64_t)x.nr * x.nr;
         }
         account_box(x.nb, x.r, x.k, p);
       }
@@ -1253,11 +1271,24 @@ struct Planner {
       }
       if (estimate) {
         f->coupling[lev].assign(2 * (size_t)nbox, -1.0);
+        std::vector<double> nu;
         for (const BoxDev& x : hb)
           if (x.nr > 0) {
             f->coupling[lev][2 * x.box] = x.est_y;
             f->coupling[lev][2 * x.box + 1] = x.est_z;
+            nu.push_back(std::max(x.est_y, x.est_z) / std::sqrt((double)x.nr));
           }
+        if (theta > 0) {
+          // nu(l) = median per-row residual coupling of the boxes eliminated on this level
+          // (oracle.noise_level), atol(l-1) = max(atol(l), theta nu(l))
+          double med = 0.0;
+          if (!nu.empty()) {
+            std::sort(nu.begin(), nu.end());
+            const size_t n = nu.size();
+            med = (n & 1) ? nu[n / 2] : 0.5 * (nu[n / 2 - 1] + nu[n / 2]);
+          }
+          atol_next = std::max(atol, theta * med);
+        }
       }
       for (const BInfo& bi : binfo) {
         Batch B;
@@ -1270,6 +1301,7 @@ struct Planner {
         B.ipool = ipool;
         B.max_nb = bi.max_nb;
         B.max_r = bi.max_r;
+        B.tri = tri;
         f->batches.push_back(std::move(B));
       }
       phase(4);
@@ -1524,9 +1556,11 @@ static rsrs_status factor_impl(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, v
     P.SC = f->sc;
     P.sym = o.symmetric != 0;
     P.symmode = o.symmetric == 0 ? 0 : (f->cplx ? 2 : 1);   // real: symmetric = Hermitian (Z = Y)
+    P.tri = o.triangular != 0;
     P.gram_blocks = o.direct_gram == 0;
     P.push_updates = o.push_updates != 0;
-    P.estimate = o.estimate_coupling != 0;
+    P.estimate = o.estimate_coupling != 0 || o.noise_factor > 0;
+    P.theta = o.noise_factor;
     P.comm = (comm && comm->nranks > 1) ? comm : nullptr;
     P.part = rsrs::make_partition(T, comm ? comm->nranks : 1, o.gather_level, o.top_level);
     P.run((double*)Y, (double*)Z, (double*)Omega, (double*)Psi, ld);
@@ -1576,8 +1610,16 @@ static rsrs_status check_args(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, vo
                                   "(opts.symmetric = 2: A = A^T, Psi = conj(Omega))");
   if (p < 1 || ld < p || (ld & 1)) return fail(RSRS_ERR_INVALID, "rsrs_factor: need 1 <= p <= ld and ld even");
   if (dt != RSRS_F64 && dt != RSRS_C128) return fail(RSRS_ERR_INVALID, "rsrs_factor: unknown dtype");
-  o = rsrs_opts{1e-6, 1.0, 1.0, 10, 2, 0, 1, nullptr, nullptr, 0, -1, 0, 0, 0, 0};
+  o = rsrs_opts{1e-6, 1.0, 1.0, 10, 2, 0, 1, nullptr, nullptr, 0, -1, 0, 0, 0, 0, 0.0, 0};
   if (opts) o = *opts;
+  if (o.triangular && (o.symmetric == 0 || dt != RSRS_F64))
+    return fail(RSRS_ERR_INVALID, "rsrs_factor: the triangular form needs a real symmetric positive definite "
+                                  "operator (RSRS_F64 with opts.symmetric)");
+  if (o.triangular && (o.estimate_coupling || o.noise_factor > 0))
+    return fail(RSRS_ERR_INVALID, "rsrs_factor: the coupling estimator is not available with the triangular form");
+  if (!(o.noise_factor >= 0)) return fail(RSRS_ERR_INVALID, "rsrs_factor: noise_factor must be >= 0");
+  if (o.noise_factor > 0 && o.nranks > 1)
+    return fail(RSRS_ERR_INVALID, "rsrs_factor: the noise-aware tolerance (noise_factor > 0) is single-rank");
   if (!(o.eps > 0) || !(o.level_growth > 0) || !(o.id_scale > 0) || o.oversample < 0 || o.top_level < 1 ||
       o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks)
     return fail(RSRS_ERR_INVALID, "rsrs_factor: invalid options");
@@ -1731,7 +1773,8 @@ static void run_sweep(rsrs_factorization f, double* x, int64_t nrhs, bool solve,
   if (solve) {
     for (const Batch& b : f->batches) {
       const size_t sm = sS * 2 * (b.max_nb + 2);
-      if (b.nbox) rsrs::solve_fwd_kernel<C><<<b.nbox, 256, sm, s>>>(b.d_boxes, b.fpool, b.ipool, x, nrhs, nr);
+      if (b.nbox && b.tri) rsrs::solve_fwd_tri_kernel<<<b.nbox, 256, sm, s>>>(b.d_boxes, b.fpool, b.ipool, x, nrhs, nr);
+      else if (b.nbox) rsrs::solve_fwd_kernel<C><<<b.nbox, 256, sm, s>>>(b.d_boxes, b.fpool, b.ipool, x, nrhs, nr);
       CK(cudaGetLastError());
       M.batch(b, 0);
     }
@@ -1741,15 +1784,19 @@ static void run_sweep(rsrs_factorization f, double* x, int64_t nrhs, bool solve,
     }
     M.list(f->d_S, f->nS);
     for (auto it = f->batches.rbegin(); it != f->batches.rend(); ++it) {
-      const size_t sm = sS * (it->max_r + it->max_nb + 4);
-      if (it->nbox) rsrs::solve_bwd_kernel<C><<<it->nbox, 256, sm, s>>>(it->d_boxes, it->fpool, it->ipool, x, nrhs, nr);
+      const size_t sm = sS * (it->max_r + 2 * it->max_nb + 4);
+      if (it->nbox && it->tri)
+        rsrs::solve_bwd_tri_kernel<<<it->nbox, 256, sm, s>>>(it->d_boxes, it->fpool, it->ipool, x, nrhs, nr);
+      else if (it->nbox)
+        rsrs::solve_bwd_kernel<C><<<it->nbox, 256, sm, s>>>(it->d_boxes, it->fpool, it->ipool, x, nrhs, nr);
       CK(cudaGetLastError());
       M.batch(*it, 1);
     }
   } else {
     for (const Batch& b : f->batches) {
       const size_t sm = sS * (b.max_r + 2 * b.max_nb + 4);
-      if (b.nbox) rsrs::apply_fwd_kernel<C><<<b.nbox, 256, sm, s>>>(b.d_boxes, b.fpool, b.ipool, x, nrhs, nr);
+      if (b.nbox && b.tri) rsrs::apply_fwd_tri_kernel<<<b.nbox, 256, sm, s>>>(b.d_boxes, b.fpool, b.ipool, x, nrhs, nr);
+      else if (b.nbox) rsrs::apply_fwd_kernel<C><<<b.nbox, 256, sm, s>>>(b.d_boxes, b.fpool, b.ipool, x, nrhs, nr);
       CK(cudaGetLastError());
       M.batch(b, 1);
     }
@@ -1759,8 +1806,11 @@ static void run_sweep(rsrs_factorization f, double* x, int64_t nrhs, bool solve,
     }
     M.list(f->d_S, f->nS);
     for (auto it = f->batches.rbegin(); it != f->batches.rend(); ++it) {
-      const size_t sm = sS * (2 * it->max_nb + 4);
-      if (it->nbox) rsrs::apply_bwd_kernel<C><<<it->nbox, 256, sm, s>>>(it->d_boxes, it->fpool, it->ipool, x, nrhs, nr);
+      const size_t sm = sS * (3 * it->max_nb + 4);
+      if (it->nbox && it->tri)
+        rsrs::apply_bwd_tri_kernel<<<it->nbox, 256, sm, s>>>(it->d_boxes, it->fpool, it->ipool, x, nrhs, nr);
+      else if (it->nbox)
+        rsrs::apply_bwd_kernel<C><<<it->nbox, 256, sm, s>>>(it->d_boxes, it->fpool, it->ipool, x, nrhs, nr);
       CK(cudaGetLastError());
       M.batch(*it, 0);
     }
@@ -1856,6 +1906,12 @@ rsrs_status rsrs_factor_coupling(rsrs_factorization f, int level, double* est, i
   if (v.empty()) return fail(RSRS_ERR_STATE, "rsrs_factor_coupling: factor without opts.estimate_coupling");
   if ((int64_t)v.size() > cap) return fail(RSRS_ERR_INVALID, "rsrs_factor_coupling: capacity too small");
   for (size_t i = 0; i < v.size(); ++i) est[i] = v[i];
+  return RSRS_OK;
+}
+
+rsrs_status rsrs_factor_atol(rsrs_factorization f, int level, double* atol) {
+  if (!f || !atol || level < 0 || level > f->L) return fail(RSRS_ERR_INVALID, "rsrs_factor_atol: invalid argument");
+  *atol = f->atol.empty() ? 0.0 : f->atol[level];
   return RSRS_OK;
 }
 

@@ -297,4 +297,181 @@ __global__ void permute_rows_kernel(const double* __restrict__ src, i64 lds, dou
   }
 }
 
+// ---------------------------------------------------------------------------
+// Triangular form (Remark PAPER.md:577-611), real symmetric spd:
+//   V = E [C 0; M_U^T I],  W = [C^T M_U; 0 I] F,  eliminated blocks of the middle factor = I.
+// Stored per box: T (f_T), C (f_Xrr, lower), C^-1 (f_Xinv, lower), M_U = C^-1 X_rc (f_GU).
+// ---------------------------------------------------------------------------
+// forward solve: x_r -= T x_s ; x_r <- C^-1 x_r ; x_c -= M_U^T x_r
+__global__ void __launch_bounds__(256) solve_fwd_tri_kernel(const BoxDev* __restrict__ boxes,
+                                                             const double* __restrict__ fpool,
+                                                             const int* __restrict__ ipool, double* __restrict__ x,
+                                                             i64 ldx, int nrhs) {
+  extern __shared__ __align__(16) double smd[];
+  const BoxDev b = boxes[blockIdx.x];
+  const int nr = b.nr, k = b.k, nc = b.nc;
+  if (nr <= 0) return;
+  const int ldn = b.ldn, ldr = b.ldr;
+  double* xs = smd;
+  double* xr = xs + k;
+  double* yr = xr + nr;
+  const int* red = ipool + b.f_red;
+  const int* skel = ipool + b.f_skel;
+  const int* cc = ipool + b.f_c;
+  const double* T = fpool + b.f_T;
+  const double* Ci = fpool + b.f_Xinv;
+  const double* MU = fpool + b.f_GU;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int col = 0; col < nrhs; ++col) {
+    for (int s = tid; s < k; s += blockDim.x) xs[s] = x[(i64)skel[s] * ldx + col];
+    __syncthreads();
+    for (int i = tid; i < nr; i += blockDim.x) {
+      double v = x[(i64)red[i] * ldx + col];
+      for (int s = 0; s < k; ++s) v -= T[(i64)i * ldn + s] * xs[s];
+      xr[i] = v;
+    }
+    __syncthreads();
+    for (int i = warp; i < nr; i += blockDim.x / 32) {       // y_r = C^-1 x_r (lower)
+      double v = 0.0;
+      for (int j = lane; j <= i; j += 32) v += Ci[(i64)i * ldn + j] * xr[j];
+      v = warp_sum(v);
+      if (lane == 0) {
+        yr[i] = v;
+        x[(i64)red[i] * ldx + col] = v;
+      }
+    }
+    __syncthreads();
+    for (int j = tid; j < nc; j += blockDim.x) {              // x_c -= M_U^T y_r
+      double v = 0.0;
+      for (int i = 0; i < nr; ++i) v += MU[(i64)i * ldr + j] * yr[i];
+      x[(i64)cc[j] * ldx + col] -= v;
+    }
+    __syncthreads();
+  }
+}
+
+// backward solve: x_r <- C^-T (x_r - M_U x_c) ; x_s -= T^T x_r
+__global__ void __launch_bounds__(256) solve_bwd_tri_kernel(const BoxDev* __restrict__ boxes,
+                                                             const double* __restrict__ fpool,
+                                                             const int* __restrict__ ipool, double* __restrict__ x,
+                                                             i64 ldx, int nrhs) {
+  extern __shared__ __align__(16) double smd[];
+  const BoxDev b = boxes[blockIdx.x];
+  const int nr = b.nr, k = b.k, nc = b.nc;
+  if (nr <= 0) return;
+  const int ldn = b.ldn, ldr = b.ldr;
+  double* xc = smd;
+  double* tr = xc + nc;
+  double* xr = tr + nr;
+  const int* red = ipool + b.f_red;
+  const int* skel = ipool + b.f_skel;
+  const int* cc = ipool + b.f_c;
+  const double* T = fpool + b.f_T;
+  const double* Ci = fpool + b.f_Xinv;
+  const double* MU = fpool + b.f_GU;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int col = 0; col < nrhs; ++col) {
+    for (int j = tid; j < nc; j += blockDim.x) xc[j] = x[(i64)cc[j] * ldx + col];
+    __syncthreads();
+    for (int i = warp; i < nr; i += blockDim.x / 32) {        // t_r = x_r - M_U x_c
+      double v = 0.0;
+      for (int j = lane; j < nc; j += 32) v += MU[(i64)i * ldr + j] * xc[j];
+      v = warp_sum(v);
+      if (lane == 0) tr[i] = x[(i64)red[i] * ldx + col] - v;
+    }
+    __syncthreads();
+    for (int i = tid; i < nr; i += blockDim.x) {              // x_r = C^-T t_r (upper)
+      double v = 0.0;
+      for (int m = i; m < nr; ++m) v += Ci[(i64)m * ldn + i] * tr[m];
+      xr[i] = v;
+      x[(i64)red[i] * ldx + col] = v;
+    }
+    __syncthreads();
+    for (int s = tid; s < k; s += blockDim.x) {               // x_s -= T^T x_r
+      double v = 0.0;
+      for (int i = 0; i < nr; ++i) v += T[(i64)i * ldn + s] * xr[i];
+      x[(i64)skel[s] * ldx + col] -= v;
+    }
+    __syncthreads();
+  }
+}
+
+// apply, forward half (W = [C^T M_U; 0 I] F): x_s += T^T x_r ; x_r <- C^T x_r + M_U x_c
+__global__ void __launch_bounds__(256) apply_fwd_tri_kernel(const BoxDev* __restrict__ boxes,
+                                                             const double* __restrict__ fpool,
+                                                             const int* __restrict__ ipool, double* __restrict__ x,
+                                                             i64 ldx, int nrhs) {
+  extern __shared__ __align__(16) double smd[];
+  const BoxDev b = boxes[blockIdx.x];
+  const int nr = b.nr, k = b.k, nc = b.nc;
+  if (nr <= 0) return;
+  const int ldn = b.ldn, ldr = b.ldr;
+  double* xc = smd;
+  double* xr = xc + nc;
+  const int* red = ipool + b.f_red;
+  const int* skel = ipool + b.f_skel;
+  const int* cc = ipool + b.f_c;
+  const double* T = fpool + b.f_T;
+  const double* Cf = fpool + b.f_Xrr;
+  const double* MU = fpool + b.f_GU;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int col = 0; col < nrhs; ++col) {
+    for (int i = tid; i < nr; i += blockDim.x) xr[i] = x[(i64)red[i] * ldx + col];
+    for (int j = tid; j < nc; j += blockDim.x) xc[j] = x[(i64)cc[j] * ldx + col];
+    __syncthreads();
+    for (int s = tid; s < k; s += blockDim.x) {
+      double v = 0.0;
+      for (int i = 0; i < nr; ++i) v += T[(i64)i * ldn + s] * xr[i];
+      x[(i64)skel[s] * ldx + col] += v;
+    }
+    for (int i = warp; i < nr; i += blockDim.x / 32) {
+      double v = 0.0;
+      for (int m = i + lane; m < nr; m += 32) v += Cf[(i64)m * ldn + i] * xr[m];
+      for (int j = lane; j < nc; j += 32) v += MU[(i64)i * ldr + j] * xc[j];
+      v = warp_sum(v);
+      if (lane == 0) x[(i64)red[i] * ldx + col] = v;
+    }
+    __syncthreads();
+  }
+}
+
+// apply, backward half (V = E [C 0; M_U^T I]): x_c += M_U^T x_r ; x_r <- C x_r ; x_r += T x_s
+__global__ void __launch_bounds__(256) apply_bwd_tri_kernel(const BoxDev* __restrict__ boxes,
+                                                             const double* __restrict__ fpool,
+                                                             const int* __restrict__ ipool, double* __restrict__ x,
+                                                             i64 ldx, int nrhs) {
+  extern __shared__ __align__(16) double smd[];
+  const BoxDev b = boxes[blockIdx.x];
+  const int nr = b.nr, k = b.k, nc = b.nc;
+  if (nr <= 0) return;
+  const int ldn = b.ldn, ldr = b.ldr;
+  double* xs = smd;
+  double* xr = xs + k;
+  const int* red = ipool + b.f_red;
+  const int* skel = ipool + b.f_skel;
+  const int* cc = ipool + b.f_c;
+  const double* T = fpool + b.f_T;
+  const double* Cf = fpool + b.f_Xrr;
+  const double* MU = fpool + b.f_GU;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int col = 0; col < nrhs; ++col) {
+    for (int i = tid; i < nr; i += blockDim.x) xr[i] = x[(i64)red[i] * ldx + col];
+    for (int s = tid; s < k; s += blockDim.x) xs[s] = x[(i64)skel[s] * ldx + col];
+    __syncthreads();
+    for (int j = tid; j < nc; j += blockDim.x) {
+      double v = 0.0;
+      for (int i = 0; i < nr; ++i) v += MU[(i64)i * ldr + j] * xr[i];
+      x[(i64)cc[j] * ldx + col] += v;
+    }
+    for (int i = warp; i < nr; i += blockDim.x / 32) {
+      double v = 0.0;
+      for (int j = lane; j <= i; j += 32) v += Cf[(i64)i * ldn + j] * xr[j];
+      for (int s = lane; s < k; s += 32) v += T[(i64)i * ldn + s] * xs[s];
+      v = warp_sum(v);
+      if (lane == 0) x[(i64)red[i] * ldx + col] = v;
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace rsrs

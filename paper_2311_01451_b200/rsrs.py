@@ -36,6 +36,7 @@ EXPORTS = [
     "rsrs_tree_partition", "rsrs_dist_owner", "rsrs_dist_halo_plan", "rsrs_dist_move_plan",
     "rsrs_comm_unique_id", "rsrs_comm_init", "rsrs_comm_destroy", "rsrs_comm_selftest",
     "rsrs_factor_emulated", "rsrs_solve_emulated", "rsrs_apply_emulated", "rsrs_factor_coupling",
+    "rsrs_factor_atol",
 ]
 
 
@@ -51,7 +52,8 @@ class Opts(ctypes.Structure):
                 ("nranks", ctypes.c_int), ("nccl_comm", ctypes.c_void_p), ("stream", ctypes.c_void_p),
                 ("profile", ctypes.c_int), ("gather_level", ctypes.c_int), ("symmetric", ctypes.c_int),
                 ("direct_gram", ctypes.c_int), ("push_updates", ctypes.c_int),
-                ("estimate_coupling", ctypes.c_int)]
+                ("estimate_coupling", ctypes.c_int), ("noise_factor", ctypes.c_double),
+                ("triangular", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):
@@ -84,6 +86,8 @@ _lib.rsrs_factor_ranks.argtypes = [_vp, _i32, _vp, _i64]
 _lib.rsrs_factor_top.argtypes = [_vp, _vp, _i64, ctypes.POINTER(_i64)]
 _lib.rsrs_factor_coupling.argtypes = [_vp, _i32, _vp, _i64]
 _lib.rsrs_factor_coupling.restype = ctypes.c_int
+_lib.rsrs_factor_atol.argtypes = [_vp, _i32, ctypes.POINTER(_d)]
+_lib.rsrs_factor_atol.restype = ctypes.c_int
 _lib.rsrs_factor_profile.argtypes = [_vp, _i32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(_d),
                                      ctypes.POINTER(_d), ctypes.POINTER(_d), ctypes.POINTER(_i64)]
 _lib.rsrs_factor_profile.restype = ctypes.c_int
@@ -304,6 +308,12 @@ class Factorization:
         _check(_lib.rsrs_factor_coupling(self._h, level, out.ctypes.data, out.shape[0]))
         return out[:2 * nboxes].reshape(nboxes, 2)
 
+    def atol(self, level: int) -> float:
+        """ID tolerance the factorization used on `level` (0 if not compressed)."""
+        v = _d()
+        _check(_lib.rsrs_factor_atol(self._h, level, ctypes.byref(v)))
+        return v.value
+
     def top(self) -> np.ndarray:
         n = _i64()
         _check(_lib.rsrs_factor_top(self._h, None, 0, ctypes.byref(n)))
@@ -348,12 +358,15 @@ def factor(tree: Tree, Y, Z, Omega, Psi, p: int, eps: float = 1e-6, level_growth
            id_scale: float = 1.0, oversample: int = 10, top_level: int = 2, stream=None,
            dtype: int | None = None, profile: bool = False, comm=None, rank: int = 0, nranks: int = 1,
            gather_level: int = -1, symmetric: bool = False, direct_gram: bool = False,
-           push_updates: bool = False, estimate_coupling: bool = False) -> Factorization:
+           push_updates: bool = False, estimate_coupling: bool = False,
+           noise_factor: float = 0.0, triangular: bool = False) -> Factorization:
     """rsrs_factor on CUDA tensors (N x ld, tree order); Y, Z, Omega, Psi are OVERWRITTEN.
 
     float64 tensors -> RSRS_F64, complex128 -> RSRS_C128 (ld in elements).
     Multi-GPU (nranks > 1): this rank's rows only (Tree.partition()) and the
     NcclComm of this rank in `comm`.
+    noise_factor > 0: noise-aware tolerance schedule (f1); triangular=True: the triangular output form for
+    real symmetric positive definite A (f4; needs symmetric=True).
     symmetric=True: the f2 shortcut -- float64: real symmetric A (Psi = Omega, Z = Y); complex128: complex
     symmetric A = A^T (Psi = conj(Omega), Z = conj(Y)); Z and Psi may be None."""
     rows = tree.N
@@ -375,7 +388,8 @@ def factor(tree: Tree, Y, Z, Omega, Psi, p: int, eps: float = 1e-6, level_growth
     symmode = 0 if not symmetric else (2 if code == RSRS_C128 else 1)
     o = Opts(eps, level_growth, id_scale, oversample, top_level, int(rank), int(nranks),
              None if comm is None else comm.handle, _stream_ptr(stream), int(profile), int(gather_level),
-             symmode, int(direct_gram), int(push_updates), int(estimate_coupling))
+             symmode, int(direct_gram), int(push_updates), int(estimate_coupling), float(noise_factor),
+             int(triangular))
     h = _vp()
     _check(_lib.rsrs_factor(tree.handle, dtype, int(p), _ptr(Y), _ptr(Z), _ptr(Omega), _ptr(Psi), int(ld),
                             ctypes.byref(o), ctypes.byref(h)))

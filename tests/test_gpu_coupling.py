@@ -53,3 +53,31 @@ def test_coupling_estimate_matches_oracle(name, cfg):
     for lev in range(L, 1, -1):
         nb = len(to.levels[lev].keys)
         assert np.array_equal(f.ranks(lev, nb), f2.ranks(lev, nb))
+
+
+@pytest.mark.parametrize("name,cfg", CASES[:2], ids=[c[0] for c in CASES[:2]])
+def test_noise_aware_tolerance_matches_oracle(name, cfg):
+    """Noise-aware schedule (rsrs_opts.noise_factor = theta = 4, R17):
+    atol(l-1) = max(atol(l), theta nu(l)) from the per-box coupling estimates.  GPU vs oracle:
+    the per-level tolerances agree (the medians come from estimates that agree to ~1e-2), and
+    the north_star parity bar holds for the resulting factorization."""
+    X, A, Y, Z, Om, Ps, b = dense_problem(cfg)
+    theta = 4.0
+    t, f = run_gpu(cfg, X, Y, Z, Om, Ps, cfg.root(), noise_factor=theta)
+    to = O.build_tree(X, cfg.leaf, *cfg.root())
+    P = to.perm
+    fo = O.factor(to, Y[P], Z[P], Om[P], Ps[P], cfg.eps, c_id=cfg.c_id, l=cfg.l, noise_factor=theta)
+    for lev, a in fo.atol.items():
+        assert abs(f.atol(lev) - a) <= 0.05 * a, (lev, f.atol(lev), a)
+    x_or = O.solve(fo, b)
+    from gpu_common import gpu_solve
+    x_g = gpu_solve(f, b)
+    eps = cfg.eps
+    assert np.linalg.norm(x_g - x_or) / np.linalg.norm(x_or) <= 10 * eps
+    assert np.linalg.norm(A @ x_g - b) / np.linalg.norm(b) <= 10 * eps
+    for lev in range(to.L, 1, -1):
+        nb = len(to.levels[lev].keys)
+        kg = f.ranks(lev, nb)
+        for bx in range(nb):
+            if fo.nb.get((lev, bx), 0) > 0:
+                assert abs(int(kg[bx]) - int(fo.ranks[(lev, bx)])) <= 2

@@ -392,3 +392,91 @@ def test_coupling_estimate_decreases_with_tolerance():
         f = O.factor(t, Y, Z, Om, Ps, eps=eps, estimate_coupling=True)
         worst.append(max(max(v) for k, v in f.coupling.items() if k[0] == t.L))
     assert worst[0] > worst[1] > worst[2]
+
+
+# ---------------------------------------------------------------------------
+# noise-aware tolerance (reading R17)
+# ---------------------------------------------------------------------------
+def test_noise_aware_schedule_zero_coupling_keeps_leaf_tolerance():
+    """Exactly block-diagonal operator: the estimates vanish, nu = 0, so every level keeps
+    atol(L) = c_id eps (the schedule never tightens and has nothing to relax for)."""
+    cfg, X, t, A, At, Y, Z, Om, Ps = small_problem()
+    Ab = _masked(At, t, 0)
+    f = O.factor(t, Ab @ Om, Ab.T @ Ps, Om, Ps, eps=1e-6, noise_factor=4.0)
+    assert set(f.atol.values()) == {1e-6}
+
+
+def test_noise_level_matches_tracked_operator():
+    """nu(l) (median per-row coupling of the eliminated boxes) from the randomized estimates
+    against the same median computed from the explicitly tracked operator A_g (within x3),
+    and the noise-aware schedule is monotone and reaches at least theta x the exact nu."""
+    cfg, X, t, A, At, Y, Z, Om, Ps = small_problem()
+    Ag = At.copy()
+    exact = {}
+
+    def on_step(s, Yc, Zc, Omc, Psc):
+        _apply_step_dense(Ag, s)
+        other = np.setdiff1d(np.arange(cfg.N), s.red)
+        exact[(s.level, s.box)] = max(np.linalg.norm(Ag[np.ix_(s.red, other)]),
+                                      np.linalg.norm(Ag[np.ix_(other, s.red)])) / math.sqrt(len(s.red))
+
+    theta = 4.0
+    f = O.factor(t, Y, Z, Om, Ps, eps=1e-6, on_step=on_step, noise_factor=theta)
+    reds = {(s.level, s.box): len(s.red) for s in f.steps}
+    levs = sorted(f.atol, reverse=True)
+    for lev in levs[:-1]:
+        ex = np.median([v for k, v in exact.items() if k[0] == lev])
+        est = O.noise_level(f.coupling, reds, lev)
+        assert ex / 3 <= est <= 3 * ex, (lev, ex, est)
+        assert f.atol[lev - 1] >= f.atol[lev]
+        assert f.atol[lev - 1] >= min(theta * ex / 3, f.atol[lev])
+    assert f.atol[t.L] == 1e-6
+
+
+def test_noise_aware_c1_against_dense_lu():
+    """c1 with the noise-aware schedule (theta = 4): solution vs LAPACK getrf/getrs within 10 eps."""
+    cfg = W.CONFIGS["c1"]
+    X = W.points(cfg)
+    t = O.build_tree(X, cfg.leaf, *cfg.root())
+    A = W.dense_matrix(cfg, X)
+    Om, Ps = W.omega_psi(cfg)
+    Y, Z = W.dense_samples(A, Om, Ps)
+    P = t.perm
+    f = O.factor(t, Y[P], Z[P], Om[P], Ps[P], cfg.eps, c_id=cfg.c_id, l=cfg.l, workers=os.cpu_count() or 1,
+                 noise_factor=4.0)
+    b = W.rhs(cfg)
+    x = O.solve(f, b)
+    xd = sla.lu_solve(sla.lu_factor(A), b)
+    assert np.linalg.norm(x - xd) / np.linalg.norm(xd) <= 10 * cfg.eps
+    assert f.atol[t.L] == cfg.c_id * cfg.eps and f.atol[t.L - 1] >= f.atol[t.L]
+
+
+# ---------------------------------------------------------------------------
+# triangular output form (Remark PAPER.md:577-611; SURVEY 8(f) f4)
+# ---------------------------------------------------------------------------
+def test_triangular_form_spd_against_dense_lu():
+    """spd c1 operator with the symmetric sketch: the triangular-form factorization solves to
+    10 eps of LAPACK getrf/getrs, K v = A v to 10 eps, solve(apply(v)) = v, C C^T = X_rr,
+    M_L = M_U^T (symmetric A, Psi = Omega), and it stores fewer scalars than G_L, G_U, X_rr."""
+    cfg = W.CONFIGS["c1"]
+    X = W.points(cfg)
+    t = O.build_tree(X, cfg.leaf, *cfg.root())
+    A = W.dense_matrix(cfg, X)
+    assert np.linalg.eigvalsh(A).min() > 0
+    Om, _ = W.omega_psi(cfg)
+    Y = A @ Om
+    P = t.perm
+    w = os.cpu_count() or 1
+    f = O.factor(t, Y[P], Y[P], Om[P], Om[P], cfg.eps, c_id=cfg.c_id, g=cfg.g, l=cfg.l, workers=w, triangular=True)
+    fb = O.factor(t, Y[P], Y[P], Om[P], Om[P], cfg.eps, c_id=cfg.c_id, g=cfg.g, l=cfg.l, workers=w)
+    b = W.rhs(cfg)
+    x = O.solve(f, b)
+    xd = sla.lu_solve(sla.lu_factor(A), b)
+    assert np.linalg.norm(x - xd) / np.linalg.norm(xd) <= 10 * cfg.eps
+    v = W.gaussian(cfg.N, 5, 1)
+    assert np.linalg.norm(O.apply(f, v) - A @ v) / np.linalg.norm(A @ v) <= 10 * cfg.eps
+    assert np.linalg.norm(O.solve(f, O.apply(f, v)) - v) <= 1e-12 * np.linalg.norm(v)
+    for s in f.steps[:50]:
+        assert np.allclose(s.C @ s.C.T, s.X_rr, rtol=0, atol=1e-13 * np.abs(s.X_rr).max())
+        assert np.allclose(s.M_L, s.M_U.T, rtol=0, atol=1e-12 * max(1.0, np.abs(s.M_U).max()))
+    assert f.memory() < fb.memory()
