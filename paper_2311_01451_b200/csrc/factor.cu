@@ -111,10 +111,14 @@ void set_smem_both() {
   set_smem(rsrs::chol_back_b_kernel<C>, rsrs::NN_SMEM);
   set_smem(rsrs::id_kernel<C>, -1);
   set_smem(rsrs::extract_lu_kernel<C>, -1);
-  set_smem(rsrs::solve_fwd_kernel<C>, -1);
-  set_smem(rsrs::solve_bwd_kernel<C>, -1);
-  set_smem(rsrs::apply_fwd_kernel<C>, -1);
-  set_smem(rsrs::apply_bwd_kernel<C>, -1);
+  set_smem(rsrs::solve_fwd_kernel<C, 1>, -1);
+  set_smem(rsrs::solve_bwd_kernel<C, 1>, -1);
+  set_smem(rsrs::apply_fwd_kernel<C, 1>, -1);
+  set_smem(rsrs::apply_bwd_kernel<C, 1>, -1);
+  set_smem(rsrs::solve_fwd_kernel<C, rsrs::sweep_nrb<C>()>, -1);
+  set_smem(rsrs::solve_bwd_kernel<C, rsrs::sweep_nrb<C>()>, -1);
+  set_smem(rsrs::apply_fwd_kernel<C, rsrs::sweep_nrb<C>()>, -1);
+  set_smem(rsrs::apply_bwd_kernel<C, rsrs::sweep_nrb<C>()>, -1);
   set_smem(rsrs::top_solve_kernel<C>, -1);
   set_smem(rsrs::top_apply_kernel<C>, -1);
   set_smem(rsrs::gblk_update_kernel<C>, rsrs::gblk_smem<C>());
@@ -1764,57 +1768,65 @@ struct Merger {
   }
 };
 
-template <bool C>
-static void run_sweep(rsrs_factorization f, double* x, int64_t nrhs, bool solve, cudaStream_t s, rsrs::Comm* comm) {
-  const size_t sS = (C ? 2 : 1) * sizeof(double);
+template <bool C, int NRB>
+static void run_sweep_nrb(rsrs_factorization f, double* x, int64_t nrhs, bool solve, cudaStream_t s,
+                          rsrs::Comm* comm) {
+  const size_t sS = (C ? 2 : 1) * sizeof(double) * NRB;   // shared bytes per tile row
   const int nr = (int)nrhs;
   Merger M{f, comm, x, f->N, (int)((C ? 2 : 1) * nrhs), s};
   M.init();
+  const size_t s1 = (C ? 2 : 1) * sizeof(double);
   if (solve) {
     for (const Batch& b : f->batches) {
-      const size_t sm = sS * 2 * (b.max_nb + 2);
-      if (b.nbox && b.tri) rsrs::solve_fwd_tri_kernel<<<b.nbox, 256, sm, s>>>(b.d_boxes, b.fpool, b.ipool, x, nrhs, nr);
-      else if (b.nbox) rsrs::solve_fwd_kernel<C><<<b.nbox, 256, sm, s>>>(b.d_boxes, b.fpool, b.ipool, x, nrhs, nr);
+      if (b.nbox && b.tri) rsrs::solve_fwd_tri_kernel<<<b.nbox, 256, s1 * 2 * (b.max_nb + 2), s>>>(b.d_boxes, b.fpool, b.ipool, x, nrhs, nr);
+      else if (b.nbox)
+        rsrs::solve_fwd_kernel<C, NRB><<<b.nbox, 256, sS * 2 * (b.max_nb + 2), s>>>(b.d_boxes, b.fpool, b.ipool, x, nrhs, nr);
       CK(cudaGetLastError());
       M.batch(b, 0);
     }
     if (f->nS > 0) {
-      rsrs::top_solve_kernel<C><<<1, 1024, sS * f->nS, s>>>(f->d_LU, f->ldS, f->nS, f->d_piv, f->d_S, x, nrhs, nr);
+      rsrs::top_solve_kernel<C><<<1, 1024, s1 * f->nS, s>>>(f->d_LU, f->ldS, f->nS, f->d_piv, f->d_S, x, nrhs, nr);
       CK(cudaGetLastError());
     }
     M.list(f->d_S, f->nS);
     for (auto it = f->batches.rbegin(); it != f->batches.rend(); ++it) {
-      const size_t sm = sS * (it->max_r + 2 * it->max_nb + 4);
       if (it->nbox && it->tri)
-        rsrs::solve_bwd_tri_kernel<<<it->nbox, 256, sm, s>>>(it->d_boxes, it->fpool, it->ipool, x, nrhs, nr);
+        rsrs::solve_bwd_tri_kernel<<<it->nbox, 256, s1 * (it->max_r + 2 * it->max_nb + 4), s>>>(it->d_boxes, it->fpool, it->ipool, x, nrhs, nr);
       else if (it->nbox)
-        rsrs::solve_bwd_kernel<C><<<it->nbox, 256, sm, s>>>(it->d_boxes, it->fpool, it->ipool, x, nrhs, nr);
+        rsrs::solve_bwd_kernel<C, NRB><<<it->nbox, 256, sS * (it->max_r + it->max_nb + 4), s>>>(it->d_boxes, it->fpool, it->ipool, x, nrhs, nr);
       CK(cudaGetLastError());
       M.batch(*it, 1);
     }
   } else {
     for (const Batch& b : f->batches) {
-      const size_t sm = sS * (b.max_r + 2 * b.max_nb + 4);
-      if (b.nbox && b.tri) rsrs::apply_fwd_tri_kernel<<<b.nbox, 256, sm, s>>>(b.d_boxes, b.fpool, b.ipool, x, nrhs, nr);
-      else if (b.nbox) rsrs::apply_fwd_kernel<C><<<b.nbox, 256, sm, s>>>(b.d_boxes, b.fpool, b.ipool, x, nrhs, nr);
+      if (b.nbox && b.tri)
+        rsrs::apply_fwd_tri_kernel<<<b.nbox, 256, s1 * (b.max_r + 2 * b.max_nb + 4), s>>>(b.d_boxes, b.fpool, b.ipool, x, nrhs, nr);
+      else if (b.nbox)
+        rsrs::apply_fwd_kernel<C, NRB><<<b.nbox, 256, sS * (b.max_r + b.max_nb + 4), s>>>(b.d_boxes, b.fpool, b.ipool, x, nrhs, nr);
       CK(cudaGetLastError());
       M.batch(b, 1);
     }
     if (f->nS > 0) {
-      rsrs::top_apply_kernel<C><<<1, 1024, sS * f->nS, s>>>(f->d_ASS, f->ldS, f->nS, f->d_S, x, nrhs, nr);
+      rsrs::top_apply_kernel<C><<<1, 1024, s1 * f->nS, s>>>(f->d_ASS, f->ldS, f->nS, f->d_S, x, nrhs, nr);
       CK(cudaGetLastError());
     }
     M.list(f->d_S, f->nS);
     for (auto it = f->batches.rbegin(); it != f->batches.rend(); ++it) {
-      const size_t sm = sS * (3 * it->max_nb + 4);
       if (it->nbox && it->tri)
-        rsrs::apply_bwd_tri_kernel<<<it->nbox, 256, sm, s>>>(it->d_boxes, it->fpool, it->ipool, x, nrhs, nr);
+        rsrs::apply_bwd_tri_kernel<<<it->nbox, 256, s1 * (3 * it->max_nb + 4), s>>>(it->d_boxes, it->fpool, it->ipool, x, nrhs, nr);
       else if (it->nbox)
-        rsrs::apply_bwd_kernel<C><<<it->nbox, 256, sm, s>>>(it->d_boxes, it->fpool, it->ipool, x, nrhs, nr);
+        rsrs::apply_bwd_kernel<C, NRB><<<it->nbox, 256, sS * (2 * it->max_nb + 4), s>>>(it->d_boxes, it->fpool, it->ipool, x, nrhs, nr);
       CK(cudaGetLastError());
       M.batch(*it, 0);
     }
   }
+}
+
+// one right-hand side: NRB = 1; several: tiles of sweep_nrb<C>() columns share each factor load
+template <bool C>
+static void run_sweep(rsrs_factorization f, double* x, int64_t nrhs, bool solve, cudaStream_t s, rsrs::Comm* comm) {
+  if (nrhs == 1) run_sweep_nrb<C, 1>(f, x, nrhs, solve, s, comm);
+  else run_sweep_nrb<C, rsrs::sweep_nrb<C>()>(f, x, nrhs, solve, s, comm);
 }
 
 extern "C" {

@@ -20,8 +20,111 @@ RSRS_DI double2 warp_sum(double2 v) {
   return v;
 }
 
-// forward solve of one box: x_r -= T x_s ; x_c -= G_L x_r ; x_r <- X_rr^-1 x_r
+// right-hand sides per tile of the multi-RHS sweep (factor bytes are read once per tile)
 template <bool C>
+constexpr int sweep_nrb() { return C ? 4 : 8; }
+
+// Matrix-times-tile from shared memory, the core of every sweep kernel:
+//   acc(i, c) = sum_j M[i, j] X[j, c],  rows i in [0, m), X = xsm[j * NRB + c] (n x NRB)
+// An 8-lane group per row (4 rows per warp in flight), each lane streaming its own
+// 16-byte chunks of the row (coalesced 128-byte row segments per group), so that a CTA
+// keeps many independent loads in flight (the 1-RHS sweep is latency / HBM bound);
+// emit(i, acc) runs on the group leader.  NRB right-hand sides share each factor load.
+template <int NRB, class F>
+RSRS_DI void gemv_rows(const double* __restrict__ M, i64 ld, int m, int n, const double* __restrict__ xsm,
+                       F&& emit) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int g = lane >> 3, gl = lane & 7;
+  for (int i0 = warp * 4; i0 < m; i0 += nw * 4) {
+    const int i = i0 + g;
+    double acc[NRB];
+#pragma unroll
+    for (int c = 0; c < NRB; ++c) acc[c] = 0.0;
+    if (i < m) {
+      const double* row = M + (i64)i * ld;
+      const int n2 = n >> 1;            // rows are 16-byte aligned (even leading dimensions)
+      const double2* row2 = reinterpret_cast<const double2*>(row);
+#pragma unroll 4
+      for (int j2 = gl; j2 < n2; j2 += 8) {
+        const double2 a = __ldg(row2 + j2);
+#pragma unroll
+        for (int c = 0; c < NRB; ++c) acc[c] = fma(a.x, xsm[(2 * j2) * NRB + c], fma(a.y, xsm[(2 * j2 + 1) * NRB + c], acc[c]));
+      }
+      if ((n & 1) && gl == 0) {
+        const double a = __ldg(row + n - 1);
+#pragma unroll
+        for (int c = 0; c < NRB; ++c) acc[c] = fma(a, xsm[(n - 1) * NRB + c], acc[c]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < NRB; ++c) {
+      acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], 4);
+      acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], 2);
+      acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], 1);
+    }
+    if (i < m && gl == 0) emit(i, acc);
+  }
+}
+template <int NRB, class F>
+RSRS_DI void gemv_rows(const double2* __restrict__ M, i64 ld, int m, int n, const double2* __restrict__ xsm,
+                       F&& emit) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int g = lane >> 3, gl = lane & 7;
+  for (int i0 = warp * 4; i0 < m; i0 += nw * 4) {
+    const int i = i0 + g;
+    double2 acc[NRB];
+#pragma unroll
+    for (int c = 0; c < NRB; ++c) acc[c] = make_double2(0.0, 0.0);
+    if (i < m) {
+      const double2* row = M + (i64)i * ld;
+#pragma unroll 4
+      for (int j = gl; j < n; j += 8) {
+        const double2 a = __ldg(row + j);
+#pragma unroll
+        for (int c = 0; c < NRB; ++c) {
+          const double2 xv = xsm[j * NRB + c];
+          acc[c].x = fma(a.x, xv.x, fma(-a.y, xv.y, acc[c].x));
+          acc[c].y = fma(a.x, xv.y, fma(a.y, xv.x, acc[c].y));
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < NRB; ++c)
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        acc[c].x += __shfl_xor_sync(0xffffffffu, acc[c].x, o);
+        acc[c].y += __shfl_xor_sync(0xffffffffu, acc[c].y, o);
+      }
+    if (i < m && gl == 0) emit(i, acc);
+  }
+}
+
+// x rows -> shared tile (rows idx[0..n), columns c0 .. c0 + NRB; zero beyond nrhs)
+template <class S, int NRB>
+RSRS_DI void load_rows(S* __restrict__ dst, const S* __restrict__ x, const int* __restrict__ idx, int n, i64 ldx,
+                       int c0, int nrhs) {
+  for (int t = threadIdx.x; t < n * NRB; t += blockDim.x) {
+    const int i = t / NRB, c = t % NRB;
+    dst[t] = (c0 + c < nrhs) ? x[(i64)idx[i] * ldx + c0 + c] : s_zero(S());
+  }
+}
+
+// x_s (-|+)= T^* x_r  (T: n_r x k, ld ldn): a thread per (s, column); coalesced over s
+template <class S, int NRB>
+RSRS_DI void t_adjoint_update(S* __restrict__ x, const int* __restrict__ skel, const S* __restrict__ T, i64 ldn,
+                              int k, int nr, const S* __restrict__ xr, i64 ldx, int c0, int nrhs, double sign) {
+  for (int t = threadIdx.x; t < k * NRB; t += blockDim.x) {
+    const int sidx = t % k, c = t / k;
+    if (c0 + c >= nrhs) continue;
+    S v = s_zero(S());
+    for (int i = 0; i < nr; ++i) v = s_add(v, s_mul(s_conj(T[(i64)i * ldn + sidx]), xr[i * NRB + c]));
+    S* xp = x + (i64)skel[sidx] * ldx + c0 + c;
+    *xp = s_add(*xp, s_scale(v, sign));
+  }
+}
+
+// forward solve of one box: x_r -= T x_s ; x_c -= G_L x_r ; x_r <- X_rr^-1 x_r
+template <bool C, int NRB>
 __global__ void __launch_bounds__(256) solve_fwd_kernel(const BoxDev* __restrict__ boxes,
                                                          const double* __restrict__ fpoold,
                                                          const int* __restrict__ ipool, double* __restrict__ xd,
@@ -31,47 +134,46 @@ __global__ void __launch_bounds__(256) solve_fwd_kernel(const BoxDev* __restrict
   S* sm = reinterpret_cast<S*>(smd);
   const S* fpool = reinterpret_cast<const S*>(fpoold);
   S* x = reinterpret_cast<S*>(xd);
-  const S zero = s_zero(S());
-  const BoxDev b = boxes[blockIdx.x];
+  const BoxDev& b = boxes[blockIdx.x];
   const int nr = b.nr, k = b.k, nc = b.nc;
   if (nr <= 0) return;
   const int ldn = b.ldn;
   S* xs = sm;
-  S* xr = xs + k;
+  S* xr = xs + k * NRB;
   const int* red = ipool + b.f_red;
   const int* skel = ipool + b.f_skel;
   const int* cc = ipool + b.f_c;
   const S* T = fpool + b.f_T;
   const S* GL = fpool + b.f_GL;
   const S* Xi = fpool + b.f_Xinv;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int col = 0; col < nrhs; ++col) {
-    for (int s = tid; s < k; s += blockDim.x) xs[s] = x[(i64)skel[s] * ldx + col];
+  for (int c0 = 0; c0 < nrhs; c0 += NRB) {
+    load_rows<S, NRB>(xs, x, skel, k, ldx, c0, nrhs);
+    load_rows<S, NRB>(xr, x, red, nr, ldx, c0, nrhs);
     __syncthreads();
-    for (int i = tid; i < nr; i += blockDim.x) {
-      S v = x[(i64)red[i] * ldx + col];
-      for (int s = 0; s < k; ++s) v = s_sub(v, s_mul(T[(i64)i * ldn + s], xs[s]));
-      xr[i] = v;
-    }
+    gemv_rows<NRB>(T, ldn, nr, k, xs, [&](int i, const S* acc) {
+#pragma unroll
+      for (int c = 0; c < NRB; ++c) xr[i * NRB + c] = s_sub(xr[i * NRB + c], acc[c]);
+    });
     __syncthreads();
-    for (int ci = warp; ci < nc; ci += blockDim.x / 32) {
-      S v = zero;
-      for (int j = lane; j < nr; j += 32) v = s_add(v, s_mul(GL[(i64)ci * ldn + j], xr[j]));
-      v = warp_sum(v);
-      if (lane == 0) x[(i64)cc[ci] * ldx + col] = s_sub(x[(i64)cc[ci] * ldx + col], v);
-    }
-    for (int i = warp; i < nr; i += blockDim.x / 32) {
-      S v = zero;
-      for (int j = lane; j < nr; j += 32) v = s_add(v, s_mul(Xi[(i64)i * ldn + j], xr[j]));
-      v = warp_sum(v);
-      if (lane == 0) x[(i64)red[i] * ldx + col] = v;
-    }
+    gemv_rows<NRB>(GL, ldn, nc, nr, xr, [&](int i, const S* acc) {
+#pragma unroll
+      for (int c = 0; c < NRB; ++c)
+        if (c0 + c < nrhs) {
+          S* xp = x + (i64)cc[i] * ldx + c0 + c;
+          *xp = s_sub(*xp, acc[c]);
+        }
+    });
+    gemv_rows<NRB>(Xi, ldn, nr, nr, xr, [&](int i, const S* acc) {
+#pragma unroll
+      for (int c = 0; c < NRB; ++c)
+        if (c0 + c < nrhs) x[(i64)red[i] * ldx + c0 + c] = acc[c];
+    });
     __syncthreads();
   }
 }
 
-// backward solve of one box: x_r -= G_U x_c ; x_s -= T^T x_r
-template <bool C>
+// backward solve of one box: x_r -= G_U x_c ; x_s -= T^* x_r
+template <bool C, int NRB>
 __global__ void __launch_bounds__(256) solve_bwd_kernel(const BoxDev* __restrict__ boxes,
                                                          const double* __restrict__ fpoold,
                                                          const int* __restrict__ ipool, double* __restrict__ xd,
@@ -81,45 +183,37 @@ __global__ void __launch_bounds__(256) solve_bwd_kernel(const BoxDev* __restrict
   S* sm = reinterpret_cast<S*>(smd);
   const S* fpool = reinterpret_cast<const S*>(fpoold);
   S* x = reinterpret_cast<S*>(xd);
-  const S zero = s_zero(S());
-  const BoxDev b = boxes[blockIdx.x];
+  const BoxDev& b = boxes[blockIdx.x];
   const int nr = b.nr, k = b.k, nc = b.nc;
   if (nr <= 0) return;
-  const int ldn = b.ldn;
-  const int ldr = b.ldr;
+  const int ldn = b.ldn, ldr = b.ldr;
   S* xc = sm;
-  S* xr = xc + nc;
+  S* xr = xc + nc * NRB;
   const int* red = ipool + b.f_red;
   const int* skel = ipool + b.f_skel;
   const int* cc = ipool + b.f_c;
   const S* T = fpool + b.f_T;
   const S* GU = fpool + b.f_GU;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int col = 0; col < nrhs; ++col) {
-    for (int j = tid; j < nc; j += blockDim.x) xc[j] = x[(i64)cc[j] * ldx + col];
+  for (int c0 = 0; c0 < nrhs; c0 += NRB) {
+    load_rows<S, NRB>(xc, x, cc, nc, ldx, c0, nrhs);
+    load_rows<S, NRB>(xr, x, red, nr, ldx, c0, nrhs);
     __syncthreads();
-    for (int i = warp; i < nr; i += blockDim.x / 32) {
-      S v = zero;
-      for (int j = lane; j < nc; j += 32) v = s_add(v, s_mul(GU[(i64)i * ldr + j], xc[j]));
-      v = warp_sum(v);
-      if (lane == 0) {
-        const S nv = s_sub(x[(i64)red[i] * ldx + col], v);
-        x[(i64)red[i] * ldx + col] = nv;
-        xr[i] = nv;
+    gemv_rows<NRB>(GU, ldr, nr, nc, xc, [&](int i, const S* acc) {
+#pragma unroll
+      for (int c = 0; c < NRB; ++c) {
+        const S v = s_sub(xr[i * NRB + c], acc[c]);
+        xr[i * NRB + c] = v;
+        if (c0 + c < nrhs) x[(i64)red[i] * ldx + c0 + c] = v;
       }
-    }
+    });
     __syncthreads();
-    for (int s = tid; s < k; s += blockDim.x) {   // x_s -= T^* x_r
-      S v = zero;
-      for (int i = 0; i < nr; ++i) v = s_add(v, s_mul(s_conj(T[(i64)i * ldn + s]), xr[i]));
-      x[(i64)skel[s] * ldx + col] = s_sub(x[(i64)skel[s] * ldx + col], v);
-    }
+    t_adjoint_update<S, NRB>(x, skel, T, ldn, k, nr, xr, ldx, c0, nrhs, -1.0);
     __syncthreads();
   }
 }
 
-// apply, forward half of one box: x_s += T^T x_r ; x_r += G_U x_c ; x_r <- X_rr x_r
-template <bool C>
+// apply, forward half of one box: x_s += T^* x_r ; x_r += G_U x_c ; x_r <- X_rr x_r
+template <bool C, int NRB>
 __global__ void __launch_bounds__(256) apply_fwd_kernel(const BoxDev* __restrict__ boxes,
                                                          const double* __restrict__ fpoold,
                                                          const int* __restrict__ ipool, double* __restrict__ xd,
@@ -129,54 +223,42 @@ __global__ void __launch_bounds__(256) apply_fwd_kernel(const BoxDev* __restrict
   S* sm = reinterpret_cast<S*>(smd);
   const S* fpool = reinterpret_cast<const S*>(fpoold);
   S* x = reinterpret_cast<S*>(xd);
-  const S zero = s_zero(S());
-  const BoxDev b = boxes[blockIdx.x];
+  const BoxDev& b = boxes[blockIdx.x];
   const int nr = b.nr, k = b.k, nc = b.nc;
   if (nr <= 0) return;
-  const int ldn = b.ldn;
-  const int ldr = b.ldr;
+  const int ldn = b.ldn, ldr = b.ldr;
   S* xc = sm;
-  S* xr = xc + nc;
-  S* xr2 = xr + nr;
+  S* xr = xc + nc * NRB;
   const int* red = ipool + b.f_red;
   const int* skel = ipool + b.f_skel;
   const int* cc = ipool + b.f_c;
   const S* T = fpool + b.f_T;
   const S* GU = fpool + b.f_GU;
   const S* Xrr = fpool + b.f_Xrr;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int col = 0; col < nrhs; ++col) {
-    for (int i = tid; i < nr; i += blockDim.x) xr[i] = x[(i64)red[i] * ldx + col];
+  for (int c0 = 0; c0 < nrhs; c0 += NRB) {
+    load_rows<S, NRB>(xr, x, red, nr, ldx, c0, nrhs);
     __syncthreads();
-    for (int s = tid; s < k; s += blockDim.x) {   // x_s += T^* x_r
-      S v = zero;
-      for (int i = 0; i < nr; ++i) v = s_add(v, s_mul(s_conj(T[(i64)i * ldn + s]), xr[i]));
-      x[(i64)skel[s] * ldx + col] = s_add(x[(i64)skel[s] * ldx + col], v);
-    }
+    // x_s += T^* x_r first: c = near \ red holds b's skeletons, so x_c is read after it
+    t_adjoint_update<S, NRB>(x, skel, T, ldn, k, nr, xr, ldx, c0, nrhs, 1.0);
     __syncthreads();
-    for (int j = tid; j < nc; j += blockDim.x) xc[j] = x[(i64)cc[j] * ldx + col];
+    load_rows<S, NRB>(xc, x, cc, nc, ldx, c0, nrhs);
     __syncthreads();
-    for (int i = warp; i < nr; i += blockDim.x / 32) {
-      S v = zero;
-      for (int j = lane; j < nc; j += 32) v = s_add(v, s_mul(GU[(i64)i * ldr + j], xc[j]));
-      v = warp_sum(v);
-      if (lane == 0) xr[i] = s_add(xr[i], v);
-    }
+    gemv_rows<NRB>(GU, ldr, nr, nc, xc, [&](int i, const S* acc) {
+#pragma unroll
+      for (int c = 0; c < NRB; ++c) xr[i * NRB + c] = s_add(xr[i * NRB + c], acc[c]);
+    });
     __syncthreads();
-    for (int i = warp; i < nr; i += blockDim.x / 32) {
-      S v = zero;
-      for (int j = lane; j < nr; j += 32) v = s_add(v, s_mul(Xrr[(i64)i * ldn + j], xr[j]));
-      v = warp_sum(v);
-      if (lane == 0) xr2[i] = v;
-    }
-    __syncthreads();
-    for (int i = tid; i < nr; i += blockDim.x) x[(i64)red[i] * ldx + col] = xr2[i];
+    gemv_rows<NRB>(Xrr, ldn, nr, nr, xr, [&](int i, const S* acc) {
+#pragma unroll
+      for (int c = 0; c < NRB; ++c)
+        if (c0 + c < nrhs) x[(i64)red[i] * ldx + c0 + c] = acc[c];
+    });
     __syncthreads();
   }
 }
 
 // apply, backward half of one box: x_c += G_L x_r ; x_r += T x_s
-template <bool C>
+template <bool C, int NRB>
 __global__ void __launch_bounds__(256) apply_bwd_kernel(const BoxDev* __restrict__ boxes,
                                                          const double* __restrict__ fpoold,
                                                          const int* __restrict__ ipool, double* __restrict__ xd,
@@ -186,41 +268,44 @@ __global__ void __launch_bounds__(256) apply_bwd_kernel(const BoxDev* __restrict
   S* sm = reinterpret_cast<S*>(smd);
   const S* fpool = reinterpret_cast<const S*>(fpoold);
   S* x = reinterpret_cast<S*>(xd);
-  const S zero = s_zero(S());
-  const BoxDev b = boxes[blockIdx.x];
+  const BoxDev& b = boxes[blockIdx.x];
   const int nr = b.nr, k = b.k, nc = b.nc;
   if (nr <= 0) return;
   const int ldn = b.ldn;
   S* xs = sm;
-  S* xr = xs + k;
+  S* xr = xs + k * NRB;
   const int* red = ipool + b.f_red;
   const int* skel = ipool + b.f_skel;
   const int* cc = ipool + b.f_c;
   const S* T = fpool + b.f_T;
   const S* GL = fpool + b.f_GL;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int col = 0; col < nrhs; ++col) {
-    for (int i = tid; i < nr; i += blockDim.x) xr[i] = x[(i64)red[i] * ldx + col];
+  for (int c0 = 0; c0 < nrhs; c0 += NRB) {
+    load_rows<S, NRB>(xr, x, red, nr, ldx, c0, nrhs);
     __syncthreads();
-    for (int ci = warp; ci < nc; ci += blockDim.x / 32) {
-      S v = zero;
-      for (int j = lane; j < nr; j += 32) v = s_add(v, s_mul(GL[(i64)ci * ldn + j], xr[j]));
-      v = warp_sum(v);
-      if (lane == 0) x[(i64)cc[ci] * ldx + col] = s_add(x[(i64)cc[ci] * ldx + col], v);
-    }
+    gemv_rows<NRB>(GL, ldn, nc, nr, xr, [&](int i, const S* acc) {
+#pragma unroll
+      for (int c = 0; c < NRB; ++c)
+        if (c0 + c < nrhs) {
+          S* xp = x + (i64)cc[i] * ldx + c0 + c;
+          *xp = s_add(*xp, acc[c]);
+        }
+    });
     __syncthreads();
-    for (int s = tid; s < k; s += blockDim.x) xs[s] = x[(i64)skel[s] * ldx + col];
+    load_rows<S, NRB>(xs, x, skel, k, ldx, c0, nrhs);   // after the x_c update (skel is part of c)
     __syncthreads();
-    for (int i = tid; i < nr; i += blockDim.x) {
-      S v = xr[i];
-      for (int s = 0; s < k; ++s) v = s_add(v, s_mul(T[(i64)i * ldn + s], xs[s]));
-      x[(i64)red[i] * ldx + col] = v;
-    }
+    gemv_rows<NRB>(T, ldn, nr, k, xs, [&](int i, const S* acc) {
+#pragma unroll
+      for (int c = 0; c < NRB; ++c)
+        if (c0 + c < nrhs) x[(i64)red[i] * ldx + c0 + c] = s_add(xr[i * NRB + c], acc[c]);
+    });
     __syncthreads();
   }
 }
 
 // top block: x_S <- A~_SS^-1 x_S (LU with pivots) or x_S <- A~_SS x_S
+// Blocked substitution: a 32 x 32 diagonal block is solved by one warp with shuffles (no
+// CTA barrier per row), the rows below / above are updated by the whole CTA: 2 barriers
+// per 32 rows instead of 2 per row.
 template <bool C>
 __global__ void __launch_bounds__(1024) top_solve_kernel(const double* __restrict__ LUd, i64 lda, int n,
                                                           const int* __restrict__ ipiv,
@@ -231,7 +316,7 @@ __global__ void __launch_bounds__(1024) top_solve_kernel(const double* __restric
   S* xs = reinterpret_cast<S*>(xsd);
   const S* LU = reinterpret_cast<const S*>(LUd);
   S* x = reinterpret_cast<S*>(xd);
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int col = 0; col < nrhs; ++col) {
     for (int i = tid; i < n; i += blockDim.x) xs[i] = x[(i64)Sidx[i] * ldx + col];
     __syncthreads();
@@ -243,16 +328,55 @@ __global__ void __launch_bounds__(1024) top_solve_kernel(const double* __restric
           xs[ipiv[c]] = t;
         }
     __syncthreads();
-    for (int c = 0; c < n; ++c) {  // unit lower
-      const S xc = xs[c];
-      for (int i = c + 1 + tid; i < n; i += blockDim.x) xs[i] = s_sub(xs[i], s_mul(LU[(i64)i * lda + c], xc));
+    for (int p0 = 0; p0 < n; p0 += 32) {          // unit lower, panels top-down
+      const int pn = min(32, n - p0);
+      if (warp == 0) {
+        S v = lane < pn ? xs[p0 + lane] : s_zero(S());
+        for (int j = 0; j < pn; ++j) {
+          S xj;
+          if constexpr (C) {
+            xj.x = __shfl_sync(0xffffffffu, v.x, j);
+            xj.y = __shfl_sync(0xffffffffu, v.y, j);
+          } else {
+            xj = __shfl_sync(0xffffffffu, v, j);
+          }
+          if (lane > j && lane < pn) v = s_sub(v, s_mul(LU[(i64)(p0 + lane) * lda + p0 + j], xj));
+        }
+        if (lane < pn) xs[p0 + lane] = v;
+      }
+      __syncthreads();
+      for (int i = p0 + pn + warp; i < n; i += blockDim.x / 32) {
+        S v = s_zero(S());
+        if (lane < pn) v = s_mul(LU[(i64)i * lda + p0 + lane], xs[p0 + lane]);
+        v = warp_sum(v);
+        if (lane == 0) xs[i] = s_sub(xs[i], v);
+      }
       __syncthreads();
     }
-    for (int c = n - 1; c >= 0; --c) {  // upper
-      if (tid == 0) xs[c] = s_div(xs[c], LU[(i64)c * lda + c]);
+    for (int p1 = n; p1 > 0; p1 -= 32) {          // upper, panels bottom-up
+      const int p0 = max(0, p1 - 32), pn = p1 - p0;
+      if (warp == 0) {
+        S v = lane < pn ? xs[p0 + lane] : s_zero(S());
+        for (int j = pn - 1; j >= 0; --j) {
+          if (lane == j) v = s_div(v, LU[(i64)(p0 + j) * lda + p0 + j]);
+          S xj;
+          if constexpr (C) {
+            xj.x = __shfl_sync(0xffffffffu, v.x, j);
+            xj.y = __shfl_sync(0xffffffffu, v.y, j);
+          } else {
+            xj = __shfl_sync(0xffffffffu, v, j);
+          }
+          if (lane < j) v = s_sub(v, s_mul(LU[(i64)(p0 + lane) * lda + p0 + j], xj));
+        }
+        if (lane < pn) xs[p0 + lane] = v;
+      }
       __syncthreads();
-      const S xc = xs[c];
-      for (int i = tid; i < c; i += blockDim.x) xs[i] = s_sub(xs[i], s_mul(LU[(i64)i * lda + c], xc));
+      for (int i = warp; i < p0; i += blockDim.x / 32) {
+        S v = s_zero(S());
+        if (lane < pn) v = s_mul(LU[(i64)i * lda + p0 + lane], xs[p0 + lane]);
+        v = warp_sum(v);
+        if (lane == 0) xs[i] = s_sub(xs[i], v);
+      }
       __syncthreads();
     }
     for (int i = tid; i < n; i += blockDim.x) x[(i64)Sidx[i] * ldx + col] = xs[i];

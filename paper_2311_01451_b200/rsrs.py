@@ -152,10 +152,11 @@ def _ptr(t) -> int:
     return t.data_ptr()
 
 
-def _check_tensor(name, t, rows, min_cols=None, dtype=None, allow_1d=False):
+def _check_tensor(name, t, rows, min_cols=None, dtype=None, allow_1d=False, aligned_rows=True):
     """Argument validation the C ABI cannot do (it only sees a pointer and a leading dimension):
-    a CUDA tensor of the factor's dtype with `rows` rows, unit column stride, 16-byte aligned
-    rows (the kernels stage rows with 16-byte cp.async)."""
+    a CUDA tensor of the factor's dtype with `rows` rows, unit column stride, a 16-byte aligned base
+    and (sample arrays: aligned_rows) 16-byte aligned rows (the kernels stage rows with 16-byte
+    cp.async); right-hand sides only need the aligned base."""
     import torch
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise ValueError(f"{name} must be a CUDA tensor")
@@ -176,7 +177,7 @@ def _check_tensor(name, t, rows, min_cols=None, dtype=None, allow_1d=False):
         raise ValueError(f"{name} needs at least {min_cols} columns")
     if t.data_ptr() % 16:
         raise ValueError(f"{name}: data pointer not 16-byte aligned")
-    if t.dim() == 2 and (t.stride(0) * t.element_size()) % 16:
+    if aligned_rows and t.dim() == 2 and (t.stride(0) * t.element_size()) % 16:
         raise ValueError(f"{name}: row stride not a multiple of 16 bytes")
 
 
@@ -324,7 +325,7 @@ class Factorization:
     def solve(self, B, stream=None):
         """B <- K^-1 B in place; B: CUDA tensor of the factor's dtype, (N,) or (N, nrhs) row-major,
         original order."""
-        _check_tensor("B", B, self.N, dtype=self.dtype, allow_1d=True)
+        _check_tensor("B", B, self.N, dtype=self.dtype, allow_1d=True, aligned_rows=False)
         nrhs = 1 if B.dim() == 1 else B.shape[1]
         ldb = 1 if B.dim() == 1 else B.stride(0)
         _check(_lib.rsrs_solve(self._h, _ptr(B), ldb, nrhs, _stream_ptr(stream)))
@@ -332,7 +333,7 @@ class Factorization:
 
     def apply(self, X, stream=None):
         """X <- K X in place (same layout as solve)."""
-        _check_tensor("X", X, self.N, dtype=self.dtype, allow_1d=True)
+        _check_tensor("X", X, self.N, dtype=self.dtype, allow_1d=True, aligned_rows=False)
         nrhs = 1 if X.dim() == 1 else X.shape[1]
         ldx = 1 if X.dim() == 1 else X.stride(0)
         _check(_lib.rsrs_apply(self._h, _ptr(X), ldx, nrhs, _stream_ptr(stream)))
@@ -448,7 +449,7 @@ def factor_emulated(tree: Tree, G: int, Y, Z, Omega, Psi, p: int, eps: float = 1
 
 def _emul_sweep(fn, fs, B):
     G = len(fs)
-    _check_tensor("B", B, fs[0].N, dtype=fs[0].dtype, allow_1d=True)
+    _check_tensor("B", B, fs[0].N, dtype=fs[0].dtype, allow_1d=True, aligned_rows=False)
     hs = (_vp * G)(*[f._h.value for f in fs])
     nrhs = 1 if B.dim() == 1 else B.shape[1]
     ld = 1 if B.dim() == 1 else B.stride(0)

@@ -77,7 +77,8 @@ def parse(cfg_name: str, csv_path: str, regions_path: str, out: str):
         except ValueError:
             continue
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9,
-                 "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}.get(unit, 1.0)
+                 "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0,
+                 "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0}.get(unit, 1.0)
         a = agg.setdefault(cls, {"dram_bytes": 0.0, "seconds": 0.0, "kernels": set()})
         if met in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             a["dram_bytes"] += v * scale
