@@ -170,6 +170,13 @@ void rsrs_tree_destroy(rsrs_tree t);
  *   Y, Z, Omega, Psi DEVICE pointers, N x ld row-major, TREE order.  BORROWED
  *                    AND OVERWRITTEN: the sweep updates them in place; their
  *                    contents are unspecified on return.
+ *                    Or (single rank, pulled L/U updates) PINNED HOST pointers,
+ *                    all four (cudaHostAlloc / cudaHostRegister; pageable memory is
+ *                    RSRS_ERR_INVALID): the library allocates the device store,
+ *                    copies Omega / Psi on `stream` and streams the Y / Z rows of
+ *                    each leaf colour batch on a copy stream one batch ahead of the
+ *                    sweep (zero-copy reads), so the transfer overlaps the compute;
+ *                    host inputs are only read.
  *   ld               leading dimension (>= p, even)
  *   opts             options (NULL: defaults eps=1e-6, g=1, c_id=1, l=10, top_level=2)
  *   out              receives the factorization handle
@@ -184,7 +191,8 @@ rsrs_status rsrs_factor(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, void* Z,
 /* ---------------------------------------------------------------------------
  * rsrs_solve -- B <- K^-1 B, K = V_1..V_n A~_diag W_n..W_1 (PAPER.md:1130-1143,
  * 958-960; elim inverse = sign toggle 572-575).
- *   B     DEVICE, N x ldb row-major in ORIGINAL point order, nrhs columns used
+ *   B     DEVICE (or pinned HOST: staged through a device buffer on stream s),
+ *         N x ldb row-major in ORIGINAL point order, nrhs columns used
  *         (ldb >= nrhs); overwritten with the solution.
  *   s     cudaStream_t (NULL = legacy default stream); stream-ordered, asynchronous.
  * Errors: RSRS_ERR_INVALID (bad arguments), RSRS_ERR_CUDA.

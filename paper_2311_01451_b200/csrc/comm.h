@@ -113,7 +113,8 @@ class NcclComm : public Comm {
     for (const Msg& m : recvs)
       if (m.bytes) chk(A.recv(m.buf, m.bytes, NCCL_UINT8, m.peer, comm_, s), "ncclRecv");
     chk(A.groupEnd(), "ncclGroupEnd");
-    if (cudaStreamSynchronize(s) != cudaSuccess) throw CommError{"exchange: stream synchronize failed"};
+    // stream-ordered: the scatter kernels that consume the received rows follow on `s`
+    // (no host round trip; errors surface at the next synchronising call)
   }
   void allreduce_max_i32(int* host, size_t n, cudaStream_t s) override {
     if (!n) return;

@@ -74,6 +74,7 @@ constexpr int SMEM_MAX = 227 * 1024 - 1024;  // dynamic-smem budget of the large
 int g_optin = 0;
 bool g_debug = false;  // RSRS_DEBUG_SYNC=1: synchronize and check after every launch
 bool g_trace = false;  // RSRS_TRACE=1: host-side time split of rsrs_factor on stderr
+bool g_wide_nt = false; // RSRS_WIDE_NT=1: keep the 32 x 64 NT tiles for small boxes (A/B timing of the narrow tiles)
 
 // host-side time split of one rsrs_factor (RSRS_TRACE)
 struct HostTrace {
@@ -122,6 +123,7 @@ void set_smem_both() {
   set_smem(rsrs::top_solve_kernel<C>, -1);
   set_smem(rsrs::top_apply_kernel<C>, -1);
   set_smem(rsrs::gblk_update_kernel<C>, rsrs::gblk_smem<C>());
+  set_smem(rsrs::gblk_update_box_kernel<C>, rsrs::gblk_box_smem<C>());
   set_smem(rsrs::skinny_nn_kernel<C>, rsrs::skinny_smem<C>());
 }
 
@@ -132,10 +134,16 @@ void init_kernels() {
   g_debug = dbg && dbg[0] == '1';
   const char* tr = getenv("RSRS_TRACE");
   g_trace = tr && tr[0] == '1';
+  const char* wn = getenv("RSRS_WIDE_NT");
+  g_wide_nt = wn && wn[0] == '1';
   int dev = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&g_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   set_smem(rsrs::gemm_nt_kernel<64>, rsrs::NT_SMEM);
+  set_smem(rsrs::gemm_nt_narrow_kernel<16>, rsrs::nt_narrow_smem(16));
+  set_smem(rsrs::gemm_nn_narrow_kernel<16>, rsrs::nn_narrow_smem(16));
+  set_smem(rsrs::gemm_nn_narrow_kernel<32>, rsrs::nn_narrow_smem(32));
+  set_smem(rsrs::gemm_nt_narrow_kernel<32>, rsrs::nt_narrow_smem(32));
   set_smem(rsrs::gemm_nn_kernel<64>, rsrs::NN_SMEM);
   set_smem(rsrs::gemm_nt_kernel_c<64>, rsrs::NT_SMEM);
   set_smem(rsrs::gemm_nn_kernel_c<64>, rsrs::NN_SMEM);
@@ -265,6 +273,14 @@ void launch_nt(bool cplx, const NTDesc* d, int n, int mmax, int nmax, cudaStream
     for (int i = 0; i < n; i += ZMAX) launch_nt(cplx, d + i, std::min(ZMAX, n - i), mmax, nmax, s, launches);
     return;
   }
+  if (!cplx && mmax <= 32 && !g_wide_nt) {
+    // small boxes: transposed narrow tiles (only the short side is padded, to 16 / 32)
+    dim3 g2((nmax + 63) / 64, 1, n);
+    if (mmax <= 16) rsrs::gemm_nt_narrow_kernel<16><<<g2, 128, rsrs::nt_narrow_smem(16), s>>>(d);
+    else rsrs::gemm_nt_narrow_kernel<32><<<g2, 128, rsrs::nt_narrow_smem(32), s>>>(d);
+    post("gemm_nt_narrow", s, launches);
+    return;
+  }
   const int TN = cplx ? rsrs::GTC : rsrs::GT;
   const int TM = mmax <= 32 ? 32 : 64;
   dim3 grid((nmax + TN - 1) / TN, (mmax + TM - 1) / TM, n);
@@ -279,8 +295,19 @@ void launch_nt(bool cplx, const NTDesc* d, int n, int mmax, int nmax, cudaStream
 }
 
 void launch_nn(bool cplx, const NNDesc* d, int n, int mmax, int nmax, cudaStream_t s, int64_t& launches,
-               int force_tm = 0) {
+               int force_tm = 0, bool narrow_ok = false) {
   if (n <= 0 || mmax <= 0 || nmax <= 0) return;
+  if (narrow_ok && !cplx && mmax <= 32 && !g_wide_nt && force_tm == 0) {
+    // small boxes, transA = 0 (projection, pulled L/U update): transposed narrow tiles
+    constexpr int ZMAX = 65535;
+    for (int i = 0; i < n; i += ZMAX) {
+      dim3 g2((nmax + 63) / 64, 1, std::min(ZMAX, n - i));
+      if (mmax <= 16) rsrs::gemm_nn_narrow_kernel<16><<<g2, 128, rsrs::nn_narrow_smem(16), s>>>(d + i);
+      else rsrs::gemm_nn_narrow_kernel<32><<<g2, 128, rsrs::nn_narrow_smem(32), s>>>(d + i);
+      post("gemm_nn_narrow", s, launches);
+    }
+    return;
+  }
   constexpr int ZMAX = 65535;
   if (n > ZMAX) {
     for (int i = 0; i < n; i += ZMAX)
@@ -303,7 +330,7 @@ void launch_nn(bool cplx, const NNDesc* d, int n, int mmax, int nmax, cudaStream
 // in-place skinny updates (E/F), see gemm.cuh
 void launch_skinny(bool cplx, const NNDesc* d, int n, int ncols, cudaStream_t s, int64_t& launches) {
   if (n <= 0 || ncols <= 0) return;
-  dim3 grid(n, (ncols + 127) / 128);
+  dim3 grid(n, (ncols + rsrs::SK_COLS - 1) / rsrs::SK_COLS);
   if (cplx) rsrs::skinny_nn_kernel<true><<<grid, 128, rsrs::skinny_smem<true>(), s>>>(d);
   else rsrs::skinny_nn_kernel<false><<<grid, 128, rsrs::skinny_smem<false>(), s>>>(d);
   post("skinny_nn", s, launches);
@@ -365,7 +392,7 @@ struct rsrs_factor_s {
   int* d_piv = nullptr;
   std::vector<int64_t> S_host;
   int64_t* d_perm = nullptr;
-  DBuf xtmp, mergebuf;
+  DBuf xtmp, mergebuf, bstage;
   int nranks = 1, rank = 0;                       // multi-GPU: this factor holds rank's boxes only
   void* nccl_comm = nullptr;                      // NCCL communicator of the factorization (borrowed)
   bool own_stream = false;                        // emulated ranks: the library created `stream`
@@ -409,6 +436,8 @@ struct Planner {
   bool cplx = false;
   bool sym = false;    // symmetric shortcut: Psi = Omega, Z = Y, only the Y / Omega side runs
   int symmode = 0;     // 1: A = A^* (Z = Y); 2: complex symmetric A = A^T (Psi = conj Omega, Z = conj Y)
+  bool host_in = false;  // Y, Z, Omega, Psi are pinned HOST arrays: the library owns the device store, copies
+                         // Omega / Psi up front and the Y / Z rows of each leaf colour batch one batch ahead
   bool tri = false;    // triangular form (Remark PAPER.md:577-611): Cholesky X_rr = C C^T
   bool gram_blocks = true;   // level-wide near-field Gram blocks (gram.cuh; single rank)
   bool level_blocks = false; // the current level uses them (account_box counts the cross products only)
@@ -463,6 +492,7 @@ struct Planner {
     pend.push_back(Pend{cur_cls, cur_a, b});
   }
   double lev_ms[RSRS_NUM_KERNEL_CLASSES] = {0};   // RSRS_TRACE=1 with opts.profile: per-level class split
+  double lev_fl0[RSRS_NUM_KERNEL_CLASSES] = {0};
   void flush_prof() {  // after a stream synchronize
     for (auto& p : pend) {
       float ms = 0;
@@ -622,6 +652,39 @@ struct Planner {
         Y = dst[0]; Z = dst[1]; Om = dst[2]; Ps = dst[3];
         ld = nld;
       }
+    }
+    // host-resident inputs: device store owned by the factorization, Omega / Psi copied now,
+    // Y / Z rows streamed per leaf colour batch (copy stream `cs`, one batch ahead)
+    DBuf hstore;
+    const double* hY = nullptr;
+    const double* hZ = nullptr;
+    i64 hld = 0;
+    cudaStream_t cs = nullptr;
+    std::vector<cudaEvent_t> hev;
+    struct StreamGuard {
+      cudaStream_t& st;
+      std::vector<cudaEvent_t>& ev;
+      ~StreamGuard() {
+        if (st) {
+          cudaStreamSynchronize(st);
+          cudaStreamDestroy(st);
+        }
+        for (auto e : ev) cudaEventDestroy(e);
+      }
+    } guard{cs, hev};
+    if (host_in) {
+      hY = Yu;
+      hZ = sym ? nullptr : Zu;
+      hld = SC * ldu;
+      hstore.alloc((size_t)sS * std::max<i64>(2, 4 * (i64)T.N * nld), s);
+      double* base = hstore.as<double>();
+      double* dst[4] = {base, base + SC * T.N * nld, base + 2 * SC * T.N * nld, base + 3 * SC * T.N * nld};
+      const double* hsrc[2] = {Omu, Psu};
+      for (int a = 0; a < (sym ? 1 : 2); ++a)
+        CK(cudaMemcpy2DAsync(dst[2 + a], sS * nld, hsrc[a], sS * ldu, sS * p, T.N, cudaMemcpyHostToDevice, s));
+      Y = dst[0]; Z = sym ? dst[0] : dst[1]; Om = dst[2]; Ps = sym ? dst[2] : dst[3];
+      ld = nld;
+      CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     }
     DBuf leaf_gidx;
     {
@@ -1016,9 +1079,33 @@ struct Planner {
 
       phase(2);
       // ---- colour batches --------------------------------------------------
+      const bool stream_rows = host_in && lev == L;
+      auto issue_rows = [&](size_t bidx) {      // Y / Z rows of batch bidx: host -> device on cs
+        if (bidx >= binfo.size()) return;
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        hev.push_back(e);
+        if (bidx == 0) {       // the box records are uploaded on s
+          CK(cudaEventRecord(e, s));
+          CK(cudaStreamWaitEvent(cs, e, 0));
+        }
+        if (binfo[bidx].count > 0) {
+          dim3 g((unsigned)binfo[bidx].count, 2);
+          rsrs::host_rows_kernel<<<g, 256, 0, cs>>>(dboxes + binfo[bidx].first, hY, hZ, hld, Y, sym ? nullptr : Z,
+                                                    SC * ld, (int)(SC * nld));
+          post("host_rows_kernel", cs, launches);
+        }
+        CK(cudaEventRecord(e, cs));
+      };
+      if (stream_rows) issue_rows(0);
       for (const BInfo& bi : binfo) {
         const int n = bi.count, q0 = bi.first;
         BoxDev* dbx = dboxes + q0;
+        if (stream_rows) {
+          const size_t bidx = &bi - &binfo[0];
+          CK(cudaStreamWaitEvent(s, hev.back(), 0));   // this batch's rows have arrived
+          issue_rows(bidx + 1);                        // the next batch's rows overlap this batch
+        }
         rsrs::HaloPlan H;
         std::vector<int4> srecs;
         int64_t nsend = 0;
@@ -1099,7 +1186,7 @@ struct Planner {
             if (cplx) rsrs::pull_assemble_kernel<true><<<n, 256, 0, s>>>(dbx, dboxes, diws, dnbr, fpool, dws, !sym);
             else rsrs::pull_assemble_kernel<false><<<n, 256, 0, s>>>(dbx, dboxes, diws, dnbr, fpool, dws, !sym);
             post("pull_assemble_kernel", s, launches);
-            launch_nn(cplx, Dpull + ns * q0, ns * n, bi.max_nb, p, s, launches);
+            launch_nn(cplx, Dpull + ns * q0, ns * n, bi.max_nb, p, s, launches, 0, true);
             toc();
           }
           tic(KC_GRAM);
@@ -1126,7 +1213,7 @@ struct Planner {
           launch_back_any(cplx, Dchol + ns * q0, ns * n, bi.max_r, bi.max_nb, s, launches);
           toc();
           tic(KC_PROJ);
-          launch_nn(cplx, Dproj + ns * q0, ns * n, bi.max_nb, p, s, launches);
+          launch_nn(cplx, Dproj + ns * q0, ns * n, bi.max_nb, p, s, launches, 0, true);
           toc();
           tic(KC_HGRAM);
           launch_nt(cplx, Dh + ns * q0, ns * n, bi.max_nb, bi.max_nb, s, launches);
@@ -1143,21 +1230,16 @@ struct Planner {
           if (bi.max_nb <= rsrs::SK_MAX) launch_skinny(cplx, Def + 2 * ns * q0, 2 * ns * n, p, s, launches);
           else launch_nn(cplx, Def + 2 * ns * q0, 2 * ns * n, bi.max_nb, p, s, launches);
           if (use_blocks) {      // keep the Gram blocks equal to F Omega Omega^* F^* (the E/F on Omega_s)
-            const size_t bi_idx = &bi - &binfo[0];
-            const int nw = (int)(gwork_off[bi_idx + 1] - gwork_off[bi_idx]);
-            if (nw > 0) {
-              double* pO = gpool->as<double>();
-              double* pP = pO + SC * gpool_side;
-              const int2* wk = gwork_b.as<int2>() + gwork_off[bi_idx];
-              dim3 gu(nw, sides);
-              if (cplx)
-                rsrs::gblk_update_kernel<true><<<gu, 256, rsrs::gblk_smem<true>(), s>>>(dboxes, wk, gtab_b.as<rsrs::GBlk>(), pO, pP, fpool,
-                                                                   diws);
-              else
-                rsrs::gblk_update_kernel<false><<<gu, 256, rsrs::gblk_smem<false>(), s>>>(dboxes, wk, gtab_b.as<rsrs::GBlk>(), pO, pP, fpool,
-                                                                    diws);
-              post("gblk_update_kernel", s, launches);
-            }
+            double* pO = gpool->as<double>();
+            double* pP = pO + SC * gpool_side;
+            dim3 gu(n, sides);
+            if (cplx)
+              rsrs::gblk_update_box_kernel<true><<<gu, 256, rsrs::gblk_box_smem<true>(), s>>>(dbx, gps_b_ptr, gtab_b.as<rsrs::GBlk>(), pO, pP,
+                                                                   fpool, diws);
+            else
+              rsrs::gblk_update_box_kernel<false><<<gu, 256, rsrs::gblk_box_smem<false>(), s>>>(dbx, gps_b_ptr, gtab_b.as<rsrs::GBlk>(), pO, pP,
+                                                                    fpool, diws);
+            post("gblk_update_box_kernel", s, launches);
           }
           toc();
           {
@@ -1400,12 +1482,17 @@ struct Planner {
       stream_sync(s);
       flush_prof();
       if (g_trace && profile) {
-        fprintf(stderr, "[rsrs trace] level %d (%d boxes, %zu colour batches):", lev, nbox, binfo.size());
+        fprintf(stderr, "[rsrs trace] level %d (%d boxes, %zu colour batches; max n_b %d, max r %d): class ms/GF/TFs", lev,
+                nbox, binfo.size(), *std::max_element(nb_all.begin(), nb_all.end()),
+                *std::max_element(rmaxv.begin(), rmaxv.end()));
         for (int c = 0; c < RSRS_NUM_KERNEL_CLASSES; ++c)
-          if (lev_ms[c] > 0) fprintf(stderr, " %s %.2f", KC_NAMES[c], lev_ms[c]);
-        fprintf(stderr, " ms\n");
+          if (lev_ms[c] > 0)
+            fprintf(stderr, " | %s %.2f/%.0f/%.1f", KC_NAMES[c], lev_ms[c], (f->kc_flops[c] - lev_fl0[c]) / 1e9,
+                    (f->kc_flops[c] - lev_fl0[c]) / (lev_ms[c] * 1e9));
+        fprintf(stderr, "\n");
         for (double& v : lev_ms) v = 0;
       }
+      for (int c = 0; c < RSRS_NUM_KERNEL_CLASSES; ++c) lev_fl0[c] = f->kc_flops[c];
       Y = nY; Z = nZ; Om = nO; Ps = nP; ld = nld;
       gidx = ng;
       cur = nxt;
@@ -1519,7 +1606,7 @@ static rsrs_status factor_impl(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, v
   try {
     init_kernels();
     f = new rsrs_factor_s();
-    f->xtmp.devsync = f->mergebuf.devsync = true;
+    f->xtmp.devsync = f->mergebuf.devsync = f->bstage.devsync = true;
     const rsrs::Tree& T = t->t;
     f->dt = dt;
     f->cplx = (dt == RSRS_C128);
@@ -1566,6 +1653,24 @@ static rsrs_status factor_impl(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, v
     P.estimate = o.estimate_coupling != 0 || o.noise_factor > 0;
     P.theta = o.noise_factor;
     P.comm = (comm && comm->nranks > 1) ? comm : nullptr;
+    {
+      // pinned host arrays (e2e through the C ABI): the library keeps its own device store
+      cudaPointerAttributes at{};
+      const bool okY = cudaPointerGetAttributes(&at, Y) == cudaSuccess;
+      cudaGetLastError();
+      if (okY && at.type == cudaMemoryTypeUnregistered)
+        throw StatusError{RSRS_ERR_INVALID, "Y is pageable host memory: pass device arrays or pinned host arrays "
+                                            "(cudaHostAlloc / cudaHostRegister)"};
+      const bool hostY = okY && at.type == cudaMemoryTypeHost;
+      cudaPointerAttributes ao{};
+      const bool hostO = cudaPointerGetAttributes(&ao, Omega) == cudaSuccess && ao.type == cudaMemoryTypeHost;
+      cudaGetLastError();
+      if (hostY != hostO)
+        throw StatusError{RSRS_ERR_INVALID, "Y, Z, Omega, Psi must all be device arrays or all pinned host arrays"};
+      if (hostY && (P.comm || o.push_updates))
+        throw StatusError{RSRS_ERR_INVALID, "pinned host inputs need a single rank and pulled L/U updates"};
+      P.host_in = hostY;
+    }
     P.part = rsrs::make_partition(T, comm ? comm->nranks : 1, o.gather_level, o.top_level);
     P.run((double*)Y, (double*)Z, (double*)Omega, (double*)Psi, ld);
     CK(cudaEventRecord(e1, s));
@@ -1842,6 +1947,20 @@ static rsrs_status sweep_comm(rsrs_factorization f, void* Bv, int64_t ldb, int64
     double* B = (double*)Bv;
     const int64_t N = f->N;
     const int SC = f->sc;
+    // pinned host right-hand sides: staged through a device buffer (copies on the same stream)
+    cudaPointerAttributes at{};
+    const bool okB = cudaPointerGetAttributes(&at, Bv) == cudaSuccess;
+    cudaGetLastError();
+    if (okB && at.type == cudaMemoryTypeUnregistered)
+      return fail(RSRS_ERR_INVALID, std::string(who) + ": B is pageable host memory (pin it or pass a device array)");
+    const bool hostB = okB && at.type == cudaMemoryTypeHost;
+    double* Bh = nullptr;
+    if (hostB) {
+      Bh = B;
+      f->bstage.ensure(sizeof(double) * SC * N * ldb, s);
+      B = f->bstage.as<double>();
+      CK(cudaMemcpyAsync(B, Bh, sizeof(double) * SC * N * ldb, cudaMemcpyHostToDevice, s));
+    }
     f->xtmp.ensure(sizeof(double) * SC * N * nrhs, s);
     double* x = f->xtmp.as<double>();
     const int nr = (int)nrhs;
@@ -1859,6 +1978,7 @@ static rsrs_status sweep_comm(rsrs_factorization f, void* Bv, int64_t ldb, int64
       rsrs::permute_rows_kernel<<<grid, blk, 0, s>>>(x, SC * nrhs, B, SC * ldb, f->d_perm, N, SC * nr, 1);
       CK(cudaGetLastError());
     }
+    if (hostB) CK(cudaMemcpyAsync(Bh, B, sizeof(double) * SC * N * ldb, cudaMemcpyDeviceToHost, s));
     return RSRS_OK;
   } catch (const StatusError& e) {
     return fail(e.st, std::string(who) + ": " + e.msg);

@@ -541,13 +541,16 @@ __global__ void __launch_bounds__(256) apply_fwd_tri_kernel(const BoxDev* __rest
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int col = 0; col < nrhs; ++col) {
     for (int i = tid; i < nr; i += blockDim.x) xr[i] = x[(i64)red[i] * ldx + col];
-    for (int j = tid; j < nc; j += blockDim.x) xc[j] = x[(i64)cc[j] * ldx + col];
     __syncthreads();
     for (int s = tid; s < k; s += blockDim.x) {
       double v = 0.0;
       for (int i = 0; i < nr; ++i) v += T[(i64)i * ldn + s] * xr[i];
       x[(i64)skel[s] * ldx + col] += v;
     }
+    __syncthreads();
+    // c = near \ red holds b's skeletons: read x_c after the F update
+    for (int j = tid; j < nc; j += blockDim.x) xc[j] = x[(i64)cc[j] * ldx + col];
+    __syncthreads();
     for (int i = warp; i < nr; i += blockDim.x / 32) {
       double v = 0.0;
       for (int m = i + lane; m < nr; m += 32) v += Cf[(i64)m * ldn + i] * xr[m];
@@ -580,13 +583,16 @@ __global__ void __launch_bounds__(256) apply_bwd_tri_kernel(const BoxDev* __rest
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int col = 0; col < nrhs; ++col) {
     for (int i = tid; i < nr; i += blockDim.x) xr[i] = x[(i64)red[i] * ldx + col];
-    for (int s = tid; s < k; s += blockDim.x) xs[s] = x[(i64)skel[s] * ldx + col];
     __syncthreads();
     for (int j = tid; j < nc; j += blockDim.x) {
       double v = 0.0;
       for (int i = 0; i < nr; ++i) v += MU[(i64)i * ldr + j] * xr[i];
       x[(i64)cc[j] * ldx + col] += v;
     }
+    __syncthreads();
+    // the skeletons are part of c: read x_s after the L update
+    for (int s = tid; s < k; s += blockDim.x) xs[s] = x[(i64)skel[s] * ldx + col];
+    __syncthreads();
     for (int i = warp; i < nr; i += blockDim.x / 32) {
       double v = 0.0;
       for (int j = lane; j <= i; j += 32) v += Cf[(i64)i * ldn + j] * xr[j];

@@ -158,8 +158,8 @@ def _check_tensor(name, t, rows, min_cols=None, dtype=None, allow_1d=False, alig
     and (sample arrays: aligned_rows) 16-byte aligned rows (the kernels stage rows with 16-byte
     cp.async); right-hand sides only need the aligned base."""
     import torch
-    if not isinstance(t, torch.Tensor) or not t.is_cuda:
-        raise ValueError(f"{name} must be a CUDA tensor")
+    if not isinstance(t, torch.Tensor) or not (t.is_cuda or t.is_pinned()):
+        raise ValueError(f"{name} must be a CUDA tensor or a pinned host tensor")
     if dtype is not None and t.dtype != dtype:
         raise ValueError(f"{name} has dtype {t.dtype}, expected {dtype}")
     if t.dtype not in (torch.float64, torch.complex128):
@@ -362,6 +362,8 @@ def factor(tree: Tree, Y, Z, Omega, Psi, p: int, eps: float = 1e-6, level_growth
            push_updates: bool = False, estimate_coupling: bool = False,
            noise_factor: float = 0.0, triangular: bool = False) -> Factorization:
     """rsrs_factor on CUDA tensors (N x ld, tree order); Y, Z, Omega, Psi are OVERWRITTEN.
+    Pinned host tensors are also accepted (end-to-end use): the library copies them into its own
+    device store, overlapping the Y / Z rows with the leaf sweep, and leaves them unchanged.
 
     float64 tensors -> RSRS_F64, complex128 -> RSRS_C128 (ld in elements).
     Multi-GPU (nranks > 1): this rank's rows only (Tree.partition()) and the
@@ -383,6 +385,8 @@ def factor(tree: Tree, Y, Z, Omega, Psi, p: int, eps: float = 1e-6, level_growth
         _check_tensor(nm, t, rows, min_cols=p, dtype=Y.dtype)
         if t.stride(0) != ld:
             raise ValueError("Y, Z, Omega, Psi must share the leading dimension")
+        if t.is_cuda != Y.is_cuda:
+            raise ValueError("Y, Z, Omega, Psi must all be CUDA tensors or all pinned host tensors")
     if dtype is not None and dtype != code:
         raise ValueError("dtype does not match the tensors")
     dtype = code

@@ -167,3 +167,32 @@ def test_sampler_rows_match_direct_sum():
             # CUDA's j0/y0 are accurate to a few ulp; log / rsqrt to ~1 ulp
             tol = (1e-12 if cfg.is_complex else 1e-13) * np.abs(ref).max() * math.sqrt(N)
             assert np.abs(got - ref).max() <= tol, (cfg.name, adjoint)
+
+
+@pytest.mark.parametrize("name,n", [("c1", None), ("c3", 8192), ("c4", 64)], ids=["c1", "sphere8k", "c4_64"])
+def test_pinned_host_inputs_bit_identical(name, n):
+    """rsrs_factor / rsrs_solve on pinned HOST arrays (the e2e path: the library copies Omega / Psi and
+    streams the Y / Z rows of each leaf colour batch one batch ahead) give bit for bit the device-input
+    factorization, and leave the host inputs unchanged."""
+    import torch
+
+    import paper_2311_01451_b200 as R
+    cfg = W.CONFIGS[name] if n is None else W.CONFIGS[name].scaled(n)
+    X, A, Y, Z, Om, Ps, b = dense_problem(cfg)
+    t = R.Tree(X, cfg.leaf, *cfg.root())
+    perm = t.perm()
+    H = [torch.from_numpy(np.ascontiguousarray(M[perm])).pin_memory() for M in (Y, Z, Om, Ps)]
+    H0 = [h.clone() for h in H]
+    D = [h.cuda() for h in H]
+    kw = dict(p=cfg.p, eps=cfg.eps, level_growth=cfg.g, id_scale=cfg.c_id, oversample=cfg.l)
+    fd = R.factor(t, *D, **kw)
+    fh = R.factor(t, *H, **kw)
+    assert all(torch.equal(h, h0) for h, h0 in zip(H, H0))
+    xd = torch.from_numpy(b.copy()).cuda()
+    fd.solve(xd)
+    xh = torch.from_numpy(b.copy()).pin_memory()
+    fh.solve(xh)
+    torch.cuda.synchronize()
+    assert np.array_equal(xd.cpu().numpy(), xh.numpy())
+    with pytest.raises(ValueError):
+        R.factor(t, H[0], D[1], H[2], H[3], **kw)          # mixed host / device
