@@ -426,7 +426,10 @@ def run_native(args, rank, world, local, pg):
         h2d = sum(t.numel() * t.element_size() for t in host) + hb.numel() * hb.element_size()
         d2h = hx.numel() * hx.element_size()
         del work[:]
+        f = None
         torch.cuda.empty_cache()
+        import paper_2311_01451_b200 as R
+        R.release_memory()          # idle arena chunks back to the driver (host mode owns a device store)
         barrier(pg, dev)
         torch.cuda.synchronize(dev)
         g0 = torch.cuda.Event(enable_timing=True)

@@ -46,7 +46,13 @@ class Arena {
           sz = bytes;
         } else {
           cudaGetLastError();
-          return nullptr;
+          // fragmented: hand the wholly idle chunks back to the driver and try once more
+          release_idle_locked();
+          sz = bytes;
+          if (cudaMalloc(&p, sz) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+          }
         }
       }
       chunks_.push_back({(char*)p, sz});
@@ -88,6 +94,13 @@ class Arena {
   // return wholly idle chunks to the driver
   void release_idle() {
     std::lock_guard<std::mutex> lk(mu_);
+    release_idle_locked();
+  }
+  size_t reserved() const { return reserved_; }
+  size_t in_use() const { return in_use_; }
+
+ private:
+  void release_idle_locked() {
     std::vector<Chunk> keep;
     for (const Chunk& c : chunks_) {
       auto it = free_by_addr_.find(c.base);
@@ -101,10 +114,6 @@ class Arena {
     }
     chunks_ = keep;
   }
-  size_t reserved() const { return reserved_; }
-  size_t in_use() const { return in_use_; }
-
- private:
   struct Chunk {
     char* base;
     size_t size;

@@ -74,7 +74,7 @@ constexpr int SMEM_MAX = 227 * 1024 - 1024;  // dynamic-smem budget of the large
 int g_optin = 0;
 bool g_debug = false;  // RSRS_DEBUG_SYNC=1: synchronize and check after every launch
 bool g_trace = false;  // RSRS_TRACE=1: host-side time split of rsrs_factor on stderr
-bool g_wide_nt = false; // RSRS_WIDE_NT=1: keep the 32 x 64 NT tiles for small boxes (A/B timing of the narrow tiles)
+int g_skinny_cols = rsrs::SK_COLS;   // RSRS_SKINNY_COLS: columns per CTA of the skinny E/F kernel
 
 // host-side time split of one rsrs_factor (RSRS_TRACE)
 struct HostTrace {
@@ -123,7 +123,6 @@ void set_smem_both() {
   set_smem(rsrs::top_solve_kernel<C>, -1);
   set_smem(rsrs::top_apply_kernel<C>, -1);
   set_smem(rsrs::gblk_update_kernel<C>, rsrs::gblk_smem<C>());
-  set_smem(rsrs::gblk_update_box_kernel<C>, rsrs::gblk_box_smem<C>());
   set_smem(rsrs::skinny_nn_kernel<C>, rsrs::skinny_smem<C>());
 }
 
@@ -134,16 +133,11 @@ void init_kernels() {
   g_debug = dbg && dbg[0] == '1';
   const char* tr = getenv("RSRS_TRACE");
   g_trace = tr && tr[0] == '1';
-  const char* wn = getenv("RSRS_WIDE_NT");
-  g_wide_nt = wn && wn[0] == '1';
+  if (const char* sc = getenv("RSRS_SKINNY_COLS")) g_skinny_cols = std::max(128, (atoi(sc) / 128) * 128);
   int dev = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&g_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   set_smem(rsrs::gemm_nt_kernel<64>, rsrs::NT_SMEM);
-  set_smem(rsrs::gemm_nt_narrow_kernel<16>, rsrs::nt_narrow_smem(16));
-  set_smem(rsrs::gemm_nn_narrow_kernel<16>, rsrs::nn_narrow_smem(16));
-  set_smem(rsrs::gemm_nn_narrow_kernel<32>, rsrs::nn_narrow_smem(32));
-  set_smem(rsrs::gemm_nt_narrow_kernel<32>, rsrs::nt_narrow_smem(32));
   set_smem(rsrs::gemm_nn_kernel<64>, rsrs::NN_SMEM);
   set_smem(rsrs::gemm_nt_kernel_c<64>, rsrs::NT_SMEM);
   set_smem(rsrs::gemm_nn_kernel_c<64>, rsrs::NN_SMEM);
@@ -273,14 +267,6 @@ void launch_nt(bool cplx, const NTDesc* d, int n, int mmax, int nmax, cudaStream
     for (int i = 0; i < n; i += ZMAX) launch_nt(cplx, d + i, std::min(ZMAX, n - i), mmax, nmax, s, launches);
     return;
   }
-  if (!cplx && mmax <= 32 && !g_wide_nt) {
-    // small boxes: transposed narrow tiles (only the short side is padded, to 16 / 32)
-    dim3 g2((nmax + 63) / 64, 1, n);
-    if (mmax <= 16) rsrs::gemm_nt_narrow_kernel<16><<<g2, 128, rsrs::nt_narrow_smem(16), s>>>(d);
-    else rsrs::gemm_nt_narrow_kernel<32><<<g2, 128, rsrs::nt_narrow_smem(32), s>>>(d);
-    post("gemm_nt_narrow", s, launches);
-    return;
-  }
   const int TN = cplx ? rsrs::GTC : rsrs::GT;
   const int TM = mmax <= 32 ? 32 : 64;
   dim3 grid((nmax + TN - 1) / TN, (mmax + TM - 1) / TM, n);
@@ -295,19 +281,8 @@ void launch_nt(bool cplx, const NTDesc* d, int n, int mmax, int nmax, cudaStream
 }
 
 void launch_nn(bool cplx, const NNDesc* d, int n, int mmax, int nmax, cudaStream_t s, int64_t& launches,
-               int force_tm = 0, bool narrow_ok = false) {
+               int force_tm = 0) {
   if (n <= 0 || mmax <= 0 || nmax <= 0) return;
-  if (narrow_ok && !cplx && mmax <= 32 && !g_wide_nt && force_tm == 0) {
-    // small boxes, transA = 0 (projection, pulled L/U update): transposed narrow tiles
-    constexpr int ZMAX = 65535;
-    for (int i = 0; i < n; i += ZMAX) {
-      dim3 g2((nmax + 63) / 64, 1, std::min(ZMAX, n - i));
-      if (mmax <= 16) rsrs::gemm_nn_narrow_kernel<16><<<g2, 128, rsrs::nn_narrow_smem(16), s>>>(d + i);
-      else rsrs::gemm_nn_narrow_kernel<32><<<g2, 128, rsrs::nn_narrow_smem(32), s>>>(d + i);
-      post("gemm_nn_narrow", s, launches);
-    }
-    return;
-  }
   constexpr int ZMAX = 65535;
   if (n > ZMAX) {
     for (int i = 0; i < n; i += ZMAX)
@@ -330,9 +305,10 @@ void launch_nn(bool cplx, const NNDesc* d, int n, int mmax, int nmax, cudaStream
 // in-place skinny updates (E/F), see gemm.cuh
 void launch_skinny(bool cplx, const NNDesc* d, int n, int ncols, cudaStream_t s, int64_t& launches) {
   if (n <= 0 || ncols <= 0) return;
-  dim3 grid(n, (ncols + rsrs::SK_COLS - 1) / rsrs::SK_COLS);
-  if (cplx) rsrs::skinny_nn_kernel<true><<<grid, 128, rsrs::skinny_smem<true>(), s>>>(d);
-  else rsrs::skinny_nn_kernel<false><<<grid, 128, rsrs::skinny_smem<false>(), s>>>(d);
+  const int cols = g_skinny_cols;
+  dim3 grid(n, (ncols + cols - 1) / cols);
+  if (cplx) rsrs::skinny_nn_kernel<true><<<grid, 128, rsrs::skinny_smem<true>(), s>>>(d, cols);
+  else rsrs::skinny_nn_kernel<false><<<grid, 128, rsrs::skinny_smem<false>(), s>>>(d, cols);
   post("skinny_nn", s, launches);
 }
 
@@ -1186,22 +1162,24 @@ struct Planner {
             if (cplx) rsrs::pull_assemble_kernel<true><<<n, 256, 0, s>>>(dbx, dboxes, diws, dnbr, fpool, dws, !sym);
             else rsrs::pull_assemble_kernel<false><<<n, 256, 0, s>>>(dbx, dboxes, diws, dnbr, fpool, dws, !sym);
             post("pull_assemble_kernel", s, launches);
-            launch_nn(cplx, Dpull + ns * q0, ns * n, bi.max_nb, p, s, launches, 0, true);
+            launch_nn(cplx, Dpull + ns * q0, ns * n, bi.max_nb, p, s, launches);
             toc();
           }
           tic(KC_GRAM);
           if (use_blocks) {
             launch_nt(cplx, Dgram + gpb * q0, gpb * n, bi.max_nb, bi.max_r, s, launches);
-            dim3 ga(n, max_nnbr);
             double* pO = gpool->as<double>();
             double* pP = pO + SC * gpool_side;
-            if (cplx)
-              rsrs::gram_assemble_kernel<true><<<ga, 256, rsrs::gram_assemble_smem(bi.max_r), s>>>(dbx, dboxes, diws, dnbr, gtab_b.as<rsrs::GBlk>(),
-                                                                  gps_b_ptr, pO, pP, dws, sides);
-            else
-              rsrs::gram_assemble_kernel<false><<<ga, 256, rsrs::gram_assemble_smem(bi.max_r), s>>>(dbx, dboxes, diws, dnbr, gtab_b.as<rsrs::GBlk>(),
-                                                                   gps_b_ptr, pO, pP, dws, sides);
-            post("gram_assemble_kernel", s, launches);
+            {
+              dim3 ga(n, max_nnbr);
+              if (cplx)
+                rsrs::gram_assemble_kernel<true><<<ga, 256, rsrs::gram_assemble_smem(bi.max_r), s>>>(dbx, dboxes, diws, dnbr, gtab_b.as<rsrs::GBlk>(),
+                                                                    gps_b_ptr, pO, pP, dws, sides);
+              else
+                rsrs::gram_assemble_kernel<false><<<ga, 256, rsrs::gram_assemble_smem(bi.max_r), s>>>(dbx, dboxes, diws, dnbr, gtab_b.as<rsrs::GBlk>(),
+                                                                     gps_b_ptr, pO, pP, dws, sides);
+              post("gram_assemble_kernel", s, launches);
+            }
           } else {
             launch_nt(cplx, Dgram + gpb * q0, gpb * n, bi.max_r, bi.max_r, s, launches);
           }
@@ -1213,7 +1191,7 @@ struct Planner {
           launch_back_any(cplx, Dchol + ns * q0, ns * n, bi.max_r, bi.max_nb, s, launches);
           toc();
           tic(KC_PROJ);
-          launch_nn(cplx, Dproj + ns * q0, ns * n, bi.max_nb, p, s, launches, 0, true);
+          launch_nn(cplx, Dproj + ns * q0, ns * n, bi.max_nb, p, s, launches);
           toc();
           tic(KC_HGRAM);
           launch_nt(cplx, Dh + ns * q0, ns * n, bi.max_nb, bi.max_nb, s, launches);
@@ -1230,16 +1208,21 @@ struct Planner {
           if (bi.max_nb <= rsrs::SK_MAX) launch_skinny(cplx, Def + 2 * ns * q0, 2 * ns * n, p, s, launches);
           else launch_nn(cplx, Def + 2 * ns * q0, 2 * ns * n, bi.max_nb, p, s, launches);
           if (use_blocks) {      // keep the Gram blocks equal to F Omega Omega^* F^* (the E/F on Omega_s)
-            double* pO = gpool->as<double>();
-            double* pP = pO + SC * gpool_side;
-            dim3 gu(n, sides);
-            if (cplx)
-              rsrs::gblk_update_box_kernel<true><<<gu, 256, rsrs::gblk_box_smem<true>(), s>>>(dbx, gps_b_ptr, gtab_b.as<rsrs::GBlk>(), pO, pP,
-                                                                   fpool, diws);
-            else
-              rsrs::gblk_update_box_kernel<false><<<gu, 256, rsrs::gblk_box_smem<false>(), s>>>(dbx, gps_b_ptr, gtab_b.as<rsrs::GBlk>(), pO, pP,
-                                                                    fpool, diws);
-            post("gblk_update_box_kernel", s, launches);
+            const size_t bi_idx = &bi - &binfo[0];
+            const int nw = (int)(gwork_off[bi_idx + 1] - gwork_off[bi_idx]);
+            if (nw > 0) {
+              double* pO = gpool->as<double>();
+              double* pP = pO + SC * gpool_side;
+              const int2* wk = gwork_b.as<int2>() + gwork_off[bi_idx];
+              dim3 gu(nw, sides);
+              if (cplx)
+                rsrs::gblk_update_kernel<true><<<gu, 256, rsrs::gblk_smem<true>(), s>>>(dboxes, wk, gtab_b.as<rsrs::GBlk>(), pO, pP, fpool,
+                                                                   diws);
+              else
+                rsrs::gblk_update_kernel<false><<<gu, 256, rsrs::gblk_smem<false>(), s>>>(dboxes, wk, gtab_b.as<rsrs::GBlk>(), pO, pP, fpool,
+                                                                    diws);
+              post("gblk_update_kernel", s, launches);
+            }
           }
           toc();
           {

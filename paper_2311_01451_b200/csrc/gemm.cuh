@@ -28,242 +28,6 @@ constexpr int nn_smem(int TM, bool C) { return 2 * (TM * GPA + (C ? GBK / 2 : GB
 // dynamic size: min(cap, *p - off) when p is set, else cap
 RSRS_DI int dyn(const int* p, int off, int cap) { return p ? min(cap, *p - off) : cap; }
 
-// Narrow NT tile for small boxes (the sphere's leaves hold ~15 points): C = alpha A_rows B_rows^T
-// with m = |A rows| <= TN (16 or 32) is computed TRANSPOSED, C^T = B_rows A_rows^T, so that the
-// long gathered dimension (n: near-field / partner rows) fills the 64-row side of the tile and only
-// the short one is padded (to 16 or 32 instead of 32 or 64).  One 64 x TN tile of C^T per CTA,
-// 4 warps x (16 x TN), two-stage cp.async; the epilogue stores C[i][j] (i < m, j < n).
-// Grid: (ceil(n / 64), 1, descriptors).
-template <int TN>
-RSRS_DI void nt_tile_narrow(const NTDesc& d, int m, int n, int K, int j0, double* smem) {
-  constexpr int NTT = TN / 8, QB = TN / 8;
-  double* Ws = smem;                       // [2][64][GPA]   wide operand: B rows j0 .. j0 + 64
-  double* Ns = smem + 2 * 64 * GPA;        // [2][TN][GPA]   narrow operand: A rows 0 .. m
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int gid = lane >> 2, tig = lane & 3;
-  const double* wptr[8];
-  const double* nptr[QB];
-  bool wval[8], nval[QB];
-  const int lrow = tid >> 4, kc = (tid & 15) * 2;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int gj = j0 + lrow + 8 * q;
-    wval[q] = gj < n;
-    const i64 br = wval[q] ? (d.rowB ? (i64)d.rowB[gj] : (i64)gj) : 0;
-    wptr[q] = d.B + br * d.ldb;
-  }
-#pragma unroll
-  for (int q = 0; q < QB; ++q) {
-    const int gi = lrow + 8 * q;
-    nval[q] = gi < m;
-    const i64 ar = nval[q] ? (d.rowA ? (i64)d.rowA[gi] : (i64)gi) : 0;
-    nptr[q] = d.A + ar * d.lda;
-  }
-  auto load_stage = [&](int s, int kt) {
-    const int k = kt * GBK + kc;
-    const int bytes = (k + 2 <= K) ? 16 : (k < K ? 8 : 0);
-    const int koff = bytes ? k : 0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      cp_async16(&Ws[(s * 64 + lrow + 8 * q) * GPA + kc], wptr[q] + koff, wval[q] ? bytes : 0);
-#pragma unroll
-    for (int q = 0; q < QB; ++q)
-      cp_async16(&Ns[(s * TN + lrow + 8 * q) * GPA + kc], nptr[q] + koff, nval[q] ? bytes : 0);
-  };
-  double acc[2][NTT][2];
-#pragma unroll
-  for (int t = 0; t < 2; ++t)
-#pragma unroll
-    for (int u = 0; u < NTT; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
-  const bool wact = j0 + warp * 16 < n;
-  const int nk = (K + GBK - 1) / GBK;
-  if (nk > 0) {
-    load_stage(0, 0);
-    cp_async_commit();
-  }
-  for (int kt = 0; kt < nk; ++kt) {
-    if (kt + 1 < nk) {
-      load_stage((kt + 1) & 1, kt + 1);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const double* ws = Ws + ((kt & 1) * 64 + warp * 16) * GPA;
-    const double* ns = Ns + (kt & 1) * TN * GPA;
-    if (wact) {
-#pragma unroll
-      for (int kk = 0; kk < GBK / 4; ++kk) {
-        double a[2], b[NTT];
-#pragma unroll
-        for (int t = 0; t < 2; ++t) a[t] = ws[(t * 8 + gid) * GPA + kk * 4 + tig];
-#pragma unroll
-        for (int u = 0; u < NTT; ++u) b[u] = ns[(u * 8 + gid) * GPA + kk * 4 + tig];
-#pragma unroll
-        for (int t = 0; t < 2; ++t)
-#pragma unroll
-          for (int u = 0; u < NTT; ++u) dmma884(acc[t][u][0], acc[t][u][1], a[t], b[u]);
-      }
-    }
-    __syncthreads();
-  }
-  // acc[t][u][e] = C^T(j0 + warp*16 + t*8 + gid, u*8 + 2*tig + e) = C(u*8 + 2*tig + e, j)
-#pragma unroll
-  for (int t = 0; t < 2; ++t) {
-    const int j = j0 + warp * 16 + t * 8 + gid;
-    if (j >= n) continue;
-#pragma unroll
-    for (int u = 0; u < NTT; ++u)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int i = u * 8 + 2 * tig + e;
-        if (i < m) {
-          double* cp = d.C + (i64)i * d.ldc + j;
-          *cp = (d.beta != 0.0 ? d.beta * *cp : 0.0) + d.alpha * acc[t][u][e];
-        }
-      }
-  }
-}
-
-template <int TN>
-__global__ void __launch_bounds__(128) gemm_nt_narrow_kernel(const NTDesc* __restrict__ descs) {
-  extern __shared__ __align__(16) double smem[];
-  const NTDesc& d = descs[blockIdx.z];
-  const int m = dyn(d.pm, 0, d.m);
-  const int n = dyn(d.pn, 0, d.n);
-  const int j0 = blockIdx.x * 64;
-  if (m <= 0 || j0 >= n) return;
-  const NTDesc dl = d;
-  nt_tile_narrow<TN>(dl, m, n, d.K, j0, smem);
-}
-constexpr int nt_narrow_smem(int TN) { return 2 * (64 + TN) * GPA * 8; }
-
-// Narrow NN tile for small boxes: D_rows = beta C_rows + alpha A B_rows with m <= TN (16 or 32)
-// rows and transA = 0 (projection Y'' = Y_b - W Omega_near, pulled L/U update), computed
-// TRANSPOSED, D^T = beta C^T + alpha B^T A^T: the long dimension (n = p columns) fills the 64-row
-// side of the tile, the short one (m) is padded only to TN.  The B tile [32 k][64 columns] is the
-// same coalesced row-gathered tile as in nn_tile; A^T fragments come from the [TN][32] A tile.
-// Grid: (ceil(n / 64), 1, descriptors).
-template <int TN>
-RSRS_DI void nn_tile_narrow(const NNDesc& d, int m, int n, int K, int j0, double* smem) {
-  constexpr int NTT = TN / 8, QA = TN / 8;
-  const bool inplace = (d.Cin == nullptr);
-  if (K <= 0 && inplace && d.beta == 1.0) return;
-  double* Ws = smem;                       // [2][32][GPB]  B rows (k) x 64 columns
-  double* Ns = smem + 2 * GBK * GPB;       // [2][TN][GPA]  A rows (m) x 32 k
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int gid = lane >> 2, tig = lane & 3;
-  int brow[8];
-  auto fetch_rows = [&](int kt) {
-    const int kr = tid >> 5;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int k = kt * GBK + kr + 4 * q;
-      brow[q] = k < K ? (d.rowB ? d.rowB[k] : k) : 0;
-    }
-  };
-  auto load_stage = [&](int s, int kt) {
-    const int k0 = kt * GBK;
-    {
-      const int lrow = tid >> 4, kc = (tid & 15) * 2;
-      const int k = k0 + kc;
-      const int bytes = (k + 2 <= K) ? 16 : (k < K ? 8 : 0);
-#pragma unroll
-      for (int q = 0; q < QA; ++q) {
-        const int row = lrow + 8 * q;
-        const bool v = row < m && bytes > 0;
-        const double* src = v ? d.A + (i64)row * d.lda + k : d.A;
-        cp_async16(&Ns[(s * TN + row) * GPA + kc], src, v ? bytes : 0);
-      }
-    }
-    {
-      const int kr = tid >> 5, jc = (tid & 31) * 2;
-      const int gj = j0 + jc;
-      const int cb = (gj + 2 <= n) ? 16 : (gj < n ? 8 : 0);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int kl = kr + 4 * q;
-        const int k = k0 + kl;
-        const bool v = k < K && cb > 0;
-        const double* src = v ? d.B + (i64)brow[q] * d.ldb + gj : d.B;
-        cp_async16(&Ws[(s * GBK + kl) * GPB + jc], src, v ? cb : 0);
-      }
-    }
-  };
-  double acc[2][NTT][2];
-#pragma unroll
-  for (int t = 0; t < 2; ++t)
-#pragma unroll
-    for (int u = 0; u < NTT; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
-  const bool wact = j0 + warp * 16 < n;
-  const int nk = K > 0 ? (K + GBK - 1) / GBK : 0;
-  if (nk > 0) {
-    fetch_rows(0);
-    load_stage(0, 0);
-    cp_async_commit();
-    if (nk > 1) fetch_rows(1);
-  }
-  for (int kt = 0; kt < nk; ++kt) {
-    if (kt + 1 < nk) {
-      load_stage((kt + 1) & 1, kt + 1);
-      cp_async_commit();
-      if (kt + 2 < nk) fetch_rows(kt + 2);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const double* ws = Ws + (kt & 1) * GBK * GPB + warp * 16;
-    const double* ns = Ns + (kt & 1) * TN * GPA;
-    if (wact)
-#pragma unroll
-      for (int kk = 0; kk < GBK / 4; ++kk) {
-        double a[2], b[NTT];
-#pragma unroll
-        for (int t = 0; t < 2; ++t) a[t] = ws[(kk * 4 + tig) * GPB + t * 8 + gid];
-#pragma unroll
-        for (int u = 0; u < NTT; ++u) b[u] = ns[(u * 8 + gid) * GPA + kk * 4 + tig];
-#pragma unroll
-        for (int t = 0; t < 2; ++t)
-#pragma unroll
-          for (int u = 0; u < NTT; ++u) dmma884(acc[t][u][0], acc[t][u][1], a[t], b[u]);
-      }
-    __syncthreads();
-  }
-  // acc[t][u][e] = (B^T A^T)(col j, row i) with j = j0 + warp*16 + t*8 + gid, i = u*8 + 2*tig + e
-#pragma unroll
-  for (int u = 0; u < NTT; ++u)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int i = u * 8 + 2 * tig + e;
-      if (i >= m) continue;
-      const i64 dr = d.rowD ? (i64)d.rowD[i] : (i64)i;
-      double* drow = d.D + dr * d.ldd;
-      const double* crow = drow;
-      if (!inplace) crow = d.Cin + (d.rowC ? (i64)d.rowC[i] : (i64)i) * d.ldc;
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        const int j = j0 + warp * 16 + t * 8 + gid;
-        if (j < n) drow[j] = (d.beta != 0.0 ? d.beta * crow[j] : 0.0) + d.alpha * acc[t][u][e];
-      }
-    }
-}
-
-template <int TN>
-__global__ void __launch_bounds__(128) gemm_nn_narrow_kernel(const NNDesc* __restrict__ descs) {
-  extern __shared__ __align__(16) double smem[];
-  const NNDesc& d = descs[blockIdx.z];
-  const int m = dyn(d.pm, 0, d.m);
-  const int n = dyn(d.pn, 0, d.n);
-  const int K = dyn(d.pK, 0, d.K);
-  const int j0 = blockIdx.x * 64;
-  if (m <= 0 || j0 >= n) return;
-  const NNDesc dl = d;
-  nn_tile_narrow<TN>(dl, m, n, K, j0, smem);
-}
-constexpr int nn_narrow_smem(int TN) { return 2 * (GBK * GPB + TN * GPA) * 8; }
-
 // One TM x 64 output tile (TM = 64 or 32 rows) of C = alpha A_rows B_rows^T + beta C (K columns).
 template <int TM = GT>
 RSRS_DI void nt_tile(const NTDesc& d, int m, int n, int K, int i0, int j0, double* smem) {
@@ -272,7 +36,11 @@ RSRS_DI void nt_tile(const NTDesc& d, int m, int n, int K, int i0, int j0, doubl
   double* Bs = smem + 2 * TM * GPA;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
-  const int wr = warp >> 1, wc = warp & 1;
+  // TM = 32 tiles of boxes with <= 16 rows: all four warps share the 16 rows and split the
+  // 64 columns (16 each) instead of two warps idling on empty rows (latency hiding)
+  const bool flat = (TM == 32) && (m - i0 <= 16);
+  const int wr = flat ? 0 : warp >> 1, wc = warp & 1;
+  const int cw = flat ? 16 : 32, cofs = flat ? warp * 16 : wc * 32;
 
   const double* aptr[QA];
   const double* bptr[8];
@@ -313,7 +81,7 @@ RSRS_DI void nt_tile(const NTDesc& d, int m, int n, int K, int i0, int j0, doubl
   bool wact;
   {
     const int sym = d.psym ? *d.psym : d.sym_rows;
-    const int rb = i0 + wr * (TM / 2), cb = j0 + wc * 32;
+    const int rb = i0 + wr * (TM / 2), cb = j0 + cofs;
     // (same condition as the tile-level skip: every row of the warp's band below sym_rows)
     wact = rb < m && cb < n && !(rb + TM / 2 <= sym && cb >= rb + TM / 2);
   }
@@ -333,7 +101,7 @@ RSRS_DI void nt_tile(const NTDesc& d, int m, int n, int K, int i0, int j0, doubl
     }
     __syncthreads();
     const double* as = As + ((kt & 1) * TM + wr * (TM / 2)) * GPA;
-    const double* bs = Bs + ((kt & 1) * GT + wc * 32) * GPA;
+    const double* bs = Bs + ((kt & 1) * GT + cofs) * GPA;
     if (wact) {
 #pragma unroll
       for (int kk = 0; kk < GBK / 4; ++kk) {
@@ -341,11 +109,12 @@ RSRS_DI void nt_tile(const NTDesc& d, int m, int n, int K, int i0, int j0, doubl
 #pragma unroll
         for (int t = 0; t < MT; ++t) a[t] = as[(t * 8 + gid) * GPA + kk * 4 + tig];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) b[u] = bs[(u * 8 + gid) * GPA + kk * 4 + tig];
+        for (int u = 0; u < 4; ++u) b[u] = (u * 8 < cw) ? bs[(u * 8 + gid) * GPA + kk * 4 + tig] : 0.0;
 #pragma unroll
         for (int t = 0; t < MT; ++t)
 #pragma unroll
-          for (int u = 0; u < 4; ++u) dmma884(acc[t][u][0], acc[t][u][1], a[t], b[u]);
+          for (int u = 0; u < 4; ++u)
+            if (u * 8 < cw) dmma884(acc[t][u][0], acc[t][u][1], a[t], b[u]);
       }
     }
     __syncthreads();
@@ -357,7 +126,8 @@ RSRS_DI void nt_tile(const NTDesc& d, int m, int n, int K, int i0, int j0, doubl
     double* crow = d.C + (i64)i * d.ldc;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int j = j0 + wc * 32 + u * 8 + 2 * tig;
+      if (u * 8 >= cw) continue;
+      const int j = j0 + cofs + u * 8 + 2 * tig;
       if (j + 1 < n) {
         double2 c = make_double2(0.0, 0.0);
         if (d.beta != 0.0) c = *reinterpret_cast<const double2*>(crow + j);
@@ -395,7 +165,9 @@ RSRS_DI void nn_tile(const NNDesc& d, int m, int n, int K, int i0, int j0, doubl
   double* Bs = smem + 2 * TM * GPA;        // [2][32][GPB]  (k, j)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
-  const int wr = warp >> 1, wc = warp & 1;
+  const bool flat = (TM == 32) && (m - i0 <= 16);   // see nt_tile
+  const int wr = flat ? 0 : warp >> 1, wc = warp & 1;
+  const int cw = flat ? 16 : 32, cofs = flat ? warp * 16 : wc * 32;
 
   // row indices of the B rows of the next stage to be loaded, fetched one stage ahead
   // so that the dependent index loads overlap the MMAs instead of stalling the cp.async
@@ -465,7 +237,7 @@ RSRS_DI void nn_tile(const NNDesc& d, int m, int n, int K, int i0, int j0, doubl
 #pragma unroll
     for (int u = 0; u < 4; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
   // a warp whose sub-tile lies wholly outside D (skinny or ragged rows) skips its MMAs
-  const bool wact = i0 + wr * (TM / 2) < m && j0 + wc * 32 < n;
+  const bool wact = i0 + wr * (TM / 2) < m && j0 + cofs < n;
 
   const int nk = K > 0 ? (K + GBK - 1) / GBK : 0;
   if (nk > 0) {
@@ -485,7 +257,7 @@ RSRS_DI void nn_tile(const NNDesc& d, int m, int n, int K, int i0, int j0, doubl
     }
     __syncthreads();
     const double* as = As + ((kt & 1) * TM + wr * (TM / 2)) * GPA;
-    const double* bs = Bs + (kt & 1) * GBK * GPB + wc * 32;
+    const double* bs = Bs + (kt & 1) * GBK * GPB + cofs;
     if (wact)
 #pragma unroll
       for (int kk = 0; kk < GBK / 4; ++kk) {
@@ -493,11 +265,12 @@ RSRS_DI void nn_tile(const NNDesc& d, int m, int n, int K, int i0, int j0, doubl
 #pragma unroll
         for (int t = 0; t < MT; ++t) a[t] = as[(t * 8 + gid) * GPA + kk * 4 + tig];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) b[u] = bs[(kk * 4 + tig) * GPB + u * 8 + gid];
+        for (int u = 0; u < 4; ++u) b[u] = (u * 8 < cw) ? bs[(kk * 4 + tig) * GPB + u * 8 + gid] : 0.0;
 #pragma unroll
         for (int t = 0; t < MT; ++t)
 #pragma unroll
-          for (int u = 0; u < 4; ++u) dmma884(acc[t][u][0], acc[t][u][1], a[t], b[u]);
+          for (int u = 0; u < 4; ++u)
+            if (u * 8 < cw) dmma884(acc[t][u][0], acc[t][u][1], a[t], b[u]);
       }
     __syncthreads();
   }
@@ -517,7 +290,8 @@ RSRS_DI void nn_tile(const NNDesc& d, int m, int n, int K, int i0, int j0, doubl
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int j = j0 + wc * 32 + u * 8 + 2 * tig;
+      if (u * 8 >= cw) continue;
+      const int j = j0 + cofs + u * 8 + 2 * tig;
       if (j + 1 < n) {
         double2 c = make_double2(0.0, 0.0);
         if (d.beta != 0.0) c = *reinterpret_cast<const double2*>(crow + j);
@@ -850,16 +624,16 @@ template <bool C> constexpr int tile_n() { return C ? GTC : GT; }
 // 16 output rows per pass, reading each B row once per pass (coalesced over columns).
 // Grid (descriptors, column chunks); dynamic shared memory skinny_smem<C>().
 constexpr int SK_MAX = 64;
-constexpr int SK_COLS = 512;   // columns per CTA
+constexpr int SK_COLS = 128;   // default columns per CTA (RSRS_SKINNY_COLS overrides; multiple of 128)
 template <bool C> constexpr int skinny_smem() { return SK_MAX * SK_MAX * (C ? 16 : 8) + 2 * SK_MAX * 4; }
 template <bool C>
-__global__ void __launch_bounds__(128) skinny_nn_kernel(const NNDesc* __restrict__ descs) {
+__global__ void __launch_bounds__(128) skinny_nn_kernel(const NNDesc* __restrict__ descs, int cols) {
   typedef typename ScalarOf<C>::T S;
   extern __shared__ __align__(16) double ssm[];
   S* As = reinterpret_cast<S*>(ssm);
   const NNDesc& d = descs[blockIdx.x];
   const int m = dyn(d.pm, 0, d.m), n = dyn(d.pn, 0, d.n), K = dyn(d.pK, 0, d.K);
-  if (m <= 0 || K <= 0 || (int)blockIdx.y * SK_COLS >= n) return;
+  if (m <= 0 || K <= 0 || (int)blockIdx.y * cols >= n) return;
   const int mp = (m + 15) & ~15;
   const S* A = reinterpret_cast<const S*>(d.A);
   const S zero = s_zero(S());
@@ -877,7 +651,7 @@ __global__ void __launch_bounds__(128) skinny_nn_kernel(const NNDesc* __restrict
   const S* B = reinterpret_cast<const S*>(d.B);
   S* D = reinterpret_cast<S*>(d.D);
   // SK_COLS columns per CTA (the staged opA serves all of them), one column per thread per pass
-  for (int j = blockIdx.y * SK_COLS + threadIdx.x; j < min(n, (int)(blockIdx.y + 1) * SK_COLS); j += 128) {
+  for (int j = blockIdx.y * cols + threadIdx.x; j < min(n, (int)(blockIdx.y + 1) * cols); j += 128) {
     for (int i0 = 0; i0 < m; i0 += 16) {
       S acc[16];
 #pragma unroll

@@ -147,64 +147,6 @@ __global__ void __launch_bounds__(256) gblk_update_kernel(const BoxDev* __restri
     }
 }
 
-// Same update, one CTA per eliminated box (grid: boxes of the colour batch x sides): T and the
-// skeleton / redundant positions are staged once, then each warp takes whole blocks of the
-// box's partner list and updates them in place in global memory (rows: lanes over columns;
-// columns: lanes over rows).  Replaces one CTA per (box, block) work item -- ~50 tiny CTAs
-// per box on the sphere's leaf level, where the block update was launch-rate bound.
-template <bool C> constexpr int gblk_box_smem() { return GB_MAX * GB_MAX * (C ? 16 : 8); }
-template <bool C>
-__global__ void __launch_bounds__(256) gblk_update_box_kernel(const BoxDev* __restrict__ boxes,
-                                                              const int* __restrict__ gpstart,
-                                                              const GBlk* __restrict__ tab, double* __restrict__ poolO,
-                                                              double* __restrict__ poolP,
-                                                              const double* __restrict__ fpoold,
-                                                              const int* __restrict__ iws) {
-  typedef typename ScalarOf<C>::T S;
-  extern __shared__ __align__(16) double gbs[];
-  S* Ts = reinterpret_cast<S*>(gbs);   // T^* staged as [q][i] (k x n_r): gblk_box_smem<C>() bytes
-  __shared__ int skl[GB_MAX], red[GB_MAX];
-  const BoxDev& b = boxes[blockIdx.x];
-  const int k = b.k, nr = b.nr;
-  if (b.status != ST_OK || nr <= 0 || k <= 0) return;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const S* T = reinterpret_cast<const S*>(fpoold) + b.f_T;
-  for (int idx = tid; idx < nr * k; idx += 256) {
-    const int i = idx / k, q = idx % k;
-    Ts[q * GB_MAX + i] = T[(i64)i * b.ldn + q];
-  }
-  for (int q = tid; q < k; q += 256) skl[q] = iws[b.off_skelrow + q] - b.row0;
-  for (int i = tid; i < nr; i += 256) red[i] = iws[b.off_redrow + i] - b.row0;
-  __syncthreads();
-  S* pool = reinterpret_cast<S*>(blockIdx.y ? poolP : poolO);
-  const int t0 = gpstart[b.box], t1 = gpstart[b.box + 1];
-  for (int t = t0 + warp; t < t1; t += 8) {
-    const GBlk e = tab[t];
-    S* B = pool + e.off;
-    if (e.mode != 1) {   // rows: B[s, :] += T^* B[r, :]   (red and skel rows are disjoint)
-      for (int c = lane; c < e.ncol; c += 32) {
-        for (int q = 0; q < k; ++q) {
-          S acc = B[(i64)skl[q] * e.ld + c];
-          for (int i = 0; i < nr; ++i) acc = s_add(acc, s_mul(s_conj(Ts[q * GB_MAX + i]), B[(i64)red[i] * e.ld + c]));
-          B[(i64)skl[q] * e.ld + c] = acc;
-        }
-      }
-      __syncwarp();
-    }
-    if (e.mode != 0) {   // columns: B[:, s] += B[:, r] T
-      for (int r = lane; r < e.nrow; r += 32) {
-        S* row = B + (i64)r * e.ld;
-        for (int q = 0; q < k; ++q) {
-          S acc = row[skl[q]];
-          for (int i = 0; i < nr; ++i) acc = s_add(acc, s_mul(row[red[i]], Ts[q * GB_MAX + i]));
-          row[skl[q]] = acc;
-        }
-      }
-      __syncwarp();
-    }
-  }
-}
-
 // C_b[pos(q1) + a, pos(q2) + c] = G(n_q1, n_q2)[act_q1[a], act_q2[c]] for slots q2 <= q1
 // of b's neighbour list (the lower block triangle of the near-field Gram).
 // Grid (boxes of the batch, neighbour slots q1).  The slot table, the partner entries
