@@ -1066,10 +1066,37 @@ struct Planner {
           CK(cudaStreamWaitEvent(cs, e, 0));
         }
         if (binfo[bidx].count > 0) {
-          dim3 g((unsigned)binfo[bidx].count, 2);
-          rsrs::host_rows_kernel<<<g, 256, 0, cs>>>(dboxes + binfo[bidx].first, hY, hZ, hld, Y, sym ? nullptr : Z,
-                                                    SC * ld, (int)(SC * nld));
-          post("host_rows_kernel", cs, launches);
+          if (hld == SC * ld) {
+            // same row pitch on host and device: every box is one contiguous block per array,
+            // copied by the DMA engines in one batched call (no SMs taken from the sweep)
+            std::vector<void*> dsts, srcs;
+            std::vector<size_t> sizes;
+            for (int q = binfo[bidx].first; q < binfo[bidx].first + binfo[bidx].count; ++q) {
+              const i64 off = SC * (i64)hb[q].row0 * ld;
+              const size_t bytes = sizeof(double) * SC * (size_t)hb[q].nb * ld;
+              if (!bytes) continue;
+              dsts.push_back(Y + off);
+              srcs.push_back(const_cast<double*>(hY) + off);
+              sizes.push_back(bytes);
+              if (!sym) {
+                dsts.push_back(Z + off);
+                srcs.push_back(const_cast<double*>(hZ) + off);
+                sizes.push_back(bytes);
+              }
+            }
+            if (!sizes.empty()) {
+              cudaMemcpyAttributes at{};
+              at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+              at.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+              size_t aidx = 0, fidx = 0;
+              CK(cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), sizes.size(), &at, &aidx, 1, &fidx, cs));
+            }
+          } else {
+            dim3 g((unsigned)binfo[bidx].count, 2);
+            rsrs::host_rows_kernel<<<g, 256, 0, cs>>>(dboxes + binfo[bidx].first, hY, hZ, hld, Y, sym ? nullptr : Z,
+                                                      SC * ld, (int)(SC * nld));
+            post("host_rows_kernel", cs, launches);
+          }
         }
         CK(cudaEventRecord(e, cs));
       };
