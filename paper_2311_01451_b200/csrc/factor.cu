@@ -75,6 +75,7 @@ int g_optin = 0;
 bool g_debug = false;  // RSRS_DEBUG_SYNC=1: synchronize and check after every launch
 bool g_trace = false;  // RSRS_TRACE=1: host-side time split of rsrs_factor on stderr
 int g_skinny_cols = rsrs::SK_COLS;   // RSRS_SKINNY_COLS: columns per CTA of the skinny E/F kernel
+bool g_host_copy_kernel = false;     // RSRS_HOST_COPY=kernel: host-input rows by the zero-copy gather kernel
 
 // host-side time split of one rsrs_factor (RSRS_TRACE)
 struct HostTrace {
@@ -134,6 +135,7 @@ void init_kernels() {
   const char* tr = getenv("RSRS_TRACE");
   g_trace = tr && tr[0] == '1';
   if (const char* sc = getenv("RSRS_SKINNY_COLS")) g_skinny_cols = std::max(128, (atoi(sc) / 128) * 128);
+  if (const char* hc = getenv("RSRS_HOST_COPY")) g_host_copy_kernel = std::string(hc) == "kernel";
   int dev = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&g_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
@@ -1066,30 +1068,16 @@ struct Planner {
           CK(cudaStreamWaitEvent(cs, e, 0));
         }
         if (binfo[bidx].count > 0) {
-          if (hld == SC * ld) {
+          if (hld == SC * ld && !g_host_copy_kernel) {
             // same row pitch on host and device: every box is one contiguous block per array,
-            // copied by the DMA engines in one batched call (no SMs taken from the sweep)
-            std::vector<void*> dsts, srcs;
-            std::vector<size_t> sizes;
+            // copied by the DMA engines (one cudaMemcpyAsync per box and array, no SMs taken)
+            const size_t W8 = sizeof(double) * SC * (size_t)ld;
             for (int q = binfo[bidx].first; q < binfo[bidx].first + binfo[bidx].count; ++q) {
               const i64 off = SC * (i64)hb[q].row0 * ld;
-              const size_t bytes = sizeof(double) * SC * (size_t)hb[q].nb * ld;
+              const size_t bytes = W8 * (size_t)hb[q].nb;
               if (!bytes) continue;
-              dsts.push_back(Y + off);
-              srcs.push_back(const_cast<double*>(hY) + off);
-              sizes.push_back(bytes);
-              if (!sym) {
-                dsts.push_back(Z + off);
-                srcs.push_back(const_cast<double*>(hZ) + off);
-                sizes.push_back(bytes);
-              }
-            }
-            if (!sizes.empty()) {
-              cudaMemcpyAttributes at{};
-              at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-              at.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-              size_t aidx = 0, fidx = 0;
-              CK(cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), sizes.size(), &at, &aidx, 1, &fidx, cs));
+              CK(cudaMemcpyAsync(Y + off, hY + off, bytes, cudaMemcpyHostToDevice, cs));
+              if (!sym) CK(cudaMemcpyAsync(Z + off, hZ + off, bytes, cudaMemcpyHostToDevice, cs));
             }
           } else {
             dim3 g((unsigned)binfo[bidx].count, 2);
