@@ -707,27 +707,6 @@ __global__ void build_near_kernel(BoxDev* __restrict__ boxes, const BoxDev* __re
 // Level-to-level merge: gather the skeleton rows of every
 // box into the next level's store, parent-major (children in Morton order).
 // ---------------------------------------------------------------------------
-// Host-resident inputs (rsrs_factor with pinned host Y, Z): copy the rows of one colour
-// batch's boxes from the host arrays (zero-copy reads over the host link, 16-byte chunks)
-// into the device store just before the batch runs, on a copy stream one batch ahead of
-// the sweep.  Grid (boxes of the batch, 2 arrays: Y, Z).  w = scalars per row in doubles.
-__global__ void __launch_bounds__(256) host_rows_kernel(const BoxDev* __restrict__ boxes,
-                                                        const double* __restrict__ hY, const double* __restrict__ hZ,
-                                                        i64 ldh, double* __restrict__ dY, double* __restrict__ dZ,
-                                                        i64 ldd, int w) {
-  const BoxDev& b = boxes[blockIdx.x];
-  const double* src = blockIdx.y ? hZ : hY;
-  double* dst = blockIdx.y ? dZ : dY;
-  if (!src) return;
-  const int w2 = w >> 1;          // w even (ld even, complex = 2 doubles)
-  const int n = b.nb * w2;
-  for (int t = threadIdx.x; t < n; t += blockDim.x) {
-    const int i = t / w2, c = t - i * w2;
-    const i64 row = b.row0 + i;
-    reinterpret_cast<double2*>(dst + row * ldd)[c] = __ldcs(reinterpret_cast<const double2*>(src + row * ldh) + c);
-  }
-}
-
 __global__ void compact_kernel(const BoxDev* __restrict__ boxes, const int* __restrict__ iws,
                                const int* __restrict__ dst_row0, const double* __restrict__ Y,
                                const double* __restrict__ Z, const double* __restrict__ Om,

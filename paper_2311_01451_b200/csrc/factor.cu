@@ -75,7 +75,7 @@ int g_optin = 0;
 bool g_debug = false;  // RSRS_DEBUG_SYNC=1: synchronize and check after every launch
 bool g_trace = false;  // RSRS_TRACE=1: host-side time split of rsrs_factor on stderr
 int g_skinny_cols = rsrs::SK_COLS;   // RSRS_SKINNY_COLS: columns per CTA of the skinny E/F kernel
-bool g_host_copy_kernel = false;     // RSRS_HOST_COPY=kernel: host-input rows by the zero-copy gather kernel
+bool g_assemble_box = false;         // RSRS_ASSEMBLE=box: one-CTA-per-box Gram assembly (A/B against per slot)
 
 // host-side time split of one rsrs_factor (RSRS_TRACE)
 struct HostTrace {
@@ -124,6 +124,7 @@ void set_smem_both() {
   set_smem(rsrs::top_solve_kernel<C>, -1);
   set_smem(rsrs::top_apply_kernel<C>, -1);
   set_smem(rsrs::gblk_update_kernel<C>, rsrs::gblk_smem<C>());
+  set_smem(rsrs::gram_assemble_box_kernel<C>, -1);
   set_smem(rsrs::skinny_nn_kernel<C>, rsrs::skinny_smem<C>());
 }
 
@@ -135,7 +136,7 @@ void init_kernels() {
   const char* tr = getenv("RSRS_TRACE");
   g_trace = tr && tr[0] == '1';
   if (const char* sc = getenv("RSRS_SKINNY_COLS")) g_skinny_cols = std::max(128, (atoi(sc) / 128) * 128);
-  if (const char* hc = getenv("RSRS_HOST_COPY")) g_host_copy_kernel = std::string(hc) == "kernel";
+  if (const char* ga = getenv("RSRS_ASSEMBLE")) g_assemble_box = std::string(ga) == "box";
   int dev = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&g_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
@@ -414,8 +415,8 @@ struct Planner {
   bool cplx = false;
   bool sym = false;    // symmetric shortcut: Psi = Omega, Z = Y, only the Y / Omega side runs
   int symmode = 0;     // 1: A = A^* (Z = Y); 2: complex symmetric A = A^T (Psi = conj Omega, Z = conj Y)
-  bool host_in = false;  // Y, Z, Omega, Psi are pinned HOST arrays: the library owns the device store, copies
-                         // Omega / Psi up front and the Y / Z rows of each leaf colour batch one batch ahead
+  bool host_in = false;  // Y, Z, Omega, Psi are pinned HOST arrays: the library owns the device store and
+                         // copies Omega / Psi, then Y / Z (overlapping the leaf Gram precompute)
   bool tri = false;    // triangular form (Remark PAPER.md:577-611): Cholesky X_rr = C C^T
   bool gram_blocks = true;   // level-wide near-field Gram blocks (gram.cuh; single rank)
   bool level_blocks = false; // the current level uses them (account_box counts the cross products only)
@@ -631,12 +632,8 @@ struct Planner {
         ld = nld;
       }
     }
-    // host-resident inputs: device store owned by the factorization, Omega / Psi copied now,
-    // Y / Z rows streamed per leaf colour batch (copy stream `cs`, one batch ahead)
+    // host-resident inputs: device store owned by the factorization (copy stream `cs`)
     DBuf hstore;
-    const double* hY = nullptr;
-    const double* hZ = nullptr;
-    i64 hld = 0;
     cudaStream_t cs = nullptr;
     std::vector<cudaEvent_t> hev;
     struct StreamGuard {
@@ -651,18 +648,37 @@ struct Planner {
       }
     } guard{cs, hev};
     if (host_in) {
-      hY = Yu;
-      hZ = sym ? nullptr : Zu;
-      hld = SC * ldu;
+      // bulk DMA copies on a copy stream, in the order they are needed: Omega / Psi (the level's
+      // Gram blocks need every row), then Y / Z, which overlap the leaf-level Gram precompute;
+      // the first colour batch waits for Y / Z.  (Per-box copies of each colour batch, a finer
+      // overlap, measured slower: thousands of ~150 KB DMA copies per batch.)
       hstore.alloc((size_t)sS * std::max<i64>(2, 4 * (i64)T.N * nld), s);
       double* base = hstore.as<double>();
       double* dst[4] = {base, base + SC * T.N * nld, base + 2 * SC * T.N * nld, base + 3 * SC * T.N * nld};
-      const double* hsrc[2] = {Omu, Psu};
-      for (int a = 0; a < (sym ? 1 : 2); ++a)
-        CK(cudaMemcpy2DAsync(dst[2 + a], sS * nld, hsrc[a], sS * ldu, sS * p, T.N, cudaMemcpyHostToDevice, s));
+      const double* hsrc[4] = {Yu, Zu, Omu, Psu};
+      CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+      cudaEvent_t e0;
+      CK(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
+      hev.push_back(e0);
+      CK(cudaEventRecord(e0, s));                 // the store was allocated on s
+      CK(cudaStreamWaitEvent(cs, e0, 0));
+      for (int a : {2, 3, 0, 1}) {
+        if (sym && (a == 1 || a == 3)) continue;
+        CK(cudaMemcpy2DAsync(dst[a], sS * nld, hsrc[a], sS * ldu, sS * p, T.N, cudaMemcpyHostToDevice, cs));
+        if (a == 3 || (sym && a == 2)) {        // Omega / Psi arrived
+          cudaEvent_t e;
+          CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+          hev.push_back(e);
+          CK(cudaEventRecord(e, cs));
+          CK(cudaStreamWaitEvent(s, e, 0));
+        }
+      }
+      cudaEvent_t eyz;
+      CK(cudaEventCreateWithFlags(&eyz, cudaEventDisableTiming));
+      hev.push_back(eyz);
+      CK(cudaEventRecord(eyz, cs));               // Y / Z arrived: waited on by the first leaf batch
       Y = dst[0]; Z = sym ? dst[0] : dst[1]; Om = dst[2]; Ps = sym ? dst[2] : dst[3];
       ld = nld;
-      CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     }
     DBuf leaf_gidx;
     {
@@ -1057,46 +1073,10 @@ struct Planner {
 
       phase(2);
       // ---- colour batches --------------------------------------------------
-      const bool stream_rows = host_in && lev == L;
-      auto issue_rows = [&](size_t bidx) {      // Y / Z rows of batch bidx: host -> device on cs
-        if (bidx >= binfo.size()) return;
-        cudaEvent_t e;
-        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        hev.push_back(e);
-        if (bidx == 0) {       // the box records are uploaded on s
-          CK(cudaEventRecord(e, s));
-          CK(cudaStreamWaitEvent(cs, e, 0));
-        }
-        if (binfo[bidx].count > 0) {
-          if (hld == SC * ld && !g_host_copy_kernel) {
-            // same row pitch on host and device: every box is one contiguous block per array,
-            // copied by the DMA engines (one cudaMemcpyAsync per box and array, no SMs taken)
-            const size_t W8 = sizeof(double) * SC * (size_t)ld;
-            for (int q = binfo[bidx].first; q < binfo[bidx].first + binfo[bidx].count; ++q) {
-              const i64 off = SC * (i64)hb[q].row0 * ld;
-              const size_t bytes = W8 * (size_t)hb[q].nb;
-              if (!bytes) continue;
-              CK(cudaMemcpyAsync(Y + off, hY + off, bytes, cudaMemcpyHostToDevice, cs));
-              if (!sym) CK(cudaMemcpyAsync(Z + off, hZ + off, bytes, cudaMemcpyHostToDevice, cs));
-            }
-          } else {
-            dim3 g((unsigned)binfo[bidx].count, 2);
-            rsrs::host_rows_kernel<<<g, 256, 0, cs>>>(dboxes + binfo[bidx].first, hY, hZ, hld, Y, sym ? nullptr : Z,
-                                                      SC * ld, (int)(SC * nld));
-            post("host_rows_kernel", cs, launches);
-          }
-        }
-        CK(cudaEventRecord(e, cs));
-      };
-      if (stream_rows) issue_rows(0);
+      if (host_in && lev == L) CK(cudaStreamWaitEvent(s, hev.back(), 0));   // Y / Z rows on the device
       for (const BInfo& bi : binfo) {
         const int n = bi.count, q0 = bi.first;
         BoxDev* dbx = dboxes + q0;
-        if (stream_rows) {
-          const size_t bidx = &bi - &binfo[0];
-          CK(cudaStreamWaitEvent(s, hev.back(), 0));   // this batch's rows have arrived
-          issue_rows(bidx + 1);                        // the next batch's rows overlap this batch
-        }
         rsrs::HaloPlan H;
         std::vector<int4> srecs;
         int64_t nsend = 0;
@@ -1185,7 +1165,16 @@ struct Planner {
             launch_nt(cplx, Dgram + gpb * q0, gpb * n, bi.max_nb, bi.max_r, s, launches);
             double* pO = gpool->as<double>();
             double* pP = pO + SC * gpool_side;
-            {
+            if (g_assemble_box) {
+              const size_t sm = rsrs::gram_assemble_box_smem(bi.max_r, max_nnbr);
+              if (cplx)
+                rsrs::gram_assemble_box_kernel<true><<<n, 256, sm, s>>>(dbx, dboxes, diws, dnbr, gtab_b.as<rsrs::GBlk>(),
+                                                                        gps_b_ptr, pO, pP, dws, sides);
+              else
+                rsrs::gram_assemble_box_kernel<false><<<n, 256, sm, s>>>(dbx, dboxes, diws, dnbr, gtab_b.as<rsrs::GBlk>(),
+                                                                         gps_b_ptr, pO, pP, dws, sides);
+              post("gram_assemble_box_kernel", s, launches);
+            } else {
               dim3 ga(n, max_nnbr);
               if (cplx)
                 rsrs::gram_assemble_kernel<true><<<ga, 256, rsrs::gram_assemble_smem(bi.max_r), s>>>(dbx, dboxes, diws, dnbr, gtab_b.as<rsrs::GBlk>(),

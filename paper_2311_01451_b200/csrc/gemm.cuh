@@ -100,8 +100,6 @@ RSRS_DI void nt_tile(const NTDesc& d, int m, int n, int K, int i0, int j0, doubl
     __syncthreads();
     const double* as = As + ((kt & 1) * TM + wr * (TM / 2)) * GPA;
     const double* bs = Bs + ((kt & 1) * GT + cofs) * GPA;
-    // warp-uniform 8-row / 8-column predication: m8n8 tiles wholly beyond m or n are not issued
-    const int rlim = m - (i0 + wr * (TM / 2)), clim = n - (j0 + cofs);
     if (wact) {
 #pragma unroll
       for (int kk = 0; kk < GBK / 4; ++kk) {
@@ -114,7 +112,7 @@ RSRS_DI void nt_tile(const NTDesc& d, int m, int n, int K, int i0, int j0, doubl
         for (int t = 0; t < MT; ++t)
 #pragma unroll
           for (int u = 0; u < 4; ++u)
-            if (u * 8 < cw && rlim > t * 8 && clim > u * 8) dmma884(acc[t][u][0], acc[t][u][1], a[t], b[u]);
+            if (u * 8 < cw) dmma884(acc[t][u][0], acc[t][u][1], a[t], b[u]);
       }
     }
     __syncthreads();
@@ -258,7 +256,6 @@ RSRS_DI void nn_tile(const NNDesc& d, int m, int n, int K, int i0, int j0, doubl
     __syncthreads();
     const double* as = As + ((kt & 1) * TM + wr * (TM / 2)) * GPA;
     const double* bs = Bs + (kt & 1) * GBK * GPB + cofs;
-    const int rlim = m - (i0 + wr * (TM / 2)), clim = n - (j0 + cofs);   // see nt_tile
     if (wact)
 #pragma unroll
       for (int kk = 0; kk < GBK / 4; ++kk) {
@@ -271,7 +268,7 @@ RSRS_DI void nn_tile(const NNDesc& d, int m, int n, int K, int i0, int j0, doubl
         for (int t = 0; t < MT; ++t)
 #pragma unroll
           for (int u = 0; u < 4; ++u)
-            if (u * 8 < cw && rlim > t * 8 && clim > u * 8) dmma884(acc[t][u][0], acc[t][u][1], a[t], b[u]);
+            if (u * 8 < cw) dmma884(acc[t][u][0], acc[t][u][1], a[t], b[u]);
       }
     __syncthreads();
   }
@@ -392,7 +389,6 @@ RSRS_DI void nt_tile_c(const NTDesc& d, int m, int n, int K, int i0, int j0, dou
     __syncthreads();
     const double* as = As + ((kt & 1) * TM + wr * (TM / 2)) * GPA;
     const double* bs = Bs + ((kt & 1) * GTC + wc * 16) * GPA;
-    const int rlim = m - (i0 + wr * (TM / 2)), clim = n - (j0 + wc * 16);
 #pragma unroll
     for (int kk = 0; kk < GBK / 4; ++kk) {
       double a[MT], b[2], b2[2];
@@ -407,7 +403,6 @@ RSRS_DI void nt_tile_c(const NTDesc& d, int m, int n, int K, int i0, int j0, dou
       for (int t = 0; t < MT; ++t)
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-          if (rlim <= t * 8 || clim <= u * 8) continue;   // m8n8 tiles beyond m / n
           dmma884(ar_[t][u][0], ar_[t][u][1], a[t], b[u]);
           dmma884(ai_[t][u][0], ai_[t][u][1], a[t], b2[u]);
         }
@@ -548,8 +543,6 @@ RSRS_DI void nn_tile_c(const NNDesc& d, int m, int n, int K, int i0, int j0, dou
     __syncthreads();
     const double* as = As + ((kt & 1) * TM + wr * (TM / 2)) * GPA;
     const double* bs = Bs + (kt & 1) * (GBK / 2) * GPB + wc * 32;
-    // 8-row tiles beyond m; 8 real columns = 4 complex columns beyond n (j0: complex tile origin)
-    const int rlim = m - (i0 + wr * (TM / 2)), clim = n - (j0 + wc * 16);
     if (wact)
 #pragma unroll
       for (int kk = 0; kk < GBK / 4; ++kk) {
@@ -565,8 +558,7 @@ RSRS_DI void nn_tile_c(const NNDesc& d, int m, int n, int K, int i0, int j0, dou
 #pragma unroll
         for (int t = 0; t < MT; ++t)
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (rlim > t * 8 && clim > u * 4) dmma884(acc[t][u][0], acc[t][u][1], a[t], b[u]);
+          for (int u = 0; u < 4; ++u) dmma884(acc[t][u][0], acc[t][u][1], a[t], b[u]);
       }
     __syncthreads();
   }

@@ -2,6 +2,10 @@
 # round 2, call 7: full-size oracle parity on c5 (N = 1,048,576: ~45 min of oracle time on the host),
 # then compute-sanitizer racecheck / synccheck of one c1 factorization + solve
 mkdir -p gpurun_out
+# Gram assembly A/B (per slot vs per box) on c3 first
+for a in slot box; do
+  RSRS_ASSEMBLE=$a CFG=c3 RUNS=1216:2 ITERS=2 RSRS_TRACE=1 python tools/quick_c2.py > gpurun_out/r2_c3_assemble_$a.log 2>&1
+done
 python tests/parity_full.py --config c5 --out gpurun_out/r02_parity_c5.json > gpurun_out/r2_parity_c5.log 2>&1
 echo "c5 parity exit $?" > gpurun_out/r2_call7.txt
 cat > /tmp/c1_once.py <<'PY'
