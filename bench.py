@@ -314,7 +314,11 @@ def run_reference(args, rank, world, pg):
     if rank != 0:
         return
     cfg = W.CONFIGS[args.config]
-    rec, times = oracle_baseline(cfg, args.cpu_n, reps=args.steps, warm=args.warmup)
+    # every step is one full oracle factor + solve of a bounded member of the family, sized so the
+    # whole --steps K --warmup W run stays within a few minutes (sphere: N = 4096, ~7 s per run on
+    # 16 cores; 2D grid: 32 x 32); --cpu-n overrides
+    n = args.cpu_n or (4096 if cfg.geometry == "sphere" else 32)
+    rec, times = oracle_baseline(cfg, n, reps=args.steps, warm=args.warmup)
     tot = sum(t[0] for t in times)
     val = rec["value"]
     line = {"metric": METRIC, "value": val, "unit": "DOF/s", "n_gpus": args.gpus, "steps": args.steps,

@@ -121,6 +121,14 @@ void set_smem_both() {
   set_smem(rsrs::solve_bwd_kernel<C, rsrs::sweep_nrb<C>()>, -1);
   set_smem(rsrs::apply_fwd_kernel<C, rsrs::sweep_nrb<C>()>, -1);
   set_smem(rsrs::apply_bwd_kernel<C, rsrs::sweep_nrb<C>()>, -1);
+  set_smem(rsrs::solve_fwd_kernel<C, 4>, -1);
+  set_smem(rsrs::solve_bwd_kernel<C, 4>, -1);
+  set_smem(rsrs::apply_fwd_kernel<C, 4>, -1);
+  set_smem(rsrs::apply_bwd_kernel<C, 4>, -1);
+  set_smem(rsrs::solve_fwd_kernel<C, C ? 4 : 8>, -1);
+  set_smem(rsrs::solve_bwd_kernel<C, C ? 4 : 8>, -1);
+  set_smem(rsrs::apply_fwd_kernel<C, C ? 4 : 8>, -1);
+  set_smem(rsrs::apply_bwd_kernel<C, C ? 4 : 8>, -1);
   set_smem(rsrs::top_solve_kernel<C>, -1);
   set_smem(rsrs::top_apply_kernel<C>, -1);
   set_smem(rsrs::gblk_update_kernel<C>, rsrs::gblk_smem<C>());
@@ -1918,6 +1926,8 @@ static void run_sweep_nrb(rsrs_factorization f, double* x, int64_t nrhs, bool so
 template <bool C>
 static void run_sweep(rsrs_factorization f, double* x, int64_t nrhs, bool solve, cudaStream_t s, rsrs::Comm* comm) {
   if (nrhs == 1) run_sweep_nrb<C, 1>(f, x, nrhs, solve, s, comm);
+  else if (nrhs <= 4) run_sweep_nrb<C, 4>(f, x, nrhs, solve, s, comm);
+  else if (C || nrhs <= 8) run_sweep_nrb<C, C ? 4 : 8>(f, x, nrhs, solve, s, comm);
   else run_sweep_nrb<C, rsrs::sweep_nrb<C>()>(f, x, nrhs, solve, s, comm);
 }
 

@@ -22,7 +22,7 @@ RSRS_DI double2 warp_sum(double2 v) {
 
 // right-hand sides per tile of the multi-RHS sweep (factor bytes are read once per tile)
 template <bool C>
-constexpr int sweep_nrb() { return C ? 4 : 8; }
+constexpr int sweep_nrb() { return C ? 4 : 16; }
 
 // Matrix-times-tile from shared memory, the core of every sweep kernel:
 //   acc(i, c) = sum_j M[i, j] X[j, c],  rows i in [0, m), X = xsm[j * NRB + c] (n x NRB)
@@ -47,8 +47,19 @@ RSRS_DI void gemv_rows(const double* __restrict__ M, i64 ld, int m, int n, const
 #pragma unroll 4
       for (int j2 = gl; j2 < n2; j2 += 8) {
         const double2 a = __ldg(row2 + j2);
+        if constexpr (NRB == 1) {
+          acc[0] = fma(a.x, xsm[2 * j2], fma(a.y, xsm[2 * j2 + 1], acc[0]));
+        } else {
+          // right-hand-side pairs as 16-byte shared loads (the x tile is the shared-memory traffic)
+          const double2* x0 = reinterpret_cast<const double2*>(xsm + (2 * j2) * NRB);
+          const double2* x1 = reinterpret_cast<const double2*>(xsm + (2 * j2 + 1) * NRB);
 #pragma unroll
-        for (int c = 0; c < NRB; ++c) acc[c] = fma(a.x, xsm[(2 * j2) * NRB + c], fma(a.y, xsm[(2 * j2 + 1) * NRB + c], acc[c]));
+          for (int c = 0; c < NRB / 2; ++c) {
+            const double2 u = x0[c], v = x1[c];
+            acc[2 * c] = fma(a.x, u.x, fma(a.y, v.x, acc[2 * c]));
+            acc[2 * c + 1] = fma(a.x, u.y, fma(a.y, v.y, acc[2 * c + 1]));
+          }
+        }
       }
       if ((n & 1) && gl == 0) {
         const double a = __ldg(row + n - 1);

@@ -1,0 +1,11 @@
+#!/bin/bash
+# round 2, call 10: multi-RHS sweep (16-wide tiles, paired shared loads) correctness + c2 solve timings;
+# c5 launch list (per-kernel time split of one factorization)
+mkdir -p gpurun_out
+python -m pytest tests/test_gpu_parity.py -x -q -k "multiple_rhs or c1_parity or pinned" > gpurun_out/r2_pytest_call10.log 2>&1
+echo "pytest exit $?" > gpurun_out/r2_call10.txt
+CFG=c2 python tools/solve_bench.py > gpurun_out/r2_solve_c2_v2.json 2> gpurun_out/r2_solve_c2_v2.err
+echo "solve exit $?" >> gpurun_out/r2_call10.txt
+timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2_launches_c5.csv \
+   env CFG=c5 RUNS=1216:2 ITERS=1 PROF=none python tools/quick_c2.py > gpurun_out/r2_launches_c5.log 2>&1
+echo "launches exit $?" >> gpurun_out/r2_call10.txt
