@@ -9,3 +9,11 @@ echo "solve exit $?" >> gpurun_out/r2_call10.txt
 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2_launches_c5.csv \
    env CFG=c5 RUNS=1216:2 ITERS=1 PROF=none python tools/quick_c2.py > gpurun_out/r2_launches_c5.log 2>&1
 echo "launches exit $?" >> gpurun_out/r2_call10.txt
+timeout 900 ncu --set full --import-source on --clock-control none --nvtx --nvtx-include "gemm_nn_lu_update/" \
+    --kernel-name regex:gemm_nn --launch-skip 2 --launch-count 2 -o gpurun_out/r2_c3_luupd -f \
+    env CFG=c3 RUNS=1216:2 ITERS=1 PROF=none python tools/quick_c2.py > gpurun_out/r2_ncu_luupd.log 2>&1
+echo "ncu luupd exit $?" >> gpurun_out/r2_call10.txt
+timeout 900 ncu --set full --import-source on --clock-control none --nvtx --nvtx-include "cholesky/" \
+    --kernel-name regex:chol_diag --launch-skip 4 --launch-count 1 -o gpurun_out/r2_c3_choldiag -f \
+    env CFG=c3 RUNS=1216:2 ITERS=1 PROF=none python tools/quick_c2.py > gpurun_out/r2_ncu_choldiag.log 2>&1
+echo "ncu choldiag exit $?" >> gpurun_out/r2_call10.txt
