@@ -495,10 +495,49 @@ def _sampler_lib():
     return _sampler
 
 
-def sample_matvec(kind: str, pts3, weight: float, X, Y, adjoint: bool = False, stream=None, kappa: float = 25.0):
+_T11_CACHE = {}
+
+
+def _t11_apply(pts3, X, Y, slab_b: int = 10):
+    """Y = T11 X for the SURVEY 8(f) f3 workload: the sparse Schur complement
+    T11 = A11 - A12 A22^-1 A21 of a 3D Poisson slab decomposition, applied exactly in its
+    eigenbasis, T11 = S2 diag(mu) S2 with S2 = S (x) S the orthonormal DST-I of the n x n
+    interface plane (mu: workloads.t11_symbol, a closed form of the slab's tridiagonal solves).
+    Harness operator (the black box RSRS samples), on cuBLAS matmuls through torch -- not the
+    factorization path.  Rows of X / Y follow pts3 (any order: a point's plane index is recovered
+    from its cell-centre coordinates)."""
+    import torch
+
+    import workloads as W
+    N = pts3.shape[0]
+    n = int(round(N ** 0.5))
+    key = (n, slab_b, str(X.device))
+    if key not in _T11_CACHE:
+        S = torch.from_numpy(W.dst_matrix(n)).to(X.device)
+        mu = torch.from_numpy(W.t11_symbol(n, slab_b)).to(X.device)
+        _T11_CACHE[key] = (S, mu)
+    S, mu = _T11_CACHE[key]
+    orig = (torch.floor(pts3[:, 1] * n).long() * n + torch.floor(pts3[:, 0] * n).long()).clamp_(0, N - 1)
+    k = 1 if X.dim() == 1 else X.shape[1]
+    Xo = torch.empty((N, k), dtype=X.dtype, device=X.device)
+    Xo[orig] = X.reshape(N, k)
+    V = Xo.view(n, n, k)
+    V = torch.einsum("ik,klc->ilc", S, V)
+    V = torch.einsum("jl,ilc->ijc", S, V) * mu[:, :, None]
+    V = torch.einsum("ik,klc->ilc", S, V)
+    V = torch.einsum("jl,ilc->ijc", S, V)
+    Y.reshape(N, k).copy_(V.reshape(N, k)[orig])
+    return Y
+
+
+def sample_matvec(kind: str, pts3, weight: float, X, Y, adjoint: bool = False, stream=None, kappa: float = 25.0,
+                  slab_b: int = 10):
     """Y = A X with the on-the-fly kernel operator (device tensors; pts3 N x 3).
 
-    helm2d is complex (X, Y complex128); the others are real (float64)."""
+    helm2d is complex (X, Y complex128); the others are real (float64); t11 is the f3 Schur
+    complement (symmetric, so adjoint is the same operator)."""
+    if kind == "t11":
+        return _t11_apply(pts3, X, Y, slab_b)
     s = _sampler_lib()
     N = pts3.shape[0]
     ncol = 1 if X.dim() == 1 else X.shape[1]
@@ -518,6 +557,12 @@ def sample_matvec(kind: str, pts3, weight: float, X, Y, adjoint: bool = False, s
 def sample_matvec_rows(kind: str, pts3, weight: float, X, Y, row0: int, adjoint: bool = False, stream=None,
                        kappa: float = 25.0):
     """Rows [row0, row0 + Y.shape[0]) of A X (multi-GPU sampling of a rank's own rows)."""
+    if kind == "t11":
+        import torch
+        full = torch.empty((pts3.shape[0],) + tuple(Y.shape[1:]), dtype=Y.dtype, device=Y.device)
+        _t11_apply(pts3, X, full)
+        Y.copy_(full[row0:row0 + Y.shape[0]])
+        return Y
     s = _sampler_lib()
     N = pts3.shape[0]
     nrows = Y.shape[0]

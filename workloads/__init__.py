@@ -88,6 +88,12 @@ CONFIGS = {
     # c_id = 0.5 for c5: with c_id = 1 the full-size residual is 9.4e-6, too close to the 10 eps bar
     # (R7 / section 4; profiles/r01_c5_dev_run.txt)
     "c5": Config("c5", "sphere", 1048576, "lap3d", "f64", p=1216, seed=5, g=2.0, c_id=0.5),
+    # the paper's only experiment (section 6.1), the sparse Schur
+    # complement T11 = A11 - A12 A22^-1 A21 of a 3D Poisson slab decomposition (slab width b = 10),
+    # N = n^2 interface points, atol = 5e-6 (the paper's tightest; its leaf m = 350 is capped here at
+    # 100-point leaves by the per-box kernels' shared memory, reading R20)
+    "t11": Config("t11", "grid2d", 320, "t11", "f64", leaf=100, p=1024, eps=5e-6, seed=6, g=2.0,
+                  extra={"slab_b": 10}),
 }
 
 
@@ -127,10 +133,54 @@ def kernel_weight(cfg: Config) -> float:
     return 1.0 / cfg.N        # w/(4 pi) with w = 4 pi / N
 
 
+# ----------------------------------------------------------------------------
+# T11: sparse Schur complement of a 3D Poisson slab decomposition
+# ----------------------------------------------------------------------------
+def dst_matrix(n: int) -> np.ndarray:
+    """Orthonormal DST-I matrix S (symmetric, S S = I): the eigenvectors of the 1D Dirichlet
+    second difference tridiag(-1, 2, -1) on n points."""
+    k = np.arange(1, n + 1)
+    return math.sqrt(2.0 / (n + 1)) * np.sin(np.pi * np.outer(k, k) / (n + 1))
+
+
+def t11_symbol(n: int, b: int) -> np.ndarray:
+    """Eigenvalues mu[i, j] of T11 = A11 - A12 A22^-1 A21 in the DST basis of the n x n interface plane.
+
+    A = 7-point stencil (diagonal 6, neighbours -1; the finite-difference Poisson operator times
+    h^2) on planes z = 0 (the interface, block 1) .. b (the slab interior, block 2), Dirichlet
+    beyond.  Per in-plane mode (i, j) with a = 6 - 2 cos t_i - 2 cos t_j, t_k = pi k / (n + 1),
+    the slab is tridiag(-1, a, -1) of size b, so mu = a - [T_b(a)^-1]_00 = a - sinh(b phi) /
+    sinh((b + 1) phi) with a = 2 cosh(phi).  (Checked against the explicit sparse Schur
+    complement in tests/test_workloads_t11.py.)"""
+    th = np.pi * np.arange(1, n + 1) / (n + 1)
+    a = 6.0 - 2.0 * np.cos(th)[:, None] - 2.0 * np.cos(th)[None, :]
+    phi = np.arccosh(a / 2.0)
+    return a - np.sinh(b * phi) / np.sinh((b + 1) * phi)
+
+
+def t11_apply(cfg: Config, V: np.ndarray) -> np.ndarray:
+    """T11 V for V in ORIGINAL point order (interface plane row-major, N x k): S2 diag(mu) S2 V with
+    S2 = S (x) S applied as two n x n transforms (T11 is symmetric: T11^* = T11)."""
+    n, b = cfg.n, cfg.extra.get("slab_b", 10)
+    S = dst_matrix(n)
+    mu = t11_symbol(n, b)
+    V3 = V.reshape(n, n, -1)
+    W3 = np.einsum("ik,jl,klc->ijc", S, S, V3, optimize=True)
+    W3 *= mu[:, :, None]
+    return np.einsum("ik,jl,klc->ijc", S, S, W3, optimize=True).reshape(V.shape)
+
+
 def kernel_block(cfg: Config, X: np.ndarray, rows: np.ndarray, cols: np.ndarray) -> np.ndarray:
     """Dense block A[rows, cols] (original point indices) of the config's operator."""
     rows = np.asarray(rows)
     cols = np.asarray(cols)
+    if cfg.kernel == "t11":
+        n, b = cfg.n, cfg.extra.get("slab_b", 10)
+        S = dst_matrix(n)
+        mu = t11_symbol(n, b).ravel()
+        R = np.einsum("ri,rj->rij", S[rows // n], S[rows % n]).reshape(len(rows), n * n)   # rows of S (x) S
+        C = np.einsum("ci,cj->cij", S[cols // n], S[cols % n]).reshape(len(cols), n * n)
+        return (R * mu) @ C.T
     xi = X[rows][:, None, :]
     xj = X[cols][None, :, :]
     r = np.sqrt(((xi - xj) ** 2).sum(-1))
