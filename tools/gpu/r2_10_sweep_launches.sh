@@ -2,7 +2,7 @@
 # round 2, call 10: multi-RHS sweep (16-wide tiles, paired shared loads) correctness + c2 solve timings;
 # c5 launch list (per-kernel time split of one factorization)
 mkdir -p gpurun_out
-python -m pytest tests/test_gpu_parity.py tests/test_gpu_t11.py -x -q -k "multiple_rhs or c1_parity or pinned or t11" > gpurun_out/r2_pytest_call10.log 2>&1
+python -m pytest tests/test_gpu_parity.py tests/test_gpu_t11.py -x -q -k "multiple_rhs or c1_parity or pinned or t11_dense" > gpurun_out/r2_pytest_call10.log 2>&1
 python tests/parity_full.py --config t11 --out gpurun_out/r02_parity_t11.json > gpurun_out/r2_parity_t11.log 2>&1
 echo "pytest exit $?" > gpurun_out/r2_call10.txt
 CFG=c2 python tools/solve_bench.py > gpurun_out/r2_solve_c2_v2.json 2> gpurun_out/r2_solve_c2_v2.err
