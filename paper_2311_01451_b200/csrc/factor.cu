@@ -76,6 +76,7 @@ bool g_debug = false;  // RSRS_DEBUG_SYNC=1: synchronize and check after every l
 bool g_trace = false;  // RSRS_TRACE=1: host-side time split of rsrs_factor on stderr
 int g_skinny_cols = rsrs::SK_COLS;   // RSRS_SKINNY_COLS: columns per CTA of the skinny E/F kernel
 bool g_assemble_box = false;         // RSRS_ASSEMBLE=box: one-CTA-per-box Gram assembly (A/B against per slot)
+bool g_nt3 = false;                  // RSRS_NT3=1: three-stage, one-barrier NT tiles (A/B)
 
 // host-side time split of one rsrs_factor (RSRS_TRACE)
 struct HostTrace {
@@ -145,10 +146,13 @@ void init_kernels() {
   g_trace = tr && tr[0] == '1';
   if (const char* sc = getenv("RSRS_SKINNY_COLS")) g_skinny_cols = std::max(128, (atoi(sc) / 128) * 128);
   if (const char* ga = getenv("RSRS_ASSEMBLE")) g_assemble_box = std::string(ga) == "box";
+  if (const char* n3 = getenv("RSRS_NT3")) g_nt3 = n3[0] == '1';
   int dev = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&g_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   set_smem(rsrs::gemm_nt_kernel<64>, rsrs::NT_SMEM);
+  set_smem(rsrs::gemm_nt_kernel<32, 3>, 3 * (32 + rsrs::GT) * rsrs::GPA * 8);
+  set_smem(rsrs::gemm_nt_kernel<64, 3>, 3 * (64 + rsrs::GT) * rsrs::GPA * 8);
   set_smem(rsrs::gemm_nn_kernel<64>, rsrs::NN_SMEM);
   set_smem(rsrs::gemm_nt_kernel_c<64>, rsrs::NT_SMEM);
   set_smem(rsrs::gemm_nn_kernel_c<64>, rsrs::NN_SMEM);
@@ -285,7 +289,9 @@ void launch_nt(bool cplx, const NTDesc* d, int n, int mmax, int nmax, cudaStream
     if (TM == 32) rsrs::gemm_nt_kernel_c<32><<<grid, 128, rsrs::nt_smem(32, true), s>>>(d);
     else rsrs::gemm_nt_kernel_c<64><<<grid, 128, rsrs::nt_smem(64, true), s>>>(d);
   } else {
-    if (TM == 32) rsrs::gemm_nt_kernel<32><<<grid, 128, rsrs::nt_smem(32, false), s>>>(d);
+    if (TM == 32 && g_nt3) rsrs::gemm_nt_kernel<32, 3><<<grid, 128, 3 * (32 + rsrs::GT) * rsrs::GPA * 8, s>>>(d);
+    else if (TM == 32) rsrs::gemm_nt_kernel<32><<<grid, 128, rsrs::nt_smem(32, false), s>>>(d);
+    else if (g_nt3) rsrs::gemm_nt_kernel<64, 3><<<grid, 128, 3 * (64 + rsrs::GT) * rsrs::GPA * 8, s>>>(d);
     else rsrs::gemm_nt_kernel<64><<<grid, 128, rsrs::NT_SMEM, s>>>(d);
   }
   post("gemm_nt", s, launches);

@@ -29,11 +29,12 @@ constexpr int nn_smem(int TM, bool C) { return 2 * (TM * GPA + (C ? GBK / 2 : GB
 RSRS_DI int dyn(const int* p, int off, int cap) { return p ? min(cap, *p - off) : cap; }
 
 // One TM x 64 output tile (TM = 64 or 32 rows) of C = alpha A_rows B_rows^T + beta C (K columns).
-template <int TM = GT>
+// STAGES = 2: two cp.async stages, two barriers per k chunk; STAGES = 3: one barrier per chunk
+template <int TM = GT, int STAGES = 2>
 RSRS_DI void nt_tile(const NTDesc& d, int m, int n, int K, int i0, int j0, double* smem) {
   constexpr int MT = TM / 16, QA = TM / 8;
   double* As = smem;
-  double* Bs = smem + 2 * TM * GPA;
+  double* Bs = smem + STAGES * TM * GPA;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const int wr = warp >> 1, wc = warp & 1;
@@ -85,21 +86,40 @@ RSRS_DI void nt_tile(const NTDesc& d, int m, int n, int K, int i0, int j0, doubl
   }
 
   const int nk = (K + GBK - 1) / GBK;
-  if (nk > 0) {
-    load_stage(0, 0);
+  if constexpr (STAGES == 2) {
+    if (nk > 0) {
+      load_stage(0, 0);
+      cp_async_commit();
+    }
+  } else {
+    if (nk > 0) load_stage(0, 0);
+    cp_async_commit();
+    if (nk > 1) load_stage(1, 1);
     cp_async_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
-    if (kt + 1 < nk) {
-      load_stage((kt + 1) & 1, kt + 1);
-      cp_async_commit();
-      cp_async_wait<1>();
+    int sb;
+    if constexpr (STAGES == 2) {
+      if (kt + 1 < nk) {
+        load_stage((kt + 1) & 1, kt + 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      sb = kt & 1;
     } else {
-      cp_async_wait<0>();
+      // chunk kt landed (one newer group may be pending); after the barrier every warp is done
+      // with chunk kt - 1, so its buffer takes chunk kt + 2
+      cp_async_wait<1>();
+      __syncthreads();
+      if (kt + 2 < nk) load_stage((kt + 2) % 3, kt + 2);
+      cp_async_commit();
+      sb = kt % 3;
     }
-    __syncthreads();
-    const double* as = As + ((kt & 1) * TM + wr * (TM / 2)) * GPA;
-    const double* bs = Bs + ((kt & 1) * GT + cofs) * GPA;
+    const double* as = As + (sb * TM + wr * (TM / 2)) * GPA;
+    const double* bs = Bs + (sb * GT + cofs) * GPA;
     if (wact) {
 #pragma unroll
       for (int kk = 0; kk < GBK / 4; ++kk) {
@@ -115,7 +135,7 @@ RSRS_DI void nt_tile(const NTDesc& d, int m, int n, int K, int i0, int j0, doubl
             if (u * 8 < cw) dmma884(acc[t][u][0], acc[t][u][1], a[t], b[u]);
       }
     }
-    __syncthreads();
+    if constexpr (STAGES == 2) __syncthreads();
   }
 #pragma unroll
   for (int t = 0; t < MT; ++t) {
@@ -139,7 +159,7 @@ RSRS_DI void nt_tile(const NTDesc& d, int m, int n, int K, int i0, int j0, doubl
   }
 }
 
-template <int TM>
+template <int TM, int STAGES = 2>
 __global__ void __launch_bounds__(128) gemm_nt_kernel(const NTDesc* __restrict__ descs) {
   extern __shared__ __align__(16) double smem[];
   const NTDesc& d = descs[blockIdx.z];
@@ -150,7 +170,7 @@ __global__ void __launch_bounds__(128) gemm_nt_kernel(const NTDesc* __restrict__
   const int sym = d.psym ? *d.psym : d.sym_rows;
   if (i0 + TM <= sym && j0 >= i0 + TM) return;  // strictly upper tile of the Gram
   const NTDesc dl = d;
-  nt_tile<TM>(dl, m, n, d.K, i0, j0, smem);
+  nt_tile<TM, STAGES>(dl, m, n, d.K, i0, j0, smem);
 }
 
 // One TM x 64 output tile (TM = 64 or 32 rows) of D_rows = beta C_rows + alpha opA B_rows.

@@ -18,3 +18,7 @@ timeout 900 ncu --set full --import-source on --clock-control none --nvtx --nvtx
     --kernel-name regex:chol_diag --launch-skip 4 --launch-count 1 -o gpurun_out/r2_c3_choldiag -f \
     env CFG=c3 RUNS=1216:2 ITERS=1 PROF=none python tools/quick_c2.py > gpurun_out/r2_ncu_choldiag.log 2>&1
 echo "ncu choldiag exit $?" >> gpurun_out/r2_call10.txt
+for v in 0 1; do
+  RSRS_NT3=$v CFG=c3 RUNS=1216:2 ITERS=2 RSRS_TRACE=1 python tools/quick_c2.py > gpurun_out/r2_c3_nt3_$v.log 2>&1
+done
+echo "nt3 ab exit $?" >> gpurun_out/r2_call10.txt
