@@ -977,30 +977,23 @@ struct Planner {
           post("gblk_work", s, launches);
         }
         gps_b_ptr = d_gps;
-        std::vector<NTDesc> pre;
-        double fl = 0;
+        // the precompute GEMM descriptors (one row block per box and side) are expanded on the
+        // device from the per-box arrays already uploaded (no host loop / 100+ B per box upload)
+        double fl = 0, rows = 0;
         for (int i = 0; i < nbox; ++i) {
           if (nb_all[i] <= 0) continue;
-          const int cols = (int)(rowl_at[i + 1] - rowl_at[i]);
-          for (int side = 0; side < sides; ++side) {
-            const double* M = side ? Ps : Om;
-            NTDesc d{};
-            d.A = M + SC * (i64)row0[i] * ld; d.rowA = nullptr; d.lda = ld;
-            d.B = M; d.rowB = growl_b.as<int>() + rowl_at[i]; d.ldb = ld;
-            d.C = poolO + SC * (side * poff + roff[i]); d.ldc = rld[i];
-            d.m = nb_all[i]; d.n = cols; d.K = p; d.sym_rows = 0; d.alpha = 1.0;
-            pre.push_back(d);
-            fl += 2.0 * nb_all[i] * cols * p;
-          }
+          fl += 2.0 * sides * nb_all[i] * (double)(rowl_at[i + 1] - rowl_at[i]) * p;
+          rows += nb_all[i];
         }
-        pre_b.alloc(sizeof(NTDesc) * std::max<size_t>(pre.size(), 1), s);
-        if (!pre.empty()) {
-          CK(cudaMemcpyAsync(pre_b.p, pre.data(), sizeof(NTDesc) * pre.size(), cudaMemcpyHostToDevice, s));
+        pre_b.alloc(sizeof(NTDesc) * std::max<size_t>((size_t)sides * nbox, 1), s);
+        if (nbox > 0 && fl > 0) {
+          rsrs::pre_desc_kernel<<<(sides * nbox + 255) / 256, 256, 0, s>>>(nbox, sides, d_nb, d_row0, d_roff, d_rld, d_rowlat,
+                                                                           Om, Ps, ld, growl_b.as<int>(), poolO, poff, p, SC,
+                                                                           pre_b.as<NTDesc>());
+          post("pre_desc_kernel", s, launches);
           tic(KC_GRAM);
-          launch_nt(cplx, pre_b.as<NTDesc>(), (int)pre.size(), maxnb, maxcols, s, launches);
+          launch_nt(cplx, pre_b.as<NTDesc>(), sides * nbox, maxnb, maxcols, s, launches);
           toc();
-          double rows = 0;
-          for (int i = 0; i < nbox; ++i) rows += nb_all[i];
           account(KC_GRAM, (cplx ? 4.0 : 1.0) * fl, (double)sS * (sides * rows * p + sides * poff));
         }
       }

@@ -24,6 +24,24 @@ struct GBlk {
   int ld, pad;
 };
 
+// Descriptors of the level's Gram-block precompute: box i, side (Omega / Psi) computes its row
+// block [G(i, j) for partners j >= i] = M_i M_partners^* (one NT GEMM; empty boxes get m = 0).
+__global__ void pre_desc_kernel(int nbox, int sides, const int* __restrict__ nb, const int* __restrict__ row0,
+                                const i64* __restrict__ roff, const int* __restrict__ rld,
+                                const i64* __restrict__ rowl_at, const double* Om, const double* Ps, i64 ld,
+                                const int* rowl, double* pool, i64 poff, int p, int SC, NTDesc* __restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= sides * nbox) return;
+  const int side = t / nbox, i = t - side * nbox;
+  const double* M = side ? Ps : Om;
+  NTDesc d{};
+  d.A = M + SC * (i64)max(row0[i], 0) * ld; d.rowA = nullptr; d.lda = ld;
+  d.B = M; d.rowB = rowl + rowl_at[i]; d.ldb = ld;
+  d.C = pool + SC * (side * poff + roff[i]); d.ldc = rld[i];
+  d.m = nb[i] > 0 ? nb[i] : 0; d.n = (int)(rowl_at[i + 1] - rowl_at[i]); d.K = p; d.sym_rows = 0; d.alpha = 1.0;
+  out[t] = d;
+}
+
 // Partner table and B-row lists of the level (one warp per box i; partner lists sorted).
 // Entry t of box i points at G(i, j) inside i's row block (j >= i: mode 0, or 2 on the
 // diagonal) or at G(j, i) inside j's row block (j < i: mode 1, columns offset by the
