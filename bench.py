@@ -54,6 +54,10 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-n", type=int, default=0,
                     help="oracle sample size N (same config family); 0 = auto (sphere 8192, 2D grid 64x64)")
+    ap.add_argument("--noise-factor", type=float, default=0.0,
+                    help="f1: noise-aware tolerance atol(l-1) = max(atol(l), theta nu(l)) (0: fixed schedule)")
+    ap.add_argument("--triangular", action="store_true",
+                    help="f4: triangular (Cholesky) output form; needs --variant symmetric (spd operators)")
     ap.add_argument("--variant", default="paper", choices=["paper", "symmetric"],
                     help="paper: two independent sketches (PAPER.md:1180-1183, the headline); symmetric: the "
                          "SURVEY 8(f) f2 shortcut Psi = Omega, Z = Y for real symmetric A (c1-c3, c5) / "
@@ -214,7 +218,8 @@ def factor_solve(pb, work, x, stream, profile=False, solve_events=None, estimate
     arrays = (work[0], None, work[1], None) if pb["symmetric"] else tuple(work)
     f = R.factor(pb["tree"], *arrays, p=cfg.p, eps=cfg.eps, level_growth=cfg.g, id_scale=cfg.c_id,
                  oversample=cfg.l, stream=stream, profile=profile, comm=pb["comm"], rank=pb["rank"],
-                 nranks=pb["world"], symmetric=pb["symmetric"], estimate_coupling=estimate)
+                 nranks=pb["world"], symmetric=pb["symmetric"], estimate_coupling=estimate and not pb["triangular"],
+                 noise_factor=pb["noise_factor"], triangular=pb["triangular"])
     if solve_events is not None:
         solve_events[0].record(stream)
     f.solve(x, stream=stream)
@@ -339,7 +344,11 @@ def run_native(args, rank, world, local, pg):
     dev = torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
     cfg = W.CONFIGS[args.config]
+    if args.triangular and args.variant != "symmetric":
+        raise SystemExit("--triangular needs --variant symmetric (the triangular form is for spd operators)")
     pb = setup_problem(cfg, dev, rank, world, pg, symmetric=args.variant == "symmetric")
+    pb["noise_factor"] = args.noise_factor
+    pb["triangular"] = args.triangular
     stream = torch.cuda.Stream(device=dev)
     work = [t.clone() for t in pb["src"]]
     x = pb["b"].clone()
@@ -398,7 +407,8 @@ def run_native(args, rank, world, local, pg):
     resid = float((ax - pb["b"][pb["P"]]).norm() / pb["b"].norm())
     # ---- coupling estimates, one extra factorization outside the timed region
     coupling = None
-    if world == 1:
+    atols = {str(lev): f.atol(lev) for lev in range(st["L"], st["top_level"] - 1, -1)}
+    if world == 1 and not pb["triangular"]:
         with torch.cuda.stream(stream):
             for w_, s_ in zip(work, pb["src"]):
                 w_.copy_(s_)
@@ -412,7 +422,7 @@ def run_native(args, rank, world, local, pg):
             e = e[e[:, 0] >= 0]
             if e.size:
                 coupling[str(lev)] = {"max": float(e.max()), "median": float(np.median(e)),
-                                      "atol": cfg.c_id * cfg.eps * cfg.g ** (st["L"] - lev)}
+                                      "atol": fe.atol(lev)}
         del fe
     # ---- e2e: the same step through the C ABI with PINNED HOST buffers: rsrs_factor reads the host
     # samples (Omega / Psi copied up front, the Y / Z rows of each leaf colour batch streamed one batch
@@ -508,13 +518,14 @@ def run_native(args, rank, world, local, pg):
             "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
             "config": {"workload": cfg.name, "N": N, "p": cfg.p, "eps": cfg.eps, "g": cfg.g, "leaf": cfg.leaf,
                        "kernel": cfg.kernel, "L": st["L"], "l2": f"inputs {sum(t.numel() * t.element_size() for t in pb['src']) / 1e9:.1f} GB > 126 MB L2 (no flush needed)",
-                       "step": "restore samples + rsrs_factor + rsrs_solve(1 rhs)", "variant": args.variant, "parallelism": (f"morton-range x{world}, halo exchange, gather at level {pb['gather_level']}"
+                       "step": "restore samples + rsrs_factor + rsrs_solve(1 rhs)", "variant": args.variant + (f", noise-aware tolerance theta = {args.noise_factor}" if args.noise_factor else "")
+                       + (", triangular form" if args.triangular else ""), "parallelism": (f"morton-range x{world}, halo exchange, gather at level {pb['gather_level']}"
                                        if world > 1 else "single GPU")},
             "factor_ms": st["factor_ms"], "solve_ms": statistics.median(solve_ms), "sample_s": pb["t_sample"], "tree_s": pb["t_tree"],
             "residual": resid, "top_size": st["top_size"], "max_rank": st["max_rank"],
             "memory_scalars": st["memory_scalars"], "sweep": sweep,
             "roofline": roof, "kernels": breakdown, "fp64_peaks": peaks, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": int(launches), "clocks": clk, "coupling_estimate": coupling}
+            "gpu_launches": int(launches), "clocks": clk, "coupling_estimate": coupling, "atol_per_level": atols}
     print(json.dumps(line), flush=True)
 
 
