@@ -75,7 +75,6 @@ int g_optin = 0;
 bool g_debug = false;  // RSRS_DEBUG_SYNC=1: synchronize and check after every launch
 bool g_trace = false;  // RSRS_TRACE=1: host-side time split of rsrs_factor on stderr
 int g_skinny_cols = rsrs::SK_COLS;   // RSRS_SKINNY_COLS: columns per CTA of the skinny E/F kernel
-bool g_assemble_box = false;         // RSRS_ASSEMBLE=box: one-CTA-per-box Gram assembly (A/B against per slot)
 bool g_nt3 = false;                  // RSRS_NT3=1: three-stage, one-barrier NT tiles (A/B)
 
 // host-side time split of one rsrs_factor (RSRS_TRACE)
@@ -133,7 +132,6 @@ void set_smem_both() {
   set_smem(rsrs::top_solve_kernel<C>, -1);
   set_smem(rsrs::top_apply_kernel<C>, -1);
   set_smem(rsrs::gblk_update_kernel<C>, rsrs::gblk_smem<C>());
-  set_smem(rsrs::gram_assemble_box_kernel<C>, -1);
   set_smem(rsrs::skinny_nn_kernel<C>, rsrs::skinny_smem<C>());
 }
 
@@ -145,7 +143,6 @@ void init_kernels() {
   const char* tr = getenv("RSRS_TRACE");
   g_trace = tr && tr[0] == '1';
   if (const char* sc = getenv("RSRS_SKINNY_COLS")) g_skinny_cols = std::max(128, (atoi(sc) / 128) * 128);
-  if (const char* ga = getenv("RSRS_ASSEMBLE")) g_assemble_box = std::string(ga) == "box";
   if (const char* n3 = getenv("RSRS_NT3")) g_nt3 = n3[0] == '1';
   int dev = 0;
   CK(cudaGetDevice(&dev));
@@ -1172,16 +1169,7 @@ struct Planner {
             launch_nt(cplx, Dgram + gpb * q0, gpb * n, bi.max_nb, bi.max_r, s, launches);
             double* pO = gpool->as<double>();
             double* pP = pO + SC * gpool_side;
-            if (g_assemble_box) {
-              const size_t sm = rsrs::gram_assemble_box_smem(bi.max_r, max_nnbr);
-              if (cplx)
-                rsrs::gram_assemble_box_kernel<true><<<n, 256, sm, s>>>(dbx, dboxes, diws, dnbr, gtab_b.as<rsrs::GBlk>(),
-                                                                        gps_b_ptr, pO, pP, dws, sides);
-              else
-                rsrs::gram_assemble_box_kernel<false><<<n, 256, sm, s>>>(dbx, dboxes, diws, dnbr, gtab_b.as<rsrs::GBlk>(),
-                                                                         gps_b_ptr, pO, pP, dws, sides);
-              post("gram_assemble_box_kernel", s, launches);
-            } else {
+            {
               dim3 ga(n, max_nnbr);
               if (cplx)
                 rsrs::gram_assemble_kernel<true><<<ga, 256, rsrs::gram_assemble_smem(bi.max_r), s>>>(dbx, dboxes, diws, dnbr, gtab_b.as<rsrs::GBlk>(),

@@ -165,93 +165,6 @@ __global__ void __launch_bounds__(256) gblk_update_kernel(const BoxDev* __restri
     }
 }
 
-// One CTA per box (grid: boxes of the batch): the same assembly, with the per-box setup done
-// ONCE per box instead of once per (box, slot) CTA: slot sizes / offsets, the active row and
-// the slot of every near row, and the partner entry of every slot pair (a merge join of the
-// sorted partner and neighbour lists), all staged in shared memory.  Then each warp copies
-// whole rows of the lower triangle (lanes over columns; rows contiguous in C_b).
-// Dynamic shared memory: gram_assemble_box_smem(max r, max neighbours).
-inline size_t gram_assemble_box_smem(int rmax, int nnmax) {
-  return sizeof(GBlk) * (size_t)nnmax * nnmax + sizeof(int) * 3 * (size_t)(rmax > 0 ? rmax : 1);
-}
-template <bool C>
-__global__ void __launch_bounds__(256) gram_assemble_box_kernel(const BoxDev* __restrict__ boxes,
-                                                                const BoxDev* __restrict__ level_boxes,
-                                                                const int* __restrict__ iws,
-                                                                const int* __restrict__ nbrrec,
-                                                                const GBlk* __restrict__ tab,
-                                                                const int* __restrict__ pstart,
-                                                                const double* __restrict__ poolO,
-                                                                const double* __restrict__ poolP,
-                                                                double* __restrict__ wsd, int sides) {
-  typedef typename ScalarOf<C>::T S;
-  extern __shared__ __align__(16) double gab[];
-  __shared__ int pos[65], cnt[64], bx[64], idxs[64];
-  const BoxDev& b = boxes[blockIdx.x];
-  if (b.status != ST_OK) return;
-  const int nn = b.nnbr;
-  const int* nd = nbrrec + b.off_nbr;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  GBlk* sE = reinterpret_cast<GBlk*>(gab);                 // [nn][nn] entry of (q1, q2 <= q1)
-  int* act = reinterpret_cast<int*>(sE + nn * nn);          // [r] active local row of near row / column
-  int* colq = act + b.rmax;                                 // [r] slot of near row / column
-  if (tid < nn) {
-    const int idx = nd[4 * tid];
-    cnt[tid] = idx >= 0 ? level_boxes[idx].k : nd[4 * tid + 2];
-    bx[tid] = nd[4 * tid + 3];
-    idxs[tid] = idx;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    int o = 0;
-    for (int q = 0; q < nn; ++q) {
-      pos[q] = o;
-      o += cnt[q];
-    }
-    pos[nn] = o;
-  }
-  if (tid < nn) {                        // merge join: partners of bx[q1] (sorted) x bx[0..q1] (sorted)
-    const int q1 = tid;
-    const int t1 = pstart[bx[q1] + 1];
-    int t = pstart[bx[q1]];
-    for (int q2 = 0; q2 <= q1; ++q2) {
-      if (cnt[q2] == 0) continue;
-      while (t < t1 && tab[t].j < bx[q2]) ++t;
-      if (t < t1) sE[q1 * nn + q2] = tab[t];
-    }
-  }
-  __syncthreads();
-  const int r = pos[nn];
-  for (int col = tid; col < r; col += 256) {
-    int lo = 0, hi = nn - 1;             // last slot with pos <= col
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (pos[mid] <= col) lo = mid;
-      else hi = mid - 1;
-    }
-    const int a = col - pos[lo], idx = idxs[lo];
-    colq[col] = lo;
-    act[col] = idx >= 0 ? iws[level_boxes[idx].off_skelrow + a] - level_boxes[idx].row0 : a;
-  }
-  __syncthreads();
-  const i64 ldr = b.ldr;
-  for (int side = 0; side < sides; ++side) {
-    const S* P = reinterpret_cast<const S*>(side ? poolP : poolO);
-    S* Cb = reinterpret_cast<S*>(wsd) + b.off_aug + (side ? (i64)(b.rmax + b.nb) * ldr : 0);
-    for (int row = warp; row < r; row += 8) {
-      const int q1 = colq[row];
-      const int ar = act[row];
-      const int ncol = pos[q1] + cnt[q1];
-      const GBlk* E = sE + q1 * nn;
-      S* crow = Cb + (i64)row * ldr;
-      for (int col = lane; col < ncol; col += 32) {
-        const GBlk& e = E[colq[col]];
-        crow[col] = e.mode != 1 ? P[e.off + (i64)ar * e.ld + act[col]] : s_conj(P[e.off + (i64)act[col] * e.ld + ar]);
-      }
-    }
-  }
-}
-
 // C_b[pos(q1) + a, pos(q2) + c] = G(n_q1, n_q2)[act_q1[a], act_q2[c]] for slots q2 <= q1
 // of b's neighbour list (the lower block triangle of the near-field Gram).
 // Grid (boxes of the batch, neighbour slots q1).  The slot table, the partner entries
