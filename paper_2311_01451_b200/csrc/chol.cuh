@@ -250,4 +250,212 @@ __global__ void __launch_bounds__(128) chol_back_b_kernel(const CholDesc* __rest
   nn_tile_t<C>(d, m, jb, jb, i0, jt, smem);   // in place: one column tile reads all of K before it writes
 }
 
+// ---------------------------------------------------------------------------
+// Fused per-matrix Cholesky (real): one 128-thread CTA runs the whole blocked
+// left-looking factorization of one near-field Gram (update tiles, diagonal
+// block, TRSM tiles, panel after panel) and, in a second launch, the whole back
+// substitution.  Same arithmetic as the per-panel kernels above (one launch per
+// colour batch instead of ~3 per panel): small near fields (the sphere's leaves,
+// r <= ~256) are latency-bound on the per-panel launch chain, and independent
+// matrices now overlap each other's serial diagonal steps on the SM.
+
+// 64 x 64 diagonal block by in-register elimination on [C_JJ | I], 128 threads:
+// thread (tr, tc) = (tid / 16, tid % 16) owns rows tr + 8 ra (ra < 8) and columns
+// tc + 16 cb (cb < 8; cb >= 4: the I part).  Row c = 8 cb8 + cc is owned by tr = cc
+// in slot ra = cb8; column c by tc = c % 16 in slot cb = cb8 / 2 (both compile time).
+RSRS_DI bool chol_diag_block128(const CholDesc& cd, int j0, int r, double* smem) {
+  constexpr int TR = 8, RA = CB / TR, CA = 2 * CB / 16;
+  // broadcast buffers alias the (idle) GEMM staging memory
+  double (*colbuf)[CB] = reinterpret_cast<double (*)[CB]>(smem);
+  double (*rowbuf)[2 * CB] = reinterpret_cast<double (*)[2 * CB]>(smem + 2 * CB);
+  double* pivs = smem + 6 * CB;
+  int& sbad = *reinterpret_cast<int*>(smem + 7 * CB);
+  const int jb = min(CB, r - j0);
+  const int tid = threadIdx.x;
+  const int tr = tid >> 4, tc = tid & 15;
+  double* A = cd.A + (i64)j0 * cd.lda + j0;
+  double a[RA][CA];
+#pragma unroll
+  for (int ra = 0; ra < RA; ++ra) {
+    const int i = tr + TR * ra;
+#pragma unroll
+    for (int cb = 0; cb < CA; ++cb) {
+      const int j = tc + 16 * cb;
+      double v;
+      if (j < CB) {
+        if (i < jb && j < jb) v = (j <= i) ? A[(i64)i * cd.lda + j] : A[(i64)j * cd.lda + i];
+        else v = (i == j) ? 1.0 : 0.0;
+      } else {
+        v = (j - CB == i) ? 1.0 : 0.0;
+      }
+      a[ra][cb] = v;
+    }
+  }
+  if (tid == 0) sbad = 0;
+  bool bad = false;
+#pragma unroll
+  for (int cb8 = 0; cb8 < CB / TR; ++cb8) {
+    const int cbc = cb8 >> 1;                 // column slot of c
+    for (int cc = 0; cc < TR && !bad; ++cc) {
+      const int c = TR * cb8 + cc;
+      if (c >= jb) break;
+      const int buf = c & 1;
+      const int ctc = (cb8 & 1) * 8 + cc;     // c % 16
+      if (tc == ctc)
+#pragma unroll
+        for (int ra = 0; ra < RA; ++ra) colbuf[buf][tr + TR * ra] = a[ra][cbc];
+      if (tr == cc) {
+        const double pv = a[cb8][cbc];
+        const double rp = 1.0 / __shfl_sync(0xffffu << (threadIdx.x & 16), pv, ctc, 16);
+#pragma unroll
+        for (int cb = 0; cb < CA; ++cb) rowbuf[buf][tc + 16 * cb] = a[cb8][cb] * rp;
+      }
+      __syncthreads();
+      const double piv = colbuf[buf][c];
+      if (!(piv > 0.0)) {
+        bad = true;
+        break;
+      }
+      if (tid < jb && tid >= c) A[(i64)tid * cd.lda + c] = colbuf[buf][tid];
+      if (tid == 0) pivs[c] = piv;
+      double rb[CA];
+#pragma unroll
+      for (int cb = 0; cb < CA; ++cb) rb[cb] = rowbuf[buf][tc + 16 * cb];
+#pragma unroll
+      for (int ra = 0; ra < RA; ++ra) {
+        if (ra < cb8) continue;               // rows below 8 cb8 are finished
+        const int i = tr + TR * ra;
+        const double m = (i > c) ? colbuf[buf][i] : 0.0;
+#pragma unroll
+        for (int cb = 0; cb < CA; ++cb) {
+          if (cb < CA / 2 && cb < cbc) continue;               // C columns below 16 cbc: never read again
+          if (cb >= CA / 2 && cb - CA / 2 > cbc) continue;     // I columns beyond 16 (cbc + 1): zero in row c
+          a[ra][cb] -= m * rb[cb];
+        }
+      }
+    }
+  }
+  if (bad) sbad = 1;                           // every thread sees the same pivot: uniform
+  __syncthreads();
+  if (sbad) return false;
+  if (tid < jb) pivs[tid] = rsqrt(pivs[tid]);
+  __syncthreads();
+  for (int idx = tid; idx < jb * jb; idx += 128) {
+    const int i = idx / jb, c = idx - i * jb;
+    if (i >= c) A[(i64)i * cd.lda + c] *= pivs[c];
+  }
+  double* linv = cd.linv + (i64)(j0 / CB) * CB * CB;
+#pragma unroll
+  for (int ra = 0; ra < RA; ++ra) {
+    const int i = tr + TR * ra;
+#pragma unroll
+    for (int cb = CA / 2; cb < CA; ++cb) {
+      const int jj = tc + 16 * (cb - CA / 2);
+      linv[i * CB + jj] = (i < jb && jj < jb) ? a[ra][cb] * pivs[i] : 0.0;
+    }
+  }
+  return true;
+}
+
+// tiles of an NT product over m rows (row tile 32 when m <= 32)
+RSRS_DI void nt_rows(const NTDesc& d, int m, int n, int K, double* smem) {
+  if (m <= 32) {
+    if (m > 0) nt_tile<32>(d, m, n, K, 0, 0, smem);
+  } else {
+    for (int i0 = 0; i0 < m; i0 += GT) nt_tile<GT>(d, m, n, K, i0, 0, smem);
+  }
+}
+RSRS_DI void nn_rows(const NNDesc& d, int m, int n, int K, double* smem) {
+  if (m <= 32) {
+    if (m > 0) nn_tile<32>(d, m, n, K, 0, 0, smem);
+  } else {
+    for (int i0 = 0; i0 < m; i0 += GT) nn_tile<GT>(d, m, n, K, i0, 0, smem);
+  }
+}
+
+__global__ void __launch_bounds__(128, 3) chol_fused_kernel(const CholDesc* __restrict__ cds) {
+  extern __shared__ __align__(16) double smem[];
+  const CholDesc& cd = cds[blockIdx.x];
+  if (cd.status && *cd.status != ST_OK) return;
+  const int r = *cd.pr;
+  for (int j0 = 0; j0 < r; j0 += CB) {
+    const int jb = min(CB, r - j0);
+    if (j0 > 0) {
+      // P[j0:, J] -= L[j0:, 0:j0] L[J, 0:j0]^T  (C rows, then the B rows)
+      for (int part = 0; part < 2; ++part) {
+        NTDesc d{};
+        d.A = part ? cd.A + (i64)cd.uoff * cd.lda : cd.A + (i64)j0 * cd.lda;
+        d.lda = cd.lda;
+        d.B = cd.A + (i64)j0 * cd.lda;
+        d.ldb = cd.lda;
+        d.C = const_cast<double*>(d.A) + j0;
+        d.ldc = cd.lda;
+        d.alpha = -1.0;
+        d.beta = 1.0;
+        nt_rows(d, part ? cd.mextra : r - j0, jb, j0, smem);
+      }
+      __syncthreads();
+    }
+    if (!chol_diag_block128(cd, j0, r, smem)) {
+      if (threadIdx.x == 0 && cd.status) *cd.status = ST_SINGULAR_GRAM;
+      return;
+    }
+    __syncthreads();
+    // rows below the diagonal block: X <- X L_JJ^-T (in place; one column tile covers J)
+    for (int part = 0; part < 2; ++part) {
+      NTDesc d{};
+      d.A = part ? cd.A + (i64)cd.uoff * cd.lda + j0 : cd.A + (i64)(j0 + CB) * cd.lda + j0;
+      d.lda = cd.lda;
+      d.B = cd.linv + (i64)(j0 / CB) * CB * CB;
+      d.ldb = CB;
+      d.C = const_cast<double*>(d.A);
+      d.ldc = cd.lda;
+      d.alpha = 1.0;
+      d.beta = 0.0;
+      nt_rows(d, part ? cd.mextra : r - j0 - CB, jb, jb, smem);
+    }
+    __syncthreads();
+  }
+}
+
+// back substitution W = u L^-1 of one matrix per CTA, column blocks descending
+__global__ void __launch_bounds__(128, 3) chol_back_fused_kernel(const CholDesc* __restrict__ cds) {
+  extern __shared__ __align__(16) double smem[];
+  const CholDesc& cd = cds[blockIdx.x];
+  if (cd.status && *cd.status != ST_OK) return;
+  const int r = *cd.pr;
+  const int m = cd.mextra;
+  double* U = cd.A + (i64)cd.uoff * cd.lda;
+  for (int j0 = ((r - 1) / CB) * CB; j0 >= 0; j0 -= CB) {
+    const int jb = min(CB, r - j0);
+    const int K = r - j0 - CB;
+    if (K > 0) {   // W[:, J] = u[:, J] - W[:, J+] L[J+, J]
+      NNDesc d{};
+      d.A = U + j0 + CB;
+      d.lda = cd.lda;
+      d.B = cd.A + (i64)(j0 + CB) * cd.lda + j0;
+      d.ldb = cd.lda;
+      d.D = U + j0;
+      d.ldd = cd.lda;
+      d.alpha = -1.0;
+      d.beta = 1.0;
+      nn_rows(d, m, jb, K, smem);
+      __syncthreads();
+    }
+    {              // W[:, J] <- W[:, J] L_JJ^-1 (in place)
+      NNDesc d{};
+      d.A = U + j0;
+      d.lda = cd.lda;
+      d.B = cd.linv + (i64)(j0 / CB) * CB * CB;
+      d.ldb = CB;
+      d.D = U + j0;
+      d.ldd = cd.lda;
+      d.alpha = 1.0;
+      d.beta = 0.0;
+      nn_rows(d, m, jb, jb, smem);
+      __syncthreads();
+    }
+  }
+}
+
 }  // namespace rsrs

@@ -359,8 +359,10 @@ __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ bo
   if (nr <= 0 || b.status != ST_OK) return;
   const int ldn = b.ldn;
   const int ldx = nr + 1;
-  S* Is = Xs + nr * ldx;
-  int* ipiv = reinterpret_cast<int*>(Is + nr * ldx);
+  // X_rr (LU factors) in shared memory; inverses / triangular factors go straight to the
+  // factor pool (ld ldn), so that boxes up to ~165 rows (real) fit.  Before X_rr is gathered
+  // the same space holds T (n_r x k <= n_b^2 / 4); the index lists sit behind n_b (n_b + 1).
+  int* ipiv = reinterpret_cast<int*>(Xs + (i64)nb * (nb + 1));
   int* redloc = ipiv + nr;
   int* skelloc = redloc + nb;
   __shared__ int singular;
@@ -381,15 +383,30 @@ __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ bo
   const S* WZ = sym ? WY : ws + b.off_aug + (i64)(b.rmax + nb) * ldr + (i64)b.rmax * ldr;
   S* XY = ws + b.off_xy;
   S* XZ = ws + b.off_xz;
-  // 1. row combination X = W_r - T W_s
+  // T staged in shared memory (the X_rr space, not yet in use)
+  S* Ts = Xs;
+  for (int idx = tid; idx < nr * k; idx += 256) Ts[idx] = T[(i64)(idx / k) * ldn + idx % k];
+  __syncthreads();
+  // 1. row combination X = W_r - T W_s; the W_s loads go out 8 at a time (one round trip each)
   for (int idx = tid; idx < nr * r; idx += 256) {
     const int i = idx / r, j = idx % r;
     S vy = WY[(i64)redloc[i] * ldr + j];
     S vz = WZ[(i64)redloc[i] * ldr + j];
-    for (int s = 0; s < k; ++s) {
-      const S t = T[(i64)i * ldn + s];
-      vy = s_sub(vy, s_mul(t, WY[(i64)skelloc[s] * ldr + j]));
-      vz = s_sub(vz, s_mul(t, WZ[(i64)skelloc[s] * ldr + j]));
+    for (int s0 = 0; s0 < k; s0 += 8) {
+      S wy[8], wz[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const bool ok = s0 + q < k;
+        wy[q] = ok ? WY[(i64)skelloc[s0 + q] * ldr + j] : zero;
+        wz[q] = ok ? WZ[(i64)skelloc[s0 + q] * ldr + j] : zero;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (s0 + q < k) {
+          const S t = Ts[i * k + s0 + q];
+          vy = s_sub(vy, s_mul(t, wy[q]));
+          vz = s_sub(vz, s_mul(t, wz[q]));
+        }
     }
     XY[(i64)i * ldr + j] = vy;
     XZ[(i64)i * ldr + j] = vz;
@@ -402,16 +419,27 @@ __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ bo
       const int col = b.self_pos + redloc[jj];
       S vy = XY[(i64)i * ldr + col];
       S vz = XZ[(i64)i * ldr + col];
-      for (int s = 0; s < k; ++s) {
-        const S t = T[(i64)jj * ldn + s];
-        vy = s_sub(vy, s_mulc(XY[(i64)i * ldr + b.self_pos + skelloc[s]], t));
-        vz = s_sub(vz, s_mulc(XZ[(i64)i * ldr + b.self_pos + skelloc[s]], t));
+      for (int s0 = 0; s0 < k; s0 += 8) {
+        S xy[8], xz[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const bool ok = s0 + q < k;
+          xy[q] = ok ? XY[(i64)i * ldr + b.self_pos + skelloc[s0 + q]] : zero;
+          xz[q] = ok ? XZ[(i64)i * ldr + b.self_pos + skelloc[s0 + q]] : zero;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (s0 + q < k) {
+            const S t = Ts[jj * k + s0 + q];
+            vy = s_sub(vy, s_mulc(xy[q], t));
+            vz = s_sub(vz, s_mulc(xz[q], t));
+          }
       }
       XY[(i64)i * ldr + col] = vy;
       XZ[(i64)i * ldr + col] = vz;
     }
-    __syncthreads();
   }
+  __syncthreads();   // Ts (the X_rr space) is dead from here on
   // 3. gather X_rr (shared + factor), X_rc (nr x nc), X_cr (nc x nr)
   S* Xrr = fpool + b.f_Xrr;
   for (int idx = tid; idx < nr * nr; idx += 256) {
@@ -480,21 +508,19 @@ __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ bo
       if (tid == 0) b.status = ST_SINGULAR_XRR;
       return;
     }
-    // C^-1 (lower) column by column: C z = e_j
+    // C^-1 (lower) column by column: C z = e_j (a thread per column, written to the pool)
+    S* Cf = fpool + b.f_Xrr;
+    S* Ci = fpool + b.f_Xinv;
     for (int j = tid; j < nr; j += 256) {
       for (int i = 0; i < nr; ++i) {
         S v = (i == j) ? s_one(S()) : zero;
-        for (int q = j; q < i; ++q) v = s_sub(v, s_mul(Xs[i * ldx + q], Is[q * ldx + j]));
-        Is[i * ldx + j] = (i < j) ? zero : s_div(v, Xs[i * ldx + i]);
+        for (int q = j; q < i; ++q) v = s_sub(v, s_mul(Xs[i * ldx + q], Ci[(i64)q * ldn + j]));
+        Ci[(i64)i * ldn + j] = (i < j) ? zero : s_div(v, Xs[i * ldx + i]);
       }
     }
-    __syncthreads();
-    S* Cf = fpool + b.f_Xrr;
-    S* Ci = fpool + b.f_Xinv;
     for (int idx = tid; idx < nr * nr; idx += 256) {
       const int i = idx / nr, j = idx % nr;
       Cf[(i64)i * ldn + j] = j <= i ? Xs[i * ldx + j] : zero;
-      Ci[(i64)i * ldn + j] = Is[i * ldx + j];
     }
     return;
   }
@@ -560,33 +586,28 @@ __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ bo
     if (tid == 0) b.status = ST_SINGULAR_XRR;
     return;
   }
-  // 5. X_rr^-1 = U^-1 L^-1 P, column by column
+  // 5. X_rr^-1 = U^-1 L^-1 P, column by column (a thread per column, in the factor pool)
+  S* Is = fpool + b.f_Xinv;
   for (int j = tid; j < nr; j += 256) {
-    for (int i = 0; i < nr; ++i) Is[i * ldx + j] = (i == j) ? s_one(S()) : zero;
+    for (int i = 0; i < nr; ++i) Is[(i64)i * ldn + j] = (i == j) ? s_one(S()) : zero;
     for (int c = 0; c < nr; ++c) {
       const int q = ipiv[c];
       if (q != c) {
-        const S t = Is[c * ldx + j];
-        Is[c * ldx + j] = Is[q * ldx + j];
-        Is[q * ldx + j] = t;
+        const S t = Is[(i64)c * ldn + j];
+        Is[(i64)c * ldn + j] = Is[(i64)q * ldn + j];
+        Is[(i64)q * ldn + j] = t;
       }
     }
     for (int i = 0; i < nr; ++i) {
-      S s = Is[i * ldx + j];
-      for (int q = 0; q < i; ++q) s = s_sub(s, s_mul(Xs[i * ldx + q], Is[q * ldx + j]));
-      Is[i * ldx + j] = s;
+      S s = Is[(i64)i * ldn + j];
+      for (int q = 0; q < i; ++q) s = s_sub(s, s_mul(Xs[i * ldx + q], Is[(i64)q * ldn + j]));
+      Is[(i64)i * ldn + j] = s;
     }
     for (int i = nr - 1; i >= 0; --i) {
-      S s = Is[i * ldx + j];
-      for (int q = i + 1; q < nr; ++q) s = s_sub(s, s_mul(Xs[i * ldx + q], Is[q * ldx + j]));
-      Is[i * ldx + j] = s_div(s, Xs[i * ldx + i]);
+      S s = Is[(i64)i * ldn + j];
+      for (int q = i + 1; q < nr; ++q) s = s_sub(s, s_mul(Xs[i * ldx + q], Is[(i64)q * ldn + j]));
+      Is[(i64)i * ldn + j] = s_div(s, Xs[i * ldx + i]);
     }
-  }
-  __syncthreads();
-  S* Xinv = fpool + b.f_Xinv;
-  for (int idx = tid; idx < nr * nr; idx += 256) {
-    const int i = idx / nr, j = idx % nr;
-    Xinv[(i64)i * ldn + j] = Is[i * ldx + j];
   }
 }
 

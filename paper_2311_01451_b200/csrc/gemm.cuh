@@ -257,6 +257,30 @@ RSRS_DI void nn_tile(const NNDesc& d, int m, int n, int K, int i0, int j0, doubl
   // a warp whose sub-tile lies wholly outside D (skinny or ragged rows) skips its MMAs
   const bool wact = i0 + wr * (TM / 2) < m && j0 + cofs < n;
 
+  // 32-row tiles: the beta * C operand of the epilogue is loaded before the K loop, so its
+  // latency overlaps the GEMM instead of following it (ncu: the epilogue's dependent loads
+  // held ~35% of the stall samples of the row-gathered L/U update)
+  constexpr bool PRE = (TM == 32);
+  double2 cpre[PRE ? MT : 1][4];
+  if constexpr (PRE) {
+#pragma unroll
+    for (int t = 0; t < MT; ++t) {
+      const int i = i0 + wr * (TM / 2) + t * 8 + gid;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) cpre[t][u] = make_double2(0.0, 0.0);
+      if (i >= m || d.beta == 0.0) continue;
+      const double* crow;
+      if (inplace) crow = d.D + (d.rowD ? (i64)d.rowD[i] : (i64)i) * d.ldd;
+      else crow = d.Cin + (d.rowC ? (i64)d.rowC[i] : (i64)i) * d.ldc;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = j0 + cofs + u * 8 + 2 * tig;
+        if (j + 1 < n) cpre[t][u] = *reinterpret_cast<const double2*>(crow + j);
+        else if (j < n) cpre[t][u].x = crow[j];
+      }
+    }
+  }
+
   const int nk = K > 0 ? (K + GBK - 1) / GBK : 0;
   if (nk > 0) {
     fetch_rows(0);
@@ -312,11 +336,14 @@ RSRS_DI void nn_tile(const NNDesc& d, int m, int n, int K, int i0, int j0, doubl
       const int j = j0 + cofs + u * 8 + 2 * tig;
       if (j + 1 < n) {
         double2 c = make_double2(0.0, 0.0);
-        if (d.beta != 0.0) c = *reinterpret_cast<const double2*>(crow + j);
+        if constexpr (PRE) c = cpre[t][u];
+        else if (d.beta != 0.0) c = *reinterpret_cast<const double2*>(crow + j);
         *reinterpret_cast<double2*>(drow + j) =
             make_double2(d.beta * c.x + d.alpha * acc[t][u][0], d.beta * c.y + d.alpha * acc[t][u][1]);
       } else if (j < n) {
-        const double c = d.beta != 0.0 ? crow[j] : 0.0;
+        double c = 0.0;
+        if constexpr (PRE) c = cpre[t][u].x;
+        else if (d.beta != 0.0) c = crow[j];
         drow[j] = d.beta * c + d.alpha * acc[t][u][0];
       }
     }
@@ -671,22 +698,29 @@ __global__ void __launch_bounds__(128) skinny_nn_kernel(const NNDesc* __restrict
   // SK_COLS columns per CTA (the staged opA serves all of them), one column per thread per pass
   for (int j = blockIdx.y * cols + threadIdx.x; j < min(n, (int)(blockIdx.y + 1) * cols); j += 128) {
     for (int i0 = 0; i0 < m; i0 += 16) {
-      S acc[16];
+      S acc[16], dv[16];
+      // the D rows of this pass are read together with the first B rows (one round trip)
+#pragma unroll
+      for (int u = 0; u < 16; ++u) dv[u] = (i0 + u < m) ? D[(i64)rD[i0 + u] * d.ldd + j] : zero;
 #pragma unroll
       for (int u = 0; u < 16; ++u) acc[u] = zero;
-      for (int t = 0; t < K; ++t) {
-        const S b = B[(i64)rB[t] * d.ldb + j];
-        const S* at = As + t * mp + i0;
+      // 8 independent B loads in flight per thread (one memory round trip per 8 rows of B)
+      for (int t0 = 0; t0 < K; t0 += 8) {
+        S bv[8];
 #pragma unroll
-        for (int u = 0; u < 16; ++u) acc[u] = s_add(acc[u], s_mul(at[u], b));
+        for (int q = 0; q < 8; ++q) bv[q] = (t0 + q < K) ? B[(i64)rB[t0 + q] * d.ldb + j] : zero;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (t0 + q >= K) break;
+          const S* at = As + (t0 + q) * mp + i0;
+#pragma unroll
+          for (int u = 0; u < 16; ++u) acc[u] = s_add(acc[u], s_mul(at[u], bv[q]));
+        }
       }
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
         const int i = i0 + u;
-        if (i < m) {
-          S* dp = D + (i64)rD[i] * d.ldd + j;
-          *dp = s_add(*dp, s_scale(acc[u], d.alpha));
-        }
+        if (i < m) D[(i64)rD[i] * d.ldd + j] = s_add(dv[u], s_scale(acc[u], d.alpha));
       }
     }
   }

@@ -313,6 +313,222 @@ __global__ void __launch_bounds__(256) apply_bwd_kernel(const BoxDev* __restrict
   }
 }
 
+// ---------------------------------------------------------------------------
+// Packed solve records (block-diagonal form).  At the end of a level the factor
+// blocks the solve reads are copied into one compact, contiguous record per box
+// (solve_pack_kernel) laid out so that every factor load of the sweep is
+// coalesced and independent of the others (one memory round trip per phase):
+//   forward  [Tt (k x nr) | GLt (nr x nc) | Xit (nr x nr)]   column-major T, G_L, X_rr^-1
+//   backward [GU (nr x nc) | Tb (nr x k)]                   row-major, no padding
+// Each sub-block starts on an even scalar offset (16-byte aligned).
+RSRS_DI i64 ev2(i64 v) { return (v + 1) & ~(i64)1; }
+RSRS_DI i64 pack_fwd_size(int nr, int k, int nc) { return ev2((i64)k * nr) + ev2((i64)nr * nc) + ev2((i64)nr * nr); }
+RSRS_DI i64 pack_bwd_size(int nr, int k, int nc) { return ev2((i64)nr * nc) + ev2((i64)nr * k); }
+
+template <bool C>
+__global__ void __launch_bounds__(256) solve_pack_kernel(const BoxDev* __restrict__ boxes,
+                                                          const double* __restrict__ fpoold,
+                                                          const i64* __restrict__ pk, double* __restrict__ packd) {
+  typedef typename ScalarOf<C>::T S;
+  const BoxDev& b = boxes[blockIdx.x];
+  const int nr = b.nr, k = b.k, nc = b.nc;
+  if (nr <= 0) return;
+  const S* fpool = reinterpret_cast<const S*>(fpoold);
+  const S* T = fpool + b.f_T;
+  const S* GL = fpool + b.f_GL;
+  const S* GU = fpool + b.f_GU;
+  const S* Xi = fpool + b.f_Xinv;
+  const int ldn = b.ldn, ldr = b.ldr;
+  S* P = reinterpret_cast<S*>(packd) + pk[blockIdx.x];
+  S* Tt = P;
+  S* GLt = Tt + ev2((i64)k * nr);
+  S* Xit = GLt + ev2((i64)nr * nc);
+  S* GUp = Xit + ev2((i64)nr * nr);
+  S* Tb = GUp + ev2((i64)nr * nc);
+  const int tid = threadIdx.x, nt = blockDim.x;
+  // writes are contiguous in the packed index, reads strided (one-time copy)
+  for (int t = tid; t < k * nr; t += nt) {
+    const int j = t / nr, i = t % nr;
+    Tt[t] = T[(i64)i * ldn + j];
+  }
+  for (i64 t = tid; t < (i64)nr * nc; t += nt) {
+    const int j = (int)(t / nc), i = (int)(t % nc);
+    GLt[t] = GL[(i64)i * ldn + j];
+  }
+  for (int t = tid; t < nr * nr; t += nt) {
+    const int j = t / nr, i = t % nr;
+    Xit[t] = Xi[(i64)i * ldn + j];
+  }
+  for (i64 t = tid; t < (i64)nr * nc; t += nt) {
+    const int i = (int)(t / nc), j = (int)(t % nc);
+    GUp[t] = GU[(i64)i * ldr + j];
+  }
+  for (int t = tid; t < nr * k; t += nt) {
+    const int i = t / k, j = t % k;
+    Tb[t] = T[(i64)i * ldn + j];
+  }
+}
+
+// forward solve of one box from its packed record:
+//   x_r -= T x_s ;  then (both from the updated x_r)  x_c -= G_L x_r ,  x_r <- X_rr^-1 x_r
+// A thread per output row; its factor loads (a column-major column walk) are coalesced
+// across the CTA and independent of each other.
+template <bool C, int NRB>
+__global__ void __launch_bounds__(256) solve_fwd_packed_kernel(const BoxDev* __restrict__ boxes,
+                                                                const i64* __restrict__ pk,
+                                                                const double* __restrict__ packd,
+                                                                const int* __restrict__ ipool,
+                                                                double* __restrict__ xd, i64 ldx, int nrhs) {
+  typedef typename ScalarOf<C>::T S;
+  extern __shared__ __align__(16) double smd[];
+  const BoxDev& b = boxes[blockIdx.x];
+  const int nr = b.nr, k = b.k, nc = b.nc;
+  if (nr <= 0) return;
+  S* sm = reinterpret_cast<S*>(smd);
+  S* x = reinterpret_cast<S*>(xd);
+  const S* Tt = reinterpret_cast<const S*>(packd) + pk[blockIdx.x];
+  const S* GLt = Tt + ev2((i64)k * nr);
+  const S* Xit = GLt + ev2((i64)nr * nc);
+  const int* red = ipool + b.f_red;
+  const int* skel = ipool + b.f_skel;
+  const int* cc = ipool + b.f_c;
+  S* xs = sm;
+  S* xr = xs + k * NRB;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int c0 = 0; c0 < nrhs; c0 += NRB) {
+    load_rows<S, NRB>(xs, x, skel, k, ldx, c0, nrhs);
+    load_rows<S, NRB>(xr, x, red, nr, ldx, c0, nrhs);
+    __syncthreads();
+    for (int i = tid; i < nr; i += nt) {
+      S acc[NRB];
+#pragma unroll
+      for (int c = 0; c < NRB; ++c) acc[c] = s_zero(S());
+      // loads in predicated chunks of 8: all in flight at once whatever the trip count
+      for (int j0 = 0; j0 < k; j0 += 8) {
+        S tv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) tv[q] = (j0 + q < k) ? __ldg(Tt + (i64)(j0 + q) * nr + i) : s_zero(S());
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (j0 + q < k)
+#pragma unroll
+            for (int c = 0; c < NRB; ++c) acc[c] = s_add(acc[c], s_mul(tv[q], xs[(j0 + q) * NRB + c]));
+      }
+#pragma unroll
+      for (int c = 0; c < NRB; ++c) xr[i * NRB + c] = s_sub(xr[i * NRB + c], acc[c]);
+    }
+    __syncthreads();
+    for (int i = tid; i < nc + nr; i += nt) {
+      const bool isc = i < nc;
+      const int ii = isc ? i : i - nc;
+      const S* col = isc ? GLt + ii : Xit + ii;
+      const i64 ldc = isc ? nc : nr;
+      S acc[NRB];
+#pragma unroll
+      for (int c = 0; c < NRB; ++c) acc[c] = s_zero(S());
+      for (int j0 = 0; j0 < nr; j0 += 8) {
+        S gv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) gv[q] = (j0 + q < nr) ? __ldg(col + (i64)(j0 + q) * ldc) : s_zero(S());
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (j0 + q < nr)
+#pragma unroll
+            for (int c = 0; c < NRB; ++c) acc[c] = s_add(acc[c], s_mul(gv[q], xr[(j0 + q) * NRB + c]));
+      }
+      if (isc) {
+        S* xp = x + (i64)cc[ii] * ldx + c0;
+#pragma unroll
+        for (int c = 0; c < NRB; ++c)
+          if (c0 + c < nrhs) xp[c] = s_sub(xp[c], acc[c]);
+      } else {
+        S* xp = x + (i64)red[ii] * ldx + c0;
+#pragma unroll
+        for (int c = 0; c < NRB; ++c)
+          if (c0 + c < nrhs) xp[c] = acc[c];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// backward solve of one box from its packed record: x_r -= G_U x_c ; x_s -= T^* x_r
+// G_U rows by whole warps (lanes over the coupled columns), T^* by a thread per skeleton.
+template <bool C, int NRB>
+__global__ void __launch_bounds__(256) solve_bwd_packed_kernel(const BoxDev* __restrict__ boxes,
+                                                                const i64* __restrict__ pk,
+                                                                const double* __restrict__ packd,
+                                                                const int* __restrict__ ipool,
+                                                                double* __restrict__ xd, i64 ldx, int nrhs) {
+  typedef typename ScalarOf<C>::T S;
+  extern __shared__ __align__(16) double smd[];
+  const BoxDev& b = boxes[blockIdx.x];
+  const int nr = b.nr, k = b.k, nc = b.nc;
+  if (nr <= 0) return;
+  S* sm = reinterpret_cast<S*>(smd);
+  S* x = reinterpret_cast<S*>(xd);
+  const S* GU = reinterpret_cast<const S*>(packd) + pk[blockIdx.x] + pack_fwd_size(nr, k, nc);
+  const S* Tb = GU + ev2((i64)nr * nc);
+  const int* red = ipool + b.f_red;
+  const int* skel = ipool + b.f_skel;
+  const int* cc = ipool + b.f_c;
+  S* xc = sm;
+  S* xr = xc + nc * NRB;
+  const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+  for (int c0 = 0; c0 < nrhs; c0 += NRB) {
+    load_rows<S, NRB>(xc, x, cc, nc, ldx, c0, nrhs);
+    load_rows<S, NRB>(xr, x, red, nr, ldx, c0, nrhs);
+    __syncthreads();
+    for (int i = warp; i < nr; i += nw) {
+      const S* row = GU + (i64)i * nc;
+      S acc[NRB];
+#pragma unroll
+      for (int c = 0; c < NRB; ++c) acc[c] = s_zero(S());
+      for (int j0 = lane; j0 < nc; j0 += 32 * 8) {
+        S gv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) gv[q] = (j0 + 32 * q < nc) ? __ldg(row + j0 + 32 * q) : s_zero(S());
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (j0 + 32 * q < nc)
+#pragma unroll
+            for (int c = 0; c < NRB; ++c) acc[c] = s_add(acc[c], s_mul(gv[q], xc[(j0 + 32 * q) * NRB + c]));
+      }
+#pragma unroll
+      for (int c = 0; c < NRB; ++c) acc[c] = warp_sum(acc[c]);
+      if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < NRB; ++c) {
+          const S v = s_sub(xr[i * NRB + c], acc[c]);
+          xr[i * NRB + c] = v;
+          if (c0 + c < nrhs) x[(i64)red[i] * ldx + c0 + c] = v;
+        }
+      }
+    }
+    __syncthreads();
+    for (int sidx = tid; sidx < k; sidx += nt) {
+      S acc[NRB];
+#pragma unroll
+      for (int c = 0; c < NRB; ++c) acc[c] = s_zero(S());
+      for (int i0 = 0; i0 < nr; i0 += 8) {
+        S tv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) tv[q] = (i0 + q < nr) ? s_conj(__ldg(Tb + (i64)(i0 + q) * k + sidx)) : s_zero(S());
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (i0 + q < nr)
+#pragma unroll
+            for (int c = 0; c < NRB; ++c) acc[c] = s_add(acc[c], s_mul(tv[q], xr[(i0 + q) * NRB + c]));
+      }
+      S* xp = x + (i64)skel[sidx] * ldx + c0;
+#pragma unroll
+      for (int c = 0; c < NRB; ++c)
+        if (c0 + c < nrhs) xp[c] = s_sub(xp[c], acc[c]);
+    }
+    __syncthreads();
+  }
+}
+
 // top block: x_S <- A~_SS^-1 x_S (LU with pivots) or x_S <- A~_SS x_S
 // Blocked substitution: a 32 x 32 diagonal block is solved by one warp with shuffles (no
 // CTA barrier per row), the rows below / above are updated by the whole CTA: 2 barriers
@@ -430,6 +646,20 @@ __global__ void permute_rows_kernel(const double* __restrict__ src, i64 lds, dou
     else
       dst[o * ldd + j] = src[t * lds + j];
   }
+}
+
+// the same for narrow right-hand sides (ncol < 32): a thread per (row, column)
+__global__ void permute_rows_flat_kernel(const double* __restrict__ src, i64 lds, double* __restrict__ dst, i64 ldd,
+                                         const int64_t* __restrict__ perm, int64_t N, int ncol, int inverse) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= N * ncol) return;
+  const int64_t t = e / ncol;
+  const int j = (int)(e - t * ncol);
+  const int64_t o = perm[t];
+  if (!inverse)
+    dst[t * ldd + j] = src[o * lds + j];
+  else
+    dst[o * ldd + j] = src[t * lds + j];
 }
 
 // ---------------------------------------------------------------------------

@@ -8,6 +8,9 @@ name = os.environ.get("CFG", "c2")
 cfg = W.CONFIGS[name]
 if os.environ.get("NSIDE"):
     cfg = cfg.scaled(int(os.environ["NSIDE"]))
+if os.environ.get("EPS"):
+    from dataclasses import replace
+    cfg = replace(cfg, eps=float(os.environ["EPS"]))
 runs = [tuple(float(v) for v in x.split(":")) for x in os.environ.get("RUNS", "1024:1").split(",")]
 pmax = max(int(r[0]) for r in runs)
 ITERS = int(os.environ.get("ITERS", "2"))
