@@ -77,6 +77,8 @@ bool g_sweep_graph = true;   // RSRS_SWEEP_GRAPH=0: launch the solve / apply swe
 bool g_debug = false;  // RSRS_DEBUG_SYNC=1: synchronize and check after every launch
 bool g_trace = false;  // RSRS_TRACE=1: host-side time split of rsrs_factor on stderr
 int g_chol_fuse_rmax = 320;          // RSRS_CHOL_FUSE_RMAX: largest real near field for the fused Cholesky (0: off)
+int g_back_fuse_rmax = 1 << 30;      // RSRS_BACK_FUSE_RMAX: the same for the fused back substitution
+int g_fuse_min_batch = 128;          // RSRS_FUSE_MIN_BATCH: fewest matrices of a launch for the fused kernels
 int g_skinny_cols = rsrs::SK_COLS;   // RSRS_SKINNY_COLS: columns per CTA of the skinny E/F kernel
 int g_tm32_nt = 32, g_tm32_nn = 32;  // RSRS_TM32_NT / RSRS_TM32_NN: 32-row tiles when every row count <= this
 // 32-row tiles for every real GEMM of the current level (set per level by the planner, per host
@@ -167,6 +169,8 @@ void init_kernels() {
   if (const char* t = getenv("RSRS_TM32_NN")) g_tm32_nn = atoi(t);
   if (const char* t = getenv("RSRS_TM32_RATIO")) g_tm32_ratio = atof(t);
   if (const char* cf = getenv("RSRS_CHOL_FUSE_RMAX")) g_chol_fuse_rmax = atoi(cf);
+  if (const char* bf = getenv("RSRS_BACK_FUSE_RMAX")) g_back_fuse_rmax = atoi(bf);
+  if (const char* fm = getenv("RSRS_FUSE_MIN_BATCH")) g_fuse_min_batch = std::max(1, atoi(fm));
   int dev = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&g_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
@@ -353,8 +357,10 @@ void launch_skinny(bool cplx, const NNDesc* d, int n, int ncols, cudaStream_t s,
 
 // real near fields up to g_chol_fuse_rmax rows: one fused launch per batch (chol.cuh)
 void launch_chol_any(bool cplx, const CholDesc* d, int nmat, int rmax, int mext, cudaStream_t s, int64_t& l) {
-  if (!cplx && rmax <= g_chol_fuse_rmax) {
-    if (nmat > 0) {
+  // (one CTA per matrix: only for batches that fill the GPU; a lone matrix such as the top block keeps
+  // the tile-parallel per-panel launches)
+  if (!cplx && rmax <= g_chol_fuse_rmax && nmat >= g_fuse_min_batch) {
+    {
       rsrs::chol_fused_kernel<<<nmat, 128, rsrs::NT_SMEM, s>>>(d);
       post("chol_fused", s, l);
     }
@@ -364,8 +370,8 @@ void launch_chol_any(bool cplx, const CholDesc* d, int nmat, int rmax, int mext,
   else launch_chol_blocked<false>(d, nmat, rmax, mext, s, l);
 }
 void launch_back_any(bool cplx, const CholDesc* d, int nmat, int rmax, int mext, cudaStream_t s, int64_t& l) {
-  if (!cplx && rmax <= g_chol_fuse_rmax) {
-    if (nmat > 0) {
+  if (!cplx && rmax <= g_back_fuse_rmax && nmat >= g_fuse_min_batch) {
+    {
       rsrs::chol_back_fused_kernel<<<nmat, 128, rsrs::NT_SMEM, s>>>(d);
       post("chol_back_fused", s, l);
     }
@@ -422,6 +428,7 @@ struct rsrs_factor_s {
   int* d_S = nullptr;                             // tree positions of S
   double* d_ASS = nullptr;                        // A~_SS
   double* d_LU = nullptr;                         // LU of A~_SS
+  double* d_Ainv = nullptr;                       // A~_SS^-1 (formed from the LU; the solve's top step)
   int* d_piv = nullptr;
   std::vector<int64_t> S_host;
   int64_t* d_perm = nullptr;
@@ -1645,6 +1652,19 @@ struct Planner {
     if (cplx) rsrs::top_lu_kernel<true><<<1, 1024, 0, s>>>(f->d_LU, ldS, nS, f->d_piv, dstat);
     else rsrs::top_lu_kernel<false><<<1, 1024, 0, s>>>(f->d_LU, ldS, nS, f->d_piv, dstat);
     post("top_lu_kernel", s, launches);
+    {
+      // explicit A~_SS^-1 = solve of LU X = I, its columns spread over the grid, so that the top step of
+      // every solve is one matrix-vector product instead of 2 |S| dependent substitution steps
+      DBuf* Ib = keep(sS * nS * ldS);
+      DBuf* io = keep(sizeof(int) * nS);
+      f->d_Ainv = Ib->as<double>();
+      rsrs::identity_iota_kernel<<<(nS + 255) / 256, 256, 0, s>>>(f->d_Ainv, ldS, nS, SC, io->as<int>());
+      post("identity_iota_kernel", s, launches);
+      const unsigned g = (unsigned)std::min(nS, 296);
+      if (cplx) rsrs::top_solve_kernel<true><<<g, 1024, sS * nS, s>>>(f->d_LU, ldS, nS, f->d_piv, io->as<int>(), f->d_Ainv, ldS, nS);
+      else rsrs::top_solve_kernel<false><<<g, 1024, sS * nS, s>>>(f->d_LU, ldS, nS, f->d_piv, io->as<int>(), f->d_Ainv, ldS, nS);
+      post("top_solve_kernel(inverse)", s, launches);
+    }
     toc();
     int hst[4];
     CK(cudaMemcpyAsync(hst, dstat, sizeof(hst), cudaMemcpyDeviceToHost, s));
@@ -1972,7 +1992,10 @@ static void run_sweep_nrb(rsrs_factorization f, double* x, int64_t nrhs, bool so
       M.batch(b, 0);
     }
     if (f->nS > 0) {
-      rsrs::top_solve_kernel<C><<<1, 1024, s1 * f->nS, s>>>(f->d_LU, f->ldS, f->nS, f->d_piv, f->d_S, x, nrhs, nr);
+      if (g_solve_packed && f->d_Ainv)
+        rsrs::top_apply_kernel<C><<<1, 1024, s1 * f->nS, s>>>(f->d_Ainv, f->ldS, f->nS, f->d_S, x, nrhs, nr);
+      else
+        rsrs::top_solve_kernel<C><<<1, 1024, s1 * f->nS, s>>>(f->d_LU, f->ldS, f->nS, f->d_piv, f->d_S, x, nrhs, nr);
       CK(cudaGetLastError());
     }
     M.list(f->d_S, f->nS);

@@ -426,12 +426,12 @@ __global__ void __launch_bounds__(256) solve_fwd_packed_kernel(const BoxDev* __r
       S acc[NRB];
 #pragma unroll
       for (int c = 0; c < NRB; ++c) acc[c] = s_zero(S());
-      for (int j0 = 0; j0 < nr; j0 += 8) {
-        S gv[8];
+      for (int j0 = 0; j0 < nr; j0 += 16) {
+        S gv[16];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) gv[q] = (j0 + q < nr) ? __ldg(col + (i64)(j0 + q) * ldc) : s_zero(S());
+        for (int q = 0; q < 16; ++q) gv[q] = (j0 + q < nr) ? __ldg(col + (i64)(j0 + q) * ldc) : s_zero(S());
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
+        for (int q = 0; q < 16; ++q)
           if (j0 + q < nr)
 #pragma unroll
             for (int c = 0; c < NRB; ++c) acc[c] = s_add(acc[c], s_mul(gv[q], xr[(j0 + q) * NRB + c]));
@@ -479,29 +479,46 @@ __global__ void __launch_bounds__(256) solve_bwd_packed_kernel(const BoxDev* __r
     load_rows<S, NRB>(xc, x, cc, nc, ldx, c0, nrhs);
     load_rows<S, NRB>(xr, x, red, nr, ldx, c0, nrhs);
     __syncthreads();
-    for (int i = warp; i < nr; i += nw) {
-      const S* row = GU + (i64)i * nc;
-      S acc[NRB];
+    // RW rows per warp at a time, 8 column loads per row and lane: 8 RW loads in flight per lane
+    constexpr int RW = NRB <= 4 ? 4 : 2;
+    for (int i0 = warp * RW; i0 < nr; i0 += nw * RW) {
+      S acc[RW][NRB];
 #pragma unroll
-      for (int c = 0; c < NRB; ++c) acc[c] = s_zero(S());
+      for (int r = 0; r < RW; ++r)
+#pragma unroll
+        for (int c = 0; c < NRB; ++c) acc[r][c] = s_zero(S());
       for (int j0 = lane; j0 < nc; j0 += 32 * 8) {
-        S gv[8];
+        S gv[RW][8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) gv[q] = (j0 + 32 * q < nc) ? __ldg(row + j0 + 32 * q) : s_zero(S());
+        for (int r = 0; r < RW; ++r)
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            gv[r][q] = (i0 + r < nr && j0 + 32 * q < nc) ? __ldg(GU + (i64)(i0 + r) * nc + j0 + 32 * q) : s_zero(S());
 #pragma unroll
         for (int q = 0; q < 8; ++q)
           if (j0 + 32 * q < nc)
 #pragma unroll
-            for (int c = 0; c < NRB; ++c) acc[c] = s_add(acc[c], s_mul(gv[q], xc[(j0 + 32 * q) * NRB + c]));
+            for (int c = 0; c < NRB; ++c) {
+              const S xv = xc[(j0 + 32 * q) * NRB + c];
+#pragma unroll
+              for (int r = 0; r < RW; ++r) acc[r][c] = s_add(acc[r][c], s_mul(gv[r][q], xv));
+            }
       }
 #pragma unroll
-      for (int c = 0; c < NRB; ++c) acc[c] = warp_sum(acc[c]);
+      for (int r = 0; r < RW; ++r)
+#pragma unroll
+        for (int c = 0; c < NRB; ++c) acc[r][c] = warp_sum(acc[r][c]);
       if (lane == 0) {
 #pragma unroll
-        for (int c = 0; c < NRB; ++c) {
-          const S v = s_sub(xr[i * NRB + c], acc[c]);
-          xr[i * NRB + c] = v;
-          if (c0 + c < nrhs) x[(i64)red[i] * ldx + c0 + c] = v;
+        for (int r = 0; r < RW; ++r) {
+          const int i = i0 + r;
+          if (i >= nr) break;
+#pragma unroll
+          for (int c = 0; c < NRB; ++c) {
+            const S v = s_sub(xr[i * NRB + c], acc[r][c]);
+            xr[i * NRB + c] = v;
+            if (c0 + c < nrhs) x[(i64)red[i] * ldx + c0 + c] = v;
+          }
         }
       }
     }
@@ -544,7 +561,7 @@ __global__ void __launch_bounds__(1024) top_solve_kernel(const double* __restric
   const S* LU = reinterpret_cast<const S*>(LUd);
   S* x = reinterpret_cast<S*>(xd);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int col = 0; col < nrhs; ++col) {
+  for (int col = blockIdx.x; col < nrhs; col += gridDim.x) {   // columns over the grid (explicit inverse)
     for (int i = tid; i < n; i += blockDim.x) xs[i] = x[(i64)Sidx[i] * ldx + col];
     __syncthreads();
     if (tid == 0)
@@ -626,12 +643,29 @@ __global__ void __launch_bounds__(1024) top_apply_kernel(const double* __restric
     __syncthreads();
     for (int i = warp; i < n; i += blockDim.x / 32) {
       S v = s_zero(S());
-      for (int j = lane; j < n; j += 32) v = s_add(v, s_mul(A[(i64)i * lda + j], xs[j]));
+      const S* row = A + (i64)i * lda;
+      for (int j0 = lane; j0 < n; j0 += 32 * 8) {   // 8 row loads in flight per lane
+        S a[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) a[q] = (j0 + 32 * q < n) ? row[j0 + 32 * q] : s_zero(S());
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (j0 + 32 * q < n) v = s_add(v, s_mul(a[q], xs[j0 + 32 * q]));
+      }
       v = warp_sum(v);
       if (lane == 0) x[(i64)Sidx[i] * ldx + col] = v;
     }
     __syncthreads();
   }
+}
+
+// X = I (n x n, ld in scalars of sc doubles) and iota[i] = i
+__global__ void identity_iota_kernel(double* __restrict__ X, i64 ld, int n, int sc, int* __restrict__ iota) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double* row = X + (i64)i * ld * sc;
+  for (int j = 0; j < n * sc; ++j) row[j] = (j == i * sc) ? 1.0 : 0.0;
+  iota[i] = i;
 }
 
 // x_tree[t, :] = b[perm[t], :]  /  b[perm[t], :] = x_tree[t, :]

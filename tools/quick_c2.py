@@ -56,7 +56,8 @@ for (pf, g) in runs:
         ks = []
         for lev in range(t.L, 1, -1):
             k = f.ranks(lev, len(t.level(lev)["keys"])); k = k[k >= 0]
-            ks.append(f"L{lev}:{k.min()}/{k.mean():.1f}/{k.max()}")
+            if k.size:
+                ks.append(f"L{lev}:{k.min()}/{k.mean():.1f}/{k.max()}")
         print(f"p={p} g={g}: residual {res.item():.3e} |S| {st['top_size']} ranks {' '.join(ks)}", flush=True)
         for c in f.profile():
             if c["launches"]:

@@ -92,7 +92,7 @@ CONFIGS = {
     # complement T11 = A11 - A12 A22^-1 A21 of a 3D Poisson slab decomposition (slab width b = 10),
     # N = n^2 interface points, atol = 5e-6 (the paper's tightest; its leaf m = 350 is capped here at
     # 100-point leaves by the per-box kernels' shared memory, reading R20)
-    "t11": Config("t11", "grid2d", 320, "t11", "f64", leaf=100, p=1024, eps=5e-6, seed=6, g=2.0,
+    "t11": Config("t11", "grid2d", 320, "t11", "f64", leaf=100, p=1536, eps=5e-6, seed=6, g=2.0,
                   extra={"slab_b": 10}),
 }
 
