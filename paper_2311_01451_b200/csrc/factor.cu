@@ -783,11 +783,13 @@ struct Planner {
       };
       const rsrs::TreeLevel& lv = T.levels[lev];
       const int nbox = (int)lv.nboxes;
+      int lvl_maxnb = 0;
       {
         int64_t p32 = 0, p64 = 0;
         for (int b = 0; b < nbox; ++b) {
           p32 += (nb_all[b] + 31) / 32 * 32;
           p64 += (nb_all[b] + 63) / 64 * 64;
+          lvl_maxnb = std::max(lvl_maxnb, nb_all[b]);
         }
         t_level_tm32 = p64 > 0 && (double)p32 < g_tm32_ratio * (double)p64;
       }
@@ -1283,13 +1285,14 @@ struct Planner {
               double* pO = gpool->as<double>();
               double* pP = pO + SC * gpool_side;
               const int2* wk = gwork_b.as<int2>() + gwork_off[bi_idx];
+              const int mbk = std::max(1, lvl_maxnb);   // largest block / T dimension (<= GB_MAX here)
               dim3 gu(nw, sides);
               if (cplx)
-                rsrs::gblk_update_kernel<true><<<gu, 256, rsrs::gblk_smem<true>(), s>>>(dboxes, wk, gtab_b.as<rsrs::GBlk>(), pO, pP, fpool,
-                                                                   diws);
+                rsrs::gblk_update_kernel<true><<<gu, 128, rsrs::gblk_smem_for<true>(mbk), s>>>(dboxes, wk, gtab_b.as<rsrs::GBlk>(), pO, pP, fpool,
+                                                                   diws, mbk);
               else
-                rsrs::gblk_update_kernel<false><<<gu, 256, rsrs::gblk_smem<false>(), s>>>(dboxes, wk, gtab_b.as<rsrs::GBlk>(), pO, pP, fpool,
-                                                                    diws);
+                rsrs::gblk_update_kernel<false><<<gu, 128, rsrs::gblk_smem_for<false>(mbk), s>>>(dboxes, wk, gtab_b.as<rsrs::GBlk>(), pO, pP, fpool,
+                                                                    diws, mbk);
               post("gblk_update_kernel", s, launches);
             }
           }

@@ -106,18 +106,22 @@ __global__ void __launch_bounds__(256) gblk_work_kernel(int nq, const BoxDev* __
 constexpr int GB_MAX = 64;
 constexpr int GB_LD = GB_MAX + 1;
 template <bool C> constexpr int gblk_smem() { return 2 * GB_MAX * GB_LD * (C ? 16 : 8) + 2 * GB_MAX * 4; }
+// shared memory of one launch whose blocks are at most mb x mb (the level's largest box): the sphere's
+// leaf blocks are <= 30 x 30, so sizing for 64 x 64 held occupancy at 3 CTAs per SM
+template <bool C> inline int gblk_smem_for(int mb) { return 2 * mb * (mb + 1) * (C ? 16 : 8) + 2 * mb * 4; }
 template <bool C>
-__global__ void __launch_bounds__(256) gblk_update_kernel(const BoxDev* __restrict__ level_boxes,
+__global__ void __launch_bounds__(128) gblk_update_kernel(const BoxDev* __restrict__ level_boxes,
                                                           const int2* __restrict__ work,
                                                           const GBlk* __restrict__ tab, double* __restrict__ poolO,
                                                           double* __restrict__ poolP, const double* __restrict__ fpoold,
-                                                          const int* __restrict__ iws) {
+                                                          const int* __restrict__ iws, int mb) {
   typedef typename ScalarOf<C>::T S;
   extern __shared__ __align__(16) double gsm[];
+  const int GB_LD = mb + 1;                 // blocks and T are at most mb x mb (mb = launch's largest box)
   S* Bs = reinterpret_cast<S*>(gsm);        // block (nrow x ncol), ld GB_LD
-  S* Ts = Bs + GB_MAX * GB_LD;              // T (n_r x k), ld GB_LD
-  int* skl = reinterpret_cast<int*>(Ts + GB_MAX * GB_LD);
-  int* red = skl + GB_MAX;
+  S* Ts = Bs + mb * GB_LD;                  // T (n_r x k), ld GB_LD
+  int* skl = reinterpret_cast<int*>(Ts + mb * GB_LD);
+  int* red = skl + mb;
   const int2 w = work[blockIdx.x];
   const BoxDev& b = level_boxes[w.x];
   const int k = b.k, nr = b.nr;
@@ -125,17 +129,17 @@ __global__ void __launch_bounds__(256) gblk_update_kernel(const BoxDev* __restri
   const GBlk e = tab[w.y];
   const int tid = threadIdx.x;
   const S* T = reinterpret_cast<const S*>(fpoold) + b.f_T;
-  for (int idx = tid; idx < nr * k; idx += 256) Ts[(idx / k) * GB_LD + idx % k] = T[(i64)(idx / k) * b.ldn + idx % k];
-  for (int q = tid; q < k; q += 256) skl[q] = iws[b.off_skelrow + q] - b.row0;
-  for (int i = tid; i < nr; i += 256) red[i] = iws[b.off_redrow + i] - b.row0;
+  for (int idx = tid; idx < nr * k; idx += blockDim.x) Ts[(idx / k) * GB_LD + idx % k] = T[(i64)(idx / k) * b.ldn + idx % k];
+  for (int q = tid; q < k; q += blockDim.x) skl[q] = iws[b.off_skelrow + q] - b.row0;
+  for (int i = tid; i < nr; i += blockDim.x) red[i] = iws[b.off_redrow + i] - b.row0;
   S* B = reinterpret_cast<S*>(blockIdx.y ? poolP : poolO) + e.off;
-  for (int idx = tid; idx < e.nrow * e.ncol; idx += 256) {
+  for (int idx = tid; idx < e.nrow * e.ncol; idx += blockDim.x) {
     const int r = idx / e.ncol, c = idx % e.ncol;
     Bs[r * GB_LD + c] = B[(i64)r * e.ld + c];
   }
   __syncthreads();
   if (e.mode != 1) {   // rows: B[s, :] += T^* B[r, :]   (red and skel rows are disjoint)
-    for (int idx = tid; idx < k * e.ncol; idx += 256) {
+    for (int idx = tid; idx < k * e.ncol; idx += blockDim.x) {
       const int q = idx / e.ncol, c = idx % e.ncol;
       S acc = Bs[skl[q] * GB_LD + c];
       for (int i = 0; i < nr; ++i) acc = s_add(acc, s_mul(s_conj(Ts[i * GB_LD + q]), Bs[red[i] * GB_LD + c]));
@@ -144,7 +148,7 @@ __global__ void __launch_bounds__(256) gblk_update_kernel(const BoxDev* __restri
     __syncthreads();
   }
   if (e.mode != 0) {   // columns: B[:, s] += B[:, r] T
-    for (int idx = tid; idx < e.nrow * k; idx += 256) {
+    for (int idx = tid; idx < e.nrow * k; idx += blockDim.x) {
       const int r = idx / k, q = idx % k;
       S acc = Bs[r * GB_LD + skl[q]];
       for (int i = 0; i < nr; ++i) acc = s_add(acc, s_mul(Bs[r * GB_LD + red[i]], Ts[i * GB_LD + q]));
@@ -154,12 +158,12 @@ __global__ void __launch_bounds__(256) gblk_update_kernel(const BoxDev* __restri
   }
   // write back only what changed: the box's rows (mode 0, 2) and columns (mode 1, 2)
   if (e.mode != 1)
-    for (int idx = tid; idx < k * e.ncol; idx += 256) {
+    for (int idx = tid; idx < k * e.ncol; idx += blockDim.x) {
       const int q = idx / e.ncol, c = idx % e.ncol;
       B[(i64)skl[q] * e.ld + c] = Bs[skl[q] * GB_LD + c];
     }
   if (e.mode != 0)
-    for (int idx = tid; idx < e.nrow * k; idx += 256) {
+    for (int idx = tid; idx < e.nrow * k; idx += blockDim.x) {
       const int r = idx / k, q = idx % k;
       B[(i64)r * e.ld + skl[q]] = Bs[r * GB_LD + skl[q]];
     }
