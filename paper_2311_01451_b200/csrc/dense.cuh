@@ -387,56 +387,86 @@ __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ bo
   S* Ts = Xs;
   for (int idx = tid; idx < nr * k; idx += 256) Ts[idx] = T[(i64)(idx / k) * ldn + idx % k];
   __syncthreads();
-  // 1. row combination X = W_r - T W_s; the W_s loads go out 8 at a time (one round trip each)
-  for (int idx = tid; idx < nr * r; idx += 256) {
-    const int i = idx / r, j = idx % r;
-    S vy = WY[(i64)redloc[i] * ldr + j];
-    S vz = WZ[(i64)redloc[i] * ldr + j];
-    for (int s0 = 0; s0 < k; s0 += 8) {
-      S wy[8], wz[8];
+  // 1. row combination X = W_r - T W_s: a thread per near column j; the column's skeleton entries
+  //    (chunks of 16) are held in registers and the redundant rows go 8 at a time, every load of a
+  //    group independent (a thread-per-element loop waited one memory round trip per element)
+  constexpr int SKC = 8;
+  for (int j = tid; j < r; j += 256) {
+    for (int s0 = 0; s0 < k || s0 == 0; s0 += SKC) {
+      S wy[SKC], wz[SKC];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < SKC; ++q) {
         const bool ok = s0 + q < k;
         wy[q] = ok ? WY[(i64)skelloc[s0 + q] * ldr + j] : zero;
         wz[q] = ok ? WZ[(i64)skelloc[s0 + q] * ldr + j] : zero;
       }
+      for (int i0 = 0; i0 < nr; i0 += 8) {
+        S vy[8], vz[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (s0 + q < k) {
-          const S t = Ts[i * k + s0 + q];
-          vy = s_sub(vy, s_mul(t, wy[q]));
-          vz = s_sub(vz, s_mul(t, wz[q]));
+        for (int u = 0; u < 8; ++u) {
+          const int i = i0 + u;
+          if (i < nr) {
+            // first chunk starts from W_r, later ones from the partial sums
+            vy[u] = s0 == 0 ? WY[(i64)redloc[i] * ldr + j] : XY[(i64)i * ldr + j];
+            vz[u] = s0 == 0 ? WZ[(i64)redloc[i] * ldr + j] : XZ[(i64)i * ldr + j];
+          } else {
+            vy[u] = vz[u] = zero;
+          }
         }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = i0 + u;
+          if (i >= nr) break;
+#pragma unroll
+          for (int q = 0; q < SKC; ++q)
+            if (s0 + q < k) {
+              const S t = Ts[i * k + s0 + q];
+              vy[u] = s_sub(vy[u], s_mul(t, wy[q]));
+              vz[u] = s_sub(vz[u], s_mul(t, wz[q]));
+            }
+          XY[(i64)i * ldr + j] = vy[u];
+          XZ[(i64)i * ldr + j] = vz[u];
+        }
+      }
     }
-    XY[(i64)i * ldr + j] = vy;
-    XZ[(i64)i * ldr + j] = vz;
   }
   __syncthreads();
-  // 2. column fix X[:, red] -= X[:, skel] T^*  (F_loc^-1 on b's own columns)
+  // 2. column fix X[:, red] -= X[:, skel] T^*  (F_loc^-1 on b's own columns): a thread per row i,
+  //    X[i, skel] in registers (chunks of 16), the redundant columns 8 at a time
   if (k > 0) {
-    for (int idx = tid; idx < nr * nr; idx += 256) {
-      const int i = idx / nr, jj = idx % nr;
-      const int col = b.self_pos + redloc[jj];
-      S vy = XY[(i64)i * ldr + col];
-      S vz = XZ[(i64)i * ldr + col];
-      for (int s0 = 0; s0 < k; s0 += 8) {
-        S xy[8], xz[8];
+    for (int i = tid; i < nr; i += 256) {
+      for (int s0 = 0; s0 < k; s0 += SKC) {
+        S xy[SKC], xz[SKC];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < SKC; ++q) {
           const bool ok = s0 + q < k;
           xy[q] = ok ? XY[(i64)i * ldr + b.self_pos + skelloc[s0 + q]] : zero;
           xz[q] = ok ? XZ[(i64)i * ldr + b.self_pos + skelloc[s0 + q]] : zero;
         }
+        for (int j0 = 0; j0 < nr; j0 += 8) {
+          S vy[8], vz[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (s0 + q < k) {
-            const S t = Ts[jj * k + s0 + q];
-            vy = s_sub(vy, s_mulc(xy[q], t));
-            vz = s_sub(vz, s_mulc(xz[q], t));
+          for (int u = 0; u < 8; ++u) {
+            const int jj = j0 + u;
+            vy[u] = jj < nr ? XY[(i64)i * ldr + b.self_pos + redloc[jj]] : zero;
+            vz[u] = jj < nr ? XZ[(i64)i * ldr + b.self_pos + redloc[jj]] : zero;
           }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int jj = j0 + u;
+            if (jj >= nr) break;
+#pragma unroll
+            for (int q = 0; q < SKC; ++q)
+              if (s0 + q < k) {
+                const S t = Ts[jj * k + s0 + q];
+                vy[u] = s_sub(vy[u], s_mulc(xy[q], t));
+                vz[u] = s_sub(vz[u], s_mulc(xz[q], t));
+              }
+            XY[(i64)i * ldr + b.self_pos + redloc[jj]] = vy[u];
+            XZ[(i64)i * ldr + b.self_pos + redloc[jj]] = vz[u];
+          }
+        }
       }
-      XY[(i64)i * ldr + col] = vy;
-      XZ[(i64)i * ldr + col] = vz;
     }
   }
   __syncthreads();   // Ts (the X_rr space) is dead from here on
@@ -471,14 +501,33 @@ __global__ void __launch_bounds__(256) extract_lu_kernel(BoxDev* __restrict__ bo
   }
   S* Xrc = ws + b.off_xrc;
   S* Xcr = ws + b.off_xcr;
-  for (int idx = tid; idx < nr * nc; idx += 256) {
-    const int i = idx / nc, j = idx % nc;
-    Xrc[(i64)i * ldr + j] = XY[(i64)i * ldr + cpos[j]];
+  // gathers 4 elements per thread per round (loads first, then stores: one round trip per 4)
+  for (int idx0 = tid; idx0 < nr * nc; idx0 += 4 * 256) {
+    S v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int idx = idx0 + u * 256;
+      v[u] = idx < nr * nc ? XY[(i64)(idx / nc) * ldr + cpos[idx % nc]] : zero;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int idx = idx0 + u * 256;
+      if (idx < nr * nc) Xrc[(i64)(idx / nc) * ldr + idx % nc] = v[u];
+    }
   }
-  for (int idx = tid; idx < nr * nc; idx += 256) {
-    const int j = idx / nr, i = idx % nr;
-    // X_cr = (X_Z)^*; complex-symmetric shortcut: X_Z = conj(X_Y) (held as X_Y), X_cr = X_Y^T
-    Xcr[(i64)j * ldn + i] = sym == 2 ? XZ[(i64)i * ldr + cpos[j]] : s_conj(XZ[(i64)i * ldr + cpos[j]]);
+  for (int idx0 = tid; idx0 < nr * nc; idx0 += 4 * 256) {
+    S v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int idx = idx0 + u * 256;
+      // X_cr = (X_Z)^*; complex-symmetric shortcut: X_Z = conj(X_Y) (held as X_Y), X_cr = X_Y^T
+      v[u] = idx < nr * nc ? XZ[(i64)(idx % nr) * ldr + cpos[idx / nr]] : zero;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int idx = idx0 + u * 256;
+      if (idx < nr * nc) Xcr[(i64)(idx / nr) * ldn + idx % nr] = sym == 2 ? v[u] : s_conj(v[u]);
+    }
   }
   __syncthreads();
   if (tri) {

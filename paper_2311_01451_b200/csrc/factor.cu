@@ -86,7 +86,9 @@ int g_tm32_nt = 32, g_tm32_nn = 32;  // RSRS_TM32_NT / RSRS_TM32_NN: 32-row tile
 // tiles do (the sphere's levels: boxes of ~15-60 rows), see Planner::run
 thread_local bool t_level_tm32 = false;
 double g_tm32_ratio = 0.85;          // RSRS_TM32_RATIO: padded rows (32-row tiles) / padded rows (64) below this
-bool g_nt3 = false;                  // RSRS_NT3=1: three-stage, one-barrier NT tiles (A/B)
+bool g_nt3 = false;
+bool g_tm16 = true;                  // RSRS_TM16=0: no 16-row NT tiles on levels of small boxes
+bool g_tm16_nn = false;              // RSRS_TM16_NN=1: the same for NN (measured: no gain on c3)                  // RSRS_NT3=1: three-stage, one-barrier NT tiles (A/B)
 
 // host-side time split of one rsrs_factor (RSRS_TRACE)
 struct HostTrace {
@@ -165,6 +167,8 @@ void init_kernels() {
   g_trace = tr && tr[0] == '1';
   if (const char* sc = getenv("RSRS_SKINNY_COLS")) g_skinny_cols = std::max(128, (atoi(sc) / 128) * 128);
   if (const char* n3 = getenv("RSRS_NT3")) g_nt3 = n3[0] == '1';
+  if (const char* t16 = getenv("RSRS_TM16")) g_tm16 = t16[0] != '0';
+  if (const char* t16 = getenv("RSRS_TM16_NN")) g_tm16_nn = t16[0] == '1';
   if (const char* t = getenv("RSRS_TM32_NT")) g_tm32_nt = atoi(t);
   if (const char* t = getenv("RSRS_TM32_NN")) g_tm32_nn = atoi(t);
   if (const char* t = getenv("RSRS_TM32_RATIO")) g_tm32_ratio = atof(t);
@@ -181,6 +185,8 @@ void init_kernels() {
   set_smem(rsrs::gemm_nt_kernel_c<64>, rsrs::NT_SMEM);
   set_smem(rsrs::gemm_nn_kernel_c<64>, rsrs::NN_SMEM);
   set_smem(rsrs::gemm_nt_kernel<32>, rsrs::NT_SMEM);
+  set_smem(rsrs::gemm_nt_kernel<16>, rsrs::nt_smem(16, false));
+  set_smem(rsrs::gemm_nn_kernel<16>, rsrs::nn_smem(16, false));
   set_smem(rsrs::gemm_nn_kernel<32>, rsrs::NN_SMEM);
   set_smem(rsrs::gemm_nt_kernel_c<32>, rsrs::NT_SMEM);
   set_smem(rsrs::gemm_nn_kernel_c<32>, rsrs::NN_SMEM);
@@ -311,6 +317,17 @@ void launch_nt(bool cplx, const NTDesc* d, int n, int mmax, int nmax, cudaStream
   const int TN = cplx ? rsrs::GTC : rsrs::GT;
   const int TM = (mmax <= (cplx ? 32 : g_tm32_nt) || (!cplx && t_level_tm32)) ? 32 : 64;
   dim3 grid((nmax + TN - 1) / TN, (mmax + TM - 1) / TM, n);
+  if (!cplx && TM == 32 && g_tm16 && t_level_tm32 && !g_nt3 && nmax > 64) {
+    // levels of small boxes: 16-row tiles for the descriptors with m <= 16, 32-row tiles for the rest
+    dim3 g16((nmax + TN - 1) / TN, 1, n);
+    rsrs::gemm_nt_kernel<16><<<g16, 128, rsrs::nt_smem(16, false), s>>>(d, 0, 16);
+    post("gemm_nt16", s, launches);
+    if (mmax > 16) {
+      rsrs::gemm_nt_kernel<32><<<grid, 128, rsrs::nt_smem(32, false), s>>>(d, 16, 1 << 30);
+      post("gemm_nt", s, launches);
+    }
+    return;
+  }
   if (cplx) {
     if (TM == 32) rsrs::gemm_nt_kernel_c<32><<<grid, 128, rsrs::nt_smem(32, true), s>>>(d);
     else rsrs::gemm_nt_kernel_c<64><<<grid, 128, rsrs::nt_smem(64, true), s>>>(d);
@@ -335,6 +352,17 @@ void launch_nn(bool cplx, const NNDesc* d, int n, int mmax, int nmax, cudaStream
   const int TN = cplx ? rsrs::GTC : rsrs::GT;
   const int TM = force_tm ? force_tm : ((mmax <= (cplx ? 32 : g_tm32_nn) || (!cplx && t_level_tm32)) ? 32 : 64);
   dim3 grid((nmax + TN - 1) / TN, (mmax + TM - 1) / TM, n);
+  if (!cplx && TM == 32 && !force_tm && g_tm16_nn && t_level_tm32) {
+    // levels of small boxes: 16-row tiles for the descriptors with m <= 16
+    dim3 g16((nmax + TN - 1) / TN, 1, n);
+    rsrs::gemm_nn_kernel<16><<<g16, 128, rsrs::nn_smem(16, false), s>>>(d, 0, 16);
+    post("gemm_nn16", s, launches);
+    if (mmax > 16) {
+      rsrs::gemm_nn_kernel<32><<<grid, 128, rsrs::nn_smem(32, false), s>>>(d, 16, 1 << 30);
+      post("gemm_nn", s, launches);
+    }
+    return;
+  }
   if (cplx) {
     if (TM == 32) rsrs::gemm_nn_kernel_c<32><<<grid, 128, rsrs::nn_smem(32, true), s>>>(d);
     else rsrs::gemm_nn_kernel_c<64><<<grid, 128, rsrs::nn_smem(64, true), s>>>(d);
@@ -1288,10 +1316,10 @@ struct Planner {
               const int mbk = std::max(1, lvl_maxnb);   // largest block / T dimension (<= GB_MAX here)
               dim3 gu(nw, sides);
               if (cplx)
-                rsrs::gblk_update_kernel<true><<<gu, 128, rsrs::gblk_smem_for<true>(mbk), s>>>(dboxes, wk, gtab_b.as<rsrs::GBlk>(), pO, pP, fpool,
+                rsrs::gblk_update_kernel<true><<<gu, mbk > 32 ? 256 : 128, rsrs::gblk_smem_for<true>(mbk), s>>>(dboxes, wk, gtab_b.as<rsrs::GBlk>(), pO, pP, fpool,
                                                                    diws, mbk);
               else
-                rsrs::gblk_update_kernel<false><<<gu, 128, rsrs::gblk_smem_for<false>(mbk), s>>>(dboxes, wk, gtab_b.as<rsrs::GBlk>(), pO, pP, fpool,
+                rsrs::gblk_update_kernel<false><<<gu, mbk > 32 ? 256 : 128, rsrs::gblk_smem_for<false>(mbk), s>>>(dboxes, wk, gtab_b.as<rsrs::GBlk>(), pO, pP, fpool,
                                                                     diws, mbk);
               post("gblk_update_kernel", s, launches);
             }

@@ -159,14 +159,17 @@ RSRS_DI void nt_tile(const NTDesc& d, int m, int n, int K, int i0, int j0, doubl
   }
 }
 
+// mlo < m <= mhi: the descriptors this launch takes (a level of small boxes is split into a 16-row
+// tile launch for m <= 16 and a 32-row one for the rest)
 template <int TM, int STAGES = 2>
-__global__ void __launch_bounds__(128) gemm_nt_kernel(const NTDesc* __restrict__ descs) {
+__global__ void __launch_bounds__(128) gemm_nt_kernel(const NTDesc* __restrict__ descs, int mlo = 0,
+                                                      int mhi = 1 << 30) {
   extern __shared__ __align__(16) double smem[];
   const NTDesc& d = descs[blockIdx.z];
   const int m = dyn(d.pm, 0, d.m);
   const int n = dyn(d.pn, 0, d.n);
   const int i0 = blockIdx.y * TM, j0 = blockIdx.x * GT;
-  if (i0 >= m || j0 >= n) return;
+  if (i0 >= m || j0 >= n || m <= mlo || m > mhi) return;
   const int sym = d.psym ? *d.psym : d.sym_rows;
   if (i0 + TM <= sym && j0 >= i0 + TM) return;  // strictly upper tile of the Gram
   const NTDesc dl = d;
@@ -260,7 +263,7 @@ RSRS_DI void nn_tile(const NNDesc& d, int m, int n, int K, int i0, int j0, doubl
   // 32-row tiles: the beta * C operand of the epilogue is loaded before the K loop, so its
   // latency overlaps the GEMM instead of following it (ncu: the epilogue's dependent loads
   // held ~35% of the stall samples of the row-gathered L/U update)
-  constexpr bool PRE = (TM == 32);
+  constexpr bool PRE = (TM <= 32);
   double2 cpre[PRE ? MT : 1][4];
   if constexpr (PRE) {
 #pragma unroll
@@ -351,14 +354,15 @@ RSRS_DI void nn_tile(const NNDesc& d, int m, int n, int K, int i0, int j0, doubl
 }
 
 template <int TM>
-__global__ void __launch_bounds__(128) gemm_nn_kernel(const NNDesc* __restrict__ descs) {
+__global__ void __launch_bounds__(128) gemm_nn_kernel(const NNDesc* __restrict__ descs, int mlo = 0,
+                                                      int mhi = 1 << 30) {
   extern __shared__ __align__(16) double smem[];
   const NNDesc& d = descs[blockIdx.z];
   const int m = dyn(d.pm, 0, d.m);
   const int n = dyn(d.pn, 0, d.n);
   const int K = dyn(d.pK, 0, d.K);
   const int i0 = blockIdx.y * TM, j0 = blockIdx.x * GT;
-  if (i0 >= m || j0 >= n) return;
+  if (i0 >= m || j0 >= n || m <= mlo || m > mhi) return;
   const NNDesc dl = d;
   nn_tile<TM>(dl, m, n, K, i0, j0, smem);
 }

@@ -110,7 +110,7 @@ template <bool C> constexpr int gblk_smem() { return 2 * GB_MAX * GB_LD * (C ? 1
 // leaf blocks are <= 30 x 30, so sizing for 64 x 64 held occupancy at 3 CTAs per SM
 template <bool C> inline int gblk_smem_for(int mb) { return 2 * mb * (mb + 1) * (C ? 16 : 8) + 2 * mb * 4; }
 template <bool C>
-__global__ void __launch_bounds__(128) gblk_update_kernel(const BoxDev* __restrict__ level_boxes,
+__global__ void __launch_bounds__(256) gblk_update_kernel(const BoxDev* __restrict__ level_boxes,
                                                           const int2* __restrict__ work,
                                                           const GBlk* __restrict__ tab, double* __restrict__ poolO,
                                                           double* __restrict__ poolP, const double* __restrict__ fpoold,
@@ -129,14 +129,26 @@ __global__ void __launch_bounds__(128) gblk_update_kernel(const BoxDev* __restri
   const GBlk e = tab[w.y];
   const int tid = threadIdx.x;
   const S* T = reinterpret_cast<const S*>(fpoold) + b.f_T;
-  for (int idx = tid; idx < nr * k; idx += blockDim.x) Ts[(idx / k) * GB_LD + idx % k] = T[(i64)(idx / k) * b.ldn + idx % k];
-  for (int q = tid; q < k; q += blockDim.x) skl[q] = iws[b.off_skelrow + q] - b.row0;
-  for (int i = tid; i < nr; i += blockDim.x) red[i] = iws[b.off_redrow + i] - b.row0;
   S* B = reinterpret_cast<S*>(blockIdx.y ? poolP : poolO) + e.off;
-  for (int idx = tid; idx < e.nrow * e.ncol; idx += blockDim.x) {
-    const int r = idx / e.ncol, c = idx % e.ncol;
-    Bs[r * GB_LD + c] = B[(i64)r * e.ld + c];
+  const int nt = blockDim.x, nT = nr * k, nB = e.nrow * e.ncol;
+  // staging in rounds of 4 block + 4 T elements per thread, all loads of a round in flight together
+  for (int r0 = tid; r0 < max(nT, nB); r0 += 4 * nt) {
+    S vb[4], vt[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int idx = r0 + u * nt;
+      vb[u] = idx < nB ? B[(i64)(idx / e.ncol) * e.ld + idx % e.ncol] : s_zero(S());
+      vt[u] = idx < nT ? T[(i64)(idx / k) * b.ldn + idx % k] : s_zero(S());
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int idx = r0 + u * nt;
+      if (idx < nB) Bs[(idx / e.ncol) * GB_LD + idx % e.ncol] = vb[u];
+      if (idx < nT) Ts[(idx / k) * GB_LD + idx % k] = vt[u];
+    }
   }
+  for (int q = tid; q < k; q += nt) skl[q] = iws[b.off_skelrow + q] - b.row0;
+  for (int i = tid; i < nr; i += nt) red[i] = iws[b.off_redrow + i] - b.row0;
   __syncthreads();
   if (e.mode != 1) {   // rows: B[s, :] += T^* B[r, :]   (red and skel rows are disjoint)
     for (int idx = tid; idx < k * e.ncol; idx += blockDim.x) {
@@ -247,18 +259,34 @@ __global__ void __launch_bounds__(256) gram_assemble_kernel(const BoxDev* __rest
   for (int side = 0; side < sides; ++side) {
     const S* P = reinterpret_cast<const S*>(side ? poolP : poolO);
     S* Cb = reinterpret_cast<S*>(wsd) + b.off_aug + (side ? (i64)(b.rmax + b.nb) * ldr : 0);
-    for (int idx = tid; idx < n1 * ncols; idx += 256) {
-      const int a = idx / ncols, col = idx - a * ncols;
-      const int q2 = colq[col];
-      const GBlk& e = sE[q2];
-      S v;
-      if (e.mode != 1) {
-        v = P[e.off + (i64)act1[a] * e.ld + act[col]];
-      } else {
-        if (big1 && cnt[q2] >= 16) continue;   // tiled below
-        v = s_conj(P[e.off + (i64)act[col] * e.ld + act1[a]]);
+    // 4 elements per thread per round: the pool loads go out together, then the stores
+    for (int idx0 = tid; idx0 < n1 * ncols; idx0 += 4 * 256) {
+      S v[4];
+      bool w[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int idx = idx0 + u * 256;
+        w[u] = false;
+        v[u] = s_zero(S());
+        if (idx >= n1 * ncols) continue;
+        const int a = idx / ncols, col = idx - a * ncols;
+        const int q2 = colq[col];
+        const GBlk& e = sE[q2];
+        if (e.mode != 1) {
+          v[u] = P[e.off + (i64)act1[a] * e.ld + act[col]];
+          w[u] = true;
+        } else if (!(big1 && cnt[q2] >= 16)) {   // large transposed blocks: tiled below
+          v[u] = s_conj(P[e.off + (i64)act[col] * e.ld + act1[a]]);
+          w[u] = true;
+        }
       }
-      Cb[(i64)(p1 + a) * ldr + col] = v;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int idx = idx0 + u * 256;
+        if (!w[u]) continue;
+        const int a = idx / ncols, col = idx - a * ncols;
+        Cb[(i64)(p1 + a) * ldr + col] = v[u];
+      }
     }
     if (!big1) continue;
     // large blocks stored transposed: 32 x 32 tiles through shared memory

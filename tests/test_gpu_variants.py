@@ -30,6 +30,9 @@ VARIANTS = {
     # 32-row tiles for every real GEMM / 64-row tiles wherever allowed
     "tiles_32": {"RSRS_TM32_NT": "100000", "RSRS_TM32_NN": "100000"},
     "tiles_64": {"RSRS_TM32_RATIO": "0"},
+    # 32-row tiles without the 16-row split for small-box descriptors
+    "no_tiles_16": {"RSRS_TM16": "0"},
+    "nn_tiles_16": {"RSRS_TM16_NN": "1"},
     # solve from the factor pools (no packed records, LU top block), kernel-by-kernel launches
     "unpacked_solve": {"RSRS_SOLVE_PACKED": "0", "RSRS_SWEEP_GRAPH": "0"},
 }
