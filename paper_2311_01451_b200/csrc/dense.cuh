@@ -684,42 +684,65 @@ __global__ void __launch_bounds__(256) pull_assemble_kernel(BoxDev* __restrict__
   S* AY = reinterpret_cast<S*>(wsd) + b.off_pull;
   S* AZ = AY + (i64)nb * b.ldr;
   int* prow = iws + b.off_prow;
-  __shared__ int K0s, offs;
-  const int tid = threadIdx.x;
-  if (tid == 0) K0s = 0;
-  __syncthreads();
-  for (int q = 0; q < b.nnbr; ++q) {
-    const int idx = nd[4 * q];
-    if (idx < 0) continue;                              // not eliminated (or the box itself)
-    const BoxDev& n = level_boxes[idx];
-    const int nr = n.nr;
-    if (nr <= 0 || n.status != ST_OK) continue;
-    if (tid == 0) {                                     // first row of b in the second group of c(n)
-      const int* crow = iws + n.off_crow;
-      int lo = n.ncp, hi = n.nc;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (crow[mid] < b.row0) lo = mid + 1;
-        else hi = mid;
-      }
-      offs = lo;
+  // K offsets of the eliminated neighbours (prefix sum in neighbour order), then one warp per
+  // neighbour: warp-parallel lower bound of b's first row in c(n) (two probes of 32 lanes instead of
+  // a serial binary search) and the copy of the G_L rows / G_U columns that touch b
+  __shared__ int kofs[65], nrs[64];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int nn = b.nnbr;
+  if (tid < nn) {
+    const int idx = nd[4 * tid];
+    int nr = 0;
+    if (idx >= 0) {
+      const BoxDev& n = level_boxes[idx];
+      if (n.nr > 0 && n.status == ST_OK) nr = n.nr;
     }
-    __syncthreads();
-    const int o = offs, K0 = K0s;
+    nrs[tid] = nr;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int o = 0;
+    for (int q = 0; q < nn; ++q) {
+      kofs[q] = o;
+      o += nrs[q];
+    }
+    kofs[nn] = o;
+    b.kpull = o;
+  }
+  __syncthreads();
+  for (int q = warp; q < nn; q += nw) {
+    const int nr = nrs[q];
+    if (nr == 0) continue;
+    const BoxDev& n = level_boxes[nd[4 * q]];
+    const int* crow = iws + n.off_crow;
+    // lower bound of row0 in crow[ncp, nc) (sorted): coarse probe on a 32-point grid, then exact
+    int lo = n.ncp, hi = n.nc;
+    while (hi - lo > 32) {
+      const int step = (hi - lo + 31) / 32;
+      const int pos = lo + lane * step;
+      const bool below = pos < hi && crow[pos] < b.row0;
+      const int cnt = __popc(__ballot_sync(0xffffffffu, below));   // probes below row0 (a prefix)
+      const int nlo = cnt > 0 ? lo + (cnt - 1) * step + 1 : lo;
+      hi = min(hi, lo + cnt * step);
+      lo = nlo;
+    }
+    {
+      const int pos = lo + lane;
+      const bool below = pos < hi && crow[pos] < b.row0;
+      lo += __popc(__ballot_sync(0xffffffffu, below));
+    }
+    const int o = lo, K0 = kofs[q];
     const S* GL = fpool + n.f_GL;      // nc x nr, ld ldn(n)
     const S* GU = fpool + n.f_GU;      // nr x nc, ld ldr(n)
-    for (int idx2 = tid; idx2 < nb * nr; idx2 += 256) {
+    for (int idx2 = lane; idx2 < nb * nr; idx2 += 32) {
       const int a = idx2 / nr, i = idx2 % nr;
       AY[(i64)a * b.ldr + K0 + i] = GL[(i64)(o + a) * n.ldn + i];
       if (zside) AZ[(i64)a * b.ldr + K0 + i] = s_conj(GU[(i64)i * n.ldr + o + a]);
     }
-    for (int i = tid; i < nr; i += 256) prow[K0 + i] = iws[n.off_redrow + i];
-    __syncthreads();
-    if (tid == 0) K0s = K0 + nr;
-    __syncthreads();
+    for (int i = lane; i < nr; i += 32) prow[K0 + i] = iws[n.off_redrow + i];
   }
-  if (tid == 0) b.kpull = K0s;
 }
+
 
 // ---------------------------------------------------------------------------
 // Near-field row list of every box of a colour batch, built on the device:
