@@ -87,6 +87,7 @@ int g_tm32_nt = 32, g_tm32_nn = 32;  // RSRS_TM32_NT / RSRS_TM32_NN: 32-row tile
 thread_local bool t_level_tm32 = false;
 double g_tm32_ratio = 0.85;          // RSRS_TM32_RATIO: padded rows (32-row tiles) / padded rows (64) below this
 bool g_nt3 = false;
+int g_gram_pack = 32;                // RSRS_GRAM_PACK: rows per packed Gram-block row block on small-box levels (0: off)
 bool g_tm16 = true;                  // RSRS_TM16=0: no 16-row NT tiles on levels of small boxes
 bool g_tm16_nn = false;              // RSRS_TM16_NN=1: the same for NN (measured: no gain on c3)                  // RSRS_NT3=1: three-stage, one-barrier NT tiles (A/B)
 
@@ -168,6 +169,7 @@ void init_kernels() {
   if (const char* sc = getenv("RSRS_SKINNY_COLS")) g_skinny_cols = std::max(128, (atoi(sc) / 128) * 128);
   if (const char* n3 = getenv("RSRS_NT3")) g_nt3 = n3[0] == '1';
   if (const char* t16 = getenv("RSRS_TM16")) g_tm16 = t16[0] != '0';
+  if (const char* gp = getenv("RSRS_GRAM_PACK")) g_gram_pack = atoi(gp);
   if (const char* t16 = getenv("RSRS_TM16_NN")) g_tm16_nn = t16[0] == '1';
   if (const char* t = getenv("RSRS_TM32_NT")) g_tm32_nt = atoi(t);
   if (const char* t = getenv("RSRS_TM32_NN")) g_tm32_nn = atoi(t);
@@ -1011,20 +1013,92 @@ struct Planner {
         std::vector<int> rld(nbox, 0);
         i64 poff = 0;
         int maxnb = 0, maxcols = 0;
+        // Small-box levels: consecutive boxes (<= g_gram_pack rows together, contiguous rows) share
+        // one row block whose columns are the union of their partners j >= i, so that one 32-row
+        // DMMA tile carries 2-3 sphere leaves instead of one ~15-row box padded to 16 or 32.
+        // Box i's blocks are then rows rowin(i).. of its pack's block (ld = the pack's), and the
+        // column of partner j is j's offset in the pack's union list (device lookup).
+        const bool packing = g_gram_pack > 0 && t_level_tm32 && !cplx;
+        int npack = 0, maxprows = 0;
+        std::vector<int> pack_of, upstart, ulist, ucol, pld, prow0, prows;
+        std::vector<i64> proff, prowl_at;
+        std::vector<int> cols_box(nbox, 0);   // useful columns of box i (partners j >= i): the flop count
         for (int i = 0; i < nbox; ++i) {
           int cols = 0;
           for (int t = gpstart[i]; t < gpstart[i + 1]; ++t)
             if (plist[t] >= i) cols += nb_all[plist[t]];
-          rld[i] = (int)even(cols);
-          roff[i] = poff;
-          poff += (i64)nb_all[i] * rld[i];
-          rowl_at[i + 1] = rowl_at[i] + cols;
-          if (nb_all[i] > 0) {
-            maxnb = std::max(maxnb, nb_all[i]);
+          cols_box[i] = cols;
+        }
+        if (packing) {
+          pack_of.assign(nbox, -1);
+          std::vector<int> rowin(nbox, 0), pfirst, plast;
+          int cur = 0, last = -1;
+          for (int i = 0; i < nbox; ++i) {
+            if (nb_all[i] <= 0) continue;
+            const bool contig = last >= 0 && row0[i] == row0[last] + nb_all[last];
+            if (pfirst.empty() || !contig || cur + nb_all[i] > g_gram_pack) {
+              pfirst.push_back(i);
+              plast.push_back(i);
+              prows.push_back(0);
+              prow0.push_back(row0[i]);
+              cur = 0;
+            }
+            pack_of[i] = (int)pfirst.size() - 1;
+            rowin[i] = cur;
+            cur += nb_all[i];
+            prows.back() = cur;
+            plast.back() = i;
+            last = i;
+          }
+          npack = (int)pfirst.size();
+          upstart.assign(npack + 1, 0);
+          proff.assign(npack, 0);
+          prowl_at.assign(npack + 1, 0);
+          pld.assign(npack, 0);
+          std::vector<int> tmp;
+          for (int P = 0; P < npack; ++P) {
+            tmp.clear();
+            for (int i = pfirst[P]; i <= plast[P]; ++i) {
+              if (pack_of[i] != P) continue;
+              for (int t = gpstart[i]; t < gpstart[i + 1]; ++t)
+                if (plist[t] >= i) tmp.push_back(plist[t]);
+            }
+            std::sort(tmp.begin(), tmp.end());
+            tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+            int cols = 0;
+            for (int j : tmp) {
+              ulist.push_back(j);
+              ucol.push_back(cols);
+              cols += nb_all[j];
+            }
+            upstart[P + 1] = (int)ulist.size();
+            pld[P] = (int)even(cols);
+            proff[P] = poff;
+            poff += (i64)prows[P] * pld[P];
+            prowl_at[P + 1] = prowl_at[P] + cols;
             maxcols = std::max(maxcols, cols);
+            maxprows = std::max(maxprows, prows[P]);
+          }
+          for (int i = 0; i < nbox; ++i) {
+            if (pack_of[i] < 0) continue;
+            roff[i] = proff[pack_of[i]] + (i64)rowin[i] * pld[pack_of[i]];
+            rld[i] = pld[pack_of[i]];
+            maxnb = std::max(maxnb, nb_all[i]);
+          }
+        } else {
+          for (int i = 0; i < nbox; ++i) {
+            const int cols = cols_box[i];
+            rld[i] = (int)even(cols);
+            roff[i] = poff;
+            poff += (i64)nb_all[i] * rld[i];
+            rowl_at[i + 1] = rowl_at[i] + cols;
+            if (nb_all[i] > 0) {
+              maxnb = std::max(maxnb, nb_all[i]);
+              maxcols = std::max(maxcols, cols);
+            }
           }
         }
-        const int64_t nrowl = rowl_at[nbox];
+        const int64_t nrowl = packing ? prowl_at[npack] : rowl_at[nbox];
         gpool_side = poff;
         gpool_buf.alloc((size_t)sS * std::max<i64>(2, sides * poff), s);
         double* poolO = gpool_buf.as<double>();
@@ -1034,9 +1108,13 @@ struct Planner {
         for (size_t bi2 = 0; bi2 < binfo.size(); ++bi2) gwork_off[bi2] = wpre[binfo[bi2].first];
         gwork_off[binfo.size()] = wpre[hb.size()];
         // one upload of the per-box arrays: gpstart | plist | nb | row0 | rld  (int), roff | rowl_at | wpre (i64)
-        const size_t ni = (size_t)(nbox + 1) + plist.size() + 3 * (size_t)nbox;
-        const size_t nl = (size_t)nbox + (size_t)(nbox + 1) + hb.size() + 1;
+        // (+ packing: pack_of | upstart | ulist | ucol | prows | prow0 | pld (int), proff | prowl_at (i64))
+        const size_t nip = packing ? (size_t)nbox + (npack + 1) + 2 * ulist.size() + 3 * (size_t)npack : 0;
+        const size_t ni = (size_t)(nbox + 1) + plist.size() + 3 * (size_t)nbox + nip;
+        const size_t nlp = packing ? (size_t)npack + (npack + 1) : 0;
+        const size_t nl = (size_t)nbox + (size_t)(nbox + 1) + hb.size() + 1 + nlp;
         std::vector<int64_t> up((ni + 1) / 2 + nl);
+        size_t o_pk = 0;
         {
           int* ip = reinterpret_cast<int*>(up.data());
           size_t o = 0;
@@ -1044,11 +1122,26 @@ struct Planner {
           std::copy(plist.begin(), plist.end(), ip + o);     o += plist.size();
           std::copy(nb_all.begin(), nb_all.begin() + nbox, ip + o); o += nbox;
           std::copy(row0.begin(), row0.begin() + nbox, ip + o);     o += nbox;
-          std::copy(rld.begin(), rld.end(), ip + o);
+          std::copy(rld.begin(), rld.end(), ip + o);                o += nbox;
+          o_pk = o;
+          if (packing) {
+            std::copy(pack_of.begin(), pack_of.end(), ip + o); o += nbox;
+            std::copy(upstart.begin(), upstart.end(), ip + o); o += npack + 1;
+            std::copy(ulist.begin(), ulist.end(), ip + o);     o += ulist.size();
+            std::copy(ucol.begin(), ucol.end(), ip + o);       o += ucol.size();
+            std::copy(prows.begin(), prows.end(), ip + o);     o += npack;
+            std::copy(prow0.begin(), prow0.end(), ip + o);     o += npack;
+            std::copy(pld.begin(), pld.end(), ip + o);         o += npack;
+          }
           int64_t* lp = up.data() + (ni + 1) / 2;
           std::copy(roff.begin(), roff.end(), lp);
           std::copy(rowl_at.begin(), rowl_at.end(), lp + nbox);
           std::copy(wpre.begin(), wpre.end(), lp + 2 * nbox + 1);
+          if (packing) {
+            int64_t* lq = lp + 2 * nbox + 1 + hb.size() + 1;
+            std::copy(proff.begin(), proff.end(), lq);
+            std::copy(prowl_at.begin(), prowl_at.end(), lq + npack);
+          }
         }
         gup_b.alloc(sizeof(int64_t) * up.size(), s);
         CK(cudaMemcpyAsync(gup_b.p, up.data(), sizeof(int64_t) * up.size(), cudaMemcpyHostToDevice, s));
@@ -1063,10 +1156,31 @@ struct Planner {
         growl_b.alloc(sizeof(int) * std::max<int64_t>(nrowl, 1), s);
         gtab_b.alloc(sizeof(rsrs::GBlk) * std::max<size_t>(plist.size(), 1), s);
         gwork_b.alloc(sizeof(int2) * std::max<int64_t>(wpre[hb.size()], 1), s);
+        const int* d_packof = d_gps + o_pk;
+        const int* d_upstart = d_packof + nbox;
+        const int* d_ulist = d_upstart + npack + 1;
+        const int* d_ucol = d_ulist + ulist.size();
+        const int* d_prows = d_ucol + ucol.size();
+        const int* d_prow0 = d_prows + npack;
+        const int* d_pld = d_prow0 + npack;
+        const i64* d_proff = d_wpre + hb.size() + 1;
+        const i64* d_prowlat = d_proff + npack;
         if (nbox > 0) {
-          rsrs::gblk_tables_kernel<<<(nbox + 7) / 8, 256, 0, s>>>(nbox, d_gps, d_pl, d_nb, d_row0, d_roff, d_rld, d_rowlat,
-                                                                  gtab_b.as<rsrs::GBlk>(), growl_b.as<int>());
-          post("gblk_tables", s, launches);
+          if (packing) {
+            rsrs::gblk_tables_packed_kernel<<<(nbox + 7) / 8, 256, 0, s>>>(nbox, d_gps, d_pl, d_nb, d_roff, d_rld, d_packof,
+                                                                           d_upstart, d_ulist, d_ucol,
+                                                                           gtab_b.as<rsrs::GBlk>());
+            post("gblk_tables_packed", s, launches);
+            if (npack > 0) {
+              rsrs::pack_rowl_kernel<<<(npack + 7) / 8, 256, 0, s>>>(npack, d_upstart, d_ulist, d_ucol, d_nb, d_row0,
+                                                                     d_prowlat, growl_b.as<int>());
+              post("pack_rowl", s, launches);
+            }
+          } else {
+            rsrs::gblk_tables_kernel<<<(nbox + 7) / 8, 256, 0, s>>>(nbox, d_gps, d_pl, d_nb, d_row0, d_roff, d_rld, d_rowlat,
+                                                                    gtab_b.as<rsrs::GBlk>(), growl_b.as<int>());
+            post("gblk_tables", s, launches);
+          }
         }
         if (!hb.empty()) {
           rsrs::gblk_work_kernel<<<((int)hb.size() + 7) / 8, 256, 0, s>>>((int)hb.size(), dboxes, d_gps, d_wpre,
@@ -1074,22 +1188,28 @@ struct Planner {
           post("gblk_work", s, launches);
         }
         gps_b_ptr = d_gps;
-        // the precompute GEMM descriptors (one row block per box and side) are expanded on the
-        // device from the per-box arrays already uploaded (no host loop / 100+ B per box upload)
+        // the precompute GEMM descriptors (one row block per box -- or per pack -- and side) are
+        // expanded on the device from the arrays already uploaded (no host loop / per-box upload)
         double fl = 0, rows = 0;
         for (int i = 0; i < nbox; ++i) {
           if (nb_all[i] <= 0) continue;
-          fl += 2.0 * sides * nb_all[i] * (double)(rowl_at[i + 1] - rowl_at[i]) * p;
+          fl += 2.0 * sides * nb_all[i] * (double)cols_box[i] * p;   // useful work (union padding not counted)
           rows += nb_all[i];
         }
-        pre_b.alloc(sizeof(NTDesc) * std::max<size_t>((size_t)sides * nbox, 1), s);
-        if (nbox > 0 && fl > 0) {
-          rsrs::pre_desc_kernel<<<(sides * nbox + 255) / 256, 256, 0, s>>>(nbox, sides, d_nb, d_row0, d_roff, d_rld, d_rowlat,
-                                                                           Om, Ps, ld, growl_b.as<int>(), poolO, poff, p, SC,
-                                                                           pre_b.as<NTDesc>());
+        const int nunit = packing ? npack : nbox;
+        pre_b.alloc(sizeof(NTDesc) * std::max<size_t>((size_t)sides * nunit, 1), s);
+        if (nunit > 0 && fl > 0) {
+          if (packing)
+            rsrs::pre_desc_kernel<<<(sides * npack + 255) / 256, 256, 0, s>>>(npack, sides, d_prows, d_prow0, d_proff, d_pld,
+                                                                              d_prowlat, Om, Ps, ld, growl_b.as<int>(), poolO,
+                                                                              poff, p, SC, pre_b.as<NTDesc>());
+          else
+            rsrs::pre_desc_kernel<<<(sides * nbox + 255) / 256, 256, 0, s>>>(nbox, sides, d_nb, d_row0, d_roff, d_rld, d_rowlat,
+                                                                             Om, Ps, ld, growl_b.as<int>(), poolO, poff, p, SC,
+                                                                             pre_b.as<NTDesc>());
           post("pre_desc_kernel", s, launches);
           tic(KC_GRAM);
-          launch_nt(cplx, pre_b.as<NTDesc>(), sides * nbox, maxnb, maxcols, s, launches);
+          launch_nt(cplx, pre_b.as<NTDesc>(), sides * nunit, packing ? maxprows : maxnb, maxcols, s, launches);
           toc();
           account(KC_GRAM, (cplx ? 4.0 : 1.0) * fl, (double)sS * (sides * rows * p + sides * poff));
         }

@@ -87,6 +87,65 @@ __global__ void __launch_bounds__(256) gblk_tables_kernel(int nbox, const int* _
   }
 }
 
+// Partner table of a level whose row blocks are shared by packs of consecutive boxes (small-box
+// levels, factor.cu): box i's rows sit at roff[i] (ld rld[i]) inside its pack's block, and the
+// column of partner j is j's offset in the pack's sorted union list (binary search).
+RSRS_DI int pack_col(const int* __restrict__ upstart, const int* __restrict__ ulist, const int* __restrict__ ucol,
+                     int P, int j) {
+  int lo = upstart[P], hi = upstart[P + 1] - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (ulist[mid] < j) lo = mid + 1;
+    else hi = mid;
+  }
+  return ucol[lo];   // j is in the list by construction
+}
+__global__ void __launch_bounds__(256) gblk_tables_packed_kernel(int nbox, const int* __restrict__ gpstart,
+                                                                 const int* __restrict__ plist, const int* __restrict__ nb,
+                                                                 const i64* __restrict__ roff, const int* __restrict__ rld,
+                                                                 const int* __restrict__ pack_of,
+                                                                 const int* __restrict__ upstart,
+                                                                 const int* __restrict__ ulist,
+                                                                 const int* __restrict__ ucol, GBlk* __restrict__ tab) {
+  const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= nbox) return;
+  for (int t = gpstart[i] + lane; t < gpstart[i + 1]; t += 32) {
+    const int j = plist[t];
+    GBlk e;
+    e.j = j;
+    e.pad = 0;
+    if (j >= i) {
+      e.mode = j == i ? 2 : 0;
+      e.off = roff[i] + pack_col(upstart, ulist, ucol, pack_of[i], j);
+      e.ld = rld[i];
+      e.nrow = nb[i];
+      e.ncol = nb[j];
+    } else {
+      e.mode = 1;
+      e.off = roff[j] + pack_col(upstart, ulist, ucol, pack_of[j], i);
+      e.ld = rld[j];
+      e.nrow = nb[j];
+      e.ncol = nb[i];
+    }
+    tab[t] = e;
+  }
+}
+// B-row lists of the packed precompute GEMMs: pack P's union columns in order
+__global__ void __launch_bounds__(256) pack_rowl_kernel(int npack, const int* __restrict__ upstart,
+                                                        const int* __restrict__ ulist, const int* __restrict__ ucol,
+                                                        const int* __restrict__ nb, const int* __restrict__ row0,
+                                                        const i64* __restrict__ prowl_at, int* __restrict__ rowl) {
+  const int P = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (P >= npack) return;
+  for (int u = upstart[P]; u < upstart[P + 1]; ++u) {
+    const int j = ulist[u];
+    int* rl = rowl + prowl_at[P] + ucol[u];
+    for (int r = lane; r < nb[j]; r += 32) rl[r] = row0[j] + r;
+  }
+}
+
 // (box, block) work items of the block update: my box q (level order) -> its partner entries.
 __global__ void __launch_bounds__(256) gblk_work_kernel(int nq, const BoxDev* __restrict__ level_boxes,
                                                         const int* __restrict__ gpstart,

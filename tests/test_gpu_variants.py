@@ -33,6 +33,8 @@ VARIANTS = {
     # 32-row tiles without the 16-row split for small-box descriptors
     "no_tiles_16": {"RSRS_TM16": "0"},
     "nn_tiles_16": {"RSRS_TM16_NN": "1"},
+    # one Gram-block row block per box on the small-box levels (no packing of consecutive boxes)
+    "no_gram_pack": {"RSRS_GRAM_PACK": "0"},
     # solve from the factor pools (no packed records, LU top block), kernel-by-kernel launches
     "unpacked_solve": {"RSRS_SOLVE_PACKED": "0", "RSRS_SWEEP_GRAPH": "0"},
 }
