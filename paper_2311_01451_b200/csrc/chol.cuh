@@ -357,6 +357,194 @@ RSRS_DI bool chol_diag_block128(const CholDesc& cd, int j0, int r, double* smem)
   return true;
 }
 
+// ---------------------------------------------------------------------------
+// Two-level diagonal block (real, 128 threads).  The 64 x 64 block A_JJ is factored
+// in 16 x 16 sub-blocks (right-looking): each diagonal sub-block is eliminated by ONE
+// warp, warp-synchronously (lane j owns column j of the augmented [A_kk | I]; 16
+// shuffle steps, no CTA barrier), giving L_kk and X_k = L_kk^-1 in the same sweep as
+// chol_diag_kernel (Gaussian elimination without pivoting: A = Lt D Lt^T, the I part
+// becomes Lt^-1, L = Lt D^1/2, L^-1 = D^-1/2 Lt^-1).  The sub-panel L_ik = A_ik X_k^T,
+// the trailing update A_ij -= L_ik L_jk^T and the block inverse
+// (L^-1)_ik = -X_i sum_{k<=m<i} L_im (L^-1)_mk run on all 128 threads from shared
+// memory: about 20 CTA barriers per 64 columns instead of 64 column steps.
+// Shared memory: S [64][65] (lower: A -> L; strictly upper blocks (k, i), k < i:
+// (L^-1)_ik^T), X [4][16][17], T [3][16][17].  Same outputs as chol_diag_kernel
+// (L in the lower triangle of A_JJ, L_JJ^-1 zero padded beyond jb in linv[J]).
+constexpr int D16_LD = CB + 1;
+constexpr int D16_XS = 16 * 17;
+constexpr int D16_SMEM = (CB * D16_LD + 7 * D16_XS) * 8 + 16;
+
+// warp: 16 x 16 diagonal sub-block k of S -> L_kk (lower, in S), X_k (to X); false on a
+// non-positive pivot (uniform over the warp)
+RSRS_DI bool chol16_warp(double* S, int k, double* X) {
+  const int lane = threadIdx.x & 31;
+  const int o = 16 * k;
+  double a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    if (lane < 16) a[i] = (i >= lane) ? S[(o + i) * D16_LD + o + lane] : S[(o + lane) * D16_LD + o + i];
+    else a[i] = (i == lane - 16) ? 1.0 : 0.0;
+  }
+  double rs[16];
+  double myrs = 1.0;
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    // the multipliers a[i][c] (lane c) are final before step c: issue their shuffles first
+    double m[16];
+#pragma unroll
+    for (int i = c + 1; i < 16; ++i) m[i] = __shfl_sync(0xffffffffu, a[i], c);
+    const double p = __shfl_sync(0xffffffffu, a[c], c);
+    ok = ok && (p > 0.0);
+    const double rp = 1.0 / p;
+    rs[c] = rsqrt(p);
+    if (lane == c) myrs = rs[c];
+    // lane c keeps its column (= L[:, c] sqrt(d_c) for rows >= c); lanes < c hold a zero in row c
+    const double rowc = (lane == c) ? 0.0 : a[c] * rp;
+#pragma unroll
+    for (int i = c + 1; i < 16; ++i) a[i] -= m[i] * rowc;
+  }
+  if (!ok) return false;
+  if (lane < 16) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (i >= lane) S[(o + i) * D16_LD + o + lane] = a[i] * myrs;
+  } else {
+    const int jj = lane - 16;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) X[i * 17 + jj] = a[i] * rs[i];   // zero above the diagonal
+  }
+  return true;
+}
+
+// false on a non-positive pivot (every thread)
+RSRS_DI bool chol_diag16(const CholDesc& cd, int j0, int r, double* smem) {
+  double* S = smem;
+  double* Xb = S + CB * D16_LD;
+  double* Tb = Xb + 4 * D16_XS;
+  int& sbad = *reinterpret_cast<int*>(Tb + 3 * D16_XS);
+  const int jb = min(CB, r - j0);
+  const int nkb = (jb + 15) >> 4;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  double* A = cd.A + (i64)j0 * cd.lda + j0;
+  for (int idx = tid; idx < CB * CB; idx += 128) {
+    const int i = idx >> 6, j = idx & 63;
+    if (j <= i && i < 16 * nkb) S[i * D16_LD + j] = (i < jb && j < jb) ? A[(i64)i * cd.lda + j] : (i == j ? 1.0 : 0.0);
+  }
+  if (tid == 0) sbad = 0;
+  __syncthreads();
+  for (int k = 0; k < nkb; ++k) {
+    if (warp == 0 && !chol16_warp(S, k, Xb + k * D16_XS) && (tid & 31) == 0) sbad = 1;
+    __syncthreads();
+    if (sbad) return false;
+    const int nb = nkb - 1 - k;
+    if (nb <= 0) break;
+    // L_ik = A_ik X_k^T (k < i < nkb), in place through registers
+    {
+      const double* Xk = Xb + k * D16_XS;
+      double v[6];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const int idx = tid + 128 * q;
+        v[q] = 0.0;
+        if (idx < nb * 256) {
+          const int ib = k + 1 + (idx >> 8), rr = (idx >> 4) & 15, cc = idx & 15;
+          const double* srow = S + (16 * ib + rr) * D16_LD + 16 * k;
+          double s = 0.0;
+#pragma unroll
+          for (int mm = 0; mm < 16; ++mm) s += (mm <= cc) ? srow[mm] * Xk[cc * 17 + mm] : 0.0;
+          v[q] = s;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const int idx = tid + 128 * q;
+        if (idx < nb * 256) {
+          const int ib = k + 1 + (idx >> 8), rr = (idx >> 4) & 15, cc = idx & 15;
+          S[(16 * ib + rr) * D16_LD + 16 * k + cc] = v[q];
+        }
+      }
+      __syncthreads();
+    }
+    // trailing A_ij -= L_ik L_jk^T, k < j <= i < nkb (lower triangle of the diagonal blocks)
+    {
+      const int npair = nb * (nb + 1) / 2;
+      for (int idx = tid; idx < npair * 256; idx += 128) {
+        int pi = idx >> 8, ib = k + 1, jbk = k + 1;
+        // pair pi -> (ib, jbk) in the order (k+1,k+1), (k+2,k+1), (k+2,k+2), ...
+        for (int t = 1; t <= nb; ++t) {
+          if (pi < t) { ib = k + t; jbk = k + 1 + pi; break; }
+          pi -= t;
+        }
+        const int rr = (idx >> 4) & 15, cc = idx & 15;
+        if (ib == jbk && cc > rr) continue;
+        const double* li = S + (16 * ib + rr) * D16_LD + 16 * k;
+        const double* lj = S + (16 * jbk + cc) * D16_LD + 16 * k;
+        double s = 0.0;
+#pragma unroll
+        for (int mm = 0; mm < 16; ++mm) s += li[mm] * lj[mm];
+        S[(16 * ib + rr) * D16_LD + 16 * jbk + cc] -= s;
+      }
+      __syncthreads();
+    }
+  }
+  // block rows of L^-1: T_k = sum_{m=k}^{i-1} L_im (L^-1)_mk, then (L^-1)_ik = -X_i T_k
+  for (int i = 1; i < nkb; ++i) {
+    for (int idx = tid; idx < i * 256; idx += 128) {
+      const int k = idx >> 8, rr = (idx >> 4) & 15, cc = idx & 15;
+      double s = 0.0;
+      for (int m = k; m < i; ++m) {
+        const double* lim = S + (16 * i + rr) * D16_LD + 16 * m;
+        if (m == k) {
+          const double* xk = Xb + k * D16_XS;
+#pragma unroll
+          for (int q = 0; q < 16; ++q) s += lim[q] * xk[q * 17 + cc];
+        } else {
+          const double* lmk = S + (16 * k + cc) * D16_LD + 16 * m;   // (L^-1)_mk[q][cc] at S[16k+cc][16m+q]
+#pragma unroll
+          for (int q = 0; q < 16; ++q) s += lim[q] * lmk[q];
+        }
+      }
+      Tb[k * D16_XS + rr * 17 + cc] = s;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < i * 256; idx += 128) {
+      const int k = idx >> 8, rr = (idx >> 4) & 15, cc = idx & 15;
+      const double* xi = Xb + i * D16_XS + rr * 17;
+      const double* tk = Tb + k * D16_XS;
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) s += (q <= rr) ? xi[q] * tk[q * 17 + cc] : 0.0;
+      S[(16 * k + cc) * D16_LD + 16 * i + rr] = -s;
+    }
+    __syncthreads();
+  }
+  // L (lower triangle of A_JJ) and L_JJ^-1 (zero padded) to global memory
+  double* linv = cd.linv + (i64)(j0 / CB) * CB * CB;
+  for (int idx = tid; idx < CB * CB; idx += 128) {
+    const int i = idx >> 6, j = idx & 63;
+    const int bi = i >> 4, bj = j >> 4;
+    double li = 0.0;
+    if (i < jb && j < jb && j <= i) {
+      A[(i64)i * cd.lda + j] = S[i * D16_LD + j];
+      li = (bi == bj) ? Xb[bi * D16_XS + (i & 15) * 17 + (j & 15)] : S[j * D16_LD + i];
+    }
+    linv[idx] = li;
+  }
+  return true;
+}
+
+// standalone diagonal step of the per-panel chain (real): one 128-thread CTA per matrix
+__global__ void __launch_bounds__(128) chol_diag16_kernel(const CholDesc* __restrict__ cds, int j0) {
+  extern __shared__ __align__(16) double smem[];
+  const CholDesc& cd = cds[blockIdx.x];
+  if (cd.status && *cd.status != ST_OK) return;
+  const int r = *cd.pr;
+  if (j0 >= r) return;
+  if (!chol_diag16(cd, j0, r, smem) && threadIdx.x == 0 && cd.status) *cd.status = ST_SINGULAR_GRAM;
+}
+
 // tiles of an NT product over m rows (row tile 32 when m <= 32)
 RSRS_DI void nt_rows(const NTDesc& d, int m, int n, int K, double* smem) {
   if (m <= 32) {
@@ -373,7 +561,7 @@ RSRS_DI void nn_rows(const NNDesc& d, int m, int n, int K, double* smem) {
   }
 }
 
-__global__ void __launch_bounds__(128, 3) chol_fused_kernel(const CholDesc* __restrict__ cds) {
+__global__ void __launch_bounds__(128, 3) chol_fused_kernel(const CholDesc* __restrict__ cds, int d16) {
   extern __shared__ __align__(16) double smem[];
   const CholDesc& cd = cds[blockIdx.x];
   if (cd.status && *cd.status != ST_OK) return;
@@ -396,7 +584,7 @@ __global__ void __launch_bounds__(128, 3) chol_fused_kernel(const CholDesc* __re
       }
       __syncthreads();
     }
-    if (!chol_diag_block128(cd, j0, r, smem)) {
+    if (!(d16 ? chol_diag16(cd, j0, r, smem) : chol_diag_block128(cd, j0, r, smem))) {
       if (threadIdx.x == 0 && cd.status) *cd.status = ST_SINGULAR_GRAM;
       return;
     }

@@ -80,6 +80,8 @@ int g_chol_fuse_rmax = 320;          // RSRS_CHOL_FUSE_RMAX: largest real near f
 int g_back_fuse_rmax = 1 << 30;      // RSRS_BACK_FUSE_RMAX: the same for the fused back substitution
 int g_fuse_min_batch = 128;          // RSRS_FUSE_MIN_BATCH: fewest matrices of a launch for the fused kernels
 int g_skinny_cols = rsrs::SK_COLS;   // RSRS_SKINNY_COLS: columns per CTA of the skinny E/F kernel
+int g_diag16 = 0;                    // RSRS_DIAG16=1: two-level 16 x 16 warp sub-block diagonal (measured slower)
+int g_skinny_fixed = 0;              // RSRS_SKINNY_FIXED=1: 64 x 64 opA shared memory on every launch (A/B)
 int g_tm32_nt = 32, g_tm32_nn = 32;  // RSRS_TM32_NT / RSRS_TM32_NN: 32-row tiles when every row count <= this
 // 32-row tiles for every real GEMM of the current level (set per level by the planner, per host
 // thread: emulated ranks run concurrently) when they pad the level's box rows much less than 64-row
@@ -166,6 +168,8 @@ void init_kernels() {
   if (const char* sp = getenv("RSRS_SOLVE_PACKED")) g_solve_packed = sp[0] != '0';
   const char* tr = getenv("RSRS_TRACE");
   g_trace = tr && tr[0] == '1';
+  if (const char* sf = getenv("RSRS_SKINNY_FIXED")) g_skinny_fixed = atoi(sf);
+  if (const char* dg = getenv("RSRS_DIAG16")) g_diag16 = atoi(dg);
   if (const char* sc = getenv("RSRS_SKINNY_COLS")) g_skinny_cols = std::max(128, (atoi(sc) / 128) * 128);
   if (const char* n3 = getenv("RSRS_NT3")) g_nt3 = n3[0] == '1';
   if (const char* t16 = getenv("RSRS_TM16")) g_tm16 = t16[0] != '0';
@@ -193,6 +197,7 @@ void init_kernels() {
   set_smem(rsrs::gemm_nt_kernel_c<32>, rsrs::NT_SMEM);
   set_smem(rsrs::gemm_nn_kernel_c<32>, rsrs::NN_SMEM);
   set_smem(rsrs::chol_fused_kernel, rsrs::NT_SMEM);
+  set_smem(rsrs::chol_diag16_kernel, rsrs::D16_SMEM);
   set_smem(rsrs::chol_back_fused_kernel, rsrs::NT_SMEM);
   set_smem_both<false>();
   set_smem_both<true>();
@@ -276,8 +281,13 @@ void launch_chol_blocked(const CholDesc* d, int nmat, int rmax, int mext, cudaSt
       rsrs::chol_update_kernel<C><<<g, 128, rsrs::NT_SMEM, s>>>(d, j0);
       post("chol_update", s, launches);
     }
-    rsrs::chol_diag_kernel<C><<<nmat, 256, 0, s>>>(d, j0);
-    post("chol_diag", s, launches);
+    if (!C && g_diag16) {
+      rsrs::chol_diag16_kernel<<<nmat, 128, rsrs::D16_SMEM, s>>>(d, j0);
+      post("chol_diag16", s, launches);
+    } else {
+      rsrs::chol_diag_kernel<C><<<nmat, 256, 0, s>>>(d, j0);
+      post("chol_diag", s, launches);
+    }
     dim3 g(gx, std::max((rmax - j0 - CB + 63) / 64, gext), 2 * nmat);
     rsrs::chol_trsm_kernel<C><<<g, 128, rsrs::NT_SMEM, s>>>(d, j0);
     post("chol_trsm", s, launches);
@@ -376,12 +386,16 @@ void launch_nn(bool cplx, const NNDesc* d, int n, int mmax, int nmax, cudaStream
 }
 
 // in-place skinny updates (E/F), see gemm.cuh
-void launch_skinny(bool cplx, const NNDesc* d, int n, int ncols, cudaStream_t s, int64_t& launches) {
+// shared memory sized by the batch's largest box (mk >= m, K): the sphere's <= 30-point leaves
+// take ~8 KB instead of the 32 KB of a 64 x 64 opA, so more CTAs (bytes in flight) per SM
+void launch_skinny(bool cplx, const NNDesc* d, int n, int ncols, int mk, cudaStream_t s, int64_t& launches) {
   if (n <= 0 || ncols <= 0) return;
   const int cols = g_skinny_cols;
   dim3 grid(n, (ncols + cols - 1) / cols);
-  if (cplx) rsrs::skinny_nn_kernel<true><<<grid, 128, rsrs::skinny_smem<true>(), s>>>(d, cols);
-  else rsrs::skinny_nn_kernel<false><<<grid, 128, rsrs::skinny_smem<false>(), s>>>(d, cols);
+  const int acap = g_skinny_fixed ? rsrs::SK_MAX * rsrs::SK_MAX : rsrs::skinny_acap(std::min(std::max(mk, 1), rsrs::SK_MAX));
+  const size_t sm = (size_t)acap * (cplx ? 16 : 8) + 2 * rsrs::SK_MAX * 4;
+  if (cplx) rsrs::skinny_nn_kernel<true><<<grid, 128, sm, s>>>(d, cols, acap);
+  else rsrs::skinny_nn_kernel<false><<<grid, 128, sm, s>>>(d, cols, acap);
   post("skinny_nn", s, launches);
 }
 
@@ -391,7 +405,7 @@ void launch_chol_any(bool cplx, const CholDesc* d, int nmat, int rmax, int mext,
   // the tile-parallel per-panel launches)
   if (!cplx && rmax <= g_chol_fuse_rmax && nmat >= g_fuse_min_batch) {
     {
-      rsrs::chol_fused_kernel<<<nmat, 128, rsrs::NT_SMEM, s>>>(d);
+      rsrs::chol_fused_kernel<<<nmat, 128, rsrs::NT_SMEM, s>>>(d, g_diag16);
       post("chol_fused", s, l);
     }
     return;
@@ -1424,7 +1438,7 @@ struct Planner {
             toc();
           }
           tic(KC_EF);
-          if (bi.max_nb <= rsrs::SK_MAX) launch_skinny(cplx, Def + 2 * ns * q0, 2 * ns * n, p, s, launches);
+          if (bi.max_nb <= rsrs::SK_MAX) launch_skinny(cplx, Def + 2 * ns * q0, 2 * ns * n, p, bi.max_nb, s, launches);
           else launch_nn(cplx, Def + 2 * ns * q0, 2 * ns * n, bi.max_nb, p, s, launches);
           if (use_blocks) {      // keep the Gram blocks equal to F Omega Omega^* F^* (the E/F on Omega_s)
             const size_t bi_idx = &bi - &binfo[0];

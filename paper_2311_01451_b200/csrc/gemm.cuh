@@ -675,8 +675,11 @@ template <bool C> constexpr int tile_n() { return C ? GTC : GT; }
 constexpr int SK_MAX = 64;
 constexpr int SK_COLS = 128;   // default columns per CTA (RSRS_SKINNY_COLS overrides; multiple of 128)
 template <bool C> constexpr int skinny_smem() { return SK_MAX * SK_MAX * (C ? 16 : 8) + 2 * SK_MAX * 4; }
+// opA capacity (scalars) for a launch whose m, K <= mk: K rows of mp = round_up(m, 16)
+constexpr int skinny_acap(int mk) { return mk * ((mk + 15) & ~15); }
 template <bool C>
-__global__ void __launch_bounds__(128) skinny_nn_kernel(const NNDesc* __restrict__ descs, int cols) {
+__global__ void __launch_bounds__(128) skinny_nn_kernel(const NNDesc* __restrict__ descs, int cols,
+                                                        int acap = SK_MAX * SK_MAX) {
   typedef typename ScalarOf<C>::T S;
   extern __shared__ __align__(16) double ssm[];
   S* As = reinterpret_cast<S*>(ssm);
@@ -686,7 +689,7 @@ __global__ void __launch_bounds__(128) skinny_nn_kernel(const NNDesc* __restrict
   const int mp = (m + 15) & ~15;
   const S* A = reinterpret_cast<const S*>(d.A);
   const S zero = s_zero(S());
-  int* rB = reinterpret_cast<int*>(As + SK_MAX * SK_MAX);   // gathered row indices, staged once
+  int* rB = reinterpret_cast<int*>(As + acap);   // gathered row indices, staged once
   int* rD = rB + SK_MAX;
   for (int t = threadIdx.x; t < K; t += 128) rB[t] = d.rowB ? d.rowB[t] : t;
   for (int i = threadIdx.x; i < m; i += 128) rD[i] = d.rowD ? d.rowD[i] : i;

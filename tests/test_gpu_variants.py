@@ -35,6 +35,8 @@ VARIANTS = {
     "nn_tiles_16": {"RSRS_TM16_NN": "1"},
     # one Gram-block row block per box on the small-box levels (no packing of consecutive boxes)
     "no_gram_pack": {"RSRS_GRAM_PACK": "0"},
+    # two-level Cholesky diagonal blocks (16 x 16 warp sub-blocks; off by default: slower on c3)
+    "diag_two_level": {"RSRS_DIAG16": "1"},
     # solve from the factor pools (no packed records, LU top block), kernel-by-kernel launches
     "unpacked_solve": {"RSRS_SOLVE_PACKED": "0", "RSRS_SWEEP_GRAPH": "0"},
 }
