@@ -1014,6 +1014,81 @@ __global__ void merge_finalize_kernel(int64_t N, double* __restrict__ x, i64 ldx
   }
 }
 
+// Compact multi-GPU solve merge (factor.cu Merger): the rows a colour batch touches on this rank, in
+// box order (the box's redundant rows, then its c rows (which 0) or skeleton rows (which 1)), the
+// same rows mark_rows_kernel marks.  Same-colour near sets are disjoint, so the lists of the ranks
+// are disjoint and their concatenation (rank order) is the batch's merge list.
+__global__ void merge_count_kernel(const BoxDev* __restrict__ boxes, int nbox, int* __restrict__ cnt) {
+  int c0 = 0, c1 = 0;
+  for (int i = threadIdx.x; i < nbox; i += blockDim.x) {
+    const BoxDev& b = boxes[i];
+    if (b.nr <= 0) continue;
+    c0 += b.nr + b.nc;
+    c1 += b.nr + b.k;
+  }
+  if (c0) atomicAdd(cnt, c0);
+  if (c1) atomicAdd(cnt + 1, c1);
+}
+
+// one 1024-thread CTA: out[t] = the t-th touched row (as a double: the lists are summed over ranks)
+__global__ void __launch_bounds__(1024) merge_list_kernel(const BoxDev* __restrict__ boxes, int nbox,
+                                                          const int* __restrict__ ipool, int which,
+                                                          double* __restrict__ out) {
+  __shared__ int sc[1024];
+  __shared__ int sbase;
+  const int tid = threadIdx.x;
+  if (tid == 0) sbase = 0;
+  __syncthreads();
+  for (int c0 = 0; c0 < nbox; c0 += 1024) {
+    const int i = c0 + tid;
+    int len = 0, n1 = 0;
+    const int *l1 = nullptr, *l2 = nullptr;
+    if (i < nbox && boxes[i].nr > 0) {
+      const BoxDev& b = boxes[i];
+      n1 = b.nr;
+      l1 = ipool + b.f_red;
+      l2 = ipool + (which == 0 ? b.f_c : b.f_skel);
+      len = n1 + (which == 0 ? b.nc : b.k);
+    }
+    sc[tid] = len;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {      // inclusive scan
+      const int v = tid >= off ? sc[tid - off] : 0;
+      __syncthreads();
+      sc[tid] += v;
+      __syncthreads();
+    }
+    const int base = sbase + sc[tid] - len;
+    for (int t = 0; t < len; ++t) out[base + t] = (double)(t < n1 ? l1[t] : l2[t - n1]);
+    __syncthreads();
+    if (tid == 1023) sbase += sc[1023];
+    __syncthreads();
+  }
+}
+
+__global__ void merge_rows_to_int_kernel(const double* __restrict__ in, int* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int)in[i];
+}
+
+// buf[t, :] = x[rows[t], :]  (this rank's part of the batch's merge buffer)
+__global__ void merge_pack_kernel(const int* __restrict__ rows, int n, const double* __restrict__ x, int w,
+                                  double* __restrict__ buf) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)n * w; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / w, j = t - i * w;
+    buf[t] = x[(int64_t)rows[i] * w + j];
+  }
+}
+
+// x[rows[t], :] = buf[t, :]  (after the sum over ranks: every touched row has exactly one writer)
+__global__ void merge_scatter_kernel(const int* __restrict__ rows, int n, const double* __restrict__ buf,
+                                     double* __restrict__ x, int w) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)n * w; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / w, j = t - i * w;
+    x[(int64_t)rows[i] * w + j] = buf[t];
+  }
+}
+
 __global__ void add_into_kernel(double* __restrict__ dst, const double* __restrict__ src, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] += src[i];

@@ -80,6 +80,8 @@ int g_chol_fuse_rmax = 320;          // RSRS_CHOL_FUSE_RMAX: largest real near f
 int g_back_fuse_rmax = 1 << 30;      // RSRS_BACK_FUSE_RMAX: the same for the fused back substitution
 int g_fuse_min_batch = 128;          // RSRS_FUSE_MIN_BATCH: fewest matrices of a launch for the fused kernels
 int g_skinny_cols = rsrs::SK_COLS;   // RSRS_SKINNY_COLS: columns per CTA of the skinny E/F kernel
+int g_level_sync = 0;                // RSRS_LEVEL_SYNC=1: drain the stream after the level setup / compaction (A/B)
+int g_merge_compact = 1;             // RSRS_MERGE_COMPACT=0: multi-GPU solve merge over the whole x per batch
 int g_diag16 = 0;                    // RSRS_DIAG16=1: two-level 16 x 16 warp sub-block diagonal (measured slower)
 int g_skinny_fixed = 0;              // RSRS_SKINNY_FIXED=1: 64 x 64 opA shared memory on every launch (A/B)
 int g_tm32_nt = 32, g_tm32_nn = 32;  // RSRS_TM32_NT / RSRS_TM32_NN: 32-row tiles when every row count <= this
@@ -89,7 +91,8 @@ int g_tm32_nt = 32, g_tm32_nn = 32;  // RSRS_TM32_NT / RSRS_TM32_NN: 32-row tile
 thread_local bool t_level_tm32 = false;
 double g_tm32_ratio = 0.85;          // RSRS_TM32_RATIO: padded rows (32-row tiles) / padded rows (64) below this
 bool g_nt3 = false;
-int g_gram_pack = 32;                // RSRS_GRAM_PACK: rows per packed Gram-block row block on small-box levels (0: off)
+int g_gram_pack = 0;                 // RSRS_GRAM_PACK=32: packed Gram-block row blocks on small-box levels (off:
+                                     // -1.5 ms of Gram kernels but +8 ms of host planning on c3)
 bool g_tm16 = true;                  // RSRS_TM16=0: no 16-row NT tiles on levels of small boxes
 bool g_tm16_nn = false;              // RSRS_TM16_NN=1: the same for NN (measured: no gain on c3)                  // RSRS_NT3=1: three-stage, one-barrier NT tiles (A/B)
 
@@ -170,6 +173,8 @@ void init_kernels() {
   g_trace = tr && tr[0] == '1';
   if (const char* sf = getenv("RSRS_SKINNY_FIXED")) g_skinny_fixed = atoi(sf);
   if (const char* dg = getenv("RSRS_DIAG16")) g_diag16 = atoi(dg);
+  if (const char* mc = getenv("RSRS_MERGE_COMPACT")) g_merge_compact = atoi(mc);
+  if (const char* ls = getenv("RSRS_LEVEL_SYNC")) g_level_sync = atoi(ls);
   if (const char* sc = getenv("RSRS_SKINNY_COLS")) g_skinny_cols = std::max(128, (atoi(sc) / 128) * 128);
   if (const char* n3 = getenv("RSRS_NT3")) g_nt3 = n3[0] == '1';
   if (const char* t16 = getenv("RSRS_TM16")) g_tm16 = t16[0] != '0';
@@ -477,6 +482,15 @@ struct rsrs_factor_s {
   std::vector<int64_t> S_host;
   int64_t* d_perm = nullptr;
   DBuf xtmp, mergebuf, bstage;
+  // compact solve merge (multi-GPU): per (batch, which) the global list of touched rows (rank order),
+  // this rank's offset / count in it; built on the first distributed sweep
+  struct MergeSeg {
+    int64_t at = 0;      // ints into mergeidx
+    int total = 0, off = 0, cnt = 0;
+  };
+  std::vector<MergeSeg> mseg;
+  int mseg_ranks = 0;
+  DBuf mergeidx, mergecbuf;
   // single-GPU solve / apply sweeps captured once per (x buffer, nrhs, direction) as CUDA graphs
   struct SweepGraph {
     cudaGraphExec_t exec;
@@ -808,6 +822,9 @@ struct Planner {
     }
     int* gidx = leaf_gidx.as<int>();
     DBuf ws, iws, nbrbuf, descbuf, dstbuf, rl_send, rl_recv, estdesc;
+    // Gram-block buffers of the current level: grow-only across levels, so that the end of a level does
+    // not drain the stream (a release synchronizes)
+    DBuf gpool_buf, gtab_b, gup_b, growl_b, gwork_b, pre_b;
     const NNDesc* Eform = nullptr;
     const NTDesc* Egram = nullptr;
     const CholDesc* Echol = nullptr;
@@ -989,7 +1006,9 @@ struct Planner {
 
         CK(cudaMemcpyAsync(dnbr, hnbr.data(), sizeof(int) * noff, cudaMemcpyHostToDevice, s));
         if (!hb.empty()) CK(cudaMemcpyAsync(dboxes, hb.data(), sizeof(BoxDev) * hb.size(), cudaMemcpyHostToDevice, s));
-        stream_sync(s);
+        // (pageable sources are staged when the call returns: no drain, so the previous level's
+        // compaction overlaps this level's host planning; RSRS_LEVEL_SYNC=1 restores the drain)
+        if (g_level_sync) stream_sync(s);
       }
 
       // ---- descriptors (sizes that depend on the near set point at BoxDev::r / nr / nc / k)
@@ -1002,7 +1021,6 @@ struct Planner {
         if (nb_all[b] > rsrs::GB_MAX || (lv.nbr_off[b + 1] - lv.nbr_off[b]) > 64) use_blocks = false;
       }
       level_blocks = use_blocks;
-      DBuf gpool_buf, gtab_b, gup_b, growl_b, gwork_b, pre_b;
       const int* gps_b_ptr = nullptr;
       std::vector<int64_t> gwork_off(binfo.size() + 1, 0);
       DBuf* gpool = &gpool_buf;
@@ -1114,7 +1132,7 @@ struct Planner {
         }
         const int64_t nrowl = packing ? prowl_at[npack] : rowl_at[nbox];
         gpool_side = poff;
-        gpool_buf.alloc((size_t)sS * std::max<i64>(2, sides * poff), s);
+        gpool_buf.ensure((size_t)sS * std::max<i64>(2, sides * poff), s);
         double* poolO = gpool_buf.as<double>();
         // (box, block) work items of the block update, per colour batch: prefix over my boxes
         std::vector<int64_t> wpre(hb.size() + 1, 0);
@@ -1157,7 +1175,7 @@ struct Planner {
             std::copy(prowl_at.begin(), prowl_at.end(), lq + npack);
           }
         }
-        gup_b.alloc(sizeof(int64_t) * up.size(), s);
+        gup_b.ensure(sizeof(int64_t) * up.size(), s);
         CK(cudaMemcpyAsync(gup_b.p, up.data(), sizeof(int64_t) * up.size(), cudaMemcpyHostToDevice, s));
         const int* d_gps = gup_b.as<int>();
         const int* d_pl = d_gps + nbox + 1;
@@ -1167,9 +1185,9 @@ struct Planner {
         const i64* d_roff = gup_b.as<i64>() + (ni + 1) / 2;
         const i64* d_rowlat = d_roff + nbox;
         const i64* d_wpre = d_rowlat + nbox + 1;
-        growl_b.alloc(sizeof(int) * std::max<int64_t>(nrowl, 1), s);
-        gtab_b.alloc(sizeof(rsrs::GBlk) * std::max<size_t>(plist.size(), 1), s);
-        gwork_b.alloc(sizeof(int2) * std::max<int64_t>(wpre[hb.size()], 1), s);
+        growl_b.ensure(sizeof(int) * std::max<int64_t>(nrowl, 1), s);
+        gtab_b.ensure(sizeof(rsrs::GBlk) * std::max<size_t>(plist.size(), 1), s);
+        gwork_b.ensure(sizeof(int2) * std::max<int64_t>(wpre[hb.size()], 1), s);
         const int* d_packof = d_gps + o_pk;
         const int* d_upstart = d_packof + nbox;
         const int* d_ulist = d_upstart + npack + 1;
@@ -1211,7 +1229,7 @@ struct Planner {
           rows += nb_all[i];
         }
         const int nunit = packing ? npack : nbox;
-        pre_b.alloc(sizeof(NTDesc) * std::max<size_t>((size_t)sides * nunit, 1), s);
+        pre_b.ensure(sizeof(NTDesc) * std::max<size_t>((size_t)sides * nunit, 1), s);
         if (nunit > 0 && fl > 0) {
           if (packing)
             rsrs::pre_desc_kernel<<<(sides * npack + 255) / 256, 256, 0, s>>>(npack, sides, d_prows, d_prow0, d_proff, d_pld,
@@ -1617,7 +1635,7 @@ struct Planner {
         if (cplx) rsrs::solve_pack_kernel<true><<<(unsigned)hb.size(), 256, 0, s>>>(dboxes, fpool, d_pk, dpack);
         else rsrs::solve_pack_kernel<false><<<(unsigned)hb.size(), 256, 0, s>>>(dboxes, fpool, d_pk, dpack);
         post("solve_pack_kernel", s, launches);
-        stream_sync(s);   // pk (pageable host vector) is consumed
+        if (g_level_sync) stream_sync(s);   // (pk is pageable: staged when the copy returns)
         for (size_t q = 0; q < binfo.size(); ++q)
           for (int i = 0; i < binfo[q].count; ++i) bmax_nc[q] = std::max(bmax_nc[q], hb[binfo[q].first + i].nc);
       }
@@ -1728,8 +1746,10 @@ struct Planner {
                          rl_recv.as<int>() + ro[q], 0, (int)b2, W, 4, true);
         }
       }
-      stream_sync(s);
-      flush_prof();
+      if (g_level_sync || (g_trace && profile) || R > 1) {   // per-level trace: the level's class times
+        stream_sync(s);
+        flush_prof();
+      }
       if (g_trace && profile) {
         fprintf(stderr, "[rsrs trace] level %d (%d boxes, %zu colour batches; max n_b %d, max r %d): class ms/GF/TFs", lev,
                 nbox, binfo.size(), *std::max_element(nb_all.begin(), nb_all.end()),
@@ -1870,6 +1890,7 @@ static rsrs_status factor_impl(rsrs_tree t, rsrs_dtype dt, int64_t p, void* Y, v
     init_kernels();
     f = new rsrs_factor_s();
     f->xtmp.devsync = f->mergebuf.devsync = f->bstage.devsync = true;
+    f->mergeidx.devsync = f->mergecbuf.devsync = true;
     const rsrs::Tree& T = t->t;
     f->dt = dt;
     f->cplx = (dt == RSRS_C128);
@@ -2114,9 +2135,76 @@ struct Merger {
     contrib = f->mergebuf.as<double>();
     mask = contrib + N * w;
     CK(cudaMemsetAsync(contrib, 0, sizeof(double) * N * (w + 1), s));
+    if (g_merge_compact) {
+      if (f->mseg_ranks != comm->nranks) build();
+      int tmax = 0;
+      for (const auto& g : f->mseg) tmax = std::max(tmax, g.total);
+      f->mergecbuf.ensure(sizeof(double) * (size_t)std::max(tmax, 1) * w, s);
+    }
+  }
+  // the merge lists of every (batch, which): counts (allreduce max over a rank-slotted vector), the
+  // rank's own lists at its offsets, summed over ranks (indices as doubles, exact), as ints
+  void build() {
+    const int nb = (int)f->batches.size(), G = comm->nranks, me = comm->rank;
+    DBuf dcnt;
+    dcnt.alloc(sizeof(int) * 2 * std::max(nb, 1), s);
+    CK(cudaMemsetAsync(dcnt.p, 0, sizeof(int) * 2 * std::max(nb, 1), s));
+    for (int bi = 0; bi < nb; ++bi) {
+      const Batch& b = f->batches[bi];
+      if (b.nbox > 0) rsrs::merge_count_kernel<<<1, 256, 0, s>>>(b.d_boxes, b.nbox, dcnt.as<int>() + 2 * bi);
+    }
+    CK(cudaGetLastError());
+    std::vector<int> mine(2 * nb, 0), all((size_t)2 * nb * G, 0);
+    if (nb) CK(cudaMemcpyAsync(mine.data(), dcnt.p, sizeof(int) * 2 * nb, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int q = 0; q < 2 * nb; ++q) all[(size_t)q * G + me] = mine[q];
+    comm->allreduce_max_i32(all.data(), all.size(), s);
+    f->mseg.assign(2 * nb, {});
+    int64_t tot = 0;
+    for (int q = 0; q < 2 * nb; ++q) {
+      auto& g = f->mseg[q];
+      g.at = tot;
+      for (int r = 0; r < G; ++r) {
+        if (r == me) g.off = g.total, g.cnt = all[(size_t)q * G + r];
+        g.total += all[(size_t)q * G + r];
+      }
+      tot += g.total;
+    }
+    f->mergeidx.alloc(sizeof(int) * std::max<int64_t>(tot, 1), s);
+    if (tot > 0) {
+      DBuf tmp;
+      tmp.alloc(sizeof(double) * tot, s);
+      CK(cudaMemsetAsync(tmp.p, 0, sizeof(double) * tot, s));
+      for (int q = 0; q < 2 * nb; ++q) {
+        const Batch& b = f->batches[q / 2];
+        const auto& g = f->mseg[q];
+        if (g.cnt > 0) rsrs::merge_list_kernel<<<1, 1024, 0, s>>>(b.d_boxes, b.nbox, b.ipool, q & 1, tmp.as<double>() + g.at + g.off);
+      }
+      CK(cudaGetLastError());
+      comm->allreduce_sum_f64(tmp.as<double>(), (size_t)tot, s);
+      rsrs::merge_rows_to_int_kernel<<<592, 256, 0, s>>>(tmp.as<double>(), f->mergeidx.as<int>(), tot);
+      CK(cudaGetLastError());
+      CK(cudaStreamSynchronize(s));
+    }
+    f->mseg_ranks = G;
   }
   void batch(const Batch& b, int which) {
     if (!comm) return;
+    if (g_merge_compact) {       // only the touched rows travel: T x w doubles instead of N x (w + 1)
+      const auto& g = f->mseg[2 * (&b - f->batches.data()) + which];
+      if (g.total == 0) return;
+      double* buf = f->mergecbuf.as<double>();
+      CK(cudaMemsetAsync(buf, 0, sizeof(double) * (size_t)g.total * w, s));
+      const int* rows = f->mergeidx.as<int>() + g.at;
+      const int64_t nw = (int64_t)g.total * w;
+      const int grid = (int)std::min<int64_t>(1184, (nw + 255) / 256);
+      if (g.cnt > 0) rsrs::merge_pack_kernel<<<grid, 256, 0, s>>>(rows + g.off, g.cnt, x, w, buf + (size_t)g.off * w);
+      CK(cudaGetLastError());
+      comm->allreduce_sum_f64(buf, (size_t)nw, s);
+      rsrs::merge_scatter_kernel<<<grid, 256, 0, s>>>(rows, g.total, buf, x, w);
+      CK(cudaGetLastError());
+      return;
+    }
     if (b.nbox > 0) {
       rsrs::mark_rows_kernel<<<b.nbox, 128, 0, s>>>(b.d_boxes, b.ipool, x, w, w, contrib, mask, which);
       CK(cudaGetLastError());

@@ -33,8 +33,10 @@ VARIANTS = {
     # 32-row tiles without the 16-row split for small-box descriptors
     "no_tiles_16": {"RSRS_TM16": "0"},
     "nn_tiles_16": {"RSRS_TM16_NN": "1"},
-    # one Gram-block row block per box on the small-box levels (no packing of consecutive boxes)
-    "no_gram_pack": {"RSRS_GRAM_PACK": "0"},
+    # packed Gram-block row blocks on the small-box levels (consecutive boxes share one 32-row block)
+    "gram_pack": {"RSRS_GRAM_PACK": "32"},
+    # stream drains after every level setup / compaction (the round-1 host schedule)
+    "level_sync": {"RSRS_LEVEL_SYNC": "1"},
     # two-level Cholesky diagonal blocks (16 x 16 warp sub-blocks; off by default: slower on c3)
     "diag_two_level": {"RSRS_DIAG16": "1"},
     # solve from the factor pools (no packed records, LU top block), kernel-by-kernel launches
