@@ -76,6 +76,14 @@ bool g_solve_packed = true;  // RSRS_SOLVE_PACKED=0: the solve reads the factor 
 bool g_sweep_graph = true;   // RSRS_SWEEP_GRAPH=0: launch the solve / apply sweeps kernel by kernel
 bool g_debug = false;  // RSRS_DEBUG_SYNC=1: synchronize and check after every launch
 bool g_trace = false;  // RSRS_TRACE=1: host-side time split of rsrs_factor on stderr
+int g_ns_kmax = 32;                  // RSRS_NS_KMAX: levels whose boxes hold at most this many points push their L/U
+                                     // updates through nn_stream_kernel (descriptors with n_r <= 32); 0: off
+int g_ks_mmax = 0;                   // RSRS_KS_MMAX: projection / pulled update of levels whose boxes hold at most this
+                                     // many points walk their columns in nn_kstream_kernel (0: off)
+int g_ks_chunks = 5;                 // RSRS_KS_CHUNKS: 64-column chunks per CTA of nn_kstream_kernel
+int g_ks_leftovers = 0;              // RSRS_KS_LEFTOVERS=1: always run the tiled pass for descriptors nn_kstream_kernel skips
+int g_ef_stream = 0;                 // RSRS_EF_STREAM=1: the E/F sample updates through nn_stream_kernel as well
+int g_ns_chunks = 7;                 // RSRS_NS_CHUNKS: 64-column chunks per CTA of nn_stream_kernel
 int g_chol_fuse_rmax = 320;          // RSRS_CHOL_FUSE_RMAX: largest real near field for the fused Cholesky (0: off)
 int g_back_fuse_rmax = 1 << 30;      // RSRS_BACK_FUSE_RMAX: the same for the fused back substitution
 int g_fuse_min_batch = 128;          // RSRS_FUSE_MIN_BATCH: fewest matrices of a launch for the fused kernels
@@ -184,6 +192,12 @@ void init_kernels() {
   if (const char* t = getenv("RSRS_TM32_NN")) g_tm32_nn = atoi(t);
   if (const char* t = getenv("RSRS_TM32_RATIO")) g_tm32_ratio = atof(t);
   if (const char* cf = getenv("RSRS_CHOL_FUSE_RMAX")) g_chol_fuse_rmax = atoi(cf);
+  if (const char* t = getenv("RSRS_NS_KMAX")) g_ns_kmax = atoi(t);
+  if (const char* t = getenv("RSRS_EF_STREAM")) g_ef_stream = atoi(t);
+  if (const char* t = getenv("RSRS_KS_MMAX")) g_ks_mmax = atoi(t);
+  if (const char* t = getenv("RSRS_KS_CHUNKS")) g_ks_chunks = std::max(1, atoi(t));
+  if (const char* t = getenv("RSRS_KS_LEFTOVERS")) g_ks_leftovers = atoi(t);
+  if (const char* t = getenv("RSRS_NS_CHUNKS")) g_ns_chunks = std::max(1, atoi(t));
   if (const char* bf = getenv("RSRS_BACK_FUSE_RMAX")) g_back_fuse_rmax = atoi(bf);
   if (const char* fm = getenv("RSRS_FUSE_MIN_BATCH")) g_fuse_min_batch = std::max(1, atoi(fm));
   int dev = 0;
@@ -199,6 +213,8 @@ void init_kernels() {
   set_smem(rsrs::gemm_nt_kernel<16>, rsrs::nt_smem(16, false));
   set_smem(rsrs::gemm_nn_kernel<16>, rsrs::nn_smem(16, false));
   set_smem(rsrs::gemm_nn_kernel<32>, rsrs::NN_SMEM);
+  set_smem(rsrs::nn_stream_kernel, rsrs::NS_SMEM);
+  set_smem(rsrs::nn_kstream_kernel, rsrs::KS_SMEM);
   set_smem(rsrs::gemm_nt_kernel_c<32>, rsrs::NT_SMEM);
   set_smem(rsrs::gemm_nn_kernel_c<32>, rsrs::NN_SMEM);
   set_smem(rsrs::chol_fused_kernel, rsrs::NT_SMEM);
@@ -358,12 +374,12 @@ void launch_nt(bool cplx, const NTDesc* d, int n, int mmax, int nmax, cudaStream
 }
 
 void launch_nn(bool cplx, const NNDesc* d, int n, int mmax, int nmax, cudaStream_t s, int64_t& launches,
-               int force_tm = 0) {
+               int force_tm = 0, int klo = -1) {
   if (n <= 0 || mmax <= 0 || nmax <= 0) return;
   constexpr int ZMAX = 65535;
   if (n > ZMAX) {
     for (int i = 0; i < n; i += ZMAX)
-      launch_nn(cplx, d + i, std::min(ZMAX, n - i), mmax, nmax, s, launches, force_tm);
+      launch_nn(cplx, d + i, std::min(ZMAX, n - i), mmax, nmax, s, launches, force_tm, klo);
     return;
   }
   const int TN = cplx ? rsrs::GTC : rsrs::GT;
@@ -372,10 +388,10 @@ void launch_nn(bool cplx, const NNDesc* d, int n, int mmax, int nmax, cudaStream
   if (!cplx && TM == 32 && !force_tm && g_tm16_nn && t_level_tm32) {
     // levels of small boxes: 16-row tiles for the descriptors with m <= 16
     dim3 g16((nmax + TN - 1) / TN, 1, n);
-    rsrs::gemm_nn_kernel<16><<<g16, 128, rsrs::nn_smem(16, false), s>>>(d, 0, 16);
+    rsrs::gemm_nn_kernel<16><<<g16, 128, rsrs::nn_smem(16, false), s>>>(d, 0, 16, klo);
     post("gemm_nn16", s, launches);
     if (mmax > 16) {
-      rsrs::gemm_nn_kernel<32><<<grid, 128, rsrs::nn_smem(32, false), s>>>(d, 16, 1 << 30);
+      rsrs::gemm_nn_kernel<32><<<grid, 128, rsrs::nn_smem(32, false), s>>>(d, 16, 1 << 30, klo);
       post("gemm_nn", s, launches);
     }
     return;
@@ -384,10 +400,57 @@ void launch_nn(bool cplx, const NNDesc* d, int n, int mmax, int nmax, cudaStream
     if (TM == 32) rsrs::gemm_nn_kernel_c<32><<<grid, 128, rsrs::nn_smem(32, true), s>>>(d);
     else rsrs::gemm_nn_kernel_c<64><<<grid, 128, rsrs::nn_smem(64, true), s>>>(d);
   } else {
-    if (TM == 32) rsrs::gemm_nn_kernel<32><<<grid, 128, rsrs::nn_smem(32, false), s>>>(d);
-    else rsrs::gemm_nn_kernel<64><<<grid, 128, rsrs::NN_SMEM, s>>>(d);
+    if (TM == 32) rsrs::gemm_nn_kernel<32><<<grid, 128, rsrs::nn_smem(32, false), s>>>(d, 0, 1 << 30, klo);
+    else rsrs::gemm_nn_kernel<64><<<grid, 128, rsrs::NN_SMEM, s>>>(d, 0, 1 << 30, klo);
   }
   post("gemm_nn", s, launches);
+}
+
+// L/U push of a batch whose boxes hold at most kmax points: the descriptors
+// with n_r <= 32 stream through nn_stream_kernel (one CTA per 32-row band and column group), the
+// others (if the level can have any) through the tiled kernel.  Real scalars only.
+void launch_nn_push(bool cplx, const NNDesc* d, int n, int mmax, int nmax, int kmax, cudaStream_t s,
+                    int64_t& launches) {
+  if (n <= 0 || mmax <= 0 || nmax <= 0) return;
+  if (cplx || kmax > g_ns_kmax) {
+    launch_nn(cplx, d, n, mmax, nmax, s, launches);
+    return;
+  }
+  constexpr int ZMAX = 65535;
+  const int nch = (nmax + rsrs::GT - 1) / rsrs::GT;
+  const int ngroups = std::max(1, (nch + g_ns_chunks - 1) / g_ns_chunks);
+  for (int i = 0; i < n; i += ZMAX) {
+    dim3 grid(ngroups, (mmax + rsrs::NS_TM - 1) / rsrs::NS_TM, std::min(ZMAX, n - i));
+    rsrs::nn_stream_kernel<<<grid, 128, rsrs::NS_SMEM, s>>>(d + i, ngroups);
+    post("nn_stream", s, launches);
+  }
+  if (kmax > rsrs::GBK) launch_nn(cplx, d, n, mmax, nmax, s, launches, 0, rsrs::GBK);
+}
+
+// Projection / pulled L/U update of a small-box level (rows per box <= g_ks_mmax): column-walking
+// nn_kstream_kernel; descriptors it does not take (K = 0 or > 1024) go to the tiled kernel.
+void launch_nn_kwalk(bool cplx, const NNDesc* d, int n, int mmax, int nmax, int kmax, cudaStream_t s,
+                     int64_t& launches) {
+  if (n <= 0 || mmax <= 0 || nmax <= 0) return;
+  if (cplx || mmax > g_ks_mmax) {
+    launch_nn(cplx, d, n, mmax, nmax, s, launches);
+    return;
+  }
+  constexpr int ZMAX = 65535;
+  const int nch = (nmax + rsrs::GT - 1) / rsrs::GT;
+  const int ngroups = std::max(1, (nch + g_ks_chunks - 1) / g_ks_chunks);
+  for (int i = 0; i < n; i += ZMAX) {
+    const int nz = std::min(ZMAX, n - i);
+    dim3 grid(ngroups, (mmax + rsrs::NS_TM - 1) / rsrs::NS_TM, nz);
+    rsrs::nn_kstream_kernel<<<grid, 128, rsrs::KS_SMEM, s>>>(d + i, ngroups);
+    post("nn_kstream", s, launches);
+    // leftovers: K = 0 (a pure beta C copy) or K > KS_KMAX
+    dim3 g2((nmax + rsrs::GT - 1) / rsrs::GT, (mmax + 31) / 32, nz);
+    if (kmax > rsrs::KS_KMAX || g_ks_leftovers) {
+      rsrs::gemm_nn_kernel<32><<<g2, 128, rsrs::nn_smem(32, false), s>>>(d + i, 0, 1 << 30, -1, 1);
+      post("gemm_nn", s, launches);
+    }
+  }
 }
 
 // in-place skinny updates (E/F), see gemm.cuh
@@ -1413,7 +1476,7 @@ struct Planner {
             if (cplx) rsrs::pull_assemble_kernel<true><<<n, 256, 0, s>>>(dbx, dboxes, diws, dnbr, fpool, dws, !sym);
             else rsrs::pull_assemble_kernel<false><<<n, 256, 0, s>>>(dbx, dboxes, diws, dnbr, fpool, dws, !sym);
             post("pull_assemble_kernel", s, launches);
-            launch_nn(cplx, Dpull + ns * q0, ns * n, bi.max_nb, p, s, launches);
+            launch_nn_kwalk(cplx, Dpull + ns * q0, ns * n, bi.max_nb, p, bi.max_r, s, launches);
             toc();
           }
           tic(KC_GRAM);
@@ -1442,7 +1505,7 @@ struct Planner {
           launch_back_any(cplx, Dchol + ns * q0, ns * n, bi.max_r, bi.max_nb, s, launches);
           toc();
           tic(KC_PROJ);
-          launch_nn(cplx, Dproj + ns * q0, ns * n, bi.max_nb, p, s, launches);
+          launch_nn_kwalk(cplx, Dproj + ns * q0, ns * n, bi.max_nb, p, bi.max_r, s, launches);
           toc();
           tic(KC_HGRAM);
           launch_nt(cplx, Dh + ns * q0, ns * n, bi.max_nb, bi.max_nb, s, launches);
@@ -1456,7 +1519,9 @@ struct Planner {
             toc();
           }
           tic(KC_EF);
-          if (bi.max_nb <= rsrs::SK_MAX) launch_skinny(cplx, Def + 2 * ns * q0, 2 * ns * n, p, bi.max_nb, s, launches);
+          if (g_ef_stream && !cplx && bi.max_nb <= g_ns_kmax)
+            launch_nn_push(cplx, Def + 2 * ns * q0, 2 * ns * n, bi.max_nb, p, bi.max_nb, s, launches);
+          else if (bi.max_nb <= rsrs::SK_MAX) launch_skinny(cplx, Def + 2 * ns * q0, 2 * ns * n, p, bi.max_nb, s, launches);
           else launch_nn(cplx, Def + 2 * ns * q0, 2 * ns * n, bi.max_nb, p, s, launches);
           if (use_blocks) {      // keep the Gram blocks equal to F Omega Omega^* F^* (the E/F on Omega_s)
             const size_t bi_idx = &bi - &binfo[0];
@@ -1490,7 +1555,7 @@ struct Planner {
           if (tri) launch_nn(cplx, Dg2 + q0, n, bi.max_r, bi.max_nb, s, launches);   // G_L = M_U^T C^-1
           toc();
           tic(KC_UPD);
-          launch_nn(cplx, Dupd + ns * q0, ns * n, bi.max_r, p, s, launches);
+          launch_nn_push(cplx, Dupd + ns * q0, ns * n, bi.max_r, p, bi.max_nb, s, launches);
           toc();
           if (estimate) {        // coupling estimator of the boxes just eliminated
             tic(KC_EST);

@@ -28,6 +28,10 @@ constexpr int nn_smem(int TM, bool C) { return 2 * (TM * GPA + (C ? GBK / 2 : GB
 // dynamic size: min(cap, *p - off) when p is set, else cap
 RSRS_DI int dyn(const int* p, int off, int cap) { return p ? min(cap, *p - off) : cap; }
 
+// descriptors nn_kstream_kernel takes (the rest of a mixed list stays with gemm_nn_kernel)
+constexpr int KS_KMAX = 1024;
+RSRS_DI bool kstream_takes(const NNDesc& d, int K) { return K > 0 && K <= KS_KMAX && !d.transA; }
+
 // One TM x 64 output tile (TM = 64 or 32 rows) of C = alpha A_rows B_rows^T + beta C (K columns).
 // STAGES = 2: two cp.async stages, two barriers per k chunk; STAGES = 3: one barrier per chunk
 template <int TM = GT, int STAGES = 2>
@@ -355,18 +359,304 @@ RSRS_DI void nn_tile(const NNDesc& d, int m, int n, int K, int i0, int j0, doubl
 
 template <int TM>
 __global__ void __launch_bounds__(128) gemm_nn_kernel(const NNDesc* __restrict__ descs, int mlo = 0,
-                                                      int mhi = 1 << 30) {
+                                                      int mhi = 1 << 30, int klo = -1, int skipks = 0) {
   extern __shared__ __align__(16) double smem[];
   const NNDesc& d = descs[blockIdx.z];
   const int m = dyn(d.pm, 0, d.m);
   const int n = dyn(d.pn, 0, d.n);
   const int K = dyn(d.pK, 0, d.K);
   const int i0 = blockIdx.y * TM, j0 = blockIdx.x * GT;
-  if (i0 >= m || j0 >= n || m <= mlo || m > mhi) return;
+  if (i0 >= m || j0 >= n || m <= mlo || m > mhi || K <= klo) return;   // K <= klo: nn_stream_kernel's
+  if (skipks && kstream_takes(d, K)) return;                            // nn_kstream_kernel's
   const NNDesc dl = d;
   nn_tile<TM>(dl, m, n, K, i0, j0, smem);
 }
 
+
+// Streaming form of the rank-K row update D_rows = beta C_rows + alpha opA B_rows for a short inner
+// dimension (K <= GBK: the L/U push of a box with n_r <= 32 redundant points).
+// The update is pure HBM traffic (read and write m x n, ~2K flop per 16 B), so one CTA keeps a
+// 32-row band and walks its share of the 64-column chunks through a 3-stage cp.async ring holding
+// the chunk of B (K rows, zero-filled to a multiple of 4) and of C: the descriptor / size /
+// row-index prologue and the A fragments (registers) are paid once per band instead of once per
+// 32 x 64 tile, and two chunks stay in flight per CTA while a third is multiplied and stored.
+// Same DMMA order per element as nn_tile<32>, so the results are bit-identical to it.
+// Descriptors with K > GBK are left to gemm_nn_kernel (launched on the same list with klo = GBK).
+constexpr int NS_STAGES = 3;
+constexpr int NS_TM = 32;
+constexpr int NS_STAGE_DBL = (GBK + NS_TM) * GPB;                  // B chunk, then C tile
+constexpr int NS_SMEM = NS_STAGES * NS_STAGE_DBL * 8 + (NS_TM + GBK) * 8;   // + row offsets
+
+__global__ void __launch_bounds__(128) nn_stream_kernel(const NNDesc* __restrict__ descs, int ngroups) {
+  extern __shared__ __align__(16) double smem[];
+  const NNDesc& dg = descs[blockIdx.z];
+  const int m = dyn(dg.pm, 0, dg.m);
+  const int n = dyn(dg.pn, 0, dg.n);
+  const int K = dyn(dg.pK, 0, dg.K);
+  const int i0 = blockIdx.y * NS_TM;
+  if (i0 >= m || K > GBK) return;
+  const NNDesc d = dg;
+  const bool inplace = (d.Cin == nullptr);
+  if (K <= 0 && inplace && d.beta == 1.0) return;
+  const int nch = (n + GT - 1) / GT;
+  const int c0 = (int)(((i64)nch * blockIdx.x) / ngroups), c1 = (int)(((i64)nch * (blockIdx.x + 1)) / ngroups);
+  if (c0 >= c1) return;
+  i64* drow_off = reinterpret_cast<i64*>(smem + NS_STAGES * NS_STAGE_DBL);   // [NS_TM] D row offsets
+  i64* brow_off = drow_off + NS_TM;                                           // [GBK]   B row offsets
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int wr = warp >> 1, wc = warp & 1;
+  const int cofs = wc * 32;
+  if (tid < NS_TM) {
+    const int i = i0 + tid;
+    drow_off[tid] = i < m ? (d.rowD ? (i64)d.rowD[i] : (i64)i) * d.ldd : -1;
+  } else if (tid < NS_TM + GBK) {
+    const int k = tid - NS_TM;
+    brow_off[k] = k < K ? (d.rowB ? (i64)d.rowB[k] : (i64)k) * d.ldb : 0;
+  }
+  // A fragments of the band (zero beyond K / m)
+  const int nkk = (K + 3) >> 2;
+  double a[2][GBK / 4];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int i = i0 + wr * 16 + t * 8 + gid;
+#pragma unroll
+    for (int kk = 0; kk < GBK / 4; ++kk) {
+      const int k = kk * 4 + tig;
+      a[t][kk] = (i < m && k < K) ? (d.transA ? d.A[(i64)k * d.lda + i] : d.A[(i64)i * d.lda + k]) : 0.0;
+    }
+  }
+  const bool needc = d.beta != 0.0;
+  // C rows: rowC / Cin when out of place (only the in-place form is staged through drow_off)
+  __syncthreads();
+  const int krows = nkk * 4;
+  auto load_chunk = [&](int s, int c) {
+    double* Bs = smem + s * NS_STAGE_DBL;
+    double* Cs = Bs + GBK * GPB;
+    const int kr = tid >> 5, jc = (tid & 31) * 2;
+    const int gj = c * GT + jc;
+    const int cb = (gj + 2 <= n) ? 16 : (gj < n ? 8 : 0);
+#pragma unroll
+    for (int q = 0; q < GBK / 4; ++q) {
+      const int kl = kr + 4 * q;
+      if (kl < krows) {
+        const bool v = kl < K && cb > 0;
+        const double* src = v ? d.B + brow_off[kl] + gj : d.B;
+        cp_async16(&Bs[kl * GPB + jc], src, v ? cb : 0);
+      }
+    }
+    if (needc) {
+#pragma unroll
+      for (int q = 0; q < NS_TM / 4; ++q) {
+        const int r = kr + 4 * q;
+        const i64 off = drow_off[r];
+        const bool v = off >= 0 && cb > 0;
+        const double* src = d.D;
+        if (v) {
+          if (inplace) src = d.D + off + gj;
+          else src = d.Cin + (d.rowC ? (i64)d.rowC[i0 + r] : (i64)(i0 + r)) * d.ldc + gj;
+        }
+        cp_async16(&Cs[r * GPB + jc], src, v ? cb : 0);
+      }
+    }
+  };
+  const int nc = c1 - c0;
+#pragma unroll
+  for (int s = 0; s < NS_STAGES - 1; ++s) {
+    if (s < nc) load_chunk(s, c0 + s);
+    cp_async_commit();
+  }
+  const bool wrow = i0 + wr * 16 < m;
+  for (int c = 0; c < nc; ++c) {
+    cp_async_wait<NS_STAGES - 2>();
+    __syncthreads();       // chunk c landed; every warp is done with chunk c - 1, whose buffer is refilled
+    if (c + NS_STAGES - 1 < nc) load_chunk((c + NS_STAGES - 1) % NS_STAGES, c0 + c + NS_STAGES - 1);
+    cp_async_commit();
+    const int j0 = (c0 + c) * GT;
+    if (!wrow || j0 + cofs >= n) continue;
+    const double* bs = smem + (c % NS_STAGES) * NS_STAGE_DBL + cofs;
+    const double* cs = smem + (c % NS_STAGES) * NS_STAGE_DBL + GBK * GPB;
+    double acc[2][4][2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < GBK / 4; ++kk) {
+      if (kk < nkk) {
+        double b[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) b[u] = bs[(kk * 4 + tig) * GPB + u * 8 + gid];
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) dmma884(acc[t][u][0], acc[t][u][1], a[t][kk], b[u]);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int rl = wr * 16 + t * 8 + gid;
+      const i64 off = drow_off[rl];
+      if (off < 0) continue;
+      double* drow = d.D + off;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int jl = cofs + u * 8 + 2 * tig;
+        const int j = j0 + jl;
+        if (j >= n) continue;
+        double2 cv = make_double2(0.0, 0.0);
+        if (needc) cv = *reinterpret_cast<const double2*>(cs + rl * GPB + jl);
+        if (j + 1 < n)
+          *reinterpret_cast<double2*>(drow + j) =
+              make_double2(d.beta * cv.x + d.alpha * acc[t][u][0], d.beta * cv.y + d.alpha * acc[t][u][1]);
+        else
+          drow[j] = d.beta * cv.x + d.alpha * acc[t][u][0];
+      }
+    }
+  }
+}
+
+// Column-walking form of nn_tile<32> for the B-bound products with few output rows and a long
+// inner dimension (projection Y'' = Y_b - W Omega_near; pulled L/U update):
+// one CTA keeps a 32-row band and walks its 64-column chunks, the (chunk, k-stage) pairs flattened
+// into one 4-stage cp.async ring, so the ring never drains between chunks and the descriptor /
+// row-index prologue is paid once per band.  Same DMMA order per element as nn_tile<32>.
+// Takes the descriptors with 0 < K <= KS_KMAX and transA == 0; the others are left to
+// gemm_nn_kernel (launched on the same list with the complementary filter).
+constexpr int KS_STAGES = 4;
+constexpr int KS_STAGE_DBL = NS_TM * GPA + GBK * GPB;
+constexpr int KS_SMEM = KS_STAGES * KS_STAGE_DBL * 8 + KS_KMAX * 4;
+
+__global__ void __launch_bounds__(128) nn_kstream_kernel(const NNDesc* __restrict__ descs, int ngroups) {
+  extern __shared__ __align__(16) double smem[];
+  const NNDesc& dg = descs[blockIdx.z];
+  const int m = dyn(dg.pm, 0, dg.m);
+  const int n = dyn(dg.pn, 0, dg.n);
+  const int K = dyn(dg.pK, 0, dg.K);
+  const int i0 = blockIdx.y * NS_TM;
+  if (i0 >= m || !kstream_takes(dg, K)) return;
+  const NNDesc d = dg;
+  const bool inplace = (d.Cin == nullptr);
+  const int nch = (n + GT - 1) / GT;
+  const int c0 = (int)(((i64)nch * blockIdx.x) / ngroups), c1 = (int)(((i64)nch * (blockIdx.x + 1)) / ngroups);
+  if (c0 >= c1) return;
+  int* browi = reinterpret_cast<int*>(smem + KS_STAGES * KS_STAGE_DBL);   // [K] gathered B rows
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int wr = warp >> 1, wc = warp & 1;
+  const int cofs = wc * 32;
+  for (int k = tid; k < K; k += 128) browi[k] = d.rowB ? d.rowB[k] : k;
+  __syncthreads();
+  const int nk = (K + GBK - 1) / GBK;
+  const int total = (c1 - c0) * nk;
+  auto load = [&](int s, int it) {
+    const int c = it / nk, kt = it - c * nk;
+    double* As = smem + s * KS_STAGE_DBL;
+    double* Bs = As + NS_TM * GPA;
+    const int k0 = kt * GBK;
+    {
+      const int lrow = tid >> 4, kc = (tid & 15) * 2;
+      const int k = k0 + kc;
+      const int bytes = (k + 2 <= K) ? 16 : (k < K ? 8 : 0);
+#pragma unroll
+      for (int q = 0; q < NS_TM / 8; ++q) {
+        const int row = lrow + 8 * q;
+        const int gi = i0 + row;
+        const bool v = gi < m && bytes > 0;
+        const double* src = v ? d.A + (i64)gi * d.lda + k : d.A;
+        cp_async16(&As[row * GPA + kc], src, v ? bytes : 0);
+      }
+    }
+    {
+      const int kr = tid >> 5, jc = (tid & 31) * 2;
+      const int gj = (c0 + c) * GT + jc;
+      const int cb = (gj + 2 <= n) ? 16 : (gj < n ? 8 : 0);
+#pragma unroll
+      for (int q = 0; q < GBK / 4; ++q) {
+        const int kl = kr + 4 * q;
+        const int k = k0 + kl;
+        const bool v = k < K && cb > 0;
+        const double* src = v ? d.B + (i64)browi[k] * d.ldb + gj : d.B;
+        cp_async16(&Bs[kl * GPB + jc], src, v ? cb : 0);
+      }
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < KS_STAGES - 1; ++s) {
+    if (s < total) load(s, s);
+    cp_async_commit();
+  }
+  const bool wrow = i0 + wr * 16 < m;
+  double acc[2][4][2];
+  double2 cpre[2][4];
+  int c = 0, kt = 0;
+  for (int it = 0; it < total; ++it) {
+    cp_async_wait<KS_STAGES - 2>();
+    __syncthreads();
+    if (it + KS_STAGES - 1 < total) load((it + KS_STAGES - 1) % KS_STAGES, it + KS_STAGES - 1);
+    cp_async_commit();
+    const int j0 = (c0 + c) * GT;
+    const bool wact = wrow && j0 + cofs < n;
+    if (kt == 0) {
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          acc[t][u][0] = acc[t][u][1] = 0.0;
+          cpre[t][u] = make_double2(0.0, 0.0);
+        }
+        const int i = i0 + wr * 16 + t * 8 + gid;
+        if (!wact || i >= m || d.beta == 0.0) continue;
+        const double* crow;
+        if (inplace) crow = d.D + (d.rowD ? (i64)d.rowD[i] : (i64)i) * d.ldd;
+        else crow = d.Cin + (d.rowC ? (i64)d.rowC[i] : (i64)i) * d.ldc;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = j0 + cofs + u * 8 + 2 * tig;
+          if (j + 1 < n) cpre[t][u] = *reinterpret_cast<const double2*>(crow + j);
+          else if (j < n) cpre[t][u].x = crow[j];
+        }
+      }
+    }
+    if (wact) {
+      const double* as = smem + (it % KS_STAGES) * KS_STAGE_DBL + wr * 16 * GPA;
+      const double* bs = smem + (it % KS_STAGES) * KS_STAGE_DBL + NS_TM * GPA + cofs;
+#pragma unroll
+      for (int kk = 0; kk < GBK / 4; ++kk) {
+        double a[2], b[4];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) a[t] = as[(t * 8 + gid) * GPA + kk * 4 + tig];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) b[u] = bs[(kk * 4 + tig) * GPB + u * 8 + gid];
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) dmma884(acc[t][u][0], acc[t][u][1], a[t], b[u]);
+      }
+      if (kt == nk - 1) {
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const int i = i0 + wr * 16 + t * 8 + gid;
+          if (i >= m) continue;
+          double* drow = d.D + (d.rowD ? (i64)d.rowD[i] : (i64)i) * d.ldd;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = j0 + cofs + u * 8 + 2 * tig;
+            if (j + 1 < n)
+              *reinterpret_cast<double2*>(drow + j) = make_double2(d.beta * cpre[t][u].x + d.alpha * acc[t][u][0],
+                                                                   d.beta * cpre[t][u].y + d.alpha * acc[t][u][1]);
+            else if (j < n)
+              drow[j] = d.beta * cpre[t][u].x + d.alpha * acc[t][u][0];
+          }
+        }
+      }
+    }
+    if (++kt == nk) {
+      kt = 0;
+      ++c;
+    }
+  }
+}
 
 // ---------------------------------------------------------------------------
 // complex128 variants (RSRS_C128; interleaved {re, im} doubles).  Leading

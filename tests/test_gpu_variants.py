@@ -39,6 +39,13 @@ VARIANTS = {
     "level_sync": {"RSRS_LEVEL_SYNC": "1"},
     # two-level Cholesky diagonal blocks (16 x 16 warp sub-blocks; off by default: slower on c3)
     "diag_two_level": {"RSRS_DIAG16": "1"},
+    # L/U push through the tiled GEMM only (no nn_stream_kernel) / E-F updates through nn_stream_kernel too
+    "no_nn_stream": {"RSRS_NS_KMAX": "0"},
+    "ef_stream": {"RSRS_EF_STREAM": "1"},
+    "nn_stream_one_chunk": {"RSRS_NS_CHUNKS": "1", "RSRS_EF_STREAM": "1"},
+    # projection / pulled L/U update through the column-walking nn_kstream_kernel
+    "nn_kstream": {"RSRS_KS_MMAX": "100000"},
+    "nn_kstream_one_chunk": {"RSRS_KS_MMAX": "100000", "RSRS_KS_CHUNKS": "1", "RSRS_KS_LEFTOVERS": "1"},
     # solve from the factor pools (no packed records, LU top block), kernel-by-kernel launches
     "unpacked_solve": {"RSRS_SOLVE_PACKED": "0", "RSRS_SWEEP_GRAPH": "0"},
 }
