@@ -83,7 +83,7 @@ int g_ks_mmax = 0;                   // RSRS_KS_MMAX: projection / pulled update
 int g_ks_chunks = 5;                 // RSRS_KS_CHUNKS: 64-column chunks per CTA of nn_kstream_kernel
 int g_ks_leftovers = 0;              // RSRS_KS_LEFTOVERS=1: always run the tiled pass for descriptors nn_kstream_kernel skips
 int g_ef_stream = 0;                 // RSRS_EF_STREAM=1: the E/F sample updates through nn_stream_kernel as well
-int g_ns_chunks = 7;                 // RSRS_NS_CHUNKS: 64-column chunks per CTA of nn_stream_kernel
+int g_ns_chunks = 32;                // RSRS_NS_CHUNKS: 64-column chunks per CTA of nn_stream_kernel
 int g_chol_fuse_rmax = 320;          // RSRS_CHOL_FUSE_RMAX: largest real near field for the fused Cholesky (0: off)
 int g_back_fuse_rmax = 1 << 30;      // RSRS_BACK_FUSE_RMAX: the same for the fused back substitution
 int g_fuse_min_batch = 128;          // RSRS_FUSE_MIN_BATCH: fewest matrices of a launch for the fused kernels

@@ -1,7 +1,12 @@
 """Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv) by kernel."""
 import collections, csv, sys
 
-HARNESS = ("matvec_real_kernel", "dmma_loop", "dfma_loop")
+HARNESS = ("dmma_loop", "dfma_loop")
+
+
+def is_harness(k):
+    """sampler (the black-box operator, timed separately), the FP64 peak probe, torch kernels"""
+    return k in HARNESS or k.startswith("matvec_") or k.startswith("at::")
 
 
 def summarize(path):
@@ -20,10 +25,10 @@ def summarize(path):
         name = name.split("(")[0].split("<")[0].strip()
         agg[name][0] += 1
         agg[name][1] += float(r[vi].replace(",", "")) * scale[r[ui]]
-    tot = sum(v[1] for k, v in agg.items() if k not in HARNESS and not k.startswith("at::"))
+    tot = sum(v[1] for k, v in agg.items() if not is_harness(k))
     lines = []
     for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1]):
-        sh = f"{100 * v[1] / tot:5.1f}%" if (k not in HARNESS and not k.startswith("at::")) else "  (harness)"
+        sh = f"{100 * v[1] / tot:5.1f}%" if not is_harness(k) else "  (harness)"
         lines.append(f"{k:28s} n={v[0]:5d} total={v[1]:10.3f} ms  share_of_sweep={sh}")
     lines.append(f"sweep total (excl. harness/torch kernels) = {tot:.2f} ms")
     return "\n".join(lines)
