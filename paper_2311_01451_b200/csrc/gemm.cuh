@@ -382,11 +382,12 @@ __global__ void __launch_bounds__(128) gemm_nn_kernel(const NNDesc* __restrict__
 // 32 x 64 tile, and two chunks stay in flight per CTA while a third is multiplied and stored.
 // Same DMMA order per element as nn_tile<32>, so the results are bit-identical to it.
 // Descriptors with K > GBK are left to gemm_nn_kernel (launched on the same list with klo = GBK).
-constexpr int NS_STAGES = 3;
 constexpr int NS_TM = 32;
 constexpr int NS_STAGE_DBL = (GBK + NS_TM) * GPB;                  // B chunk, then C tile
-constexpr int NS_SMEM = NS_STAGES * NS_STAGE_DBL * 8 + (NS_TM + GBK) * 8;   // + row offsets
+constexpr int ns_smem(int stages) { return stages * NS_STAGE_DBL * 8 + (NS_TM + GBK) * 8; }   // + row offsets
 
+// NS_STAGES = 3: 2 CTAs per SM, two chunks in flight per CTA; 2: 3 CTAs per SM, one chunk in flight
+template <int NS_STAGES>
 __global__ void __launch_bounds__(128) nn_stream_kernel(const NNDesc* __restrict__ descs, int ngroups) {
   extern __shared__ __align__(16) double smem[];
   const NNDesc& dg = descs[blockIdx.z];
