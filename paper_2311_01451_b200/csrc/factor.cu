@@ -83,7 +83,7 @@ int g_ks_mmax = 0;                   // RSRS_KS_MMAX: projection / pulled update
 int g_ks_chunks = 5;                 // RSRS_KS_CHUNKS: 64-column chunks per CTA of nn_kstream_kernel
 int g_ks_leftovers = 0;              // RSRS_KS_LEFTOVERS=1: always run the tiled pass for descriptors nn_kstream_kernel skips
 int g_ef_stream = 0;                 // RSRS_EF_STREAM=1: the E/F sample updates through nn_stream_kernel as well
-int g_ns_stages = 3;                 // RSRS_NS_STAGES: cp.async ring depth of nn_stream_kernel (2: 3 CTAs per SM)
+int g_ns_stages = 2;                 // RSRS_NS_STAGES: cp.async ring depth of nn_stream_kernel (2: 3 CTAs per SM)
 int g_ns_chunks = 32;                // RSRS_NS_CHUNKS: 64-column chunks per CTA of nn_stream_kernel
 int g_chol_fuse_rmax = 320;          // RSRS_CHOL_FUSE_RMAX: largest real near field for the fused Cholesky (0: off)
 int g_back_fuse_rmax = 1 << 30;      // RSRS_BACK_FUSE_RMAX: the same for the fused back substitution
@@ -199,7 +199,7 @@ void init_kernels() {
   if (const char* t = getenv("RSRS_KS_CHUNKS")) g_ks_chunks = std::max(1, atoi(t));
   if (const char* t = getenv("RSRS_KS_LEFTOVERS")) g_ks_leftovers = atoi(t);
   if (const char* t = getenv("RSRS_NS_CHUNKS")) g_ns_chunks = std::max(1, atoi(t));
-  if (const char* t = getenv("RSRS_NS_STAGES")) g_ns_stages = atoi(t) == 2 ? 2 : 3;
+  if (const char* t = getenv("RSRS_NS_STAGES")) g_ns_stages = atoi(t) == 3 ? 3 : 2;
   if (const char* bf = getenv("RSRS_BACK_FUSE_RMAX")) g_back_fuse_rmax = atoi(bf);
   if (const char* fm = getenv("RSRS_FUSE_MIN_BATCH")) g_fuse_min_batch = std::max(1, atoi(fm));
   int dev = 0;

@@ -376,10 +376,10 @@ __global__ void __launch_bounds__(128) gemm_nn_kernel(const NNDesc* __restrict__
 // Streaming form of the rank-K row update D_rows = beta C_rows + alpha opA B_rows for a short inner
 // dimension (K <= GBK: the L/U push of a box with n_r <= 32 redundant points).
 // The update is pure HBM traffic (read and write m x n, ~2K flop per 16 B), so one CTA keeps a
-// 32-row band and walks its share of the 64-column chunks through a 3-stage cp.async ring holding
-// the chunk of B (K rows, zero-filled to a multiple of 4) and of C: the descriptor / size /
+// 32-row band and walks its share of the 64-column chunks through a cp.async ring (depth 2 or 3)
+// holding the chunk of B (K rows, zero-filled to a multiple of 4) and of C: the descriptor / size /
 // row-index prologue and the A fragments (registers) are paid once per band instead of once per
-// 32 x 64 tile, and two chunks stay in flight per CTA while a third is multiplied and stored.
+// 32 x 64 tile, and the next chunk(s) stay in flight while the current one is multiplied and stored.
 // Same DMMA order per element as nn_tile<32>, so the results are bit-identical to it.
 // Descriptors with K > GBK are left to gemm_nn_kernel (launched on the same list with klo = GBK).
 constexpr int NS_TM = 32;
